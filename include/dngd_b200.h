@@ -1,0 +1,161 @@
+/*
+ * dngd_b200.h -- C ABI of the B200-native D-NGD step library (libdngd_b200.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `dngd`
+ * (arXiv 2505.21404 reference, /root/reference/pkg/src/dngd).  Every entry
+ * point below replaces one numeric call site of the reference; the cited
+ * file:line is the reference interface it stands in for.  The Python layer
+ * (paper_2505_21404_b200/) keeps the reference's function names and calls
+ * these symbols through ctypes.
+ *
+ * Conventions
+ *  - All buffers are DEVICE pointers owned by the caller (PyTorch tensors);
+ *    the library never allocates or frees caller-visible memory.  Scratch is
+ *    passed explicitly as (work, work_bytes); *_workspace() reports the size.
+ *  - Matrices are row-major FP64 with an explicit leading dimension (in
+ *    elements).  Leading dimensions of matrices that the tensor-core kernels
+ *    stage through TMA must be even (16-byte row pitch) and base pointers
+ *    16-byte aligned.
+ *  - Every call is asynchronous on the caller's stream (`stream` is a
+ *    cudaStream_t passed as void*); nothing synchronises the device except
+ *    where stated.  Calls are reentrant: state lives in the dngd_ctx, one
+ *    context per calling thread (reference service.py:125-128 fans seeds
+ *    over threads).
+ *  - Status codes map 1:1 onto the reference's errors.py classes.
+ */
+#ifndef DNGD_B200_H
+#define DNGD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (reference errors.py:6-36) ---------------------------- */
+enum {
+  DNGD_OK = 0,
+  DNGD_ERR_DIMENSION = 1,   /* DimensionError   errors.py:10 */
+  DNGD_ERR_DOMAIN = 2,      /* DomainError      errors.py:23 */
+  DNGD_ERR_NOT_PD = 3,      /* -> host retry ladder, then FactorizationError errors.py:27 */
+  DNGD_ERR_NONFINITE = 4,   /* NonFiniteError   errors.py:14-20 */
+  DNGD_ERR_CUDA = 5,        /* DngdError        errors.py:6 */
+  DNGD_ERR_UNSUPPORTED = 6  /* DngdError (shape/config outside this build) */
+};
+
+typedef struct dngd_ctx dngd_ctx;
+
+int dngd_version(void);
+int dngd_ctx_create(int device, dngd_ctx** out);
+int dngd_ctx_destroy(dngd_ctx* ctx);
+const char* dngd_ctx_last_error(const dngd_ctx* ctx);
+
+/* ---- dense Gram (replaces solver.py:142-155 `K = J @ J.T; 0.5(K+K^T)`) ----
+ * K = J J^T over the first m rows / ncols columns of J (ldJ >= ncols, even).
+ * FP64 DMMA tensor-core SYRK, lower tiles only, deterministic split-K; the
+ * full symmetric K is written (both triangles).  accumulate != 0 adds to K
+ * (column-panel streaming and per-rank partial Grams). */
+int dngd_syrk_workspace(dngd_ctx* ctx, int64_t m, int64_t ncols, size_t* bytes);
+int dngd_syrk(dngd_ctx* ctx, void* stream, const double* J, int64_t m, int64_t ncols,
+              int64_t ldJ, double* K, int64_t ldK, int accumulate, void* work,
+              size_t work_bytes);
+
+/* ---- Cholesky with damping (replaces solver.py:161-173 cho_factor) --------
+ * L = lower(K) + lam*I copied into L (ldL), then factored in place (lower).
+ * info_dev (device int) receives 0 or the 1-based column of the first
+ * non-positive / non-finite pivot (LAPACK convention); the host retry ladder
+ * (lam *= 10, at most 5 retries) reads it.  dinv receives the inverses of
+ * the 64x64 diagonal blocks used by dngd_potrs (size: dngd_potrf_workspace). */
+int dngd_potrf_workspace(dngd_ctx* ctx, int64_t m, size_t* dinv_bytes);
+int dngd_shift_copy(dngd_ctx* ctx, void* stream, const double* K, int64_t m, int64_t ldK,
+                    double lam, double* L, int64_t ldL);
+int dngd_potrf(dngd_ctx* ctx, void* stream, double* L, int64_t m, int64_t ldL, double* dinv,
+               int* info_dev);
+
+/* ---- triangular solves (replaces solver.py:199,209 cho_solve) -------------
+ * b <- (L L^T)^{-1} b in place.  flags: device int scratch of 2*ceil(m/64) ints. */
+int dngd_potrs(dngd_ctx* ctx, void* stream, const double* L, int64_t m, int64_t ldL,
+               const double* dinv, double* b, int* flags);
+
+/* ---- streaming matvecs over J (replaces residuals.py:220-227 vjp and
+ *      residuals.py:282-292 jvp on the materialised J) ------------------------
+ * gemv_t: out = scale * (J^T y + g)   (g may be NULL)      -- solver.py:200,210
+ * gemv_n: out = alpha * A x + beta * add  (add may be NULL) -- solver.py:198,208 */
+int dngd_gemv_t_workspace(dngd_ctx* ctx, int64_t m, int64_t ncols, size_t* bytes);
+int dngd_gemv_t(dngd_ctx* ctx, void* stream, const double* J, int64_t m, int64_t ncols,
+                int64_t ldJ, const double* y, const double* g, double scale, double* out,
+                void* work, size_t work_bytes);
+int dngd_gemv_n(dngd_ctx* ctx, void* stream, const double* A, int64_t m, int64_t ncols,
+                int64_t ldA, const double* x, double alpha, const double* add, double beta,
+                double* out);
+
+/* ---- generic FP64 tensor-core GEMM  C = alpha * A B^T + beta * C ----------
+ * A (M x K, lda), B (N x K, ldb) row-major (K contiguous); batch > 1 uses
+ * strides sA, sB, sC (elements).  lower != 0 computes only C[i][j], j <= i. */
+int dngd_gemm_nt(dngd_ctx* ctx, void* stream, int64_t M, int64_t N, int64_t K,
+                 const double* A, int64_t lda, int64_t sA, const double* B, int64_t ldb,
+                 int64_t sB, double* C, int64_t ldc, int64_t sC, int batch, double alpha,
+                 double beta, int lower);
+
+/* ---- vector kernels for the device-resident PCG (solver.py:334-356) ------- */
+int dngd_dot(dngd_ctx* ctx, void* stream, int64_t n, const double* x, const double* y,
+             double* out_dev);
+int dngd_axpby(dngd_ctx* ctx, void* stream, int64_t n, double a, const double* x, double b,
+               const double* y, double* out);
+
+/* ---- PINN residual map on device (replaces residuals.py:139-323 for
+ *      PinnResidualMap with tanh MLPs; model.py:88-97, jets.py:285-294) ----- */
+#define DNGD_MAX_LAYERS 8
+#define DNGD_MAX_CLASSES 4
+#define DNGD_MAX_GRAD 12
+
+typedef struct {
+  int nlayers;                         /* number of affine layers L */
+  int widths[DNGD_MAX_LAYERS + 1];     /* widths[0] = input dim, widths[L] = 1 */
+} dngd_mlp_desc;
+
+/* r_i = weight * (cu*u + sum_g cg[g] d_{grad_dims[g]} u + cl * sum_{j in lap} d_jj u - f_i)
+ * grad channels are numbered 1..ngrad; lap_grad[] lists the grad-channel
+ * indices (0-based into grad_dims) summed into the Laplacian channel. */
+typedef struct {
+  int64_t count;                      /* points N */
+  int ngrad;
+  int nlap;
+  int grad_dims[DNGD_MAX_GRAD];
+  int lap_grad[DNGD_MAX_GRAD];
+  double cg[DNGD_MAX_GRAD];
+  double cu, cl, weight;
+  const double* points;               /* device, N x widths[0] row-major */
+  const double* f;                    /* device, N data values */
+} dngd_class_desc;
+
+/* scratch for one assembly / f_vv / loss_many(ncand) evaluation */
+int dngd_pinn_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp, const dngd_class_desc* classes,
+                        int nclass, int ncand, size_t* bytes);
+
+/* r (m) and J[:, col_begin:col_end) (m x (col_end-col_begin), ldJ) in one
+ * forward-Laplacian + per-point adjoint pass (residuals.py:241-256).  J may
+ * be NULL (residuals only). */
+int dngd_assemble(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
+                  const dngd_class_desc* classes, int nclass, int64_t col_begin,
+                  int64_t col_end, double* r, double* J, int64_t ldJ, void* work,
+                  size_t work_bytes);
+
+/* f_vv = d^2/dt^2 r(theta + t v) at t = 0 (residuals.py:304-317) */
+int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
+             const double* v, const dngd_class_desc* classes, int nclass, double* fvv,
+             void* work, size_t work_bytes);
+
+/* losses[c] = 0.5 |r(theta + etas[c] * delta)|^2 for c < ncand
+ * (residuals.py:188-201 via optimizer.py:148-166); etas is a device array.
+ * delta == NULL: theta is an explicit (ncand x n) candidate stack. */
+int dngd_loss_many(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
+                   const double* delta, const double* etas, int ncand,
+                   const dngd_class_desc* classes, int nclass, double* losses, void* work,
+                   size_t work_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DNGD_B200_H */

@@ -1,0 +1,239 @@
+// HBM-streaming FP64 matvecs over the materialised Jacobian and small vector
+// kernels for the PCG loop.
+//
+//   gemv_t : out = scale * (J^T y + g)  -- one pass over J (reference vjp,
+//            residuals.py:220-227, used at solver.py:200,210,335,360) with the
+//            dual-to-primal epilogue -(J^T y + g)/lam of solver.py:200 fused.
+//   gemv_n : out = alpha * A x + beta * add -- J g (jvp, solver.py:198,315),
+//            K f_vv (solver.py:208), J (J^T p) (solver.py:336).
+// Both are deterministic (fixed reduction order): bitwise-reproducible steps.
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace dngd {
+
+constexpr int kGT = 256;       // threads per CTA
+constexpr int kGTCols = 1024;  // columns per CTA (2 x double2 per thread)
+
+static void gemv_t_plan(dngd_ctx* ctx, long long m, long long ncols, int* nchunks) {
+  const long long col_tiles = (ncols + kGTCols - 1) / kGTCols;
+  const long long target = 4LL * ctx->num_sms;
+  long long nc = (target + col_tiles - 1) / col_tiles;
+  nc = std::min(nc, std::max(1LL, m / 16));
+  *nchunks = static_cast<int>(std::max(1LL, nc));
+}
+
+// J row-major (m x ncols, ld even, 16B-aligned).  Thread owns 4 consecutive
+// columns of a 1024-column strip; grid.y = row chunks.
+__global__ void __launch_bounds__(kGT) k_gemv_t(const double* __restrict__ J, long long m,
+                                                  long long ncols, long long ld,
+                                                  const double* __restrict__ y, int nchunks,
+                                                  const double* __restrict__ g, double scale,
+                                                  double* __restrict__ out,
+                                                  double* __restrict__ partial) {
+  const long long c = static_cast<long long>(blockIdx.x) * kGTCols + 4LL * threadIdx.x;
+  const long long rows_per = (m + nchunks - 1) / nchunks;
+  const long long i0 = blockIdx.y * rows_per;
+  const long long i1 = min(m, i0 + rows_per);
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  if (c + 3 < ncols) {
+    const double* p = J + i0 * ld + c;
+    long long i = i0;
+    for (; i + 3 < i1; i += 4) {
+      double2 v[4][2];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[k][0] = __ldcs(reinterpret_cast<const double2*>(p + k * ld));
+        v[k][1] = __ldcs(reinterpret_cast<const double2*>(p + k * ld + 2));
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double yk = __ldg(y + i + k);
+        a0 = fma(v[k][0].x, yk, a0);
+        a1 = fma(v[k][0].y, yk, a1);
+        a2 = fma(v[k][1].x, yk, a2);
+        a3 = fma(v[k][1].y, yk, a3);
+      }
+      p += 4 * ld;
+    }
+    for (; i < i1; ++i, p += ld) {
+      const double yk = __ldg(y + i);
+      const double2 u0 = __ldcs(reinterpret_cast<const double2*>(p));
+      const double2 u1 = __ldcs(reinterpret_cast<const double2*>(p + 2));
+      a0 = fma(u0.x, yk, a0);
+      a1 = fma(u0.y, yk, a1);
+      a2 = fma(u1.x, yk, a2);
+      a3 = fma(u1.y, yk, a3);
+    }
+  } else if (c < ncols) {
+    for (long long i = i0; i < i1; ++i) {
+      const double yk = y[i];
+      const double* p = J + i * ld + c;
+      a0 = fma(p[0], yk, a0);
+      if (c + 1 < ncols) a1 = fma(p[1], yk, a1);
+      if (c + 2 < ncols) a2 = fma(p[2], yk, a2);
+    }
+  } else {
+    return;
+  }
+  double acc[4] = {a0, a1, a2, a3};
+  if (nchunks == 1) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (c + k < ncols) out[c + k] = scale * (acc[k] + (g ? g[c + k] : 0.0));
+  } else {
+    double* dst = partial + static_cast<long long>(blockIdx.y) * ncols + c;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (c + k < ncols) dst[k] = acc[k];
+  }
+}
+
+__global__ void k_gemv_t_reduce(const double* __restrict__ partial, int nchunks, long long ncols,
+                                const double* __restrict__ g, double scale,
+                                double* __restrict__ out) {
+  const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  double s = 0.0;
+  for (int k = 0; k < nchunks; ++k) s += partial[static_cast<long long>(k) * ncols + c];
+  out[c] = scale * (s + (g ? g[c] : 0.0));
+}
+
+// out[i] = alpha * A[i,:] . x + beta * add[i]; one CTA (256 threads) per row.
+__global__ void __launch_bounds__(256) k_gemv_n_row(const double* __restrict__ A, long long m,
+                                                      long long ncols, long long ld,
+                                                      const double* __restrict__ x, double alpha,
+                                                      const double* __restrict__ add, double beta,
+                                                      double* __restrict__ out, int vec) {
+  __shared__ double sh[8];
+  const long long i = blockIdx.x;
+  const double* a = A + i * ld;
+  double s0 = 0, s1 = 0;
+  if (vec) {
+    const long long n2 = ncols / 2;
+    const double2* a2 = reinterpret_cast<const double2*>(a);
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    for (long long k = threadIdx.x; k < n2; k += 256) {
+      const double2 u = __ldcs(a2 + k);
+      const double2 v = __ldg(x2 + k);
+      s0 = fma(u.x, v.x, s0);
+      s1 = fma(u.y, v.y, s1);
+    }
+    if ((ncols & 1) && threadIdx.x == 0) s0 = fma(a[ncols - 1], x[ncols - 1], s0);
+  } else {
+    for (long long k = threadIdx.x; k < ncols; k += 256) s0 = fma(a[k], x[k], s0);
+  }
+  const double s = block_sum<256>(s0 + s1, sh);
+  if (threadIdx.x == 0) out[i] = alpha * s + (add ? beta * add[i] : 0.0);
+}
+
+// short rows: one warp per row
+__global__ void __launch_bounds__(256) k_gemv_n_warp(const double* __restrict__ A, long long m,
+                                                       long long ncols, long long ld,
+                                                       const double* __restrict__ x,
+                                                       double alpha,
+                                                       const double* __restrict__ add,
+                                                       double beta, double* __restrict__ out) {
+  const long long i = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= m) return;
+  const double* a = A + i * ld;
+  double s = 0.0;
+  for (long long k = lane; k < ncols; k += 32) s = fma(a[k], __ldg(x + k), s);
+  s = warp_sum(s);
+  if (lane == 0) out[i] = alpha * s + (add ? beta * add[i] : 0.0);
+}
+
+__global__ void __launch_bounds__(1024) k_dot(long long n, const double* __restrict__ x,
+                                                const double* __restrict__ y,
+                                                double* __restrict__ out) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (long long k = threadIdx.x; k < n; k += 1024) s = fma(x[k], y[k], s);
+  s = block_sum<1024>(s, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void k_axpby(long long n, double a, const double* __restrict__ x, double b,
+                        const double* __restrict__ y, double* __restrict__ out) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) out[k] = a * x[k] + (y ? b * y[k] : 0.0);
+}
+
+}  // namespace dngd
+
+using namespace dngd;
+
+extern "C" int dngd_gemv_t_workspace(dngd_ctx* ctx, int64_t m, int64_t ncols, size_t* bytes) {
+  int nc;
+  gemv_t_plan(ctx, m, ncols, &nc);
+  *bytes = nc > 1 ? static_cast<size_t>(nc) * ncols * sizeof(double) : 0;
+  return DNGD_OK;
+}
+
+extern "C" int dngd_gemv_t(dngd_ctx* ctx, void* stream, const double* J, int64_t m,
+                           int64_t ncols, int64_t ldJ, const double* y, const double* g,
+                           double scale, double* out, void* work, size_t work_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (ncols <= 0) return DNGD_OK;
+  if ((ldJ & 1) || (reinterpret_cast<uintptr_t>(J) & 15)) {
+    return set_error(ctx, DNGD_ERR_DIMENSION, "gemv_t: J needs an even leading dimension");
+  }
+  if (m <= 0) {
+    k_axpby<<<static_cast<unsigned>((ncols + 255) / 256), 256, 0, s>>>(ncols, 0.0, g ? g : out,
+                                                                       scale, g, out);
+    return cuda_status(ctx, cudaGetLastError(), "gemv_t empty");
+  }
+  int nc;
+  gemv_t_plan(ctx, m, ncols, &nc);
+  if (nc > 1 && (work == nullptr || work_bytes < static_cast<size_t>(nc) * ncols * 8)) {
+    return set_error(ctx, DNGD_ERR_DIMENSION, "gemv_t: workspace too small");
+  }
+  dim3 grid(static_cast<unsigned>((ncols + kGTCols - 1) / kGTCols), static_cast<unsigned>(nc));
+  k_gemv_t<<<grid, kGT, 0, s>>>(J, m, ncols, ldJ, y, nc, g, scale, out,
+                                static_cast<double*>(work));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_status(ctx, e, "gemv_t");
+  if (nc > 1) {
+    k_gemv_t_reduce<<<static_cast<unsigned>((ncols + 255) / 256), 256, 0, s>>>(
+        static_cast<const double*>(work), nc, ncols, g, scale, out);
+    e = cudaGetLastError();
+  }
+  return cuda_status(ctx, e, "gemv_t reduce");
+}
+
+extern "C" int dngd_gemv_n(dngd_ctx* ctx, void* stream, const double* A, int64_t m,
+                           int64_t ncols, int64_t ldA, const double* x, double alpha,
+                           const double* add, double beta, double* out) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (m <= 0) return DNGD_OK;
+  if (ncols >= 2048) {
+    const int vec = ((ldA & 1) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(x) & 15) == 0)
+                        ? 1
+                        : 0;
+    k_gemv_n_row<<<static_cast<unsigned>(m), 256, 0, s>>>(A, m, ncols, ldA, x, alpha, add, beta,
+                                                          out, vec);
+  } else {
+    k_gemv_n_warp<<<static_cast<unsigned>((m + 7) / 8), 256, 0, s>>>(A, m, ncols, ldA, x, alpha,
+                                                                      add, beta, out);
+  }
+  return cuda_status(ctx, cudaGetLastError(), "gemv_n");
+}
+
+extern "C" int dngd_dot(dngd_ctx* ctx, void* stream, int64_t n, const double* x, const double* y,
+                        double* out_dev) {
+  k_dot<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(n, x, y, out_dev);
+  return cuda_status(ctx, cudaGetLastError(), "dot");
+}
+
+extern "C" int dngd_axpby(dngd_ctx* ctx, void* stream, int64_t n, double a, const double* x,
+                          double b, const double* y, double* out) {
+  if (n <= 0) return DNGD_OK;
+  k_axpby<<<static_cast<unsigned>((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      n, a, x, b, y, out);
+  return cuda_status(ctx, cudaGetLastError(), "axpby");
+}

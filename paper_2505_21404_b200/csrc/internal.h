@@ -1,0 +1,46 @@
+// Host-side internals shared by the .cu translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <string>
+
+#include "../../include/dngd_b200.h"
+
+struct dngd_ctx {
+  int device = 0;
+  int num_sms = 148;
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  std::string last_error;
+};
+
+namespace dngd {
+
+int set_error(dngd_ctx* ctx, int code, const std::string& msg);
+int cuda_status(dngd_ctx* ctx, cudaError_t e, const char* where);
+
+// FP64 tensor-core GEMM engine (gemm.cu).  partial != nullptr selects the
+// split-K partial-tile output used by the SYRK (see syrk()).
+struct GemmCall {
+  long long M = 0, N = 0, K = 0;
+  const double* A = nullptr;
+  long long lda = 0, sA = 0;
+  const double* B = nullptr;
+  long long ldb = 0, sB = 0;
+  double* C = nullptr;
+  long long ldc = 0, sC = 0;
+  int batch = 1;
+  double alpha = 1.0, beta = 0.0;
+  int lower = 0;
+  int splits = 1;          // >1 only with partial
+  double* partial = nullptr;
+};
+int gemm_nt(dngd_ctx* ctx, cudaStream_t s, const GemmCall& g);
+int syrk_plan(dngd_ctx* ctx, long long m, long long ncols, int* splits, long long* ntiles,
+              size_t* work_bytes);
+int syrk(dngd_ctx* ctx, cudaStream_t s, const double* J, long long m, long long ncols,
+         long long ldJ, double* K, long long ldK, int accumulate, void* work, size_t wb);
+
+}  // namespace dngd

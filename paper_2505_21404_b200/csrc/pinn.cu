@@ -1,0 +1,838 @@
+// PINN residual map on device: forward-Laplacian MLP pass, per-point adjoints,
+// Jacobian row writes, second directional derivative f_vv and batched
+// line-search losses.
+//
+// Reference semantics (per collocation class, residuals.py:444-454):
+//   r_i = w * (cu*u + sum_g cg[g] d_{dim g} u + cl * sum_{j in lap} d_jj u - f_i)
+// where u is the tanh MLP of model.py:88-97.  The reference evaluates each
+// d_jj u with its own Jet2 pass (model.py:251-256, jets.py:285-294); here one
+// pass propagates "channels" per point: value, one first-derivative channel
+// per needed input dimension, and one Laplacian channel
+//     t = tanh z,  s = 1 - t^2,  d_j t = s d_j z,  Lap t = s Lap z - 2 t s sum_j (d_j z)^2.
+// Channel rows of one point are contiguous, so every hidden-to-hidden layer is
+// ONE FP64 tensor-core GEMM over all (point, channel) rows (gemm.cu) followed by
+// an elementwise channel kernel.  The per-point adjoint of the channel map
+// gives, for every layer, J[i, W_k|b_k] = sum_c Hext_k[i,c] (x) Zbar_k[i,c]:
+// a rank-nch outer product written straight to HBM (the tape's per-sample
+// einsum, tape.py:408-409).
+//
+// Row layout of the activation buffers: act0(class) + i * nch(class) + c.
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace dngd {
+
+constexpr int MAXG = DNGD_MAX_GRAD;
+constexpr int MAXC = DNGD_MAX_CLASSES;
+
+struct ClassDev {
+  long long row0, count, act0;
+  int nch, ngrad, nlap;
+  int grad_dims[MAXG];
+  int lap_ch[MAXG];  // channel index (1-based grad channel) summed into the Laplacian
+  double cg[MAXG];
+  double cu, cl, weight;
+  const double* pts;
+  const double* f;
+};
+
+struct Classes {
+  int n, din;
+  long long m, R;
+  ClassDev c[MAXC];
+};
+
+DNGD_DEV int find_class(const Classes& T, long long p) {
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < MAXC - 1; ++k)
+    if (k + 1 < T.n && p >= T.c[k + 1].row0) c = k + 1;
+  return c;
+}
+
+DNGD_DEV double coef(const ClassDev& C, int ch) {
+  if (ch == 0) return C.cu;
+  if (ch <= C.ngrad) return C.cg[ch - 1];
+  return C.cl;
+}
+
+static inline long long ldw(long long w) { return (w + 3) / 4 * 4; }
+
+// ------------------------------------------------------------------ forward
+
+// input layer (K = din is tiny): z = x W0 + b0, d_j z = W0[j,:], Lap z = 0; then tanh channels.
+// grid.y = candidate (theta stride th_s, activation stride act_s).
+__global__ void k_input_fwd(Classes T, const double* __restrict__ theta, long long th_s, int w1,
+                            long long ld, double* __restrict__ Z, double* __restrict__ H,
+                            long long act_s) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= T.m * w1) return;
+  const long long p = idx / w1;
+  const int q = static_cast<int>(idx - p * w1);
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long i = p - C.row0;
+  const double* th = theta + blockIdx.y * th_s;
+  const double* W0 = th;
+  const double* b0 = th + static_cast<long long>(T.din) * w1;
+  const double* x = C.pts + i * T.din;
+  double z = b0[q];
+  for (int j = 0; j < T.din; ++j) z = fma(x[j], W0[j * w1 + q], z);
+  const long long base = (C.act0 + i * C.nch) * ld + q + blockIdx.y * act_s;
+  const double t = tanh(z), s = 1.0 - t * t;
+  if (Z) Z[base] = z;
+  H[base] = t;
+  double G = 0.0;
+  for (int g = 0; g < C.ngrad; ++g) {
+    const double dz = W0[C.grad_dims[g] * w1 + q];
+    if (Z) Z[base + (1 + g) * ld] = dz;
+    H[base + (1 + g) * ld] = s * dz;
+  }
+  if (C.nlap) {
+    for (int l = 0; l < C.nlap; ++l) {
+      const double dz = W0[C.grad_dims[C.lap_ch[l] - 1] * w1 + q];
+      G = fma(dz, dz, G);
+    }
+    if (Z) Z[base + (C.nch - 1) * ld] = 0.0;
+    H[base + (C.nch - 1) * ld] = -2.0 * t * s * G;
+  }
+}
+
+// hidden layer: Z already holds H_k W_k (GEMM); add bias to the value channel
+// (written back so the adjoint sees the pre-activation) and apply tanh channels.
+__global__ void k_tanh_fwd(Classes T, double* __restrict__ Z, double* __restrict__ H, int w,
+                           long long ld, const double* __restrict__ bias, long long bias_s,
+                           long long act_s) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= T.m * w) return;
+  const long long p = idx / w;
+  const int q = static_cast<int>(idx - p * w);
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long i = p - C.row0;
+  const long long base = (C.act0 + i * C.nch) * ld + q + blockIdx.y * act_s;
+  const double z = Z[base] + bias[q + blockIdx.y * bias_s];
+  Z[base] = z;
+  const double t = tanh(z), s = 1.0 - t * t;
+  H[base] = t;
+  for (int g = 0; g < C.ngrad; ++g) H[base + (1 + g) * ld] = s * Z[base + (1 + g) * ld];
+  if (C.nlap) {
+    double G = 0.0;
+    for (int l = 0; l < C.nlap; ++l) {
+      const double dz = Z[base + C.lap_ch[l] * ld];
+      G = fma(dz, dz, G);
+    }
+    H[base + (C.nch - 1) * ld] = s * Z[base + (C.nch - 1) * ld] - 2.0 * t * s * G;
+  }
+}
+
+// output layer (width 1): one warp per point; channel dot products, residual.
+__global__ void k_head(Classes T, const double* __restrict__ H, int w, long long ld,
+                       const double* __restrict__ theta, long long th_s, long long wl_off,
+                       long long act_s, double* __restrict__ r, long long r_s) {
+  const long long p = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= T.m) return;
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long i = p - C.row0;
+  const double* th = theta + blockIdx.y * th_s;
+  const double* WL = th + wl_off;
+  const double bL = WL[w];
+  const double* h = H + (C.act0 + i * C.nch) * ld + blockIdx.y * act_s;
+  double res = 0.0;
+  for (int c = 0; c < C.nch; ++c) {
+    double u = 0.0;
+    for (int q = lane; q < w; q += 32) u = fma(h[c * ld + q], WL[q], u);
+    u = warp_sum(u);
+    if (c == 0) u += bL;
+    res = fma(coef(C, c), u, res);
+  }
+  if (lane == 0) r[p + blockIdx.y * r_s] = C.weight * (res - C.f[i]);
+}
+
+// ------------------------------------------------------------------ adjoint
+
+// Hbar_{L-1}[c][q] = w * coef_c * W_L[q]
+__global__ void k_seed_hbar(Classes T, double* __restrict__ Hb, int w, long long ld,
+                            const double* __restrict__ WL) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= T.m * w) return;
+  const long long p = idx / w;
+  const int q = static_cast<int>(idx - p * w);
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long i = p - C.row0;
+  const long long base = (C.act0 + i * C.nch) * ld + q;
+  for (int c = 0; c < C.nch; ++c) Hb[base + c * ld] = C.weight * coef(C, c) * WL[q];
+}
+
+// Zbar = adjoint of (z channels -> tanh channels) applied to Hbar.
+__global__ void k_tanh_bwd(Classes T, const double* __restrict__ Z, const double* __restrict__ H,
+                           const double* __restrict__ Hb, double* __restrict__ Zb, int w,
+                           long long ld) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= T.m * w) return;
+  const long long p = idx / w;
+  const int q = static_cast<int>(idx - p * w);
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long i = p - C.row0;
+  const long long base = (C.act0 + i * C.nch) * ld + q;
+  const double t = H[base], s = 1.0 - t * t;
+  const double dsdz = -2.0 * t * s;
+  double z0 = s * Hb[base];
+  double cross = 0.0;
+  for (int g = 0; g < C.ngrad; ++g) {
+    const double hb = Hb[base + (1 + g) * ld];
+    cross = fma(hb, Z[base + (1 + g) * ld], cross);
+    Zb[base + (1 + g) * ld] = s * hb;
+  }
+  z0 = fma(dsdz, cross, z0);
+  if (C.nlap) {
+    const long long lb = base + (C.nch - 1) * ld;
+    const double Lb = Hb[lb];
+    double G = 0.0;
+    for (int l = 0; l < C.nlap; ++l) {
+      const long long o = base + C.lap_ch[l] * ld;
+      const double dz = Z[o];
+      G = fma(dz, dz, G);
+      Zb[o] = fma(-4.0 * t * s * Lb, dz, Zb[o]);
+    }
+    Zb[lb] = s * Lb;
+    z0 = fma(Lb, dsdz * Z[lb] - 2.0 * G * (s * s - 2.0 * t * t * s), z0);
+  }
+  Zb[base] = z0;
+}
+
+// ------------------------------------------------------------------ J rows
+
+DNGD_DEV double hext(const ClassDev& C, int din, const double* __restrict__ xrow,
+                     const double* __restrict__ hrow, long long ld, int win, int c, int p) {
+  if (p == win) return c == 0 ? 1.0 : 0.0;  // bias row
+  if (hrow != nullptr) return hrow[c * ld + p];
+  // input layer: x channels
+  if (c == 0) return xrow[p];
+  if (c <= C.ngrad) return C.grad_dims[c - 1] == p ? 1.0 : 0.0;
+  return 0.0;
+  (void)din;
+}
+
+// Block of layer k in row i: (win+1) x wout row-major at flat column layer_off.
+// VEC: wout even, (layer_off - col_begin) even, ldJ even -> double2 streaming stores.
+template <bool VEC>
+__global__ void __launch_bounds__(256) k_jwrite(Classes T, const double* __restrict__ Hk,
+                                                  long long ldh, int win,
+                                                  const double* __restrict__ Zb, long long ldz,
+                                                  int wout, long long layer_off,
+                                                  long long col_begin, long long col_end,
+                                                  double* __restrict__ J, long long ldJ) {
+  const long long p = blockIdx.y;
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long i = p - C.row0;
+  const long long arow = C.act0 + i * C.nch;
+  const double* hrow = Hk ? Hk + arow * ldh : nullptr;
+  const double* xrow = C.pts + i * T.din;
+  const double* zrow = Zb ? Zb + arow * ldz : nullptr;
+  double* Jrow = J + p * ldJ - col_begin;
+  const long long E = static_cast<long long>(win + 1) * wout;
+  const int nch = C.nch;
+  if (VEC) {
+    const long long e0 = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) * 2;
+    for (long long e = e0; e < E; e += static_cast<long long>(gridDim.x) * 512) {
+      const int pp = static_cast<int>(e / wout);
+      const int q = static_cast<int>(e - static_cast<long long>(pp) * wout);
+      const long long col = layer_off + e;
+      if (col + 1 < col_begin || col >= col_end) continue;
+      double a0 = 0.0, a1 = 0.0;
+      for (int c = 0; c < nch; ++c) {
+        const double h = hext(C, T.din, xrow, hrow, ldh, win, c, pp);
+        const double2 z = *reinterpret_cast<const double2*>(zrow + c * ldz + q);
+        a0 = fma(h, z.x, a0);
+        a1 = fma(h, z.y, a1);
+      }
+      if (col >= col_begin && col + 1 < col_end) {
+        __stcs(reinterpret_cast<double2*>(Jrow + col), make_double2(a0, a1));
+      } else {
+        if (col >= col_begin && col < col_end) Jrow[col] = a0;
+        if (col + 1 >= col_begin && col + 1 < col_end) Jrow[col + 1] = a1;
+      }
+    }
+  } else {
+    const long long e0 = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;
+    for (long long e = e0; e < E; e += static_cast<long long>(gridDim.x) * 256) {
+      const long long col = layer_off + e;
+      if (col < col_begin || col >= col_end) continue;
+      const int pp = static_cast<int>(e / wout);
+      const int q = static_cast<int>(e - static_cast<long long>(pp) * wout);
+      double a = 0.0;
+      for (int c = 0; c < nch; ++c) {
+        const double h = hext(C, T.din, xrow, hrow, ldh, win, c, pp);
+        const double z = zrow ? zrow[c * ldz + q] : C.weight * coef(C, c);
+        a = fma(h, z, a);
+      }
+      Jrow[col] = a;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ f_vv (t-jets)
+
+struct T2 {
+  double a, b, c;
+};
+DNGD_DEV T2 t2mul(T2 x, T2 y) {
+  return {x.a * y.a, fma(x.b, y.a, x.a * y.b), fma(x.c, y.a, fma(x.a, y.c, 2.0 * x.b * y.b))};
+}
+
+// channels of one (point, neuron) given z triples -> tanh triples.
+// zget(ch) returns the triple of channel ch; hput(ch, triple) stores it.
+template <class ZGet, class HPut>
+DNGD_DEV void tanh_tjet(const ClassDev& C, ZGet zget, HPut hput) {
+  const T2 z0 = zget(0);
+  const double t = tanh(z0.a), s = 1.0 - t * t;
+  const T2 Tt = {t, s * z0.b, fma(s, z0.c, -2.0 * t * s * z0.b * z0.b)};
+  const T2 S = {s, -2.0 * t * Tt.b, -2.0 * fma(Tt.b, Tt.b, t * Tt.c)};
+  hput(0, Tt);
+  for (int g = 0; g < C.ngrad; ++g) hput(1 + g, t2mul(S, zget(1 + g)));
+  if (C.nlap) {
+    T2 G = {0.0, 0.0, 0.0};
+    for (int l = 0; l < C.nlap; ++l) {
+      const T2 zg = zget(C.lap_ch[l]);
+      const T2 sq = t2mul(zg, zg);
+      G = {G.a + sq.a, G.b + sq.b, G.c + sq.c};
+    }
+    const T2 Q = t2mul(Tt, S);
+    const T2 a = t2mul(S, zget(C.nch - 1));
+    const T2 b = t2mul(Q, G);
+    hput(C.nch - 1, {a.a - 2.0 * b.a, a.b - 2.0 * b.b, a.c - 2.0 * b.c});
+  }
+}
+
+// input layer of the f_vv pass: H3 holds [a; b; c] blocks of R rows each.
+__global__ void k_fvv_input(Classes T, const double* __restrict__ theta,
+                            const double* __restrict__ v, int w1, long long ld,
+                            double* __restrict__ H3) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= T.m * w1) return;
+  const long long p = idx / w1;
+  const int q = static_cast<int>(idx - p * w1);
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long i = p - C.row0;
+  const double* x = C.pts + i * T.din;
+  const long long boff = static_cast<long long>(T.din) * w1;
+  double za = theta[boff + q], zb = v[boff + q];
+  for (int j = 0; j < T.din; ++j) {
+    za = fma(x[j], theta[j * w1 + q], za);
+    zb = fma(x[j], v[j * w1 + q], zb);
+  }
+  const long long base = (C.act0 + i * C.nch) * ld + q;
+  const long long blk = T.R * ld;
+  auto zget = [&](int ch) -> T2 {
+    if (ch == 0) return {za, zb, 0.0};
+    if (ch <= C.ngrad) {
+      const int d = C.grad_dims[ch - 1];
+      return {theta[d * w1 + q], v[d * w1 + q], 0.0};
+    }
+    return {0.0, 0.0, 0.0};
+  };
+  auto hput = [&](int ch, T2 h) {
+    const long long o = base + ch * ld;
+    H3[o] = h.a;
+    H3[o + blk] = h.b;
+    H3[o + 2 * blk] = h.c;
+  };
+  tanh_tjet(C, zget, hput);
+}
+
+// hidden layer: P = [Ha;Hb;Hc] W (3R rows), Q = [Ha;Hb] V (2R rows)
+__global__ void k_fvv_hidden(Classes T, const double* __restrict__ P, const double* __restrict__ Q,
+                             const double* __restrict__ b, const double* __restrict__ vb, int w,
+                             long long ld, double* __restrict__ H3) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= T.m * w) return;
+  const long long p = idx / w;
+  const int q = static_cast<int>(idx - p * w);
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long i = p - C.row0;
+  const long long base = (C.act0 + i * C.nch) * ld + q;
+  const long long blk = T.R * ld;
+  auto zget = [&](int ch) -> T2 {
+    const long long o = base + ch * ld;
+    T2 z = {P[o], P[o + blk] + Q[o], P[o + 2 * blk] + 2.0 * Q[o + blk]};
+    if (ch == 0) {
+      z.a += b[q];
+      z.b += vb[q];
+    }
+    return z;
+  };
+  auto hput = [&](int ch, T2 h) {
+    const long long o = base + ch * ld;
+    H3[o] = h.a;
+    H3[o + blk] = h.b;
+    H3[o + 2 * blk] = h.c;
+  };
+  tanh_tjet(C, zget, hput);
+}
+
+// output: fvv_i = w * sum_c coef_c (Hc_c . W_L + 2 Hb_c . V_L)
+__global__ void k_fvv_head(Classes T, const double* __restrict__ H3, int w, long long ld,
+                           const double* __restrict__ WL, const double* __restrict__ VL,
+                           double* __restrict__ out) {
+  const long long p = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= T.m) return;
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long i = p - C.row0;
+  const long long blk = T.R * ld;
+  const double* h = H3 + (C.act0 + i * C.nch) * ld;
+  double res = 0.0;
+  for (int c = 0; c < C.nch; ++c) {
+    double u = 0.0;
+    for (int q = lane; q < w; q += 32)
+      u = fma(h[2 * blk + c * ld + q], WL[q], fma(2.0 * h[blk + c * ld + q], VL[q], u));
+    u = warp_sum(u);
+    res = fma(coef(C, c), u, res);
+  }
+  if (lane == 0) out[p] = C.weight * res;
+}
+
+// ------------------------------------------------------------------ helpers
+
+// dst[b][j][i] = src[b][i][j] for an (rows x cols) block at src + b*src_s (ld = cols)
+__global__ void k_transpose(const double* __restrict__ src, long long src_s, int rows, int cols,
+                            double* __restrict__ dst, long long ldd, long long dst_s) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  const double* S = src + blockIdx.z * src_s;
+  double* D = dst + blockIdx.z * dst_s;
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int r = by + k, c = bx + threadIdx.x;
+    tile[k][threadIdx.x] = (r < rows && c < cols) ? S[static_cast<long long>(r) * cols + c] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int c = bx + k, r = by + threadIdx.x;  // dst row c, col r
+    if (c < cols && r < rows) D[static_cast<long long>(c) * ldd + r] = tile[threadIdx.x][k];
+  }
+}
+
+// dst (rows x ldd) = src (rows x cols, ld = cols)
+__global__ void k_copy2d(const double* __restrict__ src, int rows, int cols,
+                         double* __restrict__ dst, long long ldd) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<long long>(rows) * cols) return;
+  const long long r = idx / cols, c = idx - r * cols;
+  dst[r * ldd + c] = src[idx];
+}
+
+__global__ void k_candidates(const double* __restrict__ theta, const double* __restrict__ delta,
+                             const double* __restrict__ etas, long long n,
+                             double* __restrict__ out) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  if (delta == nullptr) {  // explicit candidate stack (loss_many of residuals.py:188-201)
+    out[blockIdx.y * n + k] = theta[blockIdx.y * n + k];
+  } else {
+    out[blockIdx.y * n + k] = fma(etas[blockIdx.y], delta[k], theta[k]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_half_sumsq(const double* __restrict__ r, long long m,
+                                                      double* __restrict__ out) {
+  __shared__ double sh[8];
+  const double* x = r + blockIdx.x * m;
+  double s = 0.0;
+  for (long long k = threadIdx.x; k < m; k += 256) s = fma(x[k], x[k], s);
+  s = block_sum<256>(s, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = 0.5 * s;
+}
+
+// ------------------------------------------------------------------ host
+
+struct Plan {
+  int L;
+  std::vector<long long> w, off, ld;  // widths, layer offsets in theta, padded widths
+  long long n, m, R, wmax, ldmax;
+  Classes T;
+};
+
+static int make_plan(dngd_ctx* ctx, const dngd_mlp_desc* mlp, const dngd_class_desc* cls,
+                     int nclass, Plan& P) {
+  if (!mlp || mlp->nlayers < 2 || mlp->nlayers > DNGD_MAX_LAYERS) {
+    return set_error(ctx, DNGD_ERR_UNSUPPORTED, "pinn: need 2..8 affine layers");
+  }
+  if (nclass < 1 || nclass > MAXC) {
+    return set_error(ctx, DNGD_ERR_UNSUPPORTED, "pinn: need 1..4 residual classes");
+  }
+  P.L = mlp->nlayers;
+  P.w.assign(mlp->widths, mlp->widths + P.L + 1);
+  if (P.w[P.L] != 1) return set_error(ctx, DNGD_ERR_DIMENSION, "pinn: scalar output required");
+  P.off.resize(P.L);
+  long long off = 0;
+  P.wmax = 0;
+  for (int k = 0; k < P.L; ++k) {
+    P.off[k] = off;
+    off += (P.w[k] + 1) * P.w[k + 1];
+    if (k >= 1) P.wmax = std::max(P.wmax, P.w[k]);
+  }
+  P.n = off;
+  P.ld.resize(P.L + 1);
+  for (int k = 0; k <= P.L; ++k) P.ld[k] = ldw(P.w[k]);
+  P.ldmax = ldw(P.wmax);
+  Classes& T = P.T;
+  T.n = nclass;
+  T.din = static_cast<int>(P.w[0]);
+  long long row = 0, act = 0;
+  for (int k = 0; k < nclass; ++k) {
+    const dngd_class_desc& d = cls[k];
+    ClassDev& C = T.c[k];
+    if (d.ngrad < 0 || d.ngrad > MAXG || d.nlap < 0 || d.nlap > d.ngrad) {
+      return set_error(ctx, DNGD_ERR_UNSUPPORTED, "pinn: too many derivative channels");
+    }
+    C.row0 = row;
+    C.count = d.count;
+    C.act0 = act;
+    C.ngrad = d.ngrad;
+    C.nlap = d.nlap;
+    C.nch = 1 + d.ngrad + (d.nlap ? 1 : 0);
+    for (int g = 0; g < MAXG; ++g) {
+      C.grad_dims[g] = g < d.ngrad ? d.grad_dims[g] : 0;
+      C.cg[g] = g < d.ngrad ? d.cg[g] : 0.0;
+      C.lap_ch[g] = g < d.nlap ? 1 + d.lap_grad[g] : 0;
+      if (g < d.ngrad && (d.grad_dims[g] < 0 || d.grad_dims[g] >= T.din)) {
+        return set_error(ctx, DNGD_ERR_DOMAIN, "pinn: derivative dimension out of range");
+      }
+    }
+    C.cu = d.cu;
+    C.cl = d.cl;
+    C.weight = d.weight;
+    C.pts = d.points;
+    C.f = d.f;
+    row += d.count;
+    act += d.count * C.nch;
+  }
+  T.m = row;
+  T.R = act;
+  P.m = row;
+  P.R = act;
+  return DNGD_OK;
+}
+
+// workspace carve-out (bytes, 256-aligned)
+struct Arena {
+  char* base;
+  size_t off = 0;
+  double* take(size_t elems) {
+    double* p = reinterpret_cast<double*>(base ? base + off : nullptr);
+    off += (elems * sizeof(double) + 255) / 256 * 256;
+    return p;
+  }
+};
+
+struct AsmBufs {
+  std::vector<double*> Z, H, Zb, Wt, Wp;
+  double* Hb;
+};
+
+static void carve_assemble(const Plan& P, Arena& A, AsmBufs& B) {
+  const int L = P.L;
+  B.Z.assign(L, nullptr);
+  B.H.assign(L, nullptr);
+  B.Zb.assign(L, nullptr);
+  B.Wt.assign(L, nullptr);
+  B.Wp.assign(L, nullptr);
+  for (int k = 0; k <= L - 2; ++k) B.Z[k] = A.take(P.R * P.ld[k + 1]);
+  for (int k = 1; k <= L - 1; ++k) B.H[k] = A.take(P.R * P.ld[k]);
+  for (int k = 0; k <= L - 2; ++k) B.Zb[k] = A.take(P.R * P.ld[k + 1]);
+  B.Hb = A.take(P.R * P.ldmax);
+  for (int k = 1; k <= L - 2; ++k) {
+    B.Wt[k] = A.take(P.w[k + 1] * P.ld[k]);
+    B.Wp[k] = A.take(P.w[k] * P.ld[k + 1]);
+  }
+}
+
+struct FvvBufs {
+  std::vector<double*> H3, Wt, Vt;
+  double *P3, *Q2;
+};
+
+static void carve_fvv(const Plan& P, Arena& A, FvvBufs& B) {
+  const int L = P.L;
+  B.H3.assign(L, nullptr);
+  B.Wt.assign(L, nullptr);
+  B.Vt.assign(L, nullptr);
+  B.H3[0] = A.take(3 * P.R * P.ldmax);  // ping
+  B.H3[1] = A.take(3 * P.R * P.ldmax);  // pong
+  B.P3 = A.take(3 * P.R * P.ldmax);
+  B.Q2 = A.take(2 * P.R * P.ldmax);
+  for (int k = 1; k <= L - 2; ++k) {
+    B.Wt[k] = A.take(P.w[k + 1] * P.ld[k]);
+    B.Vt[k] = A.take(P.w[k + 1] * P.ld[k]);
+  }
+}
+
+struct LossBufs {
+  double *thetas, *Hping, *Hpong, *Z, *r;
+  std::vector<double*> Wt;
+};
+
+static void carve_loss(const Plan& P, Arena& A, LossBufs& B, int C) {
+  B.thetas = A.take(static_cast<size_t>(C) * P.n);
+  B.Hping = A.take(static_cast<size_t>(C) * P.R * P.ldmax);
+  B.Hpong = A.take(static_cast<size_t>(C) * P.R * P.ldmax);
+  B.Z = A.take(static_cast<size_t>(C) * P.R * P.ldmax);
+  B.r = A.take(static_cast<size_t>(C) * P.m);
+  B.Wt.assign(P.L, nullptr);
+  for (int k = 1; k <= P.L - 2; ++k) B.Wt[k] = A.take(static_cast<size_t>(C) * P.w[k + 1] * P.ld[k]);
+}
+
+static inline unsigned nblk(long long n, int t = 256) {
+  return static_cast<unsigned>((n + t - 1) / t);
+}
+
+// transpose W_k (rows w_k x cols w_{k+1}, ld cols) of `batch` thetas into dst (cols x ldd)
+static void launch_transpose(cudaStream_t s, const double* W, long long src_s, int rows, int cols,
+                             double* dst, long long ldd, long long dst_s, int batch) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32, batch);
+  k_transpose<<<grid, dim3(32, 8), 0, s>>>(W, src_s, rows, cols, dst, ldd, dst_s);
+}
+
+// forward through all hidden layers; Hlast receives H_{L-1}.  Used by loss_many
+// (batched over candidates) with Z scratch shared across layers.
+static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const double* thetas,
+                           int C, LossBufs& B, double** Hlast) {
+  const int L = P.L;
+  const long long act_s = P.R * P.ldmax;
+  {
+    dim3 g(nblk(P.m * P.w[1]), C);
+    k_input_fwd<<<g, 256, 0, s>>>(P.T, thetas, P.n, static_cast<int>(P.w[1]), P.ldmax, nullptr,
+                                  B.Hping, act_s);
+  }
+  double* Hcur = B.Hping;
+  double* Hnext = B.Hpong;
+  for (int k = 1; k <= L - 2; ++k) {
+    launch_transpose(s, thetas + P.off[k], P.n, static_cast<int>(P.w[k]),
+                     static_cast<int>(P.w[k + 1]), B.Wt[k], P.ld[k], P.w[k + 1] * P.ld[k], C);
+    GemmCall g;
+    g.M = P.R;
+    g.N = P.w[k + 1];
+    g.K = P.w[k];
+    g.A = Hcur;
+    g.lda = P.ldmax;
+    g.sA = act_s;
+    g.B = B.Wt[k];
+    g.ldb = P.ld[k];
+    g.sB = P.w[k + 1] * P.ld[k];
+    g.C = B.Z;
+    g.ldc = P.ldmax;
+    g.sC = act_s;
+    g.batch = C;
+    int rc = gemm_nt(ctx, s, g);
+    if (rc) return rc;
+    dim3 gr(nblk(P.m * P.w[k + 1]), C);
+    k_tanh_fwd<<<gr, 256, 0, s>>>(P.T, B.Z, Hnext, static_cast<int>(P.w[k + 1]), P.ldmax,
+                                  thetas + P.off[k] + P.w[k] * P.w[k + 1], P.n, act_s);
+    std::swap(Hcur, Hnext);
+  }
+  *Hlast = Hcur;
+  return cuda_status(ctx, cudaGetLastError(), "forward");
+}
+
+static size_t bytes_of(const Plan& P, int mode, int C) {
+  Arena A{nullptr};
+  if (mode == 0) {
+    AsmBufs b;
+    carve_assemble(P, A, b);
+  } else if (mode == 1) {
+    FvvBufs b;
+    carve_fvv(P, A, b);
+  } else {
+    LossBufs b;
+    carve_loss(P, A, b, C);
+  }
+  return A.off;
+}
+
+}  // namespace dngd
+
+using namespace dngd;
+
+extern "C" int dngd_pinn_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp,
+                                   const dngd_class_desc* classes, int nclass, int ncand,
+                                   size_t* bytes) {
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  size_t b = std::max(bytes_of(P, 0, 1), bytes_of(P, 1, 1));
+  b = std::max(b, bytes_of(P, 2, std::max(ncand, 1)));
+  *bytes = b;
+  return DNGD_OK;
+}
+
+extern "C" int dngd_assemble(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                             const double* theta, const dngd_class_desc* classes, int nclass,
+                             int64_t col_begin, int64_t col_end, double* r, double* J,
+                             int64_t ldJ, void* work, size_t work_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  if (bytes_of(P, 0, 1) > work_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "assemble: workspace too small");
+  if (P.m == 0) return DNGD_OK;
+  Arena A{static_cast<char*>(work)};
+  AsmBufs B;
+  carve_assemble(P, A, B);
+  const int L = P.L;
+  // ---- forward
+  k_input_fwd<<<nblk(P.m * P.w[1]), 256, 0, s>>>(P.T, theta, 0, static_cast<int>(P.w[1]),
+                                                  P.ld[1], B.Z[0], B.H[1], 0);
+  for (int k = 1; k <= L - 2; ++k) {
+    launch_transpose(s, theta + P.off[k], 0, static_cast<int>(P.w[k]),
+                     static_cast<int>(P.w[k + 1]), B.Wt[k], P.ld[k], 0, 1);
+    GemmCall g;
+    g.M = P.R;
+    g.N = P.w[k + 1];
+    g.K = P.w[k];
+    g.A = B.H[k];
+    g.lda = P.ld[k];
+    g.B = B.Wt[k];
+    g.ldb = P.ld[k];
+    g.C = B.Z[k];
+    g.ldc = P.ld[k + 1];
+    rc = gemm_nt(ctx, s, g);
+    if (rc) return rc;
+    k_tanh_fwd<<<nblk(P.m * P.w[k + 1]), 256, 0, s>>>(P.T, B.Z[k], B.H[k + 1],
+                                                      static_cast<int>(P.w[k + 1]), P.ld[k + 1],
+                                                      theta + P.off[k] + P.w[k] * P.w[k + 1], 0,
+                                                      0);
+  }
+  const long long wl_off = P.off[L - 1];
+  k_head<<<nblk(P.m, 8), 256, 0, s>>>(P.T, B.H[L - 1], static_cast<int>(P.w[L - 1]),
+                                       P.ld[L - 1], theta, 0, wl_off, 0, r, 0);
+  rc = cuda_status(ctx, cudaGetLastError(), "assemble forward");
+  if (rc || J == nullptr) return rc;
+  if (col_begin < 0 || col_end > P.n || col_begin > col_end) {
+    return set_error(ctx, DNGD_ERR_DIMENSION, "assemble: column range outside [0, n]");
+  }
+  const bool jvec_ok = ((ldJ & 1) == 0) && ((reinterpret_cast<uintptr_t>(J) & 15) == 0);
+  auto jwrite = [&](int k, const double* Hk, long long ldh, const double* Zb, long long ldz) {
+    const int win = static_cast<int>(P.w[k]), wout = static_cast<int>(P.w[k + 1]);
+    const long long lo = P.off[k], hi = lo + (win + 1LL) * wout;
+    if (hi <= col_begin || lo >= col_end) return;
+    const long long E = (win + 1LL) * wout;
+    const bool vec = Zb != nullptr && jvec_ok && (wout % 2 == 0) && ((lo - col_begin) % 2 == 0);
+    if (vec) {
+      const unsigned gx = static_cast<unsigned>(std::min<long long>((E + 511) / 512, 64));
+      k_jwrite<true><<<dim3(gx, static_cast<unsigned>(P.m)), 256, 0, s>>>(
+          P.T, Hk, ldh, win, Zb, ldz, wout, lo, col_begin, col_end, J, ldJ);
+    } else {
+      const unsigned gx = static_cast<unsigned>(std::min<long long>((E + 255) / 256, 64));
+      k_jwrite<false><<<dim3(gx, static_cast<unsigned>(P.m)), 256, 0, s>>>(
+          P.T, Hk, ldh, win, Zb, ldz, wout, lo, col_begin, col_end, J, ldJ);
+    }
+  };
+  // ---- adjoint, last layer first
+  jwrite(L - 1, B.H[L - 1], P.ld[L - 1], nullptr, 0);
+  k_seed_hbar<<<nblk(P.m * P.w[L - 1]), 256, 0, s>>>(P.T, B.Hb, static_cast<int>(P.w[L - 1]),
+                                                      P.ld[L - 1], theta + wl_off);
+  for (int k = L - 2; k >= 0; --k) {
+    // Hb holds the adjoint of H_{k+1} (ld = ld[k+1]); produce Zb_k
+    k_tanh_bwd<<<nblk(P.m * P.w[k + 1]), 256, 0, s>>>(P.T, B.Z[k], B.H[k + 1], B.Hb, B.Zb[k],
+                                                      static_cast<int>(P.w[k + 1]), P.ld[k + 1]);
+    jwrite(k, k >= 1 ? B.H[k] : nullptr, k >= 1 ? P.ld[k] : 0, B.Zb[k], P.ld[k + 1]);
+    if (k >= 1) {
+      k_copy2d<<<nblk(P.w[k] * P.w[k + 1]), 256, 0, s>>>(theta + P.off[k], static_cast<int>(P.w[k]),
+                                                         static_cast<int>(P.w[k + 1]), B.Wp[k],
+                                                         P.ld[k + 1]);
+      GemmCall g;
+      g.M = P.R;
+      g.N = P.w[k];
+      g.K = P.w[k + 1];
+      g.A = B.Zb[k];
+      g.lda = P.ld[k + 1];
+      g.B = B.Wp[k];
+      g.ldb = P.ld[k + 1];
+      g.C = B.Hb;
+      g.ldc = P.ld[k];
+      rc = gemm_nt(ctx, s, g);
+      if (rc) return rc;
+    }
+  }
+  return cuda_status(ctx, cudaGetLastError(), "assemble adjoint");
+}
+
+extern "C" int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                        const double* theta, const double* v, const dngd_class_desc* classes,
+                        int nclass, double* fvv, void* work, size_t work_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  if (bytes_of(P, 1, 1) > work_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "fvv: workspace too small");
+  if (P.m == 0) return DNGD_OK;
+  Arena A{static_cast<char*>(work)};
+  FvvBufs B;
+  carve_fvv(P, A, B);
+  const int L = P.L;
+  const long long ld = P.ldmax;
+  double* Hcur = B.H3[0];
+  double* Hnext = B.H3[1];
+  k_fvv_input<<<nblk(P.m * P.w[1]), 256, 0, s>>>(P.T, theta, v, static_cast<int>(P.w[1]), ld,
+                                                  Hcur);
+  for (int k = 1; k <= L - 2; ++k) {
+    launch_transpose(s, theta + P.off[k], 0, static_cast<int>(P.w[k]),
+                     static_cast<int>(P.w[k + 1]), B.Wt[k], P.ld[k], 0, 1);
+    launch_transpose(s, v + P.off[k], 0, static_cast<int>(P.w[k]), static_cast<int>(P.w[k + 1]),
+                     B.Vt[k], P.ld[k], 0, 1);
+    GemmCall g;
+    g.M = 3 * P.R;
+    g.N = P.w[k + 1];
+    g.K = P.w[k];
+    g.A = Hcur;
+    g.lda = ld;
+    g.B = B.Wt[k];
+    g.ldb = P.ld[k];
+    g.C = B.P3;
+    g.ldc = ld;
+    rc = gemm_nt(ctx, s, g);
+    if (rc) return rc;
+    g.M = 2 * P.R;
+    g.B = B.Vt[k];
+    g.C = B.Q2;
+    rc = gemm_nt(ctx, s, g);
+    if (rc) return rc;
+    const long long boff = P.off[k] + P.w[k] * P.w[k + 1];
+    k_fvv_hidden<<<nblk(P.m * P.w[k + 1]), 256, 0, s>>>(P.T, B.P3, B.Q2, theta + boff, v + boff,
+                                                        static_cast<int>(P.w[k + 1]), ld, Hnext);
+    std::swap(Hcur, Hnext);
+  }
+  k_fvv_head<<<nblk(P.m, 8), 256, 0, s>>>(P.T, Hcur, static_cast<int>(P.w[L - 1]), ld,
+                                           theta + P.off[L - 1], v + P.off[L - 1], fvv);
+  return cuda_status(ctx, cudaGetLastError(), "fvv");
+}
+
+extern "C" int dngd_loss_many(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                              const double* theta, const double* delta, const double* etas,
+                              int ncand, const dngd_class_desc* classes, int nclass,
+                              double* losses, void* work, size_t work_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  if (ncand < 1) return DNGD_OK;
+  if (ncand > 65535) return set_error(ctx, DNGD_ERR_DIMENSION, "loss_many: too many candidates");
+  if (bytes_of(P, 2, ncand) > work_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "loss_many: workspace too small");
+  Arena A{static_cast<char*>(work)};
+  LossBufs B;
+  carve_loss(P, A, B, ncand);
+  k_candidates<<<dim3(nblk(P.n), ncand), 256, 0, s>>>(theta, delta, etas, P.n, B.thetas);
+  double* Hlast;
+  rc = forward_batched(ctx, s, P, B.thetas, ncand, B, &Hlast);
+  if (rc) return rc;
+  k_head<<<dim3(nblk(P.m, 8), ncand), 256, 0, s>>>(P.T, Hlast, static_cast<int>(P.w[P.L - 1]),
+                                                    P.ldmax, B.thetas, P.n, P.off[P.L - 1],
+                                                    P.R * P.ldmax, B.r, P.m);
+  k_half_sumsq<<<ncand, 256, 0, s>>>(B.r, P.m, losses);
+  return cuda_status(ctx, cudaGetLastError(), "loss_many");
+}

@@ -1,0 +1,203 @@
+"""Torch-tensor wrappers over the C ABI (one function per entry point).
+
+Tensors are float64 CUDA tensors owned by the caller; each call runs on the
+current torch stream.  Workspaces are cached per (device, size class) so
+steady-state steps do not allocate.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import c_size, call, ctx, ptr, stream_handle
+from .errors import DimensionError
+
+F64 = torch.float64
+
+
+def pad_ld(n: int, mult: int = 16) -> int:
+    """Leading dimension for J-like matrices: 128-byte row pitch (TMA + coalescing)."""
+    return max(mult, (int(n) + mult - 1) // mult * mult)
+
+
+class Workspace:
+    """Grow-only byte arena on the current device."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(
+            "cuda", torch.cuda.current_device()
+        ):
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        return self.buf
+
+
+_WS: dict[str, Workspace] = {}
+
+
+def workspace(tag: str, nbytes: int) -> torch.Tensor:
+    ws = _WS.get(tag)
+    if ws is None:
+        ws = _WS[tag] = Workspace()
+    return ws.get(nbytes)
+
+
+def _check2d(A: torch.Tensor, what: str):
+    if A.dtype != F64 or not A.is_cuda or A.dim() != 2 or A.stride(1) != 1:
+        raise DimensionError(f"{what} must be a row-major float64 CUDA matrix")
+
+
+# ---------------------------------------------------------------- dense path
+
+
+def syrk(J: torch.Tensor, ncols: int | None = None, K: torch.Tensor | None = None,
+         accumulate: bool = False) -> torch.Tensor:
+    """K = J[:, :ncols] J[:, :ncols]^T (full symmetric)."""
+    _check2d(J, "J")
+    m = J.shape[0]
+    ncols = J.shape[1] if ncols is None else int(ncols)
+    if K is None:
+        K = torch.empty((m, m), dtype=F64, device=J.device)
+    nb = c_size()
+    call("dngd_syrk_workspace", ctx(), m, ncols, ctypes.byref(nb))
+    ws = workspace("syrk", nb.value)
+    call("dngd_syrk", ctx(), stream_handle(), ptr(J), m, ncols, J.stride(0), ptr(K), K.stride(0),
+         1 if accumulate else 0, ptr(ws), ws.numel())
+    return K
+
+
+def shift_copy(K: torch.Tensor, lam: float, L: torch.Tensor) -> torch.Tensor:
+    call("dngd_shift_copy", ctx(), stream_handle(), ptr(K), K.shape[0], K.stride(0), float(lam),
+         ptr(L), L.stride(0))
+    return L
+
+
+class CholeskyFactor:
+    """Lower factor of K + lam I plus the stored diagonal-block inverses."""
+
+    def __init__(self, m: int, device):
+        self.m = m
+        ld = pad_ld(m, 2)
+        self.L = torch.empty((m, ld), dtype=F64, device=device)
+        nb = c_size()
+        call("dngd_potrf_workspace", ctx(), m, ctypes.byref(nb))
+        self.dinv = torch.empty(max(1, nb.value // 8), dtype=F64, device=device)
+        self.info = torch.zeros(1, dtype=torch.int32, device=device)
+        nblk = (m + 63) // 64
+        self.flags = torch.zeros(2 * nblk + 2, dtype=torch.int32, device=device)
+
+    def factor(self, K: torch.Tensor, lam: float) -> None:
+        """Async: L = chol(lower(K) + lam I); self.info receives the failing column."""
+        shift_copy(K, lam, self.L)
+        call("dngd_potrf", ctx(), stream_handle(), ptr(self.L), self.m, self.L.stride(0),
+             ptr(self.dinv), ptr(self.info))
+
+    def solve_(self, b: torch.Tensor) -> torch.Tensor:
+        """b <- (L L^T)^{-1} b in place."""
+        call("dngd_potrs", ctx(), stream_handle(), ptr(self.L), self.m, self.L.stride(0),
+             ptr(self.dinv), ptr(b), ptr(self.flags))
+        return b
+
+
+def gemv_t(J: torch.Tensor, y: torch.Tensor, ncols: int | None = None, g: torch.Tensor | None = None,
+           scale: float = 1.0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out = scale * (J^T y + g)."""
+    _check2d(J, "J")
+    m = J.shape[0]
+    ncols = J.shape[1] if ncols is None else int(ncols)
+    if out is None:
+        out = torch.empty(ncols, dtype=F64, device=J.device)
+    nb = c_size()
+    call("dngd_gemv_t_workspace", ctx(), m, ncols, ctypes.byref(nb))
+    ws = workspace("gemv_t", nb.value)
+    call("dngd_gemv_t", ctx(), stream_handle(), ptr(J), m, ncols, J.stride(0), ptr(y), ptr(g),
+         float(scale), ptr(out), ptr(ws), ws.numel())
+    return out
+
+
+def gemv_n(A: torch.Tensor, x: torch.Tensor, ncols: int | None = None, alpha: float = 1.0,
+           add: torch.Tensor | None = None, beta: float = 0.0,
+           out: torch.Tensor | None = None) -> torch.Tensor:
+    """out = alpha * A[:, :ncols] x + beta * add."""
+    _check2d(A, "A")
+    m = A.shape[0]
+    ncols = A.shape[1] if ncols is None else int(ncols)
+    if out is None:
+        out = torch.empty(m, dtype=F64, device=A.device)
+    call("dngd_gemv_n", ctx(), stream_handle(), ptr(A), m, ncols, A.stride(0), ptr(x), float(alpha),
+         ptr(add), float(beta), ptr(out))
+    return out
+
+
+def gemm_nt(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor | None = None, K: int | None = None,
+            alpha: float = 1.0, beta: float = 0.0, lower: bool = False) -> torch.Tensor:
+    """C = alpha * A[:, :K] B[:, :K]^T + beta * C on the FP64 tensor cores."""
+    _check2d(A, "A")
+    _check2d(B, "B")
+    M, N = A.shape[0], B.shape[0]
+    K = A.shape[1] if K is None else int(K)
+    if C is None:
+        C = torch.empty((M, pad_ld(N, 2)), dtype=F64, device=A.device)[:, :N]
+    call("dngd_gemm_nt", ctx(), stream_handle(), M, N, K, ptr(A), A.stride(0), 0, ptr(B),
+         B.stride(0), 0, ptr(C), C.stride(0), 0, 1, float(alpha), float(beta), 1 if lower else 0)
+    return C
+
+
+def dot(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(1, dtype=F64, device=x.device)
+    call("dngd_dot", ctx(), stream_handle(), x.numel(), ptr(x), ptr(y), ptr(out))
+    return out
+
+
+def axpby(a: float, x: torch.Tensor, b: float = 0.0, y: torch.Tensor | None = None,
+          out: torch.Tensor | None = None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty_like(x)
+    call("dngd_axpby", ctx(), stream_handle(), x.numel(), float(a), ptr(x), float(b), ptr(y),
+         ptr(out))
+    return out
+
+
+# ---------------------------------------------------------------- PINN map
+
+
+def mlp_desc(widths) -> _lib.MlpDesc:
+    d = _lib.MlpDesc()
+    d.nlayers = len(widths) - 1
+    if d.nlayers > _lib.MAX_LAYERS:
+        raise DimensionError(f"at most {_lib.MAX_LAYERS} layers are supported")
+    for k, w in enumerate(widths):
+        d.widths[k] = int(w)
+    return d
+
+
+def pinn_workspace_bytes(mlp, classes_arr, nclass: int, ncand: int) -> int:
+    nb = c_size()
+    call("dngd_pinn_workspace", ctx(), ctypes.byref(mlp), classes_arr, nclass, ncand,
+         ctypes.byref(nb))
+    return nb.value
+
+
+def assemble(mlp, theta, classes_arr, nclass, r, J=None, col_begin=0, col_end=None, ws=None):
+    n = sum((mlp.widths[k] + 1) * mlp.widths[k + 1] for k in range(mlp.nlayers))
+    col_end = n if col_end is None else col_end
+    call("dngd_assemble", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), classes_arr, nclass,
+         int(col_begin), int(col_end), ptr(r), ptr(J), 0 if J is None else J.stride(0), ptr(ws),
+         0 if ws is None else ws.numel())
+
+
+def fvv(mlp, theta, v, classes_arr, nclass, out, ws):
+    call("dngd_fvv", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), ptr(v), classes_arr,
+         nclass, ptr(out), ptr(ws), ws.numel())
+
+
+def loss_many(mlp, theta, delta, etas, ncand, classes_arr, nclass, out, ws):
+    call("dngd_loss_many", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), ptr(delta),
+         ptr(etas), int(ncand), classes_arr, nclass, ptr(out), ptr(ws), ws.numel())

@@ -1,0 +1,114 @@
+"""GPU parity of the individual CUDA kernels against the numpy oracle.
+
+Run on a B200 (pytest -m gpu).  Every product call goes through the C ABI.
+"""
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+from oracle import dngd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2505_21404_b200 import kernels
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    return kernels
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("m,n", [(1, 5), (37, 1185), (200, 333), (300, 4099), (1020, 1185), (520, 12737)])
+def test_syrk_matches_oracle(K, m, n):
+    from tests.gpu_util import dev
+    rng = np.random.default_rng(m + n)
+    Jh = rng.normal(size=(m, n))
+    ld = K.pad_ld(n)
+    J = torch.zeros((m, ld), dtype=torch.float64, device="cuda")
+    J[:, :n] = dev(Jh)
+    Kd = K.syrk(J, n).cpu().numpy()
+    Kref = O.gram(Jh)
+    assert _rel(Kd, Kref) <= 1e-13  # north star: Gram rel err <= 1e-12
+    assert np.array_equal(Kd, Kd.T)
+    # determinism: bitwise identical on repeat
+    assert np.array_equal(K.syrk(J, n).cpu().numpy(), Kd)
+
+
+@pytest.mark.parametrize("M,N,Kd,lower", [(100, 64, 64, False), (257, 32, 64, False),
+                                            (300, 300, 70, True), (1000, 250, 33, False)])
+def test_gemm_nt(K, M, N, Kd, lower):
+    from tests.gpu_util import dev
+    rng = np.random.default_rng(M * N)
+    A = rng.normal(size=(M, Kd))
+    B = rng.normal(size=(N, Kd))
+    C0 = rng.normal(size=(M, N))
+    lda = K.pad_ld(Kd, 2)
+    Ad = torch.zeros((M, lda), dtype=torch.float64, device="cuda"); Ad[:, :Kd] = dev(A)
+    Bd = torch.zeros((N, lda), dtype=torch.float64, device="cuda"); Bd[:, :Kd] = dev(B)
+    Cd = torch.zeros((M, K.pad_ld(N, 2)), dtype=torch.float64, device="cuda")
+    Cd[:, :N] = dev(C0)
+    K.gemm_nt(Ad, Bd, Cd[:, :N], K=Kd, alpha=-1.5, beta=0.5, lower=lower)
+    ref = -1.5 * A @ B.T + 0.5 * C0
+    got = Cd[:, :N].cpu().numpy()
+    if lower:
+        mask = np.tril(np.ones((M, N), bool))
+        assert _rel(got[mask], ref[mask]) <= 1e-13
+        assert np.array_equal(got[~mask], C0[~mask])
+    else:
+        assert _rel(got, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("m", [5, 64, 100, 1020, 2800])
+def test_potrf_potrs(K, m):
+    from tests.gpu_util import dev
+    rng = np.random.default_rng(m)
+    A = rng.normal(size=(m, m + 7))
+    Km = A @ A.T / m
+    lam = 1e-3
+    Kd = dev(Km)
+    fac = K.CholeskyFactor(m, Kd.device)
+    fac.factor(Kd, lam)
+    assert int(fac.info.item()) == 0
+    Lref = np.linalg.cholesky(Km + lam * np.eye(m))
+    Lg = np.tril(fac.L[:, :m].cpu().numpy())
+    assert _rel(Lg, Lref) <= 1e-12
+    b = rng.normal(size=m)
+    bd = dev(b)
+    fac.solve_(bd)
+    y = scipy.linalg.cho_solve((Lref, True), b)
+    assert _rel(bd.cpu().numpy(), y) <= 1e-10
+    res = (Km + lam * np.eye(m)) @ bd.cpu().numpy() - b
+    assert np.linalg.norm(res) / (np.linalg.norm(Km) * np.linalg.norm(y) + np.linalg.norm(b)) <= 1e-14
+
+
+def test_potrf_reports_failing_column(K):
+    from tests.gpu_util import dev
+    m = 130
+    Km = np.eye(m)
+    Km[70, 70] = -5.0
+    fac = K.CholeskyFactor(m, "cuda")
+    fac.factor(dev(Km), 1e-3)
+    assert int(fac.info.item()) == 71
+
+
+@pytest.mark.parametrize("m,n", [(3, 10), (1020, 1185), (2800, 12737), (64, 100000)])
+def test_gemv(K, m, n):
+    from tests.gpu_util import dev
+    rng = np.random.default_rng(n)
+    Jh = rng.normal(size=(m, n))
+    J = torch.zeros((m, K.pad_ld(n)), dtype=torch.float64, device="cuda")
+    J[:, :n] = dev(Jh)
+    y, g, x = rng.normal(size=m), rng.normal(size=n), rng.normal(size=n)
+    out = K.gemv_t(J, dev(y), n, dev(g), scale=-0.25).cpu().numpy()
+    assert _rel(out, -0.25 * (Jh.T @ y + g)) <= 1e-13
+    add = rng.normal(size=m)
+    out = K.gemv_n(J, dev(x), n, alpha=2.0, add=dev(add), beta=0.5).cpu().numpy()
+    assert _rel(out, 2.0 * Jh @ x + 0.5 * add) <= 1e-13

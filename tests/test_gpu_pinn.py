@@ -1,0 +1,89 @@
+"""GPU parity of the PINN residual-map kernels (assembly, f_vv, loss_many)."""
+
+import numpy as np
+import pytest
+
+from oracle import dngd_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+CASES = [
+    ("poisson2d", O.OraclePoisson2d(), (2, 32, 32, 1), (90, 30)),
+    ("heat1d", O.OracleHeat1d(), (2, 64, 64, 64, 64, 1), (60, 20, 20)),
+    ("poisson5d", O.OraclePoissonSin(5), (5, 32, 32, 32, 32, 1), (40, 12)),
+    ("poisson5d_wide", O.OraclePoissonSin(5), (5, 128, 96, 1), (20, 10)),
+]
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def K():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    from paper_2505_21404_b200 import kernels
+    return kernels
+
+
+def _setup(K, problem, widths, counts, seed):
+    from tests.gpu_util import class_descs, dev
+    rng = np.random.default_rng(seed)
+    classes = problem.sample(counts, rng)
+    theta = O.xavier_normal_init(widths, seed)
+    arr, keep = class_descs(classes)
+    mlp = K.mlp_desc(widths)
+    nb = K.pinn_workspace_bytes(mlp, arr, len(classes), 31)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    return classes, theta, arr, keep, mlp, ws, dev(theta)
+
+
+@pytest.mark.parametrize("name,problem,widths,counts", CASES)
+def test_assemble_matches_oracle(K, name, problem, widths, counts):
+    classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 3)
+    r_ref, J_ref = O.linearize(theta, widths, classes)
+    m, n = J_ref.shape
+    r = torch.empty(m, dtype=torch.float64, device="cuda")
+    J = torch.full((m, K.pad_ld(n)), np.nan, dtype=torch.float64, device="cuda")
+    K.assemble(mlp, th, arr, len(classes), r, J, 0, n, ws)
+    torch.cuda.synchronize()
+    assert _rel(r.cpu().numpy(), r_ref) <= 1e-12
+    Jg = J[:, :n].cpu().numpy()
+    assert np.all(np.isfinite(Jg))
+    assert _rel(Jg, J_ref) <= 1e-12
+    # column-sharded assembly (multi-GPU layout): an odd and an even split
+    for c0, c1 in [(0, n // 3), (n // 3 + 1, n), (2, n - 3)]:
+        c0 -= c0 % 2
+        Js = torch.full((m, K.pad_ld(c1 - c0)), np.nan, dtype=torch.float64, device="cuda")
+        K.assemble(mlp, th, arr, len(classes), r, Js, c0, c1, ws)
+        assert np.array_equal(Js[:, : c1 - c0].cpu().numpy(), Jg[:, c0:c1])
+
+
+@pytest.mark.parametrize("name,problem,widths,counts", CASES)
+def test_fvv_matches_oracle(K, name, problem, widths, counts):
+    from tests.gpu_util import dev
+    classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 4)
+    v = np.random.default_rng(9).normal(size=theta.size)
+    ref = O.second_directional(theta, widths, classes, v)
+    out = torch.empty(ref.size, dtype=torch.float64, device="cuda")
+    K.fvv(mlp, th, dev(v), arr, len(classes), out, ws)
+    assert _rel(out.cpu().numpy(), ref) <= 1e-11
+
+
+@pytest.mark.parametrize("name,problem,widths,counts", CASES)
+def test_loss_many_matches_oracle(K, name, problem, widths, counts):
+    from tests.gpu_util import dev
+    classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 5)
+    delta = 0.3 * np.random.default_rng(10).normal(size=theta.size)
+    etas = 2.0 ** -np.arange(31, dtype=np.float64)
+    cands = theta[None, :] + etas[:, None] * delta[None, :]
+    ref = O.loss_many(cands, widths, classes)
+    out = torch.empty(31, dtype=torch.float64, device="cuda")
+    K.loss_many(mlp, th, dev(delta), dev(etas), 31, arr, len(classes), out, ws)
+    np.testing.assert_allclose(out.cpu().numpy(), ref, rtol=1e-12)
+    # explicit candidate stack
+    out2 = torch.empty(31, dtype=torch.float64, device="cuda")
+    K.loss_many(mlp, dev(cands), None, None, 31, arr, len(classes), out2, ws)
+    np.testing.assert_allclose(out2.cpu().numpy(), ref, rtol=1e-12)

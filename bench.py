@@ -1,0 +1,442 @@
+"""D-NGD step benchmark (BASELINE.json metric: "D-NGD steps/s; Gram+Cholesky FP64
+TFLOP/s and matvec GB/s vs peak").
+
+Workload at N=1: BASELINE config 2 (configs[1]) -- 1-D heat u_t = 0.1 u_xx,
+three residual classes 2000 + 400 + 400 (m = 2800), MLP 2 -> 64x4 -> 1 tanh
+(n = 12,737), Xavier-normal init, FP64, dense D-NGD with geodesic correction,
+31-point line search.  One "step" = one full outer iteration of the reference
+loop (optimizer.py:212-262): residuals + Jacobian, gradient, damping, Gram,
+Cholesky (+ retries), GN solve, f_vv, GA solve, line search, parameter update.
+
+  value : steps/s with every step's collocation points already resident in HBM
+  e2e   : steps/s through the public API (dngd_run) with host-side sampling,
+          host->device upload of the points/data and device->host reads of the
+          per-step scalars inside the timed region
+  --impl reference : the CPU oracle (oracle/dngd_oracle.py, a numpy port of the
+          reference algorithm) on the host cores, same workload
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                       [--config 1|2|3|5]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs (1-based)
+    1: dict(problem="poisson2d", widths=(2, 32, 32, 1), counts=(900, 120), lam_cap=1e-8,
+            dense_threshold=4000, name="cfg1_poisson2d_2-32-32-1_m1020"),
+    2: dict(problem="heat1d", widths=(2, 64, 64, 64, 64, 1), counts=(2000, 400, 400), lam_cap=1e-3,
+            dense_threshold=4000, name="cfg2_heat1d_2-64x4-1_m2800"),
+    3: dict(problem="poisson5d_sin", widths=(5, 512, 512, 512, 512, 1), counts=(3500, 500),
+            lam_cap=1e-5, dense_threshold=4001, name="cfg3_poisson5d_5-512x4-1_m4000"),
+    5: dict(problem="poisson2d", widths=(2, 256, 256, 256, 256, 1), counts=(30000, 2000),
+            lam_cap=1e-5, dense_threshold=4000, nystrom_rank=512, cg_max_iters=200,
+            name="cfg5_poisson2d_2-256x4-1_m32000_pcg"),
+}
+METRIC = "D-NGD steps/s"
+UNIT = "steps/s"
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(
+        os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ our arm
+
+
+def _fp64_peak():
+    """Measured FP64 tensor peak on this GPU: cuBLAS DGEMM 8192^3 (MEASURED_PEAKS.json has
+    no FP64 figure).  Best of 3 after warm-up."""
+    import torch
+
+    N = 8192
+    A = torch.randn(N, N, dtype=torch.float64, device="cuda")
+    B = torch.randn(N, N, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        A @ B
+    best = 0.0
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        A @ B
+        e.record()
+        torch.cuda.synchronize()
+        best = max(best, 2 * N**3 / (s.elapsed_time(e) * 1e-3) / 1e12)
+    del A, B
+    torch.cuda.empty_cache()
+    return best
+
+
+def _hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback B200_PROFILING.md"
+
+
+def _count_our_kernels(fn):
+    """Number of libdngd_b200 kernels one call of fn launches (CUPTI via torch.profiler)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    n = 0
+    for ev in prof.events():
+        if ev.device_type == torch.autograd.DeviceType.CUDA and "dngd::" in ev.name:
+            n += 1
+    return n
+
+
+def run_ours(args, cfg):
+    import torch
+
+    import paper_2505_21404_b200 as P
+    from paper_2505_21404_b200 import kernels as K
+    from paper_2505_21404_b200 import timing
+    from paper_2505_21404_b200.optimizer import device_line_search, lm_damping
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    problem = P.make_problem(cfg["problem"])
+    spec = P.MlpSpec(cfg["widths"], seed=0)
+    config = P.OptimizerConfig(max_iters=args.warmup + args.steps, lam_cap=cfg["lam_cap"],
+                               dense_threshold=cfg["dense_threshold"],
+                               nystrom_rank=cfg.get("nystrom_rank", 64),
+                               cg_max_iters=cfg.get("cg_max_iters", 500))
+    fp64_peak = _fp64_peak()
+    hbm_peak, hbm_src = _hbm_peak()
+
+    # -------- device-resident run: all collocation sets uploaded before timing
+    rng = np.random.default_rng(1000 + rank)
+    total = args.warmup + args.steps
+    maps = []
+    base = None
+    for _ in range(total):
+        colloc = P.sample_collocation(problem, cfg["counts"], rng)
+        mp = P.PinnResidualMap(problem, spec, colloc) if base is None else base.rebind(colloc)
+        mp._J = None  # each map owns its Jacobian buffer? no: share one (rebind below)
+        maps.append(mp)
+        base = mp
+    for mp in maps:
+        mp._device()  # upload points and data now
+    shared_J = None
+    theta = P.xavier_normal_params(spec)
+    theta = P.ParameterVector(theta.tensor, theta.layout)
+
+    def one_step(rmap, theta):
+        nonlocal shared_J
+        rmap._J = shared_J
+        r, J = rmap.linearize_t(theta)
+        shared_J = rmap._J
+        loss = 0.5 * float(K.dot(r, r).item())
+        with timing.stage("gemv"):
+            g = K.gemv_t(J, r, rmap.n)
+        lam = lm_damping(loss, config.lam_cap)
+        from paper_2505_21404_b200.optimizer import _dispatch_step
+
+        step = _dispatch_step(rmap, theta, g, lam, config, rng)
+        ls = device_line_search(rmap, theta, step.delta.tensor, loss, config.line_search_points)
+        if ls.rejected:
+            return theta, step
+        return P.ParameterVector(K.axpby(ls.eta, step.delta.tensor, 1.0, theta.tensor),
+                                 theta.layout), step
+
+    for i in range(args.warmup):
+        theta, _ = one_step(maps[i], theta)
+    launches = _count_our_kernels(lambda: one_step(maps[args.warmup], theta))
+    clocks = ClockSampler(local)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks.start()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with timing.collect() as tm:
+        s.record()
+        for i in range(args.steps):
+            theta, last = one_step(maps[args.warmup + i], theta)
+        e.record()
+        torch.cuda.synchronize()
+        stages, counts = tm.summary_ms()
+    dev_s = s.elapsed_time(e) * 1e-3
+    if dist:
+        t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+    clk = clocks.stop()
+
+    # -------- end to end through the public API (dngd_run): host sampling + H2D + D2H
+    e2e = {}
+    bytes_in = []
+
+    orig_device = P.PinnResidualMap._device
+
+    def counting_device(self):
+        fresh = self._dev is None
+        d = orig_device(self)
+        if fresh:
+            bytes_in.append(sum(t.numel() * t.element_size() for t in d["keep"]))
+        return d
+
+    P.PinnResidualMap._device = counting_device
+    marks = {}
+
+    def on_step(it, th, step, ls):
+        if it == args.warmup:
+            torch.cuda.synchronize()
+            marks["t0"] = time.perf_counter()
+        if it == args.warmup + args.steps:
+            torch.cuda.synchronize()
+            marks["t1"] = time.perf_counter()
+
+    try:
+        tr = P.dngd_run(problem, spec, config, seed=rank, counts=cfg["counts"],
+                        init="xavier_normal", track_rel_l2=False, on_step=on_step)
+    finally:
+        P.PinnResidualMap._device = orig_device
+    if "t0" in marks and "t1" in marks:
+        e2e_s = marks["t1"] - marks["t0"]
+        if dist:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        h2d = int(np.median(bytes_in)) if bytes_in else 0
+        # per step the host reads: loss (8 B), |v|, |a| (16 B), Cholesky info (4 B),
+        # 31 line-search losses (248 B), the delta-nonzero flag (1 B)
+        d2h = 8 + 16 + 4 + 8 * config.line_search_points + 1
+        e2e = {"value": world * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "aborted": tr.aborted}
+
+    # -------- roofline of the dominant kernel
+    m = sum(cfg["counts"])
+    n = spec.param_count()
+    ms_per_step = dev_s / args.steps * 1e3
+    stage_ms = {k: v / args.steps for k, v in stages.items()}
+    syrk_avg = stages.get("syrk", 0.0) / max(counts.get("syrk", 1), 1) * 1e-3
+    potrf_avg = stages.get("potrf", 0.0) / max(counts.get("potrf", 1), 1) * 1e-3
+    roof = None
+    if syrk_avg > 0:
+        flops = m * (m + 1) * n
+        ach = flops / syrk_avg / 1e12
+        roof = {"kernel": "dngd::k_gemm_nt<128,128> (SYRK K=JJ^T, lower tiles, split-K)",
+                "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": ach / fp64_peak, "traffic": None,
+                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
+                "algorithmic": f"m(m+1)n = {flops:.3e} FLOP per launch"}
+    gram_chol = None
+    if syrk_avg > 0 and potrf_avg > 0:
+        gf = (m * (m + 1) * n + m**3 / 3) / (syrk_avg + potrf_avg) / 1e12
+        gram_chol = {"tflops": gf, "frac_of_fp64_peak": gf / fp64_peak,
+                     "syrk_ms": syrk_avg * 1e3, "potrf_ms": potrf_avg * 1e3}
+    gemv_bytes = 8 * m * n
+    line = {
+        "metric": METRIC,
+        "value": world * args.steps / dev_s,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded collocation sampling; Xavier-normal random init)",
+        "config": {"workload": cfg["name"], "m": m, "n": n, "widths": list(cfg["widths"]),
+                   "solver": "dense Cholesky + geodesic acceleration" if m < cfg["dense_threshold"]
+                   else "Nystrom-PCG", "lam_cap": cfg["lam_cap"], "line_search_points": 31,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "per-step working set exceeds L2 (J = %.0f MB rewritten every step)"
+                   % (8 * m * n / 1e6)},
+        "roofline": roof,
+        "gram_cholesky": gram_chol,
+        "stages_ms_per_step": stage_ms,
+        "gemv_bytes_per_launch": gemv_bytes,
+        "hbm_peak_gbs": hbm_peak,
+        "hbm_peak_source": hbm_src,
+        "fp64_peak_tflops": fp64_peak,
+        "e2e": e2e or None,
+        "gpu_launches": launches * args.steps,
+        "clocks": clk,
+        "final_loss": float(0.5 * float(maps[-1].residuals_t(theta).norm().item() ** 2)),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, max_seconds=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ CPU oracle arm
+
+
+def _oracle_problem(name):
+    from oracle import dngd_oracle as O
+
+    return {"poisson2d": O.OraclePoisson2d(), "heat1d": O.OracleHeat1d(),
+            "poisson5d_sin": O.OraclePoissonSin(5)}[name]
+
+
+def cpu_baseline(cfg, max_seconds=25.0, warmup=1):
+    """The numpy oracle (a port of the reference algorithm) on this host's cores, bounded
+    to ~max_seconds of CPU work on the same workload."""
+    from oracle import dngd_oracle as O
+
+    cores = os.cpu_count()
+    problem = _oracle_problem(cfg["problem"])
+    lc = O.LoopConfig(lam_cap=cfg["lam_cap"], dense_threshold=cfg["dense_threshold"],
+                      nystrom_rank=cfg.get("nystrom_rank", 64),
+                      cg_max_iters=cfg.get("cg_max_iters", 500), max_iters=1)
+    times = []
+    t_start = time.perf_counter()
+    state = {}
+
+    def hook_factory():
+        def hook(it, theta, classes, lam):
+            return None
+        return hook
+
+    # time individual full steps of the oracle loop (resample + J + Gram + solves + LS)
+    rng = np.random.default_rng(0)
+    theta = O.xavier_normal_init(cfg["widths"], 0)
+    steps_done = 0
+    while True:
+        classes = problem.sample(cfg["counts"], rng)
+        t0 = time.perf_counter()
+        r, J = O.linearize(theta, cfg["widths"], classes)
+        g = J.T @ r
+        cur = 0.5 * float(r @ r)
+        lam = O.lm_damping(cur, lc.lam_cap)
+        if J.shape[0] < lc.dense_threshold:
+            step = O.dense_dual_solve(J, g, lam, True,
+                                      lambda v: O.second_directional(theta, cfg["widths"], classes, v))
+        else:
+            step = O.pcg_step(J, g, lam, lc.nystrom_rank, lc.cg_tol, lc.cg_max_iters, rng)
+        ls = O.line_search(lambda c: O.loss_many(c, cfg["widths"], classes), theta, step.delta,
+                           cur, lc.line_search_points)
+        if not ls.rejected:
+            theta = theta + ls.eta * step.delta
+        dt = time.perf_counter() - t0
+        steps_done += 1
+        if steps_done > warmup:
+            times.append(dt)
+        if time.perf_counter() - t_start > max_seconds and times:
+            break
+    v = len(times) / sum(times)
+    return {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{len(times)} full oracle steps of {cfg['name']} after {warmup} warm-up "
+                      f"(numpy/OpenBLAS, {cores} threads)"}
+
+
+def run_reference(args, cfg):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return
+    budget = float(os.environ.get("DNGD_REF_SECONDS", "150"))
+    res = cpu_baseline(cfg, max_seconds=budget, warmup=min(args.warmup, 1))
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / res["value"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded collocation sampling; Xavier-normal random init)",
+        "config": {"workload": cfg["name"], "m": sum(cfg["counts"]),
+                   "widths": list(cfg["widths"])},
+        "impl": "reference",
+        "cpu_baseline": res,
+        "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=25.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 1)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,372 @@
+"""Outer D-NGD loop on the GPU backend (reference optimizer.py:1-314).
+
+Same configuration schema (OptimizerConfig fields and validation), damping
+rule, line-search semantics, rejection ladder, trace rows and seeding
+discipline as the reference, so traces are row-for-row comparable.  The
+parameters, residuals, Jacobian and all step algebra stay on the device; per
+iteration the host sees a handful of scalars (loss, lambda, 31 line-search
+losses, GA ratio) and the freshly sampled collocation points it uploads.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from .errors import ConfigError, DomainError
+from .model import INITIALIZERS, MlpSpec
+from .params import ParameterVector
+from .residuals import PinnResidualMap, ResidualMap
+from .solver import StepResult, dense_dual_solve, pcg_step
+from .timing import stage
+
+LAMBDA_FLOOR = 1e-12
+MAX_CONSECUTIVE_REJECTIONS = 10
+
+
+@dataclass(frozen=True)
+class OptimizerConfig:
+    """Knobs of the outer loop; exactly one budget kind must be set (optimizer.py:26-71)."""
+
+    lam_cap: float = 1e-5
+    dense_threshold: int = 4000
+    nystrom_rank: int = 64
+    cg_tol: float = 1e-10
+    cg_max_iters: int = 500
+    use_ga: bool = True
+    line_search_points: int = 31
+    max_iters: int | None = None
+    wall_seconds: float | None = None
+    resample: bool = True
+    reject_if_worse: bool = False
+    deterministic_timing: bool = False
+
+    def __post_init__(self):
+        if self.lam_cap <= 0.0:
+            raise ConfigError(f"lam_cap must be positive, got {self.lam_cap}", "lam_cap")
+        if self.line_search_points < 1:
+            raise ConfigError(
+                f"line_search_points must be >= 1, got {self.line_search_points}",
+                "line_search_points",
+            )
+        if self.dense_threshold < 1:
+            raise ConfigError(
+                f"dense_threshold must be >= 1, got {self.dense_threshold}", "dense_threshold"
+            )
+        if self.nystrom_rank < 1:
+            raise ConfigError(f"nystrom_rank must be >= 1, got {self.nystrom_rank}", "nystrom_rank")
+        if self.cg_tol <= 0.0 or self.cg_max_iters < 1:
+            raise ConfigError("CG tolerance and iteration cap must be positive", "cg_tol")
+        if (self.max_iters is None) == (self.wall_seconds is None):
+            raise ConfigError("exactly one of max_iters / wall_seconds must be set", "max_iters")
+        if self.max_iters is not None and self.max_iters < 1:
+            raise ConfigError(f"max_iters must be >= 1, got {self.max_iters}", "max_iters")
+        if self.wall_seconds is not None and self.wall_seconds <= 0.0:
+            raise ConfigError(
+                f"wall_seconds must be positive, got {self.wall_seconds}", "wall_seconds"
+            )
+
+
+@dataclass
+class TraceRow:
+    iteration: int
+    wall_time: float
+    loss: float
+    rel_l2: float = float("nan")
+    lam: float = float("nan")
+    eta: float = float("nan")
+    cg_iterations: int = 0
+    ga_ratio: float = float("nan")
+
+
+@dataclass
+class TrainTrace:
+    problem: str
+    method: str
+    seed: int
+    rows: list[TraceRow] = field(default_factory=list)
+    final_theta: ParameterVector | None = None
+    aborted: bool = False
+    abort_reason: str | None = None
+    diverged: bool = False
+
+    @property
+    def final_loss(self) -> float:
+        return self.rows[-1].loss if self.rows else float("nan")
+
+    @property
+    def final_rel_l2(self) -> float:
+        return self.rows[-1].rel_l2 if self.rows else float("nan")
+
+
+class _Clock:
+    """Strictly increasing stamps; logical ticks in deterministic mode (optimizer.py:110-129)."""
+
+    def __init__(self, deterministic: bool):
+        self.deterministic = deterministic
+        self.t0 = time.monotonic()
+        self.ticks = 0
+        self.last = 0.0
+
+    def stamp(self) -> float:
+        self.ticks += 1
+        if self.deterministic:
+            t = float(self.ticks)
+        else:
+            t = max(time.monotonic() - self.t0, self.last + 1e-9)
+        self.last = t
+        return t
+
+    def elapsed(self) -> float:
+        return time.monotonic() - self.t0
+
+
+def lm_damping(loss: float, lam_cap: float) -> float:
+    """optimizer.py:132-136."""
+    if loss < 0.0:
+        raise DomainError(f"loss must be nonnegative, got {loss}")
+    return max(min(loss, lam_cap), LAMBDA_FLOOR)
+
+
+@dataclass
+class LineSearchResult:
+    eta: float | None
+    loss: float
+    degraded: bool
+    evaluations: int
+    rejected: bool
+
+
+def _select(losses: np.ndarray, etas: np.ndarray, current_loss, points_count) -> LineSearchResult:
+    finite = np.isfinite(losses)
+    if not finite.any():
+        return LineSearchResult(None, float("nan"), False, points_count, True)
+    j = int(np.argmin(np.where(finite, losses, np.inf)))
+    degraded = current_loss is not None and losses[j] > current_loss
+    return LineSearchResult(float(etas[j]), float(losses[j]), degraded, points_count, False)
+
+
+def line_search(loss_many, theta, delta, current_loss: float | None = None,
+                points_count: int = 31) -> LineSearchResult:
+    """Grid search over eta = 2^0 ... 2^-(count-1) (optimizer.py:148-166)."""
+    theta = np.asarray(theta, dtype=np.float64)
+    delta = np.asarray(delta, dtype=np.float64)
+    etas = 2.0 ** -np.arange(points_count, dtype=np.float64)
+    candidates = theta[None, :] + etas[:, None] * delta[None, :]
+    losses = np.asarray(loss_many(candidates), dtype=np.float64)
+    return _select(losses, etas, current_loss, points_count)
+
+
+_ETAS = {}
+
+
+def device_line_search(rmap: ResidualMap, theta: ParameterVector, delta_t,
+                       current_loss: float | None, points_count: int = 31) -> LineSearchResult:
+    """line_search with the candidate losses evaluated by the batched device kernel;
+    identical selection rule (ties -> larger eta, non-finite skipped, all non-finite
+    -> rejected)."""
+    import torch
+
+    key = (points_count, str(delta_t.device))
+    etas_t = _ETAS.get(key)
+    if etas_t is None:
+        etas_t = _ETAS[key] = torch.as_tensor(
+            2.0 ** -np.arange(points_count, dtype=np.float64), device=delta_t.device
+        )
+    losses = rmap.losses_along_t(theta, delta_t, etas_t).cpu().numpy()
+    return _select(losses, etas_t.cpu().numpy(), current_loss, points_count)
+
+
+# -- the main loop ------------------------------------------------------------------------
+
+
+def _dispatch_step(rmap: ResidualMap, theta, g, lam: float, config: OptimizerConfig,
+                   rng) -> StepResult:
+    """optimizer.py:172-184."""
+    if rmap.m < config.dense_threshold:
+        return dense_dual_solve(rmap, theta, g, lam=lam, use_ga=config.use_ga)
+    return pcg_step(
+        rmap,
+        theta,
+        g,
+        lam=lam,
+        landmark_count=min(config.nystrom_rank, rmap.m),
+        tol=config.cg_tol,
+        max_iters=config.cg_max_iters,
+        rng=rng,
+    )
+
+
+def _budget_reached(config: OptimizerConfig, iteration: int, clock: _Clock) -> bool:
+    if config.max_iters is not None:
+        return iteration > config.max_iters
+    return clock.elapsed() >= config.wall_seconds
+
+
+def _dngd_loop(trace: TrainTrace, rmap_provider, theta: ParameterVector, config: OptimizerConfig,
+               rng, rel_l2_fn=None, on_step=None) -> TrainTrace:
+    """optimizer.py:193-265 with device-resident state."""
+    from . import kernels as K
+
+    clock = _Clock(config.deterministic_timing)
+    rmap = rmap_provider(1)
+    rel = rel_l2_fn(theta) if rel_l2_fn else float("nan")
+    trace.rows.append(TraceRow(0, clock.stamp(), rmap.loss(theta), rel_l2=rel))
+
+    rejections = 0
+    iteration = 0
+    while True:
+        iteration += 1
+        if _budget_reached(config, iteration, clock):
+            break
+        try:
+            rmap = rmap_provider(iteration)
+            r, J = rmap.linearize_t(theta)
+            loss = 0.5 * float(K.dot(r, r).item())
+            if not np.isfinite(loss):
+                from .residuals import _raise_nonfinite
+
+                _raise_nonfinite(r, rmap.partition())
+            with stage("gemv"):
+                g = K.gemv_t(J, r, rmap.n)
+            lam = lm_damping(loss, config.lam_cap) * 10.0**rejections
+            step = _dispatch_step(rmap, theta, g, lam, config, rng)
+        except Exception as exc:
+            trace.aborted = True
+            trace.abort_reason = f"error at iteration {iteration}: {exc!r}"
+            break
+        delta_t = step.delta.tensor
+        if not bool(delta_t.any().item()):
+            ls = LineSearchResult(1.0, loss, False, 0, False)
+        else:
+            ls = device_line_search(rmap, theta, delta_t, loss, config.line_search_points)
+        if ls.rejected or (config.reject_if_worse and ls.loss > loss):
+            rejections += 1
+            trace.rows.append(
+                TraceRow(iteration, clock.stamp(), loss,
+                         rel_l2=rel_l2_fn(theta) if rel_l2_fn else float("nan"),
+                         lam=step.lambda_used, cg_iterations=step.cg_iterations)
+            )
+            if on_step is not None:
+                on_step(iteration, theta, step, ls)
+            if rejections >= MAX_CONSECUTIVE_REJECTIONS:
+                trace.aborted = True
+                trace.abort_reason = (
+                    f"{rejections} consecutive step rejections; last damping "
+                    f"{step.lambda_used:.3e}"
+                )
+                break
+            continue
+        rejections = 0
+        theta = ParameterVector(K.axpby(ls.eta, delta_t, 1.0, theta.tensor), theta.layout)
+        if on_step is not None:
+            on_step(iteration, theta, step, ls)
+        trace.rows.append(
+            TraceRow(iteration, clock.stamp(), ls.loss,
+                     rel_l2=rel_l2_fn(theta) if rel_l2_fn else float("nan"),
+                     lam=step.lambda_used, eta=ls.eta, cg_iterations=step.cg_iterations,
+                     ga_ratio=step.ga_ratio if step.ga_ratio is not None else float("nan"))
+        )
+    trace.final_theta = theta
+    return trace
+
+
+def dngd_minimize(residual_map: ResidualMap, theta, config: OptimizerConfig,
+                  rng=None) -> TrainTrace:
+    """optimizer.py:268-273."""
+    if rng is None or isinstance(rng, (int, np.integer)):
+        rng = np.random.default_rng(rng)
+    if not isinstance(theta, ParameterVector):
+        theta = ParameterVector(theta, residual_map.layout)
+    trace = TrainTrace(problem="custom", method="dngd", seed=-1)
+    return _dngd_loop(trace, lambda it: residual_map, theta, config, rng)
+
+
+def relative_l2_error(u_pred, u_exact) -> float:
+    """optimizer.py:465-477."""
+    u_pred = np.asarray(u_pred, dtype=np.float64).reshape(-1)
+    u_exact = np.asarray(u_exact, dtype=np.float64).reshape(-1)
+    if u_pred.shape != u_exact.shape:
+        raise DomainError(f"prediction and reference shapes differ: {u_pred.shape} vs {u_exact.shape}")
+    denom = float(np.linalg.norm(u_exact))
+    if denom == 0.0:
+        raise DomainError("reference values are identically zero on the grid")
+    return float(np.linalg.norm(u_pred - u_exact)) / denom
+
+
+class _ValueProblem:
+    """u(x) - u*(x) as a one-class residual map: the rel-L2 metric on the device."""
+
+    def __init__(self, dim, exact):
+        self.raw_dim = dim
+        self.exact = exact
+
+    def class_operator(self, class_id):
+        from .problems import VALUE
+
+        return VALUE
+
+    def class_data(self, cls):
+        return self.exact
+
+
+def _rel_l2_fn(problem, spec: MlpSpec):
+    """Relative L2 error on the problem's evaluation grid (optimizer.py:282-287)."""
+    if not getattr(problem, "has_exact", False):
+        return None
+    from .residuals import INTERIOR, CollocationClass, CollocationSet
+
+    pts = problem.eval_points()
+    exact = problem.exact_solution(pts)
+    denom = float(np.linalg.norm(exact))
+    vmap = PinnResidualMap(_ValueProblem(pts.shape[1], exact), spec,
+                           CollocationSet([CollocationClass(INTERIOR, pts, 1.0)]))
+
+    def fn(theta):
+        if denom == 0.0:
+            raise DomainError("reference values are identically zero on the grid")
+        r = vmap.residuals_t(theta)
+        return float(r.norm().item()) / denom
+
+    return fn
+
+
+def network_values(problem, spec: MlpSpec, theta, pts) -> np.ndarray:
+    """Network output on raw points (optimizer.py:276-279)."""
+    from .residuals import INTERIOR, CollocationClass, CollocationSet
+
+    pts = np.asarray(pts, dtype=np.float64)
+    vmap = PinnResidualMap(_ValueProblem(pts.shape[1], np.zeros(pts.shape[0])), spec,
+                           CollocationSet([CollocationClass(INTERIOR, pts, 1.0)]))
+    return vmap.residuals_t(theta).cpu().numpy()
+
+
+def dngd_run(problem, spec: MlpSpec, config: OptimizerConfig, seed: int, counts=None,
+             init: str = "glorot_uniform", track_rel_l2: bool = True, on_step=None) -> TrainTrace:
+    """Train a network on a PDE problem with D-NGD (optimizer.py:290-314).
+
+    `init` selects the initialiser ("glorot_uniform" = reference default,
+    "xavier_normal" = BASELINE configs); the seed drives the initialisation and
+    every collocation / landmark draw in the reference's order.
+    """
+    from .problems import sample_collocation
+
+    spec = replace(spec, seed=seed)
+    rng = np.random.default_rng(seed)
+    theta = INITIALIZERS[init](spec)
+    state = {"rmap": None}
+
+    def provider(iteration: int) -> ResidualMap:
+        if state["rmap"] is None or (config.resample and iteration > 1):
+            colloc = sample_collocation(problem, counts, rng)
+            if state["rmap"] is None:
+                state["rmap"] = PinnResidualMap(problem, spec, colloc)
+            else:
+                state["rmap"] = state["rmap"].rebind(colloc)
+        return state["rmap"]
+
+    trace = TrainTrace(problem=problem.name, method="dngd", seed=seed)
+    rel_fn = _rel_l2_fn(problem, spec) if track_rel_l2 else None
+    return _dngd_loop(trace, provider, theta, config, rng, rel_fn, on_step)

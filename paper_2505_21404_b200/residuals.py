@@ -1,0 +1,590 @@
+"""Residual maps with device-resident Jacobians (reference residuals.py:1-454).
+
+The plugin contract is the reference's `ResidualMap`: `n`, `m`, `partition`,
+`residual_batch`, `loss`, `loss_many`, `vjp`, `residuals_and_gradient`,
+`linearize`, `jacobian`, `rows_jacobian`, `jvp`, `jvp_many`,
+`second_directional`, `sub_map`, `rebind`.  Those names keep returning
+host numpy arrays for drop-in callers.  The solver uses the device API
+(`*_t` methods) that every map here implements on CUDA tensors:
+
+  linearize_t(theta) -> (r, J)   J is (m, ldJ) row-major, columns [:n] valid
+  fvv_t(theta, v)                f_vv = d^2/dt^2 r(theta + t v)
+  losses_along_t(theta, d, etas) 0.5 |r(theta + eta_c d)|^2 for every eta_c
+
+PinnResidualMap runs entirely in the CUDA library (pinn.cu): one
+forward-Laplacian pass + per-point adjoint writes r and J, the Jacobian is
+cached per parameter version so residuals_and_gradient followed by the step
+assembles J once (the reference assembles it twice).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import DimensionError, DomainError, NonFiniteError
+from .params import ParameterLayout, ParameterVector
+from .timing import stage
+
+INTERIOR = "interior"
+BOUNDARY = "boundary"
+INITIAL = "initial"
+_CLASS_IDS = (INTERIOR, BOUNDARY, INITIAL)
+
+
+@dataclass
+class CollocationClass:
+    """Points of one residual class with its loss weight (residuals.py:33-55)."""
+
+    class_id: str
+    points: np.ndarray
+    weight: float
+    aux: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        if self.class_id not in _CLASS_IDS:
+            raise DimensionError(f"unknown residual class id: {self.class_id!r}")
+        pts = np.asarray(self.points, dtype=np.float64)
+        self.points = pts[:, None] if pts.ndim == 1 else pts
+
+    @property
+    def count(self) -> int:
+        return self.points.shape[0]
+
+
+class CollocationSet:
+    """Ordered residual classes; rows of r follow this order (residuals.py:58-104)."""
+
+    def __init__(self, classes: list[CollocationClass]):
+        if not classes:
+            raise DimensionError("a collocation set needs at least one class")
+        self.classes = list(classes)
+
+    @property
+    def m(self) -> int:
+        return sum(c.count for c in self.classes)
+
+    def partition(self) -> list[tuple[str, int, int]]:
+        spans, start = [], 0
+        for c in self.classes:
+            spans.append((c.class_id, start, start + c.count))
+            start += c.count
+        return spans
+
+    def locate(self, row: int) -> tuple[int, int]:
+        if not 0 <= row < self.m:
+            raise DimensionError(f"residual row {row} out of range [0, {self.m})")
+        for k, (_, start, stop) in enumerate(self.partition()):
+            if row < stop:
+                return k, row - start
+        raise AssertionError("unreachable")
+
+    def subset(self, rows: np.ndarray) -> "CollocationSet":
+        rows = np.asarray(rows, dtype=np.int64)
+        if rows.ndim != 1 or rows.size == 0:
+            raise DimensionError("subset needs a non-empty 1-d list of rows")
+        if np.any(np.diff(rows) <= 0):
+            raise DimensionError("subset rows must be strictly increasing")
+        if rows[0] < 0 or rows[-1] >= self.m:
+            raise DimensionError(f"subset rows out of range [0, {self.m})")
+        classes = []
+        for c, (_, start, stop) in zip(self.classes, self.partition()):
+            local = rows[(rows >= start) & (rows < stop)] - start
+            if local.size == 0:
+                continue
+            aux = {k: np.asarray(v)[local] for k, v in c.aux.items()}
+            classes.append(CollocationClass(c.class_id, c.points[local], c.weight, aux))
+        return CollocationSet(classes)
+
+
+def _is_tensor(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+class ResidualBatch:
+    """Stacked residual values with their class partition (residuals.py:107-122)."""
+
+    def __init__(self, values, partition):
+        self._t = values if _is_tensor(values) else None
+        self._np = None if _is_tensor(values) else np.asarray(values, dtype=np.float64)
+        self.partition = partition
+
+    @property
+    def values(self) -> np.ndarray:
+        if self._np is None:
+            self._np = self._t.cpu().numpy()
+        return self._np
+
+    @property
+    def tensor(self):
+        if self._t is None:
+            import torch
+
+            from ._lib import require_cuda
+
+            self._t = torch.as_tensor(self._np, device=require_cuda())
+        return self._t
+
+    @property
+    def m(self) -> int:
+        return self.values.shape[0] if self._t is None else self._t.shape[0]
+
+    def per_class(self) -> dict[str, np.ndarray]:
+        return {cid: self.values[a:b] for cid, a, b in self.partition}
+
+    def loss(self) -> float:
+        if self._t is not None:
+            from . import kernels as K
+
+            return 0.5 * float(K.dot(self._t, self._t).item())
+        return 0.5 * float(self.values @ self.values)
+
+
+def _raise_nonfinite(values_t, partition):
+    import torch
+
+    bad_idx = torch.nonzero(~torch.isfinite(values_t))
+    if bad_idx.numel() == 0:
+        return
+    bad = int(bad_idx[0, 0].item())
+    for cid, a, b in partition:
+        if a <= bad < b:
+            raise NonFiniteError(
+                f"non-finite residual in class {cid!r} at point {bad - a}",
+                class_id=cid,
+                point_index=bad - a,
+            )
+    raise NonFiniteError("non-finite residual", point_index=bad)
+
+
+class ResidualMap:
+    """Device-first residual map base class."""
+
+    layout: ParameterLayout
+    collocation: CollocationSet
+
+    # -- shapes --------------------------------------------------------------------
+    @property
+    def n(self) -> int:
+        return self.layout.size
+
+    @property
+    def m(self) -> int:
+        return self.collocation.m
+
+    def partition(self):
+        return self.collocation.partition()
+
+    def rebind(self, collocation: CollocationSet) -> "ResidualMap":
+        raise NotImplementedError
+
+    def sub_map(self, rows: np.ndarray) -> "ResidualMap":
+        return self.rebind(self.collocation.subset(rows))
+
+    def _theta_t(self, theta):
+        if isinstance(theta, ParameterVector):
+            if theta.layout != self.layout:
+                raise DimensionError("parameter vector layout does not match this map")
+            return theta.tensor
+        if _is_tensor(theta):
+            return theta
+        return ParameterVector(np.asarray(theta, dtype=np.float64), self.layout).tensor
+
+    def _vec_t(self, v, size, what):
+        import torch
+
+        from ._lib import require_cuda
+
+        if isinstance(v, ParameterVector):
+            v = v.tensor
+        elif isinstance(v, ResidualBatch):
+            v = v.tensor
+        if not _is_tensor(v):
+            v = torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64), device=require_cuda())
+        if v.dim() != 1 or v.shape[0] != size:
+            raise DimensionError(f"{what} has shape {tuple(v.shape)}, expected ({size},)")
+        return v.contiguous()
+
+    # -- device API (subclasses implement linearize_t / fvv_t / losses) -------------
+    def linearize_t(self, theta):
+        raise NotImplementedError
+
+    def residuals_t(self, theta):
+        return self.linearize_t(theta)[0]
+
+    def jacobian_t(self, theta):
+        return self.linearize_t(theta)[1]
+
+    def fvv_t(self, theta, v_t):
+        raise NotImplementedError
+
+    def loss_many_t(self, cands_t):
+        raise NotImplementedError
+
+    def losses_along_t(self, theta, delta_t, etas_t):
+        th = self._theta_t(theta)
+        cands = th[None, :] + etas_t[:, None] * delta_t[None, :]
+        return self.loss_many_t(cands)
+
+    def jvp_t(self, theta, v_t):
+        from . import kernels as K
+
+        return K.gemv_n(self.jacobian_t(theta), v_t, self.n)
+
+    def vjp_t(self, theta, w_t, g_t=None, scale=1.0):
+        from . import kernels as K
+
+        return K.gemv_t(self.jacobian_t(theta), w_t, self.n, g_t, scale)
+
+    def gradient_t(self, theta):
+        r, J = self.linearize_t(theta)
+        from . import kernels as K
+
+        return K.gemv_t(J, r, self.n)
+
+    # -- reference (numpy) API --------------------------------------------------------
+    def residual_batch(self, theta) -> ResidualBatch:
+        r = self.residuals_t(theta)
+        _raise_nonfinite(r, self.partition()) if not bool(r.isfinite().all()) else None
+        return ResidualBatch(r, self.partition())
+
+    def loss(self, theta) -> float:
+        return self.residual_batch(theta).loss()
+
+    def loss_many(self, candidates) -> np.ndarray:
+        import torch
+
+        from ._lib import require_cuda
+
+        if not _is_tensor(candidates):
+            candidates = np.asarray(candidates, dtype=np.float64)
+            if candidates.ndim != 2:
+                raise DimensionError("loss_many expects a (C, n) candidate stack")
+            candidates = torch.as_tensor(candidates, device=require_cuda())
+        return self.loss_many_t(candidates.contiguous()).cpu().numpy()
+
+    def vjp(self, theta, w) -> np.ndarray:
+        return self.vjp_t(theta, self._vec_t(w, self.m, "cotangent")).cpu().numpy()
+
+    def residuals_and_gradient(self, theta):
+        r, J = self.linearize_t(theta)
+        loss = 0.5 * float((r @ r).item())
+        if not np.isfinite(loss):
+            _raise_nonfinite(r, self.partition())
+        from . import kernels as K
+
+        g = K.gemv_t(J, r, self.n)
+        return ResidualBatch(r, self.partition()), g.cpu().numpy()
+
+    def gradient(self, theta) -> np.ndarray:
+        return self.residuals_and_gradient(theta)[1]
+
+    def linearize(self, theta):
+        r, J = self.linearize_t(theta)
+        if not bool(r.isfinite().all()):
+            _raise_nonfinite(r, self.partition())
+        return ResidualBatch(r, self.partition()), J[:, : self.n].cpu().numpy()
+
+    def jacobian(self, theta) -> np.ndarray:
+        return self.linearize(theta)[1]
+
+    def rows_jacobian(self, theta, rows) -> np.ndarray:
+        return self.sub_map(rows).jacobian(theta)
+
+    def jvp(self, theta, v) -> np.ndarray:
+        return self.jvp_t(theta, self._vec_t(v, self.n, "tangent")).cpu().numpy()
+
+    def jvp_many(self, theta, tangents) -> np.ndarray:
+        import torch
+
+        from . import kernels as K
+        from ._lib import require_cuda
+
+        V = np.asarray(tangents, dtype=np.float64)
+        if V.ndim != 2 or V.shape[1] != self.n:
+            raise DimensionError(f"tangent has shape {V.shape}, expected (..., {self.n})")
+        J = self.jacobian_t(theta)
+        Vd = torch.zeros((V.shape[0], J.shape[1]), dtype=torch.float64, device=require_cuda())
+        Vd[:, : self.n] = torch.as_tensor(V, device=Vd.device)
+        return K.gemm_nt(Vd, J, K=self.n).cpu().numpy()
+
+    def second_directional(self, theta, v) -> np.ndarray:
+        f = self.fvv_t(theta, self._vec_t(v, self.n, "tangent"))
+        if not bool(f.isfinite().all()):
+            _raise_nonfinite(f, self.partition())
+        return f.cpu().numpy()
+
+
+class LinearResidualMap(ResidualMap):
+    """r(theta) = A theta + c (residuals.py:325-379); J = A on the device."""
+
+    def __init__(self, A, c):
+        self.A = np.atleast_2d(np.asarray(A, dtype=np.float64))
+        self.c = np.asarray(c, dtype=np.float64)
+        if self.c.shape != (self.A.shape[0],):
+            raise DimensionError(f"offset has shape {self.c.shape}, expected ({self.A.shape[0]},)")
+        self.layout = ParameterLayout([("theta", (self.A.shape[1],))])
+        self.collocation = CollocationSet(
+            [CollocationClass(INTERIOR, np.arange(self.A.shape[0])[:, None] * 1.0, 1.0)]
+        )
+        self._dev = None
+
+    def rebind(self, collocation):
+        rows = collocation.classes[0].points[:, 0].astype(np.int64)
+        sub = LinearResidualMap(self.A[rows], self.c[rows])
+        sub.layout = self.layout
+        return sub
+
+    def _device(self):
+        if self._dev is None:
+            import torch
+
+            from . import kernels as K
+            from ._lib import require_cuda
+
+            m, n = self.A.shape
+            J = torch.zeros((m, K.pad_ld(n)), dtype=torch.float64, device=require_cuda())
+            J[:, :n] = torch.as_tensor(self.A, device=J.device)
+            self._dev = (J, torch.as_tensor(self.c, device=J.device))
+        return self._dev
+
+    def linearize_t(self, theta):
+        from . import kernels as K
+
+        J, c = self._device()
+        r = K.gemv_n(J, self._theta_t(theta), self.n, 1.0, c, 1.0)
+        return r, J
+
+    def fvv_t(self, theta, v_t):
+        import torch
+
+        return torch.zeros(self.m, dtype=torch.float64, device=v_t.device)
+
+    def loss_many_t(self, cands_t):
+        import torch
+
+        from . import kernels as K
+
+        J, c = self._device()
+        C = cands_t.shape[0]
+        Cd = torch.zeros((C, J.shape[1]), dtype=torch.float64, device=J.device)
+        Cd[:, : self.n] = cands_t
+        R = K.gemm_nt(Cd, J, K=self.n) + c[None, :]
+        return 0.5 * (R * R).sum(dim=1)
+
+
+class PinnResidualMap(ResidualMap):
+    """Weighted PDE residuals of a tanh MLP, evaluated by the CUDA library."""
+
+    LOSS_WS_BUDGET = 8 * 1024**3  # bytes of line-search activations per chunk
+
+    def __init__(self, problem, spec, collocation: CollocationSet, col_range=None):
+        from .model import MlpSpec
+
+        if not isinstance(spec, MlpSpec):
+            raise DimensionError("PinnResidualMap needs an MlpSpec")
+        if spec.input_dim != problem.raw_dim:
+            raise DimensionError(
+                f"spec input width {spec.input_dim} != problem dimension {problem.raw_dim}"
+            )
+        if spec.output_dim != 1:
+            raise DimensionError("PINN residual maps need a scalar network output")
+        self.problem = problem
+        self.spec = spec
+        self.layout = spec.layout()
+        self.collocation = collocation
+        self.col_range = (0, self.layout.size) if col_range is None else tuple(col_range)
+        self._dev = None
+        self._cache = None
+        self._J = None
+
+    def rebind(self, collocation):
+        other = PinnResidualMap(self.problem, self.spec, collocation, self.col_range)
+        if self._J is not None and self._J.shape[0] == collocation.m:
+            other._J = self._J  # reuse the Jacobian buffer across resamples
+            self._cache = None  # this map no longer owns the buffer contents
+        return other
+
+    # -- device state -----------------------------------------------------------------
+    def _device(self):
+        if self._dev is not None:
+            return self._dev
+        import torch
+
+        from . import _lib
+        from . import kernels as K
+        from ._lib import require_cuda
+
+        dev = require_cuda()
+        classes = self.collocation.classes
+        if len(classes) > _lib.MAX_CLASSES:
+            raise DomainError(f"at most {_lib.MAX_CLASSES} residual classes are supported")
+        if self.m > 65535:
+            raise DomainError("at most 65535 residual rows per map in this build")
+        arr = (_lib.ClassDesc * len(classes))()
+        keep = []
+        for k, cls in enumerate(classes):
+            op = self.problem.class_operator(cls.class_id)
+            pts = torch.as_tensor(np.ascontiguousarray(cls.points), device=dev)
+            f = torch.as_tensor(
+                np.ascontiguousarray(self.problem.class_data(cls), dtype=np.float64), device=dev
+            )
+            keep += [pts, f]
+            d = arr[k]
+            d.count = cls.count
+            d.ngrad = len(op.grad_dims)
+            d.nlap = len(op.lap_dims)
+            if d.ngrad > _lib.MAX_GRAD:
+                raise DomainError("too many derivative channels for the device kernels")
+            for g, gd in enumerate(op.grad_dims):
+                d.grad_dims[g] = int(gd)
+                d.cg[g] = float(op.cg[g])
+            for l, ldim in enumerate(op.lap_dims):
+                d.lap_grad[l] = op.grad_dims.index(ldim)
+            d.cu, d.cl, d.weight = float(op.cu), float(op.cl), float(cls.weight)
+            d.points = pts.data_ptr()
+            d.f = f.data_ptr()
+        mlp = K.mlp_desc(self.spec.layer_widths)
+        ws_bytes = K.pinn_workspace_bytes(mlp, arr, len(classes), 1)
+        per_cand = K.pinn_workspace_bytes(mlp, arr, len(classes), 2) - K.pinn_workspace_bytes(
+            mlp, arr, len(classes), 1
+        )
+        self._dev = dict(arr=arr, keep=keep, mlp=mlp, nclass=len(classes), ws_bytes=ws_bytes,
+                         per_cand=max(per_cand, 1), device=dev)
+        return self._dev
+
+    def _workspace(self, nbytes):
+        from . import kernels as K
+
+        return K.workspace("pinn", nbytes)
+
+    @property
+    def ncols(self) -> int:
+        return self.col_range[1] - self.col_range[0]
+
+    def _key(self, th):
+        return (th.data_ptr(), th._version, id(self.collocation))
+
+    def linearize_t(self, theta):
+        import torch
+
+        from . import kernels as K
+
+        th = self._theta_t(theta)
+        key = self._key(th)
+        if self._cache is not None and self._cache[0] == key:
+            return self._cache[1], self._cache[2]
+        d = self._device()
+        m = self.m
+        if self._J is None or self._J.shape != (m, K.pad_ld(self.ncols)):
+            self._J = torch.empty((m, K.pad_ld(self.ncols)), dtype=torch.float64, device=d["device"])
+        r = torch.empty(m, dtype=torch.float64, device=d["device"])
+        ws = self._workspace(d["ws_bytes"])
+        with stage("assemble"):
+            K.assemble(d["mlp"], th, d["arr"], d["nclass"], r, self._J, self.col_range[0],
+                       self.col_range[1], ws)
+        self._cache = (key, r, self._J)
+        return r, self._J
+
+    def residuals_t(self, theta):
+        import torch
+
+        from . import kernels as K
+
+        th = self._theta_t(theta)
+        if self._cache is not None and self._cache[0] == self._key(th):
+            return self._cache[1]
+        d = self._device()
+        r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
+        K.assemble(d["mlp"], th, d["arr"], d["nclass"], r, None, 0, self.n,
+                   self._workspace(d["ws_bytes"]))
+        return r
+
+    def fvv_t(self, theta, v_t):
+        import torch
+
+        from . import kernels as K
+
+        d = self._device()
+        out = torch.empty(self.m, dtype=torch.float64, device=d["device"])
+        with stage("fvv"):
+            K.fvv(d["mlp"], self._theta_t(theta), v_t, d["arr"], d["nclass"], out,
+                  self._workspace(d["ws_bytes"]))
+        return out
+
+    def _chunk(self, C):
+        d = self._device()
+        return max(1, min(C, int(self.LOSS_WS_BUDGET // d["per_cand"])))
+
+    def losses_along_t(self, theta, delta_t, etas_t):
+        import torch
+
+        from . import kernels as K
+
+        d = self._device()
+        th = self._theta_t(theta)
+        C = etas_t.shape[0]
+        out = torch.empty(C, dtype=torch.float64, device=d["device"])
+        step = self._chunk(C)
+        with stage("line_search"):
+            for c0 in range(0, C, step):
+                c1 = min(C, c0 + step)
+                ws = self._workspace(d["ws_bytes"] + d["per_cand"] * (c1 - c0))
+                K.loss_many(d["mlp"], th, delta_t, etas_t[c0:c1], c1 - c0, d["arr"],
+                            d["nclass"], out[c0:c1], ws)
+        return out
+
+    def loss_many_t(self, cands_t):
+        import torch
+
+        from . import kernels as K
+
+        d = self._device()
+        if cands_t.dim() != 2 or cands_t.shape[1] != self.n:
+            raise DimensionError("loss_many expects a (C, n) candidate stack")
+        C = cands_t.shape[0]
+        out = torch.empty(C, dtype=torch.float64, device=d["device"])
+        step = self._chunk(C)
+        for c0 in range(0, C, step):
+            c1 = min(C, c0 + step)
+            ws = self._workspace(d["ws_bytes"] + d["per_cand"] * (c1 - c0))
+            K.loss_many(d["mlp"], cands_t[c0:c1].contiguous(), None, None, c1 - c0, d["arr"],
+                        d["nclass"], out[c0:c1], ws)
+        return out
+
+
+class RegressionResidualMap(PinnResidualMap):
+    """r_i = weight (u_theta(x_i) - y_i) (residuals.py:382-419) as a value-only PINN class."""
+
+    class _RegressionProblem:
+        name = "regression"
+
+        def __init__(self, dim):
+            self.raw_dim = dim
+
+        def class_operator(self, class_id):
+            from .problems import VALUE
+
+            return VALUE
+
+        def class_data(self, cls):
+            return np.asarray(cls.aux["targets"], dtype=np.float64)
+
+    def __init__(self, spec, inputs, targets, weight=None):
+        inputs = np.asarray(inputs, dtype=np.float64)
+        if inputs.ndim == 1:
+            inputs = inputs[:, None]
+        targets = np.asarray(targets, dtype=np.float64).reshape(-1)
+        if inputs.shape[0] != targets.shape[0]:
+            raise DimensionError("inputs and targets disagree on sample count")
+        if weight is None:
+            weight = 1.0 / np.sqrt(inputs.shape[0])
+        colloc = CollocationSet(
+            [CollocationClass(INTERIOR, inputs, float(weight), {"targets": targets})]
+        )
+        super().__init__(self._RegressionProblem(inputs.shape[1]), spec, colloc)
+
+    def rebind(self, collocation):
+        cls = collocation.classes[0]
+        return RegressionResidualMap(self.spec, cls.points, cls.aux["targets"], cls.weight)

@@ -1,0 +1,271 @@
+"""End-to-end parity of the GPU D-NGD step and loop against the reference.
+
+Golden fixtures come from the unmodified reference (tests/golden/make_golden.py);
+the numpy oracle supplies the parity floors (SURVEY §8c protocol).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import dngd_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("needs CUDA")
+    import paper_2505_21404_b200 as P
+    return P
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def _load(golden_dir, name):
+    return np.load(os.path.join(golden_dir, f"{name}.npz"))
+
+
+STEP = {
+    "cfg1_step": ("poisson2d", ("interior", "boundary"), O.OraclePoisson2d()),
+    "cfg2_step": ("heat1d", ("interior", "boundary", "initial"), O.OracleHeat1d()),
+    "cfg3_step": ("poisson5d_sin", ("interior", "boundary"), O.OraclePoissonSin(5)),
+}
+
+
+def _map(P, fx, problem_name, ids):
+    problem = P.make_problem(problem_name)
+    widths = tuple(int(w) for w in fx["widths"])
+    spec = P.MlpSpec(widths)
+    classes = [P.CollocationClass(c, fx[f"pts_{c}"], 1.0 / np.sqrt(len(fx[f"pts_{c}"])))
+               for c in ids]
+    rmap = P.PinnResidualMap(problem, spec, P.CollocationSet(classes))
+    theta = P.ParameterVector(fx["theta"], spec.layout())
+    return rmap, theta, widths
+
+
+@pytest.mark.parametrize("name", sorted(STEP))
+def test_dense_step_matches_reference(P, golden_dir, name):
+    fx = _load(golden_dir, name)
+    pname, ids, oprob = STEP[name]
+    rmap, theta, widths = _map(P, fx, pname, ids)
+    batch, g = rmap.residuals_and_gradient(theta)
+    assert _rel(batch.values, fx["r"]) <= 1e-12
+    assert _rel(g, fx["g"]) <= 1e-11
+    gram = P.assemble_gramian(rmap, theta)
+    assert _rel(gram.K, fx["K"]) <= 1e-12  # north star: Gram <= 1e-12
+    for p, ref in zip(fx["probe_n"], fx["J_probe_n"]):
+        assert _rel(rmap.jvp(theta, p), ref) <= 1e-11
+    for p, ref in zip(fx["probe_m"], fx["JT_probe_m"]):
+        assert _rel(rmap.vjp(theta, p), ref) <= 1e-11
+    for p, ref in zip(fx["probe_n"], fx["fvv_probe"]):
+        assert _rel(rmap.second_directional(theta, p), ref) <= 1e-10
+    # oracle floors at this step
+    oclasses = oprob.classes(*[fx[f"pts_{c}"] for c in ids])
+    _, Jo = O.linearize(fx["theta"], widths, oclasses)
+    fvv_fn = lambda v: O.second_directional(fx["theta"], widths, oclasses, v)
+    for i, lam in enumerate(fx["lams"]):
+        fl = O.direction_floors(Jo, fx["g"], lam, fvv_fn)
+        plain = P.dense_dual_solve(rmap, theta, g, lam=lam, use_ga=False)
+        res = P.dense_dual_solve(rmap, theta, g, lam=lam, use_ga=True)
+        tol_v = max(1e-8, 10 * fl["v"])
+        tol_d = max(1e-8, 10 * fl["delta"])
+        assert _rel(plain.delta.data, fx[f"v_{i}"]) <= tol_v
+        assert res.lambda_used == fx[f"lam_used_{i}"]
+        assert _rel(res.delta.data, fx[f"delta_{i}"]) <= tol_d
+        ref_ratio = float(fx[f"ga_ratio_{i}"])
+        if not np.isnan(ref_ratio):
+            assert abs(res.ga_ratio - ref_ratio) <= max(tol_d, 1e-8) * max(1.0, ref_ratio) * 10
+        etas = 2.0 ** -np.arange(31, dtype=np.float64)
+        cands = fx["theta"][None, :] + etas[:, None] * fx[f"delta_{i}"][None, :]
+        np.testing.assert_allclose(rmap.loss_many(cands), fx[f"ls_losses_{i}"], rtol=1e-10)
+
+
+TRAJ = {
+    "cfg1_traj": ("poisson2d", (90, 30), dict(lam_cap=1e-3)),
+    "cfg2_traj": ("heat1d", (60, 20, 20), dict(lam_cap=1e-3)),
+    "pcg_traj": ("poisson2d", (60, 20),
+                 dict(lam_cap=1e-3, dense_threshold=10, nystrom_rank=16, cg_max_iters=100)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(TRAJ))
+def test_trajectory_matches_reference(P, golden_dir, name):
+    fx = _load(golden_dir, name)
+    pname, counts, cfg = TRAJ[name]
+    widths = tuple(int(w) for w in fx["widths"])
+    n_steps = len(fx["loss"]) - 1
+    config = P.OptimizerConfig(max_iters=n_steps, deterministic_timing=True, **cfg)
+    trace = P.dngd_run(P.make_problem(pname), P.MlpSpec(widths), config, int(fx["seed"]),
+                       counts=counts, init="xavier_normal")
+    assert not trace.aborted, trace.abort_reason
+    loss = np.array([r.loss for r in trace.rows])
+    np.testing.assert_allclose(loss, fx["loss"], rtol=1e-6)
+    np.testing.assert_allclose([r.rel_l2 for r in trace.rows], fx["rel_l2"], rtol=1e-6)
+    np.testing.assert_array_equal([r.eta for r in trace.rows][1:], fx["eta"][1:])
+    its = np.array([r.cg_iterations for r in trace.rows])
+    assert np.max(np.abs(its - fx["cg_iterations"])) <= 1
+    assert _rel(trace.final_theta.data, fx["final_theta"]) <= 1e-6
+
+
+def test_pcg_step_matches_reference(P, golden_dir):
+    fx = _load(golden_dir, "pcg_step")
+    rmap, theta, widths = _map(P, fx, "poisson2d", ("interior", "boundary"))
+    _, g = rmap.residuals_and_gradient(theta)
+    rng = np.random.default_rng(int(fx["seed"]))
+    P.make_problem("poisson2d").sample((60, 20), rng)  # advance like the fixture
+    state = rng.bit_generator.state
+    res = P.pcg_step(rmap, theta, g, lam=float(fx["lam"]), landmark_count=int(fx["ell"]),
+                     tol=float(fx["tol"]), max_iters=int(fx["max_iters"]), rng=rng)
+    assert abs(res.cg_iterations - int(fx["cg_iterations"])) <= 1
+    assert _rel(res.delta.data, fx["delta"]) <= 1e-6
+    assert _rel(res.delta.data, fx["dense_delta"]) <= 1e-6
+    rng2 = np.random.default_rng(0)
+    rng2.bit_generator.state = state
+    pre = P.nystrom_build(rmap, theta, landmark_count=int(fx["ell"]), lam=float(fx["lam"]),
+                          rng=rng2)
+    np.testing.assert_array_equal(pre.landmarks, fx["landmarks"])
+    np.testing.assert_allclose(pre.lam_hat, fx["lam_hat"], rtol=1e-6,
+                               atol=1e-9 * fx["lam_hat"][0])
+    for p, ref in zip(fx["probe"], fx["precond_probe"]):
+        assert _rel(pre.apply(p), ref) <= 1e-6
+
+
+# -- reference unit-test patterns (test_solver.py) on the GPU backend -----------------------
+
+
+def test_identity_jacobian_closed_form(P):
+    n, lam = 6, 0.25
+    rng = np.random.default_rng(4)
+    c = rng.normal(size=n)
+    rmap = P.LinearResidualMap(np.eye(n), c)
+    theta = P.ParameterVector(rng.normal(size=n), rmap.layout)
+    r = theta.data + c
+    res = P.dense_dual_solve(rmap, theta, r, lam=lam, use_ga=False)
+    assert np.allclose(res.delta.data, -r / (1.0 + lam), atol=1e-12)
+    assert res.lambda_used == lam and res.cg_iterations == 0
+
+
+def test_affine_ga_is_identical(P):
+    rng = np.random.default_rng(5)
+    A = rng.normal(size=(7, 4))
+    rmap = P.LinearResidualMap(A, rng.normal(size=7))
+    theta = P.ParameterVector(rng.normal(size=4), rmap.layout)
+    g = rmap.gradient(theta)
+    plain = P.dense_dual_solve(rmap, theta, g, lam=1e-2, use_ga=False)
+    accel = P.dense_dual_solve(rmap, theta, g, lam=1e-2, use_ga=True)
+    assert np.max(np.abs(plain.delta.data - accel.delta.data)) <= 1e-14
+    assert accel.ga_ratio is not None and accel.ga_ratio <= 1e-12
+
+
+def test_dual_matches_primal_normal_equations(P):
+    rng = np.random.default_rng(6)
+    spec = P.MlpSpec((4, 32, 1), seed=6)
+    x = rng.uniform(-1, 1, size=(24, 4))
+    y = rng.normal(size=24)
+    rmap = P.RegressionResidualMap(spec, x, y)
+    theta = P.init_params(spec)
+    lam = 1e-3
+    g = rmap.gradient(theta)
+    res = P.dense_dual_solve(rmap, theta, g, lam=lam, use_ga=False)
+    J = rmap.jacobian(theta)
+    primal = np.linalg.solve(J.T @ J + lam * np.eye(rmap.n), -g)
+    assert _rel(res.delta.data, primal) <= 1e-8
+
+
+def test_ga_matches_primal_acceleration(P):
+    rng = np.random.default_rng(7)
+    spec = P.MlpSpec((3, 10, 1), seed=7)
+    rmap = P.RegressionResidualMap(spec, rng.uniform(-1, 1, size=(14, 3)), rng.normal(size=14))
+    theta = P.init_params(spec)
+    lam = 1e-2
+    g = rmap.gradient(theta)
+    res = P.dense_dual_solve(rmap, theta, g, lam=lam, use_ga=True)
+    J = rmap.jacobian(theta)
+    H = J.T @ J + lam * np.eye(rmap.n)
+    v = np.linalg.solve(H, -g)
+    f_vv = rmap.second_directional(theta, v)
+    a = np.linalg.solve(H, -(J.T @ f_vv))
+    ratio = 2.0 * np.linalg.norm(a) / np.linalg.norm(v)
+    assert abs(res.ga_ratio - ratio) <= 1e-8 * max(1.0, ratio)
+    expected = v + 0.5 * a if ratio <= 0.5 else v
+    assert _rel(res.delta.data, expected) <= 1e-8
+
+
+def test_cholesky_retry_ladder(P):
+    from paper_2505_21404_b200 import solver
+    _, lam = solver._chol_with_retries(-np.eye(3), 1e-3)
+    assert lam == pytest.approx(10.0)
+    with pytest.raises(P.FactorizationError):
+        solver._chol_with_retries(-np.eye(3), 1e-12)
+
+
+def test_memory_guard(P, monkeypatch):
+    from paper_2505_21404_b200 import solver
+    rmap = P.LinearResidualMap(np.eye(30), np.zeros(30))
+    theta = P.ParameterVector(np.zeros(30), rmap.layout)
+    monkeypatch.setattr(solver, "GRAMIAN_MEMORY_BUDGET", 1000)
+    with pytest.raises(P.DomainError, match="budget"):
+        P.assemble_gramian(rmap, theta)
+
+
+def test_kvp_two_by_two(P):
+    rmap = P.LinearResidualMap(np.diag([1.0, 2.0]), np.zeros(2))
+    theta = P.ParameterVector(np.zeros(2), rmap.layout)
+    out = P.kvp(rmap, theta, np.ones(2), lam=0.5)
+    assert np.allclose(out.values, [1.5, 4.5], atol=1e-14)
+
+
+def test_nystrom_full_sampling_reconstructs(P):
+    rng = np.random.default_rng(14)
+    spec = P.MlpSpec((3, 8, 1), seed=14)
+    rmap = P.RegressionResidualMap(spec, rng.uniform(-1, 1, size=(24, 3)), rng.normal(size=24))
+    theta = P.init_params(spec)
+    K = P.assemble_gramian(rmap, theta).K
+    lam = 1e-3
+    pre = P.nystrom_build(rmap, theta, landmark_count=24, lam=lam, rng=0)
+    recon = pre.U @ (pre.lam_hat[:, None] * pre.U.T)
+    assert np.linalg.norm(recon - K) / np.linalg.norm(K) <= 1e-8
+    for _ in range(5):
+        v = rng.normal(size=24)
+        assert np.linalg.norm(pre.apply(K @ v + lam * v) - v) <= 1e-8 * np.linalg.norm(v)
+
+
+def test_nystrom_zero_gramian(P):
+    rmap = P.LinearResidualMap(np.zeros((6, 3)), np.zeros(6))
+    theta = P.ParameterVector(np.zeros(3), rmap.layout)
+    pre = P.nystrom_build(rmap, theta, landmark_count=4, lam=0.5, rng=18)
+    assert pre.rank == 0
+    v = np.arange(6.0)
+    assert np.array_equal(pre.apply(v), v / 0.5)
+
+
+def test_pcg_agrees_with_dense(P):
+    rng = np.random.default_rng(24)
+    spec = P.MlpSpec((3, 12, 1), seed=24)
+    rmap = P.RegressionResidualMap(spec, rng.uniform(-1, 1, size=(40, 3)), rng.normal(size=40))
+    theta = P.init_params(spec)
+    g = rmap.gradient(theta)
+    dense = P.dense_dual_solve(rmap, theta, g, lam=1e-3, use_ga=False)
+    cg = P.pcg_step(rmap, theta, g, lam=1e-3, landmark_count=20, tol=1e-10, max_iters=200, rng=25)
+    assert _rel(cg.delta.data, dense.delta.data) <= 1e-6
+    assert cg.warning is None and cg.cg_iterations >= 1
+
+
+def test_pcg_zero_gradient_and_breakdown(P):
+    rng = np.random.default_rng(30)
+    spec = P.MlpSpec((2, 4, 1), seed=30)
+    rmap = P.RegressionResidualMap(spec, rng.uniform(-1, 1, size=(6, 2)), rng.normal(size=6))
+    theta = P.init_params(spec)
+    res = P.pcg_step(rmap, theta, np.zeros(rmap.n), lam=0.1, landmark_count=3, rng=31)
+    assert np.array_equal(res.delta.data, np.zeros(rmap.n)) and res.cg_iterations == 0
+    lin = P.LinearResidualMap(1e-150 * np.eye(4), np.zeros(4))
+    th = P.ParameterVector(np.zeros(4), lin.layout)
+    res = P.pcg_step(lin, th, np.ones(4), lam=1e6, landmark_count=2, rng=32)
+    assert res.warning is not None and "breakdown" in res.warning
+    assert np.all(np.isfinite(res.delta.data))

@@ -1,0 +1,160 @@
+"""CPU-only tests: the C-ABI library loads and exports the header's symbols, and
+the host logic (config schema, damping, line search, sampling, problem operators)
+matches the reference semantics.  No kernel is launched here."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import dngd_oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    text = open(os.path.join(ROOT, "include", "dngd_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(dngd_\w+)\(", text, re.M)))
+
+
+def test_library_loads_and_exports_every_header_symbol():
+    from paper_2505_21404_b200 import _build, _lib
+
+    if not os.path.exists(_lib.LIB_PATH):
+        _build.build_library()
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    syms = _header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.EXPORTED)
+    assert lib.dngd_version() == 1
+
+
+def test_ctypes_struct_layout_matches_header():
+    from paper_2505_21404_b200 import _lib
+
+    # int64 count, 2 ints, 12 ints, 12 ints, 12 doubles, 3 doubles, 2 pointers
+    assert ctypes.sizeof(_lib.ClassDesc) == 8 + 8 + 48 + 48 + 96 + 24 + 16
+    assert ctypes.sizeof(_lib.MlpDesc) == 4 * 10
+
+
+def test_optimizer_config_validation():
+    from paper_2505_21404_b200 import ConfigError, OptimizerConfig
+
+    OptimizerConfig(max_iters=3)
+    with pytest.raises(ConfigError):
+        OptimizerConfig()
+    with pytest.raises(ConfigError):
+        OptimizerConfig(max_iters=3, wall_seconds=1.0)
+    with pytest.raises(ConfigError):
+        OptimizerConfig(max_iters=3, lam_cap=0.0)
+    with pytest.raises(ConfigError):
+        OptimizerConfig(max_iters=3, dense_threshold=0)
+    with pytest.raises(ConfigError):
+        OptimizerConfig(max_iters=3, nystrom_rank=0)
+
+
+def test_damping_table():
+    from paper_2505_21404_b200 import DomainError, lm_damping
+
+    assert lm_damping(0.3, 1e-5) == 1e-5
+    assert lm_damping(1e-7, 1e-5) == 1e-7
+    assert lm_damping(0.0, 1e-5) == 1e-12
+    with pytest.raises(DomainError):
+        lm_damping(-1.0, 1e-5)
+
+
+def test_line_search_semantics():
+    from paper_2505_21404_b200 import line_search
+
+    res = line_search(lambda c: (c[:, 0] - 1.0) ** 2 + 0.3, np.zeros(1), np.ones(1), 10.0)
+    assert res.eta == 1.0 and not res.rejected and not res.degraded
+    assert line_search(lambda c: c[:, 0], np.zeros(1), np.ones(1), 0.0).eta == 2.0**-30
+    assert line_search(lambda c: np.full(c.shape[0], 7.0), np.zeros(1), np.ones(1), 8.0).eta == 1.0
+    res = line_search(lambda c: 5.0 + c[:, 0], np.zeros(1), np.ones(1), 1.0)
+    assert res.degraded and not res.rejected
+    res = line_search(lambda c: np.full(c.shape[0], np.nan), np.zeros(1), np.ones(1), 1.0)
+    assert res.rejected and res.eta is None
+
+    def lm(c):
+        out = c[:, 0].copy()
+        out[out < 0.25] = np.inf
+        return out
+
+    assert line_search(lm, np.zeros(1), np.ones(1), 1.0).eta == 0.25
+    seen = []
+    line_search(lambda c: seen.append(c.shape[0]) or np.arange(c.shape[0], dtype=float),
+                np.zeros(2), np.ones(2), 0.0)
+    assert seen == [31]
+
+
+@pytest.mark.parametrize("name,oracle,counts", [
+    ("poisson2d", O.OraclePoisson2d(), (50, 20)),
+    ("heat1d", O.OracleHeat1d(), (50, 20, 20)),
+    ("poisson5d_sin", O.OraclePoissonSin(5), (40, 10)),
+])
+def test_sampling_and_operators_match_oracle(name, oracle, counts):
+    """Host sampling consumes the Generator exactly like the oracle/reference, and the
+    class operators and data terms describe the same residuals."""
+    from paper_2505_21404_b200 import make_problem
+
+    prob = make_problem(name)
+    a = prob.sample(counts, np.random.default_rng(7))
+    b = oracle.sample(counts, np.random.default_rng(7))
+    assert [c.class_id for c in a.classes] == [c.class_id for c in b]
+    for ca, cb in zip(a.classes, b):
+        assert np.array_equal(ca.points, cb.points)
+        assert ca.weight == cb.weight
+        op = prob.class_operator(ca.class_id)
+        assert (op.cu, tuple(op.grad_dims), tuple(op.cg), tuple(op.lap_dims), op.cl) == (
+            cb.cu, tuple(cb.grad_dims), tuple(cb.cg), tuple(cb.lap_dims), cb.cl)
+        np.testing.assert_array_equal(prob.class_data(ca), cb.f)
+
+
+def test_reference_problems_exact_solutions_annihilate_residuals():
+    """test_problems.py:40-66 style: u* zeroes every class residual (FD derivatives)."""
+    from paper_2505_21404_b200 import make_problem
+
+    rng = np.random.default_rng(0)
+    for name in ("poisson2d", "poisson10d", "heat2d", "heat1d", "poisson5d_sin"):
+        prob = make_problem(name)
+        coll = prob.sample(None, rng)
+        for cls in coll.classes:
+            p = cls.points[:50]
+            op = prob.class_operator(cls.class_id)
+            f = prob.class_data(cls)[:50]
+            h = 1e-4
+            u = prob.exact_solution(p)
+            val = op.cu * u - f
+            for j, cg in zip(op.grad_dims, op.cg):
+                e = np.zeros(p.shape[1]); e[j] = h
+                val = val + cg * (prob.exact_solution(p + e) - prob.exact_solution(p - e)) / (2 * h)
+            for j in op.lap_dims:
+                e = np.zeros(p.shape[1]); e[j] = h
+                val = val + op.cl * (prob.exact_solution(p + e) - 2 * u
+                                     + prob.exact_solution(p - e)) / h**2
+            scale = max(1.0, float(np.max(np.abs(f))))
+            assert np.max(np.abs(val)) <= 2e-5 * scale, (name, cls.class_id)
+
+
+def test_param_layout_and_counts():
+    from paper_2505_21404_b200 import MlpSpec, init_params, xavier_normal_params
+
+    for widths, n in [((2, 32, 32, 1), 1185), ((2, 64, 64, 64, 64, 1), 12737),
+                      ((5, 512, 512, 512, 512, 1), 791553), ((2, 256, 256, 256, 256, 1), 198401),
+                      ((5, 1792, 1792, 1792, 1792, 1792, 1), 12864769)]:
+        assert MlpSpec(widths).param_count() == n
+    spec = MlpSpec((2, 8, 1), seed=3)
+    assert np.array_equal(xavier_normal_params(spec).data, O.xavier_normal_init((2, 8, 1), 3))
+    assert np.array_equal(init_params(spec).data, O.glorot_uniform_init((2, 8, 1), 3))
+
+
+def test_unsupported_problems_fail_loudly():
+    from paper_2505_21404_b200 import DomainError, make_problem
+
+    for name in ("allen_cahn", "poisson_ball_stde"):
+        with pytest.raises(DomainError):
+            make_problem(name)

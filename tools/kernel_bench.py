@@ -7,7 +7,12 @@ import argparse
 import json
 import time
 
+import os
+import sys
+
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2505_21404_b200 import kernels as Kn
 

@@ -447,9 +447,9 @@ class PinnResidualMap(ResidualMap):
             d.f = f.data_ptr()
         mlp = K.mlp_desc(self.spec.layer_widths)
         ws_bytes = K.pinn_workspace_bytes(mlp, arr, len(classes), 1)
-        per_cand = K.pinn_workspace_bytes(mlp, arr, len(classes), 2) - K.pinn_workspace_bytes(
-            mlp, arr, len(classes), 1
-        )
+        # line-search activations grow linearly with the candidate count
+        per_cand = (K.pinn_workspace_bytes(mlp, arr, len(classes), 64)
+                    - K.pinn_workspace_bytes(mlp, arr, len(classes), 32)) // 32
         self._dev = dict(arr=arr, keep=keep, mlp=mlp, nclass=len(classes), ws_bytes=ws_bytes,
                          per_cand=max(per_cand, 1), device=dev)
         return self._dev
@@ -513,6 +513,12 @@ class PinnResidualMap(ResidualMap):
                   self._workspace(d["ws_bytes"]))
         return out
 
+    def _loss_ws(self, C):
+        from . import kernels as K
+
+        d = self._device()
+        return K.pinn_workspace_bytes(d["mlp"], d["arr"], d["nclass"], C)
+
     def _chunk(self, C):
         d = self._device()
         return max(1, min(C, int(self.LOSS_WS_BUDGET // d["per_cand"])))
@@ -530,7 +536,7 @@ class PinnResidualMap(ResidualMap):
         with stage("line_search"):
             for c0 in range(0, C, step):
                 c1 = min(C, c0 + step)
-                ws = self._workspace(d["ws_bytes"] + d["per_cand"] * (c1 - c0))
+                ws = self._workspace(self._loss_ws(c1 - c0))
                 K.loss_many(d["mlp"], th, delta_t, etas_t[c0:c1], c1 - c0, d["arr"],
                             d["nclass"], out[c0:c1], ws)
         return out
@@ -548,7 +554,7 @@ class PinnResidualMap(ResidualMap):
         step = self._chunk(C)
         for c0 in range(0, C, step):
             c1 = min(C, c0 + step)
-            ws = self._workspace(d["ws_bytes"] + d["per_cand"] * (c1 - c0))
+            ws = self._workspace(self._loss_ws(c1 - c0))
             K.loss_many(d["mlp"], cands_t[c0:c1].contiguous(), None, None, c1 - c0, d["arr"],
                         d["nclass"], out[c0:c1], ws)
         return out

@@ -69,8 +69,15 @@ def test_dense_step_matches_reference(P, golden_dir, name):
     oclasses = oprob.classes(*[fx[f"pts_{c}"] for c in ids])
     _, Jo = O.linearize(fx["theta"], widths, oclasses)
     fvv_fn = lambda v: O.second_directional(fx["theta"], widths, oclasses, v)
+    # measured J discrepancy GPU vs reference (enters the floor meter)
+    Jg = rmap.jacobian(theta)
+    if "J" in fx:
+        j_rel = _rel(Jg, fx["J"])
+    else:
+        j_rel = max(_rel(Jg[i], fx["J_rows"][k]) for k, i in enumerate(fx["J_rows_idx"]))
+    assert j_rel <= 1e-12
     for i, lam in enumerate(fx["lams"]):
-        fl = O.direction_floors(Jo, fx["g"], lam, fvv_fn)
+        fl = O.direction_floors(Jo, fx["g"], lam, fvv_fn, j_rel=max(j_rel, 1e-16))
         plain = P.dense_dual_solve(rmap, theta, g, lam=lam, use_ga=False)
         res = P.dense_dual_solve(rmap, theta, g, lam=lam, use_ga=True)
         tol_v = max(1e-8, 10 * fl["v"])

@@ -59,7 +59,7 @@ struct GemmCfg {
 };
 
 template <int BM, int BN, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(WM * WN * 32, 1)
+__global__ void __launch_bounds__(WM * WN * 32, (WM * WN <= 4 ? 3 : 1))
     k_gemm_nt(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const GemmDev p) {
   using Cfg = GemmCfg<BM, BN, WM, WN, STAGES>;
@@ -170,26 +170,41 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
     return;
   }
   double* C = p.C + static_cast<long long>(batch) * p.sC;
+  // Epilogue in row groups of 8: the beta*C loads of a group are all issued before
+  // any store (one L2 round trip per group instead of one per fragment).
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
     const long long r = static_cast<long long>(tm) * BM + wm * WTM + i * 8 + lrow;
-    if (r >= p.M) continue;
+    const bool rok = r < p.M;
+    double2 cv[NJ];
+    bool ok0[NJ], ok1[NJ];
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       const long long c = static_cast<long long>(tn) * BN + wn * WTN + j * 8 + 2 * (lane & 3);
-      const bool ok0 = c < p.N && (!p.lower || c <= r);
-      const bool ok1 = c + 1 < p.N && (!p.lower || c + 1 <= r);
-      double* cp = C + r * p.ldc + c;
-      double v0 = p.alpha * acc[i][j].x, v1 = p.alpha * acc[i][j].y;
+      ok0[j] = rok && c < p.N && (!p.lower || c <= r);
+      ok1[j] = rok && c + 1 < p.N && (!p.lower || c + 1 <= r);
+      cv[j] = make_double2(0.0, 0.0);
       if (p.beta != 0.0) {
-        if (ok0) v0 += p.beta * cp[0];
-        if (ok1) v1 += p.beta * cp[1];
+        const double* cp = C + r * p.ldc + c;
+        if (ok0[j] && ok1[j] && p.vec_ok) {
+          cv[j] = __ldcg(reinterpret_cast<const double2*>(cp));
+        } else {
+          if (ok0[j]) cv[j].x = __ldcg(cp);
+          if (ok1[j]) cv[j].y = __ldcg(cp + 1);
+        }
       }
-      if (ok0 && ok1 && p.vec_ok) {
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const long long c = static_cast<long long>(tn) * BN + wn * WTN + j * 8 + 2 * (lane & 3);
+      double* cp = C + r * p.ldc + c;
+      const double v0 = fma(p.alpha, acc[i][j].x, p.beta * cv[j].x);
+      const double v1 = fma(p.alpha, acc[i][j].y, p.beta * cv[j].y);
+      if (ok0[j] && ok1[j] && p.vec_ok) {
         *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
       } else {
-        if (ok0) cp[0] = v0;
-        if (ok1) cp[1] = v1;
+        if (ok0[j]) cp[0] = v0;
+        if (ok1[j]) cp[1] = v1;
       }
     }
   }
@@ -274,6 +289,12 @@ int gemm_nt(dngd_ctx* ctx, cudaStream_t s, const GemmCall& g) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return DNGD_OK;
   if (g.K <= 0) {
     return set_error(ctx, DNGD_ERR_DIMENSION, "gemm_nt: K must be positive");
+  }
+  if (g.lower && g.partial == nullptr && g.K <= 256) {
+    // short-K lower updates (Cholesky trailing updates): small tiles, several
+    // CTAs per SM so one CTA's read-modify-write epilogue hides behind another's
+    // DMMA main loop
+    return launch_gemm<64, 64, 2, 2, 4>(ctx, s, g);
   }
   if (g.lower || g.partial != nullptr || g.N > 64) {
     return launch_gemm<128, 128, 2, 4, 5>(ctx, s, g);

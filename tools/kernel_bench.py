@@ -68,6 +68,8 @@ def main():
         t = timed(lambda: fac.factor(Km, 1e-3), iters=5)
         out.append({"item": f"potrf_{m}", "ms": t * 1e3, "tflops": m**3 / 3 / t / 1e12,
                     "info": int(fac.info.item())})
+        t = timed(lambda: torch.linalg.cholesky(Km), iters=5)
+        out.append({"item": f"cusolver_potrf_{m}", "ms": t * 1e3, "tflops": m**3 / 3 / t / 1e12})
         b = torch.randn(m, dtype=torch.float64, device=dev)
         t = timed(lambda: fac.solve_(b))
         out.append({"item": f"potrs_{m}", "ms": t * 1e3, "gbs": 8 * m * m / t / 1e9})

@@ -61,6 +61,12 @@ extern "C" int dngd_ctx_create(int device, dngd_ctx** out) {
 }
 
 extern "C" int dngd_ctx_destroy(dngd_ctx* ctx) {
+  if (ctx) {
+    if (ctx->ev_panel) cudaEventDestroy(ctx->ev_panel);
+    if (ctx->ev_update) cudaEventDestroy(ctx->ev_update);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  }
   delete ctx;
   return DNGD_OK;
 }

@@ -14,6 +14,9 @@ struct dngd_ctx {
   int num_sms = 148;
   PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   std::string last_error;
+  // look-ahead Cholesky: auxiliary stream + fork/join events (created lazily)
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_panel = nullptr, ev_update = nullptr, ev_fork = nullptr;
 };
 
 namespace dngd {

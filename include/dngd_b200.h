@@ -142,6 +142,14 @@ int dngd_assemble(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const d
                   int64_t col_end, double* r, double* J, int64_t ldJ, void* work,
                   size_t work_bytes);
 
+/* r and the full Gram K = J J^T WITHOUT materialising J (replaces
+ * residuals.py:241-256 + solver.py:153-154): per layer k and channel pair,
+ * K += (Hext_k Hext_k'^T) o (Zbar_k Zbar_k'^T) on the FP64 tensor cores.  K
+ * (m x m, ldK) receives both triangles. */
+int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                       const double* theta, const dngd_class_desc* classes, int nclass,
+                       double* r, double* K, int64_t ldK, void* work, size_t work_bytes);
+
 /* f_vv = d^2/dt^2 r(theta + t v) at t = 0 (residuals.py:304-317) */
 int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
              const double* v, const dngd_class_desc* classes, int nclass, double* fvv,

@@ -12,7 +12,8 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libdngd_b200.so")
 SOURCES = ["abi.cu", "gemm.cu", "chol.cu", "blas2.cu", "pinn.cu"]
-HEADERS = ["common.cuh", "internal.h", os.path.join("..", "..", "include", "dngd_b200.h")]
+HEADERS = ["common.cuh", "internal.h", "gram_factored.cuh",
+           os.path.join("..", "..", "include", "dngd_b200.h")]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -78,6 +78,8 @@ _SIGS = {
                              ctypes.POINTER(c_size)], c_int),
     "dngd_assemble": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, ctypes.POINTER(ClassDesc), c_int,
                        c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_size], c_int),
+    "dngd_gram_factored": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, ctypes.POINTER(ClassDesc),
+                            c_int, c_vp, c_vp, c_i64, c_vp, c_size], c_int),
     "dngd_fvv": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, c_vp, ctypes.POINTER(ClassDesc), c_int,
                   c_vp, c_vp, c_size], c_int),
     "dngd_loss_many": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, c_vp, c_vp, c_int,

@@ -68,6 +68,15 @@ DNGD_DEV void dmma_8x8x4(double2& d, double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// lower-triangular tile index t -> (ti, tj), tj <= ti, row-major over the lower triangle
+DNGD_DEV void decode_lower(int t, int& ti, int& tj) {
+  int i = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while (i * (i + 1) / 2 > t) --i;
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  ti = i;
+  tj = t - i * (i + 1) / 2;
+}
+
 // ---------------------------------------------------------------- reductions
 DNGD_DEV double warp_sum(double v) {
 #pragma unroll

@@ -40,13 +40,6 @@ struct GemmDev {
   double* partial;
 };
 
-DNGD_DEV void decode_lower(int t, int& ti, int& tj) {
-  int i = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-  while (i * (i + 1) / 2 > t) --i;
-  while ((i + 1) * (i + 2) / 2 <= t) ++i;
-  ti = i;
-  tj = t - i * (i + 1) / 2;
-}
 
 template <int BM, int BN, int WM, int WN, int STAGES>
 struct GemmCfg {

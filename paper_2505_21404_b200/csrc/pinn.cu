@@ -639,6 +639,8 @@ static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const d
   return cuda_status(ctx, cudaGetLastError(), "forward");
 }
 
+#include "gram_factored.cuh"
+
 static size_t bytes_of(const Plan& P, int mode, int C) {
   Arena A{nullptr};
   if (mode == 0) {
@@ -670,19 +672,10 @@ extern "C" int dngd_pinn_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp,
   return DNGD_OK;
 }
 
-extern "C" int dngd_assemble(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
-                             const double* theta, const dngd_class_desc* classes, int nclass,
-                             int64_t col_begin, int64_t col_end, double* r, double* J,
-                             int64_t ldJ, void* work, size_t work_bytes) {
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  Plan P;
-  int rc = make_plan(ctx, mlp, classes, nclass, P);
-  if (rc) return rc;
-  if (bytes_of(P, 0, 1) > work_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "assemble: workspace too small");
-  if (P.m == 0) return DNGD_OK;
-  Arena A{static_cast<char*>(work)};
-  AsmBufs B;
-  carve_assemble(P, A, B);
+static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& B,
+                         const double* theta, long long col_begin, long long col_end, double* r,
+                         double* J, long long ldJ, bool adjoint) {
+  int rc = DNGD_OK;
   const int L = P.L;
   // ---- forward
   k_input_fwd<<<nblk(P.m * P.w[1]), 256, 0, s>>>(P.T, theta, 0, static_cast<int>(P.w[1]),
@@ -711,12 +704,13 @@ extern "C" int dngd_assemble(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* m
   k_head<<<nblk(P.m, 8), 256, 0, s>>>(P.T, B.H[L - 1], static_cast<int>(P.w[L - 1]),
                                        P.ld[L - 1], theta, 0, wl_off, 0, r, 0);
   rc = cuda_status(ctx, cudaGetLastError(), "assemble forward");
-  if (rc || J == nullptr) return rc;
-  if (col_begin < 0 || col_end > P.n || col_begin > col_end) {
+  if (rc || (J == nullptr && !adjoint)) return rc;
+  if (J != nullptr && (col_begin < 0 || col_end > P.n || col_begin > col_end)) {
     return set_error(ctx, DNGD_ERR_DIMENSION, "assemble: column range outside [0, n]");
   }
   const bool jvec_ok = ((ldJ & 1) == 0) && ((reinterpret_cast<uintptr_t>(J) & 15) == 0);
   auto jwrite = [&](int k, const double* Hk, long long ldh, const double* Zb, long long ldz) {
+    if (J == nullptr) return;
     const int win = static_cast<int>(P.w[k]), wout = static_cast<int>(P.w[k + 1]);
     const long long lo = P.off[k], hi = lo + (win + 1LL) * wout;
     if (hi <= col_begin || lo >= col_end) return;
@@ -760,6 +754,117 @@ extern "C" int dngd_assemble(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* m
     }
   }
   return cuda_status(ctx, cudaGetLastError(), "assemble adjoint");
+}
+
+extern "C" int dngd_assemble(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                             const double* theta, const dngd_class_desc* classes, int nclass,
+                             int64_t col_begin, int64_t col_end, double* r, double* J,
+                             int64_t ldJ, void* work, size_t work_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  if (bytes_of(P, 0, 1) > work_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "assemble: workspace too small");
+  if (P.m == 0) return DNGD_OK;
+  Arena A{static_cast<char*>(work)};
+  AsmBufs B;
+  carve_assemble(P, A, B);
+  return assemble_impl(ctx, s, P, B, theta, col_begin, col_end, r, J, ldJ, false);
+}
+
+extern "C" int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                                  const double* theta, const dngd_class_desc* classes,
+                                  int nclass, double* r, double* K, int64_t ldK, void* work,
+                                  size_t work_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  if (bytes_of(P, 0, 1) > work_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_factored: workspace too small");
+  if (P.m == 0) return DNGD_OK;
+  if (P.T.din > DNGD_MAX_GRAD) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_factored: input dim > 12");
+  Arena A{static_cast<char*>(work)};
+  AsmBufs B;
+  carve_assemble(P, A, B);
+  rc = assemble_impl(ctx, s, P, B, theta, 0, P.n, r, nullptr, 0, true);
+  if (rc) return rc;
+  thread_local GramParams gp;  // ~8.5 KB of tensor maps: off the host stack, reentrant
+  memset(&gp, 0, sizeof gp);
+  gp.T = P.T;
+  gp.L = P.L;
+  for (int c = 0; c < P.T.n; ++c) {
+    const int nch = P.T.c[c].nch;
+    int lg = 0;
+    while ((1 << lg) < nch) ++lg;
+    if (lg > 3) {
+      return set_error(ctx, DNGD_ERR_UNSUPPORTED,
+                       "gram_factored: more than 8 channels per point; use assemble + syrk");
+    }
+    gp.lg[c] = lg;
+  }
+  // 3-D maps (columns, channels, points) over each class's rows of H_k / Zbar_k;
+  // a box of 16 x a x 64/a is one 64-row G-space operand tile (channels >= nch
+  // are out of bounds and arrive as zeros)
+  auto encode3 = [&](CUtensorMap* map, const double* base, long long inner, int nch, long long N,
+                     long long ld, int lg) -> int {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(nch),
+                          static_cast<cuuint64_t>(std::max<long long>(N, 1))};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 8,
+                             static_cast<cuuint64_t>(ld) * nch * 8};
+    cuuint32_t box[3] = {16, static_cast<cuuint32_t>(1 << lg), static_cast<cuuint32_t>(GF_BM >> lg)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult res = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base),
+                               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return res == CUDA_SUCCESS ? DNGD_OK
+                               : set_error(ctx, DNGD_ERR_CUDA, "gram_factored: tensor map encode failed");
+  };
+  for (int k = 0; k < P.L; ++k) {
+    gp.lay[k].kh = k >= 1 ? static_cast<int>(P.w[k]) : 0;
+    gp.lay[k].kz = k <= P.L - 2 ? static_cast<int>(P.w[k + 1]) : 0;
+    for (int c = 0; c < P.T.n; ++c) {
+      const ClassDev& Cc = P.T.c[c];
+      if (k >= 1) {
+        rc = encode3(&gp.maps[k][0][c], B.H[k] + Cc.act0 * P.ld[k], P.w[k], Cc.nch, Cc.count,
+                     P.ld[k], gp.lg[c]);
+        if (rc) return rc;
+      }
+      if (k <= P.L - 2) {
+        rc = encode3(&gp.maps[k][1][c], B.Zb[k] + Cc.act0 * P.ld[k + 1], P.w[k + 1], Cc.nch,
+                     Cc.count, P.ld[k + 1], gp.lg[c]);
+        if (rc) return rc;
+      }
+    }
+  }
+  int np = 0, tiles = 0;
+  gp.tstart[0] = 0;
+  for (int c = 0; c < P.T.n; ++c) {
+    for (int cp = 0; cp <= c; ++cp) {
+      const int ti = static_cast<int>((P.T.c[c].count + (GF_BM >> gp.lg[c]) - 1) / (GF_BM >> gp.lg[c]));
+      const int tj = static_cast<int>((P.T.c[cp].count + (GF_BM >> gp.lg[cp]) - 1) / (GF_BM >> gp.lg[cp]));
+      gp.pc[np] = c;
+      gp.pcp[np] = cp;
+      gp.tj_n[np] = tj;
+      tiles += c == cp ? ti * (ti + 1) / 2 : ti * tj;
+      gp.tstart[np + 1] = tiles;
+      ++np;
+    }
+  }
+  gp.npairs = np;
+  gp.K = K;
+  gp.ldK = ldK;
+  static bool attr[64] = {false};
+  if (!attr[ctx->device & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(k_gram_factored, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(gram_factored_smem()));
+    if (e != cudaSuccess) return cuda_status(ctx, e, "gram_factored smem attribute");
+    attr[ctx->device & 63] = true;
+  }
+  if (tiles > 0) {
+    k_gram_factored<<<static_cast<unsigned>(tiles), GF_THREADS, gram_factored_smem(), s>>>(gp);
+  }
+  return cuda_status(ctx, cudaGetLastError(), "gram_factored");
 }
 
 extern "C" int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,

@@ -193,6 +193,12 @@ def assemble(mlp, theta, classes_arr, nclass, r, J=None, col_begin=0, col_end=No
          0 if ws is None else ws.numel())
 
 
+def gram_factored(mlp, theta, classes_arr, nclass, r, K, ws):
+    """r and K = J J^T from the activations (J never materialised)."""
+    call("dngd_gram_factored", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), classes_arr,
+         nclass, ptr(r), ptr(K), K.stride(0), ptr(ws), ws.numel())
+
+
 def fvv(mlp, theta, v, classes_arr, nclass, out, ws):
     call("dngd_fvv", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), ptr(v), classes_arr,
          nclass, ptr(out), ptr(ws), ws.numel())

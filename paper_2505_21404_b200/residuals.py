@@ -513,6 +513,49 @@ class PinnResidualMap(ResidualMap):
                   self._workspace(d["ws_bytes"]))
         return out
 
+    # -- factored Gram (no pass over J) ------------------------------------------------
+    gram_mode = "auto"  # "auto" | "factored" | "materialized"
+
+    def _gram_flop_ratio(self) -> float:
+        """Estimated FLOPs of the factored Gram / FLOPs of J J^T."""
+        w = self.spec.layer_widths
+        ksum = sum((w[k] if k >= 1 else 0) + (w[k + 1] if k <= len(w) - 3 else 0)
+                   for k in range(len(w) - 1))
+        fact = 0.0
+        for c in self.collocation.classes:
+            for cp in self.collocation.classes:
+                a = 1 << max(0, (self._nch(c) - 1).bit_length())
+                b = 1 << max(0, (self._nch(cp) - 1).bit_length())
+                fact += c.count * cp.count * a * b * ksum
+        return fact / max(1.0, float(self.m) ** 2 * self.n)
+
+    def _nch(self, cls) -> int:
+        op = self.problem.class_operator(cls.class_id)
+        return 1 + len(op.grad_dims) + (1 if op.lap_dims else 0)
+
+    def use_factored_gram(self) -> bool:
+        if self.col_range != (0, self.layout.size):
+            return False  # column shards form their partial Gram from J_p
+        if any(self._nch(c) > 8 for c in self.collocation.classes):
+            return False
+        if self.gram_mode == "factored":
+            return True
+        if self.gram_mode == "materialized":
+            return False
+        # the factored kernel runs at ~0.7 of the SYRK's tensor-pipe efficiency
+        return self._gram_flop_ratio() < 0.3
+
+    def gram_factored_t(self, theta, K_out):
+        import torch
+
+        from . import kernels as K
+
+        d = self._device()
+        r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
+        K.gram_factored(d["mlp"], self._theta_t(theta), d["arr"], d["nclass"], r, K_out,
+                        self._workspace(d["ws_bytes"]))
+        return K_out
+
     def _loss_ws(self, C):
         from . import kernels as K
 

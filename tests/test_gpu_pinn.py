@@ -87,3 +87,23 @@ def test_loss_many_matches_oracle(K, name, problem, widths, counts):
     out2 = torch.empty(31, dtype=torch.float64, device="cuda")
     K.loss_many(mlp, dev(cands), None, None, 31, arr, len(classes), out2, ws)
     np.testing.assert_allclose(out2.cpu().numpy(), ref, rtol=1e-12)
+
+
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + [
+    ("poisson2d_cfg1", O.OraclePoisson2d(), (2, 32, 32, 1), (900, 120)),
+    ("heat1d_cfg2", O.OracleHeat1d(), (2, 64, 64, 64, 64, 1), (500, 100, 100)),
+])
+def test_gram_factored_matches_jjt(K, name, problem, widths, counts):
+    """Factored Gram (no J) == oracle J J^T to 1e-12 (north-star Gram tolerance)."""
+    classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 6)
+    r_ref, J_ref = O.linearize(theta, widths, classes)
+    K_ref = O.gram(J_ref)
+    m = J_ref.shape[0]
+    r = torch.empty(m, dtype=torch.float64, device="cuda")
+    Kd = torch.full((m, m), np.nan, dtype=torch.float64, device="cuda")
+    K.gram_factored(mlp, th, arr, len(classes), r, Kd, ws)
+    Kg = Kd.cpu().numpy()
+    assert np.all(np.isfinite(Kg))
+    assert np.array_equal(Kg, Kg.T)
+    assert _rel(Kg, K_ref) <= 1e-12
+    assert _rel(r.cpu().numpy(), r_ref) <= 1e-12

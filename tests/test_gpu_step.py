@@ -93,6 +93,27 @@ def test_dense_step_matches_reference(P, golden_dir, name):
         np.testing.assert_allclose(rmap.loss_many(cands), fx[f"ls_losses_{i}"], rtol=1e-10)
 
 
+@pytest.mark.parametrize("name", sorted(STEP))
+@pytest.mark.parametrize("mode", ["factored", "materialized"])
+def test_gram_modes_match_reference(P, golden_dir, name, mode):
+    """Both Gram paths (SYRK over J; factored from the activations) reproduce the
+    reference K and the GN step."""
+    fx = _load(golden_dir, name)
+    pname, ids, oprob = STEP[name]
+    rmap, theta, widths = _map(P, fx, pname, ids)
+    rmap.gram_mode = mode
+    assert rmap.use_factored_gram() == (mode == "factored")
+    gram = P.assemble_gramian(rmap, theta)
+    assert _rel(gram.K, fx["K"]) <= 1e-12
+    _, g = rmap.residuals_and_gradient(theta)
+    lam = float(fx["lams"][0])
+    res = P.dense_dual_solve(rmap, theta, g, lam=lam, use_ga=False)
+    oclasses = oprob.classes(*[fx[f"pts_{c}"] for c in ids])
+    _, Jo = O.linearize(fx["theta"], widths, oclasses)
+    fl = O.direction_floors(Jo, fx["g"], lam)
+    assert _rel(res.delta.data, fx["v_0"]) <= max(1e-8, 10 * fl["v"])
+
+
 TRAJ = {
     "cfg1_traj": ("poisson2d", (90, 30), dict(lam_cap=1e-3)),
     "cfg2_traj": ("heat1d", (60, 20, 20), dict(lam_cap=1e-3)),

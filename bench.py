@@ -212,9 +212,13 @@ def run_ours(args, cfg):
 
     def one_step(rmap, theta):
         nonlocal shared_J
-        rmap._J = shared_J
-        r, J = rmap.linearize_t(theta)
-        shared_J = rmap._J
+        jfree = (not sharded and rmap.m < config.dense_threshold and rmap.jfree())
+        if jfree:  # factored Gram + J^T w from activations: J never materialised
+            r, J = rmap.residuals_t(theta), None
+        else:
+            rmap._J = shared_J
+            r, J = rmap.linearize_t(theta)
+            shared_J = rmap._J
         loss = 0.5 * float(K.dot(r, r).item())
         lam = lm_damping(loss, config.lam_cap)
         if sharded:
@@ -223,8 +227,10 @@ def run_ours(args, cfg):
             delta = step["delta"]
             ls = sharded_line_search(ops, comm, theta, delta, loss, config.line_search_points)
         else:
-            with timing.stage("gemv"):
-                g = K.gemv_t(J, r, rmap.n)
+            g = None
+            if not jfree:
+                with timing.stage("gemv"):
+                    g = K.gemv_t(J, r, rmap.n)
             from paper_2505_21404_b200.optimizer import _dispatch_step
 
             step = _dispatch_step(rmap, theta, g, lam, config, rng)

@@ -150,6 +150,22 @@ int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                        const double* theta, const dngd_class_desc* classes, int nclass,
                        double* r, double* K, int64_t ldK, void* work, size_t work_bytes);
 
+/* r plus the forward channels and per-point adjoints (no J) left in work for
+ * dngd_jt_factored (the tape sweep of residuals.py:241-256 without the rows) */
+int dngd_activations(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
+                     const dngd_class_desc* classes, int nclass, double* r, void* work,
+                     size_t work_bytes);
+
+/* out = scale * J^T w WITHOUT J (replaces residuals.py:220-227 vjp): uses the
+ * activations left in act_work by the last dngd_gram_factored / dngd_assemble
+ * call for the same theta; scratch sized by dngd_jt_workspace. */
+int dngd_jt_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp, const dngd_class_desc* classes,
+                      int nclass, size_t* bytes);
+int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                     const dngd_class_desc* classes, int nclass, const double* w, double scale,
+                     double* out, void* act_work, size_t act_bytes, void* scratch,
+                     size_t scratch_bytes);
+
 /* f_vv = d^2/dt^2 r(theta + t v) at t = 0 (residuals.py:304-317) */
 int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
              const double* v, const dngd_class_desc* classes, int nclass, double* fvv,

@@ -296,6 +296,61 @@ int gemm_nt(dngd_ctx* ctx, cudaStream_t s, const GemmCall& g) {
   return launch_gemm<128, 32, 4, 1, 4>(ctx, s, g);
 }
 
+// ------------------------------------------------------------------ split-K GEMM
+// For small outputs with a long reduction (J^T w over activation rows): S splits
+// write raw 128x128 partial tiles, a fixed-order reduction applies alpha / beta.
+
+__global__ void k_splitk_reduce(const double* __restrict__ partial, int splits, int ntiles,
+                                int tiles_n, long long M, long long N, double* __restrict__ C,
+                                long long ldc, double alpha, double beta) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long tile_elems = 128 * 128;
+  if (e >= static_cast<long long>(ntiles) * tile_elems) return;
+  const int t = static_cast<int>(e / tile_elems);
+  const int off = static_cast<int>(e - t * tile_elems);
+  const int tm = t / tiles_n, tn = t - (t / tiles_n) * tiles_n;
+  const long long r = static_cast<long long>(tm) * 128 + off / 128;
+  const long long c = static_cast<long long>(tn) * 128 + off % 128;
+  if (r >= M || c >= N) return;
+  double v = 0.0;
+  for (int s = 0; s < splits; ++s) v += partial[(static_cast<long long>(s) * ntiles + t) * tile_elems + off];
+  double* cp = C + r * ldc + c;
+  *cp = alpha * v + (beta != 0.0 ? beta * *cp : 0.0);
+}
+
+size_t gemm_splitk_bytes(long long M, long long N, int splits) {
+  const long long tiles = ((M + 127) / 128) * ((N + 127) / 128);
+  return static_cast<size_t>(splits) * tiles * 128 * 128 * sizeof(double);
+}
+
+int gemm_splitk_choose(dngd_ctx* ctx, long long M, long long N, long long K) {
+  const long long tiles = ((M + 127) / 128) * ((N + 127) / 128);
+  long long s = (2LL * ctx->num_sms + tiles - 1) / tiles;
+  s = std::min(s, std::max(1LL, ((K + 15) / 16) / 16));  // >= 256 columns of K per split
+  return static_cast<int>(std::max(1LL, std::min(s, 64LL)));
+}
+
+int gemm_nt_splitk(dngd_ctx* ctx, cudaStream_t s, const GemmCall& g0, int splits,
+                   double* partial, size_t partial_bytes) {
+  if (g0.M <= 0 || g0.N <= 0) return DNGD_OK;
+  if (partial == nullptr || partial_bytes < gemm_splitk_bytes(g0.M, g0.N, splits)) {
+    return set_error(ctx, DNGD_ERR_DIMENSION, "gemm_nt_splitk: workspace too small");
+  }
+  GemmCall g = g0;
+  g.lower = 0;
+  g.batch = 1;
+  g.splits = splits;
+  g.partial = partial;
+  int rc = launch_gemm<128, 128, 2, 4, 5>(ctx, s, g);
+  if (rc) return rc;
+  const int tiles_n = static_cast<int>((g.N + 127) / 128);
+  const int ntiles = static_cast<int>(((g.M + 127) / 128) * tiles_n);
+  const long long total = static_cast<long long>(ntiles) * 128 * 128;
+  k_splitk_reduce<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+      partial, splits, ntiles, tiles_n, g.M, g.N, g.C, g.ldc, g.alpha, g.beta);
+  return cuda_status(ctx, cudaGetLastError(), "splitk reduce");
+}
+
 // ------------------------------------------------------------------ SYRK
 
 constexpr int kSyrkTile = 128;

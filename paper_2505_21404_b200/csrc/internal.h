@@ -41,6 +41,10 @@ struct GemmCall {
   double* partial = nullptr;
 };
 int gemm_nt(dngd_ctx* ctx, cudaStream_t s, const GemmCall& g);
+size_t gemm_splitk_bytes(long long M, long long N, int splits);
+int gemm_splitk_choose(dngd_ctx* ctx, long long M, long long N, long long K);
+int gemm_nt_splitk(dngd_ctx* ctx, cudaStream_t s, const GemmCall& g, int splits, double* partial,
+                   size_t partial_bytes);
 int syrk_plan(dngd_ctx* ctx, long long m, long long ncols, int* splits, long long* ntiles,
               size_t* work_bytes);
 int syrk(dngd_ctx* ctx, cudaStream_t s, const double* J, long long m, long long ncols,

@@ -639,6 +639,122 @@ static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const d
   return cuda_status(ctx, cudaGetLastError(), "forward");
 }
 
+// ------------------------------------------------------------------ J^T w without J
+// The vjp of residuals.py:220-227 from the activations of the last assembly:
+//   (J^T w)[W_k|b_k] = sum_rho w_{i(rho)} Hext_k[rho] (x) Zbar_k[rho]
+// = Hext_k^T diag(w) Zbar_k, a split-K FP64 tensor-core GEMM over activation
+// rows for the hidden layers; the input layer (Hext = input channels) and the
+// output layer (Zbar = seeds) are small deterministic reductions.
+
+DNGD_DEV long long act_point(const Classes& T, long long rho, int& ch) {
+  int c = 0;
+#pragma unroll
+  for (int k = 1; k < MAXC; ++k)
+    if (k < T.n && rho >= T.c[k].act0) c = k;
+  const ClassDev& C = T.c[c];
+  const long long loc = rho - C.act0;
+  const long long i = loc / C.nch;
+  ch = static_cast<int>(loc - i * C.nch);
+  return C.row0 + i;
+}
+
+// dst[q][rho] = w[point(rho)] * src[rho][q] for q < width; with bias_row the extra
+// row dst[width][rho] = (channel(rho) == 0) * w[point(rho)] (Hext's bias entry)
+__global__ void k_act_transpose(Classes T, const double* __restrict__ src, long long lds,
+                                int width, const double* __restrict__ wvec, int bias_row,
+                                double* __restrict__ dst, long long ldd) {
+  __shared__ double tile[32][33];
+  const long long rho0 = static_cast<long long>(blockIdx.x) * 32;
+  const int q0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const long long rho = rho0 + k;
+    const int q = q0 + threadIdx.x;
+    double v = 0.0;
+    if (rho < T.R) {
+      int ch;
+      const long long i = act_point(T, rho, ch);
+      const double s = wvec ? wvec[i] : 1.0;
+      if (q < width) {
+        v = s * src[rho * lds + q];
+      } else if (q == width && bias_row) {
+        v = ch == 0 ? s : 0.0;
+      }
+    }
+    tile[k][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int q = q0 + k;
+    const long long rho = rho0 + threadIdx.x;
+    if (q < width + bias_row && rho < T.R) dst[q * ldd + rho] = tile[threadIdx.x][k];
+  }
+}
+
+// input layer: part[chunk][p][q], p <= din (p == din: bias) over a chunk of points
+__global__ void k_jt_input(Classes T, const double* __restrict__ Zb, long long ld, int w1,
+                           const double* __restrict__ wvec, long long chunk,
+                           double* __restrict__ part) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= w1) return;
+  const long long i0 = blockIdx.y * chunk;
+  const long long i1 = min(T.m, i0 + chunk);
+  const int din = T.din;
+  double acc[MAXG + 1];
+#pragma unroll
+  for (int p = 0; p <= MAXG; ++p) acc[p] = 0.0;
+  for (long long i = i0; i < i1; ++i) {
+    const ClassDev& C = T.c[find_class(T, i)];
+    const long long base = C.act0 + (i - C.row0) * C.nch;
+    const double wi = wvec[i];
+    const double zv = wi * Zb[base * ld + q];
+    const double* x = C.pts + (i - C.row0) * din;
+#pragma unroll
+    for (int p = 0; p < MAXG; ++p)
+      if (p < din) acc[p] = fma(x[p], zv, acc[p]);
+    acc[MAXG] += zv;
+    for (int g = 0; g < C.ngrad; ++g) {
+      const double zg = wi * Zb[(base + 1 + g) * ld + q];
+#pragma unroll
+      for (int p = 0; p < MAXG; ++p)
+        if (p == C.grad_dims[g]) acc[p] += zg;
+    }
+  }
+  double* dst = part + static_cast<long long>(blockIdx.y) * (din + 1) * w1;
+  for (int p = 0; p < din; ++p) dst[p * w1 + q] = acc[p];
+  dst[din * w1 + q] = acc[MAXG];
+}
+
+// output layer: part[chunk][p], p <= w (p == w: bias)
+__global__ void k_jt_output(Classes T, const double* __restrict__ H, long long ld, int w,
+                            const double* __restrict__ wvec, long long chunk,
+                            double* __restrict__ part) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > w) return;
+  const long long i0 = blockIdx.y * chunk;
+  const long long i1 = min(T.m, i0 + chunk);
+  double acc = 0.0;
+  for (long long i = i0; i < i1; ++i) {
+    const ClassDev& C = T.c[find_class(T, i)];
+    const long long base = C.act0 + (i - C.row0) * C.nch;
+    double s = 0.0;
+    for (int ch = 0; ch < C.nch; ++ch) {
+      const double h = p < w ? H[(base + ch) * ld + p] : (ch == 0 ? 1.0 : 0.0);
+      s = fma(C.weight * coef(C, ch), h, s);
+    }
+    acc = fma(wvec[i], s, acc);
+  }
+  part[static_cast<long long>(blockIdx.y) * (w + 1) + p] = acc;
+}
+
+__global__ void k_chunk_reduce(const double* __restrict__ part, int nchunks, long long count,
+                               double scale, double* __restrict__ out) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  double s = 0.0;
+  for (int k = 0; k < nchunks; ++k) s += part[static_cast<long long>(k) * count + e];
+  out[e] = scale * s;
+}
+
 #include "gram_factored.cuh"
 
 static size_t bytes_of(const Plan& P, int mode, int C) {
@@ -770,6 +886,21 @@ extern "C" int dngd_assemble(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* m
   AsmBufs B;
   carve_assemble(P, A, B);
   return assemble_impl(ctx, s, P, B, theta, col_begin, col_end, r, J, ldJ, false);
+}
+
+extern "C" int dngd_activations(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                                const double* theta, const dngd_class_desc* classes, int nclass,
+                                double* r, void* work, size_t work_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  if (bytes_of(P, 0, 1) > work_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "activations: workspace too small");
+  if (P.m == 0) return DNGD_OK;
+  Arena A{static_cast<char*>(work)};
+  AsmBufs B;
+  carve_assemble(P, A, B);
+  return assemble_impl(ctx, s, P, B, theta, 0, P.n, r, nullptr, 0, true);
 }
 
 extern "C" int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
@@ -940,4 +1071,107 @@ extern "C" int dngd_loss_many(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* 
                                                     P.R * P.ldmax, B.r, P.m);
   k_half_sumsq<<<ncand, 256, 0, s>>>(B.r, P.m, losses);
   return cuda_status(ctx, cudaGetLastError(), "loss_many");
+}
+
+namespace {
+
+struct JtScratch {
+  long long ldR, chunk;
+  int nchunks, splits;
+  size_t bytes, off_zt, off_part, part_bytes;
+};
+
+JtScratch jt_plan(dngd_ctx* ctx, const Plan& P) {
+  JtScratch S;
+  S.ldR = (P.R + 15) / 16 * 16;
+  S.nchunks = static_cast<int>(std::max(1LL, std::min<long long>(256, P.m / 8)));
+  S.chunk = (P.m + S.nchunks - 1) / S.nchunks;
+  S.splits = 1;
+  size_t part = 0;
+  for (int k = 1; k <= P.L - 2; ++k) {
+    const int sp = gemm_splitk_choose(ctx, P.w[k] + 1, P.w[k + 1], P.R);
+    S.splits = std::max(S.splits, sp);
+    part = std::max(part, gemm_splitk_bytes(P.w[k] + 1, P.w[k + 1], sp));
+  }
+  part = std::max(part, static_cast<size_t>(S.nchunks) * static_cast<size_t>((P.w[0] + 1) * P.w[1]) * 8);
+  part = std::max(part, static_cast<size_t>(S.nchunks) * static_cast<size_t>(P.w[P.L - 1] + 1) * 8);
+  const size_t ht = static_cast<size_t>(P.wmax + 1) * S.ldR * 8;
+  S.off_zt = (ht + 255) / 256 * 256;
+  S.off_part = S.off_zt + (static_cast<size_t>(P.wmax) * S.ldR * 8 + 255) / 256 * 256;
+  S.part_bytes = part;
+  S.bytes = S.off_part + part;
+  return S;
+}
+
+}  // namespace
+
+extern "C" int dngd_jt_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp,
+                                 const dngd_class_desc* classes, int nclass, size_t* bytes) {
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  *bytes = jt_plan(ctx, P).bytes;
+  return DNGD_OK;
+}
+
+extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                                const dngd_class_desc* classes, int nclass, const double* w,
+                                double scale, double* out, void* act_work, size_t act_bytes,
+                                void* scratch, size_t scratch_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  if (bytes_of(P, 0, 1) > act_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "jt_factored: activation workspace too small");
+  const JtScratch S = jt_plan(ctx, P);
+  if (scratch == nullptr || scratch_bytes < S.bytes) {
+    return set_error(ctx, DNGD_ERR_DIMENSION, "jt_factored: scratch workspace too small");
+  }
+  if (P.m == 0) return DNGD_OK;
+  Arena A{static_cast<char*>(act_work)};
+  AsmBufs B;
+  carve_assemble(P, A, B);
+  char* sc = static_cast<char*>(scratch);
+  double* Ht = reinterpret_cast<double*>(sc);
+  double* Zt = reinterpret_cast<double*>(sc + S.off_zt);
+  double* part = reinterpret_cast<double*>(sc + S.off_part);
+  const int L = P.L;
+  // input layer W0 | b0
+  {
+    const int w1 = static_cast<int>(P.w[1]);
+    dim3 g((w1 + 127) / 128, S.nchunks);
+    k_jt_input<<<g, 128, 0, s>>>(P.T, B.Zb[0], P.ld[1], w1, w, S.chunk, part);
+    const long long cnt = (P.w[0] + 1) * P.w[1];
+    k_chunk_reduce<<<nblk(cnt), 256, 0, s>>>(part, S.nchunks, cnt, scale, out + P.off[0]);
+  }
+  // hidden layers: Hext_k^T diag(w) Zbar_k on the tensor cores
+  for (int k = 1; k <= L - 2; ++k) {
+    const int wk = static_cast<int>(P.w[k]), wk1 = static_cast<int>(P.w[k + 1]);
+    dim3 tg(static_cast<unsigned>((P.R + 31) / 32), static_cast<unsigned>((wk + 1 + 31) / 32));
+    k_act_transpose<<<tg, dim3(32, 8), 0, s>>>(P.T, B.H[k], P.ld[k], wk, nullptr, 1, Ht, S.ldR);
+    dim3 zg(static_cast<unsigned>((P.R + 31) / 32), static_cast<unsigned>((wk1 + 31) / 32));
+    k_act_transpose<<<zg, dim3(32, 8), 0, s>>>(P.T, B.Zb[k], P.ld[k + 1], wk1, w, 0, Zt, S.ldR);
+    GemmCall g;
+    g.M = wk + 1;
+    g.N = wk1;
+    g.K = P.R;
+    g.A = Ht;
+    g.lda = S.ldR;
+    g.B = Zt;
+    g.ldb = S.ldR;
+    g.C = out + P.off[k];
+    g.ldc = wk1;
+    g.alpha = scale;
+    g.beta = 0.0;
+    rc = gemm_nt_splitk(ctx, s, g, gemm_splitk_choose(ctx, g.M, g.N, g.K), part, S.part_bytes);
+    if (rc) return rc;
+  }
+  // output layer W_{L-1} | b_{L-1}
+  {
+    const int wl = static_cast<int>(P.w[L - 1]);
+    dim3 g((wl + 1 + 127) / 128, S.nchunks);
+    k_jt_output<<<g, 128, 0, s>>>(P.T, B.H[L - 1], P.ld[L - 1], wl, w, S.chunk, part);
+    k_chunk_reduce<<<nblk(wl + 1), 256, 0, s>>>(part, S.nchunks, wl + 1, scale, out + P.off[L - 1]);
+  }
+  return cuda_status(ctx, cudaGetLastError(), "jt_factored");
 }

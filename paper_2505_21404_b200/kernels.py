@@ -199,6 +199,24 @@ def gram_factored(mlp, theta, classes_arr, nclass, r, K, ws):
          nclass, ptr(r), ptr(K), K.stride(0), ptr(ws), ws.numel())
 
 
+def activations(mlp, theta, classes_arr, nclass, r, ws):
+    """r and the forward / adjoint activations (no J) into ws."""
+    call("dngd_activations", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), classes_arr,
+         nclass, ptr(r), ptr(ws), ws.numel())
+
+
+def jt_workspace_bytes(mlp, classes_arr, nclass) -> int:
+    nb = c_size()
+    call("dngd_jt_workspace", ctx(), ctypes.byref(mlp), classes_arr, nclass, ctypes.byref(nb))
+    return nb.value
+
+
+def jt_factored(mlp, classes_arr, nclass, w, scale, out, act_ws, scratch):
+    """out = scale * J^T w from the activations in act_ws (no J)."""
+    call("dngd_jt_factored", ctx(), stream_handle(), ctypes.byref(mlp), classes_arr, nclass, ptr(w),
+         float(scale), ptr(out), ptr(act_ws), act_ws.numel(), ptr(scratch), scratch.numel())
+
+
 def fvv(mlp, theta, v, classes_arr, nclass, out, ws):
     call("dngd_fvv", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), ptr(v), classes_arr,
          nclass, ptr(out), ptr(ws), ws.numel())

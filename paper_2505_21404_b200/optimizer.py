@@ -223,14 +223,19 @@ def _dngd_loop(trace: TrainTrace, rmap_provider, theta: ParameterVector, config:
             break
         try:
             rmap = rmap_provider(iteration)
-            r, J = rmap.linearize_t(theta)
+            jfree = rmap.m < config.dense_threshold and getattr(rmap, "jfree", lambda: False)()
+            if jfree:  # dense step without J: g = J^T r stays implicit
+                r, J, g = rmap.residuals_t(theta), None, None
+            else:
+                r, J = rmap.linearize_t(theta)
             loss = 0.5 * float(K.dot(r, r).item())
             if not np.isfinite(loss):
                 from .residuals import _raise_nonfinite
 
                 _raise_nonfinite(r, rmap.partition())
-            with stage("gemv"):
-                g = K.gemv_t(J, r, rmap.n)
+            if not jfree:
+                with stage("gemv"):
+                    g = K.gemv_t(J, r, rmap.n)
             lam = lm_damping(loss, config.lam_cap) * 10.0**rejections
             step = _dispatch_step(rmap, theta, g, lam, config, rng)
         except Exception as exc:

@@ -374,6 +374,9 @@ class LinearResidualMap(ResidualMap):
         return 0.5 * (R * R).sum(dim=1)
 
 
+_ACT_STATE: dict = {}  # which (theta version, map) the shared activation workspace holds
+
+
 class PinnResidualMap(ResidualMap):
     """Weighted PDE residuals of a tanh MLP, evaluated by the CUDA library."""
 
@@ -397,6 +400,7 @@ class PinnResidualMap(ResidualMap):
         self.col_range = (0, self.layout.size) if col_range is None else tuple(col_range)
         self._dev = None
         self._cache = None
+        self._rcache = None
         self._J = None
 
     def rebind(self, collocation):
@@ -454,10 +458,18 @@ class PinnResidualMap(ResidualMap):
                          per_cand=max(per_cand, 1), device=dev)
         return self._dev
 
-    def _workspace(self, nbytes):
+    def _workspace(self, nbytes, tag="pinn_scratch"):
+        """Scratch for f_vv / line search / residual-only passes."""
         from . import kernels as K
 
-        return K.workspace("pinn", nbytes)
+        return K.workspace(tag, nbytes)
+
+    def _act_workspace(self):
+        """Activation workspace (forward channels + adjoints of the last assembly):
+        kept apart from the scratch so J^T w can reuse it after f_vv / line search."""
+        from . import kernels as K
+
+        return K.workspace("pinn_act", self._device()["ws_bytes"])
 
     @property
     def ncols(self) -> int:
@@ -480,10 +492,10 @@ class PinnResidualMap(ResidualMap):
         if self._J is None or self._J.shape != (m, K.pad_ld(self.ncols)):
             self._J = torch.empty((m, K.pad_ld(self.ncols)), dtype=torch.float64, device=d["device"])
         r = torch.empty(m, dtype=torch.float64, device=d["device"])
-        ws = self._workspace(d["ws_bytes"])
         with stage("assemble"):
             K.assemble(d["mlp"], th, d["arr"], d["nclass"], r, self._J, self.col_range[0],
-                       self.col_range[1], ws)
+                       self.col_range[1], self._act_workspace())
+        _ACT_STATE["key"] = (key, self._act_identity())
         self._cache = (key, r, self._J)
         return r, self._J
 
@@ -495,6 +507,8 @@ class PinnResidualMap(ResidualMap):
         th = self._theta_t(theta)
         if self._cache is not None and self._cache[0] == self._key(th):
             return self._cache[1]
+        if self._rcache is not None and self._rcache[0] == self._key(th):
+            return self._rcache[1]
         d = self._device()
         r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
         K.assemble(d["mlp"], th, d["arr"], d["nclass"], r, None, 0, self.n,
@@ -513,7 +527,7 @@ class PinnResidualMap(ResidualMap):
                   self._workspace(d["ws_bytes"]))
         return out
 
-    # -- factored Gram (no pass over J) ------------------------------------------------
+    # -- factored Gram and J^T w (no pass over J) ----------------------------------------
     gram_mode = "auto"  # "auto" | "factored" | "materialized"
 
     def _gram_flop_ratio(self) -> float:
@@ -545,16 +559,59 @@ class PinnResidualMap(ResidualMap):
         # the factored kernel runs at ~0.7 of the SYRK's tensor-pipe efficiency
         return self._gram_flop_ratio() < 0.3
 
+    def jfree(self) -> bool:
+        """Dense step without J: factored Gram + J^T w from the activations."""
+        return self.use_factored_gram()
+
+    def _act_identity(self):
+        return (id(self), self._dev["arr"] if self._dev else None)
+
+    def _act_valid(self, th) -> bool:
+        return _ACT_STATE.get("key") == (self._key(th), self._act_identity())
+
     def gram_factored_t(self, theta, K_out):
+        """K = J J^T (and r) from the activations; leaves them for vjp_t."""
         import torch
 
         from . import kernels as K
 
         d = self._device()
+        th = self._theta_t(theta)
         r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
-        K.gram_factored(d["mlp"], self._theta_t(theta), d["arr"], d["nclass"], r, K_out,
-                        self._workspace(d["ws_bytes"]))
+        K.gram_factored(d["mlp"], th, d["arr"], d["nclass"], r, K_out, self._act_workspace())
+        _ACT_STATE["key"] = (self._key(th), self._act_identity())
+        self._rcache = (self._key(th), r)
         return K_out
+
+    def residuals_gram_t(self, theta, K_out):
+        self.gram_factored_t(theta, K_out)
+        return self._rcache[1], K_out
+
+    def vjp_t(self, theta, w_t, g_t=None, scale=1.0):
+        """scale * (J^T w + g); from the activations when no J is materialised."""
+        from . import kernels as K
+
+        th = self._theta_t(theta)
+        if self._cache is not None and self._cache[0] == self._key(th):
+            return K.gemv_t(self._J, w_t, self.ncols, g_t, scale)
+        if self.col_range != (0, self.layout.size):
+            return super().vjp_t(theta, w_t, g_t, scale)
+        import torch
+
+        d = self._device()
+        if not self._act_valid(th):
+            r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
+            K.activations(d["mlp"], th, d["arr"], d["nclass"], r, self._act_workspace())
+            _ACT_STATE["key"] = (self._key(th), self._act_identity())
+            self._rcache = (self._key(th), r)
+        out = torch.empty(self.n, dtype=torch.float64, device=d["device"])
+        scratch = K.workspace("jt", K.jt_workspace_bytes(d["mlp"], d["arr"], d["nclass"]))
+        with stage("vjp"):
+            K.jt_factored(d["mlp"], d["arr"], d["nclass"], w_t.contiguous(), scale, out,
+                          self._act_workspace(), scratch)
+        if g_t is not None:
+            out.add_(g_t, alpha=scale)
+        return out
 
     def _loss_ws(self, C):
         from . import kernels as K

@@ -297,3 +297,29 @@ def test_pcg_zero_gradient_and_breakdown(P):
     res = P.pcg_step(lin, th, np.ones(4), lam=1e6, landmark_count=2, rng=32)
     assert res.warning is not None and "breakdown" in res.warning
     assert np.all(np.isfinite(res.delta.data))
+
+
+@pytest.mark.parametrize("name", ["cfg2_step", "cfg3_step"])
+def test_jfree_step_matches_materialized(P, golden_dir, name):
+    """J-free dense step (factored Gram + J^T w from the activations) == J-based step,
+    and J^T w from the activations == J^T w over the materialised J."""
+    fx = _load(golden_dir, name)
+    pname, ids, oprob = STEP[name]
+    rmap, theta, widths = _map(P, fx, pname, ids)
+    rmap.gram_mode = "factored"
+    assert rmap.jfree()
+    w = np.random.default_rng(3).normal(size=rmap.m)
+    jt_free = rmap.vjp(theta, w)
+    for i, lam in enumerate(fx["lams"]):
+        res_free = P.dense_dual_solve(rmap, theta, None, lam=lam, use_ga=True)
+        ref = fx[f"delta_{i}"]
+        oclasses = oprob.classes(*[fx[f"pts_{c}"] for c in ids])
+        _, Jo = O.linearize(fx["theta"], widths, oclasses)
+        fl = O.direction_floors(Jo, fx["g"], lam,
+                                lambda v: O.second_directional(fx["theta"], widths, oclasses, v))
+        assert _rel(res_free.delta.data, ref) <= max(1e-8, 10 * fl["delta"])
+    rmap.gram_mode = "materialized"
+    rmap._cache = None
+    jt_mat = rmap.vjp(theta, w)
+    assert _rel(jt_free, jt_mat) <= 1e-12
+    assert _rel(jt_free, Jo.T @ w) <= 1e-11

@@ -42,6 +42,9 @@ CONFIGS = {
             dense_threshold=4000, name="cfg2_heat1d_2-64x4-1_m2800"),
     3: dict(problem="poisson5d_sin", widths=(5, 512, 512, 512, 512, 1), counts=(3500, 500),
             lam_cap=1e-5, dense_threshold=4001, name="cfg3_poisson5d_5-512x4-1_m4000"),
+    4: dict(problem="poisson5d_sin", widths=(5, 1792, 1792, 1792, 1792, 1792, 1),
+            counts=(7000, 1000), lam_cap=1e-5, dense_threshold=8001,
+            name="cfg4_poisson5d_5-1792x5-1_m8000_n12.86M"),
     5: dict(problem="poisson2d", widths=(2, 256, 256, 256, 256, 1), counts=(30000, 2000),
             lam_cap=1e-5, dense_threshold=4000, nystrom_rank=512, cg_max_iters=200,
             name="cfg5_poisson2d_2-256x4-1_m32000_pcg"),
@@ -331,11 +334,24 @@ def run_ours(args, cfg):
                 "frac": ach / fp64_peak, "traffic": None,
                 "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
                 "algorithmic": f"m(m+1)n = {flops:.3e} FLOP per launch"}
+    gram_avg = stages.get("gram", 0.0) / max(counts.get("gram", 1), 1) * 1e-3
+    if gram_avg > 0 and (roof is None or gram_avg > syrk_avg):
+        flops = maps[0].factored_gram_flops()
+        ach = flops / gram_avg / 1e12
+        roof = {"kernel": "dngd::k_gram_factored (K = sum_k S (G^H_k o G^Z_k) S^T, J-free)",
+                "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": ach / fp64_peak, "traffic": None,
+                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
+                "algorithmic": f"factored Gram {flops:.3e} FLOP per launch",
+                "jjt_equivalent_tflops": m * (m + 1) * n / gram_avg / 1e12}
     gram_chol = None
-    if syrk_avg > 0 and potrf_avg > 0:
-        gf = (m * (m + 1) * n + m**3 / 3) / (syrk_avg + potrf_avg) / 1e12
+    g_avg = syrk_avg if syrk_avg > 0 else gram_avg
+    if g_avg > 0 and potrf_avg > 0:
+        # J J^T-equivalent rate of the Gram + Cholesky stage (north-star definition)
+        gf = (m * (m + 1) * n + m**3 / 3) / (g_avg + potrf_avg) / 1e12
         gram_chol = {"tflops": gf, "frac_of_fp64_peak": gf / fp64_peak,
-                     "syrk_ms": syrk_avg * 1e3, "potrf_ms": potrf_avg * 1e3}
+                     "gram_ms": g_avg * 1e3, "potrf_ms": potrf_avg * 1e3,
+                     "gram_path": "syrk" if syrk_avg > 0 else "factored"}
     gemv_bytes = 8 * m * n
     line = {
         "metric": METRIC,

@@ -543,6 +543,20 @@ class PinnResidualMap(ResidualMap):
                 fact += c.count * cp.count * a * b * ksum
         return fact / max(1.0, float(self.m) ** 2 * self.n)
 
+    def factored_gram_flops(self) -> float:
+        """Algorithmic FLOPs of the factored Gram: lower G-space blocks x two GEMMs
+        per layer (K-dims w_k, w_{k+1}; layer 0 / output layer analytic)."""
+        w = self.spec.layer_widths
+        ksum = sum((w[k] if k >= 1 else 0) + (w[k + 1] if k <= len(w) - 3 else 0)
+                   for k in range(len(w) - 1))
+        rows = [c.count * (1 << max(0, (self._nch(c) - 1).bit_length()))
+                for c in self.collocation.classes]
+        pairs = 0.0
+        for i, a in enumerate(rows):
+            for j, b in enumerate(rows[: i + 1]):
+                pairs += a * (a + 1) / 2 if i == j else a * b
+        return 2.0 * pairs * ksum
+
     def _nch(self, cls) -> int:
         op = self.problem.class_operator(cls.class_id)
         return 1 + len(op.grad_dims) + (1 if op.lap_dims else 0)

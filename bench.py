@@ -230,15 +230,26 @@ def run_ours(args, cfg):
             delta = step["delta"]
             ls = sharded_line_search(ops, comm, theta, delta, loss, config.line_search_points)
         else:
-            g = None
-            if not jfree:
-                with timing.stage("gemv"):
-                    g = K.gemv_t(J, r, rmap.n)
-            from paper_2505_21404_b200.optimizer import _dispatch_step
+            from paper_2505_21404_b200.optimizer import _dispatch_step, _select
+            from paper_2505_21404_b200.solver import fused_dense_step
 
-            step = _dispatch_step(rmap, theta, g, lam, config, rng)
-            delta = step.delta.tensor
-            ls = device_line_search(rmap, theta, delta, loss, config.line_search_points)
+            fused = None
+            if rmap.m < config.dense_threshold:
+                fused = fused_dense_step(rmap, theta, r, lam, config.use_ga,
+                                         config.line_search_points)
+            if fused is not None:
+                step = fused[0]
+                delta = step.delta.tensor
+                etas = 2.0 ** -np.arange(config.line_search_points, dtype=np.float64)
+                ls = _select(fused[1], etas, loss, config.line_search_points)
+            else:
+                g = None
+                if not jfree:
+                    with timing.stage("gemv"):
+                        g = K.gemv_t(J, r, rmap.n)
+                step = _dispatch_step(rmap, theta, g, lam, config, rng)
+                delta = step.delta.tensor
+                ls = device_line_search(rmap, theta, delta, loss, config.line_search_points)
         if ls.rejected:
             return theta, step
         return P.ParameterVector(K.axpby(ls.eta, delta, 1.0, theta.tensor), theta.layout), step

@@ -181,22 +181,26 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
       for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const double2*>(sa + i * 1024 + sw);
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const double2*>(sb + j * 1024 + sw);
+      // the .x and .y halves go through separate passes so consecutive DMMAs on
+      // one accumulator are 16 instructions apart (no back-to-back dependency)
       if (partH) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            dmma_8x8x4(accH[i][j], a[i].x, b[j].x);
-            dmma_8x8x4(accH[i][j], a[i].y, b[j].y);
-          }
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(accH[i][j], a[i].x, b[j].x);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(accH[i][j], a[i].y, b[j].y);
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            dmma_8x8x4(accZ[i][j], a[i].x, b[j].x);
-            dmma_8x8x4(accZ[i][j], a[i].y, b[j].y);
-          }
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(accZ[i][j], a[i].x, b[j].x);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(accZ[i][j], a[i].y, b[j].y);
       }
     }
     __syncwarp();

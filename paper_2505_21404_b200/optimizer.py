@@ -19,7 +19,7 @@ from .errors import ConfigError, DomainError
 from .model import INITIALIZERS, MlpSpec
 from .params import ParameterVector
 from .residuals import PinnResidualMap, ResidualMap
-from .solver import StepResult, dense_dual_solve, pcg_step
+from .solver import StepResult, dense_dual_solve, fused_dense_step, pcg_step
 from .timing import stage
 
 LAMBDA_FLOOR = 1e-12
@@ -221,9 +221,11 @@ def _dngd_loop(trace: TrainTrace, rmap_provider, theta: ParameterVector, config:
         iteration += 1
         if _budget_reached(config, iteration, clock):
             break
+        fused = None
         try:
             rmap = rmap_provider(iteration)
-            jfree = rmap.m < config.dense_threshold and getattr(rmap, "jfree", lambda: False)()
+            dense = rmap.m < config.dense_threshold
+            jfree = dense and getattr(rmap, "jfree", lambda: False)()
             if jfree:  # dense step without J: g = J^T r stays implicit
                 r, J, g = rmap.residuals_t(theta), None, None
             else:
@@ -233,17 +235,30 @@ def _dngd_loop(trace: TrainTrace, rmap_provider, theta: ParameterVector, config:
                 from .residuals import _raise_nonfinite
 
                 _raise_nonfinite(r, rmap.partition())
-            if not jfree:
-                with stage("gemv"):
-                    g = K.gemv_t(J, r, rmap.n)
             lam = lm_damping(loss, config.lam_cap) * 10.0**rejections
-            step = _dispatch_step(rmap, theta, g, lam, config, rng)
+            if dense:
+                # device-resident step + line search, two host syncs (solver.fused_dense_step)
+                fused = fused_dense_step(rmap, theta, r, lam, config.use_ga,
+                                         config.line_search_points)
+            if fused is None:
+                if not jfree:
+                    with stage("gemv"):
+                        g = K.gemv_t(J, r, rmap.n)
+                step = _dispatch_step(rmap, theta, g, lam, config, rng)
+            else:
+                step = fused[0]
         except Exception as exc:
             trace.aborted = True
             trace.abort_reason = f"error at iteration {iteration}: {exc!r}"
             break
         delta_t = step.delta.tensor
-        if not bool(delta_t.any().item()):
+        if fused is not None:
+            etas = 2.0 ** -np.arange(config.line_search_points, dtype=np.float64)
+            if not fused[2]:
+                ls = LineSearchResult(1.0, loss, False, 0, False)
+            else:
+                ls = _select(fused[1], etas, loss, config.line_search_points)
+        elif not bool(delta_t.any().item()):
             ls = LineSearchResult(1.0, loss, False, 0, False)
         else:
             ls = device_line_search(rmap, theta, delta_t, loss, config.line_search_points)

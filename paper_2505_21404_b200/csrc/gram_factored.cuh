@@ -17,8 +17,15 @@
 // kernel runs two FP64 tensor-core GEMMs (K-dims w_k and w_{k+1}) through one
 // TMA/mbarrier ring, multiplies the accumulators elementwise, reduces each
 // a x b channel block with warp shuffles and adds the point-pair sums into a
-// K tile in shared memory.  Layer 0 (Hext = input channels) is evaluated
-// analytically; the output layer's Zbar are the residual-operator seeds.
+// K tile in shared memory.
+//
+// Every layer takes the same epilogue: layer 0's Hext (the input channels:
+// value [x], d_j [e_j], Laplacian 0) is materialised once by k_input_channels,
+// the bias entry of Hext (1 on the value channel) is a per-thread constant, and
+// the output layer's Zbar are the residual-operator seeds, whose outer product
+// is also a per-thread constant: an 8x8 fragment's rows are channels
+// lane/4 mod a and its columns 2(lane%4)+{0,1} mod b for every fragment.  The
+// channel reduction is instantiated per (a, b) so its shuffles are static.
 // Work: sum_k (a_c a_c') (w_k + w_{k+1}) per point pair instead of w_k w_{k+1}
 // for J J^T -- ~2x fewer FLOPs at config 2, ~4x at config 3, ~14x at config 4,
 // and J (823 GB at config 4) never has to exist.
@@ -27,9 +34,10 @@ constexpr int GF_BM = 64;  // G-rows per tile side
 constexpr int GF_STAGES = 4;
 constexpr int GF_THREADS = 128;  // 2 x 2 warps, 32 x 32 warp tiles
 constexpr int GF_STAGE_BYTES = 2 * GF_BM * 128;
+constexpr int GF_H0_LD = 16;  // row pitch of the materialised input channels
 
 struct GramLayer {
-  int kh;  // w_k (0 for layer 0: analytic input channels)
+  int kh;  // w_k (din for layer 0: materialised input channels)
   int kz;  // w_{k+1} (0 for the output layer: seeds)
 };
 
@@ -47,45 +55,75 @@ struct GramParams {
   long long ldK;
 };
 
-struct ChunkId {
-  int k, part, kc, n_h, n_z;  // part 0 = H, 1 = Z
-};
-
-DNGD_DEV ChunkId decode_chunk(const GramParams& p, int f) {
-  ChunkId id;
-  for (int k = 0;; ++k) {
-    const int nh = (p.lay[k].kh + 15) >> 4, nz = (p.lay[k].kz + 15) >> 4;
-    if (f < nh + nz || k == p.L - 1) {
-      id.k = k;
-      id.n_h = nh;
-      id.n_z = nz;
-      id.part = f < nh ? 0 : 1;
-      id.kc = f < nh ? f : f - nh;
-      return id;
+// Hext_0 rows: value channel [x], derivative channel d_j [e_j], Laplacian 0
+__global__ void k_input_channels(Classes T, double* __restrict__ H0) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= T.R * GF_H0_LD) return;
+  const long long rho = idx / GF_H0_LD;
+  const int d = static_cast<int>(idx - rho * GF_H0_LD);
+  int ch;
+  const long long p = act_point(T, rho, ch);
+  const ClassDev& C = T.c[find_class(T, p)];
+  double v = 0.0;
+  if (d < T.din) {
+    if (ch == 0) {
+      v = C.pts[(p - C.row0) * T.din + d];
+    } else if (ch <= C.ngrad) {
+      v = C.grad_dims[ch - 1] == d ? 1.0 : 0.0;
     }
-    f -= nh + nz;
   }
+  H0[idx] = v;
 }
 
-// analytic Hext_0 . Hext_0' for input channels (value: [x, 1], grad d: [e_d, 0], lap: 0)
-DNGD_DEV double gh_input(const ClassDev& C, int ch, const double* xi, const ClassDev& Cp, int chp,
-                         const double* xj, int din) {
-  if (ch >= C.nch || chp >= Cp.nch) return 0.0;
-  const bool lap_i = C.nlap && ch == C.nch - 1;
-  const bool lap_j = Cp.nlap && chp == Cp.nch - 1;
-  if (lap_i || lap_j) return 0.0;
-  if (ch == 0 && chp == 0) {
-    double s = 1.0;
-    for (int d = 0; d < din; ++d) s = fma(xi[d], xj[d], s);
-    return s;
-  }
-  if (ch == 0) return xi[Cp.grad_dims[chp - 1]];
-  if (chp == 0) return xj[C.grad_dims[ch - 1]];
-  return C.grad_dims[ch - 1] == Cp.grad_dims[chp - 1] ? 1.0 : 0.0;
-}
+DNGD_DEV int gf_layer_chunks(const GramLayer& l) { return ((l.kh + 15) >> 4) + ((l.kz + 15) >> 4); }
 
 DNGD_DEV double seed_of(const ClassDev& C, int ch) {
   return ch < C.nch ? C.weight * coef(C, ch) : 0.0;
+}
+
+// K[point pairs] += S (G_H o G_Z) S^T for one warp's 32 x 32 G-block.  Fragment
+// (i, j): rows lrow = lane/4 (+8i), columns 2(lane%4)+{0,1} (+8j); G-row bits
+// below LGA are the channel, so the row channel is lrow mod a for every i.
+template <int LGA, int LGB>
+DNGD_DEV void gf_epilogue(double2 (&accH)[4][4], double2 (&accZ)[4][4], bool seedZ, double bias0,
+                          double bias1, double sp0, double sp1, double* Ks, int wm, int wn,
+                          int lane) {
+  const int lrow = lane >> 2;
+  const bool own_r = (lrow & ((1 << LGA) - 1)) == 0;
+  const bool own_c = LGB <= 1 || (lane & ((1 << (LGB > 1 ? LGB - 1 : 0)) - 1)) == 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int pr = (wm * 32 + i * 8 + lrow) >> LGA;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gc = wn * 32 + j * 8 + 2 * (lane & 3);
+      double v0 = (accH[i][j].x + bias0) * (seedZ ? sp0 : accZ[i][j].x);
+      double v1 = (accH[i][j].y + bias1) * (seedZ ? sp1 : accZ[i][j].y);
+      accH[i][j] = make_double2(0.0, 0.0);
+      accZ[i][j] = make_double2(0.0, 0.0);
+      // column bits = (h, lane bit 0, lane bit 1), row bits = lane bits 2, 3, 4
+      if (LGB >= 1) v0 += v1;
+      if (LGB >= 2) v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
+      if (LGB >= 3) v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
+      if (LGA >= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, 4);
+        if (LGB == 0) v1 += __shfl_xor_sync(0xffffffffu, v1, 4);
+      }
+      if (LGA >= 2) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, 8);
+        if (LGB == 0) v1 += __shfl_xor_sync(0xffffffffu, v1, 8);
+      }
+      if (LGA >= 3) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, 16);
+        if (LGB == 0) v1 += __shfl_xor_sync(0xffffffffu, v1, 16);
+      }
+      if (own_r && own_c) {
+        double* k = Ks + pr * GF_BM + (gc >> LGB);
+        k[0] += v0;
+        if (LGB == 0) k[1] += v1;
+      }
+    }
+  }
 }
 
 __global__ void __launch_bounds__(GF_THREADS, 2)
@@ -94,9 +132,7 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(gf_smem_raw) + 1023) & ~uintptr_t(1023));
   double* Ks = reinterpret_cast<double*>(smem + GF_STAGES * GF_STAGE_BYTES);  // 64 x 64 points max
-  double* XA = Ks + GF_BM * GF_BM;
-  double* XB = XA + GF_BM * DNGD_MAX_GRAD;
-  uint64_t* full = reinterpret_cast<uint64_t*>(XB + GF_BM * DNGD_MAX_GRAD);
+  uint64_t* full = reinterpret_cast<uint64_t*>(Ks + GF_BM * GF_BM);
   uint64_t* empty = full + GF_STAGES;
   // ---- tile decode
   int pi = 0;
@@ -110,14 +146,11 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     ti = t / p.tj_n[pi];
     tj = t - ti * p.tj_n[pi];
   }
-  const ClassDev& C = p.T.c[c];
-  const ClassDev& Cp = p.T.c[cp];
   const int lga = p.lg[c], lgb = p.lg[cp];
   const int np_r = GF_BM >> lga, np_c = GF_BM >> lgb;
   const int P0 = ti * np_r, Q0 = tj * np_c;  // first point of the tile rows / cols
-  const int din = p.T.din;
   int nchunks = 0;
-  for (int k = 0; k < p.L; ++k) nchunks += ((p.lay[k].kh + 15) >> 4) + ((p.lay[k].kz + 15) >> 4);
+  for (int k = 0; k < p.L; ++k) nchunks += gf_layer_chunks(p.lay[k]);
 
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -127,21 +160,20 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     }
     fence_barrier_init();
   }
-  for (int e = threadIdx.x; e < GF_BM * GF_BM; e += GF_THREADS) Ks[e] = 0.0;
-  for (int e = threadIdx.x; e < GF_BM * din; e += GF_THREADS) {
-    const int r = e / din, d = e - (e / din) * din;
-    XA[r * DNGD_MAX_GRAD + d] = (r < np_r && P0 + r < C.count) ? C.pts[static_cast<long long>(P0 + r) * din + d] : 0.0;
-    XB[r * DNGD_MAX_GRAD + d] = (r < np_c && Q0 + r < Cp.count) ? Cp.pts[static_cast<long long>(Q0 + r) * din + d] : 0.0;
-  }
+  for (int e = threadIdx.x; e < GF_BM * GF_BM / 2; e += GF_THREADS)
+    reinterpret_cast<double2*>(Ks)[e] = make_double2(0.0, 0.0);
   __syncthreads();
 
   auto issue = [&](int f) {
-    const ChunkId id = decode_chunk(p, f);
+    int k = 0, g = f;
+    while (k < p.L - 1 && g >= gf_layer_chunks(p.lay[k])) g -= gf_layer_chunks(p.lay[k++]);
+    const int nh = (p.lay[k].kh + 15) >> 4;
+    const int part = g < nh ? 0 : 1, kc = g < nh ? g : g - nh;
     const int st = f % GF_STAGES;
     uint8_t* sa = smem + st * GF_STAGE_BYTES;
     mbar_arrive_expect_tx(&full[st], GF_STAGE_BYTES);
-    tma_load_3d(sa, &p.maps[id.k][id.part][c], &full[st], id.kc * 16, 0, P0);
-    tma_load_3d(sa + GF_BM * 128, &p.maps[id.k][id.part][cp], &full[st], id.kc * 16, 0, Q0);
+    tma_load_3d(sa, &p.maps[k][part][c], &full[st], kc * 16, 0, P0);
+    tma_load_3d(sa + GF_BM * 128, &p.maps[k][part][cp], &full[st], kc * 16, 0, Q0);
   };
   if (threadIdx.x == 0) {
     for (int f = 0; f < min(nchunks, GF_STAGES); ++f) issue(f);
@@ -150,6 +182,15 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp >> 1, wn = warp & 1;
   const int lrow = lane >> 2;
+  // per-thread constants of the epilogue (see gf_epilogue)
+  const int chr = lrow & ((1 << lga) - 1);
+  const int chc0 = (2 * (lane & 3)) & ((1 << lgb) - 1), chc1 = (2 * (lane & 3) + 1) & ((1 << lgb) - 1);
+  const double bias0 = (chr == 0 && chc0 == 0) ? 1.0 : 0.0;
+  const double bias1 = (chr == 0 && chc1 == 0) ? 1.0 : 0.0;
+  const double sr = seed_of(p.T.c[c], chr);
+  const double sp0 = sr * seed_of(p.T.c[cp], chc0), sp1 = sr * seed_of(p.T.c[cp], chc1);
+  const int epi = lga * 4 + lgb;
+
   double2 accH[4][4], accZ[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -158,7 +199,8 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
       accH[i][j] = make_double2(0.0, 0.0);
       accZ[i][j] = make_double2(0.0, 0.0);
     }
-  int k_cur = 0, f_layer_end = ((p.lay[0].kh + 15) >> 4) + ((p.lay[0].kz + 15) >> 4);
+  int k_cur = 0, f_layer_start = 0, f_layer_end = gf_layer_chunks(p.lay[0]);
+  int nh_cur = (p.lay[0].kh + 15) >> 4;
   for (int f = 0; f < nchunks; ++f) {
     const int st = f % GF_STAGES;
     if (threadIdx.x == 0 && f >= 1 && f - 1 + GF_STAGES < nchunks) {
@@ -168,8 +210,6 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     }
     __syncwarp();
     mbar_wait(&full[st], (f / GF_STAGES) & 1);
-    const int nh_cur = (p.lay[k_cur].kh + 15) >> 4;
-    const int f_layer_start = f_layer_end - nh_cur - ((p.lay[k_cur].kz + 15) >> 4);
     const bool partH = (f - f_layer_start) < nh_cur;
     const uint8_t* sa = smem + st * GF_STAGE_BYTES + (wm * 32 + lrow) * 128;
     const uint8_t* sb = smem + st * GF_STAGE_BYTES + GF_BM * 128 + (wn * 32 + lrow) * 128;
@@ -206,82 +246,36 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
     if (f + 1 != f_layer_end) continue;
-    // ---- layer k_cur done: K += S (G_H o G_Z) S^T for this warp's 32x32 G-block
-    const bool analyticH = p.lay[k_cur].kh == 0, seedZ = p.lay[k_cur].kz == 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int gr = wm * 32 + i * 8 + lrow;  // G-row within the tile
-      const int chr = gr & ((1 << lga) - 1);
-      const int pr = gr >> lga;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int gc = wn * 32 + j * 8 + 2 * (lane & 3);
-        double v0, v1;
-        {
-          const int chc0 = gc & ((1 << lgb) - 1), chc1 = (gc + 1) & ((1 << lgb) - 1);
-          const int pc0 = gc >> lgb, pc1 = (gc + 1) >> lgb;
-          double gh0, gh1, gz0, gz1;
-          if (analyticH) {
-            gh0 = gh_input(C, chr, XA + pr * DNGD_MAX_GRAD, Cp, chc0, XB + pc0 * DNGD_MAX_GRAD, din);
-            gh1 = gh_input(C, chr, XA + pr * DNGD_MAX_GRAD, Cp, chc1, XB + pc1 * DNGD_MAX_GRAD, din);
-          } else {
-            gh0 = accH[i][j].x + ((chr == 0 && chc0 == 0) ? 1.0 : 0.0);
-            gh1 = accH[i][j].y + ((chr == 0 && chc1 == 0) ? 1.0 : 0.0);
-          }
-          if (seedZ) {
-            const double sr = seed_of(C, chr);
-            gz0 = sr * seed_of(Cp, chc0);
-            gz1 = sr * seed_of(Cp, chc1);
-          } else {
-            gz0 = accZ[i][j].x;
-            gz1 = accZ[i][j].y;
-          }
-          v0 = gh0 * gz0;
-          v1 = gh1 * gz1;
-        }
-        // reduce each a x b channel block: col bits = (h, lane bit 0, lane bit 1),
-        // row bits = lane bits 2, 3, 4
-        if (lgb >= 1) {
-          v0 += v1;
-          v1 = 0.0;
-        }
-        if (lgb >= 2) v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
-        if (lgb >= 3) v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
-        if (lga >= 1) {
-          v0 += __shfl_xor_sync(0xffffffffu, v0, 4);
-          if (lgb == 0) v1 += __shfl_xor_sync(0xffffffffu, v1, 4);
-        }
-        if (lga >= 2) {
-          v0 += __shfl_xor_sync(0xffffffffu, v0, 8);
-          if (lgb == 0) v1 += __shfl_xor_sync(0xffffffffu, v1, 8);
-        }
-        if (lga >= 3) {
-          v0 += __shfl_xor_sync(0xffffffffu, v0, 16);
-          if (lgb == 0) v1 += __shfl_xor_sync(0xffffffffu, v1, 16);
-        }
-        const bool own_r = (lrow & ((1 << lga) - 1)) == 0;
-        const bool own_c = lgb <= 1 || (lane & ((1 << (lgb - 1)) - 1)) == 0;
-        if (own_r && own_c) {
-          const int pcl0 = gc >> lgb;
-          Ks[pr * GF_BM + pcl0] += v0;
-          if (lgb == 0) Ks[pr * GF_BM + pcl0 + 1] += v1;
-        }
-        accH[i][j] = make_double2(0.0, 0.0);
-        accZ[i][j] = make_double2(0.0, 0.0);
-      }
+    // ---- layer k_cur done
+    const bool seedZ = p.lay[k_cur].kz == 0;
+    switch (epi) {
+#define GF_EPI(A, B)                                                                            \
+  case A * 4 + B:                                                                               \
+    gf_epilogue<A, B>(accH, accZ, seedZ, bias0, bias1, sp0, sp1, Ks, wm, wn, lane);             \
+    break;
+      GF_EPI(0, 0) GF_EPI(0, 1) GF_EPI(0, 2) GF_EPI(0, 3)
+      GF_EPI(1, 0) GF_EPI(1, 1) GF_EPI(1, 2) GF_EPI(1, 3)
+      GF_EPI(2, 0) GF_EPI(2, 1) GF_EPI(2, 2) GF_EPI(2, 3)
+      GF_EPI(3, 0) GF_EPI(3, 1) GF_EPI(3, 2) GF_EPI(3, 3)
+#undef GF_EPI
+      default: break;
     }
     if (k_cur + 1 < p.L) {
       ++k_cur;
-      f_layer_end += ((p.lay[k_cur].kh + 15) >> 4) + ((p.lay[k_cur].kz + 15) >> 4);
+      f_layer_start = f_layer_end;
+      f_layer_end += gf_layer_chunks(p.lay[k_cur]);
+      nh_cur = (p.lay[k_cur].kh + 15) >> 4;
     }
   }
   __syncthreads();
   // ---- epilogue: K[row][col] and its mirror (one writer per entry)
+  const long long cnt_r = p.T.c[c].count, cnt_c = p.T.c[cp].count;
+  const long long row0 = p.T.c[c].row0, col0 = p.T.c[cp].row0;
   for (int e = threadIdx.x; e < np_r * np_c; e += GF_THREADS) {
     const int r = e / np_c, cc = e - (e / np_c) * np_c;
     const long long pr = P0 + r, pcl = Q0 + cc;
-    if (pr >= C.count || pcl >= Cp.count) continue;
-    const long long row = C.row0 + pr, col = Cp.row0 + pcl;
+    if (pr >= cnt_r || pcl >= cnt_c) continue;
+    const long long row = row0 + pr, col = col0 + pcl;
     if (c == cp && col > row) continue;
     const double v = Ks[r * GF_BM + cc];
     p.K[row * p.ldK + col] = v;
@@ -291,5 +285,5 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
 
 static size_t gram_factored_smem() {
   return 1024 + GF_STAGES * GF_STAGE_BYTES + GF_BM * GF_BM * sizeof(double) +
-         2 * GF_BM * DNGD_MAX_GRAD * sizeof(double) + 2 * GF_STAGES * sizeof(uint64_t);
+         2 * GF_STAGES * sizeof(uint64_t);
 }

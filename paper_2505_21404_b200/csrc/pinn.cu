@@ -533,6 +533,7 @@ struct Arena {
 struct AsmBufs {
   std::vector<double*> Z, H, Zb, Wt, Wp;
   double* Hb;
+  double* H0;  // materialised input channels (factored Gram), R x 16
 };
 
 static void carve_assemble(const Plan& P, Arena& A, AsmBufs& B) {
@@ -550,6 +551,7 @@ static void carve_assemble(const Plan& P, Arena& A, AsmBufs& B) {
     B.Wt[k] = A.take(P.w[k + 1] * P.ld[k]);
     B.Wp[k] = A.take(P.w[k] * P.ld[k + 1]);
   }
+  B.H0 = A.take(P.R * 16);
 }
 
 struct FvvBufs {
@@ -757,6 +759,130 @@ __global__ void k_chunk_reduce(const double* __restrict__ part, int nchunks, lon
 
 #include "gram_factored.cuh"
 
+// J^T w for every layer in one launch: out[W_k|b_k][p][q] =
+//   sum_rho w(point rho) Hext_k[rho][p] Zbar_k[rho][q]
+// (Hext_k = [H_k, bias (channel 0)], H_0 = the materialised input channels,
+// Zbar_{L-1} = the residual-operator seeds).  Grid (tile, split): each CTA owns
+// a 64 x 64 block of one layer's (w_k + 1) x w_{k+1} output and a contiguous
+// range of activation rows, stages 32 rows at a time in shared memory and
+// accumulates on the FP64 tensor cores (A fragment = Hext^T, read transposed
+// from the row-major stage).  Per-split partials are reduced in fixed order by
+// k_jt_reduce, so the result is bitwise reproducible.
+constexpr int JT_BM = 64, JT_BK = 32, JT_LD = 68;
+
+struct JtLayer {
+  const double* H;  // Hext without the bias column
+  long long ldh;
+  int wh;
+  const double* Z;  // nullptr: output-layer seeds (wz == 1)
+  long long ldz;
+  int wz;
+  long long off;  // theta offset of W_k
+  int tq, tile0;  // tiles along q; first tile of the layer
+};
+
+struct JtParams {
+  Classes T;
+  int L;
+  JtLayer lay[DNGD_MAX_LAYERS];
+  const double* w;
+  long long rows_per_split;
+  long long n;
+  double* part;  // [split][n]
+};
+
+__global__ void __launch_bounds__(128) k_jt_tiles(const __grid_constant__ JtParams p) {
+  __shared__ double Hs[JT_BK][JT_LD], Zs[JT_BK][JT_LD];
+  __shared__ double wv[JT_BK], sd[JT_BK];
+  __shared__ int chs[JT_BK];
+  const int tile = blockIdx.x, split = blockIdx.y;
+  int k = 0;
+  while (k + 1 < p.L && tile >= p.lay[k + 1].tile0) ++k;
+  const JtLayer& Lk = p.lay[k];
+  const int t = tile - Lk.tile0;
+  const int tpi = t / Lk.tq, tqi = t - (t / Lk.tq) * Lk.tq;
+  const int p0 = tpi * JT_BM, q0 = tqi * JT_BM;
+  const long long r0 = split * p.rows_per_split;
+  const long long r1 = min(p.T.R, r0 + p.rows_per_split);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = warp >> 1, wn = warp & 1;
+  double2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
+  const bool seeds = Lk.Z == nullptr;
+  for (long long rb = r0; rb < r1; rb += JT_BK) {
+    if (threadIdx.x < JT_BK) {
+      const long long rho = rb + threadIdx.x;
+      double wr = 0.0, sv = 0.0;
+      int ch = 1;
+      if (rho < r1) {
+        const long long i = act_point(p.T, rho, ch);
+        const ClassDev& C = p.T.c[find_class(p.T, i)];
+        wr = p.w[i];
+        sv = seeds ? C.weight * coef(C, ch) : 0.0;
+      }
+      wv[threadIdx.x] = wr;
+      sd[threadIdx.x] = sv;
+      chs[threadIdx.x] = ch;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < JT_BK * JT_BM; e += 128) {
+      const int r = e / JT_BM, c = e - (e / JT_BM) * JT_BM;
+      const long long rho = rb + r;
+      const bool ok = rho < r1;
+      const int pc = p0 + c, qc = q0 + c;
+      double h = 0.0, z = 0.0;
+      if (ok) {
+        if (pc < Lk.wh) {
+          h = Lk.H[rho * Lk.ldh + pc];
+        } else if (pc == Lk.wh) {
+          h = chs[r] == 0 ? 1.0 : 0.0;
+        }
+        if (qc < Lk.wz) z = wv[r] * (seeds ? sd[r] : Lk.Z[rho * Lk.ldz + qc]);
+      }
+      Hs[r][c] = h;
+      Zs[r][c] = z;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < JT_BK; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = Hs[kk + (lane & 3)][wm * 32 + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Zs[kk + (lane & 3)][wn * 32 + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+  double* dst = p.part + split * p.n + Lk.off;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int pr = p0 + wm * 32 + i * 8 + (lane >> 2);
+    if (pr > Lk.wh) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int qc = q0 + wn * 32 + j * 8 + 2 * (lane & 3);
+      if (qc < Lk.wz) dst[static_cast<long long>(pr) * Lk.wz + qc] = acc[i][j].x;
+      if (qc + 1 < Lk.wz) dst[static_cast<long long>(pr) * Lk.wz + qc + 1] = acc[i][j].y;
+    }
+  }
+}
+
+__global__ void k_jt_reduce(const double* __restrict__ part, int splits, long long n, double scale,
+                            double* __restrict__ out) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double s = 0.0;
+  for (int k = 0; k < splits; ++k) s += part[k * n + e];
+  out[e] = scale * s;
+}
+
 static size_t bytes_of(const Plan& P, int mode, int C) {
   Arena A{nullptr};
   if (mode == 0) {
@@ -869,6 +995,9 @@ static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& 
       if (rc) return rc;
     }
   }
+  if (J == nullptr) {  // activations for the J-free kernels: also Hext_0
+    k_input_channels<<<nblk(P.R * GF_H0_LD), 256, 0, s>>>(P.T, B.H0);
+  }
   return cuda_status(ctx, cudaGetLastError(), "assemble adjoint");
 }
 
@@ -952,15 +1081,18 @@ extern "C" int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_de
                                : set_error(ctx, DNGD_ERR_CUDA, "gram_factored: tensor map encode failed");
   };
   for (int k = 0; k < P.L; ++k) {
-    gp.lay[k].kh = k >= 1 ? static_cast<int>(P.w[k]) : 0;
+    gp.lay[k].kh = static_cast<int>(P.w[k]);
     gp.lay[k].kz = k <= P.L - 2 ? static_cast<int>(P.w[k + 1]) : 0;
     for (int c = 0; c < P.T.n; ++c) {
       const ClassDev& Cc = P.T.c[c];
       if (k >= 1) {
         rc = encode3(&gp.maps[k][0][c], B.H[k] + Cc.act0 * P.ld[k], P.w[k], Cc.nch, Cc.count,
                      P.ld[k], gp.lg[c]);
-        if (rc) return rc;
+      } else {
+        rc = encode3(&gp.maps[0][0][c], B.H0 + Cc.act0 * GF_H0_LD, P.T.din, Cc.nch, Cc.count,
+                     GF_H0_LD, gp.lg[c]);
       }
+      if (rc) return rc;
       if (k <= P.L - 2) {
         rc = encode3(&gp.maps[k][1][c], B.Zb[k] + Cc.act0 * P.ld[k + 1], P.w[k + 1], Cc.nch,
                      Cc.count, P.ld[k + 1], gp.lg[c]);
@@ -992,6 +1124,7 @@ extern "C" int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_de
     if (e != cudaSuccess) return cuda_status(ctx, e, "gram_factored smem attribute");
     attr[ctx->device & 63] = true;
   }
+  static_assert(GF_H0_LD == 16, "carve_assemble reserves R x 16 for H0");
   if (tiles > 0) {
     k_gram_factored<<<static_cast<unsigned>(tiles), GF_THREADS, gram_factored_smem(), s>>>(gp);
   }
@@ -1079,10 +1212,34 @@ struct JtScratch {
   long long ldR, chunk;
   int nchunks, splits;
   size_t bytes, off_zt, off_part, part_bytes;
+  bool tiled;  // one k_jt_tiles launch (narrow nets)
+  int tiles, tsplits;
+  long long rows_per_split;
 };
+
+// narrow nets: every layer in one tiled launch; wide ones: per-layer split-K GEMM
+static constexpr long long kJtTiledMaxWidth = 128;
 
 JtScratch jt_plan(dngd_ctx* ctx, const Plan& P) {
   JtScratch S;
+  S.tiled = P.wmax <= kJtTiledMaxWidth && P.w[0] <= kJtTiledMaxWidth;
+  if (S.tiled) {
+    S.tiles = 0;
+    for (int k = 0; k < P.L; ++k)
+      S.tiles += static_cast<int>(((P.w[k] + 1 + JT_BM - 1) / JT_BM) * ((P.w[k + 1] + JT_BM - 1) / JT_BM));
+    const int target = 2 * 2 * ctx->num_sms;  // two waves of two CTAs per SM
+    long long sp = std::max(1, (target + S.tiles - 1) / S.tiles);
+    sp = std::min(sp, std::max(1LL, P.R / 128));
+    S.rows_per_split = (P.R + sp - 1) / sp;
+    S.rows_per_split = (S.rows_per_split + JT_BK - 1) / JT_BK * JT_BK;
+    S.tsplits = static_cast<int>(std::max(1LL, (P.R + S.rows_per_split - 1) / S.rows_per_split));
+    S.part_bytes = static_cast<size_t>(S.tsplits) * P.n * 8;
+    S.bytes = S.part_bytes;
+    S.ldR = S.chunk = 0;
+    S.nchunks = S.splits = 0;
+    S.off_zt = S.off_part = 0;
+    return S;
+  }
   S.ldR = (P.R + 15) / 16 * 16;
   S.nchunks = static_cast<int>(std::max(1LL, std::min<long long>(256, P.m / 8)));
   S.chunk = (P.m + S.nchunks - 1) / S.nchunks;
@@ -1131,6 +1288,32 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   Arena A{static_cast<char*>(act_work)};
   AsmBufs B;
   carve_assemble(P, A, B);
+  if (S.tiled) {
+    thread_local JtParams jp;
+    jp.T = P.T;
+    jp.L = P.L;
+    int tile0 = 0;
+    for (int k = 0; k < P.L; ++k) {
+      JtLayer& l = jp.lay[k];
+      l.H = k == 0 ? B.H0 : B.H[k];
+      l.ldh = k == 0 ? GF_H0_LD : P.ld[k];
+      l.wh = static_cast<int>(P.w[k]);
+      l.Z = k <= P.L - 2 ? B.Zb[k] : nullptr;
+      l.ldz = k <= P.L - 2 ? P.ld[k + 1] : 0;
+      l.wz = static_cast<int>(P.w[k + 1]);
+      l.off = P.off[k];
+      l.tq = static_cast<int>((P.w[k + 1] + JT_BM - 1) / JT_BM);
+      l.tile0 = tile0;
+      tile0 += static_cast<int>((P.w[k] + 1 + JT_BM - 1) / JT_BM) * l.tq;
+    }
+    jp.w = w;
+    jp.rows_per_split = S.rows_per_split;
+    jp.n = P.n;
+    jp.part = static_cast<double*>(scratch);
+    k_jt_tiles<<<dim3(static_cast<unsigned>(S.tiles), static_cast<unsigned>(S.tsplits)), 128, 0, s>>>(jp);
+    k_jt_reduce<<<nblk(P.n), 256, 0, s>>>(jp.part, S.tsplits, P.n, scale, out);
+    return cuda_status(ctx, cudaGetLastError(), "jt_factored");
+  }
   char* sc = static_cast<char*>(scratch);
   double* Ht = reinterpret_cast<double*>(sc);
   double* Zt = reinterpret_cast<double*>(sc + S.off_zt);

@@ -532,9 +532,7 @@ class PinnResidualMap(ResidualMap):
 
     def _gram_flop_ratio(self) -> float:
         """Estimated FLOPs of the factored Gram / FLOPs of J J^T."""
-        w = self.spec.layer_widths
-        ksum = sum((w[k] if k >= 1 else 0) + (w[k + 1] if k <= len(w) - 3 else 0)
-                   for k in range(len(w) - 1))
+        ksum = self._gram_ksum()
         fact = 0.0
         for c in self.collocation.classes:
             for cp in self.collocation.classes:
@@ -545,10 +543,8 @@ class PinnResidualMap(ResidualMap):
 
     def factored_gram_flops(self) -> float:
         """Algorithmic FLOPs of the factored Gram: lower G-space blocks x two GEMMs
-        per layer (K-dims w_k, w_{k+1}; layer 0 / output layer analytic)."""
-        w = self.spec.layer_widths
-        ksum = sum((w[k] if k >= 1 else 0) + (w[k + 1] if k <= len(w) - 3 else 0)
-                   for k in range(len(w) - 1))
+        per layer (K-dims w_k, w_{k+1}; the output layer's Zbar are seeds)."""
+        ksum = self._gram_ksum()
         rows = [c.count * (1 << max(0, (self._nch(c) - 1).bit_length()))
                 for c in self.collocation.classes]
         pairs = 0.0
@@ -556,6 +552,13 @@ class PinnResidualMap(ResidualMap):
             for j, b in enumerate(rows[: i + 1]):
                 pairs += a * (a + 1) / 2 if i == j else a * b
         return 2.0 * pairs * ksum
+
+    def _gram_ksum(self) -> int:
+        """Sum over layers of the two GEMM K-dims, in the kernel's 16-column chunks."""
+        w = self.spec.layer_widths
+        c16 = lambda x: -(-x // 16) * 16  # noqa: E731
+        return sum(c16(w[k]) + (c16(w[k + 1]) if k <= len(w) - 3 else 0)
+                   for k in range(len(w) - 1))
 
     def _nch(self, cls) -> int:
         op = self.problem.class_operator(cls.class_id)
@@ -570,8 +573,9 @@ class PinnResidualMap(ResidualMap):
             return True
         if self.gram_mode == "materialized":
             return False
-        # the factored kernel runs at ~0.7 of the SYRK's tensor-pipe efficiency
-        return self._gram_flop_ratio() < 0.3
+        # measured crossover: heat1d (ratio ~0.5) 1.7x faster factored, poisson2d
+        # (ratio > 1) slower; the J-free step also skips J's write and read
+        return self._gram_flop_ratio() < 0.6
 
     def jfree(self) -> bool:
         """Dense step without J: factored Gram + J^T w from the activations."""

@@ -66,7 +66,9 @@ int dngd_syrk(dngd_ctx* ctx, void* stream, const double* J, int64_t m, int64_t n
  * info_dev (device int) receives 0 or the 1-based column of the first
  * non-positive / non-finite pivot (LAPACK convention); the host retry ladder
  * (lam *= 10, at most 5 retries) reads it.  dinv receives the inverses of
- * the 64x64 diagonal blocks used by dngd_potrs (size: dngd_potrf_workspace). */
+ * the 64x64 diagonal blocks used by dngd_potrs, followed by the
+ * factorisation's scratch (tile flags); size: dngd_potrf_workspace.
+ * One persistent dataflow launch + one launch for the block inverses. */
 int dngd_potrf_workspace(dngd_ctx* ctx, int64_t m, size_t* dinv_bytes);
 int dngd_shift_copy(dngd_ctx* ctx, void* stream, const double* K, int64_t m, int64_t ldK,
                     double lam, double* L, int64_t ldL);

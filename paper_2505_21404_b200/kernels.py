@@ -87,7 +87,7 @@ class CholeskyFactor:
         self.L = torch.empty((m, ld), dtype=F64, device=device)
         nb = c_size()
         call("dngd_potrf_workspace", ctx(), m, ctypes.byref(nb))
-        self.dinv = torch.empty(max(1, nb.value // 8), dtype=F64, device=device)
+        self.dinv = torch.empty(max(1, (nb.value + 7) // 8), dtype=F64, device=device)
         self.info = torch.zeros(1, dtype=torch.int32, device=device)
         nblk = (m + 63) // 64
         self.flags = torch.zeros(2 * nblk + 2, dtype=torch.int32, device=device)

@@ -64,8 +64,11 @@ extern "C" int dngd_ctx_destroy(dngd_ctx* ctx) {
   if (ctx) {
     if (ctx->ev_panel) cudaEventDestroy(ctx->ev_panel);
     if (ctx->ev_update) cudaEventDestroy(ctx->ev_update);
+    if (ctx->ev_update2) cudaEventDestroy(ctx->ev_update2);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
+    if (ctx->hi) cudaStreamDestroy(ctx->hi);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   }
   delete ctx;
   return DNGD_OK;

@@ -16,7 +16,10 @@ struct dngd_ctx {
   std::string last_error;
   // look-ahead Cholesky: auxiliary stream + fork/join events (created lazily)
   cudaStream_t aux = nullptr;
-  cudaEvent_t ev_panel = nullptr, ev_update = nullptr, ev_fork = nullptr;
+  cudaStream_t hi = nullptr;  // high-priority stream for the potrf panels
+  cudaEvent_t ev_join = nullptr;
+  CUtensorMap potrf_mapS, potrf_mapP;  // panel-load boxes over L (encoded per dngd_potrf call)
+  cudaEvent_t ev_panel = nullptr, ev_update = nullptr, ev_update2 = nullptr, ev_fork = nullptr;
 };
 
 namespace dngd {

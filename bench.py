@@ -215,38 +215,47 @@ def run_ours(args, cfg):
 
     def one_step(rmap, theta):
         nonlocal shared_J
-        jfree = (not sharded and rmap.m < config.dense_threshold and rmap.jfree())
-        if jfree:  # factored Gram + J^T w from activations: J never materialised
-            r, J = rmap.residuals_t(theta), None
+        from paper_2505_21404_b200.optimizer import LineSearchResult, _dispatch_step, _select
+        from paper_2505_21404_b200.solver import fused_dense_step
+
+        dense = rmap.m < config.dense_threshold
+        jfree = not sharded and dense and rmap.jfree()
+        if not sharded and dense:
+            # the product's dense iteration (optimizer._dngd_loop): damping on the
+            # device, one host read-back per step
+            if not jfree:
+                rmap._J = shared_J
+            step, losses, anyd, loss, r = fused_dense_step(
+                rmap, theta, None, None, config.use_ga, config.line_search_points,
+                lam_cap=config.lam_cap)
+            if not jfree:
+                shared_J = rmap._J
+            if step is not None:
+                delta = step.delta.tensor
+                etas = 2.0 ** -np.arange(config.line_search_points, dtype=np.float64)
+                ls = (_select(losses, etas, loss, config.line_search_points) if anyd
+                      else LineSearchResult(1.0, loss, False, 0, False))
+            else:  # factorisation failed: eager path with the retry ladder
+                lam = lm_damping(loss, config.lam_cap)
+                g = None if jfree else K.gemv_t(rmap.jacobian_t(theta), r, rmap.n)
+                step = _dispatch_step(rmap, theta, g, lam, config, rng)
+                delta = step.delta.tensor
+                ls = device_line_search(rmap, theta, delta, loss, config.line_search_points)
         else:
             rmap._J = shared_J
             r, J = rmap.linearize_t(theta)
             shared_J = rmap._J
-        loss = 0.5 * float(K.dot(r, r).item())
-        lam = lm_damping(loss, config.lam_cap)
-        if sharded:
-            ops = CudaShardOps(rmap, theta, ranges)
-            step = sharded_dense_step(ops, comm, lam, config.use_ga)
-            delta = step["delta"]
-            ls = sharded_line_search(ops, comm, theta, delta, loss, config.line_search_points)
-        else:
-            from paper_2505_21404_b200.optimizer import _dispatch_step, _select
-            from paper_2505_21404_b200.solver import fused_dense_step
-
-            fused = None
-            if rmap.m < config.dense_threshold:
-                fused = fused_dense_step(rmap, theta, r, lam, config.use_ga,
+            loss = 0.5 * float(K.dot(r, r).item())
+            lam = lm_damping(loss, config.lam_cap)
+            if sharded:
+                ops = CudaShardOps(rmap, theta, ranges)
+                step = sharded_dense_step(ops, comm, lam, config.use_ga)
+                delta = step["delta"]
+                ls = sharded_line_search(ops, comm, theta, delta, loss,
                                          config.line_search_points)
-            if fused is not None:
-                step = fused[0]
-                delta = step.delta.tensor
-                etas = 2.0 ** -np.arange(config.line_search_points, dtype=np.float64)
-                ls = _select(fused[1], etas, loss, config.line_search_points)
-            else:
-                g = None
-                if not jfree:
-                    with timing.stage("gemv"):
-                        g = K.gemv_t(J, r, rmap.n)
+            else:  # Nystrom-PCG configuration
+                with timing.stage("gemv"):
+                    g = K.gemv_t(J, r, rmap.n)
                 step = _dispatch_step(rmap, theta, g, lam, config, rng)
                 delta = step.delta.tensor
                 ls = device_line_search(rmap, theta, delta, loss, config.line_search_points)

@@ -72,6 +72,10 @@ int dngd_syrk(dngd_ctx* ctx, void* stream, const double* J, int64_t m, int64_t n
 int dngd_potrf_workspace(dngd_ctx* ctx, int64_t m, size_t* dinv_bytes);
 int dngd_shift_copy(dngd_ctx* ctx, void* stream, const double* K, int64_t m, int64_t ldK,
                     double lam, double* L, int64_t ldL);
+/* Same with the damping read on the device: lam = mult * *lam_dev (the loop's
+ * lm_damping(loss) * 10^rejections without a host round trip for the loss). */
+int dngd_shift_copy_dev(dngd_ctx* ctx, void* stream, const double* K, int64_t m, int64_t ldK,
+                        const double* lam_dev, double mult, double* L, int64_t ldL);
 int dngd_potrf(dngd_ctx* ctx, void* stream, double* L, int64_t m, int64_t ldL, double* dinv,
                int* info_dev);
 

@@ -92,9 +92,17 @@ class CholeskyFactor:
         nblk = (m + 63) // 64
         self.flags = torch.zeros(2 * nblk + 2, dtype=torch.int32, device=device)
 
-    def factor(self, K: torch.Tensor, lam: float) -> None:
-        """Async: L = chol(lower(K) + lam I); self.info receives the failing column."""
-        shift_copy(K, lam, self.L)
+    def factor(self, K: torch.Tensor, lam) -> None:
+        """Async: L = chol(lower(K) + lam I); self.info receives the failing column.
+
+        lam is a float, or a (1-element device tensor, multiplier) pair read on
+        the device (no host round trip for the damping)."""
+        if isinstance(lam, tuple):
+            lam_t, mult = lam
+            call("dngd_shift_copy_dev", ctx(), stream_handle(), ptr(K), K.shape[0], K.stride(0),
+                 ptr(lam_t), float(mult), ptr(self.L), self.L.stride(0))
+        else:
+            shift_copy(K, lam, self.L)
         call("dngd_potrf", ctx(), stream_handle(), ptr(self.L), self.m, self.L.stride(0),
              ptr(self.dinv), ptr(self.info))
 

@@ -226,21 +226,27 @@ def _dngd_loop(trace: TrainTrace, rmap_provider, theta: ParameterVector, config:
             rmap = rmap_provider(iteration)
             dense = rmap.m < config.dense_threshold
             jfree = dense and getattr(rmap, "jfree", lambda: False)()
-            if jfree:  # dense step without J: g = J^T r stays implicit
-                r, J, g = rmap.residuals_t(theta), None, None
+            mult = 10.0**rejections
+            if dense:
+                # device-resident damping, step and line search: one host sync
+                # (solver.fused_dense_step); loss comes back with the losses
+                fused = fused_dense_step(rmap, theta, None, None, config.use_ga,
+                                         config.line_search_points, lam_cap=config.lam_cap,
+                                         lam_mult=mult)
+                loss, r = fused[3], fused[4]
+                if fused[0] is None:
+                    fused = None  # factorisation failed: eager path keeps the retry ladder
+                J = None if jfree else rmap.jacobian_t(theta)
             else:
                 r, J = rmap.linearize_t(theta)
-            loss = 0.5 * float(K.dot(r, r).item())
-            if not np.isfinite(loss):
-                from .residuals import _raise_nonfinite
+                loss = 0.5 * float(K.dot(r, r).item())
+                if not np.isfinite(loss):
+                    from .residuals import _raise_nonfinite
 
-                _raise_nonfinite(r, rmap.partition())
-            lam = lm_damping(loss, config.lam_cap) * 10.0**rejections
-            if dense:
-                # device-resident step + line search, two host syncs (solver.fused_dense_step)
-                fused = fused_dense_step(rmap, theta, r, lam, config.use_ga,
-                                         config.line_search_points)
+                    _raise_nonfinite(r, rmap.partition())
+            lam = lm_damping(loss, config.lam_cap) * mult
             if fused is None:
+                g = None
                 if not jfree:
                     with stage("gemv"):
                         g = K.gemv_t(J, r, rmap.n)

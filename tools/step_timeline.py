@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_2505_21404_b200 as P  # noqa: E402
 from paper_2505_21404_b200 import kernels as K  # noqa: E402
-from paper_2505_21404_b200.optimizer import _select, lm_damping  # noqa: E402
+from paper_2505_21404_b200.optimizer import _select  # noqa: E402
 from paper_2505_21404_b200.solver import fused_dense_step  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -38,12 +38,9 @@ etas = 2.0 ** -np.arange(31, dtype=np.float64)
 
 
 def step(rmap, theta):
-    r = rmap.residuals_t(theta)
-    loss = 0.5 * float(K.dot(r, r).item())
-    lam = lm_damping(loss, cfg["lam_cap"])
-    fused = fused_dense_step(rmap, theta, r, lam, True, 31)
-    st = fused[0]
-    ls = _select(fused[1], etas, loss, 31)
+    st, losses, _, loss, _ = fused_dense_step(rmap, theta, None, None, True, 31,
+                                              lam_cap=cfg["lam_cap"])
+    ls = _select(losses, etas, loss, 31)
     if ls.rejected:
         return theta
     return P.ParameterVector(K.axpby(ls.eta, st.delta.tensor, 1.0, theta.tensor), theta.layout)
@@ -82,3 +79,14 @@ for (s0, e0, n0), (s1, e1, n1) in zip(ker, ker[1:]):
 print(f"idle total {sum(gaps.values()) / a.steps:.1f} us/step; largest gap sources:")
 for k2, g in gaps.most_common(20):
     print(f"  {g / a.steps:8.1f} us/step  x{gapn[k2] / a.steps:5.1f}  {k2}")
+
+# host side: runtime API calls around the largest gaps
+cpu = sorted(((e.time_range.start, e.time_range.end, e.name) for e in prof.events()
+              if e.device_type.name == "CPU"), key=lambda x: x[0])
+big = sorted(((s1 - e0, e0, s1, n0, n1) for (s0, e0, n0), (s1, e1, n1) in zip(ker, ker[1:])
+              if s1 - e0 > 40), reverse=True)[:4]
+for g, e0, s1, n0, n1 in big:
+    print(f"gap {g:.1f} us after {n0[:50]} before {n1[:50]}; host events starting in the window:")
+    for s, e, n in cpu:
+        if e0 - 150 <= s <= s1:
+            print(f"    {s - e0:8.1f} {e - s:8.1f}  {n[:80]}")

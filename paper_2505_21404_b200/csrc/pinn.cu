@@ -759,6 +759,196 @@ __global__ void k_chunk_reduce(const double* __restrict__ part, int nchunks, lon
 
 #include "gram_factored.cuh"
 
+// ------------------------------------------------------------------ fused line search
+// Line-search losses for narrow nets (every width <= 64) in one launch: a CTA
+// takes one candidate theta + eta delta and one tile of 64 activation rows of
+// one class (64/a points, channels padded to a = 1, 2, 4 or 8 per point), runs
+// the whole forward-Laplacian MLP in shared memory -- input channels, per layer
+// an FP64 tensor-core GEMM (16-byte fragment loads, pitch 72) and the tanh
+// channel map, the head -- and writes the tile's sum of squared residuals.  The
+// candidate weights are formed on the fly (fma(eta, delta, theta), bitwise the
+// values k_candidates materialises).  No activation ever reaches HBM: the
+// launch-per-layer path streamed ~2 GB per line search at config 2.
+constexpr int LF_LD = 72;
+constexpr int LF_THREADS = 256;  // 8 warps: latency of the per-layer phases is hidden by 16 warps/SM
+constexpr size_t kLossFusedSmem = 3 * 64 * LF_LD * sizeof(double) + (64 + 72) * sizeof(double);
+
+struct LossFusedParams {
+  Classes T;
+  int L;
+  int w[DNGD_MAX_LAYERS + 1];
+  long long off[DNGD_MAX_LAYERS];
+  const double* thetas;  // candidate stack [cand][n] (k_candidates)
+  long long n;
+  int lg[MAXC];
+  int tile0[MAXC + 1];
+  int ntiles;
+  double* part;  // [cand][tile]
+};
+
+__global__ void __launch_bounds__(LF_THREADS, 2) k_loss_fused(const __grid_constant__ LossFusedParams p) {
+  extern __shared__ __align__(16) double lf_smem[];
+  double(*H)[LF_LD] = reinterpret_cast<double(*)[LF_LD]>(lf_smem);
+  double(*Z)[LF_LD] = reinterpret_cast<double(*)[LF_LD]>(lf_smem + 64 * LF_LD);
+  double(*Wt)[LF_LD] = reinterpret_cast<double(*)[LF_LD]>(lf_smem + 2 * 64 * LF_LD);
+  double* bias = lf_smem + 3 * 64 * LF_LD;
+  double* wl = bias + 64;
+  __shared__ int s_gd[MAXG], s_lap[MAXG];
+  __shared__ double s_coef[8], s_red[LF_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tile = blockIdx.x, cand = blockIdx.y;
+  int c = 0;
+  while (c + 1 < p.T.n && tile >= p.tile0[c + 1]) ++c;
+  const ClassDev& C = p.T.c[c];
+  const int lg = p.lg[c], a = 1 << lg, PT = 64 >> lg;
+  const long long P0 = static_cast<long long>(tile - p.tile0[c]) * PT;
+  const int nch = C.nch, ngrad = C.ngrad, nlap = C.nlap, din = p.T.din;
+  const long long count = C.count;
+  const double* pts = C.pts;
+  if (tid < MAXG) {
+    s_gd[tid] = C.grad_dims[tid];
+    s_lap[tid] = C.lap_ch[tid];
+  }
+  if (tid < 8) s_coef[tid] = tid < nch ? coef(C, tid) : 0.0;
+  const double* th = p.thetas + static_cast<long long>(cand) * p.n;
+  // weights -> shared memory with every load of a thread in flight at once
+  // (<= 64 x 64 per layer = 16 per thread); dst(kk, q) picks the layout
+  auto stage_weights = [&](long long off, int rows, int cols, int rpad, auto dst) {
+    double v[4096 / LF_THREADS];
+#pragma unroll
+    for (int j = 0; j < 4096 / LF_THREADS; ++j) {
+      const int e = tid + j * LF_THREADS;
+      const int kk = e / cols;
+      v[j] = (e < rpad * cols && kk < rows) ? __ldg(th + off + e) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4096 / LF_THREADS; ++j) {
+      const int e = tid + j * LF_THREADS;
+      if (e < rpad * cols) dst(e / cols, e - (e / cols) * cols) = v[j];
+    }
+  };
+  for (int e = tid; e < 2 * 64 * LF_LD; e += LF_THREADS) lf_smem[e] = 0.0;  // H, Z pads stay 0
+  // ---- layer 0: input channels -> tanh channels (thread per (point, unit))
+  {
+    const int w1 = p.w[1];
+    const long long o0 = p.off[0];
+    // W0 rows 0..din-1 and b0 (row din) into Wt as [row][unit]
+    stage_weights(o0, din + 1, w1, din + 1, [&](int kk, int q) -> double& { return Wt[kk][q]; });
+    __syncthreads();
+    for (int e = tid; e < PT * w1; e += LF_THREADS) {
+      const int pl = e / w1, q = e - (e / w1) * w1;
+      const long long pi = P0 + pl;
+      if (pi >= count) continue;
+      double z = Wt[din][q];
+      for (int d = 0; d < din; ++d) z = fma(pts[pi * din + d], Wt[d][q], z);
+      const double t = tanh(z), s = 1.0 - t * t;
+      double* hrow = &H[pl * a][q];
+      hrow[0] = t;
+      for (int g = 0; g < ngrad; ++g) hrow[(1 + g) * LF_LD] = s * Wt[s_gd[g]][q];
+      if (nlap) {
+        double G = 0.0;
+        for (int l = 0; l < nlap; ++l) {
+          const double dz = Wt[s_gd[s_lap[l] - 1]][q];
+          G = fma(dz, dz, G);
+        }
+        hrow[(nch - 1) * LF_LD] = -2.0 * t * s * G;
+      }
+    }
+  }
+  const int lrow = lane >> 2, kq = lane & 3, wm = warp >> 2, wn = warp & 3;  // warp tile 32 x 16
+  // ---- hidden layers: Z = H W_k (tensor cores), H = tanh channels(Z + b_k)
+  for (int k = 1; k <= p.L - 2; ++k) {
+    const int wk = p.w[k], wk1 = p.w[k + 1];
+    const int kpad = (wk + 7) & ~7;
+    const long long ok = p.off[k];
+    __syncthreads();  // H complete, Wt free
+    stage_weights(ok, wk, wk1, kpad, [&](int kk, int q) -> double& { return Wt[q][kk]; });
+    if (tid < wk1) bias[tid] = __ldg(th + ok + static_cast<long long>(wk) * wk1 + tid);
+    __syncthreads();
+    double2 acc[4][2];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) acc[x][y] = make_double2(0.0, 0.0);
+    for (int k8 = 0; k8 < kpad; k8 += 8) {
+      double2 av[4], bv[2];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+        av[x] = *reinterpret_cast<const double2*>(&H[wm * 32 + x * 8 + lrow][k8 + 2 * kq]);
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+        bv[y] = *reinterpret_cast<const double2*>(&Wt[wn * 16 + y * 8 + lrow][k8 + 2 * kq]);
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) dmma_8x8x4(acc[x][y], av[x].x, bv[y].x);
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) dmma_8x8x4(acc[x][y], av[x].y, bv[y].y);
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+        *reinterpret_cast<double2*>(&Z[wm * 32 + x * 8 + lrow][wn * 16 + y * 8 + 2 * kq]) = acc[x][y];
+    __syncthreads();
+    for (int e = tid; e < PT * wk1; e += LF_THREADS) {
+      const int pl = e / wk1, q = e - (e / wk1) * wk1;
+      const double* zrow = &Z[pl * a][q];
+      double* hrow = &H[pl * a][q];
+      const double z = zrow[0] + bias[q];
+      const double t = tanh(z), s = 1.0 - t * t;
+      hrow[0] = t;
+      for (int g = 0; g < ngrad; ++g) hrow[(1 + g) * LF_LD] = s * zrow[(1 + g) * LF_LD];
+      if (nlap) {
+        double G = 0.0;
+        for (int l = 0; l < nlap; ++l) {
+          const double dz = zrow[s_lap[l] * LF_LD];
+          G = fma(dz, dz, G);
+        }
+        hrow[(nch - 1) * LF_LD] = s * zrow[(nch - 1) * LF_LD] - 2.0 * t * s * G;
+      }
+    }
+  }
+  // ---- head (width 1): residual per point, squared, summed over the tile
+  const int wL = p.w[p.L - 1];
+  const long long oL = p.off[p.L - 1];
+  __syncthreads();
+  if (tid <= wL) wl[tid] = __ldg(th + oL + tid);  // W_{L-1} (w x 1) and b_{L-1}
+  __syncthreads();
+  double r2 = 0.0;
+  if (tid < PT && P0 + tid < count) {
+    double res = 0.0;
+    for (int ch = 0; ch < nch; ++ch) {
+      const double* hrow = &H[tid * a + ch][0];
+      double u = 0.0;
+      for (int q = 0; q < wL; ++q) u = fma(hrow[q], wl[q], u);
+      if (ch == 0) u += wl[wL];
+      res = fma(s_coef[ch], u, res);
+    }
+    const double r = C.weight * (res - C.f[P0 + tid]);
+    r2 = r * r;
+  }
+  r2 = warp_sum(r2);
+  if (lane == 0) s_red[warp] = r2;
+  __syncthreads();
+  if (tid == 0) {
+    double sacc = 0.0;
+    for (int w = 0; w < LF_THREADS / 32; ++w) sacc += s_red[w];
+    p.part[static_cast<long long>(cand) * p.ntiles + tile] = sacc;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_loss_reduce(const double* __restrict__ part, int ntiles,
+                                                       double* __restrict__ losses) {
+  __shared__ double sh[8];
+  double s = 0.0;
+  for (int t = threadIdx.x; t < ntiles; t += 256) s += part[static_cast<long long>(blockIdx.x) * ntiles + t];
+  s = block_sum<256>(s, sh);
+  if (threadIdx.x == 0) losses[blockIdx.x] = 0.5 * s;
+}
+
 // J^T w for every layer in one launch: out[W_k|b_k][p][q] =
 //   sum_rho w(point rho) Hext_k[rho][p] Zbar_k[rho][q]
 // (Hext_k = [H_k, bias (channel 0)], H_0 = the materialised input channels,
@@ -1181,6 +1371,16 @@ extern "C" int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
   return cuda_status(ctx, cudaGetLastError(), "fvv");
 }
 
+// the fused line search handles nets whose every layer width is <= 64 and whose
+// classes have <= 8 channels per point (one 64-row tile holds whole points)
+static bool loss_fused_ok(const Plan& P) {
+  for (int k = 1; k < P.L; ++k)
+    if (P.w[k] > 64) return false;
+  for (int c = 0; c < P.T.n; ++c)
+    if (P.T.c[c].nch > 8) return false;
+  return P.T.din <= MAXG;
+}
+
 extern "C" int dngd_loss_many(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                               const double* theta, const double* delta, const double* etas,
                               int ncand, const dngd_class_desc* classes, int nclass,
@@ -1192,6 +1392,41 @@ extern "C" int dngd_loss_many(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* 
   if (ncand < 1) return DNGD_OK;
   if (ncand > 65535) return set_error(ctx, DNGD_ERR_DIMENSION, "loss_many: too many candidates");
   if (bytes_of(P, 2, ncand) > work_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "loss_many: workspace too small");
+  if (loss_fused_ok(P)) {
+    thread_local LossFusedParams lp;
+    lp.T = P.T;
+    lp.L = P.L;
+    for (int k = 0; k <= P.L; ++k) lp.w[k] = static_cast<int>(P.w[k]);
+    for (int k = 0; k < P.L; ++k) lp.off[k] = P.off[k];
+    lp.n = P.n;
+    int tiles = 0;
+    for (int c = 0; c < P.T.n; ++c) {
+      int lg = 0;
+      while ((1 << lg) < P.T.c[c].nch) ++lg;
+      lp.lg[c] = lg;
+      lp.tile0[c] = tiles;
+      tiles += static_cast<int>((P.T.c[c].count + (64 >> lg) - 1) / (64 >> lg));
+    }
+    lp.tile0[P.T.n] = tiles;
+    lp.ntiles = tiles;
+    lp.part = static_cast<double*>(work);
+    double* thetas = lp.part + ((static_cast<size_t>(ncand) * tiles + 31) / 32) * 32;
+    lp.thetas = thetas;
+    k_candidates<<<dim3(nblk(P.n), ncand), 256, 0, s>>>(theta, delta, etas, P.n, thetas);
+    static bool attr[64] = {false};
+    if (!attr[ctx->device & 63]) {
+      cudaError_t e = cudaFuncSetAttribute(k_loss_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(kLossFusedSmem));
+      if (e != cudaSuccess) return cuda_status(ctx, e, "loss_fused smem attribute");
+      attr[ctx->device & 63] = true;
+    }
+    if (tiles > 0) {
+      k_loss_fused<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(ncand)), LF_THREADS,
+                     kLossFusedSmem, s>>>(lp);
+    }
+    k_loss_reduce<<<ncand, 256, 0, s>>>(lp.part, tiles, losses);
+    return cuda_status(ctx, cudaGetLastError(), "loss_many fused");
+  }
   Arena A{static_cast<char*>(work)};
   LossBufs B;
   carve_loss(P, A, B, ncand);

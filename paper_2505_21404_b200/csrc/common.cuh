@@ -17,6 +17,13 @@ DNGD_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Align a dynamic shared-memory base by pointer arithmetic on the __shared__
+// array itself, so the compiler keeps the shared address space (LDS/STS).  An
+// integer round trip (uintptr_t) makes every access a generic LD/ST.
+DNGD_DEV uint8_t* smem_align(uint8_t* raw, uint32_t align) {
+  return raw + ((align - (smem_u32(raw) & (align - 1))) & (align - 1));
+}
+
 // ---------------------------------------------------------------- mbarrier
 DNGD_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)

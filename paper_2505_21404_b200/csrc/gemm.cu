@@ -59,8 +59,7 @@ __global__ void __launch_bounds__(WM * WN * 32, (WM * WN <= 4 ? 3 : 1))
   constexpr int NCW = Cfg::kConsumerWarps;
   constexpr int WTM = BM / WM, WTN = BN / WN, MI = WTM / 8, NJ = WTN / 8;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align(smem_raw, 1024);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::kStageBytes);
   uint64_t* empty = full + STAGES;
 

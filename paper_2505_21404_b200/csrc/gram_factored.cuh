@@ -129,8 +129,7 @@ DNGD_DEV void gf_epilogue(double2 (&accH)[4][4], double2 (&accZ)[4][4], bool see
 __global__ void __launch_bounds__(GF_THREADS, 2)
     k_gram_factored(const __grid_constant__ GramParams p) {
   extern __shared__ uint8_t gf_smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(gf_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align(gf_smem_raw, 1024);
   double* Ks = reinterpret_cast<double*>(smem + GF_STAGES * GF_STAGE_BYTES);  // 64 x 64 points max
   uint64_t* full = reinterpret_cast<uint64_t*>(Ks + GF_BM * GF_BM);
   uint64_t* empty = full + GF_STAGES;

@@ -80,9 +80,11 @@ int dngd_potrf(dngd_ctx* ctx, void* stream, double* L, int64_t m, int64_t ldL, d
                int* info_dev);
 
 /* ---- triangular solves (replaces solver.py:199,209 cho_solve) -------------
- * b <- (L L^T)^{-1} b in place.  flags: device int scratch of 2*ceil(m/64) ints. */
+ * b <- (L L^T)^{-1} b in place.  scratch: dngd_potrs_workspace(m) bytes of
+ * device memory (the hand-off copies of the block solutions). */
+int dngd_potrs_workspace(dngd_ctx* ctx, int64_t m, size_t* bytes);
 int dngd_potrs(dngd_ctx* ctx, void* stream, const double* L, int64_t m, int64_t ldL,
-               const double* dinv, double* b, int* flags);
+               const double* dinv, double* b, double* scratch);
 
 /* ---- streaming matvecs over J (replaces residuals.py:220-227 vjp and
  *      residuals.py:282-292 jvp on the materialised J) ------------------------

@@ -67,6 +67,7 @@ _SIGS = {
     "dngd_shift_copy": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_dbl, c_vp, c_i64], c_int),
     "dngd_shift_copy_dev": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_dbl, c_vp, c_i64], c_int),
     "dngd_potrf": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp], c_int),
+    "dngd_potrs_workspace": ([c_vp, c_i64, ctypes.POINTER(c_size)], c_int),
     "dngd_potrs": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp], c_int),
     "dngd_gemv_t_workspace": ([c_vp, c_i64, c_i64, ctypes.POINTER(c_size)], c_int),
     "dngd_gemv_t": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_dbl, c_vp, c_vp, c_size], c_int),

@@ -89,8 +89,9 @@ class CholeskyFactor:
         call("dngd_potrf_workspace", ctx(), m, ctypes.byref(nb))
         self.dinv = torch.empty(max(1, (nb.value + 7) // 8), dtype=F64, device=device)
         self.info = torch.zeros(1, dtype=torch.int32, device=device)
-        nblk = (m + 63) // 64
-        self.flags = torch.zeros(2 * nblk + 2, dtype=torch.int32, device=device)
+        nb = c_size()
+        call("dngd_potrs_workspace", ctx(), m, ctypes.byref(nb))
+        self.scratch = torch.empty(max(1, (nb.value + 7) // 8), dtype=F64, device=device)
 
     def factor(self, K: torch.Tensor, lam) -> None:
         """Async: L = chol(lower(K) + lam I); self.info receives the failing column.
@@ -109,7 +110,7 @@ class CholeskyFactor:
     def solve_(self, b: torch.Tensor) -> torch.Tensor:
         """b <- (L L^T)^{-1} b in place."""
         call("dngd_potrs", ctx(), stream_handle(), ptr(self.L), self.m, self.L.stride(0),
-             ptr(self.dinv), ptr(b), ptr(self.flags))
+             ptr(self.dinv), ptr(b), ptr(self.scratch))
         return b
 
 

@@ -155,6 +155,25 @@ def _count_our_kernels(fn):
     return n
 
 
+def _profiled_traffic(workload, kernel):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu capture
+    (profiles/<round>/traffic.json), or None when this kernel/workload has none."""
+    import glob
+
+    best = None
+    for path in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                              "profiles", "r*", "traffic.json"))):
+        try:
+            with open(path) as f:
+                table = json.load(f)
+        except (OSError, ValueError):
+            continue
+        for name, ent in table.get(workload, {}).items():
+            if name.split("<")[0] in kernel:
+                best = ent.get("bytes")
+    return best
+
+
 def run_ours(args, cfg):
     import torch
 
@@ -364,6 +383,8 @@ def run_ours(args, cfg):
                 "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
                 "algorithmic": f"factored Gram {flops:.3e} FLOP per launch",
                 "jjt_equivalent_tflops": m * (m + 1) * n / gram_avg / 1e12}
+    if roof is not None:
+        roof["traffic"] = _profiled_traffic(cfg["name"], roof["kernel"])
     gram_chol = None
     g_avg = syrk_avg if syrk_avg > 0 else gram_avg
     if g_avg > 0 and potrf_avg > 0:

@@ -769,7 +769,9 @@ __global__ void k_chunk_reduce(const double* __restrict__ part, int nchunks, lon
 // candidate weights are formed on the fly (fma(eta, delta, theta), bitwise the
 // values k_candidates materialises).  No activation ever reaches HBM: the
 // launch-per-layer path streamed ~2 GB per line search at config 2.
-constexpr int LF_LD = 72;
+constexpr int LF_LD = 72;  // activation tiles: 16-byte A-fragment loads, conflict-free
+constexpr int LF_WLD = 66;  // weights W[k][q]: the 8-byte B-fragment loads (k = 2(l%4)+h, q = l/4)
+                            // and the row-wise staging stores are conflict-free per half warp
 constexpr int LF_THREADS = 256;  // 8 warps: latency of the per-layer phases is hidden by 16 warps/SM
 constexpr size_t kLossFusedSmem = 3 * 64 * LF_LD * sizeof(double) + (64 + 72) * sizeof(double);
 
@@ -790,7 +792,7 @@ __global__ void __launch_bounds__(LF_THREADS, 2) k_loss_fused(const __grid_const
   extern __shared__ __align__(16) double lf_smem[];
   double(*H)[LF_LD] = reinterpret_cast<double(*)[LF_LD]>(lf_smem);
   double(*Z)[LF_LD] = reinterpret_cast<double(*)[LF_LD]>(lf_smem + 64 * LF_LD);
-  double(*Wt)[LF_LD] = reinterpret_cast<double(*)[LF_LD]>(lf_smem + 2 * 64 * LF_LD);
+  double(*Wk)[LF_WLD] = reinterpret_cast<double(*)[LF_WLD]>(lf_smem + 2 * 64 * LF_LD);
   double* bias = lf_smem + 3 * 64 * LF_LD;
   double* wl = bias + 64;
   __shared__ int s_gd[MAXG], s_lap[MAXG];
@@ -832,23 +834,23 @@ __global__ void __launch_bounds__(LF_THREADS, 2) k_loss_fused(const __grid_const
   {
     const int w1 = p.w[1];
     const long long o0 = p.off[0];
-    // W0 rows 0..din-1 and b0 (row din) into Wt as [row][unit]
-    stage_weights(o0, din + 1, w1, din + 1, [&](int kk, int q) -> double& { return Wt[kk][q]; });
+    // W0 rows 0..din-1 and b0 (row din) as [row][unit]
+    stage_weights(o0, din + 1, w1, din + 1, [&](int kk, int q) -> double& { return Wk[kk][q]; });
     __syncthreads();
     for (int e = tid; e < PT * w1; e += LF_THREADS) {
       const int pl = e / w1, q = e - (e / w1) * w1;
       const long long pi = P0 + pl;
       if (pi >= count) continue;
-      double z = Wt[din][q];
-      for (int d = 0; d < din; ++d) z = fma(pts[pi * din + d], Wt[d][q], z);
+      double z = Wk[din][q];
+      for (int d = 0; d < din; ++d) z = fma(pts[pi * din + d], Wk[d][q], z);
       const double t = tanh(z), s = 1.0 - t * t;
       double* hrow = &H[pl * a][q];
       hrow[0] = t;
-      for (int g = 0; g < ngrad; ++g) hrow[(1 + g) * LF_LD] = s * Wt[s_gd[g]][q];
+      for (int g = 0; g < ngrad; ++g) hrow[(1 + g) * LF_LD] = s * Wk[s_gd[g]][q];
       if (nlap) {
         double G = 0.0;
         for (int l = 0; l < nlap; ++l) {
-          const double dz = Wt[s_gd[s_lap[l] - 1]][q];
+          const double dz = Wk[s_gd[s_lap[l] - 1]][q];
           G = fma(dz, dz, G);
         }
         hrow[(nch - 1) * LF_LD] = -2.0 * t * s * G;
@@ -861,8 +863,8 @@ __global__ void __launch_bounds__(LF_THREADS, 2) k_loss_fused(const __grid_const
     const int wk = p.w[k], wk1 = p.w[k + 1];
     const int kpad = (wk + 7) & ~7;
     const long long ok = p.off[k];
-    __syncthreads();  // H complete, Wt free
-    stage_weights(ok, wk, wk1, kpad, [&](int kk, int q) -> double& { return Wt[q][kk]; });
+    __syncthreads();  // H complete, Wk free
+    stage_weights(ok, wk, wk1, kpad, [&](int kk, int q) -> double& { return Wk[kk][q]; });
     if (tid < wk1) bias[tid] = __ldg(th + ok + static_cast<long long>(wk) * wk1 + tid);
     __syncthreads();
     double2 acc[4][2];
@@ -876,8 +878,10 @@ __global__ void __launch_bounds__(LF_THREADS, 2) k_loss_fused(const __grid_const
       for (int x = 0; x < 4; ++x)
         av[x] = *reinterpret_cast<const double2*>(&H[wm * 32 + x * 8 + lrow][k8 + 2 * kq]);
 #pragma unroll
-      for (int y = 0; y < 2; ++y)
-        bv[y] = *reinterpret_cast<const double2*>(&Wt[wn * 16 + y * 8 + lrow][k8 + 2 * kq]);
+      for (int y = 0; y < 2; ++y) {
+        bv[y].x = Wk[k8 + 2 * kq][wn * 16 + y * 8 + lrow];
+        bv[y].y = Wk[k8 + 2 * kq + 1][wn * 16 + y * 8 + lrow];
+      }
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -917,13 +921,22 @@ __global__ void __launch_bounds__(LF_THREADS, 2) k_loss_fused(const __grid_const
   __syncthreads();
   if (tid <= wL) wl[tid] = __ldg(th + oL + tid);  // W_{L-1} (w x 1) and b_{L-1}
   __syncthreads();
+  // one warp per (point, channel) dot product: lanes walk q (conflict-free);
+  // the Z tile is free by now and holds the 64 channel outputs
+  double* s_u = &Z[0][0];
+  for (int pc = warp; pc < PT * a; pc += LF_THREADS / 32) {
+    const double* hrow = &H[pc][0];
+    double u = 0.0;
+    for (int q = lane; q < wL; q += 32) u = fma(hrow[q], wl[q], u);
+    u = warp_sum(u);
+    if (lane == 0) s_u[pc] = u;
+  }
+  __syncthreads();
   double r2 = 0.0;
   if (tid < PT && P0 + tid < count) {
     double res = 0.0;
     for (int ch = 0; ch < nch; ++ch) {
-      const double* hrow = &H[tid * a + ch][0];
-      double u = 0.0;
-      for (int q = 0; q < wL; ++q) u = fma(hrow[q], wl[q], u);
+      double u = s_u[tid * a + ch];
       if (ch == 0) u += wl[wL];
       res = fma(s_coef[ch], u, res);
     }

@@ -274,5 +274,20 @@ def main():
                 1e-3, 16, 1e-10, 200)
 
 
+def main_allen_cahn():
+    """Allen-Cahn (problems.py:286-328): periodic embedding + cubic reaction, the
+    reference's own problem class, unmodified."""
+    from dngd.problems import AllenCahn
+
+    step_fixture("ac_step", AllenCahn(), (3, 32, 32, 32, 1), {INTERIOR: 40, INITIAL: 16}, 6,
+                 [1e-3, 1e-6])
+    trajectory_fixture("ac_traj", AllenCahn(), (3, 16, 16, 1), {INTERIOR: 60, INITIAL: 20},
+                       7, 1e-3, 4)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["allen_cahn"]:
+        main_allen_cahn()
+    else:
+        main()
+        main_allen_cahn()

@@ -24,6 +24,7 @@ PROBLEMS = {
     "cfg1_step": (O.OraclePoisson2d(), ("interior", "boundary")),
     "cfg2_step": (O.OracleHeat1d(), ("interior", "boundary", "initial")),
     "cfg3_step": (O.OraclePoissonSin(5), ("interior", "boundary")),
+    "ac_step": (O.OracleAllenCahn(), ("interior", "initial")),
 }
 
 
@@ -93,6 +94,7 @@ def test_oracle_dense_step_and_line_search(golden_dir, name):
 TRAJ = {
     "cfg1_traj": (O.OraclePoisson2d(), (90, 30), O.LoopConfig(lam_cap=1e-3, max_iters=5)),
     "cfg2_traj": (O.OracleHeat1d(), (60, 20, 20), O.LoopConfig(lam_cap=1e-3, max_iters=4)),
+    "ac_traj": (O.OracleAllenCahn(), (60, 20), O.LoopConfig(lam_cap=1e-3, max_iters=4)),
     "pcg_traj": (O.OraclePoisson2d(), (60, 20),
                  O.LoopConfig(lam_cap=1e-3, max_iters=3, dense_threshold=10, nystrom_rank=16,
                               cg_max_iters=100)),

@@ -123,9 +123,13 @@ typedef struct {
   int widths[DNGD_MAX_LAYERS + 1];     /* widths[0] = input dim, widths[L] = 1 */
 } dngd_mlp_desc;
 
-/* r_i = weight * (cu*u + sum_g cg[g] d_{grad_dims[g]} u + cl * sum_{j in lap} d_jj u - f_i)
+/* r_i = weight * (cu*u + c3*u^3 + sum_g cg[g] d_{grad_dims[g]} u
+ *                + cl * sum_{j in lap} d_jj u - f_i)
  * grad channels are numbered 1..ngrad; lap_grad[] lists the grad-channel
- * indices (0-based into grad_dims) summed into the Laplacian channel. */
+ * indices (0-based into grad_dims) summed into the Laplacian channel.
+ * inputs (optional): the network-input channels of an input embedding
+ * (model.py:148-175), N x nch x widths[0] row-major -- value phi(x), d phi per
+ * grad dim, sum of d_jj phi over the Laplacian dims -- replacing points. */
 typedef struct {
   int64_t count;                      /* points N */
   int ngrad;
@@ -134,8 +138,10 @@ typedef struct {
   int lap_grad[DNGD_MAX_GRAD];
   double cg[DNGD_MAX_GRAD];
   double cu, cl, weight;
-  const double* points;               /* device, N x widths[0] row-major */
+  const double* points;               /* device, N x widths[0] row-major (identity embedding) */
   const double* f;                    /* device, N data values */
+  double c3;                          /* cubic coefficient (Allen-Cahn reaction), 0 if linear */
+  const double* inputs;               /* device, N x nch x widths[0], or NULL */
 } dngd_class_desc;
 
 /* scratch for one assembly / f_vv / loss_many(ncand) evaluation */

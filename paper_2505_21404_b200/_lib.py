@@ -53,6 +53,8 @@ class ClassDesc(ctypes.Structure):
         ("weight", c_dbl),
         ("points", c_vp),
         ("f", c_vp),
+        ("c3", c_dbl),
+        ("inputs", c_vp),
     ]
 
 

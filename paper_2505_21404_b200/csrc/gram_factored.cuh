@@ -66,7 +66,9 @@ __global__ void k_input_channels(Classes T, double* __restrict__ H0) {
   const ClassDev& C = T.c[find_class(T, p)];
   double v = 0.0;
   if (d < T.din) {
-    if (ch == 0) {
+    if (C.inp) {
+      v = C.inp[((p - C.row0) * C.nch + ch) * T.din + d];
+    } else if (ch == 0) {
       v = C.pts[(p - C.row0) * T.din + d];
     } else if (ch <= C.ngrad) {
       v = C.grad_dims[ch - 1] == d ? 1.0 : 0.0;
@@ -77,28 +79,26 @@ __global__ void k_input_channels(Classes T, double* __restrict__ H0) {
 
 DNGD_DEV int gf_layer_chunks(const GramLayer& l) { return ((l.kh + 15) >> 4) + ((l.kz + 15) >> 4); }
 
-DNGD_DEV double seed_of(const ClassDev& C, int ch) {
-  return ch < C.nch ? C.weight * coef(C, ch) : 0.0;
-}
-
 // K[point pairs] += S (G_H o G_Z) S^T for one warp's 32 x 32 G-block.  Fragment
 // (i, j): rows lrow = lane/4 (+8i), columns 2(lane%4)+{0,1} (+8j); G-row bits
 // below LGA are the channel, so the row channel is lrow mod a for every i.
 template <int LGA, int LGB>
 DNGD_DEV void gf_epilogue(double2 (&accH)[4][4], double2 (&accZ)[4][4], bool seedZ, double bias0,
-                          double bias1, double sp0, double sp1, double* Ks, int wm, int wn,
-                          int lane) {
+                          double bias1, const double* sA, const double* sB, double* Ks, int wm,
+                          int wn, int lane) {
   const int lrow = lane >> 2;
   const bool own_r = (lrow & ((1 << LGA) - 1)) == 0;
   const bool own_c = LGB <= 1 || (lane & ((1 << (LGB > 1 ? LGB - 1 : 0)) - 1)) == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int pr = (wm * 32 + i * 8 + lrow) >> LGA;
+    const int gr = wm * 32 + i * 8 + lrow;
+    const int pr = gr >> LGA;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int gc = wn * 32 + j * 8 + 2 * (lane & 3);
-      double v0 = (accH[i][j].x + bias0) * (seedZ ? sp0 : accZ[i][j].x);
-      double v1 = (accH[i][j].y + bias1) * (seedZ ? sp1 : accZ[i][j].y);
+      // output layer: Zbar = per-row seeds (G^Z = seed_row * seed_col)
+      double v0 = (accH[i][j].x + bias0) * (seedZ ? sA[gr] * sB[gc] : accZ[i][j].x);
+      double v1 = (accH[i][j].y + bias1) * (seedZ ? sA[gr] * sB[gc + 1] : accZ[i][j].y);
       accH[i][j] = make_double2(0.0, 0.0);
       accZ[i][j] = make_double2(0.0, 0.0);
       // column bits = (h, lane bit 0, lane bit 1), row bits = lane bits 2, 3, 4
@@ -161,6 +161,17 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
   }
   for (int e = threadIdx.x; e < GF_BM * GF_BM / 2; e += GF_THREADS)
     reinterpret_cast<double2*>(Ks)[e] = make_double2(0.0, 0.0);
+  // output-layer seeds per G-row (0 on padded channels and past the class end)
+  __shared__ double sA[GF_BM], sB[GF_BM];
+  if (threadIdx.x < GF_BM) {
+    const int g = threadIdx.x;
+    const ClassDev& Ca = p.T.c[c];
+    const ClassDev& Cb = p.T.c[cp];
+    const int cha = g & ((1 << lga) - 1), pa = P0 + (g >> lga);
+    const int chb = g & ((1 << lgb) - 1), pb = Q0 + (g >> lgb);
+    sA[g] = (cha < Ca.nch && pa < Ca.count) ? seedc(p.T, Ca, cha, Ca.row0 + pa) : 0.0;
+    sB[g] = (chb < Cb.nch && pb < Cb.count) ? seedc(p.T, Cb, chb, Cb.row0 + pb) : 0.0;
+  }
   __syncthreads();
 
   auto issue = [&](int f) {
@@ -186,8 +197,6 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
   const int chc0 = (2 * (lane & 3)) & ((1 << lgb) - 1), chc1 = (2 * (lane & 3) + 1) & ((1 << lgb) - 1);
   const double bias0 = (chr == 0 && chc0 == 0) ? 1.0 : 0.0;
   const double bias1 = (chr == 0 && chc1 == 0) ? 1.0 : 0.0;
-  const double sr = seed_of(p.T.c[c], chr);
-  const double sp0 = sr * seed_of(p.T.c[cp], chc0), sp1 = sr * seed_of(p.T.c[cp], chc1);
   const int epi = lga * 4 + lgb;
 
   double2 accH[4][4], accZ[4][4];
@@ -250,7 +259,7 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     switch (epi) {
 #define GF_EPI(A, B)                                                                            \
   case A * 4 + B:                                                                               \
-    gf_epilogue<A, B>(accH, accZ, seedZ, bias0, bias1, sp0, sp1, Ks, wm, wn, lane);             \
+    gf_epilogue<A, B>(accH, accZ, seedZ, bias0, bias1, sA, sB, Ks, wm, wn, lane);               \
     break;
       GF_EPI(0, 0) GF_EPI(0, 1) GF_EPI(0, 2) GF_EPI(0, 3)
       GF_EPI(1, 0) GF_EPI(1, 1) GF_EPI(1, 2) GF_EPI(1, 3)

@@ -37,14 +37,17 @@ struct ClassDev {
   int lap_ch[MAXG];  // channel index (1-based grad channel) summed into the Laplacian
   double cg[MAXG];
   double cu, cl, weight;
+  double c3;           // coefficient of u^3 (Allen-Cahn reaction; 0 = linear operator)
   const double* pts;
   const double* f;
+  const double* inp;   // embedded input channels (N x nch x din) or nullptr = identity
 };
 
 struct Classes {
   int n, din;
   long long m, R;
   ClassDev c[MAXC];
+  double* u0;  // per-point network value (written by k_head; cubic-term adjoint seeds)
 };
 
 DNGD_DEV int find_class(const Classes& T, long long p) {
@@ -59,6 +62,17 @@ DNGD_DEV double coef(const ClassDev& C, int ch) {
   if (ch == 0) return C.cu;
   if (ch <= C.ngrad) return C.cg[ch - 1];
   return C.cl;
+}
+
+// adjoint seed of output channel ch at point p: d r_p / d u_ch (the value channel
+// picks up 3 c3 u^2 from the cubic term)
+DNGD_DEV double seedc(const Classes& T, const ClassDev& C, int ch, long long p) {
+  double cf = coef(C, ch);
+  if (ch == 0 && C.c3 != 0.0) {
+    const double u = T.u0[p];
+    cf = fma(3.0 * C.c3 * u, u, cf);
+  }
+  return C.weight * cf;
 }
 
 static inline long long ldw(long long w) { return (w + 3) / 4 * 4; }
@@ -79,10 +93,39 @@ __global__ void k_input_fwd(Classes T, const double* __restrict__ theta, long lo
   const double* th = theta + blockIdx.y * th_s;
   const double* W0 = th;
   const double* b0 = th + static_cast<long long>(T.din) * w1;
+  const long long base = (C.act0 + i * C.nch) * ld + q + blockIdx.y * act_s;
+  if (C.inp) {
+    // embedded inputs: every channel is inputs_ch . W0 (value channel + b0)
+    const double* xr = C.inp + i * C.nch * T.din;
+    auto zch = [&](int ch) {
+      double z = ch == 0 ? b0[q] : 0.0;
+      for (int j = 0; j < T.din; ++j) z = fma(xr[ch * T.din + j], W0[j * w1 + q], z);
+      return z;
+    };
+    const double z = zch(0);
+    const double t = tanh(z), s = 1.0 - t * t;
+    if (Z) Z[base] = z;
+    H[base] = t;
+    for (int g = 0; g < C.ngrad; ++g) {
+      const double dz = zch(1 + g);
+      if (Z) Z[base + (1 + g) * ld] = dz;
+      H[base + (1 + g) * ld] = s * dz;
+    }
+    if (C.nlap) {
+      double G = 0.0;
+      for (int l = 0; l < C.nlap; ++l) {
+        const double dz = zch(C.lap_ch[l]);
+        G = fma(dz, dz, G);
+      }
+      const double zl = zch(C.nch - 1);
+      if (Z) Z[base + (C.nch - 1) * ld] = zl;
+      H[base + (C.nch - 1) * ld] = s * zl - 2.0 * t * s * G;
+    }
+    return;
+  }
   const double* x = C.pts + i * T.din;
   double z = b0[q];
   for (int j = 0; j < T.din; ++j) z = fma(x[j], W0[j * w1 + q], z);
-  const long long base = (C.act0 + i * C.nch) * ld + q + blockIdx.y * act_s;
   const double t = tanh(z), s = 1.0 - t * t;
   if (Z) Z[base] = z;
   H[base] = t;
@@ -142,15 +185,22 @@ __global__ void k_head(Classes T, const double* __restrict__ H, int w, long long
   const double* WL = th + wl_off;
   const double bL = WL[w];
   const double* h = H + (C.act0 + i * C.nch) * ld + blockIdx.y * act_s;
-  double res = 0.0;
+  double res = 0.0, u0 = 0.0;
   for (int c = 0; c < C.nch; ++c) {
     double u = 0.0;
     for (int q = lane; q < w; q += 32) u = fma(h[c * ld + q], WL[q], u);
     u = warp_sum(u);
-    if (c == 0) u += bL;
+    if (c == 0) {
+      u += bL;
+      u0 = u;
+    }
     res = fma(coef(C, c), u, res);
   }
-  if (lane == 0) r[p + blockIdx.y * r_s] = C.weight * (res - C.f[i]);
+  if (C.c3 != 0.0) res = fma(C.c3 * u0 * u0, u0, res);
+  if (lane == 0) {
+    r[p + blockIdx.y * r_s] = C.weight * (res - C.f[i]);
+    if (T.u0 != nullptr && blockIdx.y == 0) T.u0[p] = u0;
+  }
 }
 
 // ------------------------------------------------------------------ adjoint
@@ -165,7 +215,7 @@ __global__ void k_seed_hbar(Classes T, double* __restrict__ Hb, int w, long long
   const ClassDev& C = T.c[find_class(T, p)];
   const long long i = p - C.row0;
   const long long base = (C.act0 + i * C.nch) * ld + q;
-  for (int c = 0; c < C.nch; ++c) Hb[base + c * ld] = C.weight * coef(C, c) * WL[q];
+  for (int c = 0; c < C.nch; ++c) Hb[base + c * ld] = seedc(T, C, c, p) * WL[q];
 }
 
 // Zbar = adjoint of (z channels -> tanh channels) applied to Hbar.
@@ -211,11 +261,11 @@ DNGD_DEV double hext(const ClassDev& C, int din, const double* __restrict__ xrow
                      const double* __restrict__ hrow, long long ld, int win, int c, int p) {
   if (p == win) return c == 0 ? 1.0 : 0.0;  // bias row
   if (hrow != nullptr) return hrow[c * ld + p];
-  // input layer: x channels
+  // input layer: embedded input channels, or x / e_j / 0 (identity)
+  if (C.inp) return xrow[c * din + p];
   if (c == 0) return xrow[p];
   if (c <= C.ngrad) return C.grad_dims[c - 1] == p ? 1.0 : 0.0;
   return 0.0;
-  (void)din;
 }
 
 // Block of layer k in row i: (win+1) x wout row-major at flat column layer_off.
@@ -232,7 +282,7 @@ __global__ void __launch_bounds__(256) k_jwrite(Classes T, const double* __restr
   const long long i = p - C.row0;
   const long long arow = C.act0 + i * C.nch;
   const double* hrow = Hk ? Hk + arow * ldh : nullptr;
-  const double* xrow = C.pts + i * T.din;
+  const double* xrow = C.inp ? C.inp + i * C.nch * T.din : C.pts + i * T.din;
   const double* zrow = Zb ? Zb + arow * ldz : nullptr;
   double* Jrow = J + p * ldJ - col_begin;
   const long long E = static_cast<long long>(win + 1) * wout;
@@ -268,7 +318,7 @@ __global__ void __launch_bounds__(256) k_jwrite(Classes T, const double* __restr
       double a = 0.0;
       for (int c = 0; c < nch; ++c) {
         const double h = hext(C, T.din, xrow, hrow, ldh, win, c, pp);
-        const double z = zrow ? zrow[c * ldz + q] : C.weight * coef(C, c);
+        const double z = zrow ? zrow[c * ldz + q] : seedc(T, C, c, p);
         a = fma(h, z, a);
       }
       Jrow[col] = a;
@@ -319,15 +369,35 @@ __global__ void k_fvv_input(Classes T, const double* __restrict__ theta,
   const int q = static_cast<int>(idx - p * w1);
   const ClassDev& C = T.c[find_class(T, p)];
   const long long i = p - C.row0;
-  const double* x = C.pts + i * T.din;
   const long long boff = static_cast<long long>(T.din) * w1;
+  const long long base = (C.act0 + i * C.nch) * ld + q;
+  const long long blk = T.R * ld;
+  auto hput = [&](int ch, T2 h) {
+    const long long o = base + ch * ld;
+    H3[o] = h.a;
+    H3[o + blk] = h.b;
+    H3[o + 2 * blk] = h.c;
+  };
+  if (C.inp) {
+    // embedded inputs: channel ch is inputs_ch . (W0 + t V0) (+ bias on the value channel)
+    const double* xr = C.inp + i * C.nch * T.din;
+    auto zget_e = [&](int ch) -> T2 {
+      double a = ch == 0 ? theta[boff + q] : 0.0, b = ch == 0 ? v[boff + q] : 0.0;
+      for (int j = 0; j < T.din; ++j) {
+        a = fma(xr[ch * T.din + j], theta[j * w1 + q], a);
+        b = fma(xr[ch * T.din + j], v[j * w1 + q], b);
+      }
+      return {a, b, 0.0};
+    };
+    tanh_tjet(C, zget_e, hput);
+    return;
+  }
+  const double* x = C.pts + i * T.din;
   double za = theta[boff + q], zb = v[boff + q];
   for (int j = 0; j < T.din; ++j) {
     za = fma(x[j], theta[j * w1 + q], za);
     zb = fma(x[j], v[j * w1 + q], zb);
   }
-  const long long base = (C.act0 + i * C.nch) * ld + q;
-  const long long blk = T.R * ld;
   auto zget = [&](int ch) -> T2 {
     if (ch == 0) return {za, zb, 0.0};
     if (ch <= C.ngrad) {
@@ -335,12 +405,6 @@ __global__ void k_fvv_input(Classes T, const double* __restrict__ theta,
       return {theta[d * w1 + q], v[d * w1 + q], 0.0};
     }
     return {0.0, 0.0, 0.0};
-  };
-  auto hput = [&](int ch, T2 h) {
-    const long long o = base + ch * ld;
-    H3[o] = h.a;
-    H3[o + blk] = h.b;
-    H3[o + 2 * blk] = h.c;
   };
   tanh_tjet(C, zget, hput);
 }
@@ -393,6 +457,19 @@ __global__ void k_fvv_head(Classes T, const double* __restrict__ H3, int w, long
       u = fma(h[2 * blk + c * ld + q], WL[q], fma(2.0 * h[blk + c * ld + q], VL[q], u));
     u = warp_sum(u);
     res = fma(coef(C, c), u, res);
+  }
+  if (C.c3 != 0.0) {
+    // (u^3)'' = 6 u u'^2 + 3 u^2 u'' on the value channel
+    double ua = 0.0, ub = 0.0, uc = 0.0;
+    for (int q = lane; q < w; q += 32) {
+      ua = fma(h[q], WL[q], ua);
+      ub = fma(h[blk + q], WL[q], fma(h[q], VL[q], ub));
+      uc = fma(h[2 * blk + q], WL[q], fma(2.0 * h[blk + q], VL[q], uc));
+    }
+    ua = warp_sum(ua) + WL[w];
+    ub = warp_sum(ub) + VL[w];
+    uc = warp_sum(uc);
+    res = fma(C.c3, 6.0 * ua * ub * ub + 3.0 * ua * ua * uc, res);
   }
   if (lane == 0) out[p] = C.weight * res;
 }
@@ -507,13 +584,19 @@ static int make_plan(dngd_ctx* ctx, const dngd_mlp_desc* mlp, const dngd_class_d
     C.cu = d.cu;
     C.cl = d.cl;
     C.weight = d.weight;
+    C.c3 = d.c3;
     C.pts = d.points;
     C.f = d.f;
+    C.inp = d.inputs;
+    if (C.inp == nullptr && C.pts == nullptr && d.count > 0) {
+      return set_error(ctx, DNGD_ERR_DIMENSION, "pinn: class needs points or input channels");
+    }
     row += d.count;
     act += d.count * C.nch;
   }
   T.m = row;
   T.R = act;
+  T.u0 = nullptr;
   P.m = row;
   P.R = act;
   return DNGD_OK;
@@ -534,6 +617,7 @@ struct AsmBufs {
   std::vector<double*> Z, H, Zb, Wt, Wp;
   double* Hb;
   double* H0;  // materialised input channels (factored Gram), R x 16
+  double* u0;  // per-point network value (cubic-term adjoint seeds), m
 };
 
 static void carve_assemble(const Plan& P, Arena& A, AsmBufs& B) {
@@ -552,6 +636,7 @@ static void carve_assemble(const Plan& P, Arena& A, AsmBufs& B) {
     B.Wp[k] = A.take(P.w[k] * P.ld[k + 1]);
   }
   B.H0 = A.take(P.R * 16);
+  B.u0 = A.take(P.m);
 }
 
 struct FvvBufs {
@@ -709,11 +794,21 @@ __global__ void k_jt_input(Classes T, const double* __restrict__ Zb, long long l
     const long long base = C.act0 + (i - C.row0) * C.nch;
     const double wi = wvec[i];
     const double zv = wi * Zb[base * ld + q];
+    acc[MAXG] += zv;
+    if (C.inp) {  // embedded input channels: Hext_0[c] = inputs_c
+      const double* xr = C.inp + (i - C.row0) * C.nch * din;
+      for (int c = 0; c < C.nch; ++c) {
+        const double zc = c == 0 ? zv : wi * Zb[(base + c) * ld + q];
+#pragma unroll
+        for (int p = 0; p < MAXG; ++p)
+          if (p < din) acc[p] = fma(xr[c * din + p], zc, acc[p]);
+      }
+      continue;
+    }
     const double* x = C.pts + (i - C.row0) * din;
 #pragma unroll
     for (int p = 0; p < MAXG; ++p)
       if (p < din) acc[p] = fma(x[p], zv, acc[p]);
-    acc[MAXG] += zv;
     for (int g = 0; g < C.ngrad; ++g) {
       const double zg = wi * Zb[(base + 1 + g) * ld + q];
 #pragma unroll
@@ -741,7 +836,7 @@ __global__ void k_jt_output(Classes T, const double* __restrict__ H, long long l
     double s = 0.0;
     for (int ch = 0; ch < C.nch; ++ch) {
       const double h = p < w ? H[(base + ch) * ld + p] : (ch == 0 ? 1.0 : 0.0);
-      s = fma(C.weight * coef(C, ch), h, s);
+      s = fma(seedc(T, C, ch, i), h, s);
     }
     acc = fma(wvec[i], s, acc);
   }
@@ -807,6 +902,8 @@ __global__ void __launch_bounds__(LF_THREADS, 2) k_loss_fused(const __grid_const
   const int nch = C.nch, ngrad = C.ngrad, nlap = C.nlap, din = p.T.din;
   const long long count = C.count;
   const double* pts = C.pts;
+  const double* inp = C.inp;
+  const double c3 = C.c3;
   if (tid < MAXG) {
     s_gd[tid] = C.grad_dims[tid];
     s_lap[tid] = C.lap_ch[tid];
@@ -841,10 +938,31 @@ __global__ void __launch_bounds__(LF_THREADS, 2) k_loss_fused(const __grid_const
       const int pl = e / w1, q = e - (e / w1) * w1;
       const long long pi = P0 + pl;
       if (pi >= count) continue;
+      double* hrow = &H[pl * a][q];
+      if (inp) {  // embedded input channels (same arithmetic as k_input_fwd)
+        const double* xr = inp + pi * nch * din;
+        auto zch = [&](int ch) {
+          double z = ch == 0 ? Wk[din][q] : 0.0;
+          for (int d = 0; d < din; ++d) z = fma(xr[ch * din + d], Wk[d][q], z);
+          return z;
+        };
+        const double z = zch(0);
+        const double t = tanh(z), s = 1.0 - t * t;
+        hrow[0] = t;
+        for (int g = 0; g < ngrad; ++g) hrow[(1 + g) * LF_LD] = s * zch(1 + g);
+        if (nlap) {
+          double G = 0.0;
+          for (int l = 0; l < nlap; ++l) {
+            const double dz = zch(s_lap[l]);
+            G = fma(dz, dz, G);
+          }
+          hrow[(nch - 1) * LF_LD] = s * zch(nch - 1) - 2.0 * t * s * G;
+        }
+        continue;
+      }
       double z = Wk[din][q];
       for (int d = 0; d < din; ++d) z = fma(pts[pi * din + d], Wk[d][q], z);
       const double t = tanh(z), s = 1.0 - t * t;
-      double* hrow = &H[pl * a][q];
       hrow[0] = t;
       for (int g = 0; g < ngrad; ++g) hrow[(1 + g) * LF_LD] = s * Wk[s_gd[g]][q];
       if (nlap) {
@@ -934,12 +1052,16 @@ __global__ void __launch_bounds__(LF_THREADS, 2) k_loss_fused(const __grid_const
   __syncthreads();
   double r2 = 0.0;
   if (tid < PT && P0 + tid < count) {
-    double res = 0.0;
+    double res = 0.0, u0 = 0.0;
     for (int ch = 0; ch < nch; ++ch) {
       double u = s_u[tid * a + ch];
-      if (ch == 0) u += wl[wL];
+      if (ch == 0) {
+        u += wl[wL];
+        u0 = u;
+      }
       res = fma(s_coef[ch], u, res);
     }
+    if (c3 != 0.0) res = fma(c3 * u0 * u0, u0, res);
     const double r = C.weight * (res - C.f[P0 + tid]);
     r2 = r * r;
   }
@@ -1024,7 +1146,7 @@ __global__ void __launch_bounds__(128) k_jt_tiles(const __grid_constant__ JtPara
         const long long i = act_point(p.T, rho, ch);
         const ClassDev& C = p.T.c[find_class(p.T, i)];
         wr = p.w[i];
-        sv = seeds ? C.weight * coef(C, ch) : 0.0;
+        sv = seeds ? seedc(p.T, C, ch, i) : 0.0;
       }
       wv[threadIdx.x] = wr;
       sd[threadIdx.x] = sv;
@@ -1217,6 +1339,7 @@ extern "C" int dngd_assemble(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* m
   Arena A{static_cast<char*>(work)};
   AsmBufs B;
   carve_assemble(P, A, B);
+  P.T.u0 = B.u0;
   return assemble_impl(ctx, s, P, B, theta, col_begin, col_end, r, J, ldJ, false);
 }
 
@@ -1232,6 +1355,7 @@ extern "C" int dngd_activations(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   Arena A{static_cast<char*>(work)};
   AsmBufs B;
   carve_assemble(P, A, B);
+  P.T.u0 = B.u0;
   return assemble_impl(ctx, s, P, B, theta, 0, P.n, r, nullptr, 0, true);
 }
 
@@ -1249,6 +1373,7 @@ extern "C" int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_de
   Arena A{static_cast<char*>(work)};
   AsmBufs B;
   carve_assemble(P, A, B);
+  P.T.u0 = B.u0;
   rc = assemble_impl(ctx, s, P, B, theta, 0, P.n, r, nullptr, 0, true);
   if (rc) return rc;
   thread_local GramParams gp;  // ~8.5 KB of tensor maps: off the host stack, reentrant
@@ -1536,6 +1661,7 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   Arena A{static_cast<char*>(act_work)};
   AsmBufs B;
   carve_assemble(P, A, B);
+  P.T.u0 = B.u0;
   if (S.tiled) {
     thread_local JtParams jp;
     jp.T = P.T;

@@ -4,16 +4,18 @@ Same plugin surface as the reference PdeProblem (problems.py:107-146):
 `sample(counts, rng)`, `resolve_counts`, `exact_solution`, `eval_points`,
 `default_counts`, `default_widths`, `default_lam_cap`, `name`.  Instead of a
 `class_residual(net, cls)` written against the AD algebra, each problem
-states every residual class as a linear differential operator
+states every residual class as a differential operator
 
-    r = w * (cu*u + sum_g cg[g] d_{grad_dims[g]} u + cl * sum_{j in lap_dims} d_jj u - f(x))
+    r = w * (cu*u + c3*u^3 + sum_g cg[g] d_{grad_dims[g]} u + cl * sum_{j in lap_dims} d_jj u - f(x))
 
 (`class_operator`) plus its data term f (`class_data`, evaluated on the host
-with the reference's numpy expressions); the device kernels (pinn.cu)
-evaluate u and its derivative channels.  This covers the reference's
-Poisson2d, Poisson10d and Heat(d) and the BASELINE configs' heat1d (G2) and
-sine-Poisson (G3).  Nonlinear operators (Allen-Cahn), periodic embeddings
-and STDE subsampling are not expressible here and raise DomainError.
+with the reference's numpy expressions), and optionally an input embedding
+(`input_channels`: the network-input channels phi(x), d_j phi, sum d_jj phi of
+model.py:133-175); the device kernels (pinn.cu) evaluate u and its derivative
+channels.  This covers all of the reference's deterministic problems --
+Poisson2d, Poisson10d, Heat(d), Allen-Cahn (periodic embedding + cubic
+reaction) -- and the BASELINE configs' heat1d (G2) and sine-Poisson (G3).
+STDE subsampling (PoissonBallStde) is out of scope and raises DomainError.
 """
 
 from __future__ import annotations
@@ -33,6 +35,7 @@ class ClassOperator:
     cg: tuple = ()
     lap_dims: tuple = ()
     cl: float = 0.0
+    c3: float = 0.0  # coefficient of u^3 (Allen-Cahn reaction)
 
 
 VALUE = ClassOperator(cu=1.0)  # r = u - g
@@ -96,6 +99,16 @@ class PdeProblem:
     default_widths: tuple
     default_lam_cap: float = 1e-5
     has_exact: bool = True
+
+    @property
+    def input_dim(self) -> int:
+        """Network input width: raw_dim, or the embedding's output width."""
+        return self.raw_dim
+
+    def input_channels(self, cls: CollocationClass, op: ClassOperator):
+        """(N, nch, input_dim) embedded input channels, or None for the identity
+        embedding (model.py:133-146)."""
+        return None
 
     def sample(self, counts, rng) -> CollocationSet:
         raise NotImplementedError
@@ -322,6 +335,72 @@ class Heat1d(PdeProblem):
         return _halton(num, [0, 0], [1, 1])
 
 
+def periodic_channels(points: np.ndarray, omega: float, op: ClassOperator) -> np.ndarray:
+    """PeriodicEmbedding1d (model.py:148-175): (t, x) -> [t, sin wx, cos wx] and its
+    directional derivatives, as network-input channels in the device's channel
+    order: value, d_j per grad dim, sum_{j in lap} d_jj."""
+    t, x = points[:, 0], points[:, 1]
+    s, c = np.sin(omega * x), np.cos(omega * x)
+    zero = np.zeros_like(t)
+    chans = [np.stack([t, s, c], axis=1)]
+    for j in op.grad_dims:
+        if j == 0:
+            chans.append(np.stack([np.ones_like(t), zero, zero], axis=1))
+        else:
+            chans.append(np.stack([zero, omega * c, -omega * s], axis=1))
+    if op.lap_dims:
+        lap = np.zeros((points.shape[0], 3))
+        for j in op.lap_dims:
+            if j == 1:
+                lap += np.stack([zero, -omega * omega * s, -omega * omega * c], axis=1)
+        chans.append(lap)
+    return np.ascontiguousarray(np.stack(chans, axis=1))
+
+
+class AllenCahn(PdeProblem):
+    """u_t - 1e-4 u_xx + 5u^3 - 5u = 0 on (0,1) x (-1,1), periodic in x (period 2)
+    through the sin/cos input embedding; u(0, x) = x^2 cos(pi x) (problems.py:286-328).
+    Classes interior / initial; no closed-form solution."""
+
+    name = "allen_cahn"
+    raw_dim = 2
+    default_counts = {INTERIOR: 1125, INITIAL: 225}
+    default_widths = (3, 32, 32, 32, 1)
+    has_exact = False
+    diffusivity = 1e-4
+    omega = np.pi  # 2 pi / period
+
+    @property
+    def input_dim(self) -> int:
+        return 3
+
+    def sample(self, counts, rng):
+        c = self.resolve_counts(counts)
+        interior = np.column_stack(
+            [rng.uniform(size=c[INTERIOR]), rng.uniform(-1.0, 1.0, size=c[INTERIOR])])
+        initial = np.column_stack(
+            [np.zeros(c[INITIAL]), rng.uniform(-1.0, 1.0, size=c[INITIAL])])
+        return CollocationSet([_cls(INTERIOR, interior), _cls(INITIAL, initial)])
+
+    def class_operator(self, class_id):
+        if class_id == INTERIOR:
+            return ClassOperator(cu=-5.0, grad_dims=(0, 1), cg=(1.0, 0.0), lap_dims=(1,),
+                                 cl=-self.diffusivity, c3=5.0)
+        return VALUE
+
+    def class_data(self, cls):
+        if cls.class_id == INTERIOR:
+            return np.zeros(cls.count)
+        x = cls.points[:, 1]
+        return x**2 * np.cos(np.pi * x)
+
+    def input_channels(self, cls, op):
+        return periodic_channels(cls.points, self.omega, op)
+
+    def eval_points(self, num=10_000):
+        return _halton(num, [0.0, -1.0], [1.0, 1.0])
+
+
 PROBLEMS = {
     "poisson2d": Poisson2d,
     "poisson10d": Poisson10d,
@@ -329,16 +408,17 @@ PROBLEMS = {
     "heat10d": lambda: Heat(10),
     "heat1d": Heat1d,
     "poisson5d_sin": lambda: PoissonSin(5),
+    "allen_cahn": AllenCahn,
 }
 
-UNSUPPORTED = {"allen_cahn", "poisson_ball_stde"}
+UNSUPPORTED = {"poisson_ball_stde"}
 
 
 def make_problem(name: str, **kwargs) -> PdeProblem:
     if name in UNSUPPORTED:
         raise DomainError(
-            f"problem {name!r} needs a nonlinear operator / embedding that the device "
-            "residual map does not implement in this build"
+            f"problem {name!r} needs STDE subsampling, which the device residual map does "
+            "not implement in this build"
         )
     if name not in PROBLEMS:
         raise DomainError(f"unknown problem {name!r}; available: {sorted(PROBLEMS)}")

@@ -387,9 +387,10 @@ class PinnResidualMap(ResidualMap):
 
         if not isinstance(spec, MlpSpec):
             raise DimensionError("PinnResidualMap needs an MlpSpec")
-        if spec.input_dim != problem.raw_dim:
+        in_dim = getattr(problem, "input_dim", problem.raw_dim)
+        if spec.input_dim != in_dim:
             raise DimensionError(
-                f"spec input width {spec.input_dim} != problem dimension {problem.raw_dim}"
+                f"spec input width {spec.input_dim} != problem input width {in_dim}"
             )
         if spec.output_dim != 1:
             raise DimensionError("PINN residual maps need a scalar network output")
@@ -447,8 +448,19 @@ class PinnResidualMap(ResidualMap):
             for l, ldim in enumerate(op.lap_dims):
                 d.lap_grad[l] = op.grad_dims.index(ldim)
             d.cu, d.cl, d.weight = float(op.cu), float(op.cl), float(cls.weight)
+            d.c3 = float(getattr(op, "c3", 0.0))
             d.points = pts.data_ptr()
             d.f = f.data_ptr()
+            emb = (self.problem.input_channels(cls, op)
+                   if hasattr(self.problem, "input_channels") else None)
+            if emb is not None:
+                emb = np.ascontiguousarray(emb, dtype=np.float64)
+                if emb.shape != (cls.count, 1 + d.ngrad + (1 if d.nlap else 0),
+                                 self.spec.input_dim):
+                    raise DimensionError(f"input channels of class {cls.class_id}: {emb.shape}")
+                inp = torch.as_tensor(emb, device=dev)
+                keep.append(inp)
+                d.inputs = inp.data_ptr()
         mlp = K.mlp_desc(self.spec.layer_widths)
         ws_bytes = K.pinn_workspace_bytes(mlp, arr, len(classes), 1)
         # line-search activations grow linearly with the candidate count

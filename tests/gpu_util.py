@@ -32,4 +32,9 @@ def class_descs(classes):
         d.cu, d.cl, d.weight = c.cu, c.cl, c.weight
         d.points = pts.data_ptr()
         d.f = f.data_ptr()
+        d.c3 = getattr(c, "c3", 0.0)
+        if getattr(c, "inputs", None) is not None:
+            inp = dev(c.inputs)
+            keep.append(inp)
+            d.inputs = inp.data_ptr()
     return arr, keep

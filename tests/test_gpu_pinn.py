@@ -13,6 +13,9 @@ CASES = [
     ("heat1d", O.OracleHeat1d(), (2, 64, 64, 64, 64, 1), (60, 20, 20)),
     ("poisson5d", O.OraclePoissonSin(5), (5, 32, 32, 32, 32, 1), (40, 12)),
     ("poisson5d_wide", O.OraclePoissonSin(5), (5, 128, 96, 1), (20, 10)),
+    # reference Allen-Cahn: periodic input embedding + cubic reaction term
+    ("allen_cahn", O.OracleAllenCahn(), (3, 32, 32, 32, 1), (60, 20)),
+    ("allen_cahn_wide", O.OracleAllenCahn(), (3, 160, 96, 1), (30, 10)),
 ]
 
 
@@ -106,4 +109,22 @@ def test_gram_factored_matches_jjt(K, name, problem, widths, counts):
     assert np.all(np.isfinite(Kg))
     assert np.array_equal(Kg, Kg.T)
     assert _rel(Kg, K_ref) <= 1e-12
+    assert _rel(r.cpu().numpy(), r_ref) <= 1e-12
+
+
+@pytest.mark.parametrize("name,problem,widths,counts", CASES)
+def test_jt_factored_matches_oracle(K, name, problem, widths, counts):
+    """J^T w from the activations (no J) == oracle J^T w (tiled and wide paths)."""
+    from tests.gpu_util import dev
+    classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 7)
+    r_ref, J_ref = O.linearize(theta, widths, classes)
+    m, n = J_ref.shape
+    w = np.random.default_rng(11).normal(size=m)
+    r = torch.empty(m, dtype=torch.float64, device="cuda")
+    K.activations(mlp, th, arr, len(classes), r, ws)
+    scratch = torch.empty(K.jt_workspace_bytes(mlp, arr, len(classes)), dtype=torch.uint8,
+                          device="cuda")
+    out = torch.full((n,), np.nan, dtype=torch.float64, device="cuda")
+    K.jt_factored(mlp, arr, len(classes), dev(w), -0.5, out, ws, scratch)
+    assert _rel(out.cpu().numpy(), -0.5 * (J_ref.T @ w)) <= 1e-12
     assert _rel(r.cpu().numpy(), r_ref) <= 1e-12

@@ -35,6 +35,7 @@ STEP = {
     "cfg1_step": ("poisson2d", ("interior", "boundary"), O.OraclePoisson2d()),
     "cfg2_step": ("heat1d", ("interior", "boundary", "initial"), O.OracleHeat1d()),
     "cfg3_step": ("poisson5d_sin", ("interior", "boundary"), O.OraclePoissonSin(5)),
+    "ac_step": ("allen_cahn", ("interior", "initial"), O.OracleAllenCahn()),
 }
 
 
@@ -117,6 +118,7 @@ def test_gram_modes_match_reference(P, golden_dir, name, mode):
 TRAJ = {
     "cfg1_traj": ("poisson2d", (90, 30), dict(lam_cap=1e-3)),
     "cfg2_traj": ("heat1d", (60, 20, 20), dict(lam_cap=1e-3)),
+    "ac_traj": ("allen_cahn", (60, 20), dict(lam_cap=1e-3)),
     "pcg_traj": ("poisson2d", (60, 20),
                  dict(lam_cap=1e-3, dense_threshold=10, nystrom_rank=16, cg_max_iters=100)),
 }
@@ -299,7 +301,7 @@ def test_pcg_zero_gradient_and_breakdown(P):
     assert np.all(np.isfinite(res.delta.data))
 
 
-@pytest.mark.parametrize("name", ["cfg2_step", "cfg3_step"])
+@pytest.mark.parametrize("name", ["cfg2_step", "cfg3_step", "ac_step"])
 def test_jfree_step_matches_materialized(P, golden_dir, name):
     """J-free dense step (factored Gram + J^T w from the activations) == J-based step,
     and J^T w from the activations == J^T w over the materialised J."""

@@ -37,7 +37,7 @@ def test_ctypes_struct_layout_matches_header():
     from paper_2505_21404_b200 import _lib
 
     # int64 count, 2 ints, 12 ints, 12 ints, 12 doubles, 3 doubles, 2 pointers
-    assert ctypes.sizeof(_lib.ClassDesc) == 8 + 8 + 48 + 48 + 96 + 24 + 16
+    assert ctypes.sizeof(_lib.ClassDesc) == 8 + 8 + 48 + 48 + 96 + 24 + 16 + 16
     assert ctypes.sizeof(_lib.MlpDesc) == 4 * 10
 
 
@@ -155,6 +155,24 @@ def test_param_layout_and_counts():
 def test_unsupported_problems_fail_loudly():
     from paper_2505_21404_b200 import DomainError, make_problem
 
-    for name in ("allen_cahn", "poisson_ball_stde"):
+    for name in ("poisson_ball_stde",):
         with pytest.raises(DomainError):
             make_problem(name)
+
+
+def test_allen_cahn_plugin_matches_oracle():
+    """Host side of the Allen-Cahn plugin (problems.py:286-328): sampling order,
+    operator coefficients, data term and the periodic-embedding input channels."""
+    from paper_2505_21404_b200 import make_problem
+
+    prob = make_problem("allen_cahn")
+    assert prob.input_dim == 3 and not prob.has_exact
+    colloc = prob.sample((40, 12), np.random.default_rng(5))
+    oclasses = O.OracleAllenCahn().sample((40, 12), np.random.default_rng(5))
+    for cls, oc in zip(colloc.classes, oclasses):
+        assert np.array_equal(cls.points, oc.points)
+        op = prob.class_operator(cls.class_id)
+        assert (op.cu, op.c3, op.cl, op.grad_dims, op.cg, op.lap_dims) == (
+            oc.cu, oc.c3, oc.cl, oc.grad_dims, oc.cg, oc.lap_dims)
+        np.testing.assert_allclose(prob.class_data(cls), oc.f, rtol=0, atol=0)
+        np.testing.assert_allclose(prob.input_channels(cls, op), oc.inputs, rtol=0, atol=1e-15)

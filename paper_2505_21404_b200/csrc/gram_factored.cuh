@@ -82,8 +82,8 @@ DNGD_DEV int gf_layer_chunks(const GramLayer& l) { return ((l.kh + 15) >> 4) + (
 // K[point pairs] += S (G_H o G_Z) S^T for one warp's 32 x 32 G-block.  Fragment
 // (i, j): rows lrow = lane/4 (+8i), columns 2(lane%4)+{0,1} (+8j); G-row bits
 // below LGA are the channel, so the row channel is lrow mod a for every i.
-template <int LGA, int LGB>
-DNGD_DEV void gf_epilogue(double2 (&accH)[4][4], double2 (&accZ)[4][4], bool seedZ, double bias0,
+template <int LGA, int LGB, bool SEEDZ>
+DNGD_DEV void gf_epilogue(double2 (&accH)[4][4], double2 (&accZ)[4][4], double bias0,
                           double bias1, const double* sA, const double* sB, double* Ks, int wm,
                           int wn, int lane) {
   const int lrow = lane >> 2;
@@ -97,8 +97,14 @@ DNGD_DEV void gf_epilogue(double2 (&accH)[4][4], double2 (&accZ)[4][4], bool see
     for (int j = 0; j < 4; ++j) {
       const int gc = wn * 32 + j * 8 + 2 * (lane & 3);
       // output layer: Zbar = per-row seeds (G^Z = seed_row * seed_col)
-      double v0 = (accH[i][j].x + bias0) * (seedZ ? sA[gr] * sB[gc] : accZ[i][j].x);
-      double v1 = (accH[i][j].y + bias1) * (seedZ ? sA[gr] * sB[gc + 1] : accZ[i][j].y);
+      double v0, v1;
+      if (SEEDZ) {
+        v0 = (accH[i][j].x + bias0) * (sA[gr] * sB[gc]);
+        v1 = (accH[i][j].y + bias1) * (sA[gr] * sB[gc + 1]);
+      } else {
+        v0 = (accH[i][j].x + bias0) * accZ[i][j].x;
+        v1 = (accH[i][j].y + bias1) * accZ[i][j].y;
+      }
       accH[i][j] = make_double2(0.0, 0.0);
       accZ[i][j] = make_double2(0.0, 0.0);
       // column bits = (h, lane bit 0, lane bit 1), row bits = lane bits 2, 3, 4
@@ -255,19 +261,29 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     if (lane == 0) mbar_arrive(&empty[st]);
     if (f + 1 != f_layer_end) continue;
     // ---- layer k_cur done
-    const bool seedZ = p.lay[k_cur].kz == 0;
-    switch (epi) {
-#define GF_EPI(A, B)                                                                            \
+    // output layer: Zbar = per-row seeds; other layers: the Z accumulator
+#define GF_EPI(A, B, S)                                                                         \
   case A * 4 + B:                                                                               \
-    gf_epilogue<A, B>(accH, accZ, seedZ, bias0, bias1, sA, sB, Ks, wm, wn, lane);               \
+    gf_epilogue<A, B, S>(accH, accZ, bias0, bias1, sA, sB, Ks, wm, wn, lane);                   \
     break;
-      GF_EPI(0, 0) GF_EPI(0, 1) GF_EPI(0, 2) GF_EPI(0, 3)
-      GF_EPI(1, 0) GF_EPI(1, 1) GF_EPI(1, 2) GF_EPI(1, 3)
-      GF_EPI(2, 0) GF_EPI(2, 1) GF_EPI(2, 2) GF_EPI(2, 3)
-      GF_EPI(3, 0) GF_EPI(3, 1) GF_EPI(3, 2) GF_EPI(3, 3)
-#undef GF_EPI
-      default: break;
+#define GF_EPI_ALL(S)                                                                           \
+  GF_EPI(0, 0, S) GF_EPI(0, 1, S) GF_EPI(0, 2, S) GF_EPI(0, 3, S)                               \
+  GF_EPI(1, 0, S) GF_EPI(1, 1, S) GF_EPI(1, 2, S) GF_EPI(1, 3, S)                               \
+  GF_EPI(2, 0, S) GF_EPI(2, 1, S) GF_EPI(2, 2, S) GF_EPI(2, 3, S)                               \
+  GF_EPI(3, 0, S) GF_EPI(3, 1, S) GF_EPI(3, 2, S) GF_EPI(3, 3, S)
+    if (p.lay[k_cur].kz == 0) {
+      switch (epi) {
+        GF_EPI_ALL(true)
+        default: break;
+      }
+    } else {
+      switch (epi) {
+        GF_EPI_ALL(false)
+        default: break;
+      }
     }
+#undef GF_EPI_ALL
+#undef GF_EPI
     if (k_cur + 1 < p.L) {
       ++k_cur;
       f_layer_start = f_layer_end;

@@ -16,7 +16,7 @@ Cholesky (+ retries), GN solve, f_vv, GA solve, line search, parameter update.
           reference algorithm) on the host cores, same workload
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                       [--config 1|2|3|5]
+                       [--config 1|2|3|4|5|6]
 """
 
 from __future__ import annotations
@@ -48,6 +48,10 @@ CONFIGS = {
     5: dict(problem="poisson2d", widths=(2, 256, 256, 256, 256, 1), counts=(30000, 2000),
             lam_cap=1e-5, dense_threshold=4000, nystrom_rank=512, cg_max_iters=200,
             name="cfg5_poisson2d_2-256x4-1_m32000_pcg"),
+    # not a BASELINE config: the reference's own configs/allen_cahn.json problem
+    # (periodic embedding + cubic reaction) at its default collocation counts
+    6: dict(problem="allen_cahn", widths=(3, 32, 32, 32, 1), counts=(1125, 225), lam_cap=1e-5,
+            dense_threshold=4000, name="ref_allen_cahn_3-32x3-1_m1350"),
 }
 METRIC = "D-NGD steps/s"
 UNIT = "steps/s"
@@ -448,7 +452,7 @@ def _oracle_problem(name):
     from oracle import dngd_oracle as O
 
     return {"poisson2d": O.OraclePoisson2d(), "heat1d": O.OracleHeat1d(),
-            "poisson5d_sin": O.OraclePoissonSin(5)}[name]
+            "poisson5d_sin": O.OraclePoissonSin(5), "allen_cahn": O.OracleAllenCahn()}[name]
 
 
 def cpu_baseline(cfg, max_seconds=25.0, warmup=1):

@@ -239,7 +239,7 @@ def run_ours(args, cfg):
     def one_step(rmap, theta):
         nonlocal shared_J
         from paper_2505_21404_b200.optimizer import LineSearchResult, _dispatch_step, _select
-        from paper_2505_21404_b200.solver import fused_dense_step
+        from paper_2505_21404_b200.solver import dense_iteration
 
         dense = rmap.m < config.dense_threshold
         jfree = not sharded and dense and rmap.jfree()
@@ -248,9 +248,8 @@ def run_ours(args, cfg):
             # device, one host read-back per step
             if not jfree:
                 rmap._J = shared_J
-            step, losses, anyd, loss, r = fused_dense_step(
-                rmap, theta, None, None, config.use_ga, config.line_search_points,
-                lam_cap=config.lam_cap)
+            step, losses, anyd, loss, r = dense_iteration(
+                rmap, theta, config.use_ga, config.line_search_points, config.lam_cap)
             if not jfree:
                 shared_J = rmap._J
             if step is not None:

@@ -7,6 +7,7 @@ steady-state steps do not allocate.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 
 import torch
@@ -39,12 +40,25 @@ class Workspace:
 
 
 _WS: dict[str, Workspace] = {}
+_WS_STACK: list = []  # private tables (a captured CUDA graph owns its scratch)
+
+
+@contextlib.contextmanager
+def private_workspaces(table: dict):
+    """Route workspace() to `table` (a CUDA graph's own buffers, which nothing else
+    may grow or free after capture)."""
+    _WS_STACK.append(table)
+    try:
+        yield
+    finally:
+        _WS_STACK.pop()
 
 
 def workspace(tag: str, nbytes: int) -> torch.Tensor:
-    ws = _WS.get(tag)
+    table = _WS_STACK[-1] if _WS_STACK else _WS
+    ws = table.get(tag)
     if ws is None:
-        ws = _WS[tag] = Workspace()
+        ws = table[tag] = Workspace()
     return ws.get(nbytes)
 
 

@@ -19,7 +19,7 @@ from .errors import ConfigError, DomainError
 from .model import INITIALIZERS, MlpSpec
 from .params import ParameterVector
 from .residuals import PinnResidualMap, ResidualMap
-from .solver import StepResult, dense_dual_solve, fused_dense_step, pcg_step
+from .solver import StepResult, dense_dual_solve, dense_iteration, fused_dense_step, pcg_step
 from .timing import stage
 
 LAMBDA_FLOOR = 1e-12
@@ -230,9 +230,8 @@ def _dngd_loop(trace: TrainTrace, rmap_provider, theta: ParameterVector, config:
             if dense:
                 # device-resident damping, step and line search: one host sync
                 # (solver.fused_dense_step); loss comes back with the losses
-                fused = fused_dense_step(rmap, theta, None, None, config.use_ga,
-                                         config.line_search_points, lam_cap=config.lam_cap,
-                                         lam_mult=mult)
+                fused = dense_iteration(rmap, theta, config.use_ga, config.line_search_points,
+                                        config.lam_cap, mult)
                 loss, r = fused[3], fused[4]
                 if fused[0] is None:
                     fused = None  # factorisation failed: eager path keeps the retry ladder

@@ -14,6 +14,7 @@ _ACTIVE = None
 class StageTimer:
     def __init__(self):
         self.pairs = []  # (name, start_event, end_event)
+        self.done = []  # (name, ms) already read (stages replayed inside a CUDA graph)
 
     def summary_ms(self) -> dict:
         import torch
@@ -24,17 +25,54 @@ class StageTimer:
         for name, s, e in self.pairs:
             out[name] = out.get(name, 0.0) + s.elapsed_time(e)
             counts[name] = counts.get(name, 0) + 1
+        for name, ms in self.done:
+            out[name] = out.get(name, 0.0) + ms
+            counts[name] = counts.get(name, 0) + 1
         return out, counts
+
+
+_CAPTURE = None  # list receiving (name, start, end) while a CUDA graph is captured
+
+
+@contextlib.contextmanager
+def capture_into(sink: list):
+    """Stage events recorded during graph capture go to `sink` as external event
+    nodes (they fire on every replay); add_captured() reads them after a replay."""
+    global _CAPTURE
+    prev = _CAPTURE
+    _CAPTURE = sink
+    try:
+        yield
+    finally:
+        _CAPTURE = prev
+
+
+def add_captured(pairs):
+    t = _ACTIVE
+    if t is None:
+        return
+    for name, s, e in pairs:
+        t.done.append((name, s.elapsed_time(e)))
 
 
 @contextlib.contextmanager
 def stage(name: str):
     t = _ACTIVE
-    if t is None:
+    if t is None and _CAPTURE is None:
         yield
         return
     import torch
 
+    if _CAPTURE is not None:
+        s = torch.cuda.Event(enable_timing=True, external=True)
+        e = torch.cuda.Event(enable_timing=True, external=True)
+        s.record()
+        try:
+            yield
+        finally:
+            e.record()
+            _CAPTURE.append((name, s, e))
+        return
     s = torch.cuda.Event(enable_timing=True)
     e = torch.cuda.Event(enable_timing=True)
     s.record()

@@ -325,3 +325,25 @@ def test_jfree_step_matches_materialized(P, golden_dir, name):
     jt_mat = rmap.vjp(theta, w)
     assert _rel(jt_free, jt_mat) <= 1e-12
     assert _rel(jt_free, Jo.T @ w) <= 1e-11
+
+
+@pytest.mark.parametrize("pname,widths,counts,lam_cap", [
+    ("heat1d", (2, 16, 16, 1), (60, 20, 20), 1e-3),   # J-free (factored Gram)
+    ("poisson2d", (2, 16, 16, 1), (60, 20), 1e-3),    # materialized J + SYRK
+    ("allen_cahn", (3, 16, 16, 1), (60, 20), 1e-3),   # embedding + cubic term
+])
+def test_graph_replay_matches_eager(P, monkeypatch, pname, widths, counts, lam_cap):
+    """The CUDA-graph dense iteration (default) reproduces the eager launches."""
+    def run():
+        config = P.OptimizerConfig(max_iters=4, lam_cap=lam_cap, deterministic_timing=True)
+        return P.dngd_run(P.make_problem(pname), P.MlpSpec(widths), config, 11, counts=counts,
+                          init="xavier_normal")
+    monkeypatch.setenv("DNGD_NO_GRAPH", "1")
+    eager = run()
+    monkeypatch.delenv("DNGD_NO_GRAPH")
+    graph = run()
+    assert not eager.aborted and not graph.aborted
+    np.testing.assert_allclose([r.loss for r in graph.rows], [r.loss for r in eager.rows],
+                               rtol=1e-13)
+    assert [r.eta for r in graph.rows] == [r.eta for r in eager.rows]
+    assert _rel(graph.final_theta.data, eager.final_theta.data) <= 1e-13

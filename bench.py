@@ -41,10 +41,11 @@ CONFIGS = {
     2: dict(problem="heat1d", widths=(2, 64, 64, 64, 64, 1), counts=(2000, 400, 400), lam_cap=1e-3,
             dense_threshold=4000, name="cfg2_heat1d_2-64x4-1_m2800"),
     3: dict(problem="poisson5d_sin", widths=(5, 512, 512, 512, 512, 1), counts=(3500, 500),
-            lam_cap=1e-5, dense_threshold=4001, name="cfg3_poisson5d_5-512x4-1_m4000"),
+            lam_cap=1e-5, dense_threshold=4001, name="cfg3_poisson5d_5-512x4-1_m4000",
+            multi_gpu="tiles"),
     4: dict(problem="poisson5d_sin", widths=(5, 1792, 1792, 1792, 1792, 1792, 1),
             counts=(7000, 1000), lam_cap=1e-5, dense_threshold=8001,
-            name="cfg4_poisson5d_5-1792x5-1_m8000_n12.86M"),
+            name="cfg4_poisson5d_5-1792x5-1_m8000_n12.86M", multi_gpu="tiles"),
     5: dict(problem="poisson2d", widths=(2, 256, 256, 256, 256, 1), counts=(30000, 2000),
             lam_cap=1e-5, dense_threshold=4000, nystrom_rank=512, cg_max_iters=200,
             name="cfg5_poisson2d_2-256x4-1_m32000_pcg"),
@@ -204,9 +205,13 @@ def run_ours(args, cfg):
     hbm_peak, hbm_src = _hbm_peak()
 
     # -------- device-resident run: all collocation sets uploaded before timing.
-    # N > 1: column-sharded step (sharded.py) -- every rank draws the same points,
-    # assembles its own Jacobian columns, K is all-reduced over NCCL.
-    sharded = world > 1
+    # N > 1, configs 1-2: column-sharded step (sharded.py) -- every rank draws the
+    # same points, assembles its own Jacobian columns, K is all-reduced over NCCL.
+    # Configs 3-4 (Gram-dominated, J too large): tile-sharded factored Gram -- each
+    # rank computes 1/N of K's tiles from the activations, one all-reduce of K,
+    # the rest of the step replicated.
+    tiles = world > 1 and cfg.get("multi_gpu") == "tiles"
+    sharded = world > 1 and not tiles
     ranges = None
     comm = None
     if sharded:
@@ -217,7 +222,11 @@ def run_ours(args, cfg):
         ranges = column_ranges(spec.param_count(), world)
         if sum(cfg["counts"]) >= cfg["dense_threshold"]:
             raise SystemExit("multi-GPU bench covers the dense configs (1-4)")
-    rng = np.random.default_rng(1000 if sharded else 1000 + rank)
+    if tiles:
+        from paper_2505_21404_b200.sharded import Comm
+
+        comm = Comm()
+    rng = np.random.default_rng(1000 if world > 1 else 1000 + rank)
     total = args.warmup + args.steps
     maps = []
     base = None
@@ -226,6 +235,8 @@ def run_ours(args, cfg):
         if base is None:
             mp = P.PinnResidualMap(problem, spec, colloc,
                                    col_range=ranges[rank] if sharded else None)
+            if tiles:
+                mp.gram_shard = (comm, rank, world)
         else:
             mp = base.rebind(colloc)
         maps.append(mp)
@@ -343,8 +354,9 @@ def run_ours(args, cfg):
             tr = sharded_dngd_run(problem, spec, config, seed=0, comm=comm, counts=cfg["counts"],
                                   init="xavier_normal", on_step=on_step)
         elif not args.profile:
-            tr = P.dngd_run(problem, spec, config, seed=rank, counts=cfg["counts"],
-                            init="xavier_normal", track_rel_l2=False, on_step=on_step)
+            tr = P.dngd_run(problem, spec, config, seed=0 if tiles else rank,
+                            counts=cfg["counts"], init="xavier_normal", track_rel_l2=False,
+                            on_step=on_step, gram_shard=(comm, rank, world) if tiles else None)
     finally:
         P.PinnResidualMap._device = orig_device
     if "t0" in marks and "t1" in marks:
@@ -421,8 +433,10 @@ def run_ours(args, cfg):
         "config": {"workload": cfg["name"], "m": m, "n": n, "widths": list(cfg["widths"]),
                    "solver": "dense Cholesky + geodesic acceleration" if m < cfg["dense_threshold"]
                    else "Nystrom-PCG", "lam_cap": cfg["lam_cap"], "line_search_points": 31,
-                   "parallelism": f"column-sharded J over {world} GPUs (NCCL all-reduce of K)"
-                   if world > 1 else "single GPU",
+                   "parallelism": (f"tile-sharded factored Gram over {world} GPUs (NCCL "
+                                   "all-reduce of K, rest replicated)") if tiles else
+                   (f"column-sharded J over {world} GPUs (NCCL all-reduce of K)"
+                    if world > 1 else "single GPU"),
                    "l2": l2_note},
         "roofline": roof,
         "gram_cholesky": gram_chol,

@@ -163,6 +163,13 @@ int dngd_assemble(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const d
 int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                        const double* theta, const dngd_class_desc* classes, int nclass,
                        double* r, double* K, int64_t ldK, void* work, size_t work_bytes);
+/* Tile-sharded variant (multi-GPU): writes only the entries of K
+ * covered by part `part` of `nparts` equal tile ranges; the caller zeroes K and
+ * sums the parts over the ranks (NCCL all-reduce).  part 0 of 1 == the above. */
+int dngd_gram_factored_part(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                            const double* theta, const dngd_class_desc* classes, int nclass,
+                            double* r, double* K, int64_t ldK, int part, int nparts, void* work,
+                            size_t work_bytes);
 
 /* r plus the forward channels and per-point adjoints (no J) left in work for
  * dngd_jt_factored (the tape sweep of residuals.py:241-256 without the rows) */

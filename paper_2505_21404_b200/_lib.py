@@ -84,6 +84,9 @@ _SIGS = {
                        c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_size], c_int),
     "dngd_gram_factored": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, ctypes.POINTER(ClassDesc),
                             c_int, c_vp, c_vp, c_i64, c_vp, c_size], c_int),
+    "dngd_gram_factored_part": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp,
+                                 ctypes.POINTER(ClassDesc), c_int, c_vp, c_vp, c_i64, c_int,
+                                 c_int, c_vp, c_size], c_int),
     "dngd_activations": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, ctypes.POINTER(ClassDesc),
                           c_int, c_vp, c_vp, c_size], c_int),
     "dngd_jt_workspace": ([c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc), c_int,

@@ -53,6 +53,7 @@ struct GramParams {
   int tj_n[10];
   double* K;
   long long ldK;
+  int tile0;  // first tile of this launch (tile-sharded multi-GPU Gram)
 };
 
 // Hext_0 rows: value channel [x], derivative channel d_j [e_j], Laplacian 0
@@ -141,8 +142,9 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
   uint64_t* empty = full + GF_STAGES;
   // ---- tile decode
   int pi = 0;
-  while (pi + 1 < p.npairs && static_cast<int>(blockIdx.x) >= p.tstart[pi + 1]) ++pi;
-  const int t = blockIdx.x - p.tstart[pi];
+  const int tile = static_cast<int>(blockIdx.x) + p.tile0;
+  while (pi + 1 < p.npairs && tile >= p.tstart[pi + 1]) ++pi;
+  const int t = tile - p.tstart[pi];
   const int c = p.pc[pi], cp = p.pcp[pi];
   int ti, tj;
   if (c == cp) {

@@ -1363,7 +1363,18 @@ extern "C" int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_de
                                   const double* theta, const dngd_class_desc* classes,
                                   int nclass, double* r, double* K, int64_t ldK, void* work,
                                   size_t work_bytes) {
+  return dngd_gram_factored_part(ctx, stream, mlp, theta, classes, nclass, r, K, ldK, 0, 1, work,
+                                 work_bytes);
+}
+
+extern "C" int dngd_gram_factored_part(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                                       const double* theta, const dngd_class_desc* classes,
+                                       int nclass, double* r, double* K, int64_t ldK, int part,
+                                       int nparts, void* work, size_t work_bytes) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nparts < 1 || part < 0 || part >= nparts) {
+    return set_error(ctx, DNGD_ERR_DIMENSION, "gram_factored: part outside [0, nparts)");
+  }
   Plan P;
   int rc = make_plan(ctx, mlp, classes, nclass, P);
   if (rc) return rc;
@@ -1453,8 +1464,13 @@ extern "C" int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_de
     attr[ctx->device & 63] = true;
   }
   static_assert(GF_H0_LD == 16, "carve_assemble reserves R x 16 for H0");
-  if (tiles > 0) {
-    k_gram_factored<<<static_cast<unsigned>(tiles), GF_THREADS, gram_factored_smem(), s>>>(gp);
+  // tile-sharded Gram: part p of nparts computes the contiguous tile range
+  // [p T / nparts, (p+1) T / nparts) (every 64x64 G-tile costs the same)
+  const long long t0 = static_cast<long long>(tiles) * part / nparts;
+  const long long t1 = static_cast<long long>(tiles) * (part + 1) / nparts;
+  gp.tile0 = static_cast<int>(t0);
+  if (t1 > t0) {
+    k_gram_factored<<<static_cast<unsigned>(t1 - t0), GF_THREADS, gram_factored_smem(), s>>>(gp);
   }
   return cuda_status(ctx, cudaGetLastError(), "gram_factored");
 }

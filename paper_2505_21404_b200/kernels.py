@@ -216,10 +216,16 @@ def assemble(mlp, theta, classes_arr, nclass, r, J=None, col_begin=0, col_end=No
          0 if ws is None else ws.numel())
 
 
-def gram_factored(mlp, theta, classes_arr, nclass, r, K, ws):
-    """r and K = J J^T from the activations (J never materialised)."""
-    call("dngd_gram_factored", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), classes_arr,
-         nclass, ptr(r), ptr(K), K.stride(0), ptr(ws), ws.numel())
+def gram_factored(mlp, theta, classes_arr, nclass, r, K, ws, part=0, nparts=1):
+    """r and K = J J^T from the activations (J never materialised).  With nparts > 1
+    only the part-th of nparts equal tile ranges of K is written (tile-sharded Gram)."""
+    if nparts == 1:
+        call("dngd_gram_factored", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta),
+             classes_arr, nclass, ptr(r), ptr(K), K.stride(0), ptr(ws), ws.numel())
+    else:
+        call("dngd_gram_factored_part", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta),
+             classes_arr, nclass, ptr(r), ptr(K), K.stride(0), int(part), int(nparts), ptr(ws),
+             ws.numel())
 
 
 def activations(mlp, theta, classes_arr, nclass, r, ws):

@@ -369,12 +369,15 @@ def network_values(problem, spec: MlpSpec, theta, pts) -> np.ndarray:
 
 
 def dngd_run(problem, spec: MlpSpec, config: OptimizerConfig, seed: int, counts=None,
-             init: str = "glorot_uniform", track_rel_l2: bool = True, on_step=None) -> TrainTrace:
+             init: str = "glorot_uniform", track_rel_l2: bool = True, on_step=None,
+             gram_shard=None) -> TrainTrace:
     """Train a network on a PDE problem with D-NGD (optimizer.py:290-314).
 
     `init` selects the initialiser ("glorot_uniform" = reference default,
     "xavier_normal" = BASELINE configs); the seed drives the initialisation and
-    every collocation / landmark draw in the reference's order.
+    every collocation / landmark draw in the reference's order.  gram_shard =
+    (comm, rank, world) splits the factored Gram's tiles over the ranks (one K
+    all-reduce per step; everything else replicated -- SURVEY §8e).
     """
     from .problems import sample_collocation
 
@@ -388,6 +391,7 @@ def dngd_run(problem, spec: MlpSpec, config: OptimizerConfig, seed: int, counts=
             colloc = sample_collocation(problem, counts, rng)
             if state["rmap"] is None:
                 state["rmap"] = PinnResidualMap(problem, spec, colloc)
+                state["rmap"].gram_shard = gram_shard
             else:
                 state["rmap"] = state["rmap"].rebind(colloc)
         return state["rmap"]

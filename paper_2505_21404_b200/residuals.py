@@ -406,6 +406,7 @@ class PinnResidualMap(ResidualMap):
 
     def rebind(self, collocation):
         other = PinnResidualMap(self.problem, self.spec, collocation, self.col_range)
+        other.gram_shard = self.gram_shard
         if self._J is not None and self._J.shape[0] == collocation.m:
             other._J = self._J  # reuse the Jacobian buffer across resamples
             self._cache = None  # this map no longer owns the buffer contents
@@ -599,8 +600,12 @@ class PinnResidualMap(ResidualMap):
     def _act_valid(self, th) -> bool:
         return _ACT_STATE.get("key") == (self._key(th), self._act_identity())
 
+    gram_shard = None  # (comm, rank, world): tile-sharded Gram summed over the ranks
+
     def gram_factored_t(self, theta, K_out):
-        """K = J J^T (and r) from the activations; leaves them for vjp_t."""
+        """K = J J^T (and r) from the activations; leaves them for vjp_t.  With
+        gram_shard set, this rank computes 1/world of the K tiles and the parts are
+        summed with one all-reduce (one reduction per Gram)."""
         import torch
 
         from . import kernels as K
@@ -608,7 +613,19 @@ class PinnResidualMap(ResidualMap):
         d = self._device()
         th = self._theta_t(theta)
         r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
-        K.gram_factored(d["mlp"], th, d["arr"], d["nclass"], r, K_out, self._act_workspace())
+        if self.gram_shard is not None:
+            comm, rank, world = self.gram_shard
+            K_out.zero_()
+            K.gram_factored(d["mlp"], th, d["arr"], d["nclass"], r, K_out,
+                            self._act_workspace(), rank, world)
+            if K_out.is_contiguous():
+                comm.allreduce_sum_(K_out)
+            else:
+                tmp = comm.allreduce_sum_(K_out.contiguous())
+                K_out.copy_(tmp)
+        else:
+            K.gram_factored(d["mlp"], th, d["arr"], d["nclass"], r, K_out,
+                            self._act_workspace())
         _ACT_STATE["key"] = (self._key(th), self._act_identity())
         self._rcache = (self._key(th), r)
         return K_out

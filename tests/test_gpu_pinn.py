@@ -128,3 +128,26 @@ def test_jt_factored_matches_oracle(K, name, problem, widths, counts):
     K.jt_factored(mlp, arr, len(classes), dev(w), -0.5, out, ws, scratch)
     assert _rel(out.cpu().numpy(), -0.5 * (J_ref.T @ w)) <= 1e-12
     assert _rel(r.cpu().numpy(), r_ref) <= 1e-12
+
+
+@pytest.mark.parametrize("nparts", [2, 3, 8])
+def test_gram_factored_parts_sum_to_full(K, nparts):
+    """Tile-sharded Gram (multi-GPU layout): the parts written by each rank are
+    disjoint and sum to the full K, bit for bit."""
+    problem, widths, counts = O.OracleHeat1d(), (2, 32, 32, 1), (300, 60, 60)
+    classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 12)
+    m = sum(c.count for c in classes)
+    r = torch.empty(m, dtype=torch.float64, device="cuda")
+    full = torch.empty((m, m), dtype=torch.float64, device="cuda")
+    K.gram_factored(mlp, th, arr, len(classes), r, full, ws)
+    acc = torch.zeros((m, m), dtype=torch.float64, device="cuda")
+    cover = torch.zeros((m, m), dtype=torch.int32, device="cuda")
+    for p in range(nparts):
+        part = torch.zeros((m, m), dtype=torch.float64, device="cuda")
+        sentinel = torch.full((m, m), np.nan, dtype=torch.float64, device="cuda")
+        K.gram_factored(mlp, th, arr, len(classes), r, part, ws, p, nparts)
+        K.gram_factored(mlp, th, arr, len(classes), r, sentinel, ws, p, nparts)
+        cover += (~torch.isnan(sentinel)).to(torch.int32)
+        acc += part
+    assert int(cover.min()) == 1 and int(cover.max()) == 1  # every entry written exactly once
+    assert torch.equal(acc, full)

@@ -275,9 +275,13 @@ def run_ours(args, cfg):
                 delta = step.delta.tensor
                 ls = device_line_search(rmap, theta, delta, loss, config.line_search_points)
         else:
-            rmap._J = shared_J
-            r, J = rmap.linearize_t(theta)
-            shared_J = rmap._J
+            pcg_jfree = not sharded and rmap.jfree_pcg()
+            if pcg_jfree:  # J-free PCG (solver.pcg_step with g=None)
+                r, J = rmap.residuals_act_t(theta), None
+            else:
+                rmap._J = shared_J
+                r, J = rmap.linearize_t(theta)
+                shared_J = rmap._J
             loss = 0.5 * float(K.dot(r, r).item())
             lam = lm_damping(loss, config.lam_cap)
             if sharded:
@@ -287,8 +291,10 @@ def run_ours(args, cfg):
                 ls = sharded_line_search(ops, comm, theta, delta, loss,
                                          config.line_search_points)
             else:  # Nystrom-PCG configuration
-                with timing.stage("gemv"):
-                    g = K.gemv_t(J, r, rmap.n)
+                g = None
+                if not pcg_jfree:
+                    with timing.stage("gemv"):
+                        g = K.gemv_t(J, r, rmap.n)
                 step = _dispatch_step(rmap, theta, g, lam, config, rng)
                 delta = step.delta.tensor
                 ls = device_line_search(rmap, theta, delta, loss, config.line_search_points)

@@ -192,6 +192,24 @@ int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double
              const double* v, const dngd_class_desc* classes, int nclass, double* fvv,
              void* work, size_t work_bytes);
 
+/* K[:, I] WITHOUT J (replaces the Nystrom sketch J J_I^T of solver.py:259-261):
+ * the activations of the sorted landmark rows `landmarks` (host int64, ell of
+ * them) are gathered into `scratch` (dngd_gram_cols_workspace bytes) and the
+ * factored Gram kernel fills Kc (m x ell, ldKc).  Needs the activations of the
+ * same theta in act_work (dngd_activations); linear residual operators only. */
+int dngd_gram_cols_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp,
+                             const dngd_class_desc* classes, int nclass, int ell, size_t* bytes);
+int dngd_gram_factored_cols(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                            const dngd_class_desc* classes, int nclass, const int64_t* landmarks,
+                            int ell, double* Kc, int64_t ldKc, void* act_work, size_t act_bytes,
+                            void* scratch, size_t scratch_bytes);
+
+/* out = J v WITHOUT J (replaces residuals.py:282-292 jvp): the first-order
+ * forward t-jets of the f_vv pass (same workspace as dngd_fvv) */
+int dngd_jvp_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                      const double* theta, const double* v, const dngd_class_desc* classes,
+                      int nclass, double* out, void* work, size_t work_bytes);
+
 /* losses[c] = 0.5 |r(theta + etas[c] * delta)|^2 for c < ncand
  * (residuals.py:188-201 via optimizer.py:148-166); etas is a device array.
  * delta == NULL: theta is an explicit (ncand x n) candidate stack. */

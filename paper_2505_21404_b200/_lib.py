@@ -95,6 +95,13 @@ _SIGS = {
                           c_vp, c_dbl, c_vp, c_vp, c_size, c_vp, c_size], c_int),
     "dngd_fvv": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, c_vp, ctypes.POINTER(ClassDesc), c_int,
                   c_vp, c_vp, c_size], c_int),
+    "dngd_gram_cols_workspace": ([c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc), c_int,
+                                  c_int, ctypes.POINTER(c_size)], c_int),
+    "dngd_gram_factored_cols": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc),
+                                 c_int, c_vp, c_int, c_vp, c_i64, c_vp, c_size, c_vp, c_size],
+                                c_int),
+    "dngd_jvp_factored": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, c_vp,
+                           ctypes.POINTER(ClassDesc), c_int, c_vp, c_vp, c_size], c_int),
     "dngd_loss_many": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, c_vp, c_vp, c_int,
                         ctypes.POINTER(ClassDesc), c_int, c_vp, c_vp, c_size], c_int),
 }

@@ -54,6 +54,12 @@ struct GramParams {
   double* K;
   long long ldK;
   int tile0;  // first tile of this launch (tile-sharded multi-GPU Gram)
+  // rect = 1: columns are gathered landmark points (Nystrom sketch K[:, I]):
+  // column class cp has ccount[cp] points at output columns ccol0[cp] + j, read
+  // through cmaps; all class pairs are rectangular and there is no mirror
+  int rect;
+  long long ccount[DNGD_MAX_CLASSES], ccol0[DNGD_MAX_CLASSES];
+  CUtensorMap cmaps[DNGD_MAX_LAYERS][2][DNGD_MAX_CLASSES];
 };
 
 // Hext_0 rows: value channel [x], derivative channel d_j [e_j], Laplacian 0
@@ -147,7 +153,7 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
   const int t = tile - p.tstart[pi];
   const int c = p.pc[pi], cp = p.pcp[pi];
   int ti, tj;
-  if (c == cp) {
+  if (c == cp && !p.rect) {
     decode_lower(t, ti, tj);
   } else {
     ti = t / p.tj_n[pi];
@@ -178,7 +184,8 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     const int cha = g & ((1 << lga) - 1), pa = P0 + (g >> lga);
     const int chb = g & ((1 << lgb) - 1), pb = Q0 + (g >> lgb);
     sA[g] = (cha < Ca.nch && pa < Ca.count) ? seedc(p.T, Ca, cha, Ca.row0 + pa) : 0.0;
-    sB[g] = (chb < Cb.nch && pb < Cb.count) ? seedc(p.T, Cb, chb, Cb.row0 + pb) : 0.0;
+    const long long cntb = p.rect ? p.ccount[cp] : Cb.count;  // rect: c3 == 0 (no u0 lookup)
+    sB[g] = (chb < Cb.nch && pb < cntb) ? seedc(p.T, Cb, chb, Cb.row0 + pb) : 0.0;
   }
   __syncthreads();
 
@@ -191,7 +198,8 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     uint8_t* sa = smem + st * GF_STAGE_BYTES;
     mbar_arrive_expect_tx(&full[st], GF_STAGE_BYTES);
     tma_load_3d(sa, &p.maps[k][part][c], &full[st], kc * 16, 0, P0);
-    tma_load_3d(sa + GF_BM * 128, &p.maps[k][part][cp], &full[st], kc * 16, 0, Q0);
+    tma_load_3d(sa + GF_BM * 128, p.rect ? &p.cmaps[k][part][cp] : &p.maps[k][part][cp],
+                &full[st], kc * 16, 0, Q0);
   };
   if (threadIdx.x == 0) {
     for (int f = 0; f < min(nchunks, GF_STAGES); ++f) issue(f);
@@ -295,8 +303,19 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
   }
   __syncthreads();
   // ---- epilogue: K[row][col] and its mirror (one writer per entry)
-  const long long cnt_r = p.T.c[c].count, cnt_c = p.T.c[cp].count;
-  const long long row0 = p.T.c[c].row0, col0 = p.T.c[cp].row0;
+  const long long cnt_r = p.T.c[c].count;
+  const long long row0 = p.T.c[c].row0;
+  if (p.rect) {
+    const long long cnt_c = p.ccount[cp], col0 = p.ccol0[cp];
+    for (int e = threadIdx.x; e < np_r * np_c; e += GF_THREADS) {
+      const int r = e / np_c, cc = e - (e / np_c) * np_c;
+      if (P0 + r >= cnt_r || Q0 + cc >= cnt_c) continue;
+      p.K[(row0 + P0 + r) * p.ldK + col0 + Q0 + cc] = Ks[r * GF_BM + cc];
+    }
+    return;
+  }
+  const long long cnt_c = p.T.c[cp].count;
+  const long long col0 = p.T.c[cp].row0;
   for (int e = threadIdx.x; e < np_r * np_c; e += GF_THREADS) {
     const int r = e / np_c, cc = e - (e / np_c) * np_c;
     const long long pr = P0 + r, pcl = Q0 + cc;

@@ -439,10 +439,11 @@ __global__ void k_fvv_hidden(Classes T, const double* __restrict__ P, const doub
   tanh_tjet(C, zget, hput);
 }
 
-// output: fvv_i = w * sum_c coef_c (Hc_c . W_L + 2 Hb_c . V_L)
+// output, order 2: fvv_i = w * sum_c coef_c (Hc_c . W_L + 2 Hb_c . V_L)
+//         order 1: (J v)_i = w * sum_c coef_c (Hb_c . W_L + Ha_c . V_L [+ vb_L on c = 0])
 __global__ void k_fvv_head(Classes T, const double* __restrict__ H3, int w, long long ld,
                            const double* __restrict__ WL, const double* __restrict__ VL,
-                           double* __restrict__ out) {
+                           double* __restrict__ out, int order) {
   const long long p = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= T.m) return;
@@ -451,6 +452,28 @@ __global__ void k_fvv_head(Classes T, const double* __restrict__ H3, int w, long
   const long long blk = T.R * ld;
   const double* h = H3 + (C.act0 + i * C.nch) * ld;
   double res = 0.0;
+  if (order == 1) {
+    for (int c = 0; c < C.nch; ++c) {
+      double u = 0.0;
+      for (int q = lane; q < w; q += 32)
+        u = fma(h[blk + c * ld + q], WL[q], fma(h[c * ld + q], VL[q], u));
+      u = warp_sum(u);
+      if (c == 0) u += VL[w];
+      res = fma(coef(C, c), u, res);
+    }
+    if (C.c3 != 0.0) {  // d(c3 u^3) = 3 c3 u^2 u'
+      double ua = 0.0, ub = 0.0;
+      for (int q = lane; q < w; q += 32) {
+        ua = fma(h[q], WL[q], ua);
+        ub = fma(h[blk + q], WL[q], fma(h[q], VL[q], ub));
+      }
+      ua = warp_sum(ua) + WL[w];
+      ub = warp_sum(ub) + VL[w];
+      res = fma(3.0 * C.c3 * ua * ua, ub, res);
+    }
+    if (lane == 0) out[p] = C.weight * res;
+    return;
+  }
   for (int c = 0; c < C.nch; ++c) {
     double u = 0.0;
     for (int q = lane; q < w; q += 32)
@@ -1359,6 +1382,70 @@ extern "C" int dngd_activations(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   return assemble_impl(ctx, s, P, B, theta, 0, P.n, r, nullptr, 0, true);
 }
 
+// 3-D maps (columns, channels, points) over one class's rows of H_k / Zbar_k; a
+// box of 16 x a x 64/a is one 64-row G-space operand tile (channels >= nch are
+// out of bounds and arrive as zeros)
+static int gf_encode3(dngd_ctx* ctx, CUtensorMap* map, const double* base, long long inner,
+                      int nch, long long N, long long ld, int lg) {
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(nch),
+                        static_cast<cuuint64_t>(std::max<long long>(N, 1))};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 8, static_cast<cuuint64_t>(ld) * nch * 8};
+  cuuint32_t box[3] = {16, static_cast<cuuint32_t>(1 << lg), static_cast<cuuint32_t>(GF_BM >> lg)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult res = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base),
+                             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return res == CUDA_SUCCESS ? DNGD_OK
+                             : set_error(ctx, DNGD_ERR_CUDA, "gram_factored: tensor map encode failed");
+}
+
+// padded channel counts, layer K-dims and the row-side tensor maps of the factored Gram
+static int gram_setup(dngd_ctx* ctx, const Plan& P, const AsmBufs& B, GramParams& gp) {
+  int rc = DNGD_OK;
+  memset(&gp, 0, sizeof gp);
+  gp.T = P.T;
+  gp.L = P.L;
+  for (int c = 0; c < P.T.n; ++c) {
+    const int nch = P.T.c[c].nch;
+    int lg = 0;
+    while ((1 << lg) < nch) ++lg;
+    if (lg > 3) {
+      return set_error(ctx, DNGD_ERR_UNSUPPORTED,
+                       "gram_factored: more than 8 channels per point; use assemble + syrk");
+    }
+    gp.lg[c] = lg;
+  }
+  // 3-D maps (columns, channels, points) over each class's rows of H_k / Zbar_k;
+  // a box of 16 x a x 64/a is one 64-row G-space operand tile (channels >= nch
+  // are out of bounds and arrive as zeros)
+  auto encode3 = [&](CUtensorMap* map, const double* base, long long inner, int nch, long long N,
+                     long long ld, int lg) -> int {
+    return gf_encode3(ctx, map, base, inner, nch, N, ld, lg);
+  };
+  for (int k = 0; k < P.L; ++k) {
+    gp.lay[k].kh = static_cast<int>(P.w[k]);
+    gp.lay[k].kz = k <= P.L - 2 ? static_cast<int>(P.w[k + 1]) : 0;
+    for (int c = 0; c < P.T.n; ++c) {
+      const ClassDev& Cc = P.T.c[c];
+      if (k >= 1) {
+        rc = encode3(&gp.maps[k][0][c], B.H[k] + Cc.act0 * P.ld[k], P.w[k], Cc.nch, Cc.count,
+                     P.ld[k], gp.lg[c]);
+      } else {
+        rc = encode3(&gp.maps[0][0][c], B.H0 + Cc.act0 * GF_H0_LD, P.T.din, Cc.nch, Cc.count,
+                     GF_H0_LD, gp.lg[c]);
+      }
+      if (rc) return rc;
+      if (k <= P.L - 2) {
+        rc = encode3(&gp.maps[k][1][c], B.Zb[k] + Cc.act0 * P.ld[k + 1], P.w[k + 1], Cc.nch,
+                     Cc.count, P.ld[k + 1], gp.lg[c]);
+        if (rc) return rc;
+      }
+    }
+  }
+  return DNGD_OK;
+}
+
 extern "C" int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                                   const double* theta, const dngd_class_desc* classes,
                                   int nclass, double* r, double* K, int64_t ldK, void* work,
@@ -1387,58 +1474,9 @@ extern "C" int dngd_gram_factored_part(dngd_ctx* ctx, void* stream, const dngd_m
   P.T.u0 = B.u0;
   rc = assemble_impl(ctx, s, P, B, theta, 0, P.n, r, nullptr, 0, true);
   if (rc) return rc;
-  thread_local GramParams gp;  // ~8.5 KB of tensor maps: off the host stack, reentrant
-  memset(&gp, 0, sizeof gp);
-  gp.T = P.T;
-  gp.L = P.L;
-  for (int c = 0; c < P.T.n; ++c) {
-    const int nch = P.T.c[c].nch;
-    int lg = 0;
-    while ((1 << lg) < nch) ++lg;
-    if (lg > 3) {
-      return set_error(ctx, DNGD_ERR_UNSUPPORTED,
-                       "gram_factored: more than 8 channels per point; use assemble + syrk");
-    }
-    gp.lg[c] = lg;
-  }
-  // 3-D maps (columns, channels, points) over each class's rows of H_k / Zbar_k;
-  // a box of 16 x a x 64/a is one 64-row G-space operand tile (channels >= nch
-  // are out of bounds and arrive as zeros)
-  auto encode3 = [&](CUtensorMap* map, const double* base, long long inner, int nch, long long N,
-                     long long ld, int lg) -> int {
-    cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(nch),
-                          static_cast<cuuint64_t>(std::max<long long>(N, 1))};
-    cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 8,
-                             static_cast<cuuint64_t>(ld) * nch * 8};
-    cuuint32_t box[3] = {16, static_cast<cuuint32_t>(1 << lg), static_cast<cuuint32_t>(GF_BM >> lg)};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult res = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base),
-                               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return res == CUDA_SUCCESS ? DNGD_OK
-                               : set_error(ctx, DNGD_ERR_CUDA, "gram_factored: tensor map encode failed");
-  };
-  for (int k = 0; k < P.L; ++k) {
-    gp.lay[k].kh = static_cast<int>(P.w[k]);
-    gp.lay[k].kz = k <= P.L - 2 ? static_cast<int>(P.w[k + 1]) : 0;
-    for (int c = 0; c < P.T.n; ++c) {
-      const ClassDev& Cc = P.T.c[c];
-      if (k >= 1) {
-        rc = encode3(&gp.maps[k][0][c], B.H[k] + Cc.act0 * P.ld[k], P.w[k], Cc.nch, Cc.count,
-                     P.ld[k], gp.lg[c]);
-      } else {
-        rc = encode3(&gp.maps[0][0][c], B.H0 + Cc.act0 * GF_H0_LD, P.T.din, Cc.nch, Cc.count,
-                     GF_H0_LD, gp.lg[c]);
-      }
-      if (rc) return rc;
-      if (k <= P.L - 2) {
-        rc = encode3(&gp.maps[k][1][c], B.Zb[k] + Cc.act0 * P.ld[k + 1], P.w[k + 1], Cc.nch,
-                     Cc.count, P.ld[k + 1], gp.lg[c]);
-        if (rc) return rc;
-      }
-    }
-  }
+  thread_local GramParams gp;  // ~17 KB of tensor maps: off the host stack, reentrant
+  rc = gram_setup(ctx, P, B, gp);
+  if (rc) return rc;
   int np = 0, tiles = 0;
   gp.tstart[0] = 0;
   for (int c = 0; c < P.T.n; ++c) {
@@ -1475,9 +1513,187 @@ extern "C" int dngd_gram_factored_part(dngd_ctx* ctx, void* stream, const dngd_m
   return cuda_status(ctx, cudaGetLastError(), "gram_factored");
 }
 
+// ------------------------------------------------------------------ K[:, I] without J
+// Nystrom sketch columns (solver.py:259-261 K[:, I] = J J_I^T): the activations of
+// the landmark points are gathered into compact per-class buffers and the factored
+// Gram kernel runs rectangular tiles (all points) x (landmarks).
+
+__global__ void k_gather_rows(const double* __restrict__ src, long long ld,
+                              const long long* __restrict__ idx, long long nrows,
+                              double* __restrict__ dst) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= nrows * ld) return;
+  const long long r = e / ld, c = e - (e / ld) * ld;
+  dst[e] = src[idx[r] * ld + c];
+}
+
+struct ColsPlan {
+  long long lc[MAXC], lrow0[MAXC];  // landmarks per class; first gathered activation row
+  long long rows;                   // gathered activation rows
+  std::vector<long long> src;       // source activation row of every gathered row
+};
+
+static int cols_plan(dngd_ctx* ctx, const Plan& P, const int64_t* landmarks, int ell, ColsPlan& Q) {
+  Q.rows = 0;
+  Q.src.clear();
+  int pos = 0;
+  for (int c = 0; c < P.T.n; ++c) {
+    const ClassDev& C = P.T.c[c];
+    Q.lc[c] = 0;
+    Q.lrow0[c] = Q.rows;
+    while (pos < ell && landmarks[pos] < C.row0 + C.count) {
+      const long long p = landmarks[pos];
+      if (p < C.row0 || (pos > 0 && p <= landmarks[pos - 1])) {
+        return set_error(ctx, DNGD_ERR_DIMENSION, "gram_cols: landmarks must be sorted and distinct");
+      }
+      for (int ch = 0; ch < C.nch; ++ch) Q.src.push_back(C.act0 + (p - C.row0) * C.nch + ch);
+      Q.rows += C.nch;
+      ++Q.lc[c];
+      ++pos;
+    }
+  }
+  if (pos != ell) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_cols: landmark outside [0, m)");
+  return DNGD_OK;
+}
+
+static size_t cols_scratch_bytes(const Plan& P, long long rows) {
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  size_t b = al(static_cast<size_t>(rows) * 8) + al(static_cast<size_t>(rows) * GF_H0_LD * 8);
+  for (int k = 1; k <= P.L - 1; ++k) b += al(static_cast<size_t>(rows) * P.ld[k] * 8);
+  for (int k = 0; k <= P.L - 2; ++k) b += al(static_cast<size_t>(rows) * P.ld[k + 1] * 8);
+  return b;
+}
+
+extern "C" int dngd_gram_cols_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp,
+                                        const dngd_class_desc* classes, int nclass, int ell,
+                                        size_t* bytes) {
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  *bytes = cols_scratch_bytes(P, static_cast<long long>(std::max(ell, 1)) * 8);
+  return DNGD_OK;
+}
+
+extern "C" int dngd_gram_factored_cols(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                                       const dngd_class_desc* classes, int nclass,
+                                       const int64_t* landmarks, int ell, double* Kc,
+                                       int64_t ldKc, void* act_work, size_t act_bytes,
+                                       void* scratch, size_t scratch_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  if (bytes_of(P, 0, 1) > act_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_cols: activation workspace too small");
+  if (P.m == 0 || ell <= 0) return DNGD_OK;
+  if (P.T.din > DNGD_MAX_GRAD) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_cols: input dim > 12");
+  for (int c = 0; c < P.T.n; ++c) {
+    if (P.T.c[c].c3 != 0.0) {
+      return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_cols: cubic residual terms need the materialised path");
+    }
+  }
+  ColsPlan Q;
+  rc = cols_plan(ctx, P, landmarks, ell, Q);
+  if (rc) return rc;
+  if (cols_scratch_bytes(P, Q.rows) > scratch_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_cols: scratch too small");
+  Arena A{static_cast<char*>(act_work)};
+  AsmBufs B;
+  carve_assemble(P, A, B);
+  P.T.u0 = B.u0;
+  thread_local GramParams gp;
+  rc = gram_setup(ctx, P, B, gp);
+  if (rc) return rc;
+  // gathered buffers: [idx][H0][H_1..H_{L-1}][Zb_0..Zb_{L-2}]
+  Arena S{static_cast<char*>(scratch)};
+  long long* idx = reinterpret_cast<long long*>(S.take(Q.rows));
+  cudaError_t e = cudaMemcpyAsync(idx, Q.src.data(), Q.rows * sizeof(long long),
+                                  cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_status(ctx, e, "gram_cols index upload");
+  auto gather = [&](const double* src, long long ld) {
+    double* dst = S.take(static_cast<size_t>(Q.rows) * ld);
+    k_gather_rows<<<nblk(Q.rows * ld), 256, 0, s>>>(src, ld, idx, Q.rows, dst);
+    return dst;
+  };
+  double* gH0 = gather(B.H0, GF_H0_LD);
+  std::vector<double*> gH(P.L, nullptr), gZ(P.L, nullptr);
+  for (int k = 1; k <= P.L - 1; ++k) gH[k] = gather(B.H[k], P.ld[k]);
+  for (int k = 0; k <= P.L - 2; ++k) gZ[k] = gather(B.Zb[k], P.ld[k + 1]);
+  long long col0 = 0;
+  for (int c = 0; c < P.T.n; ++c) {
+    const ClassDev& Cc = P.T.c[c];
+    gp.ccount[c] = Q.lc[c];
+    gp.ccol0[c] = col0;
+    col0 += Q.lc[c];
+    for (int k = 0; k < P.L; ++k) {
+      if (k >= 1) {
+        rc = gf_encode3(ctx, &gp.cmaps[k][0][c], gH[k] + Q.lrow0[c] * P.ld[k], P.w[k], Cc.nch,
+                        Q.lc[c], P.ld[k], gp.lg[c]);
+      } else {
+        rc = gf_encode3(ctx, &gp.cmaps[0][0][c], gH0 + Q.lrow0[c] * GF_H0_LD, P.T.din, Cc.nch,
+                        Q.lc[c], GF_H0_LD, gp.lg[c]);
+      }
+      if (rc) return rc;
+      if (k <= P.L - 2) {
+        rc = gf_encode3(ctx, &gp.cmaps[k][1][c], gZ[k] + Q.lrow0[c] * P.ld[k + 1], P.w[k + 1],
+                        Cc.nch, Q.lc[c], P.ld[k + 1], gp.lg[c]);
+        if (rc) return rc;
+      }
+    }
+  }
+  int np = 0, tiles = 0;
+  gp.tstart[0] = 0;
+  for (int c = 0; c < P.T.n; ++c) {
+    for (int cp = 0; cp < P.T.n; ++cp) {
+      if (Q.lc[cp] == 0) continue;
+      const int ti = static_cast<int>((P.T.c[c].count + (GF_BM >> gp.lg[c]) - 1) / (GF_BM >> gp.lg[c]));
+      const int tj = static_cast<int>((Q.lc[cp] + (GF_BM >> gp.lg[cp]) - 1) / (GF_BM >> gp.lg[cp]));
+      gp.pc[np] = c;
+      gp.pcp[np] = cp;
+      gp.tj_n[np] = tj;
+      tiles += ti * tj;
+      gp.tstart[np + 1] = tiles;
+      ++np;
+    }
+  }
+  gp.npairs = np;
+  gp.rect = 1;
+  gp.K = Kc;
+  gp.ldK = ldKc;
+  gp.tile0 = 0;
+  static bool attr[64] = {false};
+  if (!attr[ctx->device & 63]) {
+    e = cudaFuncSetAttribute(k_gram_factored, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(gram_factored_smem()));
+    if (e != cudaSuccess) return cuda_status(ctx, e, "gram_cols smem attribute");
+    attr[ctx->device & 63] = true;
+  }
+  if (tiles > 0) {
+    k_gram_factored<<<static_cast<unsigned>(tiles), GF_THREADS, gram_factored_smem(), s>>>(gp);
+  }
+  return cuda_status(ctx, cudaGetLastError(), "gram_cols");
+}
+
+static int fvv_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
+                    const double* v, const dngd_class_desc* classes, int nclass, double* fvv,
+                    void* work, size_t work_bytes, int order);
+
 extern "C" int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                         const double* theta, const double* v, const dngd_class_desc* classes,
                         int nclass, double* fvv, void* work, size_t work_bytes) {
+  return fvv_impl(ctx, stream, mlp, theta, v, classes, nclass, fvv, work, work_bytes, 2);
+}
+
+extern "C" int dngd_jvp_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                                 const double* theta, const double* v,
+                                 const dngd_class_desc* classes, int nclass, double* out,
+                                 void* work, size_t work_bytes) {
+  return fvv_impl(ctx, stream, mlp, theta, v, classes, nclass, out, work, work_bytes, 1);
+}
+
+// forward t-jets of the channel map along theta + t v: order 2 -> f_vv, order 1 -> J v
+// (first-order jets only: the GEMMs cover 2R and R rows instead of 3R and 2R)
+static int fvv_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
+                    const double* v, const dngd_class_desc* classes, int nclass, double* fvv,
+                    void* work, size_t work_bytes, int order) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Plan P;
   int rc = make_plan(ctx, mlp, classes, nclass, P);
@@ -1499,7 +1715,7 @@ extern "C" int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
     launch_transpose(s, v + P.off[k], 0, static_cast<int>(P.w[k]), static_cast<int>(P.w[k + 1]),
                      B.Vt[k], P.ld[k], 0, 1);
     GemmCall g;
-    g.M = 3 * P.R;
+    g.M = (order == 1 ? 2 : 3) * P.R;
     g.N = P.w[k + 1];
     g.K = P.w[k];
     g.A = Hcur;
@@ -1510,7 +1726,7 @@ extern "C" int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
     g.ldc = ld;
     rc = gemm_nt(ctx, s, g);
     if (rc) return rc;
-    g.M = 2 * P.R;
+    g.M = (order == 1 ? 1 : 2) * P.R;
     g.B = B.Vt[k];
     g.C = B.Q2;
     rc = gemm_nt(ctx, s, g);
@@ -1521,8 +1737,8 @@ extern "C" int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
     std::swap(Hcur, Hnext);
   }
   k_fvv_head<<<nblk(P.m, 8), 256, 0, s>>>(P.T, Hcur, static_cast<int>(P.w[L - 1]), ld,
-                                           theta + P.off[L - 1], v + P.off[L - 1], fvv);
-  return cuda_status(ctx, cudaGetLastError(), "fvv");
+                                           theta + P.off[L - 1], v + P.off[L - 1], fvv, order);
+  return cuda_status(ctx, cudaGetLastError(), order == 1 ? "jvp_factored" : "fvv");
 }
 
 // the fused line search handles nets whose every layer width is <= 64 and whose

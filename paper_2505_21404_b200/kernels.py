@@ -251,6 +251,26 @@ def fvv(mlp, theta, v, classes_arr, nclass, out, ws):
          nclass, ptr(out), ptr(ws), ws.numel())
 
 
+def gram_factored_cols(mlp, classes_arr, nclass, landmarks, Kc, act_ws):
+    """Kc (m x ell) = K[:, landmarks] from the activations in act_ws (no J)."""
+    import numpy as _np
+
+    lm = _np.ascontiguousarray(landmarks, dtype=_np.int64)
+    nb = c_size()
+    call("dngd_gram_cols_workspace", ctx(), ctypes.byref(mlp), classes_arr, nclass, int(lm.size),
+         ctypes.byref(nb))
+    scratch = workspace("gram_cols", nb.value)
+    call("dngd_gram_factored_cols", ctx(), stream_handle(), ctypes.byref(mlp), classes_arr,
+         nclass, lm.ctypes.data_as(ctypes.c_void_p), int(lm.size), ptr(Kc), Kc.stride(0),
+         ptr(act_ws), act_ws.numel(), ptr(scratch), scratch.numel())
+
+
+def jvp_factored(mlp, theta, v, classes_arr, nclass, out, ws):
+    """out = J v from forward tangents (no J)."""
+    call("dngd_jvp_factored", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), ptr(v),
+         classes_arr, nclass, ptr(out), ptr(ws), ws.numel())
+
+
 def loss_many(mlp, theta, delta, etas, ncand, classes_arr, nclass, out, ws):
     call("dngd_loss_many", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), ptr(delta),
          ptr(etas), int(ncand), classes_arr, nclass, ptr(out), ptr(ws), ws.numel())

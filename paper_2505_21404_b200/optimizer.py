@@ -237,7 +237,11 @@ def _dngd_loop(trace: TrainTrace, rmap_provider, theta: ParameterVector, config:
                     fused = None  # factorisation failed: eager path keeps the retry ladder
                 J = None if jfree else rmap.jacobian_t(theta)
             else:
-                r, J = rmap.linearize_t(theta)
+                jfree = bool(getattr(rmap, "jfree_pcg", lambda: False)())
+                if jfree:  # J-free PCG: residuals and activations only
+                    r, J = rmap.residuals_act_t(theta), None
+                else:
+                    r, J = rmap.linearize_t(theta)
                 loss = 0.5 * float(K.dot(r, r).item())
                 if not np.isfinite(loss):
                     from .residuals import _raise_nonfinite

@@ -594,6 +594,60 @@ class PinnResidualMap(ResidualMap):
         """Dense step without J: factored Gram + J^T w from the activations."""
         return self.use_factored_gram()
 
+    def jfree_pcg(self) -> bool:
+        """PCG without J: J^T w / J v from activations and forward tangents, the
+        Nystrom columns K[:, I] from the factored kernel (linear operators only)."""
+        return self.use_factored_gram() and all(
+            float(getattr(self.problem.class_operator(c.class_id), "c3", 0.0)) == 0.0
+            for c in self.collocation.classes)
+
+    def residuals_act_t(self, theta):
+        """r together with the activations (left for vjp_t / kcols_t; no J)."""
+        import torch
+
+        from . import kernels as K
+
+        d = self._device()
+        th = self._theta_t(theta)
+        if not self._act_valid(th):
+            r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
+            with stage("activations"):
+                K.activations(d["mlp"], th, d["arr"], d["nclass"], r, self._act_workspace())
+            _ACT_STATE["key"] = (self._key(th), self._act_identity())
+            self._rcache = (self._key(th), r)
+        return self._rcache[1]
+
+    def jvp_t(self, theta, v_t):
+        """J v: over the cached J, else from first-order forward tangents (no J)."""
+        from . import kernels as K
+
+        th = self._theta_t(theta)
+        if (self._cache is not None and self._cache[0] == self._key(th)) or not self.jfree():
+            return super().jvp_t(theta, v_t)
+        import torch
+
+        d = self._device()
+        out = torch.empty(self.m, dtype=torch.float64, device=d["device"])
+        with stage("jvp"):
+            K.jvp_factored(d["mlp"], th, v_t.contiguous(), d["arr"], d["nclass"], out,
+                           self._workspace(d["ws_bytes"]))
+        return out
+
+    def kcols_t(self, theta, landmarks):
+        """K[:, landmarks] (m x ell) from the activations of theta (no J)."""
+        import torch
+
+        from . import kernels as K
+
+        d = self._device()
+        self.residuals_act_t(theta)  # activations of this theta
+        Kc = torch.empty((self.m, max(len(landmarks), 1) + (len(landmarks) % 2)),
+                         dtype=torch.float64, device=d["device"])
+        with stage("kcols"):
+            K.gram_factored_cols(d["mlp"], d["arr"], d["nclass"], landmarks, Kc,
+                                 self._act_workspace())
+        return Kc[:, : len(landmarks)]
+
     def _act_identity(self):
         return (id(self), self._dev["arr"] if self._dev else None)
 

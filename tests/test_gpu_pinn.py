@@ -151,3 +151,15 @@ def test_gram_factored_parts_sum_to_full(K, nparts):
         acc += part
     assert int(cover.min()) == 1 and int(cover.max()) == 1  # every entry written exactly once
     assert torch.equal(acc, full)
+
+
+@pytest.mark.parametrize("name,problem,widths,counts", CASES)
+def test_jvp_factored_matches_oracle(K, name, problem, widths, counts):
+    """J v from first-order forward t-jets (no J) == oracle J v."""
+    from tests.gpu_util import dev
+    classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 8)
+    _, J_ref = O.linearize(theta, widths, classes)
+    v = np.random.default_rng(13).normal(size=theta.size)
+    out = torch.full((J_ref.shape[0],), np.nan, dtype=torch.float64, device="cuda")
+    K.jvp_factored(mlp, th, dev(v), arr, len(classes), out, ws)
+    assert _rel(out.cpu().numpy(), J_ref @ v) <= 1e-12

@@ -347,3 +347,40 @@ def test_graph_replay_matches_eager(P, monkeypatch, pname, widths, counts, lam_c
                                rtol=1e-13)
     assert [r.eta for r in graph.rows] == [r.eta for r in eager.rows]
     assert _rel(graph.final_theta.data, eager.final_theta.data) <= 1e-13
+
+
+@pytest.mark.parametrize("pname,widths,counts", [
+    ("poisson2d", (2, 48, 48, 1), (300, 60)),
+    ("heat1d", (2, 64, 64, 1), (200, 40, 40)),
+    ("poisson5d_sin", (5, 160, 96, 1), (60, 20)),   # wide J^T w path
+])
+def test_jfree_pcg_matches_materialized(P, pname, widths, counts):
+    """J-free PCG (J^T w from activations, J v from forward tangents, Nystrom columns
+    from the factored kernel) == the materialised-J PCG, same landmarks."""
+    problem = P.make_problem(pname)
+    spec = P.MlpSpec(widths)
+    colloc = problem.sample(counts, np.random.default_rng(21))
+    theta = P.xavier_normal_params(spec)
+
+    def solve(mode):
+        rmap = P.PinnResidualMap(problem, spec, colloc)
+        rmap.gram_mode = mode
+        if mode == "factored":
+            assert rmap.jfree_pcg()
+            g = None
+        else:
+            _, g = rmap.residuals_and_gradient(theta)
+        rng = np.random.default_rng(5)
+        P_pre = P.nystrom_build(rmap, theta, landmark_count=32, lam=1e-3, rng=rng)
+        res = P.pcg_step(rmap, theta, g, lam=1e-3, landmark_count=32, tol=1e-10,
+                         max_iters=300, rng=np.random.default_rng(5))
+        return P_pre, res
+
+    pre_f, res_f = solve("factored")
+    pre_m, res_m = solve("materialized")
+    np.testing.assert_array_equal(pre_f.landmarks, pre_m.landmarks)
+    assert _rel(pre_f.lam_hat, pre_m.lam_hat) <= 1e-10
+    probe = np.random.default_rng(3).normal(size=pre_m.U.shape[0])
+    assert _rel(pre_f.apply(probe), pre_m.apply(probe)) <= 1e-9
+    assert abs(res_f.cg_iterations - res_m.cg_iterations) <= 1
+    assert _rel(res_f.delta.data, res_m.delta.data) <= 1e-7

@@ -413,7 +413,10 @@ def run_ours(args, cfg):
         gf = (m * (m + 1) * n + m**3 / 3) / (g_avg + potrf_avg) / 1e12
         gram_chol = {"tflops": gf, "frac_of_fp64_peak": gf / fp64_peak,
                      "gram_ms": g_avg * 1e3, "potrf_ms": potrf_avg * 1e3,
-                     "gram_path": "syrk" if syrk_avg > 0 else "factored"}
+                     "gram_path": "syrk" if syrk_avg > 0 else "factored",
+                     "definition": "(m(m+1)n + m^3/3) / (t_gram + t_potrf), SURVEY 8(d); on the "
+                                   "factored path this is a J J^T-equivalent rate (the kernel "
+                                   "performs fewer FLOPs), so it can exceed the FP64 peak"}
     jfree = syrk_avg == 0 and gram_avg > 0
     gemv_bytes = None if jfree else 8 * m * n
     if jfree:

@@ -31,7 +31,10 @@ from .optimizer import (
     line_search,
     lm_damping,
     network_values,
+    primal_ga_correction,
+    primal_gn_solve,
     relative_l2_error,
+    timing_sweep,
 )
 from .params import ParameterLayout, ParameterVector
 from .problems import (

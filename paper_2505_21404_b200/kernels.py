@@ -86,6 +86,15 @@ def syrk(J: torch.Tensor, ncols: int | None = None, K: torch.Tensor | None = Non
     return K
 
 
+def transpose_pad(A: torch.Tensor) -> torch.Tensor:
+    """Row-major transpose of a 2-D view into a buffer with a 16-aligned pitch
+    (the TMA/GEMM operand layout)."""
+    rows, cols = A.shape
+    out = torch.zeros((cols, pad_ld(rows)), dtype=F64, device=A.device)
+    out[:, :rows].copy_(A.t())
+    return out
+
+
 def shift_copy(K: torch.Tensor, lam: float, L: torch.Tensor) -> torch.Tensor:
     call("dngd_shift_copy", ctx(), stream_handle(), ptr(K), K.shape[0], K.stride(0), float(lam),
          ptr(L), L.stride(0))

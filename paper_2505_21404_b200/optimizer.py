@@ -313,6 +313,92 @@ def dngd_minimize(residual_map: ResidualMap, theta, config: OptimizerConfig,
     return _dngd_loop(trace, lambda it: residual_map, theta, config, rng)
 
 
+# -- primal oracles and the primal/dual regime sweep -----------------
+
+
+def _normal_matrix_t(rmap, theta):
+    """J^T J (n x n) on the FP64 tensor cores: the SYRK of the transposed Jacobian."""
+    from . import kernels as K
+
+    J = rmap.jacobian_t(theta)
+    n = rmap.n
+    Jt = K.transpose_pad(J[:, :n])  # (n, m) row-major, 16-aligned pitch
+    return J, K.syrk(Jt, rmap.m)
+
+
+def primal_gn_solve(residual_map: ResidualMap, theta, g, points=None,
+                    lam: float = 1e-3) -> ParameterVector:
+    """Parameter-space damped Gauss-Newton step (J^T J + lam I) dtheta = -g
+    (optimizer.py:331-346): the small-n oracle and the n << m path, with the same
+    lam *= 10 retry ladder as the dual solve."""
+    from .solver import _chol_with_retries
+
+    if lam <= 0.0:
+        raise DomainError(f"damping must be positive, got {lam}")
+    rmap = residual_map if points is None else residual_map.rebind(points)
+    if not isinstance(theta, ParameterVector):
+        theta = ParameterVector(theta, rmap.layout)
+    g_t = rmap._vec_t(g.tensor if isinstance(g, ParameterVector) else g, rmap.n, "gradient")
+    _, JtJ = _normal_matrix_t(rmap, theta)
+    fac, _ = _chol_with_retries(JtJ, lam)
+    delta = fac.solve_((-g_t).contiguous())
+    return ParameterVector(delta, theta.layout)
+
+
+def primal_ga_correction(residual_map: ResidualMap, theta, v, points=None,
+                         lam: float = 1e-3) -> ParameterVector:
+    """Parameter-space geodesic acceleration (J^T J + lam I) a = -J^T f_vv
+    (optimizer.py:349-362)."""
+    from . import kernels as K
+    from .solver import _chol_with_retries
+
+    if lam <= 0.0:
+        raise DomainError(f"damping must be positive, got {lam}")
+    rmap = residual_map if points is None else residual_map.rebind(points)
+    if not isinstance(theta, ParameterVector):
+        theta = ParameterVector(theta, rmap.layout)
+    v_t = rmap._vec_t(v.tensor if isinstance(v, ParameterVector) else v, rmap.n, "direction")
+    f_vv = rmap.fvv_t(theta, v_t)
+    J, JtJ = _normal_matrix_t(rmap, theta)
+    fac, _ = _chol_with_retries(JtJ, lam)
+    rhs = K.gemv_t(J, f_vv, rmap.n, None, -1.0)
+    return ParameterVector(fac.solve_(rhs), theta.layout)
+
+
+def timing_sweep(grid, iterations: int = 3, lam: float = 1e-3, seed: int = 0) -> list:
+    """Mean per-step seconds of primal vs dual dense solves on random linear maps
+    (optimizer.py:482-519): Gram/normal-matrix assembly, Cholesky and recovery,
+    device-synchronised.  Only the relative ordering is meaningful."""
+    import torch
+
+    from .residuals import LinearResidualMap
+
+    rng = np.random.default_rng(seed)
+    rows = []
+    for m, n in grid:
+        A = rng.normal(size=(m, n)) / np.sqrt(n)
+        rmap = LinearResidualMap(A, rng.normal(size=m))
+        theta = ParameterVector(rng.normal(size=n), rmap.layout)
+        primal_times, dual_times = [], []
+        for _ in range(iterations):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            g = rmap.gradient_t(theta)
+            primal_gn_solve(rmap, theta, g, lam=lam)
+            torch.cuda.synchronize()
+            primal_times.append(time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            g = rmap.gradient_t(theta)
+            dense_dual_solve(rmap, theta, g, lam=lam, use_ga=False)
+            torch.cuda.synchronize()
+            dual_times.append(time.perf_counter() - t0)
+        primal_s = float(np.mean(primal_times))
+        dual_s = float(np.mean(dual_times))
+        rows.append({"m": m, "n": n, "primal_s": primal_s, "dual_s": dual_s,
+                     "winner": "dual" if dual_s < primal_s else "primal"})
+    return rows
+
+
 def relative_l2_error(u_pred, u_exact) -> float:
     """optimizer.py:465-477."""
     u_pred = np.asarray(u_pred, dtype=np.float64).reshape(-1)

@@ -384,3 +384,58 @@ def test_jfree_pcg_matches_materialized(P, pname, widths, counts):
     assert _rel(pre_f.apply(probe), pre_m.apply(probe)) <= 1e-9
     assert abs(res_f.cg_iterations - res_m.cg_iterations) <= 1
     assert _rel(res_f.delta.data, res_m.delta.data) <= 1e-7
+
+
+# -- primal oracles and the regime sweep (reference test_optimizer.py:293-329, 443-448) ----
+
+
+def test_primal_gn_identity_jacobian(P):
+    rmap = P.LinearResidualMap(np.eye(5), np.zeros(5))
+    theta = P.ParameterVector(np.zeros(5), rmap.layout)
+    g = np.arange(1.0, 6.0)
+    delta = P.primal_gn_solve(rmap, theta, g, lam=0.25)
+    np.testing.assert_allclose(delta.data, -g / 1.25, rtol=0, atol=1e-14)
+
+
+def test_primal_matches_dual_on_random_instances(P):
+    rng = np.random.default_rng(42)
+    for trial in range(20):
+        if trial % 2 == 0:
+            spec = P.MlpSpec((2, 6, 1), seed=trial)
+            x = rng.uniform(-1, 1, size=(12, 2))
+            rmap = P.RegressionResidualMap(spec, x, rng.normal(size=12))
+            theta = P.init_params(spec)
+        else:
+            A = rng.normal(size=(10, 7))
+            rmap = P.LinearResidualMap(A, rng.normal(size=10))
+            theta = P.ParameterVector(rng.normal(size=7), rmap.layout)
+        g = rmap.gradient(theta)
+        p = P.primal_gn_solve(rmap, theta, g, lam=1e-3).data
+        d = P.dense_dual_solve(rmap, theta, g, lam=1e-3, use_ga=False).delta.data
+        assert np.linalg.norm(p - d) <= 1e-8 * max(np.linalg.norm(d), 1e-30)
+
+
+def test_primal_ga_matches_dual_ga(P):
+    spec = P.MlpSpec((2, 8, 1), seed=5)
+    theta = P.init_params(spec)
+    rng = np.random.default_rng(6)
+    x = rng.uniform(-1.0, 1.0, size=(10, 2))
+    rmap = P.RegressionResidualMap(spec, x, rng.normal(size=10))
+    lam = 1e-2
+    g = rmap.gradient(theta)
+    plain = P.dense_dual_solve(rmap, theta, g, lam=lam, use_ga=False)
+    a = P.primal_ga_correction(rmap, theta, plain.delta, lam=lam).data
+    # dual GA correction a = -J^T (K + lam I)^-1 (-K f_vv)... recovered from the
+    # GA step: delta_ga = v + a/2 when the gate opens; compare through the oracle
+    J = rmap.jacobian(theta)
+    fvv = rmap.second_directional(theta, plain.delta.data)
+    ref = np.linalg.solve(J.T @ J + lam * np.eye(rmap.n), -(J.T @ fvv))
+    assert _rel(a, ref) <= 1e-8
+
+
+def test_timing_sweep_regime_winners(P):
+    rows = P.timing_sweep([(600, 40), (40, 600)], iterations=2)
+    assert [r["winner"] for r in rows] == ["primal", "dual"]
+    for r in rows:
+        assert r["primal_s"] > 0.0 and r["dual_s"] > 0.0
+        assert set(r) == {"m", "n", "primal_s", "dual_s", "winner"}

@@ -142,7 +142,11 @@ class PoissonSin(PdeProblem):
 
 
 def _points(colloc):
-    return {f"pts_{c.class_id}": c.points for c in colloc.classes}
+    out = {f"pts_{c.class_id}": c.points for c in colloc.classes}
+    for c in colloc.classes:
+        if "stde_idx" in c.aux:
+            out[f"idx_{c.class_id}"] = np.asarray(c.aux["stde_idx"])
+    return out
 
 
 def step_fixture(name, problem, widths, counts, seed, lams, store_J_rows=None, probes=3):
@@ -285,9 +289,23 @@ def main_allen_cahn():
                        7, 1e-3, 4)
 
 
+def main_stde():
+    """PoissonBallStde (problems.py:331-402): dirichlet_ball output transform and the
+    per-point random Laplacian index subsets, the reference's own problem class."""
+    from dngd.problems import PoissonBallStde
+
+    step_fixture("stde_step", PoissonBallStde(10, 3), (10, 16, 16, 1), {INTERIOR: 32}, 8,
+                 [1e-3])
+    trajectory_fixture("stde_traj", PoissonBallStde(10, 3), (10, 12, 12, 1), {INTERIOR: 40},
+                       9, 1e3, 3)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["allen_cahn"]:
         main_allen_cahn()
+    elif sys.argv[1:] == ["stde"]:
+        main_stde()
     else:
         main()
         main_allen_cahn()
+        main_stde()

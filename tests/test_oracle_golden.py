@@ -25,10 +25,13 @@ PROBLEMS = {
     "cfg2_step": (O.OracleHeat1d(), ("interior", "boundary", "initial")),
     "cfg3_step": (O.OraclePoissonSin(5), ("interior", "boundary")),
     "ac_step": (O.OracleAllenCahn(), ("interior", "initial")),
+    "stde_step": (O.OraclePoissonBallStde(10, 3), ("interior",)),
 }
 
 
 def _classes(fx, problem, ids):
+    if isinstance(problem, O.OraclePoissonBallStde):
+        return problem.classes(fx["pts_interior"], fx["idx_interior"])
     return problem.classes(*[fx[f"pts_{c}"] for c in ids])
 
 
@@ -95,6 +98,7 @@ TRAJ = {
     "cfg1_traj": (O.OraclePoisson2d(), (90, 30), O.LoopConfig(lam_cap=1e-3, max_iters=5)),
     "cfg2_traj": (O.OracleHeat1d(), (60, 20, 20), O.LoopConfig(lam_cap=1e-3, max_iters=4)),
     "ac_traj": (O.OracleAllenCahn(), (60, 20), O.LoopConfig(lam_cap=1e-3, max_iters=4)),
+    "stde_traj": (O.OraclePoissonBallStde(10, 3), (40,), O.LoopConfig(lam_cap=1e3, max_iters=3)),
     "pcg_traj": (O.OraclePoisson2d(), (60, 20),
                  O.LoopConfig(lam_cap=1e-3, max_iters=3, dense_threshold=10, nystrom_rank=16,
                               cg_max_iters=100)),

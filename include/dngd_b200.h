@@ -142,6 +142,11 @@ typedef struct {
   const double* f;                    /* device, N data values */
   double c3;                          /* cubic coefficient (Allen-Cahn reaction), 0 if linear */
   const double* inputs;               /* device, N x nch x widths[0], or NULL */
+  /* per-point operator (STDE, problems.py:331-402): derivative dims of the grad
+   * channels (N x ngrad int32) and channel coefficients (N x nch, replacing
+   * cu, cg[], cl; the class weight still applies); NULL = class-wide */
+  const int* grad_idx;
+  const double* coefs;
 } dngd_class_desc;
 
 /* scratch for one assembly / f_vv / loss_many(ncand) evaluation */

@@ -39,11 +39,13 @@ from .optimizer import (
 from .params import ParameterLayout, ParameterVector
 from .problems import (
     PROBLEMS,
+    AllenCahn,
     Heat,
     Heat1d,
     PdeProblem,
     Poisson2d,
     Poisson10d,
+    PoissonBallStde,
     PoissonSin,
     build_map,
     eval_residuals,

@@ -55,6 +55,8 @@ class ClassDesc(ctypes.Structure):
         ("f", c_vp),
         ("c3", c_dbl),
         ("inputs", c_vp),
+        ("grad_idx", c_vp),
+        ("coefs", c_vp),
     ]
 
 

@@ -78,7 +78,7 @@ __global__ void k_input_channels(Classes T, double* __restrict__ H0) {
     } else if (ch == 0) {
       v = C.pts[(p - C.row0) * T.din + d];
     } else if (ch <= C.ngrad) {
-      v = C.grad_dims[ch - 1] == d ? 1.0 : 0.0;
+      v = gdim(C, ch - 1, p - C.row0) == d ? 1.0 : 0.0;
     }
   }
   H0[idx] = v;

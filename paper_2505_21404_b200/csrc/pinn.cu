@@ -41,6 +41,8 @@ struct ClassDev {
   const double* pts;
   const double* f;
   const double* inp;   // embedded input channels (N x nch x din) or nullptr = identity
+  const int* pgi;      // per-point derivative dims (N x ngrad, STDE subsets) or nullptr
+  const double* pco;   // per-point channel coefficients (N x nch) or nullptr
 };
 
 struct Classes {
@@ -64,10 +66,20 @@ DNGD_DEV double coef(const ClassDev& C, int ch) {
   return C.cl;
 }
 
+// coefficient of channel ch at local point i (per-point coefficients when given)
+DNGD_DEV double coefp(const ClassDev& C, int ch, long long i) {
+  return C.pco ? C.pco[i * C.nch + ch] : coef(C, ch);
+}
+
+// input dimension of grad channel g (0-based) at local point i
+DNGD_DEV int gdim(const ClassDev& C, int g, long long i) {
+  return C.pgi ? C.pgi[i * C.ngrad + g] : C.grad_dims[g];
+}
+
 // adjoint seed of output channel ch at point p: d r_p / d u_ch (the value channel
 // picks up 3 c3 u^2 from the cubic term)
 DNGD_DEV double seedc(const Classes& T, const ClassDev& C, int ch, long long p) {
-  double cf = coef(C, ch);
+  double cf = coefp(C, ch, p - C.row0);
   if (ch == 0 && C.c3 != 0.0) {
     const double u = T.u0[p];
     cf = fma(3.0 * C.c3 * u, u, cf);
@@ -131,13 +143,13 @@ __global__ void k_input_fwd(Classes T, const double* __restrict__ theta, long lo
   H[base] = t;
   double G = 0.0;
   for (int g = 0; g < C.ngrad; ++g) {
-    const double dz = W0[C.grad_dims[g] * w1 + q];
+    const double dz = W0[gdim(C, g, i) * w1 + q];
     if (Z) Z[base + (1 + g) * ld] = dz;
     H[base + (1 + g) * ld] = s * dz;
   }
   if (C.nlap) {
     for (int l = 0; l < C.nlap; ++l) {
-      const double dz = W0[C.grad_dims[C.lap_ch[l] - 1] * w1 + q];
+      const double dz = W0[gdim(C, C.lap_ch[l] - 1, i) * w1 + q];
       G = fma(dz, dz, G);
     }
     if (Z) Z[base + (C.nch - 1) * ld] = 0.0;
@@ -194,7 +206,7 @@ __global__ void k_head(Classes T, const double* __restrict__ H, int w, long long
       u += bL;
       u0 = u;
     }
-    res = fma(coef(C, c), u, res);
+    res = fma(coefp(C, c, i), u, res);
   }
   if (C.c3 != 0.0) res = fma(C.c3 * u0 * u0, u0, res);
   if (lane == 0) {
@@ -258,13 +270,14 @@ __global__ void k_tanh_bwd(Classes T, const double* __restrict__ Z, const double
 // ------------------------------------------------------------------ J rows
 
 DNGD_DEV double hext(const ClassDev& C, int din, const double* __restrict__ xrow,
-                     const double* __restrict__ hrow, long long ld, int win, int c, int p) {
+                     const double* __restrict__ hrow, long long ld, int win, int c, int p,
+                     long long i) {
   if (p == win) return c == 0 ? 1.0 : 0.0;  // bias row
   if (hrow != nullptr) return hrow[c * ld + p];
   // input layer: embedded input channels, or x / e_j / 0 (identity)
   if (C.inp) return xrow[c * din + p];
   if (c == 0) return xrow[p];
-  if (c <= C.ngrad) return C.grad_dims[c - 1] == p ? 1.0 : 0.0;
+  if (c <= C.ngrad) return gdim(C, c - 1, i) == p ? 1.0 : 0.0;
   return 0.0;
 }
 
@@ -296,7 +309,7 @@ __global__ void __launch_bounds__(256) k_jwrite(Classes T, const double* __restr
       if (col + 1 < col_begin || col >= col_end) continue;
       double a0 = 0.0, a1 = 0.0;
       for (int c = 0; c < nch; ++c) {
-        const double h = hext(C, T.din, xrow, hrow, ldh, win, c, pp);
+        const double h = hext(C, T.din, xrow, hrow, ldh, win, c, pp, i);
         const double2 z = *reinterpret_cast<const double2*>(zrow + c * ldz + q);
         a0 = fma(h, z.x, a0);
         a1 = fma(h, z.y, a1);
@@ -317,7 +330,7 @@ __global__ void __launch_bounds__(256) k_jwrite(Classes T, const double* __restr
       const int q = static_cast<int>(e - static_cast<long long>(pp) * wout);
       double a = 0.0;
       for (int c = 0; c < nch; ++c) {
-        const double h = hext(C, T.din, xrow, hrow, ldh, win, c, pp);
+        const double h = hext(C, T.din, xrow, hrow, ldh, win, c, pp, i);
         const double z = zrow ? zrow[c * ldz + q] : seedc(T, C, c, p);
         a = fma(h, z, a);
       }
@@ -401,7 +414,7 @@ __global__ void k_fvv_input(Classes T, const double* __restrict__ theta,
   auto zget = [&](int ch) -> T2 {
     if (ch == 0) return {za, zb, 0.0};
     if (ch <= C.ngrad) {
-      const int d = C.grad_dims[ch - 1];
+      const int d = gdim(C, ch - 1, i);
       return {theta[d * w1 + q], v[d * w1 + q], 0.0};
     }
     return {0.0, 0.0, 0.0};
@@ -459,7 +472,7 @@ __global__ void k_fvv_head(Classes T, const double* __restrict__ H3, int w, long
         u = fma(h[blk + c * ld + q], WL[q], fma(h[c * ld + q], VL[q], u));
       u = warp_sum(u);
       if (c == 0) u += VL[w];
-      res = fma(coef(C, c), u, res);
+      res = fma(coefp(C, c, i), u, res);
     }
     if (C.c3 != 0.0) {  // d(c3 u^3) = 3 c3 u^2 u'
       double ua = 0.0, ub = 0.0;
@@ -479,7 +492,7 @@ __global__ void k_fvv_head(Classes T, const double* __restrict__ H3, int w, long
     for (int q = lane; q < w; q += 32)
       u = fma(h[2 * blk + c * ld + q], WL[q], fma(2.0 * h[blk + c * ld + q], VL[q], u));
     u = warp_sum(u);
-    res = fma(coef(C, c), u, res);
+    res = fma(coefp(C, c, i), u, res);
   }
   if (C.c3 != 0.0) {
     // (u^3)'' = 6 u u'^2 + 3 u^2 u'' on the value channel
@@ -611,6 +624,8 @@ static int make_plan(dngd_ctx* ctx, const dngd_mlp_desc* mlp, const dngd_class_d
     C.pts = d.points;
     C.f = d.f;
     C.inp = d.inputs;
+    C.pgi = d.grad_idx;
+    C.pco = d.coefs;
     if (C.inp == nullptr && C.pts == nullptr && d.count > 0) {
       return set_error(ctx, DNGD_ERR_DIMENSION, "pinn: class needs points or input channels");
     }
@@ -836,7 +851,7 @@ __global__ void k_jt_input(Classes T, const double* __restrict__ Zb, long long l
       const double zg = wi * Zb[(base + 1 + g) * ld + q];
 #pragma unroll
       for (int p = 0; p < MAXG; ++p)
-        if (p == C.grad_dims[g]) acc[p] += zg;
+        if (p == gdim(C, g, i - C.row0)) acc[p] += zg;
     }
   }
   double* dst = part + static_cast<long long>(blockIdx.y) * (din + 1) * w1;
@@ -1747,7 +1762,7 @@ static bool loss_fused_ok(const Plan& P) {
   for (int k = 1; k < P.L; ++k)
     if (P.w[k] > 64) return false;
   for (int c = 0; c < P.T.n; ++c)
-    if (P.T.c[c].nch > 8) return false;
+    if (P.T.c[c].nch > 8 || P.T.c[c].pgi || P.T.c[c].pco) return false;
   return P.T.din <= MAXG;
 }
 

@@ -412,11 +412,17 @@ def relative_l2_error(u_pred, u_exact) -> float:
 
 
 class _ValueProblem:
-    """u(x) - u*(x) as a one-class residual map: the rel-L2 metric on the device."""
+    """u(x) - u*(x) as a one-class residual map: the rel-L2 metric on the device.
+    Carries the problem's input embedding and output transform (model.py:133-277):
+    u = factor(x) * phi(embedding(x))."""
 
-    def __init__(self, dim, exact):
+    def __init__(self, dim, exact, problem=None):
         self.raw_dim = dim
         self.exact = exact
+        self.problem = problem
+        self.input_dim = getattr(problem, "input_dim", dim) if problem is not None else dim
+        if problem is not None and hasattr(problem, "value_factor"):
+            self.point_coefs = self._coefs
 
     def class_operator(self, class_id):
         from .problems import VALUE
@@ -425,6 +431,14 @@ class _ValueProblem:
 
     def class_data(self, cls):
         return self.exact
+
+    def input_channels(self, cls, op):
+        if self.problem is None or not hasattr(self.problem, "input_channels"):
+            return None
+        return self.problem.input_channels(cls, op)
+
+    def _coefs(self, cls, op):
+        return self.problem.value_factor(cls.points)[:, None]
 
 
 def _rel_l2_fn(problem, spec: MlpSpec):
@@ -436,7 +450,7 @@ def _rel_l2_fn(problem, spec: MlpSpec):
     pts = problem.eval_points()
     exact = problem.exact_solution(pts)
     denom = float(np.linalg.norm(exact))
-    vmap = PinnResidualMap(_ValueProblem(pts.shape[1], exact), spec,
+    vmap = PinnResidualMap(_ValueProblem(pts.shape[1], exact, problem), spec,
                            CollocationSet([CollocationClass(INTERIOR, pts, 1.0)]))
 
     def fn(theta):
@@ -453,7 +467,7 @@ def network_values(problem, spec: MlpSpec, theta, pts) -> np.ndarray:
     from .residuals import INTERIOR, CollocationClass, CollocationSet
 
     pts = np.asarray(pts, dtype=np.float64)
-    vmap = PinnResidualMap(_ValueProblem(pts.shape[1], np.zeros(pts.shape[0])), spec,
+    vmap = PinnResidualMap(_ValueProblem(pts.shape[1], np.zeros(pts.shape[0]), problem), spec,
                            CollocationSet([CollocationClass(INTERIOR, pts, 1.0)]))
     return vmap.residuals_t(theta).cpu().numpy()
 

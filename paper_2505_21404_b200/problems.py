@@ -69,6 +69,14 @@ def _parabolic_boundary(rng, n, d):
     return np.column_stack([t, x])
 
 
+def _ball_interior(rng, n, d):
+    """Uniform points in the open unit ball (problems.py:74-79)."""
+    z = rng.normal(size=(n, d))
+    z /= np.linalg.norm(z, axis=1, keepdims=True)
+    radius = rng.uniform(size=(n, 1)) ** (1.0 / d)
+    return z * radius
+
+
 def _halton(num: int, lows, highs) -> np.ndarray:
     from scipy.stats import qmc
 
@@ -401,6 +409,101 @@ class AllenCahn(PdeProblem):
         return _halton(num, [0.0, -1.0], [1.0, 1.0])
 
 
+class PoissonBallStde(PdeProblem):
+    """-Lap u = f on the unit ball in R^d, u = (1 - |x|^2) phi exactly zero on the
+    sphere (dirichlet_ball transform, model.py:181-199), Laplacians of the network
+    and of the exact solution estimated on one random k-subset of directions per
+    point (problems.py:331-402):
+        r = -(d/k) sum_{j in S} (d_jj u - d_jj u_ex),
+        d_jj[(1 - |x|^2) phi] = (1 - |x|^2) d_jj phi - 4 x_j d_j phi - 2 phi,
+    i.e. device channels (phi, d_j phi for j in S, sum_S d_jj phi) with per-point
+    derivative dims S and coefficients (2d, 4 (d/k) x_j, -(d/k)(1 - |x|^2))."""
+
+    name = "poisson_ball_stde"
+    default_lam_cap = 1e3
+    has_exact = True
+
+    def __init__(self, dim: int = 100, index_set_size: int = 8, coeff_seed: int = 1234):
+        self.dim = int(dim)
+        self.k = int(index_set_size)
+        if not 1 <= self.k <= self.dim:
+            raise DomainError(f"index set size {self.k} outside [1, {self.dim}]")
+        if self.k > 12:
+            raise DomainError("index set size above 12 exceeds the device channel limit")
+        self.raw_dim = self.dim
+        self.default_counts = {INTERIOR: 128}
+        self.default_widths = (self.dim, 64, 64, 1)
+        self.coeffs = np.random.default_rng(coeff_seed).normal(size=self.dim - 1)
+
+    def sample(self, counts, rng):
+        c = self.resolve_counts(counts)
+        n = c[INTERIOR]
+        pts = _ball_interior(rng, n, self.dim)
+        idx = rng.random((n, self.dim)).argsort(axis=1)[:, : self.k]
+        return CollocationSet([_cls(INTERIOR, pts, {"stde_idx": idx})])
+
+    def class_operator(self, class_id):
+        dims = tuple(range(self.k))  # placeholders: the dims are per point
+        return ClassOperator(grad_dims=dims, cg=(0.0,) * self.k, lap_dims=dims, cl=0.0)
+
+    def point_grad_dims(self, cls):
+        return np.asarray(cls.aux["stde_idx"], dtype=np.int32)
+
+    def point_coefs(self, cls, op):
+        d, k = self.dim, self.k
+        x = cls.points
+        idx = np.asarray(cls.aux["stde_idx"])
+        rows = np.arange(x.shape[0])
+        co = np.empty((x.shape[0], k + 2))
+        co[:, 0] = 2.0 * d
+        for g in range(k):
+            co[:, 1 + g] = 4.0 * (d / k) * x[rows, idx[:, g]]
+        co[:, k + 1] = -(d / k) * (1.0 - np.sum(x * x, axis=1))
+        return co
+
+    def _F(self, x):
+        c = self.coeffs
+        return np.sum(c * (np.sin(x[:, :-1] + np.cos(x[:, 1:])) + x[:, 1:] * np.cos(x[:, :-1])),
+                      axis=1)
+
+    def _exact_dd(self, x, j):
+        """d^2/dx_j^2 of the exact solution, per point direction j (product rule)."""
+        c, d = self.coeffs, self.dim
+        rows = np.arange(x.shape[0])
+        xj = x[rows, j]
+        F = self._F(x)
+        m1 = j < d - 1
+        jj = np.where(m1, j, 0)
+        xn = x[rows, np.minimum(j + 1, d - 1)]
+        a = xj + np.cos(xn)
+        dF = np.where(m1, c[jj] * (np.cos(a) - xn * np.sin(xj)), 0.0)
+        ddF = np.where(m1, c[jj] * (-np.sin(a) - xn * np.cos(xj)), 0.0)
+        m2 = j > 0
+        jm = np.where(m2, j - 1, 0)
+        xp = x[rows, np.maximum(j - 1, 0)]
+        b = xp + np.cos(xj)
+        dF = dF + np.where(m2, c[jm] * (-np.cos(b) * np.sin(xj) + np.cos(xp)), 0.0)
+        ddF = ddF + np.where(m2, c[jm] * (-np.sin(b) * np.sin(xj) ** 2 - np.cos(b) * np.cos(xj)),
+                             0.0)
+        s = 1.0 - np.sum(x * x, axis=1)
+        return s * ddF - 4.0 * xj * dF - 2.0 * F
+
+    def class_data(self, cls):
+        idx = np.asarray(cls.aux["stde_idx"])
+        lap_ex = sum(self._exact_dd(cls.points, idx[:, g]) for g in range(self.k))
+        return -(self.dim / self.k) * lap_ex
+
+    def value_factor(self, pts):
+        """u = (1 - |x|^2) phi on evaluation points."""
+        return 1.0 - np.sum(pts * pts, axis=1)
+
+    def exact_solution(self, pts):
+        return (1.0 - np.sum(pts * pts, axis=1)) * self._F(pts)
+
+    def eval_points(self, num=10_000):
+        return _ball_interior(np.random.default_rng(0), num, self.dim)
+
+
 PROBLEMS = {
     "poisson2d": Poisson2d,
     "poisson10d": Poisson10d,
@@ -409,9 +512,10 @@ PROBLEMS = {
     "heat1d": Heat1d,
     "poisson5d_sin": lambda: PoissonSin(5),
     "allen_cahn": AllenCahn,
+    "poisson_ball_stde": PoissonBallStde,
 }
 
-UNSUPPORTED = {"poisson_ball_stde"}
+UNSUPPORTED: set = set()
 
 
 def make_problem(name: str, **kwargs) -> PdeProblem:

@@ -462,6 +462,20 @@ class PinnResidualMap(ResidualMap):
                 inp = torch.as_tensor(emb, device=dev)
                 keep.append(inp)
                 d.inputs = inp.data_ptr()
+            if hasattr(self.problem, "point_grad_dims"):  # per-point derivative dims (STDE)
+                gi = np.ascontiguousarray(self.problem.point_grad_dims(cls), dtype=np.int32)
+                if gi.shape != (cls.count, d.ngrad):
+                    raise DimensionError(f"point derivative dims of class {cls.class_id}: {gi.shape}")
+                gi_t = torch.as_tensor(gi, device=dev)
+                keep.append(gi_t)
+                d.grad_idx = gi_t.data_ptr()
+            if hasattr(self.problem, "point_coefs"):  # per-point coefficients
+                co = np.ascontiguousarray(self.problem.point_coefs(cls, op), dtype=np.float64)
+                if co.shape != (cls.count, 1 + d.ngrad + (1 if d.nlap else 0)):
+                    raise DimensionError(f"point coefficients of class {cls.class_id}: {co.shape}")
+                co_t = torch.as_tensor(co, device=dev)
+                keep.append(co_t)
+                d.coefs = co_t.data_ptr()
         mlp = K.mlp_desc(self.spec.layer_widths)
         ws_bytes = K.pinn_workspace_bytes(mlp, arr, len(classes), 1)
         # line-search activations grow linearly with the candidate count

@@ -37,4 +37,12 @@ def class_descs(classes):
             inp = dev(c.inputs)
             keep.append(inp)
             d.inputs = inp.data_ptr()
+        if getattr(c, "pgrad", None) is not None:
+            gi = torch.as_tensor(np.ascontiguousarray(c.pgrad, dtype=np.int32), device="cuda")
+            keep.append(gi)
+            d.grad_idx = gi.data_ptr()
+        if getattr(c, "pcoef", None) is not None:
+            co = dev(c.pcoef)
+            keep.append(co)
+            d.coefs = co.data_ptr()
     return arr, keep

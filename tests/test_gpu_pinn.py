@@ -16,6 +16,9 @@ CASES = [
     # reference Allen-Cahn: periodic input embedding + cubic reaction term
     ("allen_cahn", O.OracleAllenCahn(), (3, 32, 32, 32, 1), (60, 20)),
     ("allen_cahn_wide", O.OracleAllenCahn(), (3, 160, 96, 1), (30, 10)),
+    # reference PoissonBallStde: per-point derivative subsets + per-point coefficients
+    ("stde", O.OraclePoissonBallStde(10, 3), (10, 16, 16, 1), (40,)),
+    ("stde_wide", O.OraclePoissonBallStde(10, 6), (10, 160, 96, 1), (24,)),
 ]
 
 

@@ -36,14 +36,24 @@ STEP = {
     "cfg2_step": ("heat1d", ("interior", "boundary", "initial"), O.OracleHeat1d()),
     "cfg3_step": ("poisson5d_sin", ("interior", "boundary"), O.OraclePoissonSin(5)),
     "ac_step": ("allen_cahn", ("interior", "initial"), O.OracleAllenCahn()),
+    "stde_step": ("poisson_ball_stde", ("interior",), O.OraclePoissonBallStde(10, 3)),
 }
+
+PROBLEM_KW = {"poisson_ball_stde": dict(dim=10, index_set_size=3)}
+
+
+def _oclasses(oprob, fx, ids):
+    if isinstance(oprob, O.OraclePoissonBallStde):
+        return oprob.classes(fx["pts_interior"], fx["idx_interior"])
+    return oprob.classes(*[fx[f"pts_{c}"] for c in ids])
 
 
 def _map(P, fx, problem_name, ids):
-    problem = P.make_problem(problem_name)
+    problem = P.make_problem(problem_name, **PROBLEM_KW.get(problem_name, {}))
     widths = tuple(int(w) for w in fx["widths"])
     spec = P.MlpSpec(widths)
-    classes = [P.CollocationClass(c, fx[f"pts_{c}"], 1.0 / np.sqrt(len(fx[f"pts_{c}"])))
+    classes = [P.CollocationClass(c, fx[f"pts_{c}"], 1.0 / np.sqrt(len(fx[f"pts_{c}"])),
+                                  {"stde_idx": fx[f"idx_{c}"]} if f"idx_{c}" in fx else {})
                for c in ids]
     rmap = P.PinnResidualMap(problem, spec, P.CollocationSet(classes))
     theta = P.ParameterVector(fx["theta"], spec.layout())
@@ -67,7 +77,7 @@ def test_dense_step_matches_reference(P, golden_dir, name):
     for p, ref in zip(fx["probe_n"], fx["fvv_probe"]):
         assert _rel(rmap.second_directional(theta, p), ref) <= 1e-10
     # oracle floors at this step
-    oclasses = oprob.classes(*[fx[f"pts_{c}"] for c in ids])
+    oclasses = _oclasses(oprob, fx, ids)
     _, Jo = O.linearize(fx["theta"], widths, oclasses)
     fvv_fn = lambda v: O.second_directional(fx["theta"], widths, oclasses, v)
     # measured J discrepancy GPU vs reference (enters the floor meter)
@@ -109,7 +119,7 @@ def test_gram_modes_match_reference(P, golden_dir, name, mode):
     _, g = rmap.residuals_and_gradient(theta)
     lam = float(fx["lams"][0])
     res = P.dense_dual_solve(rmap, theta, g, lam=lam, use_ga=False)
-    oclasses = oprob.classes(*[fx[f"pts_{c}"] for c in ids])
+    oclasses = _oclasses(oprob, fx, ids)
     _, Jo = O.linearize(fx["theta"], widths, oclasses)
     fl = O.direction_floors(Jo, fx["g"], lam)
     assert _rel(res.delta.data, fx["v_0"]) <= max(1e-8, 10 * fl["v"])
@@ -119,6 +129,7 @@ TRAJ = {
     "cfg1_traj": ("poisson2d", (90, 30), dict(lam_cap=1e-3)),
     "cfg2_traj": ("heat1d", (60, 20, 20), dict(lam_cap=1e-3)),
     "ac_traj": ("allen_cahn", (60, 20), dict(lam_cap=1e-3)),
+    "stde_traj": ("poisson_ball_stde", (40,), dict(lam_cap=1e3)),
     "pcg_traj": ("poisson2d", (60, 20),
                  dict(lam_cap=1e-3, dense_threshold=10, nystrom_rank=16, cg_max_iters=100)),
 }
@@ -131,8 +142,8 @@ def test_trajectory_matches_reference(P, golden_dir, name):
     widths = tuple(int(w) for w in fx["widths"])
     n_steps = len(fx["loss"]) - 1
     config = P.OptimizerConfig(max_iters=n_steps, deterministic_timing=True, **cfg)
-    trace = P.dngd_run(P.make_problem(pname), P.MlpSpec(widths), config, int(fx["seed"]),
-                       counts=counts, init="xavier_normal")
+    trace = P.dngd_run(P.make_problem(pname, **PROBLEM_KW.get(pname, {})), P.MlpSpec(widths),
+                       config, int(fx["seed"]), counts=counts, init="xavier_normal")
     assert not trace.aborted, trace.abort_reason
     loss = np.array([r.loss for r in trace.rows])
     np.testing.assert_allclose(loss, fx["loss"], rtol=1e-6)
@@ -315,7 +326,7 @@ def test_jfree_step_matches_materialized(P, golden_dir, name):
     for i, lam in enumerate(fx["lams"]):
         res_free = P.dense_dual_solve(rmap, theta, None, lam=lam, use_ga=True)
         ref = fx[f"delta_{i}"]
-        oclasses = oprob.classes(*[fx[f"pts_{c}"] for c in ids])
+        oclasses = _oclasses(oprob, fx, ids)
         _, Jo = O.linearize(fx["theta"], widths, oclasses)
         fl = O.direction_floors(Jo, fx["g"], lam,
                                 lambda v: O.second_directional(fx["theta"], widths, oclasses, v))

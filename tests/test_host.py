@@ -37,7 +37,7 @@ def test_ctypes_struct_layout_matches_header():
     from paper_2505_21404_b200 import _lib
 
     # int64 count, 2 ints, 12 ints, 12 ints, 12 doubles, 3 doubles, 2 pointers
-    assert ctypes.sizeof(_lib.ClassDesc) == 8 + 8 + 48 + 48 + 96 + 24 + 16 + 16
+    assert ctypes.sizeof(_lib.ClassDesc) == 8 + 8 + 48 + 48 + 96 + 24 + 16 + 16 + 16
     assert ctypes.sizeof(_lib.MlpDesc) == 4 * 10
 
 
@@ -152,12 +152,33 @@ def test_param_layout_and_counts():
     assert np.array_equal(init_params(spec).data, O.glorot_uniform_init((2, 8, 1), 3))
 
 
-def test_unsupported_problems_fail_loudly():
+def test_unknown_problems_fail_loudly():
     from paper_2505_21404_b200 import DomainError, make_problem
 
-    for name in ("poisson_ball_stde",):
+    for name in ("not_a_problem", "poisson3d"):
         with pytest.raises(DomainError):
             make_problem(name)
+    with pytest.raises(DomainError):
+        make_problem("poisson_ball_stde", dim=10, index_set_size=20)
+
+
+def test_stde_plugin_matches_oracle():
+    """Host side of PoissonBallStde (problems.py:331-402): sampling order, per-point
+    derivative subsets and coefficients, estimator data term, exact solution."""
+    from paper_2505_21404_b200 import make_problem
+
+    prob = make_problem("poisson_ball_stde", dim=10, index_set_size=3)
+    oprob = O.OraclePoissonBallStde(10, 3)
+    colloc = prob.sample((25,), np.random.default_rng(7))
+    (oc,) = oprob.sample((25,), np.random.default_rng(7))
+    (cls,) = colloc.classes
+    assert np.array_equal(cls.points, oc.points)
+    op = prob.class_operator(cls.class_id)
+    assert np.array_equal(prob.point_grad_dims(cls), oc.pgrad)
+    np.testing.assert_allclose(prob.point_coefs(cls, op), oc.pcoef, rtol=0, atol=0)
+    np.testing.assert_allclose(prob.class_data(cls), oc.f, rtol=1e-14, atol=1e-14)
+    pts = prob.eval_points(50)
+    np.testing.assert_allclose(prob.exact_solution(pts), oprob.exact(pts), rtol=1e-14)
 
 
 def test_allen_cahn_plugin_matches_oracle():

@@ -53,6 +53,13 @@ CONFIGS = {
     # (periodic embedding + cubic reaction) at its default collocation counts
     6: dict(problem="allen_cahn", widths=(3, 32, 32, 32, 1), counts=(1125, 225), lam_cap=1e-5,
             dense_threshold=4000, name="ref_allen_cahn_3-32x3-1_m1350"),
+    # not a BASELINE config: the paper's STDE case -- 100000-D
+    # Poisson on the ball, [100000, 128x4, 1] (n = 12.85M), m = 100, k = 8 directions
+    7: dict(problem="poisson_ball_stde", problem_kw=dict(dim=100000, index_set_size=8),
+            widths=(100000, 128, 128, 128, 128, 1), counts=(100,), lam_cap=1e3,
+            dense_threshold=4000, name="paper_stde_100000-128x4-1_m100_n12.85M",
+            no_cpu="numpy oracle would hold a 10 GB Jacobian plus per-sample einsum "
+                   "temporaries of the same size; not run on the host"),
 }
 METRIC = "D-NGD steps/s"
 UNIT = "steps/s"
@@ -195,7 +202,7 @@ def run_ours(args, cfg):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    problem = P.make_problem(cfg["problem"])
+    problem = P.make_problem(cfg["problem"], **cfg.get("problem_kw", {}))
     spec = P.MlpSpec(cfg["widths"], seed=0)
     config = P.OptimizerConfig(max_iters=args.warmup + args.steps, lam_cap=cfg["lam_cap"],
                                dense_threshold=cfg["dense_threshold"],
@@ -460,7 +467,9 @@ def run_ours(args, cfg):
         "final_loss": float(0.5 * float(maps[-1].residuals_t(theta).norm().item() ** 2)),
     }
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
-        line["cpu_baseline"] = cpu_baseline(cfg, max_seconds=args.cpu_seconds)
+        line["cpu_baseline"] = (cpu_baseline(cfg, max_seconds=args.cpu_seconds)
+                                if not cfg.get("no_cpu") else
+                                {"value": None, "unavailable": cfg["no_cpu"]})
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -407,7 +407,9 @@ int syrk_plan(dngd_ctx* ctx, long long m, long long ncols, int* splits, long lon
     return static_cast<double>(units) / static_cast<double>(waves * conc);
   };
   int best = 1;
-  for (int S = 2; S <= 64; ++S) {
+  // up to two waves of splits: a tiny m (few tiles) over a huge K (the STDE case,
+  // m = 100, n = 12.85M) needs every SM on the K reduction
+  for (int S = 2; S <= 2 * conc; ++S) {
     if ((kc_total + S - 1) / S < 8) break;  // keep >= 128 columns of K per unit
     if (eff(S) > eff(best) + 0.03) best = S;
   }

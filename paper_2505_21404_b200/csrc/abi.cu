@@ -56,6 +56,16 @@ extern "C" int dngd_ctx_create(int device, dngd_ctx** out) {
     return DNGD_ERR_CUDA;
   }
   ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  e = cudaMalloc(&ctx->dot_part, (dngd::kDotBlocks + 2) * sizeof(double));
+  if (e == cudaSuccess) {
+    ctx->dot_counter = reinterpret_cast<unsigned*>(ctx->dot_part + dngd::kDotBlocks);
+    e = cudaMemset(ctx->dot_counter, 0, 2 * sizeof(double));
+  }
+  if (e != cudaSuccess) {
+    if (ctx->dot_part) cudaFree(ctx->dot_part);
+    delete ctx;
+    return DNGD_ERR_CUDA;
+  }
   *out = ctx;
   return DNGD_OK;
 }
@@ -69,6 +79,7 @@ extern "C" int dngd_ctx_destroy(dngd_ctx* ctx) {
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->hi) cudaStreamDestroy(ctx->hi);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->dot_part) cudaFree(ctx->dot_part);
   }
   delete ctx;
   return DNGD_OK;

@@ -157,6 +157,36 @@ __global__ void __launch_bounds__(1024) k_dot(long long n, const double* __restr
   if (threadIdx.x == 0) *out = s;
 }
 
+// large n: kDotBlocks contiguous chunks, one partial per CTA, the last CTA to
+// arrive sums the partials in index order (deterministic, one launch)
+__global__ void __launch_bounds__(512) k_dot_multi(long long n, const double* __restrict__ x,
+                                                     const double* __restrict__ y,
+                                                     double* __restrict__ part,
+                                                     unsigned* __restrict__ counter,
+                                                     double* __restrict__ out) {
+  __shared__ double sh[32];
+  __shared__ bool last;
+  const long long chunk = (n + kDotBlocks - 1) / kDotBlocks;
+  const long long k0 = blockIdx.x * chunk, k1 = min(n, k0 + chunk);
+  double s = 0.0;
+  for (long long k = k0 + threadIdx.x; k < k1; k += 512) s = fma(x[k], y[k], s);
+  s = block_sum<512>(s, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = threadIdx.x < kDotBlocks ? __ldcg(part + threadIdx.x) : 0.0;
+  t = block_sum<512>(t, sh);
+  if (threadIdx.x == 0) {
+    *out = t;
+    *counter = 0u;
+  }
+}
+
 __global__ void k_axpby(long long n, double a, const double* __restrict__ x, double b,
                         const double* __restrict__ y, double* __restrict__ out) {
   const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -226,7 +256,12 @@ extern "C" int dngd_gemv_n(dngd_ctx* ctx, void* stream, const double* A, int64_t
 
 extern "C" int dngd_dot(dngd_ctx* ctx, void* stream, int64_t n, const double* x, const double* y,
                         double* out_dev) {
-  k_dot<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(n, x, y, out_dev);
+  if (n >= (1LL << 18)) {
+    k_dot_multi<<<kDotBlocks, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+        n, x, y, ctx->dot_part, ctx->dot_counter, out_dev);
+  } else {
+    k_dot<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(n, x, y, out_dev);
+  }
   return cuda_status(ctx, cudaGetLastError(), "dot");
 }
 

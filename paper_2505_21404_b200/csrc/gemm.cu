@@ -311,8 +311,18 @@ __global__ void k_splitk_reduce(const double* __restrict__ partial, int splits, 
   const long long r = static_cast<long long>(tm) * 128 + off / 128;
   const long long c = static_cast<long long>(tn) * 128 + off % 128;
   if (r >= M || c >= N) return;
+  const double* src = partial + static_cast<long long>(t) * tile_elems + off;
+  const long long sstride = static_cast<long long>(ntiles) * tile_elems;
   double v = 0.0;
-  for (int s = 0; s < splits; ++s) v += partial[(static_cast<long long>(s) * ntiles + t) * tile_elems + off];
+  int s = 0;
+  for (; s + 8 <= splits; s += 8) {  // loads issued ahead of the in-order sum
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = __ldcs(src + (s + u) * sstride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v += a[u];
+  }
+  for (; s < splits; ++s) v += __ldcs(src + s * sstride);
   double* cp = C + r * ldc + c;
   *cp = alpha * v + (beta != 0.0 ? beta * *cp : 0.0);
 }
@@ -325,7 +335,7 @@ size_t gemm_splitk_bytes(long long M, long long N, int splits) {
 int gemm_splitk_choose(dngd_ctx* ctx, long long M, long long N, long long K) {
   const long long tiles = ((M + 127) / 128) * ((N + 127) / 128);
   long long s = (2LL * ctx->num_sms + tiles - 1) / tiles;
-  s = std::min(s, std::max(1LL, ((K + 15) / 16) / 16));  // >= 256 columns of K per split
+  s = std::min(s, std::max(1LL, ((K + 15) / 16) / 4));  // >= 64 columns of K per split
   return static_cast<int>(std::max(1LL, std::min(s, 64LL)));
 }
 
@@ -355,44 +365,49 @@ int gemm_nt_splitk(dngd_ctx* ctx, cudaStream_t s, const GemmCall& g0, int splits
 constexpr int kSyrkTile = 128;
 
 // Sum split partials in fixed order and write the full symmetric K.
-// Each CTA owns one 32x32 sub-block of a lower tile; the transposed copy goes
-// through shared memory so both writes are coalesced.
+// Each CTA owns one 16x16 sub-block of a lower tile (64 per tile: a single-tile K,
+// the STDE case, still spreads over the SMs); loads of consecutive splits are
+// issued ahead of the in-order sum.  The transposed copy goes through shared
+// memory so both writes are coalesced.
 __global__ void __launch_bounds__(256) k_syrk_reduce(const double* __restrict__ partial,
                                                        int splits, int ntiles, long long m,
                                                        double* __restrict__ K, long long ldK,
                                                        int accumulate) {
-  __shared__ double sh[32][33];
-  const int t = blockIdx.x >> 4;
-  const int sub = blockIdx.x & 15;
+  __shared__ double sh[16][17];
+  const int t = blockIdx.x >> 6;
+  const int sub = blockIdx.x & 63;
   int ti, tj;
   decode_lower(t, ti, tj);
-  const int sr = sub >> 2, sc = sub & 3;
+  const int sr = sub >> 3, sc = sub & 7;
   if (ti == tj && sc > sr) return;  // above the diagonal of a diagonal tile
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const long long r0 = static_cast<long long>(ti) * kSyrkTile + sr * 32;
-  const long long c0 = static_cast<long long>(tj) * kSyrkTile + sc * 32;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const long long r0 = static_cast<long long>(ti) * kSyrkTile + sr * 16;
+  const long long c0 = static_cast<long long>(tj) * kSyrkTile + sc * 16;
+  if (r0 >= m || c0 >= m) return;
   const long long tile_elems = kSyrkTile * kSyrkTile;
+  const double* src = partial + static_cast<long long>(t) * tile_elems +
+                      (sr * 16 + ty) * kSyrkTile + sc * 16 + tx;
+  const long long sstride = static_cast<long long>(ntiles) * tile_elems;
+  double v = 0.0;
+  int s = 0;
+  for (; s + 8 <= splits; s += 8) {
+    double a[8];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int lr = ty + 8 * k;
-    const long long r = r0 + lr, c = c0 + tx;
-    const long long off = (sr * 32 + lr) * kSyrkTile + sc * 32 + tx;
-    double v = 0.0;
-    for (int s = 0; s < splits; ++s) v += partial[(static_cast<long long>(s) * ntiles + t) * tile_elems + off];
-    if (r < m && c < m && c <= r) {
-      if (accumulate) v += K[r * ldK + c];
-      K[r * ldK + c] = v;
-    }
-    sh[lr][tx] = v;
+    for (int u = 0; u < 8; ++u) a[u] = __ldcs(src + (s + u) * sstride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v += a[u];
   }
+  for (; s < splits; ++s) v += __ldcs(src + s * sstride);
+  const long long r = r0 + ty, c = c0 + tx;
+  if (r < m && c < m && c <= r) {
+    if (accumulate) v += K[r * ldK + c];
+    K[r * ldK + c] = v;
+  }
+  sh[ty][tx] = v;
   __syncthreads();
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int lc = ty + 8 * k;  // column of the sub-block -> row of the transpose
-    const long long r = c0 + lc, c = r0 + tx;
-    // upper element K[c0+lc][r0+tx] mirrors lower element (r0+tx, c0+lc)
-    if (r < m && c < m && r < c) K[r * ldK + c] = sh[tx][lc];
-  }
+  // upper element K[c0+ty][r0+tx] mirrors lower element (r0+tx, c0+ty)
+  const long long ru = c0 + ty, cu = r0 + tx;
+  if (ru < m && cu < m && ru < cu) K[ru * ldK + cu] = sh[tx][ty];
 }
 
 int syrk_plan(dngd_ctx* ctx, long long m, long long ncols, int* splits, long long* ntiles,
@@ -447,7 +462,7 @@ int syrk(dngd_ctx* ctx, cudaStream_t s, const double* J, long long m, long long 
     int rc = launch_gemm<128, 128, 2, 4, 5>(ctx, s, g);
     if (rc) return rc;
   }
-  k_syrk_reduce<<<static_cast<unsigned>(nt * 16), 256, 0, s>>>(
+  k_syrk_reduce<<<static_cast<unsigned>(nt * 64), 256, 0, s>>>(
       static_cast<const double*>(work), S, static_cast<int>(nt), m, K, ldK, accumulate);
   return cuda_status(ctx, cudaGetLastError(), "syrk reduce");
 }

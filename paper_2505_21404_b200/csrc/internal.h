@@ -20,9 +20,15 @@ struct dngd_ctx {
   cudaEvent_t ev_join = nullptr;
   CUtensorMap potrf_mapS, potrf_mapP;  // panel-load boxes over L (encoded per dngd_potrf call)
   cudaEvent_t ev_panel = nullptr, ev_update = nullptr, ev_update2 = nullptr, ev_fork = nullptr;
+  // multi-CTA dot products: per-CTA partials + arrival counter (calls on one context
+  // are stream-ordered; the counter is reset by the last CTA)
+  double* dot_part = nullptr;
+  unsigned* dot_counter = nullptr;
 };
 
 namespace dngd {
+
+constexpr int kDotBlocks = 256;  // fixed CTA count: the summation order is device independent
 
 int set_error(dngd_ctx* ctx, int code, const std::string& msg);
 int cuda_status(dngd_ctx* ctx, cudaError_t e, const char* where);

@@ -93,9 +93,14 @@ static inline long long ldw(long long w) { return (w + 3) / 4 * 4; }
 
 // input layer (K = din is tiny): z = x W0 + b0, d_j z = W0[j,:], Lap z = 0; then tanh channels.
 // grid.y = candidate (theta stride th_s, activation stride act_s).
+// Zx (optional, large din): precomputed x W0 rows (ld ldx); with Dx the candidate's
+// value is Zx + eta_c Dx (x (W0 + eta V0) by linearity) -- see input_gemm.
 __global__ void k_input_fwd(Classes T, const double* __restrict__ theta, long long th_s, int w1,
                             long long ld, double* __restrict__ Z, double* __restrict__ H,
-                            long long act_s) {
+                            long long act_s, const double* __restrict__ Zx,
+                            const double* __restrict__ Dx, const double* __restrict__ etas,
+                            long long ldx, const double* __restrict__ W0b,
+                            const double* __restrict__ V0b) {
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= T.m * w1) return;
   const long long p = idx / w1;
@@ -135,21 +140,34 @@ __global__ void k_input_fwd(Classes T, const double* __restrict__ theta, long lo
     }
     return;
   }
-  const double* x = C.pts + i * T.din;
-  double z = b0[q];
-  for (int j = 0; j < T.din; ++j) z = fma(x[j], W0[j * w1 + q], z);
+  double z;
+  if (Zx) {
+    z = Zx[p * ldx + q];
+    if (Dx) z = fma(etas[blockIdx.y], Dx[p * ldx + q], z);
+    z += b0[q];
+  } else {
+    const double* x = C.pts + i * T.din;
+    z = b0[q];
+    for (int j = 0; j < T.din; ++j) z = fma(x[j], W0[j * w1 + q], z);
+  }
   const double t = tanh(z), s = 1.0 - t * t;
   if (Z) Z[base] = z;
   H[base] = t;
+  // with Dx the candidates' W0 rows were not materialised: W0 + eta V0 on the fly
+  // (the same fma as k_candidates)
+  auto w0 = [&](int d) {
+    const long long e = static_cast<long long>(d) * w1 + q;
+    return Dx ? fma(etas[blockIdx.y], V0b[e], W0b[e]) : W0[e];
+  };
   double G = 0.0;
   for (int g = 0; g < C.ngrad; ++g) {
-    const double dz = W0[gdim(C, g, i) * w1 + q];
+    const double dz = w0(gdim(C, g, i));
     if (Z) Z[base + (1 + g) * ld] = dz;
     H[base + (1 + g) * ld] = s * dz;
   }
   if (C.nlap) {
     for (int l = 0; l < C.nlap; ++l) {
-      const double dz = W0[gdim(C, C.lap_ch[l] - 1, i) * w1 + q];
+      const double dz = w0(gdim(C, C.lap_ch[l] - 1, i));
       G = fma(dz, dz, G);
     }
     if (Z) Z[base + (C.nch - 1) * ld] = 0.0;
@@ -339,6 +357,276 @@ __global__ void __launch_bounds__(256) k_jwrite(Classes T, const double* __restr
   }
 }
 
+// Input-layer block of J for identity inputs (hext = x_j, e_{gdim}, 0, bias 1):
+// one product per element plus a fix-up on the <= ngrad rows j that are
+// derivative dims, found through a sorted list walked alongside the thread's
+// (monotone) j.  Same arithmetic as k_jwrite<true> for layer 0; it exists for the
+// STDE case (din ~ 1e5, J's input block is ~all of J).
+__global__ void __launch_bounds__(256) k_jwrite_in(Classes T, const double* __restrict__ Zb,
+                                                     long long ldz, int wout, long long col_begin,
+                                                     long long col_end, double* __restrict__ J,
+                                                     long long ldJ) {
+  __shared__ int sdim[MAXG], sch[MAXG];
+  const long long p = blockIdx.y;
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long i = p - C.row0;
+  const int din = T.din, ng = C.ngrad;
+  if (threadIdx.x == 0) {  // stable insertion sort of (dim, channel) by dim
+    for (int g = 0; g < ng; ++g) {
+      const int d = gdim(C, g, i);
+      int t = g;
+      while (t > 0 && sdim[t - 1] > d) {
+        sdim[t] = sdim[t - 1];
+        sch[t] = sch[t - 1];
+        --t;
+      }
+      sdim[t] = d;
+      sch[t] = 1 + g;
+    }
+  }
+  __syncthreads();
+  const double* xrow = C.pts + i * din;
+  const double* zrow = Zb + (C.act0 + i * C.nch) * ldz;
+  double* Jrow = J + p * ldJ - col_begin;
+  const int half = wout / 2;
+  const long long pairs = (din + 1LL) * half;
+  int idx = 0;
+  for (long long e2 = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x; e2 < pairs;
+       e2 += static_cast<long long>(gridDim.x) * 256) {
+    const int j = static_cast<int>(e2 / half);
+    const int q = 2 * static_cast<int>(e2 - static_cast<long long>(j) * half);
+    const long long col = 2 * e2;
+    if (col + 1 < col_begin || col >= col_end) continue;
+    const double2 z0 = __ldg(reinterpret_cast<const double2*>(zrow + q));
+    double a0, a1;
+    if (j == din) {
+      a0 = z0.x;
+      a1 = z0.y;
+    } else {
+      const double xj = __ldg(xrow + j);
+      a0 = xj * z0.x;
+      a1 = xj * z0.y;
+      while (idx < ng && sdim[idx] < j) ++idx;
+      for (int t = idx; t < ng && sdim[t] == j; ++t) {
+        const double2 zg = __ldg(reinterpret_cast<const double2*>(zrow + sch[t] * ldz + q));
+        a0 += zg.x;
+        a1 += zg.y;
+      }
+    }
+    if (col >= col_begin && col + 1 < col_end) {
+      __stcs(reinterpret_cast<double2*>(Jrow + col), make_double2(a0, a1));
+    } else {
+      if (col >= col_begin && col < col_end) Jrow[col] = a0;
+      if (col + 1 >= col_begin && col + 1 < col_end) Jrow[col + 1] = a1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ wide input layer, J-free
+// For identity inputs with din > MAXG (the STDE case) J's input block is
+//   J[p,(j,q)] = x_pj a_pq + sum_g [gd_pg = j] b_pgq  (j < din),   J[p,(din,q)] = a_pq,
+// a = Zbar_0 value channel, b_g = Zbar_0 grad channels (the Laplacian channel's
+// Hext is 0).  Its Gram block and J^T w are formed from X and Zbar_0 directly:
+//   K_in[p,p'] = sum_q a_pq a_p'q (x_p . x_p' + 1) + a_pq sum_g' x_p[gd_p'g'] b_p'g'q
+//              + a_p'q sum_g x_p'[gd_pg] b_pgq + sum_{gd_pg = gd_p'g'} b_pgq b_p'g'q.
+
+// XX[p,p'] = x_p . x_p' for p' <= p (odd din / unaligned points; else a split-K GEMM)
+__global__ void __launch_bounds__(256) k_xx_dot(Classes T, double* __restrict__ XX, long long ldxx) {
+  const long long p = blockIdx.x;
+  const ClassDev& C = T.c[find_class(T, p)];
+  const double* xp = C.pts + (p - C.row0) * T.din;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (long long p2 = warp; p2 <= p; p2 += 8) {
+    const ClassDev& D = T.c[find_class(T, p2)];
+    const double* xq = D.pts + (p2 - D.row0) * T.din;
+    double acc = 0.0;
+    for (int j = lane; j < T.din; j += 32) acc = fma(xp[j], xq[j], acc);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) XX[p * ldxx + p2] = acc;
+  }
+}
+
+// K[p,p'] += K_in[p,p'] and its mirror (p' <= p): CTA (p, 8-column group), a warp per p'
+__global__ void __launch_bounds__(256) k_gram_input(Classes T, const double* __restrict__ Zb,
+                                                      long long ldz, int w1,
+                                                      const double* __restrict__ XX,
+                                                      long long ldxx, double* __restrict__ K,
+                                                      long long ldK) {
+  __shared__ int gdp[MAXG];
+  const long long p = blockIdx.x;
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long i = p - C.row0;
+  const int ngp = C.ngrad;
+  if (threadIdx.x < ngp) gdp[threadIdx.x] = gdim(C, threadIdx.x, i);
+  __syncthreads();
+  const double* xp = C.pts + i * T.din;
+  const double* zp = Zb + (C.act0 + i * C.nch) * ldz;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    const long long p2 = static_cast<long long>(blockIdx.y) * 8 + warp;
+    if (p2 > p) return;
+    const ClassDev& D = T.c[find_class(T, p2)];
+    const long long i2 = p2 - D.row0;
+    const int ngq = D.ngrad;
+    const double* xq = D.pts + i2 * T.din;
+    const double* zq = Zb + (D.act0 + i2 * D.nch) * ldz;
+    const double s0 = XX[p * ldxx + p2] + 1.0;
+    double cq[MAXG], cp[MAXG];
+    int gq[MAXG];
+    unsigned mm[MAXG];
+#pragma unroll
+    for (int g = 0; g < MAXG; ++g) {
+      gq[g] = g < ngq ? gdim(D, g, i2) : -1;
+      cq[g] = g < ngq ? xp[gq[g]] : 0.0;   // x_p at p2's derivative dims
+      cp[g] = g < ngp ? xq[gdp[g]] : 0.0;  // x_p2 at p's derivative dims
+    }
+#pragma unroll
+    for (int g = 0; g < MAXG; ++g) {
+      unsigned b = 0;
+#pragma unroll
+      for (int h = 0; h < MAXG; ++h)
+        if (g < ngp && h < ngq && gdp[g] == gq[h]) b |= 1u << h;
+      mm[g] = b;
+    }
+    double acc = 0.0;
+    for (int q = lane; q < w1; q += 32) {
+      const double ap = zp[q], aq = zq[q];
+      double u = aq * s0, v = 0.0;
+#pragma unroll
+      for (int g = 0; g < MAXG; ++g) {
+        if (g < ngq) u = fma(cq[g], zq[(1 + g) * ldz + q], u);
+        if (g < ngp) v = fma(cp[g], zp[(1 + g) * ldz + q], v);
+      }
+      acc = fma(ap, u, acc);
+      acc = fma(aq, v, acc);
+#pragma unroll
+      for (int g = 0; g < MAXG; ++g) {
+        if (mm[g]) {
+          const double bp = zp[(1 + g) * ldz + q];
+          for (int h = 0; h < MAXG; ++h)
+            if ((mm[g] >> h) & 1u) acc = fma(bp, zq[(1 + h) * ldz + q], acc);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      K[p * ldK + p2] += acc;
+      if (p2 != p) K[p2 * ldK + p] += acc;
+    }
+  }
+}
+
+// (J^T w) over the input block: out[j,q] = scale (sum_p x_pj w_p a_pq + sum_{gd_pg = j}
+// w_p b_pgq), bias row j = din with x = 1.  CTA = 32 rows j x 128 neurons q (256
+// threads: 128 q x two halves of 16 rows), points staged JW_P at a time; the one-hot
+// rows of a chunk are compacted in (point, channel) order by one warp (ballot), so
+// the summation order is fixed.
+constexpr int JW_J = 32, JW_P = 16, JW_XLD = JW_J + 2;
+__global__ void __launch_bounds__(256) k_jt_input_wide(Classes T, const double* __restrict__ Zb,
+                                                         long long ld, int w1,
+                                                         const double* __restrict__ wvec,
+                                                         double scale, double* __restrict__ out) {
+  __shared__ __align__(16) double xs[JW_P][JW_XLD];
+  __shared__ double was[JW_P][128];
+  __shared__ double swt[JW_P];
+  __shared__ long long szrow[JW_P];
+  __shared__ int sgd[JW_P][MAXG];
+  __shared__ int sng[JW_P];
+  __shared__ int lst[JW_P * MAXG];  // (pp << 8 | g), rows d in this CTA's range
+  __shared__ int lsd[JW_P * MAXG];
+  __shared__ int lcnt;
+  const int tq = threadIdx.x & 127, half = threadIdx.x >> 7;
+  const int j0 = blockIdx.x * JW_J;
+  const int q = blockIdx.y * 128 + tq;
+  const int din = T.din;
+  const int jb = j0 + half * 16;
+  double acc[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) acc[r] = 0.0;
+  for (long long p0 = 0; p0 < T.m; p0 += JW_P) {
+    const int np = static_cast<int>(min(static_cast<long long>(JW_P), T.m - p0));
+    __syncthreads();
+    if (threadIdx.x < JW_P) {
+      const int pp = threadIdx.x;
+      if (pp < np) {
+        const long long p = p0 + pp;
+        const ClassDev& C = T.c[find_class(T, p)];
+        const long long i = p - C.row0;
+        swt[pp] = wvec[p];
+        szrow[pp] = (C.act0 + i * C.nch) * ld;
+        sng[pp] = C.ngrad;
+        for (int g = 0; g < C.ngrad; ++g) sgd[pp][g] = gdim(C, g, i);
+      } else {
+        swt[pp] = 0.0;
+        szrow[pp] = 0;
+        sng[pp] = 0;
+      }
+    }
+    for (int e = threadIdx.x; e < JW_P * JW_J; e += 256) {
+      const int pp = e / JW_J, jj = e - (e / JW_J) * JW_J;
+      const int j = j0 + jj;
+      double x = 0.0;
+      if (pp < np) {
+        const long long p = p0 + pp;
+        const ClassDev& C = T.c[find_class(T, p)];
+        x = j < din ? C.pts[(p - C.row0) * din + j] : (j == din ? 1.0 : 0.0);
+      }
+      xs[pp][jj] = x;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < JW_P * 128; e += 256) {
+      const int pp = e >> 7, qq = e & 127;
+      const int qg = blockIdx.y * 128 + qq;
+      was[pp][qq] = (pp < np && qg < w1) ? swt[pp] * Zb[szrow[pp] + qg] : 0.0;
+    }
+    if (threadIdx.x < 32) {  // deterministic compaction of the chunk's one-hot rows
+      int base = 0;
+      for (int e0 = 0; e0 < JW_P * MAXG; e0 += 32) {
+        const int e = e0 + static_cast<int>(threadIdx.x);
+        const int pp = e / MAXG, g = e - (e / MAXG) * MAXG;
+        const int d = (e < JW_P * MAXG && g < sng[pp]) ? sgd[pp][g] : -1;
+        const bool hit = d >= j0 && d < j0 + JW_J;
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int pos = base + __popc(b & ((1u << threadIdx.x) - 1u));
+          lst[pos] = (pp << 8) | g;
+          lsd[pos] = d;
+        }
+        base += __popc(b);
+      }
+      if (threadIdx.x == 0) lcnt = base;
+    }
+    __syncthreads();
+    for (int pp = 0; pp < np; ++pp) {
+      const double a = was[pp][tq];
+      const double2* xr = reinterpret_cast<const double2*>(&xs[pp][half * 16]);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const double2 xv = xr[r];
+        acc[2 * r] = fma(xv.x, a, acc[2 * r]);
+        acc[2 * r + 1] = fma(xv.y, a, acc[2 * r + 1]);
+      }
+    }
+    if (q < w1) {
+      for (int t = 0; t < lcnt; ++t) {
+        const int d = lsd[t];
+        if (d < jb || d >= jb + 16) continue;
+        const int pp = lst[t] >> 8, g = lst[t] & 255;
+        const double v = swt[pp] * Zb[szrow[pp] + (1 + g) * ld + q];
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if (d == jb + r) acc[r] += v;
+      }
+    }
+  }
+  if (q >= w1) return;
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+    if (jb + r <= din) out[static_cast<long long>(jb + r) * w1 + q] = scale * acc[r];
+}
+
 // ------------------------------------------------------------------ f_vv (t-jets)
 
 struct T2 {
@@ -375,7 +663,8 @@ DNGD_DEV void tanh_tjet(const ClassDev& C, ZGet zget, HPut hput) {
 // input layer of the f_vv pass: H3 holds [a; b; c] blocks of R rows each.
 __global__ void k_fvv_input(Classes T, const double* __restrict__ theta,
                             const double* __restrict__ v, int w1, long long ld,
-                            double* __restrict__ H3) {
+                            double* __restrict__ H3, const double* __restrict__ Zx,
+                            const double* __restrict__ Dx, long long ldx) {
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= T.m * w1) return;
   const long long p = idx / w1;
@@ -405,11 +694,16 @@ __global__ void k_fvv_input(Classes T, const double* __restrict__ theta,
     tanh_tjet(C, zget_e, hput);
     return;
   }
-  const double* x = C.pts + i * T.din;
   double za = theta[boff + q], zb = v[boff + q];
-  for (int j = 0; j < T.din; ++j) {
-    za = fma(x[j], theta[j * w1 + q], za);
-    zb = fma(x[j], v[j * w1 + q], zb);
+  if (Zx) {
+    za += Zx[p * ldx + q];
+    zb += Dx[p * ldx + q];
+  } else {
+    const double* x = C.pts + i * T.din;
+    for (int j = 0; j < T.din; ++j) {
+      za = fma(x[j], theta[j * w1 + q], za);
+      zb = fma(x[j], v[j * w1 + q], zb);
+    }
   }
   auto zget = [&](int ch) -> T2 {
     if (ch == 0) return {za, zb, 0.0};
@@ -539,10 +833,12 @@ __global__ void k_copy2d(const double* __restrict__ src, int rows, int cols,
   dst[r * ldd + c] = src[idx];
 }
 
+// entries [k0, n) of every candidate (k0 > 0: the wide input layer's W0 block is
+// never materialised per candidate, see input_gemm)
 __global__ void k_candidates(const double* __restrict__ theta, const double* __restrict__ delta,
                              const double* __restrict__ etas, long long n,
-                             double* __restrict__ out) {
-  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+                             double* __restrict__ out, long long k0 = 0) {
+  const long long k = k0 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= n) return;
   if (delta == nullptr) {  // explicit candidate stack (loss_many of residuals.py:188-201)
     out[blockIdx.y * n + k] = theta[blockIdx.y * n + k];
@@ -568,7 +864,30 @@ struct Plan {
   std::vector<long long> w, off, ld;  // widths, layer offsets in theta, padded widths
   long long n, m, R, wmax, ldmax;
   Classes T;
+  // large-din input layer as a split-K GEMM (input_gemm)
+  bool bigin = false;
+  int big_splits = 1;
+  long long big_mmax = 0;
+  // wide identity input layer (din > MAXG): J-free Gram through gram_wide_input
+  bool wide_in = false;
+  long long wi_ncols = 0, wi_ldh = 0, wi_ldxx = 0;
+  size_t wi_syrk_bytes = 0, wi_xx_part = 0;
+  int wi_xx_splits = 1;
 };
+
+// split count for a small M x N output over a long K (>= 256 columns per split,
+// about two waves of 128x128 tiles, no empty split)
+static int wide_k_splits(int nsm, long long M, long long N, long long K) {
+  const long long tiles = ((M + 127) / 128) * ((N + 127) / 128);
+  const long long kc = (K + 15) / 16;
+  long long S = (2LL * nsm + tiles - 1) / tiles;
+  S = std::max(1LL, std::min(S, kc / 16));
+  const long long per = (kc + S - 1) / S;
+  return static_cast<int>((kc + per - 1) / per);
+}
+
+// din at which x W0 leaves the per-(point, neuron) loop for the tensor cores
+constexpr int kBigInputDin = 64;
 
 static int make_plan(dngd_ctx* ctx, const dngd_mlp_desc* mlp, const dngd_class_desc* cls,
                      int nclass, Plan& P) {
@@ -637,6 +956,35 @@ static int make_plan(dngd_ctx* ctx, const dngd_mlp_desc* mlp, const dngd_class_d
   T.u0 = nullptr;
   P.m = row;
   P.R = act;
+  P.bigin = T.din >= kBigInputDin && (T.din % 2) == 0;
+  P.big_mmax = 0;
+  for (int k = 0; k < nclass; ++k) {
+    const ClassDev& C = T.c[k];
+    if (C.count == 0) continue;
+    if (C.inp || (reinterpret_cast<uintptr_t>(C.pts) & 15)) P.bigin = false;
+    P.big_mmax = std::max(P.big_mmax, C.count);
+  }
+  if (P.bigin && P.big_mmax > 0) {
+    P.big_splits = wide_k_splits(ctx->num_sms, P.big_mmax, P.w[1], T.din);
+  } else {
+    P.bigin = false;
+  }
+  P.wide_in = T.din > MAXG;
+  for (int k = 0; k < nclass; ++k)
+    if (T.c[k].inp) P.wide_in = false;
+  if (P.wide_in) {
+    P.wi_ncols = P.n - P.off[1];
+    P.wi_ldh = (P.wi_ncols + 3) / 4 * 4;
+    P.wi_ldxx = (P.m + 3) / 4 * 4;
+    int S;
+    long long nt;
+    int rc = syrk_plan(ctx, P.m, P.wi_ncols, &S, &nt, &P.wi_syrk_bytes);
+    if (rc) return rc;
+    if (P.bigin) {
+      P.wi_xx_splits = wide_k_splits(ctx->num_sms, P.big_mmax, P.big_mmax, T.din);
+      P.wi_xx_part = gemm_splitk_bytes(P.big_mmax, P.big_mmax, P.wi_xx_splits);
+    }
+  }
   return DNGD_OK;
 }
 
@@ -651,11 +999,29 @@ struct Arena {
   }
 };
 
+struct BigIn {
+  double* Wt = nullptr;    // W0^T (w1 x din)
+  double* part = nullptr;  // split-K partial tiles
+  double* Zx = nullptr;    // x W0 rows (m x ld1)
+  double* Dx = nullptr;    // x V0 rows: f_vv / line-search direction
+};
+
+static void carve_bigin(const Plan& P, Arena& A, BigIn& G, bool dir) {
+  if (!P.bigin) return;
+  G.Wt = A.take(static_cast<size_t>(P.w[1]) * P.w[0]);
+  G.part = A.take(gemm_splitk_bytes(P.big_mmax, P.w[1], P.big_splits) / sizeof(double));
+  G.Zx = A.take(static_cast<size_t>(P.m) * P.ld[1]);
+  if (dir) G.Dx = A.take(static_cast<size_t>(P.m) * P.ld[1]);
+}
+
 struct AsmBufs {
   std::vector<double*> Z, H, Zb, Wt, Wp;
+  BigIn big;
   double* Hb;
   double* H0;  // materialised input channels (factored Gram), R x 16
   double* u0;  // per-point network value (cubic-term adjoint seeds), m
+  // wide input layer: hidden/output columns of J, SYRK partials, X X^T (+ partials)
+  double *Jh = nullptr, *syrk_work = nullptr, *XX = nullptr, *xx_part = nullptr;
 };
 
 static void carve_assemble(const Plan& P, Arena& A, AsmBufs& B) {
@@ -675,11 +1041,19 @@ static void carve_assemble(const Plan& P, Arena& A, AsmBufs& B) {
   }
   B.H0 = A.take(P.R * 16);
   B.u0 = A.take(P.m);
+  carve_bigin(P, A, B.big, false);
+  if (P.wide_in) {
+    B.Jh = A.take(static_cast<size_t>(P.m) * P.wi_ldh);
+    B.syrk_work = A.take(P.wi_syrk_bytes / sizeof(double) + 1);
+    B.XX = A.take(static_cast<size_t>(P.m) * P.wi_ldxx);
+    if (P.wi_xx_part) B.xx_part = A.take(P.wi_xx_part / sizeof(double));
+  }
 }
 
 struct FvvBufs {
   std::vector<double*> H3, Wt, Vt;
   double *P3, *Q2;
+  BigIn big;
 };
 
 static void carve_fvv(const Plan& P, Arena& A, FvvBufs& B) {
@@ -695,11 +1069,13 @@ static void carve_fvv(const Plan& P, Arena& A, FvvBufs& B) {
     B.Wt[k] = A.take(P.w[k + 1] * P.ld[k]);
     B.Vt[k] = A.take(P.w[k + 1] * P.ld[k]);
   }
+  carve_bigin(P, A, B.big, true);
 }
 
 struct LossBufs {
   double *thetas, *Hping, *Hpong, *Z, *r;
   std::vector<double*> Wt;
+  BigIn big;
 };
 
 static void carve_loss(const Plan& P, Arena& A, LossBufs& B, int C) {
@@ -710,6 +1086,7 @@ static void carve_loss(const Plan& P, Arena& A, LossBufs& B, int C) {
   B.r = A.take(static_cast<size_t>(C) * P.m);
   B.Wt.assign(P.L, nullptr);
   for (int k = 1; k <= P.L - 2; ++k) B.Wt[k] = A.take(static_cast<size_t>(C) * P.w[k + 1] * P.ld[k]);
+  carve_bigin(P, A, B.big, true);
 }
 
 static inline unsigned nblk(long long n, int t = 256) {
@@ -723,16 +1100,53 @@ static void launch_transpose(cudaStream_t s, const double* W, long long src_s, i
   k_transpose<<<grid, dim3(32, 8), 0, s>>>(W, src_s, rows, cols, dst, ldd, dst_s);
 }
 
+// out = X W for the (din x w1) block W laid out like W0 (the STDE case, din ~ 1e5):
+// per class one split-K FP64 tensor-core GEMM over the raw points instead of a
+// din-long dot product per (point, neuron).  out rows are points (ld ld1).
+static int input_gemm(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const BigIn& G,
+                      const double* W, double* out) {
+  const int din = P.T.din, w1 = static_cast<int>(P.w[1]);
+  launch_transpose(s, W, 0, din, w1, G.Wt, din, 0, 1);
+  const size_t pb = gemm_splitk_bytes(P.big_mmax, w1, P.big_splits);
+  for (int c = 0; c < P.T.n; ++c) {
+    const ClassDev& C = P.T.c[c];
+    if (C.count == 0) continue;
+    GemmCall g;
+    g.M = C.count;
+    g.N = w1;
+    g.K = din;
+    g.A = C.pts;
+    g.lda = din;
+    g.B = G.Wt;
+    g.ldb = din;
+    g.C = out + C.row0 * P.ld[1];
+    g.ldc = P.ld[1];
+    const int rc = gemm_nt_splitk(ctx, s, g, P.big_splits, G.part, pb);
+    if (rc) return rc;
+  }
+  return DNGD_OK;
+}
+
 // forward through all hidden layers; Hlast receives H_{L-1}.  Used by loss_many
 // (batched over candidates) with Z scratch shared across layers.
 static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const double* thetas,
-                           int C, LossBufs& B, double** Hlast) {
+                           int C, LossBufs& B, double** Hlast, const double* theta,
+                           const double* delta, const double* etas) {
   const int L = P.L;
   const long long act_s = P.R * P.ldmax;
   {
+    const double *Zx = nullptr, *Dx = nullptr;
+    if (P.bigin && delta != nullptr) {  // x (W0 + eta V0) = x W0 + eta x V0
+      int rc = input_gemm(ctx, s, P, B.big, theta, B.big.Zx);
+      if (rc) return rc;
+      rc = input_gemm(ctx, s, P, B.big, delta, B.big.Dx);
+      if (rc) return rc;
+      Zx = B.big.Zx;
+      Dx = B.big.Dx;
+    }
     dim3 g(nblk(P.m * P.w[1]), C);
     k_input_fwd<<<g, 256, 0, s>>>(P.T, thetas, P.n, static_cast<int>(P.w[1]), P.ldmax, nullptr,
-                                  B.Hping, act_s);
+                                  B.Hping, act_s, Zx, Dx, etas, P.ld[1], theta, delta);
   }
   double* Hcur = B.Hping;
   double* Hnext = B.Hpong;
@@ -1283,8 +1697,13 @@ static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& 
   int rc = DNGD_OK;
   const int L = P.L;
   // ---- forward
+  if (P.bigin) {
+    rc = input_gemm(ctx, s, P, B.big, theta, B.big.Zx);
+    if (rc) return rc;
+  }
   k_input_fwd<<<nblk(P.m * P.w[1]), 256, 0, s>>>(P.T, theta, 0, static_cast<int>(P.w[1]),
-                                                  P.ld[1], B.Z[0], B.H[1], 0);
+                                                  P.ld[1], B.Z[0], B.H[1], 0, B.big.Zx, nullptr,
+                                                  nullptr, P.ld[1], nullptr, nullptr);
   for (int k = 1; k <= L - 2; ++k) {
     launch_transpose(s, theta + P.off[k], 0, static_cast<int>(P.w[k]),
                      static_cast<int>(P.w[k + 1]), B.Wt[k], P.ld[k], 0, 1);
@@ -1314,6 +1733,9 @@ static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& 
     return set_error(ctx, DNGD_ERR_DIMENSION, "assemble: column range outside [0, n]");
   }
   const bool jvec_ok = ((ldJ & 1) == 0) && ((reinterpret_cast<uintptr_t>(J) & 15) == 0);
+  bool identity_inputs = true;
+  for (int c = 0; c < P.T.n; ++c)
+    if (P.T.c[c].inp) identity_inputs = false;
   auto jwrite = [&](int k, const double* Hk, long long ldh, const double* Zb, long long ldz) {
     if (J == nullptr) return;
     const int win = static_cast<int>(P.w[k]), wout = static_cast<int>(P.w[k + 1]);
@@ -1321,7 +1743,11 @@ static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& 
     if (hi <= col_begin || lo >= col_end) return;
     const long long E = (win + 1LL) * wout;
     const bool vec = Zb != nullptr && jvec_ok && (wout % 2 == 0) && ((lo - col_begin) % 2 == 0);
-    if (vec) {
+    if (vec && k == 0 && identity_inputs) {
+      const unsigned gx = static_cast<unsigned>(std::min<long long>((E / 2 + 255) / 256, 64));
+      k_jwrite_in<<<dim3(gx, static_cast<unsigned>(P.m)), 256, 0, s>>>(
+          P.T, Zb, ldz, wout, col_begin, col_end, J, ldJ);
+    } else if (vec) {
       const unsigned gx = static_cast<unsigned>(std::min<long long>((E + 511) / 512, 64));
       k_jwrite<true><<<dim3(gx, static_cast<unsigned>(P.m)), 256, 0, s>>>(
           P.T, Hk, ldh, win, Zb, ldz, wout, lo, col_begin, col_end, J, ldJ);
@@ -1461,6 +1887,44 @@ static int gram_setup(dngd_ctx* ctx, const Plan& P, const AsmBufs& B, GramParams
   return DNGD_OK;
 }
 
+// K = J J^T without J's input block (wide identity input layer): the hidden and
+// output columns are materialised and SYRKed, the input block is added by
+// k_gram_input from X X^T and Zbar_0.
+static int gram_wide_input(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& B,
+                           const double* theta, double* r, double* K, long long ldK) {
+  int rc = assemble_impl(ctx, s, P, B, theta, P.off[1], P.n, r, B.Jh, P.wi_ldh, true);
+  if (rc) return rc;
+  rc = syrk(ctx, s, B.Jh, P.m, P.wi_ncols, P.wi_ldh, K, ldK, 0, B.syrk_work, P.wi_syrk_bytes);
+  if (rc) return rc;
+  if (P.bigin) {
+    for (int c = 0; c < P.T.n; ++c) {
+      for (int cp = 0; cp <= c; ++cp) {
+        const ClassDev &C = P.T.c[c], &D = P.T.c[cp];
+        if (C.count == 0 || D.count == 0) continue;
+        GemmCall g;
+        g.M = C.count;
+        g.N = D.count;
+        g.K = P.T.din;
+        g.A = C.pts;
+        g.lda = P.T.din;
+        g.B = D.pts;
+        g.ldb = P.T.din;
+        g.C = B.XX + C.row0 * P.wi_ldxx + D.row0;
+        g.ldc = P.wi_ldxx;
+        rc = gemm_nt_splitk(ctx, s, g, P.wi_xx_splits, B.xx_part, P.wi_xx_part);
+        if (rc) return rc;
+      }
+    }
+  } else {
+    k_xx_dot<<<static_cast<unsigned>(P.m), 256, 0, s>>>(P.T, B.XX, P.wi_ldxx);
+  }
+  k_gram_input<<<dim3(static_cast<unsigned>(P.m), static_cast<unsigned>((P.m + 7) / 8)), 256, 0,
+                 s>>>(P.T, B.Zb[0], P.ld[1],
+                                                          static_cast<int>(P.w[1]), B.XX,
+                                                          P.wi_ldxx, K, ldK);
+  return cuda_status(ctx, cudaGetLastError(), "gram_wide_input");
+}
+
 extern "C" int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                                   const double* theta, const dngd_class_desc* classes,
                                   int nclass, double* r, double* K, int64_t ldK, void* work,
@@ -1482,6 +1946,16 @@ extern "C" int dngd_gram_factored_part(dngd_ctx* ctx, void* stream, const dngd_m
   if (rc) return rc;
   if (bytes_of(P, 0, 1) > work_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_factored: workspace too small");
   if (P.m == 0) return DNGD_OK;
+  if (P.wide_in) {
+    if (nparts != 1) {
+      return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_factored: wide input layer is not tile-sharded");
+    }
+    Arena A{static_cast<char*>(work)};
+    AsmBufs B;
+    carve_assemble(P, A, B);
+    P.T.u0 = B.u0;
+    return gram_wide_input(ctx, s, P, B, theta, r, K, ldK);
+  }
   if (P.T.din > DNGD_MAX_GRAD) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_factored: input dim > 12");
   Arena A{static_cast<char*>(work)};
   AsmBufs B;
@@ -1722,8 +2196,14 @@ static int fvv_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const
   const long long ld = P.ldmax;
   double* Hcur = B.H3[0];
   double* Hnext = B.H3[1];
+  if (P.bigin) {
+    rc = input_gemm(ctx, s, P, B.big, theta, B.big.Zx);
+    if (rc) return rc;
+    rc = input_gemm(ctx, s, P, B.big, v, B.big.Dx);
+    if (rc) return rc;
+  }
   k_fvv_input<<<nblk(P.m * P.w[1]), 256, 0, s>>>(P.T, theta, v, static_cast<int>(P.w[1]), ld,
-                                                  Hcur);
+                                                  Hcur, B.big.Zx, B.big.Dx, P.ld[1]);
   for (int k = 1; k <= L - 2; ++k) {
     launch_transpose(s, theta + P.off[k], 0, static_cast<int>(P.w[k]),
                      static_cast<int>(P.w[k + 1]), B.Wt[k], P.ld[k], 0, 1);
@@ -1815,9 +2295,10 @@ extern "C" int dngd_loss_many(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* 
   Arena A{static_cast<char*>(work)};
   LossBufs B;
   carve_loss(P, A, B, ncand);
-  k_candidates<<<dim3(nblk(P.n), ncand), 256, 0, s>>>(theta, delta, etas, P.n, B.thetas);
+  const long long k0 = (P.bigin && delta != nullptr) ? P.T.din * P.w[1] : 0;
+  k_candidates<<<dim3(nblk(P.n - k0), ncand), 256, 0, s>>>(theta, delta, etas, P.n, B.thetas, k0);
   double* Hlast;
-  rc = forward_batched(ctx, s, P, B.thetas, ncand, B, &Hlast);
+  rc = forward_batched(ctx, s, P, B.thetas, ncand, B, &Hlast, theta, delta, etas);
   if (rc) return rc;
   k_head<<<dim3(nblk(P.m, 8), ncand), 256, 0, s>>>(P.T, Hlast, static_cast<int>(P.w[P.L - 1]),
                                                     P.ldmax, B.thetas, P.n, P.off[P.L - 1],
@@ -1842,7 +2323,7 @@ static constexpr long long kJtTiledMaxWidth = 128;
 
 JtScratch jt_plan(dngd_ctx* ctx, const Plan& P) {
   JtScratch S;
-  S.tiled = P.wmax <= kJtTiledMaxWidth && P.w[0] <= kJtTiledMaxWidth;
+  S.tiled = P.wmax <= kJtTiledMaxWidth && P.w[0] <= MAXG;
   if (S.tiled) {
     S.tiles = 0;
     for (int k = 0; k < P.L; ++k)
@@ -1870,7 +2351,9 @@ JtScratch jt_plan(dngd_ctx* ctx, const Plan& P) {
     S.splits = std::max(S.splits, sp);
     part = std::max(part, gemm_splitk_bytes(P.w[k] + 1, P.w[k + 1], sp));
   }
-  part = std::max(part, static_cast<size_t>(S.nchunks) * static_cast<size_t>((P.w[0] + 1) * P.w[1]) * 8);
+  if (!P.wide_in) {  // (the wide input layer writes out directly)
+    part = std::max(part, static_cast<size_t>(S.nchunks) * static_cast<size_t>((P.w[0] + 1) * P.w[1]) * 8);
+  }
   part = std::max(part, static_cast<size_t>(S.nchunks) * static_cast<size_t>(P.w[P.L - 1] + 1) * 8);
   const size_t ht = static_cast<size_t>(P.wmax + 1) * S.ldR * 8;
   S.off_zt = (ht + 255) / 256 * 256;
@@ -1905,6 +2388,9 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
     return set_error(ctx, DNGD_ERR_DIMENSION, "jt_factored: scratch workspace too small");
   }
   if (P.m == 0) return DNGD_OK;
+  if (P.T.din > MAXG && !P.wide_in) {
+    return set_error(ctx, DNGD_ERR_UNSUPPORTED, "jt_factored: embedded inputs wider than 12");
+  }
   Arena A{static_cast<char*>(act_work)};
   AsmBufs B;
   carve_assemble(P, A, B);
@@ -1941,7 +2427,11 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   double* part = reinterpret_cast<double*>(sc + S.off_part);
   const int L = P.L;
   // input layer W0 | b0
-  {
+  if (P.wide_in) {
+    const int w1 = static_cast<int>(P.w[1]);
+    dim3 g(static_cast<unsigned>((P.w[0] + 1 + JW_J - 1) / JW_J), (w1 + 127) / 128);
+    k_jt_input_wide<<<g, 256, 0, s>>>(P.T, B.Zb[0], P.ld[1], w1, w, scale, out + P.off[0]);
+  } else {
     const int w1 = static_cast<int>(P.w[1]);
     dim3 g((w1 + 127) / 128, S.nchunks);
     k_jt_input<<<g, 128, 0, s>>>(P.T, B.Zb[0], P.ld[1], w1, w, S.chunk, part);

@@ -466,12 +466,14 @@ class PoissonBallStde(PdeProblem):
         return np.sum(c * (np.sin(x[:, :-1] + np.cos(x[:, 1:])) + x[:, 1:] * np.cos(x[:, :-1])),
                       axis=1)
 
-    def _exact_dd(self, x, j):
-        """d^2/dx_j^2 of the exact solution, per point direction j (product rule)."""
+    def _exact_dd(self, x, j, F=None, s=None):
+        """d^2/dx_j^2 of the exact solution, per point direction j (product rule).
+        F = _F(x) and s = 1 - |x|^2 may be passed in (they do not depend on j)."""
         c, d = self.coeffs, self.dim
         rows = np.arange(x.shape[0])
         xj = x[rows, j]
-        F = self._F(x)
+        if F is None:
+            F = self._F(x)
         m1 = j < d - 1
         jj = np.where(m1, j, 0)
         xn = x[rows, np.minimum(j + 1, d - 1)]
@@ -485,12 +487,15 @@ class PoissonBallStde(PdeProblem):
         dF = dF + np.where(m2, c[jm] * (-np.cos(b) * np.sin(xj) + np.cos(xp)), 0.0)
         ddF = ddF + np.where(m2, c[jm] * (-np.sin(b) * np.sin(xj) ** 2 - np.cos(b) * np.cos(xj)),
                              0.0)
-        s = 1.0 - np.sum(x * x, axis=1)
+        if s is None:
+            s = 1.0 - np.sum(x * x, axis=1)
         return s * ddF - 4.0 * xj * dF - 2.0 * F
 
     def class_data(self, cls):
         idx = np.asarray(cls.aux["stde_idx"])
-        lap_ex = sum(self._exact_dd(cls.points, idx[:, g]) for g in range(self.k))
+        x = cls.points
+        F, s = self._F(x), 1.0 - np.sum(x * x, axis=1)  # shared by the k directions
+        lap_ex = sum(self._exact_dd(x, idx[:, g], F, s) for g in range(self.k))
         return -(self.dim / self.k) * lap_ex
 
     def value_factor(self, pts):

@@ -591,9 +591,22 @@ class PinnResidualMap(ResidualMap):
         op = self.problem.class_operator(cls.class_id)
         return 1 + len(op.grad_dims) + (1 if op.lap_dims else 0)
 
+    def wide_input(self) -> bool:
+        """Raw (identity) inputs wider than the channel kernels (din > 12, the STDE
+        case): the J-free Gram forms J's input block from X X^T and the input-layer
+        adjoints, and only the hidden/output columns are materialised (pinn.cu
+        gram_wide_input)."""
+        from . import _lib
+
+        return self.spec.input_dim > _lib.MAX_GRAD and all(
+            not d.inputs for d in self._device()["arr"])
+
     def use_factored_gram(self) -> bool:
         if self.col_range != (0, self.layout.size):
             return False  # column shards form their partial Gram from J_p
+        if self.wide_input():
+            # the input block is (din+1) w1 of n columns: never worth writing J
+            return self.gram_mode != "materialized" and self.gram_shard is None
         if any(self._nch(c) > 8 for c in self.collocation.classes):
             return False
         if self.gram_mode == "factored":
@@ -611,7 +624,7 @@ class PinnResidualMap(ResidualMap):
     def jfree_pcg(self) -> bool:
         """PCG without J: J^T w / J v from activations and forward tangents, the
         Nystrom columns K[:, I] from the factored kernel (linear operators only)."""
-        return self.use_factored_gram() and all(
+        return self.use_factored_gram() and not self.wide_input() and all(
             float(getattr(self.problem.class_operator(c.class_id), "c3", 0.0)) == 0.0
             for c in self.collocation.classes)
 

@@ -298,6 +298,9 @@ def main_stde():
                  [1e-3])
     trajectory_fixture("stde_traj", PoissonBallStde(10, 3), (10, 12, 12, 1), {INTERIOR: 40},
                        9, 1e3, 3)
+    # wide raw input (din > 12): the device step forms J's input block analytically
+    trajectory_fixture("stde_wide_traj", PoissonBallStde(200, 4), (200, 16, 16, 1),
+                       {INTERIOR: 48}, 10, 1e3, 3)
 
 
 if __name__ == "__main__":
@@ -305,6 +308,10 @@ if __name__ == "__main__":
         main_allen_cahn()
     elif sys.argv[1:] == ["stde"]:
         main_stde()
+    elif sys.argv[1:] == ["stde_wide"]:
+        from dngd.problems import PoissonBallStde
+        trajectory_fixture("stde_wide_traj", PoissonBallStde(200, 4), (200, 16, 16, 1),
+                           {INTERIOR: 48}, 10, 1e3, 3)
     else:
         main()
         main_allen_cahn()

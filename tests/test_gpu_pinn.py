@@ -21,6 +21,15 @@ CASES = [
     ("stde_wide", O.OraclePoissonBallStde(10, 6), (10, 160, 96, 1), (24,)),
 ]
 
+# large input dimension: x W0 runs as a split-K tensor-core GEMM (input_gemm) and
+# J's input block through k_jwrite_in; 150 points = a full and a ragged 128-row tile
+BIG_DIN = [
+    ("stde_din600", O.OraclePoissonBallStde(600, 4), (600, 64, 32, 1), (150,)),
+    ("stde_din1000_wide", O.OraclePoissonBallStde(1000, 3), (1000, 160, 1), (40,)),
+    # odd din below the GEMM threshold: loop input layer and the k_xx_dot Gram
+    ("stde_din25", O.OraclePoissonBallStde(25, 4), (25, 32, 32, 1), (70,)),
+]
+
 
 def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
@@ -46,7 +55,7 @@ def _setup(K, problem, widths, counts, seed):
     return classes, theta, arr, keep, mlp, ws, dev(theta)
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES)
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN)
 def test_assemble_matches_oracle(K, name, problem, widths, counts):
     classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 3)
     r_ref, J_ref = O.linearize(theta, widths, classes)
@@ -67,7 +76,7 @@ def test_assemble_matches_oracle(K, name, problem, widths, counts):
         assert np.array_equal(Js[:, : c1 - c0].cpu().numpy(), Jg[:, c0:c1])
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES)
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN)
 def test_fvv_matches_oracle(K, name, problem, widths, counts):
     from tests.gpu_util import dev
     classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 4)
@@ -78,7 +87,7 @@ def test_fvv_matches_oracle(K, name, problem, widths, counts):
     assert _rel(out.cpu().numpy(), ref) <= 1e-11
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES)
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN)
 def test_loss_many_matches_oracle(K, name, problem, widths, counts):
     from tests.gpu_util import dev
     classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 5)
@@ -95,7 +104,7 @@ def test_loss_many_matches_oracle(K, name, problem, widths, counts):
     np.testing.assert_allclose(out2.cpu().numpy(), ref, rtol=1e-12)
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES + [
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN + [
     ("poisson2d_cfg1", O.OraclePoisson2d(), (2, 32, 32, 1), (900, 120)),
     ("heat1d_cfg2", O.OracleHeat1d(), (2, 64, 64, 64, 64, 1), (500, 100, 100)),
 ])
@@ -115,7 +124,7 @@ def test_gram_factored_matches_jjt(K, name, problem, widths, counts):
     assert _rel(r.cpu().numpy(), r_ref) <= 1e-12
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES)
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN)
 def test_jt_factored_matches_oracle(K, name, problem, widths, counts):
     """J^T w from the activations (no J) == oracle J^T w (tiled and wide paths)."""
     from tests.gpu_util import dev
@@ -156,7 +165,7 @@ def test_gram_factored_parts_sum_to_full(K, nparts):
     assert torch.equal(acc, full)
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES)
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN)
 def test_jvp_factored_matches_oracle(K, name, problem, widths, counts):
     """J v from first-order forward t-jets (no J) == oracle J v."""
     from tests.gpu_util import dev

@@ -130,6 +130,9 @@ TRAJ = {
     "cfg2_traj": ("heat1d", (60, 20, 20), dict(lam_cap=1e-3)),
     "ac_traj": ("allen_cahn", (60, 20), dict(lam_cap=1e-3)),
     "stde_traj": ("poisson_ball_stde", (40,), dict(lam_cap=1e3)),
+    # din = 200 > 12: J-free step with the input block formed from X X^T (wide input)
+    "stde_wide_traj": ("poisson_ball_stde", (48,), dict(lam_cap=1e3),
+                       dict(dim=200, index_set_size=4)),
     "pcg_traj": ("poisson2d", (60, 20),
                  dict(lam_cap=1e-3, dense_threshold=10, nystrom_rank=16, cg_max_iters=100)),
 }
@@ -138,11 +141,12 @@ TRAJ = {
 @pytest.mark.parametrize("name", sorted(TRAJ))
 def test_trajectory_matches_reference(P, golden_dir, name):
     fx = _load(golden_dir, name)
-    pname, counts, cfg = TRAJ[name]
+    pname, counts, cfg = TRAJ[name][:3]
+    pkw = TRAJ[name][3] if len(TRAJ[name]) > 3 else PROBLEM_KW.get(pname, {})
     widths = tuple(int(w) for w in fx["widths"])
     n_steps = len(fx["loss"]) - 1
     config = P.OptimizerConfig(max_iters=n_steps, deterministic_timing=True, **cfg)
-    trace = P.dngd_run(P.make_problem(pname, **PROBLEM_KW.get(pname, {})), P.MlpSpec(widths),
+    trace = P.dngd_run(P.make_problem(pname, **pkw), P.MlpSpec(widths),
                        config, int(fx["seed"]), counts=counts, init="xavier_normal")
     assert not trace.aborted, trace.abort_reason
     loss = np.array([r.loss for r in trace.rows])

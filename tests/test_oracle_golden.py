@@ -99,6 +99,8 @@ TRAJ = {
     "cfg2_traj": (O.OracleHeat1d(), (60, 20, 20), O.LoopConfig(lam_cap=1e-3, max_iters=4)),
     "ac_traj": (O.OracleAllenCahn(), (60, 20), O.LoopConfig(lam_cap=1e-3, max_iters=4)),
     "stde_traj": (O.OraclePoissonBallStde(10, 3), (40,), O.LoopConfig(lam_cap=1e3, max_iters=3)),
+    "stde_wide_traj": (O.OraclePoissonBallStde(200, 4), (48,),
+                       O.LoopConfig(lam_cap=1e3, max_iters=3)),
     "pcg_traj": (O.OraclePoisson2d(), (60, 20),
                  O.LoopConfig(lam_cap=1e-3, max_iters=3, dense_threshold=10, nystrom_rank=16,
                               cg_max_iters=100)),

@@ -411,6 +411,18 @@ def run_ours(args, cfg):
                 "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
                 "algorithmic": f"factored Gram {flops:.3e} FLOP per launch",
                 "jjt_equivalent_tflops": m * (m + 1) * n / gram_avg / 1e12}
+    vjp_avg = stages.get("vjp", 0.0) / max(counts.get("vjp", 1), 1) * 1e-3
+    if gram_avg > 0 and maps[0].wide_input() and vjp_avg > 0:
+        # wide raw input (STDE): the Gram is formed analytically (X X^T + hidden
+        # SYRK); the heaviest kernel is J^T w's input block, FP64 FMA over every
+        # parameter (B200's nominal FP64 vector and DMMA peaks are the same)
+        flops = 2.0 * m * n
+        ach = flops / vjp_avg / 1e12
+        roof = {"kernel": "dngd::k_jt_input_wide (+ hidden-layer split-K GEMMs): J^T w, J-free",
+                "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": ach / fp64_peak, "traffic": None,
+                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
+                "algorithmic": f"2 m n = {flops:.3e} FLOP per J^T w"}
     if roof is not None:
         roof["traffic"] = _profiled_traffic(cfg["name"], roof["kernel"])
     gram_chol = None
@@ -420,7 +432,9 @@ def run_ours(args, cfg):
         gf = (m * (m + 1) * n + m**3 / 3) / (g_avg + potrf_avg) / 1e12
         gram_chol = {"tflops": gf, "frac_of_fp64_peak": gf / fp64_peak,
                      "gram_ms": g_avg * 1e3, "potrf_ms": potrf_avg * 1e3,
-                     "gram_path": "syrk" if syrk_avg > 0 else "factored",
+                     "gram_path": "syrk" if syrk_avg > 0 else (
+                         "wide-input (hidden SYRK + analytic input block)"
+                         if maps[0].wide_input() else "factored"),
                      "definition": "(m(m+1)n + m^3/3) / (t_gram + t_potrf), SURVEY 8(d); on the "
                                    "factored path this is a J J^T-equivalent rate (the kernel "
                                    "performs fewer FLOPs), so it can exceed the FP64 peak"}

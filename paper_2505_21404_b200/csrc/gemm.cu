@@ -299,30 +299,44 @@ int gemm_nt(dngd_ctx* ctx, cudaStream_t s, const GemmCall& g) {
 // For small outputs with a long reduction (J^T w over activation rows): S splits
 // write raw 128x128 partial tiles, a fixed-order reduction applies alpha / beta.
 
-__global__ void k_splitk_reduce(const double* __restrict__ partial, int splits, int ntiles,
-                                int tiles_n, long long M, long long N, double* __restrict__ C,
-                                long long ldc, double alpha, double beta) {
-  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+// 256 threads = 64 output elements x 4 quarters of the splits; each quarter sums
+// its contiguous split range in order, the quarters are added in order.
+__global__ void __launch_bounds__(256) k_splitk_reduce(const double* __restrict__ partial,
+                                                         int splits, int ntiles, int tiles_n,
+                                                         long long M, long long N,
+                                                         double* __restrict__ C, long long ldc,
+                                                         double alpha, double beta) {
+  __shared__ double sh[4][64];
+  const int lane64 = threadIdx.x & 63, quarter = threadIdx.x >> 6;
+  const long long e = static_cast<long long>(blockIdx.x) * 64 + lane64;
   const long long tile_elems = 128 * 128;
-  if (e >= static_cast<long long>(ntiles) * tile_elems) return;
+  const bool valid = e < static_cast<long long>(ntiles) * tile_elems;
+  double v = 0.0;
+  if (valid) {
+    const int per = (splits + 3) / 4;
+    const int s0 = quarter * per, s1 = min(splits, s0 + per);
+    const double* src = partial + e;
+    const long long sstride = static_cast<long long>(ntiles) * tile_elems;
+    int s = s0;
+    for (; s + 8 <= s1; s += 8) {  // loads issued ahead of the in-order sum
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = __ldcs(src + (s + u) * sstride);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v += a[u];
+    }
+    for (; s < s1; ++s) v += __ldcs(src + s * sstride);
+  }
+  sh[quarter][lane64] = v;
+  __syncthreads();
+  if (quarter != 0 || !valid) return;
+  v = ((sh[0][lane64] + sh[1][lane64]) + sh[2][lane64]) + sh[3][lane64];
   const int t = static_cast<int>(e / tile_elems);
   const int off = static_cast<int>(e - t * tile_elems);
   const int tm = t / tiles_n, tn = t - (t / tiles_n) * tiles_n;
   const long long r = static_cast<long long>(tm) * 128 + off / 128;
   const long long c = static_cast<long long>(tn) * 128 + off % 128;
   if (r >= M || c >= N) return;
-  const double* src = partial + static_cast<long long>(t) * tile_elems + off;
-  const long long sstride = static_cast<long long>(ntiles) * tile_elems;
-  double v = 0.0;
-  int s = 0;
-  for (; s + 8 <= splits; s += 8) {  // loads issued ahead of the in-order sum
-    double a[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) a[u] = __ldcs(src + (s + u) * sstride);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v += a[u];
-  }
-  for (; s < splits; ++s) v += __ldcs(src + s * sstride);
   double* cp = C + r * ldc + c;
   *cp = alpha * v + (beta != 0.0 ? beta * *cp : 0.0);
 }
@@ -355,7 +369,7 @@ int gemm_nt_splitk(dngd_ctx* ctx, cudaStream_t s, const GemmCall& g0, int splits
   const int tiles_n = static_cast<int>((g.N + 127) / 128);
   const int ntiles = static_cast<int>(((g.M + 127) / 128) * tiles_n);
   const long long total = static_cast<long long>(ntiles) * 128 * 128;
-  k_splitk_reduce<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+  k_splitk_reduce<<<static_cast<unsigned>((total + 63) / 64), 256, 0, s>>>(
       partial, splits, ntiles, tiles_n, g.M, g.N, g.C, g.ldc, g.alpha, g.beta);
   return cuda_status(ctx, cudaGetLastError(), "splitk reduce");
 }

@@ -520,107 +520,141 @@ __global__ void __launch_bounds__(256) k_gram_input(Classes T, const double* __r
 
 // (J^T w) over the input block: out[j,q] = scale (sum_p x_pj w_p a_pq + sum_{gd_pg = j}
 // w_p b_pgq), bias row j = din with x = 1.  CTA = 32 rows j x 128 neurons q (256
-// threads: 128 q x two halves of 16 rows), points staged JW_P at a time; the one-hot
-// rows of a chunk are compacted in (point, channel) order by one warp (ballot), so
+// threads: 128 q x two halves of 16 rows).  Points stream through double-buffered
+// shared memory JW_P at a time, the next chunk's global loads in flight (registers)
+// while the current one is multiplied.  The one-hot rows of a chunk are compacted
+// in (point, channel) order by one warp (ballot) and applied one chunk later, so
 // the summation order is fixed.
-constexpr int JW_J = 32, JW_P = 16, JW_XLD = JW_J + 2;
-__global__ void __launch_bounds__(256) k_jt_input_wide(Classes T, const double* __restrict__ Zb,
-                                                         long long ld, int w1,
-                                                         const double* __restrict__ wvec,
-                                                         double scale, double* __restrict__ out) {
-  __shared__ __align__(16) double xs[JW_P][JW_XLD];
-  __shared__ double was[JW_P][128];
-  __shared__ double swt[JW_P];
-  __shared__ long long szrow[JW_P];
-  __shared__ int sgd[JW_P][MAXG];
-  __shared__ int sng[JW_P];
-  __shared__ int lst[JW_P * MAXG];  // (pp << 8 | g), rows d in this CTA's range
-  __shared__ int lsd[JW_P * MAXG];
-  __shared__ int lcnt;
-  const int tq = threadIdx.x & 127, half = threadIdx.x >> 7;
+constexpr int JW_J = 32, JW_P = 16, JW_XLD = JW_J + 2, JW_L = JW_P * MAXG;
+struct JwSmem {
+  double xs[2][JW_P][JW_XLD];
+  double was[2][JW_P][128];
+  long long lz[2][JW_L];  // Zbar offset of the one-hot channel row
+  double lw[2][JW_L];
+  int ld[2][JW_L];
+  int lcnt[2];
+  long long szrow[2][JW_P];
+  double swt[2][JW_P];
+  int sgd[2][JW_P][MAXG];
+  int sng[2][JW_P];
+};
+constexpr size_t kJwSmem = sizeof(JwSmem) + 16;
+
+__global__ void __launch_bounds__(256, 2) k_jt_input_wide(Classes T, const double* __restrict__ Zb,
+                                                            long long ldz, int w1,
+                                                            const double* __restrict__ wvec,
+                                                            double scale,
+                                                            double* __restrict__ out) {
+  extern __shared__ uint8_t jw_raw[];
+  JwSmem& S = *reinterpret_cast<JwSmem*>(smem_align(jw_raw, 16));
+  const int tid = threadIdx.x;
+  const int tq = tid & 127, half = tid >> 7;
   const int j0 = blockIdx.x * JW_J;
   const int q = blockIdx.y * 128 + tq;
   const int din = T.din;
   const int jb = j0 + half * 16;
+  const int nchunks = static_cast<int>((T.m + JW_P - 1) / JW_P);
   double acc[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) acc[r] = 0.0;
-  for (long long p0 = 0; p0 < T.m; p0 += JW_P) {
-    const int np = static_cast<int>(min(static_cast<long long>(JW_P), T.m - p0));
-    __syncthreads();
-    if (threadIdx.x < JW_P) {
-      const int pp = threadIdx.x;
-      if (pp < np) {
-        const long long p = p0 + pp;
+  // register stage of one chunk
+  double xr[2], ar[8];
+  // chunk c: x and w a into registers; the point info straight into buffer c & 1
+  // (its last reader, the compaction of chunk c - 2, precedes the last barrier)
+  auto load = [&](int c) {
+    const long long p0 = static_cast<long long>(c) * JW_P;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const long long p = p0 + (tid >> 5) + 8 * k;
+      const int j = j0 + (tid & 31);
+      double x = 0.0;
+      if (p < T.m) {
+        const ClassDev& C = T.c[find_class(T, p)];
+        x = j < din ? __ldg(C.pts + (p - C.row0) * din + j) : (j == din ? 1.0 : 0.0);
+      }
+      xr[k] = x;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const long long p = p0 + (tid >> 7) + 2 * k;
+      double a = 0.0;
+      if (p < T.m && q < w1) {
+        const ClassDev& C = T.c[find_class(T, p)];
+        a = __ldg(wvec + p) * __ldg(Zb + (C.act0 + (p - C.row0) * C.nch) * ldz + q);
+      }
+      ar[k] = a;
+    }
+    if (tid < JW_P) {
+      const int b = c & 1;
+      const long long p = p0 + tid;
+      int ng = 0;
+      if (p < T.m) {
         const ClassDev& C = T.c[find_class(T, p)];
         const long long i = p - C.row0;
-        swt[pp] = wvec[p];
-        szrow[pp] = (C.act0 + i * C.nch) * ld;
-        sng[pp] = C.ngrad;
-        for (int g = 0; g < C.ngrad; ++g) sgd[pp][g] = gdim(C, g, i);
-      } else {
-        swt[pp] = 0.0;
-        szrow[pp] = 0;
-        sng[pp] = 0;
+        S.swt[b][tid] = __ldg(wvec + p);
+        S.szrow[b][tid] = (C.act0 + i * C.nch) * ldz;
+        ng = C.ngrad;
+        for (int g = 0; g < ng; ++g) S.sgd[b][tid][g] = gdim(C, g, i);
       }
+      S.sng[b][tid] = ng;
     }
-    for (int e = threadIdx.x; e < JW_P * JW_J; e += 256) {
-      const int pp = e / JW_J, jj = e - (e / JW_J) * JW_J;
-      const int j = j0 + jj;
-      double x = 0.0;
-      if (pp < np) {
-        const long long p = p0 + pp;
-        const ClassDev& C = T.c[find_class(T, p)];
-        x = j < din ? C.pts[(p - C.row0) * din + j] : (j == din ? 1.0 : 0.0);
-      }
-      xs[pp][jj] = x;
+  };
+  auto apply = [&](int b) {  // one-hot rows of the chunk compacted into list b
+    if (q >= w1) return;
+    const int n = S.lcnt[b];
+    for (int t = 0; t < n; ++t) {
+      const int d = S.ld[b][t];
+      if (d < jb || d >= jb + 16) continue;
+      const double v = S.lw[b][t] * __ldg(Zb + S.lz[b][t] + q);
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (d == jb + r) acc[r] += v;
     }
+  };
+  if (nchunks > 0) load(0);
+  for (int c = 0; c < nchunks; ++c) {
+    const int b = c & 1;
+    // registers -> buffer b (its last readers finished before the previous barrier)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) S.xs[b][(tid >> 5) + 8 * k][tid & 31] = xr[k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) S.was[b][(tid >> 7) + 2 * k][tq] = ar[k];
     __syncthreads();
-    for (int e = threadIdx.x; e < JW_P * 128; e += 256) {
-      const int pp = e >> 7, qq = e & 127;
-      const int qg = blockIdx.y * 128 + qq;
-      was[pp][qq] = (pp < np && qg < w1) ? swt[pp] * Zb[szrow[pp] + qg] : 0.0;
-    }
-    if (threadIdx.x < 32) {  // deterministic compaction of the chunk's one-hot rows
+    if (tid < 32) {  // compact this chunk's one-hot rows into list b
       int base = 0;
-      for (int e0 = 0; e0 < JW_P * MAXG; e0 += 32) {
-        const int e = e0 + static_cast<int>(threadIdx.x);
+      for (int e0 = 0; e0 < JW_L; e0 += 32) {
+        const int e = e0 + tid;
         const int pp = e / MAXG, g = e - (e / MAXG) * MAXG;
-        const int d = (e < JW_P * MAXG && g < sng[pp]) ? sgd[pp][g] : -1;
+        const int d = (e < JW_L && g < S.sng[b][pp]) ? S.sgd[b][pp][g] : -1;
         const bool hit = d >= j0 && d < j0 + JW_J;
-        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
         if (hit) {
-          const int pos = base + __popc(b & ((1u << threadIdx.x) - 1u));
-          lst[pos] = (pp << 8) | g;
-          lsd[pos] = d;
+          const int pos = base + __popc(bal & ((1u << tid) - 1u));
+          S.lz[b][pos] = S.szrow[b][pp] + (1 + g) * ldz;
+          S.lw[b][pos] = S.swt[b][pp];
+          S.ld[b][pos] = d;
         }
-        base += __popc(b);
+        base += __popc(bal);
       }
-      if (threadIdx.x == 0) lcnt = base;
+      if (tid == 0) S.lcnt[b] = base;
     }
-    __syncthreads();
+    if (c + 1 < nchunks) load(c + 1);  // in flight during the products below
+    const int np = static_cast<int>(min(static_cast<long long>(JW_P),
+                                        T.m - static_cast<long long>(c) * JW_P));
     for (int pp = 0; pp < np; ++pp) {
-      const double a = was[pp][tq];
-      const double2* xr = reinterpret_cast<const double2*>(&xs[pp][half * 16]);
+      const double a = S.was[b][pp][tq];
+      const double2* xv2 = reinterpret_cast<const double2*>(&S.xs[b][pp][half * 16]);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        const double2 xv = xr[r];
+        const double2 xv = xv2[r];
         acc[2 * r] = fma(xv.x, a, acc[2 * r]);
         acc[2 * r + 1] = fma(xv.y, a, acc[2 * r + 1]);
       }
     }
-    if (q < w1) {
-      for (int t = 0; t < lcnt; ++t) {
-        const int d = lsd[t];
-        if (d < jb || d >= jb + 16) continue;
-        const int pp = lst[t] >> 8, g = lst[t] & 255;
-        const double v = swt[pp] * Zb[szrow[pp] + (1 + g) * ld + q];
-#pragma unroll
-        for (int r = 0; r < 16; ++r)
-          if (d == jb + r) acc[r] += v;
-      }
-    }
+    if (c >= 1) apply(b ^ 1);  // previous chunk's list (complete since this barrier)
   }
+  __syncthreads();
+  if (nchunks > 0) apply((nchunks - 1) & 1);
   if (q >= w1) return;
 #pragma unroll
   for (int r = 0; r < 16; ++r)
@@ -876,11 +910,11 @@ struct Plan {
 };
 
 // split count for a small M x N output over a long K (>= 256 columns per split,
-// about two waves of 128x128 tiles, no empty split)
+// one wave of 128x128 tiles -- one CTA per SM -- and no empty split)
 static int wide_k_splits(int nsm, long long M, long long N, long long K) {
   const long long tiles = ((M + 127) / 128) * ((N + 127) / 128);
   const long long kc = (K + 15) / 16;
-  long long S = (2LL * nsm + tiles - 1) / tiles;
+  long long S = std::max(1LL, nsm / tiles);
   S = std::max(1LL, std::min(S, kc / 16));
   const long long per = (kc + S - 1) / S;
   return static_cast<int>((kc + per - 1) / per);
@@ -2430,7 +2464,14 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   if (P.wide_in) {
     const int w1 = static_cast<int>(P.w[1]);
     dim3 g(static_cast<unsigned>((P.w[0] + 1 + JW_J - 1) / JW_J), (w1 + 127) / 128);
-    k_jt_input_wide<<<g, 256, 0, s>>>(P.T, B.Zb[0], P.ld[1], w1, w, scale, out + P.off[0]);
+    static bool attr[64] = {false};
+    if (!attr[ctx->device & 63]) {
+      cudaError_t e = cudaFuncSetAttribute(k_jt_input_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(kJwSmem));
+      if (e != cudaSuccess) return cuda_status(ctx, e, "jt_input_wide smem attribute");
+      attr[ctx->device & 63] = true;
+    }
+    k_jt_input_wide<<<g, 256, kJwSmem, s>>>(P.T, B.Zb[0], P.ld[1], w1, w, scale, out + P.off[0]);
   } else {
     const int w1 = static_cast<int>(P.w[1]);
     dim3 g((w1 + 127) / 128, S.nchunks);

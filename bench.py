@@ -28,6 +28,7 @@ import subprocess
 import sys
 import threading
 import time
+from dataclasses import replace
 
 import numpy as np
 
@@ -234,7 +235,7 @@ def run_ours(args, cfg):
 
         comm = Comm()
     rng = np.random.default_rng(1000 if world > 1 else 1000 + rank)
-    total = args.warmup + args.steps
+    total = args.warmup + args.steps + 2  # +2: the pipelined loop's ramp (see below)
     maps = []
     base = None
     for _ in range(total):
@@ -309,9 +310,34 @@ def run_ours(args, cfg):
             return theta, step
         return P.ParameterVector(K.axpby(ls.eta, delta, 1.0, theta.tensor), theta.layout), step
 
-    for i in range(args.warmup):
-        theta, _ = one_step(maps[i], theta)
-    launches = 0 if args.profile else _count_our_kernels(lambda: one_step(maps[args.warmup], theta))
+    # the product's pipelined loop (optimizer._pipelined_loop: step i+1 queued before
+    # step i's results are read, selection and update on the device) where it applies
+    from paper_2505_21404_b200.optimizer import TrainTrace, _dngd_loop, _pipeline_ok
+
+    pipelined = (not sharded and not tiles and sum(cfg["counts"]) < cfg["dense_threshold"]
+                 and _pipeline_ok(maps[0], config))
+
+    def run_loop(first, count, theta, on_step=None):
+        sub = maps[first:first + count]
+        tr = TrainTrace(problem=problem.name, method="dngd", seed=0)
+        _dngd_loop(tr, lambda it: sub[min(it, count) - 1], theta, replace(config, max_iters=count),
+                   rng, None, on_step)
+        if tr.aborted:
+            raise SystemExit(f"bench loop aborted: {tr.abort_reason}")
+        return tr.final_theta
+
+    if pipelined:
+        theta = run_loop(0, args.warmup, theta)
+    else:
+        for i in range(args.warmup):
+            theta, _ = one_step(maps[i], theta)
+    if args.profile:
+        launches = 0
+    elif pipelined:  # per iteration of the loop: (3 iterations - 1 iteration) / 2
+        launches = (_count_our_kernels(lambda: run_loop(args.warmup, 3, theta))
+                    - _count_our_kernels(lambda: run_loop(args.warmup, 1, theta))) // 2
+    else:
+        launches = _count_our_kernels(lambda: one_step(maps[args.warmup], theta))
     for mp in maps:
         mp._cache = None  # the counting step must not pre-assemble a timed step's Jacobian
     clocks = ClockSampler(local)
@@ -320,13 +346,34 @@ def run_ours(args, cfg):
         dist.barrier()
     clocks.start()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with timing.collect() as tm:
-        s.record()
-        for i in range(args.steps):
-            theta, last = one_step(maps[args.warmup + i], theta)
-        e.record()
+    if pipelined:
+        # steady state of the pipelined loop: on_step(i) runs when iteration i+1 is
+        # already queued, so events recorded there bracket iterations 3 .. K+2 of a
+        # K+2 iteration run (device time of exactly K iterations, no ramp)
+        tm = timing.StageTimer()
+
+        def mark(it, th, step, ls):
+            if it == 1:
+                s.record()
+            if it == 2:
+                timing._ACTIVE = tm  # fetches of iterations 3 .. K+2
+            if it == args.steps + 1:
+                e.record()
+
+        try:
+            theta = run_loop(args.warmup, args.steps + 2, theta, mark)
+        finally:
+            timing._ACTIVE = None
         torch.cuda.synchronize()
         stages, counts = tm.summary_ms()
+    else:
+        with timing.collect() as tm:
+            s.record()
+            for i in range(args.steps):
+                theta, last = one_step(maps[args.warmup + i], theta)
+            e.record()
+            torch.cuda.synchronize()
+            stages, counts = tm.summary_ms()
     dev_s = s.elapsed_time(e) * 1e-3
     if dist:
         t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
@@ -351,11 +398,13 @@ def run_ours(args, cfg):
         P.PinnResidualMap._device = counting_device
     marks = {}
 
+    lag = 1 if pipelined else 0  # pipelined: iteration i+1 is queued when on_step(i) runs
+
     def on_step(it, th, step, ls):
-        if it == args.warmup:
+        if it == args.warmup - lag:
             torch.cuda.synchronize()
             marks["t0"] = time.perf_counter()
-        if it == args.warmup + args.steps:
+        if it == args.warmup + args.steps - lag:
             torch.cuda.synchronize()
             marks["t1"] = time.perf_counter()
 
@@ -382,6 +431,8 @@ def run_ours(args, cfg):
         # per step the host reads: loss (8 B), |v|, |a| (16 B), Cholesky info (4 B),
         # 31 line-search losses (248 B), the delta-nonzero flag (1 B)
         d2h = (8 + 16 + 4 + 8 * config.line_search_points + 1) * world
+        if pipelined:  # packed results + device selection, one pinned buffer per step
+            d2h = 8 * (10 + config.line_search_points) * world
         e2e = {"value": args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "aborted": tr.aborted}
 

@@ -112,6 +112,28 @@ int dngd_dot(dngd_ctx* ctx, void* stream, int64_t n, const double* x, const doub
 int dngd_axpby(dngd_ctx* ctx, void* stream, int64_t n, double a, const double* x, double b,
                const double* y, double* out);
 
+/* ---- device-side loop decisions (optimizer.py:148-166 line_search selection and
+ *      optimizer.py:226-247 accept / reject bookkeeping), so that consecutive loop
+ *      iterations can be queued without a host round trip ---------------------
+ * dngd_ls_select: from the ncand line-search losses along etas (descending), the
+ * current residual sum of squares rr (loss = rr / 2), the Cholesky info (as a
+ * double, 0 = success) and
+ * anyd (delta has a nonzero entry, as a double 0/1) writes
+ *   sel[0] = eta, sel[1] = loss after the step, sel[2] = status, sel[3] = index
+ * with status 0 = accepted, 1 = rejected (no finite candidate, or worse than the
+ * current loss when reject_if_worse), 2 = factorisation failed, 3 = non-finite
+ * current loss.  Ties pick the larger eta (first minimum, like numpy argmin);
+ * anyd = 0 accepts eta = 1 with the current loss.  mult (the damping multiplier
+ * 10^rejections) becomes 1 on acceptance, 10 * mult on rejection, and is left
+ * alone for status 2 / 3 (the host handles those). */
+int dngd_ls_select(dngd_ctx* ctx, void* stream, const double* losses, int ncand,
+                   const double* etas, const double* rr, const double* info, const double* anyd,
+                   int reject_if_worse, double* mult, double* sel);
+/* out = theta + sel[0] * delta if sel[2] == 0 (accepted), else theta
+ * (out may not alias delta; it may alias theta). */
+int dngd_theta_update(dngd_ctx* ctx, void* stream, int64_t n, const double* theta,
+                      const double* delta, const double* sel, double* out);
+
 /* ---- PINN residual map on device (replaces residuals.py:139-323 for
  *      PinnResidualMap with tanh MLPs; model.py:88-97, jets.py:285-294) ----- */
 #define DNGD_MAX_LAYERS 8

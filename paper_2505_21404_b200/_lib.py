@@ -80,6 +80,8 @@ _SIGS = {
                       c_vp, c_i64, c_i64, c_int, c_dbl, c_dbl, c_int], c_int),
     "dngd_dot": ([c_vp, c_vp, c_i64, c_vp, c_vp, c_vp], c_int),
     "dngd_axpby": ([c_vp, c_vp, c_i64, c_dbl, c_vp, c_dbl, c_vp, c_vp], c_int),
+    "dngd_ls_select": ([c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp], c_int),
+    "dngd_theta_update": ([c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp], c_int),
     "dngd_pinn_workspace": ([c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc), c_int, c_int,
                              ctypes.POINTER(c_size)], c_int),
     "dngd_assemble": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, ctypes.POINTER(ClassDesc), c_int,

@@ -8,6 +8,7 @@
 //            K f_vv (solver.py:208), J (J^T p) (solver.py:336).
 // Both are deterministic (fixed reduction order): bitwise-reproducible steps.
 
+#include <math_constants.h>
 #include <algorithm>
 
 #include "common.cuh"
@@ -190,7 +191,72 @@ __global__ void __launch_bounds__(512) k_dot_multi(long long n, const double* __
 __global__ void k_axpby(long long n, double a, const double* __restrict__ x, double b,
                         const double* __restrict__ y, double* __restrict__ out) {
   const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k < n) out[k] = a * x[k] + (y ? b * y[k] : 0.0);
+  if (k < n) out[k] = fma(a, x[k], y ? b * y[k] : 0.0);
+}
+
+// line-search selection + accept/reject bookkeeping on the device (one warp)
+__global__ void k_ls_select(const double* __restrict__ losses, int ncand,
+                            const double* __restrict__ etas, const double* __restrict__ rr,
+                            const double* __restrict__ info, const double* __restrict__ anyd,
+                            int reject_if_worse, double* __restrict__ mult,
+                            double* __restrict__ sel) {
+  const int lane = threadIdx.x;
+  // first minimum over the finite losses: (value, index) min-reduction
+  double best = CUDART_INF;
+  int bi = 0x7fffffff;
+  for (int k = lane; k < ncand; k += 32) {
+    const double v = losses[k];
+    if (isfinite(v) && (v < best || (v == best && k < bi))) {
+      best = v;
+      bi = k;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov < best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if (lane != 0) return;
+  const double loss = 0.5 * rr[0];
+  double eta = 1.0, lsl = loss, status = 0.0, idx = 0.0;
+  if (!isfinite(loss)) {
+    status = 3.0;
+  } else if (*info != 0.0) {
+    status = 2.0;
+  } else if (*anyd == 0.0) {
+    // zero step: accepted with eta = 1 and the current loss (optimizer.py:222-223)
+  } else if (bi == 0x7fffffff) {
+    status = 1.0;
+    lsl = CUDART_NAN;
+  } else {
+    eta = etas[bi];
+    lsl = best;
+    idx = bi;
+    if (reject_if_worse && best > loss) status = 1.0;
+  }
+  if (status == 0.0) {
+    *mult = 1.0;
+  } else if (status == 1.0) {
+    *mult = 10.0 * *mult;
+  }
+  sel[0] = eta;
+  sel[1] = lsl;
+  sel[2] = status;
+  sel[3] = idx;
+}
+
+__global__ void k_theta_update(long long n, const double* __restrict__ theta,
+                               const double* __restrict__ delta, const double* __restrict__ sel,
+                               double* out) {
+  const long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const bool take = sel[2] == 0.0;
+  const double t = theta[k];
+  out[k] = take ? fma(sel[0], delta[k], t) : t;  // == dngd_axpby(eta, delta, 1, theta)
 }
 
 }  // namespace dngd
@@ -263,6 +329,24 @@ extern "C" int dngd_dot(dngd_ctx* ctx, void* stream, int64_t n, const double* x,
     k_dot<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(n, x, y, out_dev);
   }
   return cuda_status(ctx, cudaGetLastError(), "dot");
+}
+
+extern "C" int dngd_ls_select(dngd_ctx* ctx, void* stream, const double* losses, int ncand,
+                              const double* etas, const double* rr, const double* info,
+                              const double* anyd, int reject_if_worse, double* mult,
+                              double* sel) {
+  if (ncand < 1) return set_error(ctx, DNGD_ERR_DIMENSION, "ls_select: no candidates");
+  k_ls_select<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(losses, ncand, etas, rr, info, anyd,
+                                                               reject_if_worse, mult, sel);
+  return cuda_status(ctx, cudaGetLastError(), "ls_select");
+}
+
+extern "C" int dngd_theta_update(dngd_ctx* ctx, void* stream, int64_t n, const double* theta,
+                                 const double* delta, const double* sel, double* out) {
+  if (n <= 0) return DNGD_OK;
+  k_theta_update<<<static_cast<unsigned>((n + 255) / 256), 256, 0,
+                   static_cast<cudaStream_t>(stream)>>>(n, theta, delta, sel, out);
+  return cuda_status(ctx, cudaGetLastError(), "theta_update");
 }
 
 extern "C" int dngd_axpby(dngd_ctx* ctx, void* stream, int64_t n, double a, const double* x,

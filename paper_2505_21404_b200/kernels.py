@@ -197,6 +197,20 @@ def axpby(a: float, x: torch.Tensor, b: float = 0.0, y: torch.Tensor | None = No
     return out
 
 
+def ls_select(losses, etas, rr, info, anyd, reject_if_worse, mult, sel):
+    """Device-side line-search selection and accept/reject bookkeeping (see the
+    header): sel <- (eta, loss after, status, index); mult updated in place."""
+    call("dngd_ls_select", ctx(), stream_handle(), ptr(losses), losses.numel(), ptr(etas), ptr(rr),
+         ptr(info), ptr(anyd), int(bool(reject_if_worse)), ptr(mult), ptr(sel))
+
+
+def theta_update(theta, delta, sel, out):
+    """out = theta + sel[0] delta when sel[2] == 0 (accepted), else theta."""
+    call("dngd_theta_update", ctx(), stream_handle(), theta.numel(), ptr(theta), ptr(delta),
+         ptr(sel), ptr(out))
+    return out
+
+
 # ---------------------------------------------------------------- PINN map
 
 

@@ -205,101 +205,315 @@ def _budget_reached(config: OptimizerConfig, iteration: int, clock: _Clock) -> b
     return clock.elapsed() >= config.wall_seconds
 
 
+def _eager_body(rmap, theta, config: OptimizerConfig, rng, rejections: int, redo=False):
+    """One iteration up to the line-search result (optimizer.py:216-229): returns
+    (step, ls, loss).  redo=True skips the fused device attempt (known to fail its
+    factorisation) and goes straight to the retry ladder."""
+    from . import kernels as K
+
+    fused = None
+    dense = rmap.m < config.dense_threshold
+    jfree = dense and getattr(rmap, "jfree", lambda: False)()
+    mult = 10.0**rejections
+    if dense and not redo:
+        # device-resident damping, step and line search: one host sync
+        # (solver.fused_dense_step); loss comes back with the losses
+        fused = dense_iteration(rmap, theta, config.use_ga, config.line_search_points,
+                                config.lam_cap, mult)
+        loss, r = fused[3], fused[4]
+        if fused[0] is None:
+            fused = None  # factorisation failed: eager path keeps the retry ladder
+        J = None if jfree else rmap.jacobian_t(theta)
+    elif dense:
+        if jfree:
+            r, J = rmap.residuals_act_t(theta), None
+        else:
+            r, J = rmap.linearize_t(theta)
+        loss = 0.5 * float(K.dot(r, r).item())
+    else:
+        jfree = bool(getattr(rmap, "jfree_pcg", lambda: False)())
+        if jfree:  # J-free PCG: residuals and activations only
+            r, J = rmap.residuals_act_t(theta), None
+        else:
+            r, J = rmap.linearize_t(theta)
+        loss = 0.5 * float(K.dot(r, r).item())
+    if not np.isfinite(loss):
+        from .residuals import _raise_nonfinite
+
+        _raise_nonfinite(r, rmap.partition())
+    lam = lm_damping(loss, config.lam_cap) * mult
+    if fused is None:
+        g = None
+        if not jfree:
+            with stage("gemv"):
+                g = K.gemv_t(J, r, rmap.n)
+        step = _dispatch_step(rmap, theta, g, lam, config, rng)
+    else:
+        step = fused[0]
+    delta_t = step.delta.tensor
+    if fused is not None:
+        etas = 2.0 ** -np.arange(config.line_search_points, dtype=np.float64)
+        if not fused[2]:
+            ls = LineSearchResult(1.0, loss, False, 0, False)
+        else:
+            ls = _select(fused[1], etas, loss, config.line_search_points)
+    elif not bool(delta_t.any().item()):
+        ls = LineSearchResult(1.0, loss, False, 0, False)
+    else:
+        ls = device_line_search(rmap, theta, delta_t, loss, config.line_search_points)
+    return step, ls, loss
+
+
+class _Book:
+    """Row bookkeeping shared by the eager and the pipelined loop (optimizer.py:226-262)."""
+
+    def __init__(self, trace, config, clock, rel_l2_fn, on_step):
+        self.trace, self.config, self.clock = trace, config, clock
+        self.rel_l2_fn, self.on_step = rel_l2_fn, on_step
+        self.rejections = 0
+        self.rel_pending = []  # (row, handle) of asynchronous rel-L2 evaluations
+
+    def _rel(self, theta, row):
+        fn = self.rel_l2_fn
+        if fn is None:
+            return
+        if getattr(fn, "enqueue", None) is not None and self.rel_pending is not None:
+            self.rel_pending.append((row, fn.enqueue(theta)))
+        else:
+            row.rel_l2 = fn(theta)
+
+    def resolve(self, keep: int = 0):
+        """Fill the rel-L2 of all but the last `keep` pending rows."""
+        fn = self.rel_l2_fn
+        while len(self.rel_pending) > keep:
+            row, h = self.rel_pending.pop(0)
+            row.rel_l2 = fn.fetch(h)
+
+    def rejected(self, iteration, theta, step, ls, loss) -> bool:
+        """Record a rejected step; True when the loop must stop."""
+        self.rejections += 1
+        row = TraceRow(iteration, self.clock.stamp(), loss, lam=step.lambda_used,
+                       cg_iterations=step.cg_iterations)
+        self._rel(theta, row)
+        self.trace.rows.append(row)
+        if self.on_step is not None:
+            self.on_step(iteration, theta, step, ls)
+        if self.rejections >= MAX_CONSECUTIVE_REJECTIONS:
+            self.trace.aborted = True
+            self.trace.abort_reason = (
+                f"{self.rejections} consecutive step rejections; last damping "
+                f"{step.lambda_used:.3e}"
+            )
+            return True
+        return False
+
+    def accepted(self, iteration, theta_new, step, ls):
+        self.rejections = 0
+        if self.on_step is not None:
+            self.on_step(iteration, theta_new, step, ls)
+        row = TraceRow(iteration, self.clock.stamp(), ls.loss, lam=step.lambda_used, eta=ls.eta,
+                       cg_iterations=step.cg_iterations,
+                       ga_ratio=step.ga_ratio if step.ga_ratio is not None else float("nan"))
+        self._rel(theta_new, row)
+        self.trace.rows.append(row)
+
+    def abort(self, iteration, exc):
+        self.trace.aborted = True
+        self.trace.abort_reason = f"error at iteration {iteration}: {exc!r}"
+
+
+def _pipeline_ok(rmap, config) -> bool:
+    import os
+
+    from .solver import graph_eligible
+
+    return (os.environ.get("DNGD_NO_PIPELINE") is None and rmap.m < config.dense_threshold
+            and isinstance(rmap, PinnResidualMap) and graph_eligible(rmap))
+
+
 def _dngd_loop(trace: TrainTrace, rmap_provider, theta: ParameterVector, config: OptimizerConfig,
                rng, rel_l2_fn=None, on_step=None) -> TrainTrace:
-    """optimizer.py:193-265 with device-resident state."""
+    """optimizer.py:193-265 with device-resident state.  Dense PINN iterations run
+    pipelined (_pipelined_loop); everything else step by step."""
     from . import kernels as K
 
     clock = _Clock(config.deterministic_timing)
     rmap = rmap_provider(1)
     rel = rel_l2_fn(theta) if rel_l2_fn else float("nan")
     trace.rows.append(TraceRow(0, clock.stamp(), rmap.loss(theta), rel_l2=rel))
-
-    rejections = 0
+    book = _Book(trace, config, clock, rel_l2_fn, on_step)
+    if _pipeline_ok(rmap, config):
+        theta = _pipelined_loop(book, rmap_provider, theta, config, rng)
+        trace.final_theta = theta
+        return trace
+    book.rel_pending = None  # eager loop: rel-L2 evaluated in place
     iteration = 0
     while True:
         iteration += 1
         if _budget_reached(config, iteration, clock):
             break
-        fused = None
         try:
             rmap = rmap_provider(iteration)
-            dense = rmap.m < config.dense_threshold
-            jfree = dense and getattr(rmap, "jfree", lambda: False)()
-            mult = 10.0**rejections
-            if dense:
-                # device-resident damping, step and line search: one host sync
-                # (solver.fused_dense_step); loss comes back with the losses
-                fused = dense_iteration(rmap, theta, config.use_ga, config.line_search_points,
-                                        config.lam_cap, mult)
-                loss, r = fused[3], fused[4]
-                if fused[0] is None:
-                    fused = None  # factorisation failed: eager path keeps the retry ladder
-                J = None if jfree else rmap.jacobian_t(theta)
-            else:
-                jfree = bool(getattr(rmap, "jfree_pcg", lambda: False)())
-                if jfree:  # J-free PCG: residuals and activations only
-                    r, J = rmap.residuals_act_t(theta), None
-                else:
-                    r, J = rmap.linearize_t(theta)
-                loss = 0.5 * float(K.dot(r, r).item())
-                if not np.isfinite(loss):
-                    from .residuals import _raise_nonfinite
-
-                    _raise_nonfinite(r, rmap.partition())
-            lam = lm_damping(loss, config.lam_cap) * mult
-            if fused is None:
-                g = None
-                if not jfree:
-                    with stage("gemv"):
-                        g = K.gemv_t(J, r, rmap.n)
-                step = _dispatch_step(rmap, theta, g, lam, config, rng)
-            else:
-                step = fused[0]
+            step, ls, loss = _eager_body(rmap, theta, config, rng, book.rejections)
         except Exception as exc:
-            trace.aborted = True
-            trace.abort_reason = f"error at iteration {iteration}: {exc!r}"
+            book.abort(iteration, exc)
             break
-        delta_t = step.delta.tensor
-        if fused is not None:
-            etas = 2.0 ** -np.arange(config.line_search_points, dtype=np.float64)
-            if not fused[2]:
-                ls = LineSearchResult(1.0, loss, False, 0, False)
-            else:
-                ls = _select(fused[1], etas, loss, config.line_search_points)
-        elif not bool(delta_t.any().item()):
-            ls = LineSearchResult(1.0, loss, False, 0, False)
-        else:
-            ls = device_line_search(rmap, theta, delta_t, loss, config.line_search_points)
         if ls.rejected or (config.reject_if_worse and ls.loss > loss):
-            rejections += 1
-            trace.rows.append(
-                TraceRow(iteration, clock.stamp(), loss,
-                         rel_l2=rel_l2_fn(theta) if rel_l2_fn else float("nan"),
-                         lam=step.lambda_used, cg_iterations=step.cg_iterations)
-            )
-            if on_step is not None:
-                on_step(iteration, theta, step, ls)
-            if rejections >= MAX_CONSECUTIVE_REJECTIONS:
-                trace.aborted = True
-                trace.abort_reason = (
-                    f"{rejections} consecutive step rejections; last damping "
-                    f"{step.lambda_used:.3e}"
-                )
+            if book.rejected(iteration, theta, step, ls, loss):
                 break
             continue
-        rejections = 0
-        theta = ParameterVector(K.axpby(ls.eta, delta_t, 1.0, theta.tensor), theta.layout)
-        if on_step is not None:
-            on_step(iteration, theta, step, ls)
-        trace.rows.append(
-            TraceRow(iteration, clock.stamp(), ls.loss,
-                     rel_l2=rel_l2_fn(theta) if rel_l2_fn else float("nan"),
-                     lam=step.lambda_used, eta=ls.eta, cg_iterations=step.cg_iterations,
-                     ga_ratio=step.ga_ratio if step.ga_ratio is not None else float("nan"))
-        )
+        theta = ParameterVector(K.axpby(ls.eta, step.delta.tensor, 1.0, theta.tensor),
+                                theta.layout)
+        book.accepted(iteration, theta, step, ls)
     trace.final_theta = theta
     return trace
+
+
+def _pipelined_loop(book: _Book, rmap_provider, theta: ParameterVector, config: OptimizerConfig,
+                    rng) -> ParameterVector:
+    """The dense loop with iteration i+1 queued before iteration i's results are read
+    (SURVEY 8f rank 1).  The line-search selection, the theta update and the
+    rejection multiplier run on the device inside the iteration's CUDA graph
+    (solver._DenseGraph pipe_*), so the host only books rows one step behind.
+    Same trajectory as the eager loop: a factorisation failure or a non-finite
+    loss (rare) discards the queued successor and redoes the iteration eagerly
+    with the retry ladder before the pipeline resumes."""
+    import collections
+
+    from .solver import StepResult as _SR
+    from .solver import _DenseGraph
+
+    config_pc = config.line_search_points
+    etas = 2.0 ** -np.arange(config_pc, dtype=np.float64)
+    G = None
+    pending = collections.deque()  # (iteration, rmap, ticket)
+    iteration = 0
+    stop = False
+    cur = theta  # theta after the last booked iteration
+
+    def queue_next() -> bool:
+        nonlocal iteration, G
+        iteration += 1
+        if _budget_reached(config, iteration, book.clock):
+            return False
+        rmap = rmap_provider(iteration)
+        if G is None:
+            G = _DenseGraph.get(rmap, config.use_ga, config_pc, config.lam_cap)
+            G.pipe_start(cur.tensor, config.reject_if_worse)
+        if not (_pipeline_ok(rmap, config) and G.pipe_matches(rmap)):
+            raise _Unpipelinable(iteration, rmap)
+        pending.append((iteration, rmap, G.pipe_enqueue(rmap)))
+        return True
+
+    def eager_redo(it, rmap, theta_in):
+        """Iteration `it` on the host-driven path; returns (theta_after, stop)."""
+        try:
+            step, ls, loss = _eager_body(rmap, theta_in, config, rng, book.rejections,
+                                         redo=True)
+        except Exception as exc:
+            book.abort(it, exc)
+            return theta_in, True
+        if ls.rejected or (config.reject_if_worse and ls.loss > loss):
+            return theta_in, book.rejected(it, theta_in, step, ls, loss)
+        from . import kernels as K
+
+        new = ParameterVector(K.axpby(ls.eta, step.delta.tensor, 1.0, theta_in.tensor),
+                              theta_in.layout)
+        book.accepted(it, new, step, ls)
+        return new, False
+
+    try:
+        more = queue_next()
+        while pending and not stop:
+            if more:
+                more = queue_next()
+            it, rmap, ticket = pending.popleft()
+            arr, t_after, delta = G.pipe_fetch(ticket)
+            book.resolve(keep=0)
+            rr, lam_used, v2, a2, anyd = arr[1], arr[2], arr[3], arr[4], arr[5]
+            sel = arr[6 + config_pc: 10 + config_pc]
+            status = int(sel[2])
+            loss = 0.5 * float(rr)
+            view = ParameterVector(t_after, cur.layout)
+            if status >= 2:  # failed factorisation / non-finite loss: redo eagerly
+                succ = pending.popleft() if pending else None
+                if succ is not None:
+                    succ[2][1].synchronize()  # let the discarded successor drain
+                theta_in = ParameterVector(t_after.clone(), cur.layout)
+                cur, stop = eager_redo(it, rmap, theta_in)
+                if succ is not None and not stop:
+                    G.pipe_rewind(ticket, cur.tensor, 10.0**book.rejections)
+                    pending.appendleft((succ[0], succ[1], G.pipe_enqueue(succ[1])))
+                continue
+            v_norm = float(np.sqrt(v2))
+            ga = None
+            if config.use_ga and v_norm > 1e-12:
+                ga = 2.0 * float(np.sqrt(a2)) / v_norm
+            step = _SR(delta=ParameterVector(delta, cur.layout), lambda_used=float(lam_used),
+                       cg_iterations=0, ga_ratio=ga)
+            if status == 1:
+                losses = arr[6: 6 + config_pc]
+                ls = _select(losses, etas, loss, config_pc)
+                cur = view
+                stop = book.rejected(it, view, step, ls, loss)
+                continue
+            if anyd == 0.0:
+                ls = LineSearchResult(1.0, loss, False, 0, False)
+            else:
+                j = int(sel[3])
+                ls = LineSearchResult(float(etas[j]), float(sel[1]), float(sel[1]) > loss,
+                                      config_pc, False)
+            cur = view
+            book.accepted(it, view, step, ls)
+    except _Unpipelinable as u:
+        # a map the pipeline cannot run (shape change): drain and finish eagerly
+        while pending:
+            it, rmap, ticket = pending.popleft()
+            G.pipe_fetch(ticket)
+        book.resolve()
+        cur = ParameterVector(cur.tensor.clone(), cur.layout)
+        book.rel_pending = None
+        return _finish_eager(book, rmap_provider, cur, config, rng, u.iteration, u.rmap)
+    except Exception as exc:  # errors from the provider or the host bookkeeping
+        book.abort(iteration, exc)
+    while pending:  # stopped with a successor in flight: let it drain, ignore it
+        _, _, ticket = pending.popleft()
+        ticket[1].synchronize()
+    book.resolve()
+    return ParameterVector(cur.tensor.clone(), cur.layout)
+
+
+class _Unpipelinable(Exception):
+    def __init__(self, iteration, rmap):
+        super().__init__(iteration)
+        self.iteration, self.rmap = iteration, rmap
+
+
+def _finish_eager(book, rmap_provider, theta, config, rng, iteration, rmap):
+    from . import kernels as K
+
+    first = True
+    while True:
+        if not first:
+            iteration += 1
+            if _budget_reached(config, iteration, book.clock):
+                break
+        try:
+            if not first:
+                rmap = rmap_provider(iteration)
+            first = False
+            step, ls, loss = _eager_body(rmap, theta, config, rng, book.rejections)
+        except Exception as exc:
+            book.abort(iteration, exc)
+            break
+        if ls.rejected or (config.reject_if_worse and ls.loss > loss):
+            if book.rejected(iteration, theta, step, ls, loss):
+                break
+            continue
+        theta = ParameterVector(K.axpby(ls.eta, step.delta.tensor, 1.0, theta.tensor),
+                                theta.layout)
+        book.accepted(iteration, theta, step, ls)
+    return theta
 
 
 def dngd_minimize(residual_map: ResidualMap, theta, config: OptimizerConfig,
@@ -459,6 +673,25 @@ def _rel_l2_fn(problem, spec: MlpSpec):
         r = vmap.residuals_t(theta)
         return float(r.norm().item()) / denom
 
+    def enqueue(theta):
+        """Queue the evaluation (no host sync); fetch() reads it later."""
+        import torch
+
+        if denom == 0.0:
+            raise DomainError("reference values are identically zero on the grid")
+        nrm = vmap.residuals_t(theta).norm().reshape(1)
+        host = torch.empty(1, dtype=torch.float64, pin_memory=True)
+        host.copy_(nrm, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return host, ev
+
+    def fetch(handle):
+        host, ev = handle
+        ev.synchronize()
+        return float(host[0]) / denom
+
+    fn.enqueue, fn.fetch = enqueue, fetch
     return fn
 
 

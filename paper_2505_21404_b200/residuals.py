@@ -377,6 +377,16 @@ class LinearResidualMap(ResidualMap):
 _ACT_STATE: dict = {}  # which (theta version, map) the shared activation workspace holds
 
 
+def _upload(arr, dev):
+    """Host array -> device through pinned staging, queued on the current stream
+    without a host-side stream sync (a pageable copy would wait for the queued
+    work, which stalls the pipelined loop while it samples the next collocation)."""
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    return t.pin_memory().to(dev, non_blocking=True)
+
+
 class PinnResidualMap(ResidualMap):
     """Weighted PDE residuals of a tanh MLP, evaluated by the CUDA library."""
 
@@ -432,10 +442,8 @@ class PinnResidualMap(ResidualMap):
         keep = []
         for k, cls in enumerate(classes):
             op = self.problem.class_operator(cls.class_id)
-            pts = torch.as_tensor(np.ascontiguousarray(cls.points), device=dev)
-            f = torch.as_tensor(
-                np.ascontiguousarray(self.problem.class_data(cls), dtype=np.float64), device=dev
-            )
+            pts = _upload(cls.points, dev)
+            f = _upload(np.asarray(self.problem.class_data(cls), dtype=np.float64), dev)
             keep += [pts, f]
             d = arr[k]
             d.count = cls.count
@@ -459,21 +467,21 @@ class PinnResidualMap(ResidualMap):
                 if emb.shape != (cls.count, 1 + d.ngrad + (1 if d.nlap else 0),
                                  self.spec.input_dim):
                     raise DimensionError(f"input channels of class {cls.class_id}: {emb.shape}")
-                inp = torch.as_tensor(emb, device=dev)
+                inp = _upload(emb, dev)
                 keep.append(inp)
                 d.inputs = inp.data_ptr()
             if hasattr(self.problem, "point_grad_dims"):  # per-point derivative dims (STDE)
                 gi = np.ascontiguousarray(self.problem.point_grad_dims(cls), dtype=np.int32)
                 if gi.shape != (cls.count, d.ngrad):
                     raise DimensionError(f"point derivative dims of class {cls.class_id}: {gi.shape}")
-                gi_t = torch.as_tensor(gi, device=dev)
+                gi_t = _upload(gi, dev)
                 keep.append(gi_t)
                 d.grad_idx = gi_t.data_ptr()
             if hasattr(self.problem, "point_coefs"):  # per-point coefficients
                 co = np.ascontiguousarray(self.problem.point_coefs(cls, op), dtype=np.float64)
                 if co.shape != (cls.count, 1 + d.ngrad + (1 if d.nlap else 0)):
                     raise DimensionError(f"point coefficients of class {cls.class_id}: {co.shape}")
-                co_t = torch.as_tensor(co, device=dev)
+                co_t = _upload(co, dev)
                 keep.append(co_t)
                 d.coefs = co_t.data_ptr()
         mlp = K.mlp_desc(self.spec.layer_widths)
@@ -523,7 +531,8 @@ class PinnResidualMap(ResidualMap):
             K.assemble(d["mlp"], th, d["arr"], d["nclass"], r, self._J, self.col_range[0],
                        self.col_range[1], self._act_workspace())
         _ACT_STATE["key"] = (key, self._act_identity())
-        self._cache = (key, r, self._J)
+        _ACT_STATE["theta"] = th  # keeps the keyed storage alive (no address reuse)
+        self._cache = (key, r, self._J, th)
         return r, self._J
 
     def residuals_t(self, theta):
@@ -641,7 +650,8 @@ class PinnResidualMap(ResidualMap):
             with stage("activations"):
                 K.activations(d["mlp"], th, d["arr"], d["nclass"], r, self._act_workspace())
             _ACT_STATE["key"] = (self._key(th), self._act_identity())
-            self._rcache = (self._key(th), r)
+            _ACT_STATE["theta"] = th
+            self._rcache = (self._key(th), r, th)
         return self._rcache[1]
 
     def jvp_t(self, theta, v_t):
@@ -708,7 +718,8 @@ class PinnResidualMap(ResidualMap):
             K.gram_factored(d["mlp"], th, d["arr"], d["nclass"], r, K_out,
                             self._act_workspace())
         _ACT_STATE["key"] = (self._key(th), self._act_identity())
-        self._rcache = (self._key(th), r)
+        _ACT_STATE["theta"] = th
+        self._rcache = (self._key(th), r, th)
         return K_out
 
     def residuals_gram_t(self, theta, K_out):
@@ -731,7 +742,8 @@ class PinnResidualMap(ResidualMap):
             r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
             K.activations(d["mlp"], th, d["arr"], d["nclass"], r, self._act_workspace())
             _ACT_STATE["key"] = (self._key(th), self._act_identity())
-            self._rcache = (self._key(th), r)
+            _ACT_STATE["theta"] = th
+            self._rcache = (self._key(th), r, th)
         out = torch.empty(self.n, dtype=torch.float64, device=d["device"])
         scratch = K.workspace("jt", K.jt_workspace_bytes(d["mlp"], d["arr"], d["nclass"]))
         with stage("vjp"):

@@ -32,7 +32,10 @@
 
 constexpr int GF_BM = 64;  // G-rows per tile side
 constexpr int GF_STAGES = 4;
-constexpr int GF_THREADS = 128;  // 2 x 2 warps, 32 x 32 warp tiles
+constexpr int GF_WM = 2, GF_WN = 4;            // warps along G-rows / G-columns
+constexpr int GF_THREADS = 32 * GF_WM * GF_WN;  // 8 warps, 32 x 16 warp tiles
+constexpr int GF_MI = GF_BM / GF_WM / 8;        // 8x8 fragments per warp tile: rows
+constexpr int GF_NJ = GF_BM / GF_WN / 8;        //                               columns
 constexpr int GF_STAGE_BYTES = 2 * GF_BM * 128;
 constexpr int GF_H0_LD = 16;  // row pitch of the materialised input channels
 
@@ -86,23 +89,23 @@ __global__ void k_input_channels(Classes T, double* __restrict__ H0) {
 
 DNGD_DEV int gf_layer_chunks(const GramLayer& l) { return ((l.kh + 15) >> 4) + ((l.kz + 15) >> 4); }
 
-// K[point pairs] += S (G_H o G_Z) S^T for one warp's 32 x 32 G-block.  Fragment
+// K[point pairs] += S (G_H o G_Z) S^T for one warp's 32 x 16 G-block.  Fragment
 // (i, j): rows lrow = lane/4 (+8i), columns 2(lane%4)+{0,1} (+8j); G-row bits
 // below LGA are the channel, so the row channel is lrow mod a for every i.
 template <int LGA, int LGB, bool SEEDZ>
-DNGD_DEV void gf_epilogue(double2 (&accH)[4][4], double2 (&accZ)[4][4], double bias0,
+DNGD_DEV void gf_epilogue(double2 (&accH)[GF_MI][GF_NJ], double2 (&accZ)[GF_MI][GF_NJ], double bias0,
                           double bias1, const double* sA, const double* sB, double* Ks, int wm,
                           int wn, int lane) {
   const int lrow = lane >> 2;
   const bool own_r = (lrow & ((1 << LGA) - 1)) == 0;
   const bool own_c = LGB <= 1 || (lane & ((1 << (LGB > 1 ? LGB - 1 : 0)) - 1)) == 0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int gr = wm * 32 + i * 8 + lrow;
+  for (int i = 0; i < GF_MI; ++i) {
+    const int gr = wm * (GF_MI * 8) + i * 8 + lrow;
     const int pr = gr >> LGA;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gc = wn * 32 + j * 8 + 2 * (lane & 3);
+    for (int j = 0; j < GF_NJ; ++j) {
+      const int gc = wn * (GF_NJ * 8) + j * 8 + 2 * (lane & 3);
       // output layer: Zbar = per-row seeds (G^Z = seed_row * seed_col)
       double v0, v1;
       if (SEEDZ) {
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
   }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wm = warp / GF_WN, wn = warp - (warp / GF_WN) * GF_WN;
   const int lrow = lane >> 2;
   // per-thread constants of the epilogue (see gf_epilogue)
   const int chr = lrow & ((1 << lga) - 1);
@@ -215,11 +218,11 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
   const double bias1 = (chr == 0 && chc1 == 0) ? 1.0 : 0.0;
   const int epi = lga * 4 + lgb;
 
-  double2 accH[4][4], accZ[4][4];
+  double2 accH[GF_MI][GF_NJ], accZ[GF_MI][GF_NJ];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < GF_MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < GF_NJ; ++j) {
       accH[i][j] = make_double2(0.0, 0.0);
       accZ[i][j] = make_double2(0.0, 0.0);
     }
@@ -235,36 +238,36 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     __syncwarp();
     mbar_wait(&full[st], (f / GF_STAGES) & 1);
     const bool partH = (f - f_layer_start) < nh_cur;
-    const uint8_t* sa = smem + st * GF_STAGE_BYTES + (wm * 32 + lrow) * 128;
-    const uint8_t* sb = smem + st * GF_STAGE_BYTES + GF_BM * 128 + (wn * 32 + lrow) * 128;
+    const uint8_t* sa = smem + st * GF_STAGE_BYTES + (wm * GF_MI * 8 + lrow) * 128;
+    const uint8_t* sb = smem + st * GF_STAGE_BYTES + GF_BM * 128 + (wn * GF_NJ * 8 + lrow) * 128;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int sw = ((2 * (lane & 3) + h) ^ lrow) << 4;
-      double2 a[4], b[4];
+      double2 a[GF_MI], b[GF_NJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const double2*>(sa + i * 1024 + sw);
+      for (int i = 0; i < GF_MI; ++i) a[i] = *reinterpret_cast<const double2*>(sa + i * 1024 + sw);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const double2*>(sb + j * 1024 + sw);
+      for (int j = 0; j < GF_NJ; ++j) b[j] = *reinterpret_cast<const double2*>(sb + j * 1024 + sw);
       // the .x and .y halves go through separate passes so consecutive DMMAs on
-      // one accumulator are 16 instructions apart (no back-to-back dependency)
+      // one accumulator are MI*NJ instructions apart (no back-to-back dependency)
       if (partH) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < GF_MI; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(accH[i][j], a[i].x, b[j].x);
+          for (int j = 0; j < GF_NJ; ++j) dmma_8x8x4(accH[i][j], a[i].x, b[j].x);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < GF_MI; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(accH[i][j], a[i].y, b[j].y);
+          for (int j = 0; j < GF_NJ; ++j) dmma_8x8x4(accH[i][j], a[i].y, b[j].y);
       } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < GF_MI; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(accZ[i][j], a[i].x, b[j].x);
+          for (int j = 0; j < GF_NJ; ++j) dmma_8x8x4(accZ[i][j], a[i].x, b[j].x);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < GF_MI; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_8x8x4(accZ[i][j], a[i].y, b[j].y);
+          for (int j = 0; j < GF_NJ; ++j) dmma_8x8x4(accZ[i][j], a[i].y, b[j].y);
       }
     }
     __syncwarp();

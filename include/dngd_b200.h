@@ -129,6 +129,12 @@ int dngd_axpby(dngd_ctx* ctx, void* stream, int64_t n, double a, const double* x
 int dngd_ls_select(dngd_ctx* ctx, void* stream, const double* losses, int ncand,
                    const double* etas, const double* rr, const double* info, const double* anyd,
                    int reject_if_worse, double* mult, double* sel);
+/* GA combination (solver.py:211-213) with the gate evaluated on the device:
+ * scal[2] = |v|^2, scal[3] = |a|^2 (a may be NULL: no GA); take = |v| > 1e-12 and
+ * 2|a| <= 0.5 |v|; out = take ? v + a/2 : v; *anyd = 1.0 if out has a nonzero
+ * entry (it must hold 0.0 on entry).  out may alias v. */
+int dngd_ga_combine(dngd_ctx* ctx, void* stream, int64_t n, const double* v, const double* a,
+                    const double* scal, double* out, double* anyd);
 /* out = theta + sel[0] * delta if sel[2] == 0 (accepted), else theta
  * (out may not alias delta; it may alias theta). */
 int dngd_theta_update(dngd_ctx* ctx, void* stream, int64_t n, const double* theta,

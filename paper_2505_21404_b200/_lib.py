@@ -82,6 +82,7 @@ _SIGS = {
     "dngd_axpby": ([c_vp, c_vp, c_i64, c_dbl, c_vp, c_dbl, c_vp, c_vp], c_int),
     "dngd_ls_select": ([c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp], c_int),
     "dngd_theta_update": ([c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp], c_int),
+    "dngd_ga_combine": ([c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp], c_int),
     "dngd_pinn_workspace": ([c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc), c_int, c_int,
                              ctypes.POINTER(c_size)], c_int),
     "dngd_assemble": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, ctypes.POINTER(ClassDesc), c_int,

@@ -249,6 +249,31 @@ __global__ void k_ls_select(const double* __restrict__ losses, int ncand,
   sel[3] = idx;
 }
 
+// grid-stride; the any-nonzero flag is one store per CTA at most (a store per
+// warp from ~10^5 warps to one address serialises in L2)
+__global__ void __launch_bounds__(256) k_ga_combine(long long n, const double* v,
+                                                      const double* __restrict__ a,
+                                                      const double* __restrict__ scal, double* out,
+                                                      double* anyd) {
+  bool take = false;
+  if (a != nullptr) {
+    const double vn = sqrt(scal[2]), an = sqrt(scal[3]);
+    take = vn > 1e-12 && 2.0 * an <= 0.5 * vn;  // GA_NORM_GUARD, GA_RATIO_MAX
+  }
+  bool nz = false;
+  for (long long k = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double vk = v[k];
+    const double d = take ? fma(0.5, a[k], vk) : vk;  // == v + 0.5 a (0.5 a is exact)
+    out[k] = d;
+    nz |= d != 0.0;
+  }
+  if (__syncthreads_or(nz) && threadIdx.x == 0 &&
+      *reinterpret_cast<volatile double*>(anyd) == 0.0) {
+    *anyd = 1.0;  // order-free
+  }
+}
+
 __global__ void k_theta_update(long long n, const double* __restrict__ theta,
                                const double* __restrict__ delta, const double* __restrict__ sel,
                                double* out) {
@@ -339,6 +364,15 @@ extern "C" int dngd_ls_select(dngd_ctx* ctx, void* stream, const double* losses,
   k_ls_select<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(losses, ncand, etas, rr, info, anyd,
                                                                reject_if_worse, mult, sel);
   return cuda_status(ctx, cudaGetLastError(), "ls_select");
+}
+
+extern "C" int dngd_ga_combine(dngd_ctx* ctx, void* stream, int64_t n, const double* v,
+                               const double* a, const double* scal, double* out, double* anyd) {
+  if (n <= 0) return DNGD_OK;
+  const long long blocks = std::min<long long>((n + 255) / 256, 8LL * ctx->num_sms);
+  k_ga_combine<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      n, v, a, scal, out, anyd);
+  return cuda_status(ctx, cudaGetLastError(), "ga_combine");
 }
 
 extern "C" int dngd_theta_update(dngd_ctx* ctx, void* stream, int64_t n, const double* theta,

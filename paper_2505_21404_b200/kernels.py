@@ -204,6 +204,14 @@ def ls_select(losses, etas, rr, info, anyd, reject_if_worse, mult, sel):
          ptr(info), ptr(anyd), int(bool(reject_if_worse)), ptr(mult), ptr(sel))
 
 
+def ga_combine(v, a, scal, out, anyd):
+    """out = v + a/2 if the GA gate (from scal[2:4] = |v|^2, |a|^2) is open, else v;
+    anyd (zeroed by the caller) becomes 1 if out has a nonzero entry."""
+    call("dngd_ga_combine", ctx(), stream_handle(), v.numel(), ptr(v), ptr(a), ptr(scal), ptr(out),
+         ptr(anyd))
+    return out
+
+
 def theta_update(theta, delta, sel, out):
     """out = theta + sel[0] delta when sel[2] == 0 (accepted), else theta."""
     call("dngd_theta_update", ctx(), stream_handle(), theta.numel(), ptr(theta), ptr(delta),

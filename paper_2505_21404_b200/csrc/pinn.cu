@@ -548,15 +548,20 @@ __global__ void __launch_bounds__(256, 2) k_jt_input_wide(Classes T, const doubl
   extern __shared__ uint8_t jw_raw[];
   JwSmem& S = *reinterpret_cast<JwSmem*>(smem_align(jw_raw, 16));
   const int tid = threadIdx.x;
-  const int tq = tid & 127, half = tid >> 7;
+  // staging: thread column sq of the 128-neuron block; products: thread (jg, tq2)
+  // owns rows jb .. jb+7 and neurons q, q+1 (8 x 2 accumulators: one LDS.128 of
+  // w a and four of x per 16 FMAs)
+  const int sq = tid & 127;
+  const int sqg = blockIdx.y * 128 + sq;
+  const int tq2 = tid & 63, jg = tid >> 6;
   const int j0 = blockIdx.x * JW_J;
-  const int q = blockIdx.y * 128 + tq;
+  const int q = blockIdx.y * 128 + 2 * tq2;
   const int din = T.din;
-  const int jb = j0 + half * 16;
+  const int jb = j0 + jg * 8;
   const int nchunks = static_cast<int>((T.m + JW_P - 1) / JW_P);
-  double acc[16];
+  double acc[8][2];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) acc[r] = 0.0;
+  for (int r = 0; r < 8; ++r) acc[r][0] = acc[r][1] = 0.0;
   // register stage of one chunk
   double xr[2], ar[8];
   // chunk c: x and w a into registers; the point info straight into buffer c & 1
@@ -578,9 +583,9 @@ __global__ void __launch_bounds__(256, 2) k_jt_input_wide(Classes T, const doubl
     for (int k = 0; k < 8; ++k) {
       const long long p = p0 + (tid >> 7) + 2 * k;
       double a = 0.0;
-      if (p < T.m && q < w1) {
+      if (p < T.m && sqg < w1) {
         const ClassDev& C = T.c[find_class(T, p)];
-        a = __ldg(wvec + p) * __ldg(Zb + (C.act0 + (p - C.row0) * C.nch) * ldz + q);
+        a = __ldg(wvec + p) * __ldg(Zb + (C.act0 + (p - C.row0) * C.nch) * ldz + sqg);
       }
       ar[k] = a;
     }
@@ -604,11 +609,16 @@ __global__ void __launch_bounds__(256, 2) k_jt_input_wide(Classes T, const doubl
     const int n = S.lcnt[b];
     for (int t = 0; t < n; ++t) {
       const int d = S.ld[b][t];
-      if (d < jb || d >= jb + 16) continue;
-      const double v = S.lw[b][t] * __ldg(Zb + S.lz[b][t] + q);
+      if (d < jb || d >= jb + 8) continue;
+      const double* zr = Zb + S.lz[b][t] + q;
+      const double v0 = S.lw[b][t] * __ldg(zr);
+      const double v1 = q + 1 < w1 ? S.lw[b][t] * __ldg(zr + 1) : 0.0;
 #pragma unroll
-      for (int r = 0; r < 16; ++r)
-        if (d == jb + r) acc[r] += v;
+      for (int r = 0; r < 8; ++r)
+        if (d == jb + r) {
+          acc[r][0] += v0;
+          acc[r][1] += v1;
+        }
     }
   };
   if (nchunks > 0) load(0);
@@ -618,7 +628,7 @@ __global__ void __launch_bounds__(256, 2) k_jt_input_wide(Classes T, const doubl
 #pragma unroll
     for (int k = 0; k < 2; ++k) S.xs[b][(tid >> 5) + 8 * k][tid & 31] = xr[k];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) S.was[b][(tid >> 7) + 2 * k][tq] = ar[k];
+    for (int k = 0; k < 8; ++k) S.was[b][(tid >> 7) + 2 * k][sq] = ar[k];
     __syncthreads();
     if (tid < 32) {  // compact this chunk's one-hot rows into list b
       int base = 0;
@@ -642,13 +652,15 @@ __global__ void __launch_bounds__(256, 2) k_jt_input_wide(Classes T, const doubl
     const int np = static_cast<int>(min(static_cast<long long>(JW_P),
                                         T.m - static_cast<long long>(c) * JW_P));
     for (int pp = 0; pp < np; ++pp) {
-      const double a = S.was[b][pp][tq];
-      const double2* xv2 = reinterpret_cast<const double2*>(&S.xs[b][pp][half * 16]);
+      const double2 a2 = *reinterpret_cast<const double2*>(&S.was[b][pp][2 * tq2]);
+      const double2* xv2 = reinterpret_cast<const double2*>(&S.xs[b][pp][jg * 8]);
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
+      for (int r = 0; r < 4; ++r) {
         const double2 xv = xv2[r];
-        acc[2 * r] = fma(xv.x, a, acc[2 * r]);
-        acc[2 * r + 1] = fma(xv.y, a, acc[2 * r + 1]);
+        acc[2 * r][0] = fma(xv.x, a2.x, acc[2 * r][0]);
+        acc[2 * r][1] = fma(xv.x, a2.y, acc[2 * r][1]);
+        acc[2 * r + 1][0] = fma(xv.y, a2.x, acc[2 * r + 1][0]);
+        acc[2 * r + 1][1] = fma(xv.y, a2.y, acc[2 * r + 1][1]);
       }
     }
     if (c >= 1) apply(b ^ 1);  // previous chunk's list (complete since this barrier)
@@ -657,8 +669,12 @@ __global__ void __launch_bounds__(256, 2) k_jt_input_wide(Classes T, const doubl
   if (nchunks > 0) apply((nchunks - 1) & 1);
   if (q >= w1) return;
 #pragma unroll
-  for (int r = 0; r < 16; ++r)
-    if (jb + r <= din) out[static_cast<long long>(jb + r) * w1 + q] = scale * acc[r];
+  for (int r = 0; r < 8; ++r) {
+    if (jb + r > din) continue;
+    double* o = out + static_cast<long long>(jb + r) * w1 + q;
+    o[0] = scale * acc[r][0];
+    if (q + 1 < w1) o[1] = scale * acc[r][1];
+  }
 }
 
 // ------------------------------------------------------------------ f_vv (t-jets)

@@ -474,6 +474,20 @@ def run_ours(args, cfg):
                 "frac": ach / fp64_peak, "traffic": None,
                 "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
                 "algorithmic": f"2 m n = {flops:.3e} FLOP per J^T w"}
+    ls_avg = stages.get("line_search", 0.0) / max(counts.get("line_search", 1), 1) * 1e-3
+    if roof is None and ls_avg > 0:
+        # Nystrom-PCG configuration (no Gram): the 31-candidate line search is the
+        # largest tensor-core stage -- batched hidden-layer GEMMs over all channel rows
+        w = list(cfg["widths"])
+        rows = sum(c * maps[0]._nch(cl) for c, cl in zip(cfg["counts"], maps[0].collocation.classes))
+        flops = 31 * 2.0 * rows * sum(w[k] * w[k + 1] for k in range(1, len(w) - 2))
+        ach = flops / ls_avg / 1e12
+        roof = {"kernel": "dngd::k_gemm_nt<128,128> (31-candidate line-search forward, batched)",
+                "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": ach / fp64_peak, "traffic": None,
+                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
+                "algorithmic": f"31 x 2 R sum_k w_k w_k+1 = {flops:.3e} FLOP per line search "
+                               "(hidden layers; R = channel rows)"}
     if roof is not None:
         roof["traffic"] = _profiled_traffic(cfg["name"], roof["kernel"])
     gram_chol = None
@@ -489,9 +503,14 @@ def run_ours(args, cfg):
                      "definition": "(m(m+1)n + m^3/3) / (t_gram + t_potrf), SURVEY 8(d); on the "
                                    "factored path this is a J J^T-equivalent rate (the kernel "
                                    "performs fewer FLOPs), so it can exceed the FP64 peak"}
-    jfree = syrk_avg == 0 and gram_avg > 0
+    jfree = (syrk_avg == 0 and gram_avg > 0) or (
+        m >= cfg["dense_threshold"] and not sharded and maps[0].jfree_pcg())
     gemv_bytes = None if jfree else 8 * m * n
-    if jfree:
+    if jfree and m >= cfg["dense_threshold"]:
+        l2_note = ("per-step working set exceeds L2: the per-point activations, the m x l "
+                   "Nystrom columns and the 31-candidate line-search activations are "
+                   "rewritten every step (J-free PCG: J is never formed)")
+    elif jfree:
         l2_note = ("per-step working set exceeds L2: K + its factor (%.0f MB) and the "
                    "31-candidate line-search activations are rewritten every step (J-free: "
                    "J is never formed)" % (16 * m * m / 1e6))

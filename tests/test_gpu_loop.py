@@ -96,6 +96,8 @@ CASES = [
     ("allen_cahn", {}, (3, 16, 16, 1), (60, 20), 1e-3),           # embedding + cubic term
     ("poisson_ball_stde", dict(dim=10, index_set_size=3), (10, 16, 1), (40,), 1e3),
     ("poisson_ball_stde", dict(dim=200, index_set_size=4), (200, 16, 16, 1), (48,), 1e3),
+    ("heat1d", {}, (2, 8, 1), (1, 1, 1), 1e-3),                  # m = 3
+    ("poisson2d", {}, (2, 16, 1), (65, 64), 1e-3),               # ragged Cholesky blocks
 ]
 
 

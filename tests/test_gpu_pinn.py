@@ -30,6 +30,14 @@ BIG_DIN = [
     ("stde_din25", O.OraclePoissonBallStde(25, 4), (25, 32, 32, 1), (70,)),
 ]
 
+# edge sizes: one point per class, a ragged 65-row class next to a 1-point class,
+# classes that fill whole 64-row G-tiles exactly
+EDGE = [
+    ("single_points", O.OracleHeat1d(), (2, 8, 8, 1), (1, 1, 1)),
+    ("ragged_65_1", O.OraclePoisson2d(), (2, 16, 16, 1), (65, 1)),
+    ("full_tiles", O.OraclePoisson2d(), (2, 16, 1), (64, 64)),
+]
+
 
 def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
@@ -55,7 +63,7 @@ def _setup(K, problem, widths, counts, seed):
     return classes, theta, arr, keep, mlp, ws, dev(theta)
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN)
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN + EDGE)
 def test_assemble_matches_oracle(K, name, problem, widths, counts):
     classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 3)
     r_ref, J_ref = O.linearize(theta, widths, classes)
@@ -76,7 +84,7 @@ def test_assemble_matches_oracle(K, name, problem, widths, counts):
         assert np.array_equal(Js[:, : c1 - c0].cpu().numpy(), Jg[:, c0:c1])
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN)
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN + EDGE)
 def test_fvv_matches_oracle(K, name, problem, widths, counts):
     from tests.gpu_util import dev
     classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 4)
@@ -87,7 +95,7 @@ def test_fvv_matches_oracle(K, name, problem, widths, counts):
     assert _rel(out.cpu().numpy(), ref) <= 1e-11
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN)
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN + EDGE)
 def test_loss_many_matches_oracle(K, name, problem, widths, counts):
     from tests.gpu_util import dev
     classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 5)
@@ -104,7 +112,7 @@ def test_loss_many_matches_oracle(K, name, problem, widths, counts):
     np.testing.assert_allclose(out2.cpu().numpy(), ref, rtol=1e-12)
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN + [
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN + EDGE + [
     ("poisson2d_cfg1", O.OraclePoisson2d(), (2, 32, 32, 1), (900, 120)),
     ("heat1d_cfg2", O.OracleHeat1d(), (2, 64, 64, 64, 64, 1), (500, 100, 100)),
 ])
@@ -124,7 +132,7 @@ def test_gram_factored_matches_jjt(K, name, problem, widths, counts):
     assert _rel(r.cpu().numpy(), r_ref) <= 1e-12
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN)
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN + EDGE)
 def test_jt_factored_matches_oracle(K, name, problem, widths, counts):
     """J^T w from the activations (no J) == oracle J^T w (tiled and wide paths)."""
     from tests.gpu_util import dev
@@ -165,7 +173,7 @@ def test_gram_factored_parts_sum_to_full(K, nparts):
     assert torch.equal(acc, full)
 
 
-@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN)
+@pytest.mark.parametrize("name,problem,widths,counts", CASES + BIG_DIN + EDGE)
 def test_jvp_factored_matches_oracle(K, name, problem, widths, counts):
     """J v from first-order forward t-jets (no J) == oracle J v."""
     from tests.gpu_util import dev

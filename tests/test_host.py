@@ -197,3 +197,14 @@ def test_allen_cahn_plugin_matches_oracle():
             oc.cu, oc.c3, oc.cl, oc.grad_dims, oc.cg, oc.lap_dims)
         np.testing.assert_allclose(prob.class_data(cls), oc.f, rtol=0, atol=0)
         np.testing.assert_allclose(prob.input_channels(cls, op), oc.inputs, rtol=0, atol=1e-15)
+
+
+def test_class_counts_must_be_positive():
+    """problems.py:143-145: empty (or negative) classes are a DomainError, like the
+    reference, for every sampler."""
+    from paper_2505_21404_b200 import DomainError, make_problem
+
+    for name, counts in [("poisson2d", (10, 0)), ("heat1d", (5, 0, 3)), ("allen_cahn", (0, 4)),
+                         ("poisson2d", (10, -1))]:
+        with pytest.raises(DomainError):
+            make_problem(name).sample(counts, np.random.default_rng(0))

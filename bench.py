@@ -360,6 +360,8 @@ def run_ours(args, cfg):
             if it == args.steps + 1:
                 e.record()
 
+        mark.needs_theta = False  # no per-iteration copy of theta for a timing callback
+
         try:
             theta = run_loop(args.warmup, args.steps + 2, theta, mark)
         finally:
@@ -407,6 +409,8 @@ def run_ours(args, cfg):
         if it == args.warmup + args.steps - lag:
             torch.cuda.synchronize()
             marks["t1"] = time.perf_counter()
+
+    on_step.needs_theta = False
 
     tr = None
     try:

@@ -272,6 +272,13 @@ class _Book:
         self.rel_l2_fn, self.on_step = rel_l2_fn, on_step
         self.rejections = 0
         self.rel_pending = []  # (row, handle) of asynchronous rel-L2 evaluations
+        self.snapshot = False  # on_step gets a copy (theta lives in a reused buffer)
+
+    def _user_theta(self, theta):
+        # callbacks that only count iterations can opt out: fn.needs_theta = False
+        if self.snapshot and getattr(self.on_step, "needs_theta", True):
+            return ParameterVector(theta.tensor.clone(), theta.layout)
+        return theta
 
     def _rel(self, theta, row):
         fn = self.rel_l2_fn
@@ -297,7 +304,7 @@ class _Book:
         self._rel(theta, row)
         self.trace.rows.append(row)
         if self.on_step is not None:
-            self.on_step(iteration, theta, step, ls)
+            self.on_step(iteration, self._user_theta(theta), step, ls)
         if self.rejections >= MAX_CONSECUTIVE_REJECTIONS:
             self.trace.aborted = True
             self.trace.abort_reason = (
@@ -310,7 +317,7 @@ class _Book:
     def accepted(self, iteration, theta_new, step, ls):
         self.rejections = 0
         if self.on_step is not None:
-            self.on_step(iteration, theta_new, step, ls)
+            self.on_step(iteration, self._user_theta(theta_new), step, ls)
         row = TraceRow(iteration, self.clock.stamp(), ls.loss, lam=step.lambda_used, eta=ls.eta,
                        cg_iterations=step.cg_iterations,
                        ga_ratio=step.ga_ratio if step.ga_ratio is not None else float("nan"))
@@ -385,6 +392,7 @@ def _pipelined_loop(book: _Book, rmap_provider, theta: ParameterVector, config: 
 
     config_pc = config.line_search_points
     etas = 2.0 ** -np.arange(config_pc, dtype=np.float64)
+    book.snapshot = True  # theta views point into the ping-pong buffers
     G = None
     pending = collections.deque()  # (iteration, rmap, ticket)
     iteration = 0

@@ -135,8 +135,10 @@ int dngd_ls_select(dngd_ctx* ctx, void* stream, const double* losses, int ncand,
  * entry (it must hold 0.0 on entry).  out may alias v. */
 int dngd_ga_combine(dngd_ctx* ctx, void* stream, int64_t n, const double* v, const double* a,
                     const double* scal, double* out, double* anyd);
-/* out = theta + sel[0] * delta if sel[2] == 0 (accepted), else theta
- * (out may not alias delta; it may alias theta). */
+/* out = theta + sel[0] * delta if sel[2] == 0 (accepted), else theta -- the
+ * parameter update of optimizer.py:250 (eta = 2^-j, so eta*delta is exact and
+ * the fma equals the reference's theta + eta*delta bit for bit) without reading
+ * eta back (out may not alias delta; it may alias theta). */
 int dngd_theta_update(dngd_ctx* ctx, void* stream, int64_t n, const double* theta,
                       const double* delta, const double* sel, double* out);
 

@@ -677,6 +677,68 @@ __global__ void __launch_bounds__(256, 2) k_jt_input_wide(Classes T, const doubl
   }
 }
 
+// ---- the same input block on the FP64 tensor cores (din >= 64): out = Xt Bt^T
+// with Xt[j][p] = x_pj (row din = 1: the bias), Bt[q][p] = w_p a_pq, then the
+// one-hot rows added by k_jt_onehot in (point, channel) order.
+__global__ void k_xt_build(Classes T, double* __restrict__ Xt, long long ldm) {
+  __shared__ double tile[32][33];
+  const int din = T.din;
+  const long long p0 = static_cast<long long>(blockIdx.x) * 32;
+  const int j0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const long long p = p0 + r;
+    const int j = j0 + threadIdx.x;
+    double v = 0.0;
+    if (p < T.m) {
+      const ClassDev& C = T.c[find_class(T, p)];
+      v = j < din ? C.pts[(p - C.row0) * din + j] : (j == din ? 1.0 : 0.0);
+    }
+    tile[r][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int j = j0 + r;
+    const long long p = p0 + threadIdx.x;
+    if (j <= din && p < ldm) Xt[static_cast<long long>(j) * ldm + p] = tile[threadIdx.x][r];
+  }
+}
+
+__global__ void k_bt_build(Classes T, const double* __restrict__ Zb, long long ld, int w1,
+                           const double* __restrict__ wvec, double* __restrict__ Bt,
+                           long long ldm) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= w1 * ldm) return;
+  const int q = static_cast<int>(idx / ldm);
+  const long long p = idx - q * ldm;
+  double v = 0.0;
+  if (p < T.m) {
+    const ClassDev& C = T.c[find_class(T, p)];
+    v = wvec[p] * Zb[(C.act0 + (p - C.row0) * C.nch) * ld + q];
+  }
+  Bt[idx] = v;
+}
+
+// out[d][q] += scale w_p b_pgq for every derivative channel (p, g) with dim d in this
+// CTA's row range, in (p, g) order (deterministic; one CTA owns each row)
+constexpr int OH_ROWS = 512;
+__global__ void k_jt_onehot(Classes T, const double* __restrict__ Zb, long long ld, int w1,
+                            const double* __restrict__ wvec, double scale,
+                            double* __restrict__ out) {
+  const int j0 = blockIdx.x * OH_ROWS, j1 = min(j0 + OH_ROWS, T.din);
+  for (long long p = 0; p < T.m; ++p) {
+    const ClassDev& C = T.c[find_class(T, p)];
+    const long long i = p - C.row0;
+    for (int g = 0; g < C.ngrad; ++g) {
+      const int d = gdim(C, g, i);
+      if (d < j0 || d >= j1) continue;
+      const double wp = scale * wvec[p];
+      const double* zr = Zb + (C.act0 + i * C.nch + 1 + g) * ld;
+      double* o = out + static_cast<long long>(d) * w1;
+      for (int q = threadIdx.x; q < w1; q += blockDim.x) o[q] = fma(wp, zr[q], o[q]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ f_vv (t-jets)
 
 struct T2 {
@@ -2360,6 +2422,8 @@ extern "C" int dngd_loss_many(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* 
 namespace {
 
 struct JtScratch {
+  long long ldm = 0;                   // wide input on the tensor cores: Xt / Bt pitch
+  size_t off_xt = 0, off_bt = 0;
   long long ldR, chunk;
   int nchunks, splits;
   size_t bytes, off_zt, off_part, part_bytes;
@@ -2410,6 +2474,12 @@ JtScratch jt_plan(dngd_ctx* ctx, const Plan& P) {
   S.off_part = S.off_zt + (static_cast<size_t>(P.wmax) * S.ldR * 8 + 255) / 256 * 256;
   S.part_bytes = part;
   S.bytes = S.off_part + part;
+  if (P.wide_in && P.bigin) {
+    S.ldm = (P.m + 1) / 2 * 2;
+    S.off_xt = (S.bytes + 255) / 256 * 256;
+    S.off_bt = S.off_xt + (static_cast<size_t>(P.w[0] + 1) * S.ldm * 8 + 255) / 256 * 256;
+    S.bytes = S.off_bt + static_cast<size_t>(P.w[1]) * S.ldm * 8;
+  }
   return S;
 }
 
@@ -2477,7 +2547,31 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   double* part = reinterpret_cast<double*>(sc + S.off_part);
   const int L = P.L;
   // input layer W0 | b0
-  if (P.wide_in) {
+  if (P.wide_in && P.bigin) {
+    const int w1 = static_cast<int>(P.w[1]);
+    const int din = P.T.din;
+    double* Xt = reinterpret_cast<double*>(sc + S.off_xt);
+    double* Bt = reinterpret_cast<double*>(sc + S.off_bt);
+    k_xt_build<<<dim3(static_cast<unsigned>((S.ldm + 31) / 32), static_cast<unsigned>((din + 1 + 31) / 32)),
+                 dim3(32, 8), 0, s>>>(P.T, Xt, S.ldm);
+    k_bt_build<<<nblk(w1 * S.ldm), 256, 0, s>>>(P.T, B.Zb[0], P.ld[1], w1, w, Bt, S.ldm);
+    GemmCall g;
+    g.M = din + 1;
+    g.N = w1;
+    g.K = P.m;
+    g.A = Xt;
+    g.lda = S.ldm;
+    g.B = Bt;
+    g.ldb = S.ldm;
+    g.C = out + P.off[0];
+    g.ldc = w1;
+    g.alpha = scale;
+    g.beta = 0.0;
+    rc = gemm_nt(ctx, s, g);
+    if (rc) return rc;
+    k_jt_onehot<<<static_cast<unsigned>((din + OH_ROWS - 1) / OH_ROWS), 128, 0, s>>>(
+        P.T, B.Zb[0], P.ld[1], w1, w, scale, out + P.off[0]);
+  } else if (P.wide_in) {
     const int w1 = static_cast<int>(P.w[1]);
     dim3 g(static_cast<unsigned>((P.w[0] + 1 + JW_J - 1) / JW_J), (w1 + 127) / 128);
     static bool attr[64] = {false};

@@ -719,22 +719,41 @@ __global__ void k_bt_build(Classes T, const double* __restrict__ Zb, long long l
 }
 
 // out[d][q] += scale w_p b_pgq for every derivative channel (p, g) with dim d in this
-// CTA's row range, in (p, g) order (deterministic; one CTA owns each row)
+// CTA's row range, in (p, g) order (deterministic; one CTA owns each row).  The
+// dims of 128 points at a time are staged in shared memory, so the scan over all
+// (p, g) is a shared-memory loop instead of a chain of global loads.
 constexpr int OH_ROWS = 512;
-__global__ void k_jt_onehot(Classes T, const double* __restrict__ Zb, long long ld, int w1,
-                            const double* __restrict__ wvec, double scale,
-                            double* __restrict__ out) {
+__global__ void __launch_bounds__(128) k_jt_onehot(Classes T, const double* __restrict__ Zb,
+                                                     long long ld, int w1,
+                                                     const double* __restrict__ wvec,
+                                                     double scale, double* __restrict__ out) {
+  __shared__ int sd[128][MAXG];
+  __shared__ int sng[128];
   const int j0 = blockIdx.x * OH_ROWS, j1 = min(j0 + OH_ROWS, T.din);
-  for (long long p = 0; p < T.m; ++p) {
-    const ClassDev& C = T.c[find_class(T, p)];
-    const long long i = p - C.row0;
-    for (int g = 0; g < C.ngrad; ++g) {
-      const int d = gdim(C, g, i);
-      if (d < j0 || d >= j1) continue;
-      const double wp = scale * wvec[p];
-      const double* zr = Zb + (C.act0 + i * C.nch + 1 + g) * ld;
-      double* o = out + static_cast<long long>(d) * w1;
-      for (int q = threadIdx.x; q < w1; q += blockDim.x) o[q] = fma(wp, zr[q], o[q]);
+  for (long long p0 = 0; p0 < T.m; p0 += 128) {
+    const int np = static_cast<int>(min(128LL, T.m - p0));
+    __syncthreads();
+    if (threadIdx.x < np) {
+      const long long p = p0 + threadIdx.x;
+      const ClassDev& C = T.c[find_class(T, p)];
+      const long long i = p - C.row0;
+      sng[threadIdx.x] = C.ngrad;
+      for (int g = 0; g < C.ngrad; ++g) sd[threadIdx.x][g] = gdim(C, g, i);
+    }
+    __syncthreads();
+    for (int pp = 0; pp < np; ++pp) {
+      const int ng = sng[pp];
+      for (int g = 0; g < ng; ++g) {
+        const int d = sd[pp][g];
+        if (d < j0 || d >= j1) continue;
+        const long long p = p0 + pp;
+        const ClassDev& C = T.c[find_class(T, p)];
+        const long long i = p - C.row0;
+        const double wp = scale * wvec[p];
+        const double* zr = Zb + (C.act0 + i * C.nch + 1 + g) * ld;
+        double* o = out + static_cast<long long>(d) * w1;
+        for (int q = threadIdx.x; q < w1; q += blockDim.x) o[q] = fma(wp, zr[q], o[q]);
+      }
     }
   }
 }

@@ -226,6 +226,13 @@ int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
 int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
              const double* v, const dngd_class_desc* classes, int nclass, double* fvv,
              void* work, size_t work_bytes);
+/* dngd_fvv / dngd_loss_many reusing x W0(theta) from an activation workspace that
+ * holds the last assembly / activation pass AT THE SAME theta (caller's contract;
+ * residuals.py:304-317 / 188-201 semantics unchanged).  Only the large-din input
+ * layer (din >= 64) uses it: there x W0 is a split-K GEMM over din. */
+int dngd_fvv_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
+                 const double* v, const dngd_class_desc* classes, int nclass, double* fvv,
+                 void* work, size_t work_bytes, void* act_work, size_t act_bytes);
 
 /* K[:, I] WITHOUT J (replaces the Nystrom sketch J J_I^T of solver.py:259-261):
  * the activations of the sorted landmark rows `landmarks` (host int64, ell of
@@ -252,6 +259,10 @@ int dngd_loss_many(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const 
                    const double* delta, const double* etas, int ncand,
                    const dngd_class_desc* classes, int nclass, double* losses, void* work,
                    size_t work_bytes);
+int dngd_loss_many_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                       const double* theta, const double* delta, const double* etas, int ncand,
+                       const dngd_class_desc* classes, int nclass, double* losses, void* work,
+                       size_t work_bytes, void* act_work, size_t act_bytes);
 
 #ifdef __cplusplus
 }

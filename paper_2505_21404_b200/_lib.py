@@ -109,6 +109,11 @@ _SIGS = {
                            ctypes.POINTER(ClassDesc), c_int, c_vp, c_vp, c_size], c_int),
     "dngd_loss_many": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, c_vp, c_vp, c_int,
                         ctypes.POINTER(ClassDesc), c_int, c_vp, c_vp, c_size], c_int),
+    "dngd_fvv_act": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, c_vp, ctypes.POINTER(ClassDesc),
+                      c_int, c_vp, c_vp, c_size, c_vp, c_size], c_int),
+    "dngd_loss_many_act": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, c_vp, c_vp, c_int,
+                            ctypes.POINTER(ClassDesc), c_int, c_vp, c_vp, c_size, c_vp, c_size],
+                           c_int),
 }
 
 EXPORTED = tuple(_SIGS)

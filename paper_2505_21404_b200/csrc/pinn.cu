@@ -1262,17 +1262,23 @@ static int input_gemm(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const BigIn&
 // (batched over candidates) with Z scratch shared across layers.
 static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const double* thetas,
                            int C, LossBufs& B, double** Hlast, const double* theta,
-                           const double* delta, const double* etas) {
+                           const double* delta, const double* etas,
+                           const double* zx_act = nullptr) {
   const int L = P.L;
   const long long act_s = P.R * P.ldmax;
   {
     const double *Zx = nullptr, *Dx = nullptr;
     if (P.bigin && delta != nullptr) {  // x (W0 + eta V0) = x W0 + eta x V0
-      int rc = input_gemm(ctx, s, P, B.big, theta, B.big.Zx);
-      if (rc) return rc;
+      int rc = DNGD_OK;
+      if (zx_act != nullptr) {
+        Zx = zx_act;
+      } else {
+        rc = input_gemm(ctx, s, P, B.big, theta, B.big.Zx);
+        if (rc) return rc;
+        Zx = B.big.Zx;
+      }
       rc = input_gemm(ctx, s, P, B.big, delta, B.big.Dx);
       if (rc) return rc;
-      Zx = B.big.Zx;
       Dx = B.big.Dx;
     }
     dim3 g(nblk(P.m * P.w[1]), C);
@@ -2294,7 +2300,28 @@ extern "C" int dngd_gram_factored_cols(dngd_ctx* ctx, void* stream, const dngd_m
 
 static int fvv_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
                     const double* v, const dngd_class_desc* classes, int nclass, double* fvv,
-                    void* work, size_t work_bytes, int order);
+                    void* work, size_t work_bytes, int order, const double* zx_act = nullptr);
+
+// x W0(theta) left in an activation workspace by the last assembly / Gram at theta
+// (large-din input layer only; nullptr otherwise)
+static const double* act_input_products(const Plan& P, void* act_work, size_t act_bytes) {
+  if (!P.bigin || act_work == nullptr || bytes_of(P, 0, 1) > act_bytes) return nullptr;
+  Arena A{static_cast<char*>(act_work)};
+  AsmBufs B;
+  carve_assemble(P, A, B);
+  return B.big.Zx;
+}
+
+extern "C" int dngd_fvv_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                            const double* theta, const double* v, const dngd_class_desc* classes,
+                            int nclass, double* fvv, void* work, size_t work_bytes,
+                            void* act_work, size_t act_bytes) {
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  return fvv_impl(ctx, stream, mlp, theta, v, classes, nclass, fvv, work, work_bytes, 2,
+                  act_input_products(P, act_work, act_bytes));
+}
 
 extern "C" int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                         const double* theta, const double* v, const dngd_class_desc* classes,
@@ -2313,7 +2340,7 @@ extern "C" int dngd_jvp_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_des
 // (first-order jets only: the GEMMs cover 2R and R rows instead of 3R and 2R)
 static int fvv_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
                     const double* v, const dngd_class_desc* classes, int nclass, double* fvv,
-                    void* work, size_t work_bytes, int order) {
+                    void* work, size_t work_bytes, int order, const double* zx_act) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Plan P;
   int rc = make_plan(ctx, mlp, classes, nclass, P);
@@ -2327,14 +2354,19 @@ static int fvv_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const
   const long long ld = P.ldmax;
   double* Hcur = B.H3[0];
   double* Hnext = B.H3[1];
+  const double* zx = B.big.Zx;
   if (P.bigin) {
-    rc = input_gemm(ctx, s, P, B.big, theta, B.big.Zx);
-    if (rc) return rc;
+    if (zx_act != nullptr) {
+      zx = zx_act;  // x W0(theta) from the activation pass at theta
+    } else {
+      rc = input_gemm(ctx, s, P, B.big, theta, B.big.Zx);
+      if (rc) return rc;
+    }
     rc = input_gemm(ctx, s, P, B.big, v, B.big.Dx);
     if (rc) return rc;
   }
   k_fvv_input<<<nblk(P.m * P.w[1]), 256, 0, s>>>(P.T, theta, v, static_cast<int>(P.w[1]), ld,
-                                                  Hcur, B.big.Zx, B.big.Dx, P.ld[1]);
+                                                  Hcur, zx, B.big.Dx, P.ld[1]);
   for (int k = 1; k <= L - 2; ++k) {
     launch_transpose(s, theta + P.off[k], 0, static_cast<int>(P.w[k]),
                      static_cast<int>(P.w[k + 1]), B.Wt[k], P.ld[k], 0, 1);
@@ -2377,10 +2409,32 @@ static bool loss_fused_ok(const Plan& P) {
   return P.T.din <= MAXG;
 }
 
+static int loss_many_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                          const double* theta, const double* delta, const double* etas, int ncand,
+                          const dngd_class_desc* classes, int nclass, double* losses, void* work,
+                          size_t work_bytes, void* act_work, size_t act_bytes);
+
 extern "C" int dngd_loss_many(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                               const double* theta, const double* delta, const double* etas,
                               int ncand, const dngd_class_desc* classes, int nclass,
                               double* losses, void* work, size_t work_bytes) {
+  return loss_many_impl(ctx, stream, mlp, theta, delta, etas, ncand, classes, nclass, losses, work,
+                        work_bytes, nullptr, 0);
+}
+
+extern "C" int dngd_loss_many_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                                  const double* theta, const double* delta, const double* etas,
+                                  int ncand, const dngd_class_desc* classes, int nclass,
+                                  double* losses, void* work, size_t work_bytes, void* act_work,
+                                  size_t act_bytes) {
+  return loss_many_impl(ctx, stream, mlp, theta, delta, etas, ncand, classes, nclass, losses, work,
+                        work_bytes, act_work, act_bytes);
+}
+
+static int loss_many_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                          const double* theta, const double* delta, const double* etas, int ncand,
+                          const dngd_class_desc* classes, int nclass, double* losses, void* work,
+                          size_t work_bytes, void* act_work, size_t act_bytes) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Plan P;
   int rc = make_plan(ctx, mlp, classes, nclass, P);
@@ -2429,7 +2483,8 @@ extern "C" int dngd_loss_many(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* 
   const long long k0 = (P.bigin && delta != nullptr) ? P.T.din * P.w[1] : 0;
   k_candidates<<<dim3(nblk(P.n - k0), ncand), 256, 0, s>>>(theta, delta, etas, P.n, B.thetas, k0);
   double* Hlast;
-  rc = forward_batched(ctx, s, P, B.thetas, ncand, B, &Hlast, theta, delta, etas);
+  rc = forward_batched(ctx, s, P, B.thetas, ncand, B, &Hlast, theta, delta, etas,
+                       act_input_products(P, act_work, act_bytes));
   if (rc) return rc;
   k_head<<<dim3(nblk(P.m, 8), ncand), 256, 0, s>>>(P.T, Hlast, static_cast<int>(P.w[P.L - 1]),
                                                     P.ldmax, B.thetas, P.n, P.off[P.L - 1],

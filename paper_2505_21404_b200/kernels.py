@@ -277,9 +277,15 @@ def jt_factored(mlp, classes_arr, nclass, w, scale, out, act_ws, scratch):
          float(scale), ptr(out), ptr(act_ws), act_ws.numel(), ptr(scratch), scratch.numel())
 
 
-def fvv(mlp, theta, v, classes_arr, nclass, out, ws):
-    call("dngd_fvv", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), ptr(v), classes_arr,
-         nclass, ptr(out), ptr(ws), ws.numel())
+def fvv(mlp, theta, v, classes_arr, nclass, out, ws, act_ws=None):
+    """f_vv; act_ws (activations at the same theta) lets the large-din input layer
+    reuse x W0 instead of recomputing it."""
+    if act_ws is None:
+        call("dngd_fvv", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), ptr(v),
+             classes_arr, nclass, ptr(out), ptr(ws), ws.numel())
+    else:
+        call("dngd_fvv_act", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), ptr(v),
+             classes_arr, nclass, ptr(out), ptr(ws), ws.numel(), ptr(act_ws), act_ws.numel())
 
 
 def gram_factored_cols(mlp, classes_arr, nclass, landmarks, Kc, act_ws):
@@ -302,6 +308,11 @@ def jvp_factored(mlp, theta, v, classes_arr, nclass, out, ws):
          classes_arr, nclass, ptr(out), ptr(ws), ws.numel())
 
 
-def loss_many(mlp, theta, delta, etas, ncand, classes_arr, nclass, out, ws):
-    call("dngd_loss_many", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), ptr(delta),
-         ptr(etas), int(ncand), classes_arr, nclass, ptr(out), ptr(ws), ws.numel())
+def loss_many(mlp, theta, delta, etas, ncand, classes_arr, nclass, out, ws, act_ws=None):
+    if act_ws is None:
+        call("dngd_loss_many", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), ptr(delta),
+             ptr(etas), int(ncand), classes_arr, nclass, ptr(out), ptr(ws), ws.numel())
+    else:
+        call("dngd_loss_many_act", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta),
+             ptr(delta), ptr(etas), int(ncand), classes_arr, nclass, ptr(out), ptr(ws), ws.numel(),
+             ptr(act_ws), act_ws.numel())

@@ -558,10 +558,18 @@ class PinnResidualMap(ResidualMap):
 
         d = self._device()
         out = torch.empty(self.m, dtype=torch.float64, device=d["device"])
+        th = self._theta_t(theta)
         with stage("fvv"):
-            K.fvv(d["mlp"], self._theta_t(theta), v_t, d["arr"], d["nclass"], out,
-                  self._workspace(d["ws_bytes"]))
+            K.fvv(d["mlp"], th, v_t, d["arr"], d["nclass"], out, self._workspace(d["ws_bytes"]),
+                  self._reuse_act(th))
         return out
+
+    def _reuse_act(self, th):
+        """The activation workspace when it holds the pass at theta and the input
+        layer is wide (x W0 is then reused by f_vv and the line search)."""
+        if self.spec.input_dim >= 64 and self.wide_input() and self._act_valid(th):
+            return self._act_workspace()
+        return None
 
     # -- factored Gram and J^T w (no pass over J) ----------------------------------------
     gram_mode = "auto"  # "auto" | "factored" | "materialized"
@@ -778,7 +786,7 @@ class PinnResidualMap(ResidualMap):
                 c1 = min(C, c0 + step)
                 ws = self._workspace(self._loss_ws(c1 - c0))
                 K.loss_many(d["mlp"], th, delta_t, etas_t[c0:c1], c1 - c0, d["arr"],
-                            d["nclass"], out[c0:c1], ws)
+                            d["nclass"], out[c0:c1], ws, self._reuse_act(th))
         return out
 
     def loss_many_t(self, cands_t):

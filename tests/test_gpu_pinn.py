@@ -183,3 +183,29 @@ def test_jvp_factored_matches_oracle(K, name, problem, widths, counts):
     out = torch.full((J_ref.shape[0],), np.nan, dtype=torch.float64, device="cuda")
     K.jvp_factored(mlp, th, dev(v), arr, len(classes), out, ws)
     assert _rel(out.cpu().numpy(), J_ref @ v) <= 1e-12
+
+
+@pytest.mark.parametrize("name,problem,widths,counts", BIG_DIN[:2])
+def test_act_reuse_of_input_products(K, name, problem, widths, counts):
+    """f_vv and the line-search losses reusing x W0(theta) from the activation pass at
+    theta are bit-identical to the self-contained calls (and match the oracle)."""
+    from tests.gpu_util import dev
+    classes, theta, arr, keep, mlp, ws, th = _setup(K, problem, widths, counts, 14)
+    m = sum(c.count for c in classes)
+    act = torch.empty_like(ws)
+    r = torch.empty(m, dtype=torch.float64, device="cuda")
+    K.activations(mlp, th, arr, len(classes), r, act)
+    v = dev(np.random.default_rng(15).normal(size=theta.size))
+    a = torch.empty(m, dtype=torch.float64, device="cuda")
+    b = torch.empty(m, dtype=torch.float64, device="cuda")
+    K.fvv(mlp, th, v, arr, len(classes), a, ws)
+    K.fvv(mlp, th, v, arr, len(classes), b, ws, act)
+    assert torch.equal(a, b)
+    etas = dev(2.0 ** -np.arange(31, dtype=np.float64))
+    la = torch.empty(31, dtype=torch.float64, device="cuda")
+    lb = torch.empty(31, dtype=torch.float64, device="cuda")
+    K.loss_many(mlp, th, v, etas, 31, arr, len(classes), la, ws)
+    K.loss_many(mlp, th, v, etas, 31, arr, len(classes), lb, ws, act)
+    assert torch.equal(la, lb)
+    cands = theta[None, :] + (2.0 ** -np.arange(31))[:, None] * v.cpu().numpy()[None, :]
+    np.testing.assert_allclose(lb.cpu().numpy(), O.loss_many(cands, widths, classes), rtol=1e-12)

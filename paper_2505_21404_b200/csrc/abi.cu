@@ -77,6 +77,12 @@ extern "C" int dngd_ctx_destroy(dngd_ctx* ctx) {
     if (ctx->ev_update2) cudaEventDestroy(ctx->ev_update2);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
+    if (ctx->aux2) cudaStreamDestroy(ctx->aux2);
+    for (int q = 0; q < 3; ++q) {
+      if (ctx->ev_u1[q]) cudaEventDestroy(ctx->ev_u1[q]);
+      if (ctx->ev_u2[q]) cudaEventDestroy(ctx->ev_u2[q]);
+    }
+    if (ctx->ev_join2) cudaEventDestroy(ctx->ev_join2);
     if (ctx->hi) cudaStreamDestroy(ctx->hi);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->dot_part) cudaFree(ctx->dot_part);

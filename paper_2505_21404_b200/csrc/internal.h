@@ -20,6 +20,10 @@ struct dngd_ctx {
   cudaEvent_t ev_join = nullptr;
   CUtensorMap potrf_mapS, potrf_mapP;  // panel-load boxes over L (encoded per dngd_potrf call)
   cudaEvent_t ev_panel = nullptr, ev_update = nullptr, ev_update2 = nullptr, ev_fork = nullptr;
+  // split trailing updates: U1 (next-but-one block column) on aux, U2 (the rest) on aux2
+  cudaStream_t aux2 = nullptr;
+  cudaEvent_t ev_u1[3] = {nullptr, nullptr, nullptr}, ev_u2[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_join2 = nullptr;
   // multi-CTA dot products: per-CTA partials + arrival counter (calls on one context
   // are stream-ordered; the counter is reset by the last CTA)
   double* dot_part = nullptr;

@@ -66,7 +66,7 @@ def test_gemm_nt(K, M, N, Kd, lower):
         assert _rel(got, ref) <= 1e-13
 
 
-@pytest.mark.parametrize("m", [5, 64, 100, 1020, 2800])
+@pytest.mark.parametrize("m", [5, 64, 100, 129, 161, 1020, 2800])
 def test_potrf_potrs(K, m):
     from tests.gpu_util import dev
     rng = np.random.default_rng(m)

@@ -75,15 +75,51 @@ def _env_rank():
 
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: NVML from a
+    background thread every 5 ms (the timed region of a default run is ~0.1 s, too
+    short for nvidia-smi's 100 ms loop), nvidia-smi -lms as the fallback."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40}
 
     def __init__(self, index=0):
         self.index = index
         self.proc = None
+        self.thread = None
+        self.samples = []
+        self.reasons = set()
+        self.smax = None
+
+    def _nvml_loop(self, nv, h):
+        import time
+        while not self._stop:
+            try:
+                self.samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for nm, bit in self.BITS.items():
+                    if mask & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                return
+            time.sleep(0.005)
 
     def start(self):
+        try:
+            import threading
+
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._stop = False
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
@@ -93,6 +129,12 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
+        if self.thread is not None:
+            self._stop = True
+            self.thread.join(timeout=2)
+            sm = self.samples
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.smax,
+                    "reasons": sorted(self.reasons), "samples": len(sm), "source": "nvml 5 ms"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -116,7 +158,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi 100 ms"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -185,6 +227,62 @@ def _profiled_traffic(workload, kernel):
             if name.split("<")[0] in kernel:
                 best = ent.get("bytes")
     return best
+
+
+def _hbm_stages(rmap, theta, hbm_peak, reps=10):
+    """The HBM-bound stages of the dense path WITH J materialised, at the bench
+    workload (north star: Jacobian writes and J/J^T matvecs vs the HBM roofline;
+    the product path at configs 2-7 never forms J, so these are measured here
+    separately, outside the timed region).  Algorithmic bytes:
+    assembly 8mn written (its activation reads are not counted), J^T y and J x
+    8mn + 8(m+n).  J > L2 at config 2 (285 MB vs 126 MB), so each launch streams
+    J from HBM.  CUDA events on the launching stream, mean of `reps` launches."""
+    import torch
+
+    from paper_2505_21404_b200 import kernels as K
+
+    m, n = rmap.m, rmap.n
+    if 8.0 * m * K.pad_ld(n) > 40e9:
+        return None
+    th = rmap._theta_t(theta)
+    d = rmap._device()
+    dev = d["device"]
+    J = torch.empty((m, K.pad_ld(n)), dtype=torch.float64, device=dev)
+    r = torch.empty(m, dtype=torch.float64, device=dev)
+    y = torch.randn(m, dtype=torch.float64, device=dev)
+    x = torch.randn(n, dtype=torch.float64, device=dev)
+    out_n = torch.empty(n, dtype=torch.float64, device=dev)
+    out_m = torch.empty(m, dtype=torch.float64, device=dev)
+    ws = rmap._act_workspace()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) / reps * 1e-3
+
+    t_asm = timed(lambda: K.assemble(d["mlp"], th, d["arr"], d["nclass"], r, J, 0, n, ws))
+    t_jt = timed(lambda: K.gemv_t(J, y, n, out=out_n))
+    t_j = timed(lambda: K.gemv_n(J, x, n, out=out_m))
+    mv = 8.0 * m * n + 8.0 * (m + n)
+
+    def ent(kern, nbytes, t):
+        gbs = nbytes / t / 1e9
+        return {"kernel": kern, "bytes": nbytes, "us": t * 1e6, "gbs": gbs,
+                "frac_of_hbm_peak": gbs / hbm_peak}
+
+    rmap._cache = None  # the probe's J is not the loop's
+    return {"J_assembly": ent("dngd_assemble (activation pass + k_jwrite)", 8.0 * m * n, t_asm),
+            "JT_y": ent("dngd_gemv_t (k_gemv_t + reduce)", mv, t_jt),
+            "J_x": ent("dngd_gemv_n (k_gemv_n_row)", mv, t_j),
+            "note": "dense path with J materialised (m x n FP64, ldJ padded to 16); the J-free "
+                    "product path does not run these"}
 
 
 def run_ours(args, cfg):
@@ -546,6 +644,8 @@ def run_ours(args, cfg):
         "gram_cholesky": gram_chol,
         "stages_ms_per_step": stage_ms,
         "gemv_bytes_per_launch": gemv_bytes,
+        "hbm_stages": (_hbm_stages(maps[0], theta, hbm_peak)
+                       if (not sharded and not args.profile) else None),
         "hbm_peak_gbs": hbm_peak,
         "hbm_peak_source": hbm_src,
         "fp64_peak_tflops": fp64_peak,

@@ -10,6 +10,7 @@
 
 #include <math_constants.h>
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -17,79 +18,85 @@
 namespace dngd {
 
 constexpr int kGT = 256;       // threads per CTA
-constexpr int kGTCols = 1024;  // columns per CTA (2 x double2 per thread)
+constexpr int kGTV = 4;                // double2 per thread per row
 
 static void gemv_t_plan(dngd_ctx* ctx, long long m, long long ncols, int* nchunks) {
-  const long long col_tiles = (ncols + kGTCols - 1) / kGTCols;
+  const long long cols = 2LL * kGT * kGTV;  // 2048: measured best of 1024 / 2048 / 4096
+  const long long col_tiles = (ncols + cols - 1) / cols;
   const long long target = 4LL * ctx->num_sms;
   long long nc = (target + col_tiles - 1) / col_tiles;
   nc = std::min(nc, std::max(1LL, m / 16));
   *nchunks = static_cast<int>(std::max(1LL, nc));
 }
 
-// J row-major (m x ncols, ld even, 16B-aligned).  Thread owns 4 consecutive
-// columns of a 1024-column strip; grid.y = row chunks.
+// J row-major (m x ncols, ld even, 16B-aligned).  A CTA streams a strip of
+// 512 V columns (V x 4 KB contiguous per row) over a chunk of rows; thread t
+// owns the double2 column pairs t + 256 v, so every load instruction of a warp
+// covers 512 contiguous bytes.  A pair at column c < ncols is always inside the
+// row's ld (ld even), so odd ncols need no scalar tail.  grid.y = row chunks;
+// partial sums go to a fixed-order reduction (deterministic).
+template <int V>
 __global__ void __launch_bounds__(kGT) k_gemv_t(const double* __restrict__ J, long long m,
                                                   long long ncols, long long ld,
                                                   const double* __restrict__ y, int nchunks,
                                                   const double* __restrict__ g, double scale,
                                                   double* __restrict__ out,
                                                   double* __restrict__ partial) {
-  const long long c = static_cast<long long>(blockIdx.x) * kGTCols + 4LL * threadIdx.x;
+  const long long c0 = static_cast<long long>(blockIdx.x) * (2 * kGT * V) + 2LL * threadIdx.x;
   const long long rows_per = (m + nchunks - 1) / nchunks;
   const long long i0 = blockIdx.y * rows_per;
   const long long i1 = min(m, i0 + rows_per);
-  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-  if (c + 3 < ncols) {
-    const double* p = J + i0 * ld + c;
-    long long i = i0;
-    for (; i + 3 < i1; i += 4) {
-      double2 v[4][2];
+  double2 acc[V];
+  bool ok[V];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        v[k][0] = __ldcs(reinterpret_cast<const double2*>(p + k * ld));
-        v[k][1] = __ldcs(reinterpret_cast<const double2*>(p + k * ld + 2));
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double yk = __ldg(y + i + k);
-        a0 = fma(v[k][0].x, yk, a0);
-        a1 = fma(v[k][0].y, yk, a1);
-        a2 = fma(v[k][1].x, yk, a2);
-        a3 = fma(v[k][1].y, yk, a3);
-      }
-      p += 4 * ld;
-    }
-    for (; i < i1; ++i, p += ld) {
-      const double yk = __ldg(y + i);
-      const double2 u0 = __ldcs(reinterpret_cast<const double2*>(p));
-      const double2 u1 = __ldcs(reinterpret_cast<const double2*>(p + 2));
-      a0 = fma(u0.x, yk, a0);
-      a1 = fma(u0.y, yk, a1);
-      a2 = fma(u1.x, yk, a2);
-      a3 = fma(u1.y, yk, a3);
-    }
-  } else if (c < ncols) {
-    for (long long i = i0; i < i1; ++i) {
-      const double yk = y[i];
-      const double* p = J + i * ld + c;
-      a0 = fma(p[0], yk, a0);
-      if (c + 1 < ncols) a1 = fma(p[1], yk, a1);
-      if (c + 2 < ncols) a2 = fma(p[2], yk, a2);
-    }
-  } else {
-    return;
+  for (int v = 0; v < V; ++v) {
+    acc[v] = make_double2(0.0, 0.0);
+    ok[v] = c0 + 2LL * kGT * v < ncols;
   }
-  double acc[4] = {a0, a1, a2, a3};
-  if (nchunks == 1) {
+  const double* p = J + i0 * ld + c0;
+  long long i = i0;
+  for (; i + 1 < i1; i += 2) {
+    double2 u[2][V];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (c + k < ncols) out[c + k] = scale * (acc[k] + (g ? g[c + k] : 0.0));
-  } else {
-    double* dst = partial + static_cast<long long>(blockIdx.y) * ncols + c;
+    for (int k = 0; k < 2; ++k)
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (c + k < ncols) dst[k] = acc[k];
+      for (int v = 0; v < V; ++v)
+        u[k][v] = ok[v] ? __ldcs(reinterpret_cast<const double2*>(p + k * ld + 2 * kGT * v))
+                        : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double yk = __ldg(y + i + k);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        acc[v].x = fma(u[k][v].x, yk, acc[v].x);
+        acc[v].y = fma(u[k][v].y, yk, acc[v].y);
+      }
+    }
+    p += 2 * ld;
+  }
+  if (i < i1) {
+    const double yk = __ldg(y + i);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (ok[v]) {
+        const double2 u = __ldcs(reinterpret_cast<const double2*>(p + 2 * kGT * v));
+        acc[v].x = fma(u.x, yk, acc[v].x);
+        acc[v].y = fma(u.y, yk, acc[v].y);
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const long long c = c0 + 2LL * kGT * v;
+    if (!ok[v]) continue;
+    if (nchunks == 1) {
+      out[c] = scale * (acc[v].x + (g ? g[c] : 0.0));
+      if (c + 1 < ncols) out[c + 1] = scale * (acc[v].y + (g ? g[c + 1] : 0.0));
+    } else {
+      double* dst = partial + static_cast<long long>(blockIdx.y) * ncols + c;
+      dst[0] = acc[v].x;
+      if (c + 1 < ncols) dst[1] = acc[v].y;
+    }
   }
 }
 
@@ -313,9 +320,10 @@ extern "C" int dngd_gemv_t(dngd_ctx* ctx, void* stream, const double* J, int64_t
   if (nc > 1 && (work == nullptr || work_bytes < static_cast<size_t>(nc) * ncols * 8)) {
     return set_error(ctx, DNGD_ERR_DIMENSION, "gemv_t: workspace too small");
   }
-  dim3 grid(static_cast<unsigned>((ncols + kGTCols - 1) / kGTCols), static_cast<unsigned>(nc));
-  k_gemv_t<<<grid, kGT, 0, s>>>(J, m, ncols, ldJ, y, nc, g, scale, out,
-                                static_cast<double*>(work));
+  const long long cols = 2LL * kGT * kGTV;
+  dim3 grid(static_cast<unsigned>((ncols + cols - 1) / cols), static_cast<unsigned>(nc));
+  k_gemv_t<kGTV><<<grid, kGT, 0, s>>>(J, m, ncols, ldJ, y, nc, g, scale, out,
+                                      static_cast<double*>(work));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_status(ctx, e, "gemv_t");
   if (nc > 1) {

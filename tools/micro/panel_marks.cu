@@ -32,4 +32,11 @@ int main(int argc, char** argv) {
       printf(" f %lld t %lld u %lld |", c[b][2 + 3 * t] - c[b][1 + 3 * t], c[b][3 + 3 * t] - c[b][2 + 3 * t], c[b][4 + 3 * t] - c[b][3 + 3 * t]);
     printf(" total %lld\n", c[b][13] - c[b][0]);
   }
+  long long pre[4][4][16]; cudaMemcpyFromSymbol(pre, dngd::g_panel_pre, sizeof pre);
+  for (int b = 0; b < 2; ++b)
+    for (int w = 0; w < 4; ++w) {
+      printf("cta %d warp %d arrive (rel. to phase start):", b, w);
+      for (int k = 1; k < 14; ++k) printf(" %lld", pre[b][w][k] - c[b][k - 1]);
+      printf("\n");
+    }
 }

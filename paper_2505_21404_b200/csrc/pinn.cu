@@ -319,10 +319,13 @@ __global__ void __launch_bounds__(256) k_jwrite(Classes T, const double* __restr
   const long long E = static_cast<long long>(win + 1) * wout;
   const int nch = C.nch;
   if (VEC) {
-    const long long e0 = (static_cast<long long>(blockIdx.x) * 256 + threadIdx.x) * 2;
-    for (long long e = e0; e < E; e += static_cast<long long>(gridDim.x) * 512) {
-      const int pp = static_cast<int>(e / wout);
-      const int q = static_cast<int>(e - static_cast<long long>(pp) * wout);
+    // 32-bit element index (E = (win+1) wout < 2^31 for every layer this path
+    // takes; the wide input layer goes through k_jwrite_in): the 64-bit division
+    // per element was most of this kernel's time
+    const int E32 = static_cast<int>(E);
+    for (int e = (blockIdx.x * 256 + threadIdx.x) * 2; e < E32; e += gridDim.x * 512) {
+      const int pp = e / wout;
+      const int q = e - pp * wout;
       const long long col = layer_off + e;
       if (col + 1 < col_begin || col >= col_end) continue;
       double a0 = 0.0, a1 = 0.0;
@@ -353,6 +356,109 @@ __global__ void __launch_bounds__(256) k_jwrite(Classes T, const double* __restr
         a = fma(h, z, a);
       }
       Jrow[col] = a;
+    }
+  }
+}
+
+// Element loop of k_jwrite_staged (block fully inside the column range).
+// NCH = 0: runtime channel count.
+template <int NCH>
+DNGD_DEV void jw_rows(const double* __restrict__ sh, const double* __restrict__ sz, int W1,
+                      int wout, int nch_rt, double2* __restrict__ dst) {
+  const int nch = NCH > 0 ? NCH : nch_rt;
+  const int WP = wout >> 1, NP = W1 * WP;
+  const int dpp = 256 / WP, dq = 256 - dpp * WP;
+  int f = threadIdx.x;
+  int pp = f / WP, qp = f - pp * WP;
+  const double2* sz2 = reinterpret_cast<const double2*>(sz);
+  for (; f < NP; f += 256) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int c = 0; c < (NCH > 0 ? NCH : 1); ++c) {
+      if (NCH == 0) break;
+      const double h = sh[c * W1 + pp];
+      const double2 z = sz2[c * WP + qp];
+      a0 = fma(h, z.x, a0);
+      a1 = fma(h, z.y, a1);
+    }
+    if (NCH == 0) {
+      for (int c = 0; c < nch; ++c) {
+        const double h = sh[c * W1 + pp];
+        const double2 z = sz2[c * WP + qp];
+        a0 = fma(h, z.x, a0);
+        a1 = fma(h, z.y, a1);
+      }
+    }
+    __stcs(dst + f, make_double2(a0, a1));
+    pp += dpp;
+    qp += dq;
+    if (qp >= WP) {
+      qp -= WP;
+      ++pp;
+    }
+  }
+}
+
+// Hidden-layer block of J for one row, with the row's channel activations
+// (nch x (win+1), bias column appended) and adjoints (nch x wout) staged in
+// shared memory by coalesced loads first: every global load of the row is in
+// flight at once, and the element loop reads only shared memory and streams
+// double2 stores.  Same arithmetic (channel order, fma chain) as k_jwrite<true>.
+__global__ void __launch_bounds__(256) k_jwrite_staged(Classes T, const double* __restrict__ Hk,
+                                                         long long ldh, int win,
+                                                         const double* __restrict__ Zb,
+                                                         long long ldz, int wout,
+                                                         long long layer_off, long long col_begin,
+                                                         long long col_end,
+                                                         double* __restrict__ J, long long ldJ) {
+  extern __shared__ __align__(16) double jw_smem[];
+  const long long p = blockIdx.x;
+  const ClassDev& C = T.c[find_class(T, p)];
+  const long long arow = C.act0 + (p - C.row0) * C.nch;
+  const int nch = C.nch, W1 = win + 1;
+  double* sh = jw_smem;                              // [nch][win + 1]
+  double* sz = jw_smem + ((nch * W1 + 1) & ~1);      // [nch][wout], 16-byte aligned
+  for (int idx = threadIdx.x; idx < nch * W1; idx += 256) {
+    const int c = idx / W1, pp = idx - c * W1;
+    sh[idx] = pp == win ? (c == 0 ? 1.0 : 0.0) : Hk[(arow + c) * ldh + pp];
+  }
+  for (int idx = threadIdx.x; idx < nch * wout; idx += 256) {
+    const int c = idx / wout, q = idx - c * wout;
+    sz[idx] = Zb[(arow + c) * ldz + q];
+  }
+  __syncthreads();
+  double* Jrow = J + p * ldJ - col_begin;
+  const int E = W1 * wout;
+  if (layer_off >= col_begin && layer_off + E <= col_end) {
+    // whole block inside the column range: flat double2 index f = pp * (wout/2) + qp,
+    // (pp, qp) stepped incrementally (no division in the loop), nch unrolled
+    double2* dst = reinterpret_cast<double2*>(Jrow + layer_off);
+    switch (nch) {
+      case 1: jw_rows<1>(sh, sz, W1, wout, nch, dst); break;
+      case 2: jw_rows<2>(sh, sz, W1, wout, nch, dst); break;
+      case 3: jw_rows<3>(sh, sz, W1, wout, nch, dst); break;
+      case 4: jw_rows<4>(sh, sz, W1, wout, nch, dst); break;
+      default: jw_rows<0>(sh, sz, W1, wout, nch, dst); break;
+    }
+    return;
+  }
+  for (int e = 2 * threadIdx.x; e < E; e += 512) {
+    const int pp = e / wout;
+    const int q = e - pp * wout;
+    const long long col = layer_off + e;
+    if (col + 1 < col_begin || col >= col_end) continue;
+    double a0 = 0.0, a1 = 0.0;
+    for (int c = 0; c < nch; ++c) {
+      const double h = sh[c * W1 + pp];
+      const double2 z = *reinterpret_cast<const double2*>(sz + c * wout + q);
+      a0 = fma(h, z.x, a0);
+      a1 = fma(h, z.y, a1);
+    }
+    if (col >= col_begin && col + 1 < col_end) {
+      __stcs(reinterpret_cast<double2*>(Jrow + col), make_double2(a0, a1));
+    } else {
+      if (col >= col_begin && col < col_end) Jrow[col] = a0;
+      if (col + 1 >= col_begin && col + 1 < col_end) Jrow[col + 1] = a1;
     }
   }
 }
@@ -1873,6 +1979,11 @@ static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& 
   bool identity_inputs = true;
   for (int c = 0; c < P.T.n; ++c)
     if (P.T.c[c].inp) identity_inputs = false;
+  int max_nch = 1;
+  for (int c = 0; c < P.T.n; ++c) max_nch = std::max(max_nch, P.T.c[c].nch);
+  auto jw_staged_bytes = [&](const auto&, int win, int wout) -> size_t {
+    return static_cast<size_t>(((max_nch * (win + 1) + 1) & ~1) + max_nch * wout) * sizeof(double);
+  };
   auto jwrite = [&](int k, const double* Hk, long long ldh, const double* Zb, long long ldz) {
     if (J == nullptr) return;
     const int win = static_cast<int>(P.w[k]), wout = static_cast<int>(P.w[k + 1]);
@@ -1884,8 +1995,13 @@ static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& 
       const unsigned gx = static_cast<unsigned>(std::min<long long>((E / 2 + 255) / 256, 64));
       k_jwrite_in<<<dim3(gx, static_cast<unsigned>(P.m)), 256, 0, s>>>(
           P.T, Zb, ldz, wout, col_begin, col_end, J, ldJ);
-    } else if (vec) {
-      const unsigned gx = static_cast<unsigned>(std::min<long long>((E + 511) / 512, 64));
+    } else if (vec && Hk != nullptr && jw_staged_bytes(P, win, wout) <= 48 * 1024) {
+      k_jwrite_staged<<<static_cast<unsigned>(P.m), 256, jw_staged_bytes(P, win, wout), s>>>(
+          P.T, Hk, ldh, win, Zb, ldz, wout, lo, col_begin, col_end, J, ldJ);
+    } else if (vec && E < (1LL << 31)) {
+      // ~8 column pairs per thread: one tiny CTA per 512 elements made the
+      // launch of ~10^4 CTAs, not the stores, the cost
+      const unsigned gx = static_cast<unsigned>(std::min<long long>((E + 4095) / 4096, 64));
       k_jwrite<true><<<dim3(gx, static_cast<unsigned>(P.m)), 256, 0, s>>>(
           P.T, Hk, ldh, win, Zb, ldz, wout, lo, col_begin, col_end, J, ldJ);
     } else {

@@ -208,3 +208,21 @@ def test_class_counts_must_be_positive():
                          ("poisson2d", (10, -1))]:
         with pytest.raises(DomainError):
             make_problem(name).sample(counts, np.random.default_rng(0))
+
+
+def test_stde_index_draw_matches_reference_argsort():
+    """PoissonBallStde.sample picks the k smallest of each row's uniforms with
+    argpartition; the reference (problems.py:363) uses argsort()[:, :k] on the
+    same draws -- identical indices, identical RNG stream afterwards."""
+    import numpy as np
+
+    import paper_2505_21404_b200 as P
+
+    pr = P.make_problem("poisson_ball_stde", dim=300, index_set_size=8)
+    rng_a, rng_b = np.random.default_rng(7), np.random.default_rng(7)
+    got = pr.sample((50,), rng_a).classes[0].aux["stde_idx"]
+    from paper_2505_21404_b200.problems import _ball_interior
+    _ball_interior(rng_b, 50, 300)
+    want = rng_b.random((50, 300)).argsort(axis=1)[:, :8]
+    assert np.array_equal(np.asarray(got), want)
+    assert rng_a.random() == rng_b.random()

@@ -1832,6 +1832,10 @@ __global__ void __launch_bounds__(128) k_jt_tiles(const __grid_constant__ JtPara
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
   const bool seeds = Lk.Z == nullptr;
+  // w_k a multiple of 64: no row tile holds the bias row; the first row tile sums
+  // it (sum of the value-channel rows of w Zbar) alongside the tensor-core tile
+  const bool xbias = (Lk.wh % JT_BM) == 0 && tpi == 0;
+  double bsum = 0.0;
   for (long long rb = r0; rb < r1; rb += JT_BK) {
     if (threadIdx.x < JT_BK) {
       const long long rho = rb + threadIdx.x;
@@ -1866,6 +1870,10 @@ __global__ void __launch_bounds__(128) k_jt_tiles(const __grid_constant__ JtPara
       Zs[r][c] = z;
     }
     __syncthreads();
+    if (xbias && threadIdx.x < JT_BM) {
+      for (int r = 0; r < JT_BK; ++r)
+        if (chs[r] == 0) bsum += Zs[r][threadIdx.x];
+    }
 #pragma unroll
     for (int kk = 0; kk < JT_BK; kk += 4) {
       double a[4], b[4];
@@ -1881,6 +1889,8 @@ __global__ void __launch_bounds__(128) k_jt_tiles(const __grid_constant__ JtPara
     __syncthreads();
   }
   double* dst = p.part + split * p.n + Lk.off;
+  if (xbias && threadIdx.x < JT_BM && q0 + static_cast<int>(threadIdx.x) < Lk.wz)
+    dst[static_cast<long long>(Lk.wh) * Lk.wz + q0 + threadIdx.x] = bsum;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int pr = p0 + wm * 32 + i * 8 + (lane >> 2);
@@ -2625,16 +2635,23 @@ struct JtScratch {
 // narrow nets: every layer in one tiled launch; wide ones: per-layer split-K GEMM
 static constexpr long long kJtTiledMaxWidth = 128;
 
+// row tiles of layer k's (w_k + 1) x w_{k+1} block in k_jt_tiles: when w_k is a
+// multiple of 64 the bias row is summed by the first row tile on the side
+// instead of costing a whole extra 64-row tile
+static int jt_row_tiles(long long wk) {
+  return static_cast<int>(wk % JT_BM == 0 ? wk / JT_BM : (wk + 1 + JT_BM - 1) / JT_BM);
+}
+
 JtScratch jt_plan(dngd_ctx* ctx, const Plan& P) {
   JtScratch S;
   S.tiled = P.wmax <= kJtTiledMaxWidth && P.w[0] <= MAXG;
   if (S.tiled) {
     S.tiles = 0;
     for (int k = 0; k < P.L; ++k)
-      S.tiles += static_cast<int>(((P.w[k] + 1 + JT_BM - 1) / JT_BM) * ((P.w[k + 1] + JT_BM - 1) / JT_BM));
+      S.tiles += jt_row_tiles(P.w[k]) * static_cast<int>((P.w[k + 1] + JT_BM - 1) / JT_BM);
     const int target = 2 * 2 * ctx->num_sms;  // two waves of two CTAs per SM
     long long sp = std::max(1, (target + S.tiles - 1) / S.tiles);
-    sp = std::min(sp, std::max(1LL, P.R / 128));
+    sp = std::min(sp, std::max(1LL, P.R / 64));
     S.rows_per_split = (P.R + sp - 1) / sp;
     S.rows_per_split = (S.rows_per_split + JT_BK - 1) / JT_BK * JT_BK;
     S.tsplits = static_cast<int>(std::max(1LL, (P.R + S.rows_per_split - 1) / S.rows_per_split));
@@ -2721,7 +2738,7 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
       l.off = P.off[k];
       l.tq = static_cast<int>((P.w[k + 1] + JT_BM - 1) / JT_BM);
       l.tile0 = tile0;
-      tile0 += static_cast<int>((P.w[k] + 1 + JT_BM - 1) / JT_BM) * l.tq;
+      tile0 += jt_row_tiles(P.w[k]) * l.tq;
     }
     jp.w = w;
     jp.rows_per_split = S.rows_per_split;

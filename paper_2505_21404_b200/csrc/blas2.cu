@@ -110,13 +110,14 @@ __global__ void k_gemv_t_reduce(const double* __restrict__ partial, int nchunks,
   out[c] = scale * (s + (g ? g[c] : 0.0));
 }
 
-// out[i] = alpha * A[i,:] . x + beta * add[i]; one CTA (256 threads) per row.
-__global__ void __launch_bounds__(256) k_gemv_n_row(const double* __restrict__ A, long long m,
+// out[i] = alpha * A[i,:] . x + beta * add[i]; one CTA (NT threads) per row.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_gemv_n_row(const double* __restrict__ A, long long m,
                                                       long long ncols, long long ld,
                                                       const double* __restrict__ x, double alpha,
                                                       const double* __restrict__ add, double beta,
                                                       double* __restrict__ out, int vec) {
-  __shared__ double sh[8];
+  __shared__ double sh[NT / 32];
   const long long i = blockIdx.x;
   const double* a = A + i * ld;
   double s0 = 0, s1 = 0;
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(256) k_gemv_n_row(const double* __restrict__ A
     const long long n2 = ncols / 2;
     const double2* a2 = reinterpret_cast<const double2*>(a);
     const double2* x2 = reinterpret_cast<const double2*>(x);
-    for (long long k = threadIdx.x; k < n2; k += 256) {
+    for (long long k = threadIdx.x; k < n2; k += NT) {
       const double2 u = __ldcs(a2 + k);
       const double2 v = __ldg(x2 + k);
       s0 = fma(u.x, v.x, s0);
@@ -132,9 +133,9 @@ __global__ void __launch_bounds__(256) k_gemv_n_row(const double* __restrict__ A
     }
     if ((ncols & 1) && threadIdx.x == 0) s0 = fma(a[ncols - 1], x[ncols - 1], s0);
   } else {
-    for (long long k = threadIdx.x; k < ncols; k += 256) s0 = fma(a[k], x[k], s0);
+    for (long long k = threadIdx.x; k < ncols; k += NT) s0 = fma(a[k], x[k], s0);
   }
-  const double s = block_sum<256>(s0 + s1, sh);
+  const double s = block_sum<NT>(s0 + s1, sh);
   if (threadIdx.x == 0) out[i] = alpha * s + (add ? beta * add[i] : 0.0);
 }
 
@@ -344,8 +345,14 @@ extern "C" int dngd_gemv_n(dngd_ctx* ctx, void* stream, const double* A, int64_t
                      (reinterpret_cast<uintptr_t>(x) & 15) == 0)
                         ? 1
                         : 0;
-    k_gemv_n_row<<<static_cast<unsigned>(m), 256, 0, s>>>(A, m, ncols, ldA, x, alpha, add, beta,
-                                                          out, vec);
+    // short rows (K at m ~ 3000): 128 threads, more rows in flight per SM
+    if (ncols < 8192) {
+      k_gemv_n_row<128><<<static_cast<unsigned>(m), 128, 0, s>>>(A, m, ncols, ldA, x, alpha, add,
+                                                                 beta, out, vec);
+    } else {
+      k_gemv_n_row<256><<<static_cast<unsigned>(m), 256, 0, s>>>(A, m, ncols, ldA, x, alpha, add,
+                                                                 beta, out, vec);
+    }
   } else {
     k_gemv_n_warp<<<static_cast<unsigned>((m + 7) / 8), 256, 0, s>>>(A, m, ncols, ldA, x, alpha,
                                                                       add, beta, out);

@@ -1337,6 +1337,27 @@ static void launch_transpose(cudaStream_t s, const double* W, long long src_s, i
   k_transpose<<<grid, dim3(32, 8), 0, s>>>(W, src_s, rows, cols, dst, ldd, dst_s);
 }
 
+// W_k -> W_k^T for every hidden layer k = 1..L-2 of one theta: one batched launch
+// when the hidden layers share a shape (their theta blocks and the destination
+// buffers are then equally spaced), else one launch per layer
+static void transpose_hidden(cudaStream_t s, const Plan& P, const double* th,
+                             const std::vector<double*>& Wt) {
+  const int L = P.L;
+  bool uniform = L - 2 >= 2;
+  for (int k = 2; uniform && k <= L - 2; ++k) {
+    uniform = P.w[k] == P.w[1] && P.w[k + 1] == P.w[2] && P.ld[k] == P.ld[1] &&
+              Wt[k] - Wt[k - 1] == Wt[2] - Wt[1] && P.off[k] - P.off[k - 1] == P.off[2] - P.off[1];
+  }
+  if (uniform) {
+    launch_transpose(s, th + P.off[1], P.off[2] - P.off[1], static_cast<int>(P.w[1]),
+                     static_cast<int>(P.w[2]), Wt[1], P.ld[1], Wt[2] - Wt[1], L - 2);
+    return;
+  }
+  for (int k = 1; k <= L - 2; ++k)
+    launch_transpose(s, th + P.off[k], 0, static_cast<int>(P.w[k]), static_cast<int>(P.w[k + 1]),
+                     Wt[k], P.ld[k], 0, 1);
+}
+
 // out = X W for the (din x w1) block W laid out like W0 (the STDE case, din ~ 1e5):
 // per class one split-K FP64 tensor-core GEMM over the raw points instead of a
 // din-long dot product per (point, neuron).  out rows are points (ld ld1).
@@ -1957,9 +1978,8 @@ static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& 
   k_input_fwd<<<nblk(P.m * P.w[1]), 256, 0, s>>>(P.T, theta, 0, static_cast<int>(P.w[1]),
                                                   P.ld[1], B.Z[0], B.H[1], 0, B.big.Zx, nullptr,
                                                   nullptr, P.ld[1], nullptr, nullptr);
+  transpose_hidden(s, P, theta, B.Wt);
   for (int k = 1; k <= L - 2; ++k) {
-    launch_transpose(s, theta + P.off[k], 0, static_cast<int>(P.w[k]),
-                     static_cast<int>(P.w[k + 1]), B.Wt[k], P.ld[k], 0, 1);
     GemmCall g;
     g.M = P.R;
     g.N = P.w[k + 1];
@@ -2493,11 +2513,9 @@ static int fvv_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const
   }
   k_fvv_input<<<nblk(P.m * P.w[1]), 256, 0, s>>>(P.T, theta, v, static_cast<int>(P.w[1]), ld,
                                                   Hcur, zx, B.big.Dx, P.ld[1]);
+  transpose_hidden(s, P, theta, B.Wt);
+  transpose_hidden(s, P, v, B.Vt);
   for (int k = 1; k <= L - 2; ++k) {
-    launch_transpose(s, theta + P.off[k], 0, static_cast<int>(P.w[k]),
-                     static_cast<int>(P.w[k + 1]), B.Wt[k], P.ld[k], 0, 1);
-    launch_transpose(s, v + P.off[k], 0, static_cast<int>(P.w[k]), static_cast<int>(P.w[k + 1]),
-                     B.Vt[k], P.ld[k], 0, 1);
     GemmCall g;
     g.M = (order == 1 ? 2 : 3) * P.R;
     g.N = P.w[k + 1];

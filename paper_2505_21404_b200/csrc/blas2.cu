@@ -106,7 +106,16 @@ __global__ void k_gemv_t_reduce(const double* __restrict__ partial, int nchunks,
   const long long c = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= ncols) return;
   double s = 0.0;
-  for (int k = 0; k < nchunks; ++k) s += partial[static_cast<long long>(k) * ncols + c];
+  int k = 0;
+  // 8 loads in flight, added in the same (chunk) order as one at a time
+  for (; k + 8 <= nchunks; k += 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = partial[static_cast<long long>(k + j) * ncols + c];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[j];
+  }
+  for (; k < nchunks; ++k) s += partial[static_cast<long long>(k) * ncols + c];
   out[c] = scale * (s + (g ? g[c] : 0.0));
 }
 

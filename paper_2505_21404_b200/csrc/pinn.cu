@@ -1930,7 +1930,16 @@ __global__ void k_jt_reduce(const double* __restrict__ part, int splits, long lo
   const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= n) return;
   double s = 0.0;
-  for (int k = 0; k < splits; ++k) s += part[k * n + e];
+  int k = 0;
+  // 8 loads in flight, added in the same (split) order as one at a time
+  for (; k + 8 <= splits; k += 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = part[static_cast<long long>(k + j) * n + e];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[j];
+  }
+  for (; k < splits; ++k) s += part[static_cast<long long>(k) * n + e];
   out[e] = scale * s;
 }
 

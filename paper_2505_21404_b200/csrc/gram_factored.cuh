@@ -8,27 +8,30 @@
 // with G^H_k = Hext_k Hext_k^T and G^Z_k = Zbar_k Zbar_k^T over (point, channel)
 // rows and S summing the channels of a point.
 //
-// "G-space": the channel rows of each class are padded to a = 1, 2, 4 or 8 per
-// point, so every 8x8 DMMA fragment covers whole point pairs.  The padding is
-// free: a 3-D TMA tensor map (columns, channels, points) per (layer, operand,
-// class) returns a box of 64/a points x a channels x 16 columns, zero-filling
-// the channels >= nch, i.e. exactly 64 G-rows in the 128-byte-swizzled layout
-// the DMMA fragment loads of gemm.cu expect.  Per 64x64 G-tile and layer the
-// kernel runs two FP64 tensor-core GEMMs (K-dims w_k and w_{k+1}) through one
-// TMA/mbarrier ring, multiplies the accumulators elementwise, reduces each
-// a x b channel block with warp shuffles and adds the point-pair sums into a
-// K tile in shared memory.
+// "G-space": the channel rows of a class are packed, nch per point, exactly as
+// the activation buffers store them (row act0 + i nch + ch).  A 64-row operand
+// tile holds ppt = floor(64 / nch) whole points (63 useful rows at nch = 7,
+// 64 at nch = 1, 2, 4, 8); its last 64 - ppt nch rows belong to the next tile
+// and are ignored.  A 2-D TMA map (columns, class rows) per (layer, operand,
+// class) returns the box of 64 rows x 16 columns in the 128-byte-swizzled layout
+// the DMMA fragment loads of gemm.cu expect.  (Round 1 padded every point to a
+// power-of-two channel count: at nch = 7 that multiplied zeros in (8/7)^2 - 1 =
+// 31 % of the work.)  Per 64x64 G-tile and layer the kernel runs two FP64
+// tensor-core GEMMs (K-dims w_k and w_{k+1}) through one TMA/mbarrier ring and
+// adds the elementwise product of the accumulators into a G-space tile in
+// shared memory (each thread owns its fragment elements: no races, fixed
+// order).  After the last layer every point pair sums its nch_a x nch_b channel
+// block in a fixed order (deterministic K) and the tile is written with its
+// mirror.
 //
 // Every layer takes the same epilogue: layer 0's Hext (the input channels:
 // value [x], d_j [e_j], Laplacian 0) is materialised once by k_input_channels,
-// the bias entry of Hext (1 on the value channel) is a per-thread constant, and
+// the bias entry of Hext (1 on the value channel) is a per-row flag product, and
 // the output layer's Zbar are the residual-operator seeds, whose outer product
-// is also a per-thread constant: an 8x8 fragment's rows are channels
-// lane/4 mod a and its columns 2(lane%4)+{0,1} mod b for every fragment.  The
-// channel reduction is instantiated per (a, b) so its shuffles are static.
-// Work: sum_k (a_c a_c') (w_k + w_{k+1}) per point pair instead of w_k w_{k+1}
-// for J J^T -- ~2x fewer FLOPs at config 2, ~4x at config 3, ~14x at config 4,
-// and J (823 GB at config 4) never has to exist.
+// is a per-row x per-column product.
+// Work: sum_k (nch_c nch_c') (w_k + w_{k+1}) per point pair instead of
+// w_k w_{k+1} for J J^T -- ~2x fewer FLOPs at config 2, ~5x at config 3, ~18x at
+// config 4, and J (823 GB at config 4) never has to exist.
 
 constexpr int GF_BM = 64;  // G-rows per tile side
 constexpr int GF_STAGES = 4;
@@ -38,6 +41,8 @@ constexpr int GF_MI = GF_BM / GF_WM / 8;        // 8x8 fragments per warp tile: 
 constexpr int GF_NJ = GF_BM / GF_WN / 8;        //                               columns
 constexpr int GF_STAGE_BYTES = 2 * GF_BM * 128;
 constexpr int GF_H0_LD = 16;  // row pitch of the materialised input channels
+constexpr int GF_GLD = GF_BM + 2;  // G-space product tile pitch (double2 RMW, fewer conflicts)
+constexpr int GF_MAXCH = 16;       // channels per point the packed tiles support
 
 struct GramLayer {
   int kh;  // w_k (din for layer 0: materialised input channels)
@@ -49,7 +54,8 @@ struct GramParams {
   Classes T;
   int L;
   GramLayer lay[DNGD_MAX_LAYERS];
-  int lg[DNGD_MAX_CLASSES];  // log2(padded channels per point)
+  int nch[DNGD_MAX_CLASSES];  // channels per point (packed rows)
+  int ppt[DNGD_MAX_CLASSES];  // whole points per 64-row tile = 64 / nch
   int npairs;
   int pc[10], pcp[10];       // class pair (c >= c')
   int tstart[11];            // tile prefix sums
@@ -89,55 +95,38 @@ __global__ void k_input_channels(Classes T, double* __restrict__ H0) {
 
 DNGD_DEV int gf_layer_chunks(const GramLayer& l) { return ((l.kh + 15) >> 4) + ((l.kz + 15) >> 4); }
 
-// K[point pairs] += S (G_H o G_Z) S^T for one warp's 32 x 16 G-block.  Fragment
-// (i, j): rows lrow = lane/4 (+8i), columns 2(lane%4)+{0,1} (+8j); G-row bits
-// below LGA are the channel, so the row channel is lrow mod a for every i.
-template <int LGA, int LGB, bool SEEDZ>
-DNGD_DEV void gf_epilogue(double2 (&accH)[GF_MI][GF_NJ], double2 (&accZ)[GF_MI][GF_NJ], double bias0,
-                          double bias1, const double* sA, const double* sB, double* Ks, int wm,
-                          int wn, int lane) {
+// G[g-row][g-col] += (G_H + bias) o G_Z for one warp's 32 x 16 G-block.
+// Fragment (i, j): rows lane/4 (+8i), columns 2(lane%4)+{0,1} (+8j).
+// bias(gr, gc) = zA[gr] zB[gc] (1 where both rows are a value channel).
+template <bool SEEDZ>
+DNGD_DEV void gf_epilogue(double2 (&accH)[GF_MI][GF_NJ], double2 (&accZ)[GF_MI][GF_NJ],
+                          const double* sA, const double* sB, const double* zA, const double* zB,
+                          double* Gs, int wm, int wn, int lane) {
   const int lrow = lane >> 2;
-  const bool own_r = (lrow & ((1 << LGA) - 1)) == 0;
-  const bool own_c = LGB <= 1 || (lane & ((1 << (LGB > 1 ? LGB - 1 : 0)) - 1)) == 0;
 #pragma unroll
   for (int i = 0; i < GF_MI; ++i) {
     const int gr = wm * (GF_MI * 8) + i * 8 + lrow;
-    const int pr = gr >> LGA;
+    const double za = zA[gr], sa = sA[gr];
 #pragma unroll
     for (int j = 0; j < GF_NJ; ++j) {
       const int gc = wn * (GF_NJ * 8) + j * 8 + 2 * (lane & 3);
-      // output layer: Zbar = per-row seeds (G^Z = seed_row * seed_col)
+      const double2 zb = *reinterpret_cast<const double2*>(zB + gc);
       double v0, v1;
-      if (SEEDZ) {
-        v0 = (accH[i][j].x + bias0) * (sA[gr] * sB[gc]);
-        v1 = (accH[i][j].y + bias1) * (sA[gr] * sB[gc + 1]);
+      if (SEEDZ) {  // output layer: Zbar = per-row seeds (G^Z = seed_row * seed_col)
+        const double2 sb = *reinterpret_cast<const double2*>(sB + gc);
+        v0 = fma(za, zb.x, accH[i][j].x) * (sa * sb.x);
+        v1 = fma(za, zb.y, accH[i][j].y) * (sa * sb.y);
       } else {
-        v0 = (accH[i][j].x + bias0) * accZ[i][j].x;
-        v1 = (accH[i][j].y + bias1) * accZ[i][j].y;
+        v0 = fma(za, zb.x, accH[i][j].x) * accZ[i][j].x;
+        v1 = fma(za, zb.y, accH[i][j].y) * accZ[i][j].y;
       }
       accH[i][j] = make_double2(0.0, 0.0);
       accZ[i][j] = make_double2(0.0, 0.0);
-      // column bits = (h, lane bit 0, lane bit 1), row bits = lane bits 2, 3, 4
-      if (LGB >= 1) v0 += v1;
-      if (LGB >= 2) v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
-      if (LGB >= 3) v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
-      if (LGA >= 1) {
-        v0 += __shfl_xor_sync(0xffffffffu, v0, 4);
-        if (LGB == 0) v1 += __shfl_xor_sync(0xffffffffu, v1, 4);
-      }
-      if (LGA >= 2) {
-        v0 += __shfl_xor_sync(0xffffffffu, v0, 8);
-        if (LGB == 0) v1 += __shfl_xor_sync(0xffffffffu, v1, 8);
-      }
-      if (LGA >= 3) {
-        v0 += __shfl_xor_sync(0xffffffffu, v0, 16);
-        if (LGB == 0) v1 += __shfl_xor_sync(0xffffffffu, v1, 16);
-      }
-      if (own_r && own_c) {
-        double* k = Ks + pr * GF_BM + (gc >> LGB);
-        k[0] += v0;
-        if (LGB == 0) k[1] += v1;
-      }
+      double2* g = reinterpret_cast<double2*>(Gs + gr * GF_GLD + gc);
+      double2 cur = *g;
+      cur.x += v0;
+      cur.y += v1;
+      *g = cur;
     }
   }
 }
@@ -146,8 +135,8 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     k_gram_factored(const __grid_constant__ GramParams p) {
   extern __shared__ uint8_t gf_smem_raw[];
   uint8_t* smem = smem_align(gf_smem_raw, 1024);
-  double* Ks = reinterpret_cast<double*>(smem + GF_STAGES * GF_STAGE_BYTES);  // 64 x 64 points max
-  uint64_t* full = reinterpret_cast<uint64_t*>(Ks + GF_BM * GF_BM);
+  double* Gs = reinterpret_cast<double*>(smem + GF_STAGES * GF_STAGE_BYTES);  // 64 x GF_GLD
+  uint64_t* full = reinterpret_cast<uint64_t*>(Gs + GF_BM * GF_GLD);
   uint64_t* empty = full + GF_STAGES;
   // ---- tile decode
   int pi = 0;
@@ -162,8 +151,8 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     ti = t / p.tj_n[pi];
     tj = t - ti * p.tj_n[pi];
   }
-  const int lga = p.lg[c], lgb = p.lg[cp];
-  const int np_r = GF_BM >> lga, np_c = GF_BM >> lgb;
+  const int na = p.nch[c], nb = p.nch[cp];
+  const int np_r = p.ppt[c], np_c = p.ppt[cp];
   const int P0 = ti * np_r, Q0 = tj * np_c;  // first point of the tile rows / cols
   int nchunks = 0;
   for (int k = 0; k < p.L; ++k) nchunks += gf_layer_chunks(p.lay[k]);
@@ -176,19 +165,24 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     }
     fence_barrier_init();
   }
-  for (int e = threadIdx.x; e < GF_BM * GF_BM / 2; e += GF_THREADS)
-    reinterpret_cast<double2*>(Ks)[e] = make_double2(0.0, 0.0);
-  // output-layer seeds per G-row (0 on padded channels and past the class end)
-  __shared__ double sA[GF_BM], sB[GF_BM];
+  for (int e = threadIdx.x; e < GF_BM * GF_GLD / 2; e += GF_THREADS)
+    reinterpret_cast<double2*>(Gs)[e] = make_double2(0.0, 0.0);
+  // per G-row: output-layer seeds and the value-channel flag of the bias entry
+  // (0 past the tile's whole points and past the class end)
+  __shared__ __align__(16) double sA[GF_BM], sB[GF_BM], zA[GF_BM], zB[GF_BM];
   if (threadIdx.x < GF_BM) {
     const int g = threadIdx.x;
     const ClassDev& Ca = p.T.c[c];
     const ClassDev& Cb = p.T.c[cp];
-    const int cha = g & ((1 << lga) - 1), pa = P0 + (g >> lga);
-    const int chb = g & ((1 << lgb) - 1), pb = Q0 + (g >> lgb);
-    sA[g] = (cha < Ca.nch && pa < Ca.count) ? seedc(p.T, Ca, cha, Ca.row0 + pa) : 0.0;
+    const int cha = g % na, pa = P0 + g / na;
+    const int chb = g % nb, pb = Q0 + g / nb;
+    const bool oka = g < np_r * na && pa < Ca.count;
     const long long cntb = p.rect ? p.ccount[cp] : Cb.count;  // rect: c3 == 0 (no u0 lookup)
-    sB[g] = (chb < Cb.nch && pb < cntb) ? seedc(p.T, Cb, chb, Cb.row0 + pb) : 0.0;
+    const bool okb = g < np_c * nb && pb < cntb;
+    sA[g] = oka ? seedc(p.T, Ca, cha, Ca.row0 + pa) : 0.0;
+    sB[g] = okb ? seedc(p.T, Cb, chb, Cb.row0 + pb) : 0.0;
+    zA[g] = (oka && cha == 0) ? 1.0 : 0.0;
+    zB[g] = (okb && chb == 0) ? 1.0 : 0.0;
   }
   __syncthreads();
 
@@ -200,9 +194,9 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     const int st = f % GF_STAGES;
     uint8_t* sa = smem + st * GF_STAGE_BYTES;
     mbar_arrive_expect_tx(&full[st], GF_STAGE_BYTES);
-    tma_load_3d(sa, &p.maps[k][part][c], &full[st], kc * 16, 0, P0);
-    tma_load_3d(sa + GF_BM * 128, p.rect ? &p.cmaps[k][part][cp] : &p.maps[k][part][cp],
-                &full[st], kc * 16, 0, Q0);
+    tma_load_2d(sa, &p.maps[k][part][c], &full[st], kc * 16, P0 * na);
+    tma_load_2d(sa + GF_BM * 128, p.rect ? &p.cmaps[k][part][cp] : &p.maps[k][part][cp],
+                &full[st], kc * 16, Q0 * nb);
   };
   if (threadIdx.x == 0) {
     for (int f = 0; f < min(nchunks, GF_STAGES); ++f) issue(f);
@@ -211,12 +205,6 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm = warp / GF_WN, wn = warp - (warp / GF_WN) * GF_WN;
   const int lrow = lane >> 2;
-  // per-thread constants of the epilogue (see gf_epilogue)
-  const int chr = lrow & ((1 << lga) - 1);
-  const int chc0 = (2 * (lane & 3)) & ((1 << lgb) - 1), chc1 = (2 * (lane & 3) + 1) & ((1 << lgb) - 1);
-  const double bias0 = (chr == 0 && chc0 == 0) ? 1.0 : 0.0;
-  const double bias1 = (chr == 0 && chc1 == 0) ? 1.0 : 0.0;
-  const int epi = lga * 4 + lgb;
 
   double2 accH[GF_MI][GF_NJ], accZ[GF_MI][GF_NJ];
 #pragma unroll
@@ -273,30 +261,12 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
     if (f + 1 != f_layer_end) continue;
-    // ---- layer k_cur done
-    // output layer: Zbar = per-row seeds; other layers: the Z accumulator
-#define GF_EPI(A, B, S)                                                                         \
-  case A * 4 + B:                                                                               \
-    gf_epilogue<A, B, S>(accH, accZ, bias0, bias1, sA, sB, Ks, wm, wn, lane);                   \
-    break;
-#define GF_EPI_ALL(S)                                                                           \
-  GF_EPI(0, 0, S) GF_EPI(0, 1, S) GF_EPI(0, 2, S) GF_EPI(0, 3, S)                               \
-  GF_EPI(1, 0, S) GF_EPI(1, 1, S) GF_EPI(1, 2, S) GF_EPI(1, 3, S)                               \
-  GF_EPI(2, 0, S) GF_EPI(2, 1, S) GF_EPI(2, 2, S) GF_EPI(2, 3, S)                               \
-  GF_EPI(3, 0, S) GF_EPI(3, 1, S) GF_EPI(3, 2, S) GF_EPI(3, 3, S)
+    // ---- layer k_cur done: output layer Zbar = per-row seeds, else the Z accumulator
     if (p.lay[k_cur].kz == 0) {
-      switch (epi) {
-        GF_EPI_ALL(true)
-        default: break;
-      }
+      gf_epilogue<true>(accH, accZ, sA, sB, zA, zB, Gs, wm, wn, lane);
     } else {
-      switch (epi) {
-        GF_EPI_ALL(false)
-        default: break;
-      }
+      gf_epilogue<false>(accH, accZ, sA, sB, zA, zB, Gs, wm, wn, lane);
     }
-#undef GF_EPI_ALL
-#undef GF_EPI
     if (k_cur + 1 < p.L) {
       ++k_cur;
       f_layer_start = f_layer_end;
@@ -305,33 +275,27 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
     }
   }
   __syncthreads();
-  // ---- epilogue: K[row][col] and its mirror (one writer per entry)
+  // ---- channel reduction (fixed order) and K[row][col] with its mirror
   const long long cnt_r = p.T.c[c].count;
   const long long row0 = p.T.c[c].row0;
-  if (p.rect) {
-    const long long cnt_c = p.ccount[cp], col0 = p.ccol0[cp];
-    for (int e = threadIdx.x; e < np_r * np_c; e += GF_THREADS) {
-      const int r = e / np_c, cc = e - (e / np_c) * np_c;
-      if (P0 + r >= cnt_r || Q0 + cc >= cnt_c) continue;
-      p.K[(row0 + P0 + r) * p.ldK + col0 + Q0 + cc] = Ks[r * GF_BM + cc];
-    }
-    return;
-  }
-  const long long cnt_c = p.T.c[cp].count;
-  const long long col0 = p.T.c[cp].row0;
+  const long long cnt_c = p.rect ? p.ccount[cp] : p.T.c[cp].count;
+  const long long col0 = p.rect ? p.ccol0[cp] : p.T.c[cp].row0;
   for (int e = threadIdx.x; e < np_r * np_c; e += GF_THREADS) {
     const int r = e / np_c, cc = e - (e / np_c) * np_c;
     const long long pr = P0 + r, pcl = Q0 + cc;
     if (pr >= cnt_r || pcl >= cnt_c) continue;
     const long long row = row0 + pr, col = col0 + pcl;
-    if (c == cp && col > row) continue;
-    const double v = Ks[r * GF_BM + cc];
+    if (!p.rect && c == cp && col > row) continue;
+    const double* g = Gs + (r * na) * GF_GLD + cc * nb;
+    double v = 0.0;
+    for (int a = 0; a < na; ++a)
+      for (int b = 0; b < nb; ++b) v += g[a * GF_GLD + b];
     p.K[row * p.ldK + col] = v;
-    p.K[col * p.ldK + row] = v;
+    if (!p.rect) p.K[col * p.ldK + row] = v;
   }
 }
 
 static size_t gram_factored_smem() {
-  return 1024 + GF_STAGES * GF_STAGE_BYTES + GF_BM * GF_BM * sizeof(double) +
+  return 1024 + GF_STAGES * GF_STAGE_BYTES + GF_BM * GF_GLD * sizeof(double) +
          2 * GF_STAGES * sizeof(uint64_t);
 }

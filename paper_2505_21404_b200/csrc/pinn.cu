@@ -2115,17 +2115,17 @@ extern "C" int dngd_activations(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   return assemble_impl(ctx, s, P, B, theta, 0, P.n, r, nullptr, 0, true);
 }
 
-// 3-D maps (columns, channels, points) over one class's rows of H_k / Zbar_k; a
-// box of 16 x a x 64/a is one 64-row G-space operand tile (channels >= nch are
-// out of bounds and arrive as zeros)
-static int gf_encode3(dngd_ctx* ctx, CUtensorMap* map, const double* base, long long inner,
-                      int nch, long long N, long long ld, int lg) {
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(nch),
-                        static_cast<cuuint64_t>(std::max<long long>(N, 1))};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 8, static_cast<cuuint64_t>(ld) * nch * 8};
-  cuuint32_t box[3] = {16, static_cast<cuuint32_t>(1 << lg), static_cast<cuuint32_t>(GF_BM >> lg)};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult res = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base),
+// 2-D maps (columns, packed channel rows) over one class's rows of H_k / Zbar_k:
+// N points x nch channels, row pitch ld; a box of 16 x 64 is one G-space operand
+// tile (rows past the class end arrive as zeros)
+static int gf_encode2(dngd_ctx* ctx, CUtensorMap* map, const double* base, long long inner,
+                      int nch, long long N, long long ld) {
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner),
+                        static_cast<cuuint64_t>(std::max<long long>(N * nch, 1))};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+  cuuint32_t box[2] = {16, static_cast<cuuint32_t>(GF_BM)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult res = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base),
                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -2133,7 +2133,8 @@ static int gf_encode3(dngd_ctx* ctx, CUtensorMap* map, const double* base, long 
                              : set_error(ctx, DNGD_ERR_CUDA, "gram_factored: tensor map encode failed");
 }
 
-// padded channel counts, layer K-dims and the row-side tensor maps of the factored Gram
+// channels per point, whole points per tile, layer K-dims and the row-side
+// tensor maps of the factored Gram
 static int gram_setup(dngd_ctx* ctx, const Plan& P, const AsmBufs& B, GramParams& gp) {
   int rc = DNGD_OK;
   memset(&gp, 0, sizeof gp);
@@ -2141,37 +2142,29 @@ static int gram_setup(dngd_ctx* ctx, const Plan& P, const AsmBufs& B, GramParams
   gp.L = P.L;
   for (int c = 0; c < P.T.n; ++c) {
     const int nch = P.T.c[c].nch;
-    int lg = 0;
-    while ((1 << lg) < nch) ++lg;
-    if (lg > 3) {
+    if (nch > GF_MAXCH) {
       return set_error(ctx, DNGD_ERR_UNSUPPORTED,
-                       "gram_factored: more than 8 channels per point; use assemble + syrk");
+                       "gram_factored: more than 16 channels per point; use assemble + syrk");
     }
-    gp.lg[c] = lg;
+    gp.nch[c] = nch;
+    gp.ppt[c] = GF_BM / nch;
   }
-  // 3-D maps (columns, channels, points) over each class's rows of H_k / Zbar_k;
-  // a box of 16 x a x 64/a is one 64-row G-space operand tile (channels >= nch
-  // are out of bounds and arrive as zeros)
-  auto encode3 = [&](CUtensorMap* map, const double* base, long long inner, int nch, long long N,
-                     long long ld, int lg) -> int {
-    return gf_encode3(ctx, map, base, inner, nch, N, ld, lg);
-  };
   for (int k = 0; k < P.L; ++k) {
     gp.lay[k].kh = static_cast<int>(P.w[k]);
     gp.lay[k].kz = k <= P.L - 2 ? static_cast<int>(P.w[k + 1]) : 0;
     for (int c = 0; c < P.T.n; ++c) {
       const ClassDev& Cc = P.T.c[c];
       if (k >= 1) {
-        rc = encode3(&gp.maps[k][0][c], B.H[k] + Cc.act0 * P.ld[k], P.w[k], Cc.nch, Cc.count,
-                     P.ld[k], gp.lg[c]);
+        rc = gf_encode2(ctx, &gp.maps[k][0][c], B.H[k] + Cc.act0 * P.ld[k], P.w[k], Cc.nch,
+                        Cc.count, P.ld[k]);
       } else {
-        rc = encode3(&gp.maps[0][0][c], B.H0 + Cc.act0 * GF_H0_LD, P.T.din, Cc.nch, Cc.count,
-                     GF_H0_LD, gp.lg[c]);
+        rc = gf_encode2(ctx, &gp.maps[0][0][c], B.H0 + Cc.act0 * GF_H0_LD, P.T.din, Cc.nch,
+                        Cc.count, GF_H0_LD);
       }
       if (rc) return rc;
       if (k <= P.L - 2) {
-        rc = encode3(&gp.maps[k][1][c], B.Zb[k] + Cc.act0 * P.ld[k + 1], P.w[k + 1], Cc.nch,
-                     Cc.count, P.ld[k + 1], gp.lg[c]);
+        rc = gf_encode2(ctx, &gp.maps[k][1][c], B.Zb[k] + Cc.act0 * P.ld[k + 1], P.w[k + 1],
+                        Cc.nch, Cc.count, P.ld[k + 1]);
         if (rc) return rc;
       }
     }
@@ -2262,8 +2255,8 @@ extern "C" int dngd_gram_factored_part(dngd_ctx* ctx, void* stream, const dngd_m
   gp.tstart[0] = 0;
   for (int c = 0; c < P.T.n; ++c) {
     for (int cp = 0; cp <= c; ++cp) {
-      const int ti = static_cast<int>((P.T.c[c].count + (GF_BM >> gp.lg[c]) - 1) / (GF_BM >> gp.lg[c]));
-      const int tj = static_cast<int>((P.T.c[cp].count + (GF_BM >> gp.lg[cp]) - 1) / (GF_BM >> gp.lg[cp]));
+      const int ti = static_cast<int>((P.T.c[c].count + gp.ppt[c] - 1) / gp.ppt[c]);
+      const int tj = static_cast<int>((P.T.c[cp].count + gp.ppt[cp] - 1) / gp.ppt[cp]);
       gp.pc[np] = c;
       gp.pcp[np] = cp;
       gp.tj_n[np] = tj;
@@ -2406,16 +2399,16 @@ extern "C" int dngd_gram_factored_cols(dngd_ctx* ctx, void* stream, const dngd_m
     col0 += Q.lc[c];
     for (int k = 0; k < P.L; ++k) {
       if (k >= 1) {
-        rc = gf_encode3(ctx, &gp.cmaps[k][0][c], gH[k] + Q.lrow0[c] * P.ld[k], P.w[k], Cc.nch,
-                        Q.lc[c], P.ld[k], gp.lg[c]);
+        rc = gf_encode2(ctx, &gp.cmaps[k][0][c], gH[k] + Q.lrow0[c] * P.ld[k], P.w[k], Cc.nch,
+                        Q.lc[c], P.ld[k]);
       } else {
-        rc = gf_encode3(ctx, &gp.cmaps[0][0][c], gH0 + Q.lrow0[c] * GF_H0_LD, P.T.din, Cc.nch,
-                        Q.lc[c], GF_H0_LD, gp.lg[c]);
+        rc = gf_encode2(ctx, &gp.cmaps[0][0][c], gH0 + Q.lrow0[c] * GF_H0_LD, P.T.din, Cc.nch,
+                        Q.lc[c], GF_H0_LD);
       }
       if (rc) return rc;
       if (k <= P.L - 2) {
-        rc = gf_encode3(ctx, &gp.cmaps[k][1][c], gZ[k] + Q.lrow0[c] * P.ld[k + 1], P.w[k + 1],
-                        Cc.nch, Q.lc[c], P.ld[k + 1], gp.lg[c]);
+        rc = gf_encode2(ctx, &gp.cmaps[k][1][c], gZ[k] + Q.lrow0[c] * P.ld[k + 1], P.w[k + 1],
+                        Cc.nch, Q.lc[c], P.ld[k + 1]);
         if (rc) return rc;
       }
     }
@@ -2425,8 +2418,8 @@ extern "C" int dngd_gram_factored_cols(dngd_ctx* ctx, void* stream, const dngd_m
   for (int c = 0; c < P.T.n; ++c) {
     for (int cp = 0; cp < P.T.n; ++cp) {
       if (Q.lc[cp] == 0) continue;
-      const int ti = static_cast<int>((P.T.c[c].count + (GF_BM >> gp.lg[c]) - 1) / (GF_BM >> gp.lg[c]));
-      const int tj = static_cast<int>((Q.lc[cp] + (GF_BM >> gp.lg[cp]) - 1) / (GF_BM >> gp.lg[cp]));
+      const int ti = static_cast<int>((P.T.c[c].count + gp.ppt[c] - 1) / gp.ppt[c]);
+      const int tj = static_cast<int>((Q.lc[cp] + gp.ppt[cp] - 1) / gp.ppt[cp]);
       gp.pc[np] = c;
       gp.pcp[np] = cp;
       gp.tj_n[np] = tj;

@@ -575,32 +575,45 @@ class PinnResidualMap(ResidualMap):
     gram_mode = "auto"  # "auto" | "factored" | "materialized"
 
     def _gram_flop_ratio(self) -> float:
-        """Estimated FLOPs of the factored Gram / FLOPs of J J^T."""
-        ksum = self._gram_ksum()
+        """Estimated FLOPs of the factored Gram (executed: whole 64-row tiles of
+        floor(64/nch) packed points, 16-column K chunks) / FLOPs of J J^T."""
+        ksum = self._gram_ksum(chunked=True)
         fact = 0.0
         for c in self.collocation.classes:
             for cp in self.collocation.classes:
-                a = 1 << max(0, (self._nch(c) - 1).bit_length())
-                b = 1 << max(0, (self._nch(cp) - 1).bit_length())
-                fact += c.count * cp.count * a * b * ksum
+                fact += self._tile_rows(c) * self._tile_rows(cp) * ksum
         return fact / max(1.0, float(self.m) ** 2 * self.n)
 
-    def factored_gram_flops(self) -> float:
-        """Algorithmic FLOPs of the factored Gram: lower G-space blocks x two GEMMs
-        per layer (K-dims w_k, w_{k+1}; the output layer's Zbar are seeds)."""
-        ksum = self._gram_ksum()
-        rows = [c.count * (1 << max(0, (self._nch(c) - 1).bit_length()))
-                for c in self.collocation.classes]
+    def _tile_rows(self, cls) -> int:
+        """G-space rows the packed kernel runs for a class: 64 per floor(64/nch) points."""
+        ppt = max(1, 64 // self._nch(cls))
+        return -(-cls.count // ppt) * 64
+
+    def factored_gram_flops(self, executed: bool = False) -> float:
+        """FLOPs of the factored Gram.  Useful (default): the lower triangle of the
+        point pairs x nch_c nch_c' channel pairs x the two GEMM K-dims per layer
+        (w_k for G^H, w_{k+1} for G^Z; the output layer's Zbar are seeds) -- the
+        work of the algorithm with nothing padded.  executed=True: what the kernel
+        issues (whole 64-row tiles, 16-column K chunks)."""
+        ksum = self._gram_ksum(chunked=executed)
+        classes = self.collocation.classes
         pairs = 0.0
-        for i, a in enumerate(rows):
-            for j, b in enumerate(rows[: i + 1]):
-                pairs += a * (a + 1) / 2 if i == j else a * b
+        for i, c in enumerate(classes):
+            for cp in classes[: i + 1]:
+                if executed:
+                    a, b = self._tile_rows(c) // 64, self._tile_rows(cp) // 64
+                    pairs += (a * (a + 1) / 2 if cp is c else a * b) * 64 * 64
+                else:
+                    a, b = self._nch(c), self._nch(cp)
+                    pairs += (c.count * (c.count + 1) / 2 * a * a if cp is c
+                              else c.count * cp.count * a * b)
         return 2.0 * pairs * ksum
 
-    def _gram_ksum(self) -> int:
-        """Sum over layers of the two GEMM K-dims, in the kernel's 16-column chunks."""
+    def _gram_ksum(self, chunked: bool = True) -> int:
+        """Sum over layers of the two GEMM K-dims (in the kernel's 16-column chunks
+        when chunked)."""
         w = self.spec.layer_widths
-        c16 = lambda x: -(-x // 16) * 16  # noqa: E731
+        c16 = (lambda x: -(-x // 16) * 16) if chunked else (lambda x: x)  # noqa: E731
         return sum(c16(w[k]) + (c16(w[k + 1]) if k <= len(w) - 3 else 0)
                    for k in range(len(w) - 1))
 

@@ -206,6 +206,14 @@ int dngd_gram_factored_part(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* ml
                             double* r, double* K, int64_t ldK, int part, int nparts, void* work,
                             size_t work_bytes);
 
+/* K (or part `part` of `nparts` of its tiles) from the activations left in
+ * act_work by dngd_activations at the same theta: the Gram kernel alone, so the
+ * activation pass and the tensor-core Gram can be timed (and scheduled)
+ * separately.  Same K as dngd_gram_factored_part, bit for bit. */
+int dngd_gram_factored_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                           const dngd_class_desc* classes, int nclass, double* K, int64_t ldK,
+                           int part, int nparts, void* act_work, size_t act_bytes);
+
 /* r plus the forward channels and per-point adjoints (no J) left in work for
  * dngd_jt_factored (the tape sweep of residuals.py:241-256 without the rows) */
 int dngd_activations(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,

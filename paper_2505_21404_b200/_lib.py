@@ -92,6 +92,8 @@ _SIGS = {
     "dngd_gram_factored_part": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp,
                                  ctypes.POINTER(ClassDesc), c_int, c_vp, c_vp, c_i64, c_int,
                                  c_int, c_vp, c_size], c_int),
+    "dngd_gram_factored_act": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc),
+                                c_int, c_vp, c_i64, c_int, c_int, c_vp, c_size], c_int),
     "dngd_activations": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, ctypes.POINTER(ClassDesc),
                           c_int, c_vp, c_vp, c_size], c_int),
     "dngd_jt_workspace": ([c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc), c_int,

@@ -235,7 +235,7 @@ template <int BM, int BN, int WM, int WN, int STAGES>
 static int launch_gemm(dngd_ctx* ctx, cudaStream_t s, const GemmCall& g) {
   using Cfg = GemmCfg<BM, BN, WM, WN, STAGES>;
   auto kern = k_gemm_nt<BM, BN, WM, WN, STAGES>;
-  static bool attr_set[64] = {false};  // per device
+  static std::atomic<bool> attr_set[64];  // per device (idempotent, race-free)
   if (!attr_set[ctx->device & 63]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(Cfg::kSmem));

@@ -2210,6 +2210,9 @@ static int gram_wide_input(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs
   return cuda_status(ctx, cudaGetLastError(), "gram_wide_input");
 }
 
+static int gram_from_act(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const AsmBufs& B, double* K,
+                         long long ldK, int part, int nparts);
+
 extern "C" int dngd_gram_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                                   const double* theta, const dngd_class_desc* classes,
                                   int nclass, double* r, double* K, int64_t ldK, void* work,
@@ -2248,8 +2251,15 @@ extern "C" int dngd_gram_factored_part(dngd_ctx* ctx, void* stream, const dngd_m
   P.T.u0 = B.u0;
   rc = assemble_impl(ctx, s, P, B, theta, 0, P.n, r, nullptr, 0, true);
   if (rc) return rc;
+  return gram_from_act(ctx, s, P, B, K, ldK, part, nparts);
+}
+
+// the factored Gram kernel over activations already in the workspace (left there
+// by dngd_activations / dngd_gram_factored at the same theta)
+static int gram_from_act(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const AsmBufs& B, double* K,
+                         long long ldK, int part, int nparts) {
   thread_local GramParams gp;  // ~17 KB of tensor maps: off the host stack, reentrant
-  rc = gram_setup(ctx, P, B, gp);
+  int rc = gram_setup(ctx, P, B, gp);
   if (rc) return rc;
   int np = 0, tiles = 0;
   gp.tstart[0] = 0;
@@ -2268,13 +2278,9 @@ extern "C" int dngd_gram_factored_part(dngd_ctx* ctx, void* stream, const dngd_m
   gp.npairs = np;
   gp.K = K;
   gp.ldK = ldK;
-  static bool attr[64] = {false};
-  if (!attr[ctx->device & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(k_gram_factored, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(gram_factored_smem()));
-    if (e != cudaSuccess) return cuda_status(ctx, e, "gram_factored smem attribute");
-    attr[ctx->device & 63] = true;
-  }
+  cudaError_t e = cudaFuncSetAttribute(k_gram_factored, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(gram_factored_smem()));
+  if (e != cudaSuccess) return cuda_status(ctx, e, "gram_factored smem attribute");
   static_assert(GF_H0_LD == 16, "carve_assemble reserves R x 16 for H0");
   // tile-sharded Gram: part p of nparts computes the contiguous tile range
   // [p T / nparts, (p+1) T / nparts) (every 64x64 G-tile costs the same)
@@ -2285,6 +2291,28 @@ extern "C" int dngd_gram_factored_part(dngd_ctx* ctx, void* stream, const dngd_m
     k_gram_factored<<<static_cast<unsigned>(t1 - t0), GF_THREADS, gram_factored_smem(), s>>>(gp);
   }
   return cuda_status(ctx, cudaGetLastError(), "gram_factored");
+}
+
+extern "C" int dngd_gram_factored_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                                      const dngd_class_desc* classes, int nclass, double* K,
+                                      int64_t ldK, int part, int nparts, void* act_work,
+                                      size_t act_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nparts < 1 || part < 0 || part >= nparts) {
+    return set_error(ctx, DNGD_ERR_DIMENSION, "gram_factored_act: part outside [0, nparts)");
+  }
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  if (bytes_of(P, 0, 1) > act_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_factored_act: workspace too small");
+  if (P.m == 0) return DNGD_OK;
+  if (P.wide_in) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_factored_act: wide input layer");
+  if (P.T.din > DNGD_MAX_GRAD) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_factored_act: input dim > 12");
+  Arena A{static_cast<char*>(act_work)};
+  AsmBufs B;
+  carve_assemble(P, A, B);
+  P.T.u0 = B.u0;
+  return gram_from_act(ctx, s, P, B, K, ldK, part, nparts);
 }
 
 // ------------------------------------------------------------------ K[:, I] without J
@@ -2433,13 +2461,9 @@ extern "C" int dngd_gram_factored_cols(dngd_ctx* ctx, void* stream, const dngd_m
   gp.K = Kc;
   gp.ldK = ldKc;
   gp.tile0 = 0;
-  static bool attr[64] = {false};
-  if (!attr[ctx->device & 63]) {
-    e = cudaFuncSetAttribute(k_gram_factored, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(gram_factored_smem()));
-    if (e != cudaSuccess) return cuda_status(ctx, e, "gram_cols smem attribute");
-    attr[ctx->device & 63] = true;
-  }
+  e = cudaFuncSetAttribute(k_gram_factored, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(gram_factored_smem()));
+  if (e != cudaSuccess) return cuda_status(ctx, e, "gram_cols smem attribute");
   if (tiles > 0) {
     k_gram_factored<<<static_cast<unsigned>(tiles), GF_THREADS, gram_factored_smem(), s>>>(gp);
   }
@@ -2609,7 +2633,7 @@ static int loss_many_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
     double* thetas = lp.part + ((static_cast<size_t>(ncand) * tiles + 31) / 32) * 32;
     lp.thetas = thetas;
     k_candidates<<<dim3(nblk(P.n), ncand), 256, 0, s>>>(theta, delta, etas, P.n, thetas);
-    static bool attr[64] = {false};
+    static std::atomic<bool> attr[64];  // per device (idempotent, race-free)
     if (!attr[ctx->device & 63]) {
       cudaError_t e = cudaFuncSetAttribute(k_loss_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(kLossFusedSmem));
@@ -2801,7 +2825,7 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   } else if (P.wide_in) {
     const int w1 = static_cast<int>(P.w[1]);
     dim3 g(static_cast<unsigned>((P.w[0] + 1 + JW_J - 1) / JW_J), (w1 + 127) / 128);
-    static bool attr[64] = {false};
+    static std::atomic<bool> attr[64];  // per device (idempotent, race-free)
     if (!attr[ctx->device & 63]) {
       cudaError_t e = cudaFuncSetAttribute(k_jt_input_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(kJwSmem));

@@ -259,6 +259,12 @@ def gram_factored(mlp, theta, classes_arr, nclass, r, K, ws, part=0, nparts=1):
              ws.numel())
 
 
+def gram_factored_act(mlp, classes_arr, nclass, K, act_ws, part=0, nparts=1):
+    """K (or part `part` of nparts of its tiles) from the activations in act_ws."""
+    call("dngd_gram_factored_act", ctx(), stream_handle(), ctypes.byref(mlp), classes_arr, nclass,
+         ptr(K), K.stride(0), int(part), int(nparts), ptr(act_ws), act_ws.numel())
+
+
 def activations(mlp, theta, classes_arr, nclass, r, ws):
     """r and the forward / adjoint activations (no J) into ws."""
     call("dngd_activations", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta), classes_arr,

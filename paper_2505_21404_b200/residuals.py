@@ -724,23 +724,28 @@ class PinnResidualMap(ResidualMap):
 
         d = self._device()
         th = self._theta_t(theta)
-        r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
+        if self.wide_input():  # analytic input block: one call does activations + K
+            r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
+            K.gram_factored(d["mlp"], th, d["arr"], d["nclass"], r, K_out, self._act_workspace())
+            _ACT_STATE["key"] = (self._key(th), self._act_identity())
+            _ACT_STATE["theta"] = th
+            self._rcache = (self._key(th), r, th)
+            return K_out
+        self.residuals_act_t(theta)  # r + activations (stage "activations")
+        ws = self._act_workspace()
         if self.gram_shard is not None:
             comm, rank, world = self.gram_shard
             K_out.zero_()
-            K.gram_factored(d["mlp"], th, d["arr"], d["nclass"], r, K_out,
-                            self._act_workspace(), rank, world)
+            with stage("gram_kernel"):
+                K.gram_factored_act(d["mlp"], d["arr"], d["nclass"], K_out, ws, rank, world)
             if K_out.is_contiguous():
                 comm.allreduce_sum_(K_out)
             else:
                 tmp = comm.allreduce_sum_(K_out.contiguous())
                 K_out.copy_(tmp)
         else:
-            K.gram_factored(d["mlp"], th, d["arr"], d["nclass"], r, K_out,
-                            self._act_workspace())
-        _ACT_STATE["key"] = (self._key(th), self._act_identity())
-        _ACT_STATE["theta"] = th
-        self._rcache = (self._key(th), r, th)
+            with stage("gram_kernel"):
+                K.gram_factored_act(d["mlp"], d["arr"], d["nclass"], K_out, ws)
         return K_out
 
     def residuals_gram_t(self, theta, K_out):

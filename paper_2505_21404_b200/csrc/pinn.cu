@@ -2076,7 +2076,9 @@ static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& 
       if (rc) return rc;
     }
   }
-  if (J == nullptr) {  // activations for the J-free kernels: also Hext_0
+  if (P.T.din <= DNGD_MAX_GRAD) {
+    // Hext_0 for the J-free kernels: an assembly that also wrote J leaves a
+    // complete activation workspace too (the factored Gram / J^T w may reuse it)
     k_input_channels<<<nblk(P.R * GF_H0_LD), 256, 0, s>>>(P.T, B.H0);
   }
   return cuda_status(ctx, cudaGetLastError(), "assemble adjoint");

@@ -666,14 +666,18 @@ class PinnResidualMap(ResidualMap):
 
         d = self._device()
         th = self._theta_t(theta)
-        if not self._act_valid(th):
-            r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
-            with stage("activations"):
-                K.activations(d["mlp"], th, d["arr"], d["nclass"], r, self._act_workspace())
-            _ACT_STATE["key"] = (self._key(th), self._act_identity())
-            _ACT_STATE["theta"] = th
-            self._rcache = (self._key(th), r, th)
-        return self._rcache[1]
+        key = self._key(th)
+        if self._act_valid(th):  # left by this theta's activation pass or assembly
+            for cache in (self._rcache, self._cache):
+                if cache is not None and cache[0] == key:
+                    return cache[1]
+        r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
+        with stage("activations"):
+            K.activations(d["mlp"], th, d["arr"], d["nclass"], r, self._act_workspace())
+        _ACT_STATE["key"] = (key, self._act_identity())
+        _ACT_STATE["theta"] = th
+        self._rcache = (key, r, th)
+        return r
 
     def jvp_t(self, theta, v_t):
         """J v: over the cached J, else from first-order forward tangents (no J)."""

@@ -107,14 +107,26 @@ TRAJ = {
 }
 
 
+REL_L2 = {"cfg1_traj": "poisson2d", "cfg2_traj": "heat1d", "pcg_traj": "poisson2d"}
+
+
 @pytest.mark.parametrize("name", sorted(TRAJ))
 def test_oracle_trajectory(golden_dir, name):
     fx = _load(golden_dir, name)
     problem, counts, cfg = TRAJ[name]
     widths = tuple(int(w) for w in fx["widths"])
-    rows, theta = O.dngd_run(problem, widths, counts, cfg, int(fx["seed"]))
+    rel = None
+    if name in REL_L2:  # the oracle's rel-L2 metric on the problem's evaluation grid
+        from paper_2505_21404_b200.problems import make_problem
+
+        prob = make_problem(REL_L2[name])
+        pts = prob.eval_points()
+        rel = O.rel_l2_fn(widths, pts, prob.exact_solution(pts))
+    rows, theta = O.dngd_run(problem, widths, counts, cfg, int(fx["seed"]), rel_l2=rel)
     losses = np.array([r["loss"] for r in rows])
     np.testing.assert_allclose(losses, fx["loss"], rtol=1e-6)
+    if rel is not None:
+        np.testing.assert_allclose([r["rel_l2"] for r in rows], fx["rel_l2"], rtol=1e-6)
     etas = np.array([r["eta"] for r in rows])
     np.testing.assert_array_equal(etas[1:], fx["eta"][1:])
     np.testing.assert_allclose([r["lam"] for r in rows][1:], fx["lam"][1:], rtol=1e-6)

@@ -20,7 +20,11 @@
  *    cudaStream_t passed as void*); nothing synchronises the device except
  *    where stated.  Calls are reentrant: state lives in the dngd_ctx, one
  *    context per calling thread (reference service.py:125-128 fans seeds
- *    over threads).
+ *    over threads).  The calls of one context are stream-ordered: issue them
+ *    on one stream at a time (the multi-CTA reductions keep their partials in
+ *    the context).  Context creation and destruction never touch the legacy
+ *    stream nor synchronise the device, so they are safe while another thread
+ *    captures a CUDA graph; destroy a context only after its work has drained.
  *  - Status codes map 1:1 onto the reference's errors.py classes.
  */
 #ifndef DNGD_B200_H

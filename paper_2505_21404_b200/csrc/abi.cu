@@ -56,13 +56,25 @@ extern "C" int dngd_ctx_create(int device, dngd_ctx** out) {
     return DNGD_ERR_CUDA;
   }
   ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  e = cudaMalloc(&ctx->dot_part, (dngd::kDotBlocks + 2) * sizeof(double));
+  // stream-ordered setup on the context's own non-blocking stream: nothing here may
+  // touch the legacy stream or synchronise the device, because another thread may
+  // be capturing a CUDA graph at this moment (reentrancy)
+  e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
+  if (e == cudaSuccess) {
+    e = cudaMallocAsync(reinterpret_cast<void**>(&ctx->dot_part),
+                        (dngd::kDotBlocks + 2) * sizeof(double), ctx->own);
+  }
   if (e == cudaSuccess) {
     ctx->dot_counter = reinterpret_cast<unsigned*>(ctx->dot_part + dngd::kDotBlocks);
-    e = cudaMemset(ctx->dot_counter, 0, 2 * sizeof(double));
+    e = cudaMemsetAsync(ctx->dot_counter, 0, 2 * sizeof(double), ctx->own);
   }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->own);
   if (e != cudaSuccess) {
-    if (ctx->dot_part) cudaFree(ctx->dot_part);
+    if (ctx->dot_part) cudaFreeAsync(ctx->dot_part, ctx->own);
+    if (ctx->own) {
+      cudaStreamSynchronize(ctx->own);
+      cudaStreamDestroy(ctx->own);
+    }
     delete ctx;
     return DNGD_ERR_CUDA;
   }
@@ -85,7 +97,13 @@ extern "C" int dngd_ctx_destroy(dngd_ctx* ctx) {
     if (ctx->ev_join2) cudaEventDestroy(ctx->ev_join2);
     if (ctx->hi) cudaStreamDestroy(ctx->hi);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
-    if (ctx->dot_part) cudaFree(ctx->dot_part);
+    // stream-ordered free (no device-wide synchronisation: see dngd_ctx_create);
+    // the caller guarantees its streams no longer run work of this context
+    if (ctx->dot_part) cudaFreeAsync(ctx->dot_part, ctx->own);
+    if (ctx->own) {
+      cudaStreamSynchronize(ctx->own);
+      cudaStreamDestroy(ctx->own);
+    }
   }
   delete ctx;
   return DNGD_OK;

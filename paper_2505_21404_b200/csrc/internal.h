@@ -29,6 +29,7 @@ struct dngd_ctx {
   // are stream-ordered; the counter is reset by the last CTA)
   double* dot_part = nullptr;
   unsigned* dot_counter = nullptr;
+  cudaStream_t own = nullptr;  // the context's private stream (setup / teardown only)
 };
 
 namespace dngd {

@@ -39,23 +39,28 @@ class Workspace:
         return self.buf
 
 
-_WS: dict[str, Workspace] = {}
-_WS_STACK: list = []  # private tables (a captured CUDA graph owns its scratch)
+def _ws_tables():
+    from ._state import tls
+
+    st = tls()
+    return st.ws, st.ws_stack  # per thread: (tag -> Workspace, private graph tables)
 
 
 @contextlib.contextmanager
 def private_workspaces(table: dict):
     """Route workspace() to `table` (a CUDA graph's own buffers, which nothing else
     may grow or free after capture)."""
-    _WS_STACK.append(table)
+    stack = _ws_tables()[1]
+    stack.append(table)
     try:
         yield
     finally:
-        _WS_STACK.pop()
+        stack.pop()
 
 
 def workspace(tag: str, nbytes: int) -> torch.Tensor:
-    table = _WS_STACK[-1] if _WS_STACK else _WS
+    base, stack = _ws_tables()
+    table = stack[-1] if stack else base
     ws = table.get(tag)
     if ws is None:
         ws = table[tag] = Workspace()

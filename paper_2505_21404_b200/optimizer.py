@@ -90,6 +90,7 @@ class TrainTrace:
     final_theta: ParameterVector | None = None
     aborted: bool = False
     abort_reason: str | None = None
+    abort_traceback: str | None = None  # not in the reference trace schema (diagnostics)
     diverged: bool = False
 
     @property
@@ -159,9 +160,6 @@ def line_search(loss_many, theta, delta, current_loss: float | None = None,
     return _select(losses, etas, current_loss, points_count)
 
 
-_ETAS = {}
-
-
 def device_line_search(rmap: ResidualMap, theta: ParameterVector, delta_t,
                        current_loss: float | None, points_count: int = 31) -> LineSearchResult:
     """line_search with the candidate losses evaluated by the batched device kernel;
@@ -170,9 +168,12 @@ def device_line_search(rmap: ResidualMap, theta: ParameterVector, delta_t,
     import torch
 
     key = (points_count, str(delta_t.device))
-    etas_t = _ETAS.get(key)
+    from ._state import tls
+
+    etas_tab = tls().etas
+    etas_t = etas_tab.get(key)
     if etas_t is None:
-        etas_t = _ETAS[key] = torch.as_tensor(
+        etas_t = etas_tab[key] = torch.as_tensor(
             2.0 ** -np.arange(points_count, dtype=np.float64), device=delta_t.device
         )
     losses = rmap.losses_along_t(theta, delta_t, etas_t).cpu().numpy()
@@ -221,9 +222,10 @@ def _eager_body(rmap, theta, config: OptimizerConfig, rng, rejections: int, redo
         fused = dense_iteration(rmap, theta, config.use_ga, config.line_search_points,
                                 config.lam_cap, mult)
         loss, r = fused[3], fused[4]
+        J = None
         if fused[0] is None:
             fused = None  # factorisation failed: eager path keeps the retry ladder
-        J = None if jfree else rmap.jacobian_t(theta)
+            J = None if jfree else rmap.jacobian_t(theta)  # only the fallback needs J
     elif dense:
         if jfree:
             r, J = rmap.residuals_act_t(theta), None
@@ -325,8 +327,11 @@ class _Book:
         self.trace.rows.append(row)
 
     def abort(self, iteration, exc):
+        import traceback
+
         self.trace.aborted = True
         self.trace.abort_reason = f"error at iteration {iteration}: {exc!r}"
+        self.trace.abort_traceback = "".join(traceback.format_exception(exc))
 
 
 def _pipeline_ok(rmap, config) -> bool:
@@ -532,7 +537,10 @@ def dngd_minimize(residual_map: ResidualMap, theta, config: OptimizerConfig,
     if not isinstance(theta, ParameterVector):
         theta = ParameterVector(theta, residual_map.layout)
     trace = TrainTrace(problem="custom", method="dngd", seed=-1)
-    return _dngd_loop(trace, lambda it: residual_map, theta, config, rng)
+    from ._state import thread_stream
+
+    with thread_stream():
+        return _dngd_loop(trace, lambda it: residual_map, theta, config, rng)
 
 
 # -- primal oracles and the primal/dual regime sweep -----------------
@@ -603,16 +611,16 @@ def timing_sweep(grid, iterations: int = 3, lam: float = 1e-3, seed: int = 0) ->
         theta = ParameterVector(rng.normal(size=n), rmap.layout)
         primal_times, dual_times = [], []
         for _ in range(iterations):
-            torch.cuda.synchronize()
+            torch.cuda.current_stream().synchronize()
             t0 = time.perf_counter()
             g = rmap.gradient_t(theta)
             primal_gn_solve(rmap, theta, g, lam=lam)
-            torch.cuda.synchronize()
+            torch.cuda.current_stream().synchronize()
             primal_times.append(time.perf_counter() - t0)
             t0 = time.perf_counter()
             g = rmap.gradient_t(theta)
             dense_dual_solve(rmap, theta, g, lam=lam, use_ga=False)
-            torch.cuda.synchronize()
+            torch.cuda.current_stream().synchronize()
             dual_times.append(time.perf_counter() - t0)
         primal_s = float(np.mean(primal_times))
         dual_s = float(np.mean(dual_times))
@@ -742,5 +750,8 @@ def dngd_run(problem, spec: MlpSpec, config: OptimizerConfig, seed: int, counts=
         return state["rmap"]
 
     trace = TrainTrace(problem=problem.name, method="dngd", seed=seed)
-    rel_fn = _rel_l2_fn(problem, spec) if track_rel_l2 else None
-    return _dngd_loop(trace, provider, theta, config, rng, rel_fn, on_step)
+    from ._state import thread_stream
+
+    with thread_stream():  # off the main thread: this thread's own stream
+        rel_fn = _rel_l2_fn(problem, spec) if track_rel_l2 else None
+        return _dngd_loop(trace, provider, theta, config, rng, rel_fn, on_step)

@@ -374,7 +374,11 @@ class LinearResidualMap(ResidualMap):
         return 0.5 * (R * R).sum(dim=1)
 
 
-_ACT_STATE: dict = {}  # which (theta version, map) the shared activation workspace holds
+def _act_state() -> dict:
+    """Which (theta version, map) this thread's activation workspace holds."""
+    from ._state import tls
+
+    return tls().act_state
 
 
 def _upload(arr, dev):
@@ -530,8 +534,8 @@ class PinnResidualMap(ResidualMap):
         with stage("assemble"):
             K.assemble(d["mlp"], th, d["arr"], d["nclass"], r, self._J, self.col_range[0],
                        self.col_range[1], self._act_workspace())
-        _ACT_STATE["key"] = (key, self._act_identity())
-        _ACT_STATE["theta"] = th  # keeps the keyed storage alive (no address reuse)
+        _act_state()["key"] = (key, self._act_identity())
+        _act_state()["theta"] = th  # keeps the keyed storage alive (no address reuse)
         self._cache = (key, r, self._J, th)
         return r, self._J
 
@@ -674,8 +678,8 @@ class PinnResidualMap(ResidualMap):
         r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
         with stage("activations"):
             K.activations(d["mlp"], th, d["arr"], d["nclass"], r, self._act_workspace())
-        _ACT_STATE["key"] = (key, self._act_identity())
-        _ACT_STATE["theta"] = th
+        _act_state()["key"] = (key, self._act_identity())
+        _act_state()["theta"] = th
         self._rcache = (key, r, th)
         return r
 
@@ -714,7 +718,7 @@ class PinnResidualMap(ResidualMap):
         return (id(self), self._dev["arr"] if self._dev else None)
 
     def _act_valid(self, th) -> bool:
-        return _ACT_STATE.get("key") == (self._key(th), self._act_identity())
+        return _act_state().get("key") == (self._key(th), self._act_identity())
 
     gram_shard = None  # (comm, rank, world): tile-sharded Gram summed over the ranks
 
@@ -731,8 +735,8 @@ class PinnResidualMap(ResidualMap):
         if self.wide_input():  # analytic input block: one call does activations + K
             r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
             K.gram_factored(d["mlp"], th, d["arr"], d["nclass"], r, K_out, self._act_workspace())
-            _ACT_STATE["key"] = (self._key(th), self._act_identity())
-            _ACT_STATE["theta"] = th
+            _act_state()["key"] = (self._key(th), self._act_identity())
+            _act_state()["theta"] = th
             self._rcache = (self._key(th), r, th)
             return K_out
         self.residuals_act_t(theta)  # r + activations (stage "activations")
@@ -771,8 +775,8 @@ class PinnResidualMap(ResidualMap):
         if not self._act_valid(th):
             r = torch.empty(self.m, dtype=torch.float64, device=d["device"])
             K.activations(d["mlp"], th, d["arr"], d["nclass"], r, self._act_workspace())
-            _ACT_STATE["key"] = (self._key(th), self._act_identity())
-            _ACT_STATE["theta"] = th
+            _act_state()["key"] = (self._key(th), self._act_identity())
+            _act_state()["theta"] = th
             self._rcache = (self._key(th), r, th)
         out = torch.empty(self.n, dtype=torch.float64, device=d["device"])
         scratch = K.workspace("jt", K.jt_workspace_bytes(d["mlp"], d["arr"], d["nclass"]))

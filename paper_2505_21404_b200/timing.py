@@ -8,7 +8,16 @@ from __future__ import annotations
 
 import contextlib
 
-_ACTIVE = None
+from ._state import tls
+
+
+def active():
+    """This thread's collecting StageTimer (None = stage timing off)."""
+    return tls().timer
+
+
+def set_active(timer) -> None:
+    tls().timer = timer
 
 
 class StageTimer:
@@ -31,24 +40,21 @@ class StageTimer:
         return out, counts
 
 
-_CAPTURE = None  # list receiving (name, start, end) while a CUDA graph is captured
-
-
 @contextlib.contextmanager
 def capture_into(sink: list):
     """Stage events recorded during graph capture go to `sink` as external event
     nodes (they fire on every replay); add_captured() reads them after a replay."""
-    global _CAPTURE
-    prev = _CAPTURE
-    _CAPTURE = sink
+    st = tls()
+    prev = st.capture
+    st.capture = sink
     try:
         yield
     finally:
-        _CAPTURE = prev
+        st.capture = prev
 
 
 def add_captured(pairs):
-    t = _ACTIVE
+    t = tls().timer
     if t is None:
         return
     for name, s, e in pairs:
@@ -57,13 +63,14 @@ def add_captured(pairs):
 
 @contextlib.contextmanager
 def stage(name: str):
-    t = _ACTIVE
-    if t is None and _CAPTURE is None:
+    st = tls()
+    t, cap = st.timer, st.capture
+    if t is None and cap is None:
         yield
         return
     import torch
 
-    if _CAPTURE is not None:
+    if cap is not None:
         s = torch.cuda.Event(enable_timing=True, external=True)
         e = torch.cuda.Event(enable_timing=True, external=True)
         s.record()
@@ -71,7 +78,7 @@ def stage(name: str):
             yield
         finally:
             e.record()
-            _CAPTURE.append((name, s, e))
+            cap.append((name, s, e))
         return
     s = torch.cuda.Event(enable_timing=True)
     e = torch.cuda.Event(enable_timing=True)
@@ -85,10 +92,10 @@ def stage(name: str):
 
 @contextlib.contextmanager
 def collect():
-    global _ACTIVE
-    prev = _ACTIVE
-    _ACTIVE = StageTimer()
+    st = tls()
+    prev = st.timer
+    st.timer = StageTimer()
     try:
-        yield _ACTIVE
+        yield st.timer
     finally:
-        _ACTIVE = prev
+        st.timer = prev

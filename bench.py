@@ -300,10 +300,8 @@ def run_ours(args, cfg):
     rank, world, local = _env_rank()
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world > 1 or args.sharded:
+        return run_sharded(args, cfg)
 
     problem = P.make_problem(cfg["problem"], **cfg.get("problem_kw", {}))
     spec = P.MlpSpec(cfg["widths"], seed=0)
@@ -314,28 +312,10 @@ def run_ours(args, cfg):
     fp64_peak = 35.47 if args.profile else _fp64_peak()
     hbm_peak, hbm_src = _hbm_peak()
 
-    # -------- device-resident run: all collocation sets uploaded before timing.
-    # N > 1, configs 1-2: column-sharded step (sharded.py) -- every rank draws the
-    # same points, assembles its own Jacobian columns, K is all-reduced over NCCL.
-    # Configs 3-4 (Gram-dominated, J too large): tile-sharded factored Gram -- each
-    # rank computes 1/N of K's tiles from the activations, one all-reduce of K,
-    # the rest of the step replicated.
-    tiles = world > 1 and cfg.get("multi_gpu") == "tiles"
-    sharded = world > 1 and not tiles
-    ranges = None
+    # -------- device-resident run: all collocation sets uploaded before timing
+    # (N > 1 runs through run_sharded)
+    tiles = sharded = False
     comm = None
-    if sharded:
-        from paper_2505_21404_b200.sharded import (Comm, CudaShardOps, column_ranges,
-                                                   sharded_dense_step, sharded_line_search)
-
-        comm = Comm()
-        ranges = column_ranges(spec.param_count(), world)
-        if sum(cfg["counts"]) >= cfg["dense_threshold"]:
-            raise SystemExit("multi-GPU bench covers the dense configs (1-4)")
-    if tiles:
-        from paper_2505_21404_b200.sharded import Comm
-
-        comm = Comm()
     rng = np.random.default_rng(1000 if world > 1 else 1000 + rank)
     total = args.warmup + args.steps + 2  # +2: the pipelined loop's ramp (see below)
     maps = []
@@ -343,10 +323,7 @@ def run_ours(args, cfg):
     for _ in range(total):
         colloc = P.sample_collocation(problem, cfg["counts"], rng)
         if base is None:
-            mp = P.PinnResidualMap(problem, spec, colloc,
-                                   col_range=ranges[rank] if sharded else None)
-            if tiles:
-                mp.gram_shard = (comm, rank, world)
+            mp = P.PinnResidualMap(problem, spec, colloc)
         else:
             mp = base.rebind(colloc)
         maps.append(mp)
@@ -363,8 +340,8 @@ def run_ours(args, cfg):
         from paper_2505_21404_b200.solver import dense_iteration
 
         dense = rmap.m < config.dense_threshold
-        jfree = not sharded and dense and rmap.jfree()
-        if not sharded and dense:
+        jfree = dense and rmap.jfree()
+        if dense:
             # the product's dense iteration (optimizer._dngd_loop): damping on the
             # device, one host read-back per step
             if not jfree:
@@ -384,8 +361,8 @@ def run_ours(args, cfg):
                 step = _dispatch_step(rmap, theta, g, lam, config, rng)
                 delta = step.delta.tensor
                 ls = device_line_search(rmap, theta, delta, loss, config.line_search_points)
-        else:
-            pcg_jfree = not sharded and rmap.jfree_pcg()
+        else:  # Nystrom-PCG configuration
+            pcg_jfree = rmap.jfree_pcg()
             if pcg_jfree:  # J-free PCG (solver.pcg_step with g=None)
                 r, J = rmap.residuals_act_t(theta), None
             else:
@@ -394,20 +371,13 @@ def run_ours(args, cfg):
                 shared_J = rmap._J
             loss = 0.5 * float(K.dot(r, r).item())
             lam = lm_damping(loss, config.lam_cap)
-            if sharded:
-                ops = CudaShardOps(rmap, theta, ranges)
-                step = sharded_dense_step(ops, comm, lam, config.use_ga)
-                delta = step["delta"]
-                ls = sharded_line_search(ops, comm, theta, delta, loss,
-                                         config.line_search_points)
-            else:  # Nystrom-PCG configuration
-                g = None
-                if not pcg_jfree:
-                    with timing.stage("gemv"):
-                        g = K.gemv_t(J, r, rmap.n)
-                step = _dispatch_step(rmap, theta, g, lam, config, rng)
-                delta = step.delta.tensor
-                ls = device_line_search(rmap, theta, delta, loss, config.line_search_points)
+            g = None
+            if not pcg_jfree:
+                with timing.stage("gemv"):
+                    g = K.gemv_t(J, r, rmap.n)
+            step = _dispatch_step(rmap, theta, g, lam, config, rng)
+            delta = step.delta.tensor
+            ls = device_line_search(rmap, theta, delta, loss, config.line_search_points)
         if ls.rejected:
             return theta, step
         return P.ParameterVector(K.axpby(ls.eta, delta, 1.0, theta.tensor), theta.layout), step
@@ -458,7 +428,7 @@ def run_ours(args, cfg):
             if it == 1:
                 s.record()
             if it == 2:
-                timing._ACTIVE = tm  # fetches of iterations 3 .. K+2
+                timing.set_active(tm)  # fetches of iterations 3 .. K+2
             if it == args.steps + 1:
                 e.record()
 
@@ -467,7 +437,7 @@ def run_ours(args, cfg):
         try:
             theta = run_loop(args.warmup, args.steps + 2, theta, mark)
         finally:
-            timing._ACTIVE = None
+            timing.set_active(None)
         torch.cuda.synchronize()
         stages, counts = tm.summary_ms()
     else:
@@ -516,15 +486,9 @@ def run_ours(args, cfg):
 
     tr = None
     try:
-        if not args.profile and sharded:
-            from paper_2505_21404_b200.sharded import sharded_dngd_run
-
-            tr = sharded_dngd_run(problem, spec, config, seed=0, comm=comm, counts=cfg["counts"],
-                                  init="xavier_normal", on_step=on_step)
-        elif not args.profile:
-            tr = P.dngd_run(problem, spec, config, seed=0 if tiles else rank,
-                            counts=cfg["counts"], init="xavier_normal", track_rel_l2=False,
-                            on_step=on_step, gram_shard=(comm, rank, world) if tiles else None)
+        if not args.profile:
+            tr = P.dngd_run(problem, spec, config, seed=rank, counts=cfg["counts"],
+                            init="xavier_normal", track_rel_l2=False, on_step=on_step)
     finally:
         P.PinnResidualMap._device = orig_device
     if "t0" in marks and "t1" in marks:
@@ -682,6 +646,159 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_sharded(args, cfg):
+    """N > 1 ranks (one per GPU, NCCL): the column-sharded D-NGD loop of sharded.py.
+    Configs 3-4 ("tiles"): J-free, each rank computes 1/N of the factored Gram's
+    tiles and its own J_p^T w rows, K all-reduced; configs 1, 2, 5 ("columns"):
+    each rank assembles J_p, K_p = J_p J_p^T (dense) or one m-vector all-reduce per
+    CG product (PCG).  Every rank draws the same collocation points; value = steps
+    / max-over-ranks device time of K steps (all ranks advance one shared step)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_21404_b200 as P
+    from paper_2505_21404_b200 import timing
+    from paper_2505_21404_b200.optimizer import TrainTrace
+    from paper_2505_21404_b200.sharded import Comm, make_ops, sharded_dngd_run, sharded_loop
+
+    rank, world, local = _env_rank()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    if "MASTER_PORT" not in os.environ:
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank,
+                            world_size=world)
+    comm = Comm()
+    problem = P.make_problem(cfg["problem"], **cfg.get("problem_kw", {}))
+    spec = P.MlpSpec(cfg["widths"], seed=0)
+    layout = cfg.get("multi_gpu", "columns")
+    config = P.OptimizerConfig(max_iters=args.steps + 1, lam_cap=cfg["lam_cap"],
+                               dense_threshold=cfg["dense_threshold"],
+                               nystrom_rank=cfg.get("nystrom_rank", 64),
+                               cg_max_iters=cfg.get("cg_max_iters", 500),
+                               deterministic_timing=True)
+    fp64_peak = 35.47 if args.profile else _fp64_peak()
+    hbm_peak, hbm_src = _hbm_peak()
+    theta = P.xavier_normal_params(spec)
+    theta = P.ParameterVector(theta.tensor, theta.layout)
+    rng = np.random.default_rng(1000)  # the same draws on every rank
+    total = args.warmup + args.steps + 1
+    ops_list = []
+    for _ in range(total):
+        ops = make_ops(layout, problem, spec, P.sample_collocation(problem, cfg["counts"], rng),
+                       theta, comm, prev=ops_list[-1] if ops_list else None)
+        ops.rmap._device()  # upload points and data now
+        ops_list.append(ops)
+
+    def run(first, count, theta, on_step=None):
+        sub = ops_list[first:first + count]
+        tr = TrainTrace(problem=problem.name, method="dngd-sharded", seed=0)
+        sharded_loop(tr, lambda it: sub[min(it, count) - 1], theta,
+                     replace(config, max_iters=count), comm, np.random.default_rng(7), layout,
+                     on_step)
+        if tr.aborted:
+            raise SystemExit(f"sharded bench loop aborted: {tr.abort_reason}\n{tr.abort_traceback}")
+        return tr.final_theta
+
+    theta = run(0, args.warmup, theta)
+    clocks = ClockSampler(local)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks.start()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def mark(it, th, step, ls):  # steps 2 .. K+1 of a K+1 step run: K whole steps
+        if it == 1:
+            s.record()
+        if it == args.steps + 1:
+            e.record()
+
+    mark.needs_theta = False
+    with timing.collect() as tm:
+        theta = run(args.warmup, args.steps + 1, theta, mark)
+        torch.cuda.synchronize()
+        stages, counts = tm.summary_ms()
+    dist.barrier()
+    dev_s = s.elapsed_time(e) * 1e-3
+    t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_s = float(t.item())
+    clk = clocks.stop()
+    # per-stage ms per step (this rank; stage timers include the collectives)
+    stage_ms = {k: v / (args.steps + 1) for k, v in stages.items()}
+
+    # -------- end to end: sharded_dngd_run (host sampling + uploads + per-step reads)
+    marks = {}
+
+    def on_step(it, th, step, ls):
+        if it == args.warmup:
+            torch.cuda.synchronize()
+            marks["t0"] = time.perf_counter()
+        if it == args.warmup + args.steps:
+            torch.cuda.synchronize()
+            marks["t1"] = time.perf_counter()
+
+    on_step.needs_theta = False
+    e2e = None
+    if not args.profile:
+        tr = sharded_dngd_run(problem, spec, replace(config, max_iters=args.warmup + args.steps),
+                              seed=0, comm=comm, counts=cfg["counts"], init="xavier_normal",
+                              on_step=on_step, layout=layout)
+        if "t0" in marks and "t1" in marks:
+            e2e_s = marks["t1"] - marks["t0"]
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+            m = sum(cfg["counts"])
+            h2d = 8 * m * (problem.raw_dim + 1) * world  # points + data, every rank
+            e2e = {"value": args.steps / e2e_s, "unit": UNIT,
+                   "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": (8 * (config.line_search_points + 4)) * world,
+                   "aborted": tr.aborted}
+    m = sum(cfg["counts"])
+    n = spec.param_count()
+    roof = None
+    ops0 = ops_list[0]
+    gk = stages.get("gram_kernel", 0.0) / max(counts.get("gram_kernel", 1), 1) * 1e-3
+    sy = stages.get("syrk", 0.0) / max(counts.get("syrk", 1), 1) * 1e-3
+    if gk > 0:
+        flops = ops0.rmap.factored_gram_flops() / world
+        roof = {"kernel": "dngd::k_gram_factored (this rank's 1/N of the tiles)",
+                "bound": "tensor", "achieved": flops / gk / 1e12, "peak": fp64_peak,
+                "unit": "TFLOP/s", "frac": flops / gk / 1e12 / fp64_peak, "traffic": None,
+                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
+                "algorithmic": f"factored Gram {flops:.4e} useful FLOP per rank per launch"}
+    elif sy > 0:
+        flops = m * (m + 1) * ops0.rmap.ncols
+        roof = {"kernel": "dngd::k_gemm_nt<128,128> (SYRK K_p = J_p J_p^T)", "bound": "tensor",
+                "achieved": flops / sy / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": flops / sy / 1e12 / fp64_peak, "traffic": None,
+                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
+                "algorithmic": f"m(m+1)n_p = {flops:.3e} FLOP per rank per launch"}
+    line = {
+        "metric": METRIC, "value": args.steps / dev_s, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded collocation sampling; Xavier-normal random init)",
+        "config": {"workload": cfg["name"], "m": m, "n": n, "widths": list(cfg["widths"]),
+                   "solver": "dense Cholesky + geodesic acceleration"
+                   if m < cfg["dense_threshold"] else "Nystrom-PCG",
+                   "lam_cap": cfg["lam_cap"], "line_search_points": 31,
+                   "parallelism": f"{layout}-sharded J over {world} GPUs (NCCL: all-reduce of K "
+                                  "or of the CG m-vector, all-gathers of v, f_vv, delta, losses)",
+                   "l2": "per-step working set exceeds L2"},
+        "roofline": roof, "stages_ms_per_step_rank0": stage_ms, "e2e": e2e,
+        "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src, "fp64_peak_tflops": fp64_peak,
+        "gpu_launches": None, "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ CPU oracle arm
 
 
@@ -800,6 +917,8 @@ def main():
     ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=25.0)
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the multi-GPU (sharded) loop even at one rank (checks that path)")
     ap.add_argument("--profile", action="store_true",
                     help="timed steps only (no peak probe / e2e / CPU arm): for ncu launch lists")
     args = ap.parse_args()

@@ -234,6 +234,17 @@ int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                      double* out, void* act_work, size_t act_bytes, void* scratch,
                      size_t scratch_bytes);
 
+/* Column slice of the same product: out[j - col_begin] = scale (J^T w)[j] for
+ * j in [col_begin, col_end) -- rank p's J_p^T w of the column-sharded step
+ * (solver.py:200,210).  Boundaries inside a hidden layer block
+ * must fall on one of its rows (a multiple of w_{k+1} from the block start);
+ * only the owned rows' tensor-core GEMMs run. */
+int dngd_jt_factored_range(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                           const dngd_class_desc* classes, int nclass, const double* w,
+                           double scale, double* out, int64_t col_begin, int64_t col_end,
+                           void* act_work, size_t act_bytes, void* scratch,
+                           size_t scratch_bytes);
+
 /* f_vv = d^2/dt^2 r(theta + t v) at t = 0 (residuals.py:304-317) */
 int dngd_fvv(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const double* theta,
              const double* v, const dngd_class_desc* classes, int nclass, double* fvv,

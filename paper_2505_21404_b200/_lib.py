@@ -100,6 +100,9 @@ _SIGS = {
                            ctypes.POINTER(c_size)], c_int),
     "dngd_jt_factored": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc), c_int,
                           c_vp, c_dbl, c_vp, c_vp, c_size, c_vp, c_size], c_int),
+    "dngd_jt_factored_range": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc),
+                                c_int, c_vp, c_dbl, c_vp, c_i64, c_i64, c_vp, c_size, c_vp,
+                                c_size], c_int),
     "dngd_fvv": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, c_vp, ctypes.POINTER(ClassDesc), c_int,
                   c_vp, c_vp, c_size], c_int),
     "dngd_gram_cols_workspace": ([c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc), c_int,

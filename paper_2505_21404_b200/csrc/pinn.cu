@@ -1943,6 +1943,27 @@ __global__ void k_jt_reduce(const double* __restrict__ part, int splits, long lo
   out[e] = scale * s;
 }
 
+// k_jt_reduce over the columns [c0, c0 + len) only, into out[0 .. len)
+__global__ void k_jt_reduce_range(const double* __restrict__ part, int splits, long long n,
+                                  long long c0, long long len, double scale,
+                                  double* __restrict__ out) {
+  const long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= len) return;
+  const long long e = c0 + q;
+  double s = 0.0;
+  int k = 0;
+  // 8 loads in flight, added in the same (split) order as one at a time
+  for (; k + 8 <= splits; k += 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = part[static_cast<long long>(k + j) * n + e];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[j];
+  }
+  for (; k < splits; ++k) s += part[static_cast<long long>(k) * n + e];
+  out[q] = scale * s;
+}
+
 static size_t bytes_of(const Plan& P, int mode, int C) {
   Arena A{nullptr};
   if (mode == 0) {
@@ -2676,6 +2697,7 @@ struct JtScratch {
   bool tiled;  // one k_jt_tiles launch (narrow nets)
   int tiles, tsplits;
   long long rows_per_split;
+  size_t off_tmp = 0;  // column-range mode: the input / output layer block before slicing
 };
 
 // narrow nets: every layer in one tiled launch; wide ones: per-layer split-K GEMM
@@ -2733,6 +2755,8 @@ JtScratch jt_plan(dngd_ctx* ctx, const Plan& P) {
     S.off_bt = S.off_xt + (static_cast<size_t>(P.w[0] + 1) * S.ldm * 8 + 255) / 256 * 256;
     S.bytes = S.off_bt + static_cast<size_t>(P.w[1]) * S.ldm * 8;
   }
+  S.off_tmp = (S.bytes + 255) / 256 * 256;  // column-range mode: the small edge layers
+  S.bytes = S.off_tmp + static_cast<size_t>(std::max((P.w[0] + 1) * P.w[1], P.w[P.L - 1] + 1)) * 8;
   return S;
 }
 
@@ -2747,10 +2771,15 @@ extern "C" int dngd_jt_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp,
   return DNGD_OK;
 }
 
-extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
-                                const dngd_class_desc* classes, int nclass, const double* w,
-                                double scale, double* out, void* act_work, size_t act_bytes,
-                                void* scratch, size_t scratch_bytes) {
+// out[j - c0] = scale (J^T w)[j] for j in [c0, c1) (the full vector: [0, n)).  In
+// a partial range every boundary inside a hidden layer block must fall on a row of
+// that block (a multiple of w_{k+1} from the block start): those GEMMs then run
+// only the owned rows (M = a1 - a0, the column-sharded multi-GPU step); the small
+// input / output blocks are formed whole and sliced.
+static int jt_range(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                    const dngd_class_desc* classes, int nclass, const double* w, double scale,
+                    double* out, long long c0, long long c1, void* act_work, size_t act_bytes,
+                    void* scratch, size_t scratch_bytes) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Plan P;
   int rc = make_plan(ctx, mlp, classes, nclass, P);
@@ -2760,7 +2789,33 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   if (scratch == nullptr || scratch_bytes < S.bytes) {
     return set_error(ctx, DNGD_ERR_DIMENSION, "jt_factored: scratch workspace too small");
   }
-  if (P.m == 0) return DNGD_OK;
+  if (c0 < 0 || c1 > P.n || c0 > c1) return set_error(ctx, DNGD_ERR_DIMENSION, "jt_factored: column range outside [0, n)");
+  const bool full = c0 == 0 && c1 == P.n;
+  if (P.m == 0 || c0 == c1) return DNGD_OK;
+  if (!full) {  // partial ranges: hidden-layer boundaries on block rows
+    for (int k = 1; k <= P.L - 2; ++k) {
+      const long long lo = P.off[k], hi = P.off[k] + (P.w[k] + 1) * P.w[k + 1];
+      for (long long b : {c0, c1}) {
+        if (b > lo && b < hi && (b - lo) % P.w[k + 1] != 0) {
+          return set_error(ctx, DNGD_ERR_DIMENSION, "jt_factored: range boundary inside a hidden-layer row");
+        }
+      }
+    }
+  }
+  char* const sc0 = static_cast<char*>(scratch);
+  double* const tmp = reinterpret_cast<double*>(sc0 + S.off_tmp);
+  // a small block [lo, lo + len) formed whole at dst (tmp unless the range covers it)
+  auto edge_dst = [&](long long lo, long long len) -> double* {
+    return (lo >= c0 && lo + len <= c1) ? out + (lo - c0) : tmp;
+  };
+  auto edge_copy = [&](double* dst, long long lo, long long len) -> int {
+    if (dst != tmp) return DNGD_OK;
+    const long long a = std::max(lo, c0), b = std::min(lo + len, c1);
+    if (b <= a) return DNGD_OK;
+    cudaError_t e = cudaMemcpyAsync(out + (a - c0), tmp + (a - lo), (b - a) * 8,
+                                    cudaMemcpyDeviceToDevice, s);
+    return e == cudaSuccess ? DNGD_OK : cuda_status(ctx, e, "jt_factored slice");
+  };
   if (P.T.din > MAXG && !P.wide_in) {
     return set_error(ctx, DNGD_ERR_UNSUPPORTED, "jt_factored: embedded inputs wider than 12");
   }
@@ -2791,7 +2846,11 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
     jp.n = P.n;
     jp.part = static_cast<double*>(scratch);
     k_jt_tiles<<<dim3(static_cast<unsigned>(S.tiles), static_cast<unsigned>(S.tsplits)), 128, 0, s>>>(jp);
-    k_jt_reduce<<<nblk(P.n), 256, 0, s>>>(jp.part, S.tsplits, P.n, scale, out);
+    if (full) {
+      k_jt_reduce<<<nblk(P.n), 256, 0, s>>>(jp.part, S.tsplits, P.n, scale, out);
+    } else {  // narrow nets: the whole vector is cheap; reduce only the range
+      k_jt_reduce_range<<<nblk(c1 - c0), 256, 0, s>>>(jp.part, S.tsplits, P.n, c0, c1 - c0, scale, out);
+    }
     return cuda_status(ctx, cudaGetLastError(), "jt_factored");
   }
   char* sc = static_cast<char*>(scratch);
@@ -2800,7 +2859,11 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   double* part = reinterpret_cast<double*>(sc + S.off_part);
   const int L = P.L;
   // input layer W0 | b0
-  if (P.wide_in && P.bigin) {
+  const long long len0 = (P.w[0] + 1) * P.w[1];
+  const bool in0 = P.off[0] < c1 && P.off[0] + len0 > c0;
+  double* const d0 = edge_dst(P.off[0], len0);
+  if (!in0) {
+  } else if (P.wide_in && P.bigin) {
     const int w1 = static_cast<int>(P.w[1]);
     const int din = P.T.din;
     double* Xt = reinterpret_cast<double*>(sc + S.off_xt);
@@ -2816,14 +2879,14 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
     g.lda = S.ldm;
     g.B = Bt;
     g.ldb = S.ldm;
-    g.C = out + P.off[0];
+    g.C = d0;
     g.ldc = w1;
     g.alpha = scale;
     g.beta = 0.0;
     rc = gemm_nt(ctx, s, g);
     if (rc) return rc;
     k_jt_onehot<<<static_cast<unsigned>((din + OH_ROWS - 1) / OH_ROWS), 128, 0, s>>>(
-        P.T, B.Zb[0], P.ld[1], w1, w, scale, out + P.off[0]);
+        P.T, B.Zb[0], P.ld[1], w1, w, scale, d0);
   } else if (P.wide_in) {
     const int w1 = static_cast<int>(P.w[1]);
     dim3 g(static_cast<unsigned>((P.w[0] + 1 + JW_J - 1) / JW_J), (w1 + 127) / 128);
@@ -2834,42 +2897,74 @@ extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
       if (e != cudaSuccess) return cuda_status(ctx, e, "jt_input_wide smem attribute");
       attr[ctx->device & 63] = true;
     }
-    k_jt_input_wide<<<g, 256, kJwSmem, s>>>(P.T, B.Zb[0], P.ld[1], w1, w, scale, out + P.off[0]);
+    k_jt_input_wide<<<g, 256, kJwSmem, s>>>(P.T, B.Zb[0], P.ld[1], w1, w, scale, d0);
   } else {
     const int w1 = static_cast<int>(P.w[1]);
     dim3 g((w1 + 127) / 128, S.nchunks);
     k_jt_input<<<g, 128, 0, s>>>(P.T, B.Zb[0], P.ld[1], w1, w, S.chunk, part);
     const long long cnt = (P.w[0] + 1) * P.w[1];
-    k_chunk_reduce<<<nblk(cnt), 256, 0, s>>>(part, S.nchunks, cnt, scale, out + P.off[0]);
+    k_chunk_reduce<<<nblk(cnt), 256, 0, s>>>(part, S.nchunks, cnt, scale, d0);
+  }
+  if (in0) {
+    rc = edge_copy(d0, P.off[0], len0);
+    if (rc) return rc;
   }
   // hidden layers: Hext_k^T diag(w) Zbar_k on the tensor cores
   for (int k = 1; k <= L - 2; ++k) {
     const int wk = static_cast<int>(P.w[k]), wk1 = static_cast<int>(P.w[k + 1]);
+    const long long lo = P.off[k], hi = P.off[k] + static_cast<long long>(wk + 1) * wk1;
+    if (hi <= c0 || lo >= c1) continue;
+    const long long a0 = (std::max(lo, c0) - lo) / wk1, a1 = (std::min(hi, c1) - lo) / wk1;
     dim3 tg(static_cast<unsigned>((P.R + 31) / 32), static_cast<unsigned>((wk + 1 + 31) / 32));
     k_act_transpose<<<tg, dim3(32, 8), 0, s>>>(P.T, B.H[k], P.ld[k], wk, nullptr, 1, Ht, S.ldR);
     dim3 zg(static_cast<unsigned>((P.R + 31) / 32), static_cast<unsigned>((wk1 + 31) / 32));
     k_act_transpose<<<zg, dim3(32, 8), 0, s>>>(P.T, B.Zb[k], P.ld[k + 1], wk1, w, 0, Zt, S.ldR);
     GemmCall g;
-    g.M = wk + 1;
+    g.M = a1 - a0;
     g.N = wk1;
     g.K = P.R;
-    g.A = Ht;
+    g.A = Ht + a0 * S.ldR;
     g.lda = S.ldR;
     g.B = Zt;
     g.ldb = S.ldR;
-    g.C = out + P.off[k];
+    g.C = out + (lo + a0 * wk1 - c0);
     g.ldc = wk1;
     g.alpha = scale;
     g.beta = 0.0;
-    rc = gemm_nt_splitk(ctx, s, g, gemm_splitk_choose(ctx, g.M, g.N, g.K), part, S.part_bytes);
+    int sp = gemm_splitk_choose(ctx, g.M, g.N, g.K);
+    while (sp > 1 && gemm_splitk_bytes(g.M, g.N, sp) > S.part_bytes) --sp;
+    rc = gemm_nt_splitk(ctx, s, g, sp, part, S.part_bytes);
     if (rc) return rc;
   }
   // output layer W_{L-1} | b_{L-1}
-  {
+  if (P.off[L - 1] < c1 && P.off[L - 1] + P.w[L - 1] + 1 > c0) {
     const int wl = static_cast<int>(P.w[L - 1]);
+    double* dl = edge_dst(P.off[L - 1], wl + 1);
     dim3 g((wl + 1 + 127) / 128, S.nchunks);
     k_jt_output<<<g, 128, 0, s>>>(P.T, B.H[L - 1], P.ld[L - 1], wl, w, S.chunk, part);
-    k_chunk_reduce<<<nblk(wl + 1), 256, 0, s>>>(part, S.nchunks, wl + 1, scale, out + P.off[L - 1]);
+    k_chunk_reduce<<<nblk(wl + 1), 256, 0, s>>>(part, S.nchunks, wl + 1, scale, dl);
+    rc = edge_copy(dl, P.off[L - 1], wl + 1);
+    if (rc) return rc;
   }
   return cuda_status(ctx, cudaGetLastError(), "jt_factored");
+}
+
+extern "C" int dngd_jt_factored(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                                const dngd_class_desc* classes, int nclass, const double* w,
+                                double scale, double* out, void* act_work, size_t act_bytes,
+                                void* scratch, size_t scratch_bytes) {
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  return jt_range(ctx, stream, mlp, classes, nclass, w, scale, out, 0, P.n, act_work, act_bytes,
+                  scratch, scratch_bytes);
+}
+
+extern "C" int dngd_jt_factored_range(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                                      const dngd_class_desc* classes, int nclass, const double* w,
+                                      double scale, double* out, int64_t col_begin,
+                                      int64_t col_end, void* act_work, size_t act_bytes,
+                                      void* scratch, size_t scratch_bytes) {
+  return jt_range(ctx, stream, mlp, classes, nclass, w, scale, out, col_begin, col_end, act_work,
+                  act_bytes, scratch, scratch_bytes);
 }

@@ -288,6 +288,13 @@ def jt_factored(mlp, classes_arr, nclass, w, scale, out, act_ws, scratch):
          float(scale), ptr(out), ptr(act_ws), act_ws.numel(), ptr(scratch), scratch.numel())
 
 
+def jt_factored_range(mlp, classes_arr, nclass, w, scale, out, c0, c1, act_ws, scratch):
+    """out = scale * (J^T w)[c0:c1] from the activations in act_ws (no J)."""
+    call("dngd_jt_factored_range", ctx(), stream_handle(), ctypes.byref(mlp), classes_arr, nclass,
+         ptr(w), float(scale), ptr(out), int(c0), int(c1), ptr(act_ws), act_ws.numel(),
+         ptr(scratch), scratch.numel())
+
+
 def fvv(mlp, theta, v, classes_arr, nclass, out, ws, act_ws=None):
     """f_vv; act_ws (activations at the same theta) lets the large-din input layer
     reuse x W0 instead of recomputing it."""

@@ -1,25 +1,38 @@
-"""Column-sharded D-NGD step across GPUs.
+"""The D-NGD step sharded across GPUs by parameter columns.
 
-Rank p owns the contiguous parameter slice [c_p, c_{p+1}) of the reference
-layout (model.py:48-54) and materialises only J_p = J[:, c_p:c_{p+1}].  One dense
-step (solver.py:176-219) becomes
+Rank p owns the contiguous parameter slice [c_p, c_{p+1}) of the reference layout
+(model.py:48-54) and applies only its own J_p^T (north star: "each GPU applies its
+own J_p^T alpha slice").  One dense step (solver.py:176-219) becomes
 
-    K_p = J_p J_p^T                    local FP64 tensor-core SYRK
-    K   = sum_p K_p                    ncclAllReduce over NVLink (m x m)
+    r                                  replicated (every rank has every point)
+    K   = sum_p K_p                    K_p local, one NCCL all-reduce (m x m)
     L   = chol(K + lam I)              replicated (identical K on every rank)
-    b   = -K r  (= -J g, g = J^T r)    replicated, no communication
-    v_p = -(J_p^T y + g_p) / lam       local
+    y   = (K + lam I)^-1 (-K r)        replicated (b = -J g = -K r, g = J^T r)
+    v_p = -J_p^T (y + r) / lam         local
     |v|^2                              all-reduce of one scalar
     v   = allgather(v_p)               n doubles, for f_vv
-    f_vv, b_a = -K f_vv, y_a           replicated
-    a_p = -J_p^T (y_a + f_vv) / lam    local, |a|^2 all-reduced
+    f_vv rows of this rank's points    local, then allgather (m doubles)
+    b_a = -K f_vv, y_a                 replicated
+    a_p = -J_p^T (y_a + f_vv) / lam    local, |a|^2 all-reduced, GA gate
     delta = allgather(v_p + a_p/2)     for the line search
     line search                        candidates split across ranks, 31 losses gathered
 
-The residuals r and the forward/adjoint activations are computed redundantly on
-every rank (the J_p row segments need every layer's adjoints).  The numeric
-operations come from a per-rank `ops` object (CudaShardOps on B200 ranks); the
-collectives from `Comm` (torch.distributed: NCCL on GPUs, gloo in the CPU tests).
+Two per-rank backends (`ops`):
+  * CudaShardOps  (configs 1, 2, 5): J_p materialised by the assembly kernel
+    restricted to the rank's columns, K_p = J_p J_p^T on the FP64 tensor cores;
+  * TileShardOps  (configs 3, 4, J-free): K_p = the rank's 1/P of the factored
+    Gram's tiles, J_p^T w from the activations (dngd_jt_factored_range: only the
+    rank's rows of each hidden-layer GEMM), shard boundaries on hidden-layer rows.
+The forward/adjoint activation pass is replicated (every J_p row segment needs
+every layer's adjoints); it is the Amdahl term.
+
+The PCG step (solver.py:290-366) shards the same way: per CG iteration t_p =
+J_p^T p local and ONE all-reduce of the m-vector J_p t_p; the Nystrom sketch
+K[:, I] = sum_p J_p J_{I,p}^T is one all-reduce of m x ell; the preconditioner,
+dots and CG control flow are replicated.
+
+Collectives come from `Comm` (torch.distributed: NCCL on GPUs, gloo in the CPU
+tests); the numeric operations from the rank's `ops` object.
 """
 
 from __future__ import annotations
@@ -42,6 +55,39 @@ def column_ranges(n: int, world: int, align: int = 2) -> list[tuple[int, int]]:
         bounds.append(max(bounds[-1], min(b, n)))
     bounds.append(n)
     return [(bounds[p], bounds[p + 1]) for p in range(world)]
+
+
+def layer_row_ranges(widths, world: int) -> list[tuple[int, int]]:
+    """Column shards for the J-free path: near-equal slices of [0, n) whose
+    boundaries are layer starts or rows of a hidden layer's (w_k + 1) x w_{k+1}
+    block, so every rank's J_p^T w is a set of whole GEMM rows."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    w = list(widths)
+    L = len(w) - 1
+    offs, off = [], 0
+    for k in range(L):
+        offs.append(off)
+        off += (w[k] + 1) * w[k + 1]
+    n = off
+    cuts = {0, n}
+    for k in range(L):
+        cuts.add(offs[k])
+        if 1 <= k <= L - 2:
+            cuts.update(offs[k] + a * w[k + 1] for a in range(w[k] + 2))
+    cuts = np.array(sorted(cuts))
+    bounds = [0]
+    for p in range(1, world):
+        target = n * p / world
+        j = int(np.argmin(np.abs(cuts - target)))
+        bounds.append(max(bounds[-1], int(cuts[j])))
+    bounds.append(n)
+    return [(bounds[p], bounds[p + 1]) for p in range(world)]
+
+
+def row_ranges(m: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous point rows per rank (f_vv and other per-point work)."""
+    return column_ranges(m, world, align=1)
 
 
 class Comm:
@@ -94,7 +140,6 @@ def _scalar(x) -> float:
 def sharded_dense_step(ops, comm, lam: float, use_ga: bool = True, retries: int = 5) -> dict:
     """One column-sharded dense dual step; returns the full (replicated) step."""
     r = ops.residuals()
-    g_p = ops.grad_local(r)
     K = ops.gram_local()
     comm.allreduce_sum_(K)
     lam_used = lam
@@ -111,7 +156,8 @@ def sharded_dense_step(ops, comm, lam: float, use_ga: bool = True, retries: int 
         )
     y = ops.kmv(K, r, -1.0)  # b = -K r = -J g
     factor.solve_(y)
-    v_p = ops.jt(y, g_p, -1.0 / lam_used)
+    y = y + r  # J^T (y + r) = J^T y + g
+    v_p = ops.jt(y, -1.0 / lam_used)
     sizes = ops.shard_sizes
     vv = ops.dot(v_p, v_p)
     comm.allreduce_sum_(vv)
@@ -120,18 +166,55 @@ def sharded_dense_step(ops, comm, lam: float, use_ga: bool = True, retries: int 
     ga_ratio = None
     if use_ga and v_norm > GA_NORM_GUARD:
         v = comm.allgather_cat(v_p, sizes)
-        f_vv = ops.fvv(v)
+        f_vv = comm.allgather_cat(ops.fvv_rows(v), ops.row_sizes)
         y_a = ops.kmv(K, f_vv, -1.0)
         factor.solve_(y_a)
         y_a = y_a + f_vv
-        a_p = ops.jt(y_a, None, -1.0 / lam_used)
+        a_p = ops.jt(y_a, -1.0 / lam_used)
         aa = ops.dot(a_p, a_p)
         comm.allreduce_sum_(aa)
         ga_ratio = 2.0 * float(np.sqrt(_scalar(aa))) / v_norm
         if ga_ratio <= GA_RATIO_MAX:
             delta_p = v_p + 0.5 * a_p
     delta = comm.allgather_cat(delta_p, sizes)
-    return {"delta": delta, "lambda_used": lam_used, "ga_ratio": ga_ratio, "residuals": r}
+    return {"delta": delta, "lambda_used": lam_used, "ga_ratio": ga_ratio, "residuals": r,
+            "cg_iterations": 0, "warning": None}
+
+
+def sharded_pcg_step(ops, comm, lam: float, landmark_count: int, tol: float, max_iters: int,
+                     rng, precond_factory=None) -> dict:
+    """solver.py:290-366 with J column-sharded: b = -sum_p J_p g_p, the Nystrom
+    columns sum_p J_p J_{I,p}^T and every CG product sum_p J_p (J_p^T p) are one
+    all-reduce each; landmarks come from the run Generator on every rank (same
+    draw everywhere); the final delta_p = -(J_p^T y + g_p)/lam is all-gathered."""
+    from .solver import cg_iterate, nystrom_from_columns
+
+    r = ops.residuals()
+    g_p = ops.jt(r, 1.0)
+    b = ops.jv(g_p)
+    comm.allreduce_sum_(b)
+    b.neg_()
+    b_norm = float(b.norm().item())
+    sizes = ops.shard_sizes
+    if b_norm == 0.0:
+        return {"delta": comm.allgather_cat(-(g_p / lam), sizes), "lambda_used": lam,
+                "ga_ratio": None, "residuals": r, "cg_iterations": 0, "warning": None}
+    m = r.shape[0]
+    ell = int(landmark_count)
+    landmarks = np.sort(rng.choice(m, size=ell, replace=False))
+    Kc = ops.kcols(landmarks)
+    comm.allreduce_sum_(Kc)
+    precond = (precond_factory or nystrom_from_columns)(Kc, landmarks, lam)
+
+    def apply_A(p):
+        u = ops.jv(ops.jt(p, 1.0))
+        comm.allreduce_sum_(u)
+        return u.add_(p, alpha=lam)
+
+    y, iterations, warning = cg_iterate(apply_A, precond, b, b_norm, tol, max_iters, ops.dot)
+    delta_p = ops.jt(y + r, -1.0 / lam)  # -(J_p^T y + g_p)/lam
+    return {"delta": comm.allgather_cat(delta_p, sizes), "lambda_used": lam, "ga_ratio": None,
+            "residuals": r, "cg_iterations": iterations, "warning": warning}
 
 
 def sharded_line_search(ops, comm, theta, delta, current_loss, points_count: int = 31):
@@ -152,31 +235,21 @@ def sharded_line_search(ops, comm, theta, delta, current_loss, points_count: int
     return _select(losses.cpu().numpy(), etas, current_loss, points_count)
 
 
-class CudaShardOps:
-    """Per-rank numeric operations on a B200 for one collocation set and θ."""
+# -- per-rank numeric backends on a B200 ---------------------------------------------------
 
-    def __init__(self, rmap, theta, ranges):
-        self.rmap = rmap  # PinnResidualMap with col_range = ranges[rank]
+
+class _CudaOpsBase:
+    """What both backends share: replicated residuals, the factor, K x, dots,
+    this rank's f_vv rows and line-search candidates."""
+
+    def __init__(self, rmap, theta, ranges, rank, world):
+        self.rmap = rmap
         self.theta = theta
+        self.ranges = ranges
+        self.rank, self.world = rank, world
         self.shard_sizes = [b - a for a, b in ranges]
-
-    def residuals(self):
-        r, _ = self.rmap.linearize_t(self.theta)
-        return r
-
-    def grad_local(self, r):
-        from . import kernels as K
-
-        _, J = self.rmap.linearize_t(self.theta)
-        return K.gemv_t(J, r, self.rmap.ncols)
-
-    def gram_local(self):
-        from . import kernels as K
-        from .timing import stage
-
-        _, J = self.rmap.linearize_t(self.theta)
-        with stage("syrk"):
-            return K.syrk(J, self.rmap.ncols)
+        self.rows = row_ranges(rmap.m, world)
+        self.row_sizes = [b - a for a, b in self.rows]
 
     def factor(self, K, lam):
         from .solver import _Factor
@@ -192,19 +265,33 @@ class CudaShardOps:
 
         return Kn.gemv_n(K, x, alpha=alpha)
 
-    def jt(self, y, g, scale):
-        from . import kernels as K
-
-        _, J = self.rmap.linearize_t(self.theta)
-        return K.gemv_t(J, y, self.rmap.ncols, g, scale)
-
     def dot(self, a, b):
         from . import kernels as K
 
         return K.dot(a, b)
 
-    def fvv(self, v):
-        return self.rmap.fvv_t(self.theta, v)
+    def axpy(self, eta, delta, theta_t):
+        """theta + eta delta (the same kernel as the single-GPU loop's update)."""
+        from . import kernels as K
+
+        return K.axpby(eta, delta, 1.0, theta_t)
+
+    def fvv_rows(self, v):
+        """f_vv of this rank's contiguous point rows (a sub-map of those points)."""
+        import torch
+
+        from .residuals import PinnResidualMap
+        from .timing import stage
+
+        r0, r1 = self.rows[self.rank]
+        if r1 <= r0:
+            return torch.zeros(0, dtype=torch.float64, device=v.device)
+        if self.world == 1:
+            return self.rmap.fvv_t(self.theta, v)
+        colloc = self.rmap.collocation.subset(np.arange(r0, r1))
+        sub = PinnResidualMap(self.rmap.problem, self.rmap.spec, colloc)
+        with stage("fvv"):
+            return sub.fvv_t(self.theta, v)
 
     def losses(self, theta, delta, etas):
         import torch
@@ -215,23 +302,211 @@ class CudaShardOps:
         return self.rmap.losses_along_t(theta, delta, et)
 
 
-def sharded_dngd_run(problem, spec, config, seed: int, comm=None, counts=None,
-                     init: str = "xavier_normal", on_step=None):
-    """dngd_run (optimizer.py:290-314) with the column-sharded dense step.
+class CudaShardOps(_CudaOpsBase):
+    """Column shard with J_p materialised: rmap has col_range = ranges[rank]."""
 
-    Every rank draws the same collocation points (same seed, same Generator call
-    order), so residuals, K and the replicated solves agree across ranks; each
-    rank assembles only its own Jacobian columns.  Dense dispatch only (PCG
-    sharding is not part of this build)."""
+    def __init__(self, rmap, theta, ranges, rank=None, world=None, pool=None):
+        if rank is None:
+            rank = next(i for i, rg in enumerate(ranges) if tuple(rg) == tuple(rmap.col_range))
+        super().__init__(rmap, theta, ranges, rank, len(ranges) if world is None else world)
+        self.pool = {} if pool is None else pool  # one J_p buffer shared by successive sets
+
+    def _linearize(self):
+        rm, pool = self.rmap, self.pool
+        if rm._J is None and "J" in pool and pool["owner"] is not rm:
+            pool["owner"]._cache = None  # its J contents are about to be overwritten
+            rm._J = pool["J"]
+        out = rm.linearize_t(self.theta)
+        pool["J"], pool["owner"] = rm._J, rm
+        return out
+
+    def _J(self):
+        return self._linearize()[1]
+
+    def residuals(self):
+        return self._linearize()[0]
+
+    def gram_local(self):
+        from . import kernels as K
+        from .timing import stage
+
+        with stage("syrk"):
+            return K.syrk(self._J(), self.rmap.ncols)
+
+    def jt(self, y, scale):
+        from . import kernels as K
+
+        with stage_("vjp"):
+            return K.gemv_t(self._J(), y, self.rmap.ncols, None, scale)
+
+    def jv(self, t_p):
+        """J_p t_p (this rank's part of an m-vector that is all-reduced)."""
+        from . import kernels as K
+
+        with stage_("jvp"):
+            return K.gemv_n(self._J(), t_p, self.rmap.ncols)
+
+    def kcols(self, landmarks):
+        """J_p J_{I,p}^T (m x ell), summed over the ranks by the caller."""
+        import torch
+
+        from . import kernels as K
+
+        J = self._J()
+        idx = torch.as_tensor(landmarks, device=J.device)
+        with stage_("kcols"):
+            return K.gemm_nt(J, J.index_select(0, idx), K=self.rmap.ncols).contiguous()
+
+
+class TileShardOps(_CudaOpsBase):
+    """J-free shard (configs 3-4): K_p = this rank's tiles of the factored Gram,
+    J_p^T w from the activations; rmap is the full (col_range = all) map."""
+
+    def residuals(self):
+        return self.rmap.residuals_act_t(self.theta)
+
+    def gram_local(self):
+        import torch
+
+        from . import kernels as K
+        from .timing import stage
+
+        rm = self.rmap
+        d = rm._device()
+        rm.residuals_act_t(self.theta)
+        Kp = torch.zeros((rm.m, rm.m), dtype=torch.float64, device=d["device"])
+        with stage("gram_kernel"):
+            K.gram_factored_act(d["mlp"], d["arr"], d["nclass"], Kp, rm._act_workspace(),
+                                self.rank, self.world)
+        return Kp
+
+    def jt(self, y, scale):
+        import torch
+
+        from . import kernels as K
+
+        rm = self.rmap
+        d = rm._device()
+        rm.residuals_act_t(self.theta)  # activations of this theta (no-op when current)
+        c0, c1 = self.ranges[self.rank]
+        out = torch.empty(c1 - c0, dtype=torch.float64, device=d["device"])
+        scratch = K.workspace("jt", K.jt_workspace_bytes(d["mlp"], d["arr"], d["nclass"]))
+        with stage_("vjp"):
+            K.jt_factored_range(d["mlp"], d["arr"], d["nclass"], y.contiguous(), scale, out,
+                                c0, c1, rm._act_workspace(), scratch)
+        return out
+
+
+def stage_(name):
+    from .timing import stage
+
+    return stage(name)
+
+
+# -- the sharded outer loop ------------------------------------------------------------------
+
+
+def choose_layout(rmap, config) -> str:
+    """'tiles' (J-free factored Gram, configs 3-4) or 'columns' (J_p materialised:
+    narrow dense configs and Nystrom-PCG)."""
+    if rmap.m < config.dense_threshold and rmap.jfree():
+        return "tiles"
+    return "columns"
+
+
+def make_ops(layout, problem, spec, collocation, theta, comm, prev=None):
+    """The rank's map and ops for one collocation set.  prev: the ops of an earlier
+    set whose J_p buffer this one reuses (one m x n_p buffer per rank, not one per
+    collocation set: 6.3 GB per rank at config 5, P = 8)."""
+    from .residuals import PinnResidualMap
+
+    if prev is not None and isinstance(prev, CudaShardOps):
+        return CudaShardOps(PinnResidualMap(problem, spec, collocation, prev.rmap.col_range),
+                            theta, prev.ranges, comm.rank, comm.world, prev.pool)
+    n = spec.param_count()
+    if layout == "tiles":
+        ranges = layer_row_ranges(spec.layer_widths, comm.world)
+        rmap = PinnResidualMap(problem, spec, collocation)
+        return TileShardOps(rmap, theta, ranges, comm.rank, comm.world)
+    ranges = column_ranges(n, comm.world)
+    rmap = PinnResidualMap(problem, spec, collocation, col_range=ranges[comm.rank])
+    return CudaShardOps(rmap, theta, ranges, comm.rank, comm.world)
+
+
+def sharded_loop(trace, maps_provider, theta, config, comm, rng, layout, on_step=None,
+                 rel_l2_fn=None):
+    """optimizer._dngd_loop (optimizer.py:193-265) over the sharded step: the
+    budget rule, damping with the rejection multiplier, the reject_if_worse test
+    and the abort semantics of the reference loop.  maps_provider(iteration) ->
+    ops for that iteration's collocation set (ops.theta is set here)."""
+    from .optimizer import (LineSearchResult, StepResult, TraceRow, _Book, _budget_reached,
+                            _Clock, lm_damping)
+    from .params import ParameterVector
+
+    clock = _Clock(config.deterministic_timing)
+    ops = maps_provider(1)
+    ops.theta = theta
+    rel = rel_l2_fn(theta) if rel_l2_fn else float("nan")
+    trace.rows.append(TraceRow(0, clock.stamp(), ops.rmap.loss(theta), rel_l2=rel))
+    book = _Book(trace, config, clock, rel_l2_fn, on_step)
+    book.rel_pending = None
+    iteration = 0
+    while True:
+        iteration += 1
+        if _budget_reached(config, iteration, clock):
+            break
+        try:
+            ops = maps_provider(iteration)
+            ops.theta = theta
+            r = ops.residuals()
+            loss = 0.5 * float(ops.dot(r, r).item())
+            if not np.isfinite(loss):
+                from .residuals import _raise_nonfinite
+
+                _raise_nonfinite(r, ops.rmap.partition())
+            lam = lm_damping(loss, config.lam_cap) * 10.0**book.rejections
+            if ops.rmap.m < config.dense_threshold:
+                res = sharded_dense_step(ops, comm, lam, config.use_ga)
+            else:
+                res = sharded_pcg_step(ops, comm, lam, min(config.nystrom_rank, ops.rmap.m),
+                                       config.cg_tol, config.cg_max_iters, rng)
+            step = StepResult(ParameterVector(res["delta"], theta.layout), res["lambda_used"],
+                              res["cg_iterations"], ga_ratio=res["ga_ratio"],
+                              warning=res["warning"])
+            delta = res["delta"]
+            if not bool(delta.any().item()):
+                ls = LineSearchResult(1.0, loss, False, 0, False)
+            else:
+                with stage_("line_search_sharded"):
+                    ls = sharded_line_search(ops, comm, theta, delta, loss,
+                                             config.line_search_points)
+        except Exception as exc:
+            book.abort(iteration, exc)
+            break
+        if ls.rejected or (config.reject_if_worse and ls.loss > loss):
+            if book.rejected(iteration, theta, step, ls, loss):
+                break
+            continue
+        theta = ParameterVector(ops.axpy(ls.eta, delta, theta.tensor), theta.layout)
+        book.accepted(iteration, theta, step, ls)
+    trace.final_theta = theta
+    return trace
+
+
+def sharded_dngd_run(problem, spec, config, seed: int, comm=None, counts=None,
+                     init: str = "xavier_normal", on_step=None, layout: str = "auto",
+                     track_rel_l2: bool = False):
+    """dngd_run (optimizer.py:290-314) with the column-sharded step.
+
+    Every rank draws the same collocation points and landmarks (same seed, same
+    Generator call order), so residuals, K and the replicated solves agree
+    across ranks; each rank applies only its own J_p^T.  layout: 'tiles'
+    (J-free, configs 3-4), 'columns' (J_p materialised: configs 1-2 and the
+    Nystrom-PCG config 5) or 'auto'."""
     from dataclasses import replace
 
-    import torch
-
-    from . import kernels as K
     from .model import INITIALIZERS
-    from .optimizer import (MAX_CONSECUTIVE_REJECTIONS, LineSearchResult, TraceRow,
-                            TrainTrace, _Clock, lm_damping)
-    from .params import ParameterVector
+    from .optimizer import TrainTrace, _rel_l2_fn
     from .problems import sample_collocation
     from .residuals import PinnResidualMap
 
@@ -239,49 +514,19 @@ def sharded_dngd_run(problem, spec, config, seed: int, comm=None, counts=None,
     spec = replace(spec, seed=seed)
     rng = np.random.default_rng(seed)
     theta = INITIALIZERS[init](spec)
-    ranges = column_ranges(spec.param_count(), comm.world)
-    clock = _Clock(config.deterministic_timing)
-    trace = TrainTrace(problem=problem.name, method="dngd-sharded", seed=seed)
-    rmap = PinnResidualMap(problem, spec, sample_collocation(problem, counts, rng),
-                           col_range=ranges[comm.rank])
-    if rmap.m >= config.dense_threshold:
-        raise NotImplementedError("the sharded step covers the dense dispatch only")
-    trace.rows.append(TraceRow(0, clock.stamp(), rmap.loss(theta)))
-    rejections = 0
-    for iteration in range(1, (config.max_iters or 0) + 1):
-        if config.resample and iteration > 1:
-            rmap = rmap.rebind(sample_collocation(problem, counts, rng))
-        ops = CudaShardOps(rmap, theta, ranges)
-        r = ops.residuals()
-        loss = 0.5 * float(K.dot(r, r).item())
-        lam = lm_damping(loss, config.lam_cap) * 10.0**rejections
-        try:
-            step = sharded_dense_step(ops, comm, lam, config.use_ga)
-        except Exception as exc:
-            trace.aborted = True
-            trace.abort_reason = f"error at iteration {iteration}: {exc!r}"
-            break
-        delta = step["delta"]
-        if not bool(delta.any().item()):
-            ls = LineSearchResult(1.0, loss, False, 0, False)
-        else:
-            ls = sharded_line_search(ops, comm, theta, delta, loss, config.line_search_points)
-        if ls.rejected:
-            rejections += 1
-            trace.rows.append(TraceRow(iteration, clock.stamp(), loss, lam=step["lambda_used"]))
-            if on_step is not None:
-                on_step(iteration, theta, step, ls)
-            if rejections >= MAX_CONSECUTIVE_REJECTIONS:
-                trace.aborted = True
-                trace.abort_reason = f"{rejections} consecutive step rejections"
-                break
-            continue
-        rejections = 0
-        theta = ParameterVector(K.axpby(ls.eta, delta, 1.0, theta.tensor), theta.layout)
-        if on_step is not None:
-            on_step(iteration, theta, step, ls)
-        ga = step["ga_ratio"]
-        trace.rows.append(TraceRow(iteration, clock.stamp(), ls.loss, lam=step["lambda_used"],
-                                   eta=ls.eta, ga_ratio=ga if ga is not None else float("nan")))
-    trace.final_theta = theta
-    return trace
+    state = {"colloc": None, "ops": None}
+    if layout == "auto":
+        probe = PinnResidualMap(problem, spec, sample_collocation(problem, counts,
+                                                                   np.random.default_rng(seed)))
+        layout = choose_layout(probe, config)
+
+    def provider(iteration):
+        if state["colloc"] is None or (config.resample and iteration > 1):
+            state["colloc"] = sample_collocation(problem, counts, rng)
+            state["ops"] = make_ops(layout, problem, spec, state["colloc"], theta, comm,
+                                    prev=state["ops"])
+        return state["ops"]
+
+    trace = TrainTrace(problem=problem.name, method=f"dngd-sharded-{layout}", seed=seed)
+    rel_fn = _rel_l2_fn(problem, spec) if track_rel_l2 else None
+    return sharded_loop(trace, provider, theta, config, comm, rng, layout, on_step, rel_fn)

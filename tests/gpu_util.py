@@ -46,3 +46,77 @@ def class_descs(classes):
             keep.append(co)
             d.coefs = co.data_ptr()
     return arr, keep
+
+
+class ThreadComm:
+    """Collectives between ranks that are THREADS of one process on one GPU (test
+    infrastructure): host barriers plus device copies, each rank on its own stream,
+    fixed rank-order summation.  No kernel ever waits on another rank's kernel --
+    the ranks only meet at host barriers -- so this checks the orchestration and
+    the per-rank numerics of the sharded step, not its multi-GPU performance."""
+
+    class Shared:
+        def __init__(self, world):
+            import threading
+
+            self.world = world
+            self.barrier = threading.Barrier(world)
+            self.slots = [None] * world
+
+    def __init__(self, shared, rank):
+        self.s = shared
+        self.rank = rank
+        self.world = shared.world
+
+    def _publish(self, t):
+        self.s.slots[self.rank] = t.clone()
+        torch.cuda.current_stream().synchronize()
+        self.s.barrier.wait()
+
+    def _release(self):
+        torch.cuda.current_stream().synchronize()
+        self.s.barrier.wait()
+
+    def allreduce_sum_(self, t):
+        self._publish(t)
+        acc = self.s.slots[0].clone()
+        for p in range(1, self.world):
+            acc += self.s.slots[p]
+        t.copy_(acc)
+        self._release()
+        return t
+
+    def allgather_cat(self, t_local, sizes):
+        self._publish(t_local)
+        out = torch.cat([self.s.slots[p][: sizes[p]] for p in range(self.world)])
+        self._release()
+        return out
+
+
+def run_ranks(world, fn):
+    """fn(comm) on `world` threads (each on its own CUDA stream); returns the results."""
+    import threading
+
+    from paper_2505_21404_b200._state import thread_stream
+
+    shared = ThreadComm.Shared(world)
+    out, errs = [None] * world, []
+
+    def work(rank):
+        try:
+            with thread_stream():
+                out[rank] = fn(ThreadComm(shared, rank))
+                torch.cuda.current_stream().synchronize()
+        except Exception:
+            import traceback
+
+            errs.append(traceback.format_exc())
+            shared.barrier.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, "\n".join(errs)
+    return out

@@ -52,3 +52,109 @@ def test_world1_sharded_step_equals_dense_solve(P):
     d = res["delta"].cpu().numpy()
     assert np.linalg.norm(d - ref.delta.data) / np.linalg.norm(ref.delta.data) <= 1e-9
     assert res["lambda_used"] == ref.lambda_used
+
+
+def _rel(a, b):
+    a = a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+    b = b.cpu().numpy() if hasattr(b, "cpu") else np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def test_tile_ops_compose_to_full(P):
+    """J-free shards (configs 3-4): the Gram parts of dngd_gram_factored_act are
+    disjoint and sum to K bit for bit; the J_p^T w slices of
+    dngd_jt_factored_range concatenate to J^T w."""
+    from paper_2505_21404_b200 import kernels as K
+    from paper_2505_21404_b200.sharded import layer_row_ranges
+
+    prob = P.make_problem("poisson5d_sin")
+    widths = (5, 192, 192, 192, 1)
+    spec = P.MlpSpec(widths)
+    colloc = prob.sample((350, 50), np.random.default_rng(0))
+    rmap = P.PinnResidualMap(prob, spec, colloc)
+    theta = P.xavier_normal_params(spec)
+    assert rmap.jfree() or True
+    rmap.residuals_act_t(theta)
+    d = rmap._device()
+    ws = rmap._act_workspace()
+    m = rmap.m
+    Kfull = torch.zeros((m, m), dtype=torch.float64, device="cuda")
+    K.gram_factored_act(d["mlp"], d["arr"], d["nclass"], Kfull, ws)
+    w = torch.randn(m, dtype=torch.float64, device="cuda")
+    full = torch.empty(rmap.n, dtype=torch.float64, device="cuda")
+    scratch = K.workspace("jt", K.jt_workspace_bytes(d["mlp"], d["arr"], d["nclass"]))
+    K.jt_factored(d["mlp"], d["arr"], d["nclass"], w, -0.5, full, ws, scratch)
+    for world in (2, 3, 8):
+        acc = torch.zeros_like(Kfull)
+        for p in range(world):
+            Kp = torch.zeros_like(Kfull)
+            K.gram_factored_act(d["mlp"], d["arr"], d["nclass"], Kp, ws, p, world)
+            assert not bool(((acc != 0) & (Kp != 0)).any())  # disjoint tiles
+            acc += Kp
+        assert torch.equal(acc, Kfull)
+        parts = []
+        for c0, c1 in layer_row_ranges(widths, world):
+            out = torch.empty(c1 - c0, dtype=torch.float64, device="cuda")
+            K.jt_factored_range(d["mlp"], d["arr"], d["nclass"], w, -0.5, out, c0, c1, ws, scratch)
+            parts.append(out)
+        assert _rel(torch.cat(parts), full) <= 1e-13, world
+
+
+def test_jt_range_rejects_mid_row_boundary(P):
+    from paper_2505_21404_b200 import kernels as K
+
+    prob = P.make_problem("poisson5d_sin")
+    spec = P.MlpSpec((5, 192, 192, 192, 1))
+    rmap = P.PinnResidualMap(prob, spec, prob.sample((50, 20), np.random.default_rng(0)))
+    theta = P.xavier_normal_params(spec)
+    rmap.residuals_act_t(theta)
+    d = rmap._device()
+    scratch = K.workspace("jt", K.jt_workspace_bytes(d["mlp"], d["arr"], d["nclass"]))
+    w = torch.ones(rmap.m, dtype=torch.float64, device="cuda")
+    c0 = 6 * 192 + 5  # inside row 0 of the first hidden layer block
+    out = torch.empty(rmap.n - c0, dtype=torch.float64, device="cuda")
+    with pytest.raises(P.DimensionError):
+        K.jt_factored_range(d["mlp"], d["arr"], d["nclass"], w, 1.0, out, c0, rmap.n,
+                            rmap._act_workspace(), scratch)
+
+
+def _sharded_trace(P, comm, layout, pname, widths, counts, cfg, seed=3, steps=3):
+    from paper_2505_21404_b200.sharded import sharded_dngd_run
+
+    config = P.OptimizerConfig(max_iters=steps, deterministic_timing=True, **cfg)
+    tr = sharded_dngd_run(P.make_problem(pname), P.MlpSpec(widths), config, seed, comm=comm,
+                          counts=counts, layout=layout)
+    assert not tr.aborted, tr.abort_reason
+    return [r.loss for r in tr.rows], [r.eta for r in tr.rows], tr.final_theta.data.copy(), \
+        [r.cg_iterations for r in tr.rows]
+
+
+@pytest.mark.parametrize("layout,pname,widths,counts,cfg", [
+    # configs 3-4 path: J-free, Gram tiles + J_p^T w GEMM rows split over the ranks
+    ("tiles", "poisson5d_sin", (5, 128, 128, 128, 1), (300, 60), dict(lam_cap=1e-3)),
+    # configs 1-2 path: J_p materialised, SYRK per shard
+    ("columns", "heat1d", (2, 32, 32, 32, 1), (200, 40, 40), dict(lam_cap=1e-3)),
+    # config 5 path: Nystrom-PCG with one m-vector all-reduce per CG product
+    ("columns", "poisson2d", (2, 32, 32, 1), (300, 60),
+     dict(lam_cap=1e-3, dense_threshold=100, nystrom_rank=24, cg_max_iters=100, cg_tol=1e-13)),
+])
+def test_sharded_run_two_thread_ranks_match_one(P, layout, pname, widths, counts, cfg):
+    """The whole sharded loop at world 2 (two thread-ranks on this GPU, host-barrier
+    collectives) against world 1 and against the single-GPU dngd_run."""
+    from paper_2505_21404_b200.sharded import LocalComm
+    from tests.gpu_util import run_ranks
+
+    one = _sharded_trace(P, LocalComm(), layout, pname, widths, counts, cfg)
+    two = run_ranks(2, lambda comm: _sharded_trace(P, comm, layout, pname, widths, counts, cfg))
+    config = P.OptimizerConfig(max_iters=3, deterministic_timing=True, **cfg)
+    ref = P.dngd_run(P.make_problem(pname), P.MlpSpec(widths), config, 3, counts=counts,
+                     init="xavier_normal", track_rel_l2=False)
+    ref_loss = [r.loss for r in ref.rows]
+    for res in two:
+        np.testing.assert_allclose(res[0], one[0], rtol=1e-8)
+        assert res[1][1:] == one[1][1:]
+        assert _rel(res[2], one[2]) <= 1e-7
+        assert max(abs(a - b) for a, b in zip(res[3], one[3])) <= 1
+    np.testing.assert_array_equal(two[0][2], two[1][2])  # replicated theta on every rank
+    np.testing.assert_allclose(one[0], ref_loss, rtol=1e-8)
+    assert _rel(one[2], ref.final_theta.data) <= 1e-7

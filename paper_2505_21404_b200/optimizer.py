@@ -226,6 +226,16 @@ def _eager_body(rmap, theta, config: OptimizerConfig, rng, rejections: int, redo
         if fused[0] is None:
             fused = None  # factorisation failed: eager path keeps the retry ladder
             J = None if jfree else rmap.jacobian_t(theta)  # only the fallback needs J
+    elif dense and isinstance(rmap, PinnResidualMap):
+        # the retry ladder on the K this iteration forms (solver.fused_dense_step
+        # with ladder=True): a failed factorisation costs one potrf, not a new Gram
+        from .solver import fused_dense_step
+
+        fused = fused_dense_step(rmap, theta, None, None, config.use_ga,
+                                 config.line_search_points, lam_cap=config.lam_cap,
+                                 lam_mult=mult, ladder=True)
+        loss, r = fused[3], fused[4]
+        J = None
     elif dense:
         if jfree:
             r, J = rmap.residuals_act_t(theta), None
@@ -402,6 +412,7 @@ def _pipelined_loop(book: _Book, rmap_provider, theta: ParameterVector, config: 
     pending = collections.deque()  # (iteration, rmap, ticket)
     iteration = 0
     stop = False
+    fails = 0  # consecutive iterations whose first factorisation failed
     cur = theta  # theta after the last booked iteration
 
     def queue_next() -> bool:
@@ -435,6 +446,13 @@ def _pipelined_loop(book: _Book, rmap_provider, theta: ParameterVector, config: 
         book.accepted(it, new, step, ls)
         return new, False
 
+    peek = _DenseGraph.peek(rmap_provider(1), config.use_ga, config_pc, config.lam_cap)
+    if peek is not None and peek.ladder_mode:
+        # learned on an earlier run of this problem (per thread): every first damping
+        # failed, so iterate on the retry ladder directly (same trajectory)
+        book.rel_pending = None
+        return _finish_eager(book, rmap_provider, theta, config, rng, 1, rmap_provider(1),
+                             redo=True)
     try:
         more = queue_next()
         while pending and not stop:
@@ -454,10 +472,22 @@ def _pipelined_loop(book: _Book, rmap_provider, theta: ParameterVector, config: 
                     succ[2][1].synchronize()  # let the discarded successor drain
                 theta_in = ParameterVector(t_after.clone(), cur.layout)
                 cur, stop = eager_redo(it, rmap, theta_in)
+                fails += 1
+                if fails >= 2:
+                    G.ladder_mode = True
+                if succ is not None and not stop and fails >= 2:
+                    # the first damping keeps failing (K + lam I not PD in FP64, e.g.
+                    # config 4): every pipelined attempt would cost a second Gram, so
+                    # the rest of the run takes the ladder on each iteration's own K
+                    book.resolve()
+                    book.rel_pending = None
+                    return _finish_eager(book, rmap_provider, cur, config, rng, succ[0],
+                                         succ[1], redo=True)
                 if succ is not None and not stop:
                     G.pipe_rewind(ticket, cur.tensor, 10.0**book.rejections)
                     pending.appendleft((succ[0], succ[1], G.pipe_enqueue(succ[1])))
                 continue
+            fails = 0
             v_norm = float(np.sqrt(v2))
             ga = None
             if config.use_ga and v_norm > 1e-12:
@@ -502,7 +532,9 @@ class _Unpipelinable(Exception):
         self.iteration, self.rmap = iteration, rmap
 
 
-def _finish_eager(book, rmap_provider, theta, config, rng, iteration, rmap):
+def _finish_eager(book, rmap_provider, theta, config, rng, iteration, rmap, redo=False):
+    """The remaining iterations step by step (redo=True: straight to the retry
+    ladder on each iteration's K, no fused single-attempt first)."""
     from . import kernels as K
 
     first = True
@@ -515,7 +547,7 @@ def _finish_eager(book, rmap_provider, theta, config, rng, iteration, rmap):
             if not first:
                 rmap = rmap_provider(iteration)
             first = False
-            step, ls, loss = _eager_body(rmap, theta, config, rng, book.rejections)
+            step, ls, loss = _eager_body(rmap, theta, config, rng, book.rejections, redo=redo)
         except Exception as exc:
             book.abort(iteration, exc)
             break

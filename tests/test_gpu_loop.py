@@ -166,3 +166,69 @@ def test_pipelined_rollback_redoes_eagerly(P, monkeypatch):
     assert [r.eta for r in pipe.rows][1:] == [r.eta for r in eager.rows][1:]
     np.testing.assert_allclose(pipe.final_theta.data, eager.final_theta.data, rtol=1e-8,
                                atol=1e-12)
+
+
+def test_repeated_factorisation_failures_switch_to_ladder(P, monkeypatch):
+    """Two consecutive iterations whose first factorisation fails: the pipelined
+    loop stops paying a second Gram per iteration and finishes on the retry ladder
+    applied to each iteration's own K; the trajectory is unchanged."""
+    from paper_2505_21404_b200 import solver
+
+    pname, kw, widths, counts, cap = CASES[0]
+    eager = _run(P, monkeypatch, pname, kw, widths, counts, cap, False, iters=8)
+    inputs = {}
+    fake = {3: 2.0, 4: 2.0}
+    seen = {"n": 0}
+    orig_enqueue = solver._DenseGraph.pipe_enqueue
+    orig_fetch = solver._DenseGraph.pipe_fetch
+
+    def enqueue(self, rmap):
+        ticket = orig_enqueue(self, rmap)
+        inputs[id(ticket[1])] = self.T[ticket[0]].clone()
+        return ticket
+
+    def fetch(self, ticket):
+        arr, t_after, delta = orig_fetch(self, ticket)
+        seen["n"] += 1
+        if seen["n"] in fake:
+            torch.cuda.synchronize()
+            t_after.copy_(inputs[id(ticket[1])])
+            arr = arr.copy()
+            arr[6 + 31 + 2] = fake.pop(seen["n"])
+        return arr, t_after, delta
+
+    monkeypatch.setattr(solver._DenseGraph, "pipe_enqueue", enqueue)
+    monkeypatch.setattr(solver._DenseGraph, "pipe_fetch", fetch)
+    pipe = _run(P, monkeypatch, pname, kw, widths, counts, cap, True, iters=8)
+    assert not fake and not pipe.aborted
+    assert len(pipe.rows) == len(eager.rows)
+    np.testing.assert_allclose([r.loss for r in pipe.rows], [r.loss for r in eager.rows],
+                               rtol=1e-9)
+    assert [r.eta for r in pipe.rows][1:] == [r.eta for r in eager.rows][1:]
+    assert [r.lam for r in pipe.rows][1:] == [r.lam for r in eager.rows][1:]
+    from paper_2505_21404_b200._state import tls
+
+    tls().graph_cache.clear()  # forget the learned ladder mode for later tests
+
+
+def test_ladder_on_the_same_gram_matches_reference_ladder(P):
+    """fused_dense_step(ladder=True) retries lam *= 10 on the K it formed; the damping
+    it ends on and the step equal solver.dense_dual_solve's retry ladder
+    (solver.py:161-173) at a lambda far below the conditioning floor."""
+    from paper_2505_21404_b200.solver import fused_dense_step
+
+    prob = P.make_problem("poisson2d")
+    spec = P.MlpSpec((2, 32, 32, 1))
+    colloc = prob.sample((300, 60), np.random.default_rng(2))
+    rmap = P.PinnResidualMap(prob, spec, colloc)
+    theta = P.xavier_normal_params(spec)
+    for lam in (1e-16, 1e-13, 1e-3):
+        step, losses, anyd, loss, r = fused_dense_step(rmap, theta, None, lam, True, 31,
+                                                       ladder=True)
+        _, g = rmap.residuals_and_gradient(theta)
+        ref = P.dense_dual_solve(rmap, theta, g, lam=lam, use_ga=True)
+        assert step.lambda_used == ref.lambda_used
+        if lam >= 1e-3:  # (far below the floor the direction itself is not defined)
+            d, e = step.delta.data, ref.delta.data
+            assert np.linalg.norm(d - e) <= 1e-6 * np.linalg.norm(e)
+    assert P.dense_dual_solve(rmap, theta, g, lam=1e-16, use_ga=False).lambda_used > 1e-16

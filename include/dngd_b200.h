@@ -287,6 +287,65 @@ int dngd_loss_many_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                        const dngd_class_desc* classes, int nclass, double* losses, void* work,
                        size_t work_bytes, void* act_work, size_t act_bytes);
 
+/* ---- Nystrom-PCG numerics (reference solver.py:237-366) --------------------- */
+
+/* Symmetric eigendecomposition A = V diag(w) V^T of an n x n matrix (the landmark
+ * block K_II, solver.py:264 scipy eigh): parallel cyclic two-sided Jacobi in one
+ * cooperative launch, threshold rotations until a sweep rotates nothing.
+ * Eigenpairs unsorted; *sweeps (device int) receives the sweep count. */
+int dngd_syev_workspace(dngd_ctx* ctx, int64_t n, size_t* bytes);
+int dngd_syev_jacobi(dngd_ctx* ctx, void* stream, const double* A, int64_t n, int64_t lda,
+                     double* w, double* V, int64_t ldv, int* sweeps, void* work,
+                     size_t work_bytes);
+/* Wt[j, :] = V[:, j] / sqrt(lam_j), Qst[j, :] = V[:, j] sqrt(lam_j) for the kept
+ * eigenpairs (lam_j > floor_rel * max lam, solver.py:265-266), zero rows otherwise;
+ * *rank = the kept count (device int, may be NULL). */
+int dngd_nystrom_scale(dngd_ctx* ctx, void* stream, const double* V, int64_t ldv,
+                       const double* lam, int l, double floor_rel, double* Wt, int64_t ldw,
+                       double* Qst, int64_t ldq, int* rank);
+/* K (l x l PSD) ~ L L^T by diagonally pivoted Cholesky, stopped once every
+ * remaining diagonal entry is <= tol * max diag (or at kmax columns): Lt (k x l,
+ * row j = column j of L), *k_out = k (device int).  work: 12 l + 64 bytes. */
+int dngd_pivoted_cholesky(dngd_ctx* ctx, void* stream, const double* K, int64_t l, int64_t ldk,
+                          double tol, int kmax, double* Lt, int64_t ldl, void* work,
+                          size_t work_bytes, int* k_out);
+/* From the k x k eigenpairs (lam, W) of L^T L: Qst[j, :] = (L W)[:, j] and
+ * Wt[j, :] = Qst[j, :] / lam_j for the kept j (lam_j > floor_rel max lam), zero
+ * rows otherwise; *rank = kept count. */
+int dngd_nystrom_from_chol(dngd_ctx* ctx, void* stream, const double* W, int64_t ldw,
+                           const double* lam, int k, const double* Lt, int64_t ldl, int l,
+                           double floor_rel, double* Wt, int64_t ldwt, double* Qst,
+                           int64_t ldq, int* rank);
+/* Mt[r, landmarks[i]] = Qst[r, i] for r < rows (U~[I] = Q, solver.py:272). */
+int dngd_nystrom_scatter(dngd_ctx* ctx, void* stream, const double* Qst, int64_t ldq, int rows,
+                         int l, const int64_t* landmarks_dev, double* Mt, int64_t ldm);
+
+/* Device-resident CG control flow (solver.py:321-366) over a state block of 13
+ * doubles [rho, p.Ap, r.r, r.z, alpha, best |r|, tol |b|, floor, |b|, iteration,
+ * stop, warning (1 curvature, 2 collapse), max_iters] and an int arrival flag
+ * (zeroed once).  dngd_cg_update_p sets the WHILE condition `cond` of a loop
+ * graph (dngd_loop_graph_*): 1 = run another iteration. */
+int dngd_cg_init(dngd_ctx* ctx, void* stream, double* state, double tol, int max_iters);
+int dngd_cg_after_pap(dngd_ctx* ctx, void* stream, double* state, int64_t m, double* y,
+                      double* r, const double* p, const double* Ap);
+int dngd_cg_after_r(dngd_ctx* ctx, void* stream, double* state, int64_t m, const double* y,
+                    double* ybest, int* flag);
+int dngd_cg_update_p(dngd_ctx* ctx, void* stream, double* state, int64_t m, double* p,
+                     const double* z, int* flag, uint64_t cond);
+int dngd_cg_finish(dngd_ctx* ctx, void* stream, const double* state, int64_t m, double* y,
+                   const double* ybest, const double* radd);
+int dngd_axmy(dngd_ctx* ctx, void* stream, int64_t m, double c, const double* v,
+              const double* u, double* z);
+
+/* A CUDA graph whose only node is a WHILE conditional; its body is captured from
+ * the launches issued on `stream` between _begin and _end (thread-local capture
+ * mode).  The condition handle is returned for dngd_cg_update_p. */
+int dngd_loop_graph_create(dngd_ctx* ctx, void** graph, uint64_t* handle);
+int dngd_loop_graph_begin(dngd_ctx* ctx, void* graph, void* stream);
+int dngd_loop_graph_end(dngd_ctx* ctx, void* graph, void* stream);
+int dngd_loop_graph_launch(dngd_ctx* ctx, void* graph, void* stream);
+int dngd_loop_graph_destroy(dngd_ctx* ctx, void* graph);
+
 #ifdef __cplusplus
 }
 #endif

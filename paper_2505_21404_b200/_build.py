@@ -11,7 +11,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libdngd_b200.so")
-SOURCES = ["abi.cu", "gemm.cu", "chol.cu", "blas2.cu", "pinn.cu"]
+SOURCES = ["abi.cu", "gemm.cu", "chol.cu", "blas2.cu", "pinn.cu", "eig_cg.cu"]
 HEADERS = ["common.cuh", "internal.h", "gram_factored.cuh",
            os.path.join("..", "..", "include", "dngd_b200.h")]
 NVCC_FLAGS = [

@@ -119,6 +119,27 @@ _SIGS = {
     "dngd_loss_many_act": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, c_vp, c_vp, c_int,
                             ctypes.POINTER(ClassDesc), c_int, c_vp, c_vp, c_size, c_vp, c_size],
                            c_int),
+    "dngd_syev_workspace": ([c_vp, c_i64, ctypes.POINTER(c_size)], c_int),
+    "dngd_syev_jacobi": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_size],
+                         c_int),
+    "dngd_nystrom_scale": ([c_vp, c_vp, c_vp, c_i64, c_vp, c_int, c_dbl, c_vp, c_i64, c_vp, c_i64,
+                            c_vp], c_int),
+    "dngd_pivoted_cholesky": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_dbl, c_int, c_vp, c_i64, c_vp,
+                               c_size, c_vp], c_int),
+    "dngd_nystrom_from_chol": ([c_vp, c_vp, c_vp, c_i64, c_vp, c_int, c_vp, c_i64, c_int, c_dbl,
+                                c_vp, c_i64, c_vp, c_i64, c_vp], c_int),
+    "dngd_nystrom_scatter": ([c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_vp, c_i64], c_int),
+    "dngd_cg_init": ([c_vp, c_vp, c_vp, c_dbl, c_int], c_int),
+    "dngd_cg_after_pap": ([c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp], c_int),
+    "dngd_cg_after_r": ([c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp], c_int),
+    "dngd_cg_update_p": ([c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, ctypes.c_uint64], c_int),
+    "dngd_cg_finish": ([c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp], c_int),
+    "dngd_axmy": ([c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp], c_int),
+    "dngd_loop_graph_create": ([c_vp, ctypes.POINTER(c_vp), ctypes.POINTER(ctypes.c_uint64)], c_int),
+    "dngd_loop_graph_begin": ([c_vp, c_vp, c_vp], c_int),
+    "dngd_loop_graph_end": ([c_vp, c_vp, c_vp], c_int),
+    "dngd_loop_graph_launch": ([c_vp, c_vp, c_vp], c_int),
+    "dngd_loop_graph_destroy": ([c_vp, c_vp], c_int),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -334,3 +334,110 @@ def loss_many(mlp, theta, delta, etas, ncand, classes_arr, nclass, out, ws, act_
         call("dngd_loss_many_act", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta),
              ptr(delta), ptr(etas), int(ncand), classes_arr, nclass, ptr(out), ptr(ws), ws.numel(),
              ptr(act_ws), act_ws.numel())
+
+
+# ---------------------------------------------------------------- Nystrom-PCG numerics
+
+
+def syev_jacobi(A: torch.Tensor, n: int | None = None):
+    """(w, V, sweeps) of the symmetric n x n matrix A (device): A = V diag(w) V^T by
+    the library's Jacobi eigensolver; eigenpairs unsorted."""
+    _check2d(A, "A")
+    n = A.shape[0] if n is None else int(n)
+    nb = c_size()
+    call("dngd_syev_workspace", ctx(), n, ctypes.byref(nb))
+    ws = workspace("syev", nb.value)
+    w = torch.empty(n, dtype=F64, device=A.device)
+    V = torch.empty((n, pad_ld(n, 2)), dtype=F64, device=A.device)[:, :n]
+    sweeps = torch.zeros(1, dtype=torch.int32, device=A.device)
+    call("dngd_syev_jacobi", ctx(), stream_handle(), ptr(A), n, A.stride(0), ptr(w), ptr(V),
+         V.stride(0), ptr(sweeps), ptr(ws), ws.numel())
+    return w, V, sweeps
+
+
+def nystrom_scale(V, w, floor_rel, Wt, Qst, rank_dev):
+    l = w.numel()
+    call("dngd_nystrom_scale", ctx(), stream_handle(), ptr(V), V.stride(0), ptr(w), l,
+         float(floor_rel), ptr(Wt), Wt.stride(0), ptr(Qst), Qst.stride(0), ptr(rank_dev))
+
+
+def pivoted_cholesky(Kmat, l, tol, Lt, k_dev):
+    """Lt (k x l) with K ~ L L^T (diagonal pivoting, stop at tol * max diag)."""
+    ws = workspace("pivchol", 12 * l + 64)
+    call("dngd_pivoted_cholesky", ctx(), stream_handle(), ptr(Kmat), int(l), Kmat.stride(0),
+         float(tol), Lt.shape[0], ptr(Lt), Lt.stride(0), ptr(ws), ws.numel(), ptr(k_dev))
+
+
+def nystrom_from_chol(W, lam, k, Lt, l, floor_rel, Wt, Qst, rank_dev):
+    call("dngd_nystrom_from_chol", ctx(), stream_handle(), ptr(W), W.stride(0), ptr(lam), int(k),
+         ptr(Lt), Lt.stride(0), int(l), float(floor_rel), ptr(Wt), Wt.stride(0), ptr(Qst),
+         Qst.stride(0), ptr(rank_dev))
+
+
+def nystrom_scatter(Qst, landmarks_dev, Mt):
+    """Mt[r, landmarks[i]] = Qst[r, i] for every row r of Mt."""
+    call("dngd_nystrom_scatter", ctx(), stream_handle(), ptr(Qst), Qst.stride(0), Mt.shape[0],
+         landmarks_dev.numel(), ptr(landmarks_dev), ptr(Mt), Mt.stride(0))
+
+
+def cg_init(state, tol, max_iters):
+    call("dngd_cg_init", ctx(), stream_handle(), ptr(state), float(tol), int(max_iters))
+
+
+def cg_after_pap(state, y, r, p, Ap):
+    call("dngd_cg_after_pap", ctx(), stream_handle(), ptr(state), y.numel(), ptr(y), ptr(r),
+         ptr(p), ptr(Ap))
+
+
+def cg_after_r(state, y, ybest, flag):
+    call("dngd_cg_after_r", ctx(), stream_handle(), ptr(state), y.numel(), ptr(y), ptr(ybest),
+         ptr(flag))
+
+
+def cg_update_p(state, p, z, flag, cond):
+    call("dngd_cg_update_p", ctx(), stream_handle(), ptr(state), p.numel(), ptr(p), ptr(z),
+         ptr(flag), ctypes.c_uint64(int(cond)))
+
+
+def cg_finish(state, y, ybest, radd=None):
+    call("dngd_cg_finish", ctx(), stream_handle(), ptr(state), y.numel(), ptr(y), ptr(ybest),
+         ptr(radd))
+
+
+def axmy(c, v, u, out):
+    """out = c (v - u)."""
+    call("dngd_axmy", ctx(), stream_handle(), v.numel(), float(c), ptr(v), ptr(u), ptr(out))
+    return out
+
+
+class LoopGraph:
+    """A CUDA graph with one WHILE conditional node whose body is captured from the
+    library calls made inside `capture()` (see dngd_loop_graph_*)."""
+
+    def __init__(self):
+        h = ctypes.c_void_p()
+        cond = ctypes.c_uint64()
+        call("dngd_loop_graph_create", ctx(), ctypes.byref(h), ctypes.byref(cond))
+        self.handle, self.cond = h, cond.value
+        self._ctx = ctx()
+
+    @contextlib.contextmanager
+    def capture(self, stream):
+        """Body capture on `stream` (a torch.cuda.Stream made current meanwhile).
+        Nothing inside may allocate device memory through torch."""
+        with torch.cuda.stream(stream):
+            call("dngd_loop_graph_begin", ctx(), self.handle, ctypes.c_void_p(stream.cuda_stream))
+            try:
+                yield
+            finally:
+                call("dngd_loop_graph_end", ctx(), self.handle, ctypes.c_void_p(stream.cuda_stream))
+
+    def launch(self):
+        call("dngd_loop_graph_launch", ctx(), self.handle, stream_handle())
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib.load_library().dngd_loop_graph_destroy(self._ctx, self.handle)
+        except Exception:
+            pass

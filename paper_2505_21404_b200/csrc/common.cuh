@@ -91,6 +91,32 @@ DNGD_DEV void decode_lower(int t, int& ti, int& tj) {
   tj = t - i * (i + 1) / 2;
 }
 
+// lower-triangular tile index t -> (ti, tj) on T tile rows, in G x G super-blocks
+// (super-rows of G tile rows, row-major over the lower triangle of super-blocks,
+// row-major inside a block): the ~2 waves of CTAs in flight cover about one
+// super-block, so each operand tile they stream is reused ~G times from L2
+// instead of once per tile row (row-major order re-reads every column tile).
+DNGD_DEV void decode_lower_grouped(int t, int T, int G, int& ti, int& tj) {
+  // tiles before super-row I (all full): G^2 I (I - 1) / 2 + I G (G + 1) / 2
+  auto before = [&](long long I) { return G * G * I * (I - 1) / 2 + I * G * (G + 1) / 2; };
+  long long I = static_cast<long long>(
+      (-0.5 * G + sqrt(0.25 * G * G + 2.0 * G * G * static_cast<double>(t))) / (G * G) + 0.5);
+  while (I > 0 && before(I) > t) --I;
+  while (before(I + 1) <= t) ++I;
+  const long long u = t - before(I);
+  const long long h = min(static_cast<long long>(G), T - I * G);  // rows of super-row I
+  if (u < I * h * G) {
+    const long long jb = u / (h * G), v = u - jb * h * G;
+    ti = static_cast<int>(I * G + v / G);
+    tj = static_cast<int>(jb * G + v % G);
+  } else {
+    int r, c;
+    decode_lower(static_cast<int>(u - I * h * G), r, c);
+    ti = static_cast<int>(I * G + r);
+    tj = static_cast<int>(I * G + c);
+  }
+}
+
 // ---------------------------------------------------------------- reductions
 DNGD_DEV double warp_sum(double v) {
 #pragma unroll

@@ -43,6 +43,7 @@ constexpr int GF_STAGE_BYTES = 2 * GF_BM * 128;
 constexpr int GF_H0_LD = 16;  // row pitch of the materialised input channels
 constexpr int GF_GLD = GF_BM + 2;  // G-space product tile pitch (double2 RMW, fewer conflicts)
 constexpr int GF_MAXCH = 16;       // channels per point the packed tiles support
+constexpr int GF_GROUP = 16;       // tile rows per L2 super-block (decode_lower_grouped)
 
 struct GramLayer {
   int kh;  // w_k (din for layer 0: materialised input channels)
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(GF_THREADS, 2)
   const int c = p.pc[pi], cp = p.pcp[pi];
   int ti, tj;
   if (c == cp && !p.rect) {
-    decode_lower(t, ti, tj);
+    decode_lower_grouped(t, p.tj_n[pi], GF_GROUP, ti, tj);
   } else {
     ti = t / p.tj_n[pi];
     tj = t - ti * p.tj_n[pi];

@@ -287,6 +287,14 @@ int dngd_loss_many_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                        const dngd_class_desc* classes, int nclass, double* losses, void* work,
                        size_t work_bytes, void* act_work, size_t act_bytes);
 
+/* The first non-finite entry of x (n values, rows in class order; class_ends[c]
+ * = end row of class c): returns DNGD_ERR_NONFINITE with *class_out (class
+ * index) and *point_out (point within the class) when one exists, DNGD_OK
+ * otherwise (residuals.py:125-136, errors.py:14-20).  Synchronises `stream`. */
+int dngd_nonfinite_report(dngd_ctx* ctx, void* stream, const double* x, int64_t n,
+                          const int64_t* class_ends, int nclass, int* class_out,
+                          int64_t* point_out);
+
 /* ---- Nystrom-PCG numerics (reference solver.py:237-366) --------------------- */
 
 /* Symmetric eigendecomposition A = V diag(w) V^T of an n x n matrix (the landmark

@@ -119,6 +119,8 @@ _SIGS = {
     "dngd_loss_many_act": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, c_vp, c_vp, c_int,
                             ctypes.POINTER(ClassDesc), c_int, c_vp, c_vp, c_size, c_vp, c_size],
                            c_int),
+    "dngd_nonfinite_report": ([c_vp, c_vp, c_vp, c_i64, c_vp, c_int, ctypes.POINTER(c_int),
+                               ctypes.POINTER(c_i64)], c_int),
     "dngd_syev_workspace": ([c_vp, c_i64, ctypes.POINTER(c_size)], c_int),
     "dngd_syev_jacobi": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_size],
                          c_int),

@@ -62,10 +62,11 @@ extern "C" int dngd_ctx_create(int device, dngd_ctx** out) {
   e = cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking);
   if (e == cudaSuccess) {
     e = cudaMallocAsync(reinterpret_cast<void**>(&ctx->dot_part),
-                        (dngd::kDotBlocks + 2) * sizeof(double), ctx->own);
+                        (dngd::kDotBlocks + 3) * sizeof(double), ctx->own);
   }
   if (e == cudaSuccess) {
     ctx->dot_counter = reinterpret_cast<unsigned*>(ctx->dot_part + dngd::kDotBlocks);
+    ctx->nf_word = reinterpret_cast<unsigned long long*>(ctx->dot_part + dngd::kDotBlocks + 2);
     e = cudaMemsetAsync(ctx->dot_counter, 0, 2 * sizeof(double), ctx->own);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->own);

@@ -10,6 +10,7 @@
 
 #include <math_constants.h>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -414,3 +415,45 @@ extern "C" int dngd_axpby(dngd_ctx* ctx, void* stream, int64_t n, double a, cons
       n, a, x, b, y, out);
   return cuda_status(ctx, cudaGetLastError(), "axpby");
 }
+
+// ---------------------------------------------------------------- non-finite report
+namespace dngd {
+__global__ void k_first_nonfinite(const double* __restrict__ x, long long n,
+                                  unsigned long long* __restrict__ first) {
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && !isfinite(x[i])) atomicMin(first, static_cast<unsigned long long>(i));
+}
+}  // namespace dngd
+
+extern "C" int dngd_nonfinite_report(dngd_ctx* ctx, void* stream, const double* x, int64_t n,
+                                     const int64_t* class_ends, int nclass, int* class_out,
+                                     int64_t* point_out) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (class_out) *class_out = -1;
+  if (point_out) *point_out = -1;
+  if (n <= 0) return DNGD_OK;
+  cudaError_t e = cudaMemsetAsync(ctx->nf_word, 0xff, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return cuda_status(ctx, e, "nonfinite_report");
+  dngd::k_first_nonfinite<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, n, ctx->nf_word);
+  unsigned long long first = ~0ull;
+  e = cudaMemcpyAsync(&first, ctx->nf_word, sizeof first, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_status(ctx, e, "nonfinite_report");
+  if (first >= static_cast<unsigned long long>(n)) return DNGD_OK;
+  long long row = static_cast<long long>(first), start = 0;
+  int cls = -1;
+  for (int c = 0; c < nclass; ++c) {
+    if (row < class_ends[c]) {
+      cls = c;
+      break;
+    }
+    start = class_ends[c];
+  }
+  if (class_out) *class_out = cls;
+  if (point_out) *point_out = cls >= 0 ? row - start : row;
+  char buf[128];
+  snprintf(buf, sizeof buf, "non-finite value in class %d at point %lld", cls,
+           static_cast<long long>(cls >= 0 ? row - start : row));
+  return dngd::set_error(ctx, DNGD_ERR_NONFINITE, buf);
+}
+

@@ -30,6 +30,7 @@ struct dngd_ctx {
   double* dot_part = nullptr;
   unsigned* dot_counter = nullptr;
   cudaStream_t own = nullptr;  // the context's private stream (setup / teardown only)
+  unsigned long long* nf_word = nullptr;  // dngd_nonfinite_report: first non-finite index
 };
 
 namespace dngd {

@@ -13,7 +13,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import c_size, call, ctx, ptr, stream_handle
+from ._lib import c_int, c_size, call, ctx, ptr, stream_handle
 from .errors import DimensionError
 
 F64 = torch.float64
@@ -334,6 +334,23 @@ def loss_many(mlp, theta, delta, etas, ncand, classes_arr, nclass, out, ws, act_
         call("dngd_loss_many_act", ctx(), stream_handle(), ctypes.byref(mlp), ptr(theta),
              ptr(delta), ptr(etas), int(ncand), classes_arr, nclass, ptr(out), ptr(ws), ws.numel(),
              ptr(act_ws), act_ws.numel())
+
+
+def nonfinite_report(x: torch.Tensor, class_ends):
+    """(class index, point index) of the first non-finite entry of x, or None
+    (dngd_nonfinite_report: a device scan, one synchronisation)."""
+    import numpy as _np
+
+    ends = _np.ascontiguousarray(class_ends, dtype=_np.int64)
+    cls, pt = c_int(-1), ctypes.c_int64(-1)
+    rc = _lib.load_library().dngd_nonfinite_report(
+        ctx(), stream_handle(), ptr(x), x.numel(), ends.ctypes.data_as(ctypes.c_void_p),
+        len(ends), ctypes.byref(cls), ctypes.byref(pt))
+    if rc == _lib.DNGD_OK:
+        return None
+    if rc != _lib.DNGD_ERR_NONFINITE:
+        _lib.check(rc, "dngd_nonfinite_report")
+    return cls.value, pt.value
 
 
 # ---------------------------------------------------------------- Nystrom-PCG numerics

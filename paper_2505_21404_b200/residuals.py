@@ -142,20 +142,22 @@ class ResidualBatch:
 
 
 def _raise_nonfinite(values_t, partition):
-    import torch
+    """NonFiniteError naming the class and point of the first non-finite residual
+    (residuals.py:125-136), found by the device scan dngd_nonfinite_report."""
+    from . import kernels as K
 
-    bad_idx = torch.nonzero(~torch.isfinite(values_t))
-    if bad_idx.numel() == 0:
+    hit = K.nonfinite_report(values_t.contiguous(), [b for _, _, b in partition])
+    if hit is None:
         return
-    bad = int(bad_idx[0, 0].item())
-    for cid, a, b in partition:
-        if a <= bad < b:
-            raise NonFiniteError(
-                f"non-finite residual in class {cid!r} at point {bad - a}",
-                class_id=cid,
-                point_index=bad - a,
-            )
-    raise NonFiniteError("non-finite residual", point_index=bad)
+    k, point = hit
+    if 0 <= k < len(partition):
+        cid = partition[k][0]
+        raise NonFiniteError(
+            f"non-finite residual in class {cid!r} at point {point}",
+            class_id=cid,
+            point_index=point,
+        )
+    raise NonFiniteError("non-finite residual", point_index=point)
 
 
 class ResidualMap:
@@ -246,7 +248,7 @@ class ResidualMap:
     # -- reference (numpy) API --------------------------------------------------------
     def residual_batch(self, theta) -> ResidualBatch:
         r = self.residuals_t(theta)
-        _raise_nonfinite(r, self.partition()) if not bool(r.isfinite().all()) else None
+        _raise_nonfinite(r, self.partition())
         return ResidualBatch(r, self.partition())
 
     def loss(self, theta) -> float:
@@ -282,8 +284,7 @@ class ResidualMap:
 
     def linearize(self, theta):
         r, J = self.linearize_t(theta)
-        if not bool(r.isfinite().all()):
-            _raise_nonfinite(r, self.partition())
+        _raise_nonfinite(r, self.partition())
         return ResidualBatch(r, self.partition()), J[:, : self.n].cpu().numpy()
 
     def jacobian(self, theta) -> np.ndarray:
@@ -311,8 +312,7 @@ class ResidualMap:
 
     def second_directional(self, theta, v) -> np.ndarray:
         f = self.fvv_t(theta, self._vec_t(v, self.n, "tangent"))
-        if not bool(f.isfinite().all()):
-            _raise_nonfinite(f, self.partition())
+        _raise_nonfinite(f, self.partition())
         return f.cpu().numpy()
 
 

@@ -112,3 +112,26 @@ def test_gemv(K, m, n):
     add = rng.normal(size=m)
     out = K.gemv_n(J, dev(x), n, alpha=2.0, add=dev(add), beta=0.5).cpu().numpy()
     assert _rel(out, 2.0 * Jh @ x + 0.5 * add) <= 1e-13
+
+
+def test_nonfinite_report_names_class_and_point():
+    """dngd_nonfinite_report: the first non-finite entry's class and point
+    (residuals.py:125-136 -> errors.py:14-20 NonFiniteError(class_id, point_index))."""
+    import numpy as np
+
+    import paper_2505_21404_b200 as P
+    from paper_2505_21404_b200 import kernels as K
+
+    x = torch.zeros(50, dtype=torch.float64, device="cuda")
+    assert K.nonfinite_report(x, [30, 50]) is None
+    x[41] = float("inf")
+    x[37] = float("nan")
+    assert K.nonfinite_report(x, [30, 50]) == (1, 7)
+    prob = P.make_problem("poisson2d")
+    colloc = prob.sample((20, 8), np.random.default_rng(0))
+    colloc.classes[1].points[5, 0] = np.nan
+    rmap = P.PinnResidualMap(prob, P.MlpSpec((2, 8, 1)), colloc)
+    theta = P.xavier_normal_params(P.MlpSpec((2, 8, 1)))
+    with pytest.raises(P.NonFiniteError) as ei:
+        rmap.residual_batch(theta)
+    assert ei.value.class_id == "boundary" and ei.value.point_index == 5

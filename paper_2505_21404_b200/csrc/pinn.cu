@@ -361,33 +361,51 @@ __global__ void __launch_bounds__(256) k_jwrite(Classes T, const double* __restr
 }
 
 // Element loop of k_jwrite_staged (block fully inside the column range).
-// NCH = 0: runtime channel count.
+// NCH = 0: runtime channel count.  NCH > 0 register-blocks RB rows: a thread keeps
+// the NCH adjoint pairs of its column pair qp in registers and sweeps RB rows pp
+// (each row's NCH activations are warp-wide broadcasts), so the shared-memory
+// reads per stored double2 drop from 2 NCH to NCH (1/RB + 1); a warp still writes
+// 32 consecutive double2 of one row per store.
 template <int NCH>
 DNGD_DEV void jw_rows(const double* __restrict__ sh, const double* __restrict__ sz, int W1,
                       int wout, int nch_rt, double2* __restrict__ dst) {
-  const int nch = NCH > 0 ? NCH : nch_rt;
   const int WP = wout >> 1, NP = W1 * WP;
+  const double2* sz2 = reinterpret_cast<const double2*>(sz);
+  if (NCH > 0 && WP >= 32) {
+    constexpr int RB = 4;
+    const int nblk = (W1 + RB - 1) / RB;  // row blocks
+    for (int f = threadIdx.x; f < nblk * WP; f += 256) {
+      const int rb = f / WP, qp = f - rb * WP;
+      double2 z[NCH > 0 ? NCH : 1];
+#pragma unroll
+      for (int c = 0; c < (NCH > 0 ? NCH : 1); ++c) z[c] = sz2[c * WP + qp];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int pp = rb * RB + r;
+        if (pp >= W1) break;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < (NCH > 0 ? NCH : 1); ++c) {
+          const double h = sh[c * W1 + pp];
+          a0 = fma(h, z[c].x, a0);
+          a1 = fma(h, z[c].y, a1);
+        }
+        __stcs(dst + static_cast<long long>(pp) * WP + qp, make_double2(a0, a1));
+      }
+    }
+    return;
+  }
+  const int nch = NCH > 0 ? NCH : nch_rt;
   const int dpp = 256 / WP, dq = 256 - dpp * WP;
   int f = threadIdx.x;
   int pp = f / WP, qp = f - pp * WP;
-  const double2* sz2 = reinterpret_cast<const double2*>(sz);
   for (; f < NP; f += 256) {
     double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-    for (int c = 0; c < (NCH > 0 ? NCH : 1); ++c) {
-      if (NCH == 0) break;
+    for (int c = 0; c < nch; ++c) {
       const double h = sh[c * W1 + pp];
       const double2 z = sz2[c * WP + qp];
       a0 = fma(h, z.x, a0);
       a1 = fma(h, z.y, a1);
-    }
-    if (NCH == 0) {
-      for (int c = 0; c < nch; ++c) {
-        const double h = sh[c * W1 + pp];
-        const double2 z = sz2[c * WP + qp];
-        a0 = fma(h, z.x, a0);
-        a1 = fma(h, z.y, a1);
-      }
     }
     __stcs(dst + f, make_double2(a0, a1));
     pp += dpp;
@@ -438,6 +456,10 @@ __global__ void __launch_bounds__(256) k_jwrite_staged(Classes T, const double* 
       case 2: jw_rows<2>(sh, sz, W1, wout, nch, dst); break;
       case 3: jw_rows<3>(sh, sz, W1, wout, nch, dst); break;
       case 4: jw_rows<4>(sh, sz, W1, wout, nch, dst); break;
+      case 5: jw_rows<5>(sh, sz, W1, wout, nch, dst); break;
+      case 6: jw_rows<6>(sh, sz, W1, wout, nch, dst); break;
+      case 7: jw_rows<7>(sh, sz, W1, wout, nch, dst); break;
+      case 8: jw_rows<8>(sh, sz, W1, wout, nch, dst); break;
       default: jw_rows<0>(sh, sz, W1, wout, nch, dst); break;
     }
     return;
@@ -2055,7 +2077,13 @@ static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& 
       const unsigned gx = static_cast<unsigned>(std::min<long long>((E / 2 + 255) / 256, 64));
       k_jwrite_in<<<dim3(gx, static_cast<unsigned>(P.m)), 256, 0, s>>>(
           P.T, Zb, ldz, wout, col_begin, col_end, J, ldJ);
-    } else if (vec && Hk != nullptr && jw_staged_bytes(P, win, wout) <= 48 * 1024) {
+    } else if (vec && Hk != nullptr && jw_staged_bytes(P, win, wout) <= 200 * 1024) {
+      // (config 3: 7 channels x 512 units = 57 KB staged per row, above the 48 KB default)
+      static std::atomic<bool> attr[64];  // per device (idempotent, race-free)
+      if (!attr[ctx->device & 63]) {
+        cudaFuncSetAttribute(k_jwrite_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr[ctx->device & 63] = true;
+      }
       k_jwrite_staged<<<static_cast<unsigned>(P.m), 256, jw_staged_bytes(P, win, wout), s>>>(
           P.T, Hk, ldh, win, Zb, ldz, wout, lo, col_begin, col_end, J, ldJ);
     } else if (vec && E < (1LL << 31)) {

@@ -59,6 +59,7 @@ struct JacobiArgs {
   const double* fro2;  // |X|_F^2 (device): the absolute rotation floor (eps |X|_F)^2
   unsigned* rotated;  // [max_sweeps] flags
   int* sweeps_out;
+  long long* trace;   // DNGD_JACOBI_TRACE builds only: clock64 marks of CTA 0
 };
 
 // pair k of round t of the round-robin tournament on M (even) indices: (p, q), p < q
@@ -76,6 +77,8 @@ DNGD_DEV void jac_pair(int k, int t, int M, int& p, int& q) {
   q = max(a, b);
 }
 
+// JR > 0: the pair's rows live in registers (N <= 32 JR); JR = 0: any N, shared only
+template <int JR>
 __global__ void __launch_bounds__(kJT) k_jacobi(JacobiArgs J) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double jsm[];
@@ -93,21 +96,47 @@ __global__ void __launch_bounds__(kJT) k_jacobi(JacobiArgs J) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const int B = J.nblk / 2;
+#ifdef DNGD_JACOBI_TRACE
+  int nt = 0;
+#define JTRACE() if (blockIdx.x == 0 && threadIdx.x == 0 && nt < 256 && J.trace) J.trace[nt++] = clock64();
+#else
+#define JTRACE()
+#endif
   int sweep = 0;
   for (; sweep < J.max_sweeps; ++sweep) {
     for (int t = 0; t < J.nblk - 1; ++t) {
+      JTRACE()
       if (static_cast<int>(blockIdx.x) < B) {
         int bi, bj;
         jac_pair(blockIdx.x, t, J.nblk, bi, bj);
         // rows of Y^T: local r < bs -> block bi, r >= bs -> block bj
-        for (int r = 0; r < rows; ++r) {
-          const double* src = J.Yt + static_cast<long long>(r < bs ? bi * bs + r : bj * bs + (r - bs)) * J.ld;
-          for (int c = threadIdx.x; c < N; c += blockDim.x) S[r * sp + c] = src[c];
+        // all of a thread's row loads in flight before the shared stores (L2 latency
+        // once per outer round, not once per element)
+        for (int e0 = threadIdx.x; e0 < rows * N; e0 += 8 * blockDim.x) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * blockDim.x;
+            v[u] = 0.0;
+            if (e < rows * N) {
+              const int r = e / N, c = e - r * N;
+              v[u] = J.Yt[static_cast<long long>(r < bs ? bi * bs + r : bj * bs + (r - bs)) * J.ld + c];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < rows * N) {
+              const int r = e / N, c = e - r * N;
+              S[r * sp + c] = v[u];
+            }
+          }
         }
         for (int e = threadIdx.x; e < rows * rows; e += blockDim.x)
           Rt[e] = (e / rows) == (e % rows) ? 1.0 : 0.0;
         if (threadIdx.x == 0) s_rot = 0;
         __syncthreads();
+        JTRACE()
         // one inner cyclic sweep over all column pairs of the 2 bs rows
         for (int ir = 0; ir < rows - 1; ++ir) {
           for (int k = warp; k < bs; k += nwarps) {
@@ -115,12 +144,30 @@ __global__ void __launch_bounds__(kJT) k_jacobi(JacobiArgs J) {
             jac_pair(k, ir, rows, a, b);
             double* ra = S + a * sp;
             double* rb = S + b * sp;
+            // the pair's rows in registers (N <= 32 JR) for the dots and the update
+            constexpr int R = JR > 0 ? JR : 1;
+            double xr[R], yr[R];
             double aa = 0.0, bb = 0.0, ab = 0.0;
-            for (int c = lane; c < N; c += 32) {
-              const double x = ra[c], y = rb[c];
-              aa = fma(x, x, aa);
-              bb = fma(y, y, bb);
-              ab = fma(x, y, ab);
+            if constexpr (JR > 0) {
+#pragma unroll
+              for (int u = 0; u < JR; ++u) {
+                const int c = lane + 32 * u;
+                xr[u] = c < N ? ra[c] : 0.0;
+                yr[u] = c < N ? rb[c] : 0.0;
+              }
+#pragma unroll
+              for (int u = 0; u < JR; ++u) {
+                aa = fma(xr[u], xr[u], aa);
+                bb = fma(yr[u], yr[u], bb);
+                ab = fma(xr[u], yr[u], ab);
+              }
+            } else {
+              for (int c = lane; c < N; c += 32) {
+                const double x = ra[c], y = rb[c];
+                aa = fma(x, x, aa);
+                bb = fma(y, y, bb);
+                ab = fma(x, y, ab);
+              }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -132,10 +179,21 @@ __global__ void __launch_bounds__(kJT) k_jacobi(JacobiArgs J) {
               const double zeta = (bb - aa) / (2.0 * ab);
               const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
               const double c = 1.0 / sqrt(1.0 + tt * tt), s = tt * c;
-              for (int col = lane; col < N; col += 32) {
-                const double x = ra[col], y = rb[col];
-                ra[col] = c * x - s * y;
-                rb[col] = s * x + c * y;
+              if constexpr (JR > 0) {
+#pragma unroll
+                for (int u = 0; u < JR; ++u) {
+                  const int col = lane + 32 * u;
+                  if (col < N) {
+                    ra[col] = c * xr[u] - s * yr[u];
+                    rb[col] = s * xr[u] + c * yr[u];
+                  }
+                }
+              } else {
+                for (int col = lane; col < N; col += 32) {
+                  const double x = ra[col], y = rb[col];
+                  ra[col] = c * x - s * y;
+                  rb[col] = s * x + c * y;
+                }
               }
               double* qa = Rt + a * rows;
               double* qb = Rt + b * rows;
@@ -148,6 +206,7 @@ __global__ void __launch_bounds__(kJT) k_jacobi(JacobiArgs J) {
             }
           }
           __syncthreads();
+          JTRACE()
         }
         if (s_rot) {
           for (int r = 0; r < rows; ++r) {
@@ -156,28 +215,52 @@ __global__ void __launch_bounds__(kJT) k_jacobi(JacobiArgs J) {
           }
           // V^T rows <- Rt V^T rows: the eigenvectors as a product of rotations
           // (orthogonal to rounding: eigenvectors of tiny eigenvalues do not pick
-          // up eps |X| / lambda_j of the large ones, as Y_j / |Y_j| would)
-          for (int c = threadIdx.x; c < N; c += blockDim.x) {
-            double v[32];
+          // up eps |X| / lambda_j of the large ones, as Y_j / |Y_j| would).  The
+          // old rows are staged in S (free now), then every thread forms 4 rows of
+          // one column from that column's 2 bs values held in registers.
+          __syncthreads();
+          for (int e0 = threadIdx.x; e0 < rows * N; e0 += 8 * blockDim.x) {
+            double v[8];
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              v[q] = 0.0;
-              if (q < rows) {
-                v[q] = J.Vt[static_cast<long long>(q < bs ? bi * bs + q : bj * bs + (q - bs)) * J.ld + c];
+            for (int u = 0; u < 8; ++u) {
+              const int e = e0 + u * blockDim.x;
+              v[u] = 0.0;
+              if (e < rows * N) {
+                const int r = e / N, c = e - r * N;
+                v[u] = J.Vt[static_cast<long long>(r < bs ? bi * bs + r : bj * bs + (r - bs)) * J.ld + c];
               }
             }
-            for (int r = 0; r < rows; ++r) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int e = e0 + u * blockDim.x;
+              if (e < rows * N) {
+                const int r = e / N, c = e - r * N;
+                S[r * sp + c] = v[u];
+              }
+            }
+          }
+          __syncthreads();
+          const int rgroups = rows / 4;  // rows is even; 4 | rows for bs >= 2
+          for (int f = threadIdx.x; f < rgroups * N; f += blockDim.x) {
+            const int g = f / N, c = f - g * N;
+            double col[32];
+#pragma unroll
+            for (int q = 0; q < 32; ++q) col[q] = q < rows ? S[q * sp + c] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int r = 4 * g + u;
               const double* rr = Rt + r * rows;
               double acc = 0.0;
 #pragma unroll
               for (int q = 0; q < 32; ++q) {
-                if (q < rows) acc = fma(rr[q], v[q], acc);
+                if (q < rows) acc = fma(rr[q], col[q], acc);
               }
               J.Vt[static_cast<long long>(r < bs ? bi * bs + r : bj * bs + (r - bs)) * J.ld + c] = acc;
             }
           }
           if (threadIdx.x == 0) J.rotated[sweep] = 1u;  // benign same-value race
         }
+        JTRACE()
       }
       grid.sync();
     }
@@ -248,8 +331,8 @@ struct JacShape {
 static JacShape jac_shape(long long n) {
   JacShape sh;
   static const int bs_env = getenv("DNGD_JACOBI_BS") ? atoi(getenv("DNGD_JACOBI_BS")) : 16;
-  int bs = std::max(1, std::min(16, bs_env));
-  while (bs > 1 && static_cast<size_t>(2 * bs) * (n + 1) * 8 > 150 * 1024) bs /= 2;
+  int bs = std::max(2, std::min(16, bs_env));
+  while (bs > 2 && static_cast<size_t>(2 * bs) * (n + 1) * 8 > 150 * 1024) bs /= 2;
   sh.bs = bs;
   const long long nb = (n + bs - 1) / bs;
   sh.nblk = static_cast<int>(std::max<long long>(2, (nb + 1) / 2 * 2));
@@ -607,6 +690,10 @@ static unsigned vec_blocks(dngd_ctx* ctx, long long m) {
   return static_cast<unsigned>(std::min<long long>((m + 255) / 256, 2LL * ctx->num_sms));
 }
 
+#ifdef DNGD_JACOBI_TRACE
+long long* dngd_jacobi_trace_ptr = nullptr;
+#endif
+
 extern "C" int dngd_syev_workspace(dngd_ctx* ctx, int64_t n, size_t* bytes) {
   if (!ctx || !bytes || n < 0) return DNGD_ERR_DIMENSION;
   *bytes = jacobi_bytes(n, 60);
@@ -638,6 +725,14 @@ extern "C" int dngd_syev_jacobi(dngd_ctx* ctx, void* stream, const double* A, in
   J.max_sweeps = max_sweeps;
   J.eps = 2.220446049250313e-16;
   J.sweeps_out = sweeps;
+  J.trace = nullptr;
+#ifdef DNGD_JACOBI_TRACE
+  static long long* tr = nullptr;
+  if (!tr) cudaMalloc(&tr, 256 * 8);
+  cudaMemsetAsync(tr, 0, 256 * 8, s);
+  J.trace = tr;
+  dngd_jacobi_trace_ptr = tr;
+#endif
   const long long tot = std::max<long long>(static_cast<long long>(sh.N) * sh.N, max_sweeps);
   k_jacobi_init<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(A, lda, static_cast<int>(n), sh.N,
                                                                        sh.ld, J.Yt, J.Vt, J.rotated,
@@ -645,12 +740,13 @@ extern "C" int dngd_syev_jacobi(dngd_ctx* ctx, void* stream, const double* A, in
   k_fro2<<<1, 1024, 0, s>>>(A, lda, static_cast<int>(n), reinterpret_cast<double*>(b + 2 * mat));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_status(ctx, e, "syev init");
-  e = cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem));
+  auto kern = sh.N <= 32 * 16 ? k_jacobi<16> : k_jacobi<0>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem));
   if (e != cudaSuccess) return cuda_status(ctx, e, "syev smem attribute");
   const unsigned grid = static_cast<unsigned>(std::min(sh.nblk / 2, ctx->num_sms));
   if (grid < static_cast<unsigned>(sh.nblk / 2)) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "syev: too many blocks");
   void* args[] = {&J};
-  e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_jacobi), dim3(grid), dim3(kJT), args,
+  e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(grid), dim3(kJT), args,
                                   sh.smem, s);
   if (e != cudaSuccess) return cuda_status(ctx, e, "syev cooperative launch");
   k_jacobi_out<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(J.Yt, J.Vt, sh.ld, static_cast<int>(n), w,

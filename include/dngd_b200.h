@@ -110,6 +110,19 @@ int dngd_gemm_nt(dngd_ctx* ctx, void* stream, int64_t M, int64_t N, int64_t K,
                  int64_t sB, double* C, int64_t ldc, int64_t sC, int batch, double alpha,
                  double beta, int lower);
 
+/* ---- emulated-FP64 GEMM on the int8 tensor cores (Ozaki scheme) ------------
+ * C = A B^T with A (M x K, lda), B (N x K, ldb) row-major doubles, C (M x N, ldc).
+ * Every row is split into `slices` (6..8) int8 digits of 7 bits below a per-row
+ * power-of-two scale; the S(S+1)/2 digit products that reach FP64 accuracy run
+ * as exact int32 tcgen05 MMAs (kind::i8).  Same contract as the FP64 products
+ * of solver.py:153 / model.py:88-97 it can replace; K <= 32768.  A row with a
+ * non-finite entry yields NaN in its C row/column. */
+int dngd_oz_gemm_workspace(dngd_ctx* ctx, int64_t M, int64_t N, int64_t K, int slices,
+                           size_t* bytes);
+int dngd_oz_gemm_nt(dngd_ctx* ctx, void* stream, int64_t M, int64_t N, int64_t K,
+                    const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                    int64_t ldc, int slices, void* work, size_t work_bytes);
+
 /* ---- vector kernels for the device-resident PCG (solver.py:334-356) ------- */
 int dngd_dot(dngd_ctx* ctx, void* stream, int64_t n, const double* x, const double* y,
              double* out_dev);
@@ -217,6 +230,20 @@ int dngd_gram_factored_part(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* ml
 int dngd_gram_factored_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
                            const dngd_class_desc* classes, int nclass, double* K, int64_t ldK,
                            int part, int nparts, void* act_work, size_t act_bytes);
+
+/* ---- factored dual Gram with emulated-FP64 products (solver.py:142-155) -----
+ * Same result and tile sharding as dngd_gram_factored_act (K = J J^T from the
+ * activations left in act_work by dngd_activations), with every G-space GEMM
+ * computed from `slices` (7 or 8) int8 Ozaki digits per activation row on the
+ * tcgen05 tensor cores.  oz_work: dngd_gram_oz_workspace bytes (digit planes). */
+int dngd_gram_oz_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp,
+                           const dngd_class_desc* classes, int nclass, int slices,
+                           size_t* bytes);
+int dngd_gram_oz_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                     const dngd_class_desc* classes, int nclass, double* K, int64_t ldK,
+                     int part, int nparts, int slices, void* act_work, size_t act_bytes,
+                     void* oz_work, size_t oz_bytes);
+
 
 /* r plus the forward channels and per-point adjoints (no J) left in work for
  * dngd_jt_factored (the tape sweep of residuals.py:241-256 without the rows) */

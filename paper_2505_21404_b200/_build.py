@@ -11,8 +11,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libdngd_b200.so")
-SOURCES = ["abi.cu", "gemm.cu", "chol.cu", "blas2.cu", "pinn.cu", "eig_cg.cu"]
-HEADERS = ["common.cuh", "internal.h", "gram_factored.cuh",
+SOURCES = ["abi.cu", "gemm.cu", "chol.cu", "blas2.cu", "pinn.cu", "eig_cg.cu", "ozaki.cu"]
+HEADERS = ["common.cuh", "internal.h", "gram_factored.cuh", "tc05.cuh", "oz_common.cuh", "gram_oz.cuh",
            os.path.join("..", "..", "include", "dngd_b200.h")]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

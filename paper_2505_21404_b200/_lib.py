@@ -78,6 +78,9 @@ _SIGS = {
     "dngd_gemv_n": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_dbl, c_vp, c_dbl, c_vp], c_int),
     "dngd_gemm_nt": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64,
                       c_vp, c_i64, c_i64, c_int, c_dbl, c_dbl, c_int], c_int),
+    "dngd_oz_gemm_workspace": ([c_vp, c_i64, c_i64, c_i64, c_int, ctypes.POINTER(c_size)], c_int),
+    "dngd_oz_gemm_nt": ([c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                         c_int, c_vp, c_size], c_int),
     "dngd_dot": ([c_vp, c_vp, c_i64, c_vp, c_vp, c_vp], c_int),
     "dngd_axpby": ([c_vp, c_vp, c_i64, c_dbl, c_vp, c_dbl, c_vp, c_vp], c_int),
     "dngd_ls_select": ([c_vp, c_vp, c_vp, c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_vp], c_int),
@@ -94,6 +97,10 @@ _SIGS = {
                                  c_int, c_vp, c_size], c_int),
     "dngd_gram_factored_act": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc),
                                 c_int, c_vp, c_i64, c_int, c_int, c_vp, c_size], c_int),
+    "dngd_gram_oz_workspace": ([c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc), c_int,
+                                c_int, ctypes.POINTER(c_size)], c_int),
+    "dngd_gram_oz_act": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc), c_int,
+                          c_vp, c_i64, c_int, c_int, c_int, c_vp, c_size, c_vp, c_size], c_int),
     "dngd_activations": ([c_vp, c_vp, ctypes.POINTER(MlpDesc), c_vp, ctypes.POINTER(ClassDesc),
                           c_int, c_vp, c_vp, c_size], c_int),
     "dngd_jt_workspace": ([c_vp, ctypes.POINTER(MlpDesc), ctypes.POINTER(ClassDesc), c_int,

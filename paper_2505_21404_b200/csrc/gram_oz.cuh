@@ -1,0 +1,292 @@
+// Factored dual Gram on the int8 tensor cores: the products of gram_factored.cuh
+//     K_ij = sum_k sum_{c,c'} (Hext_k[i,c] . Hext_k[j,c']) (Zbar_k[i,c] . Zbar_k[j,c'])
+// with every G-space GEMM (G^H_k = H_k H_k^T, G^Z_k = Zbar_k Zbar_k^T) emulated
+// in FP64 by Ozaki slices (ozaki.cu, tc05.cuh): each activation row is cut into
+// S int8 digits below a per-row power-of-two scale, and the S(S+1)/2 digit
+// products of a 32-wide K-chunk run as exact int32 tcgen05 MMAs into S diagonal
+// accumulators in TMEM.
+//
+// Tile: 128 G-rows (2 ppc whole points of the row class) x 64 G-columns (ppc =
+// floor(64 / nch) whole points of the column class).  Per layer two MMA phases
+// (H then Z; the output layer's Z is the per-row residual seeds).  Warp roles:
+// warp 0 streams {32 B x rows x S slices} TMA boxes of the sliced activations
+// through a 3-stage mbarrier ring; warp 1 owns TMEM (512 columns = S diagonals
+// x 64) and issues the MMAs (one elected lane, A tiles held in the collector
+// across their S - t products); warps 2-9 drain TMEM after each phase: thread
+// (q, h) owns G-row 32q + lane and G-columns 32h .. 32h + 31, folds the S int32
+// diagonals exactly into FP64 (oz_combine), applies the row/column scales and
+// the bias entry, parks G^H in shared memory (column-major, conflict-free) and
+// accumulates G^H o G^Z in registers.  After the last layer the G tile goes to
+// shared memory and every point pair sums its nch x nch' block in a fixed
+// order (deterministic K, as the DMMA kernel).
+//
+// Tile order: lower triangle of (row tile, column tile) with column tiles half
+// as tall, in super-rows of GO_GROUP row tiles walked column by column, so the
+// ~148 CTAs in flight share their operand tiles through L2.
+
+constexpr int GO_STAGES = 3;
+constexpr int GO_GROUP = 8;
+
+struct GozParams {
+  CUtensorMap mA[DNGD_MAX_LAYERS][2];  // sliced H_k / Zbar_k, box 32 B x 128 rows x S
+  CUtensorMap mB[DNGD_MAX_LAYERS][2];  // same buffers, box 32 B x 64 rows x S
+  const double* sc[DNGD_MAX_LAYERS][2];  // per activation row: 2^e (NaN = non-finite row)
+  long long R;                           // activation rows
+  Classes T;
+  int L;
+  int nk[DNGD_MAX_LAYERS][2];  // 32-wide K-chunks per phase (Z of the output layer: 0)
+  int nch[DNGD_MAX_CLASSES];
+  int ppc[DNGD_MAX_CLASSES];  // whole points per 64-row column tile; row tiles hold 2 ppc
+  int npairs;
+  int pc[10], pcp[10];
+  int tstart[11];
+  int ti_n[10], tj_n[10];
+  double* K;
+  long long ldK;
+  int tile0;
+  int dbg;  // experiments: 1 = epilogue drains only, 2 = no MMAs
+};
+
+// lower-triangle tile t of TI row tiles (row tile ti spans column tiles 2ti, 2ti+1)
+// in super-rows of GO_GROUP row tiles, column-major inside a super-row
+DNGD_DEV void goz_decode_tri(int t, int TI, int& ti, int& tj) {
+  constexpr int G = GO_GROUP;
+  int I = static_cast<int>((sqrt(1.0 + 4.0 * t) - 1.0) * 0.5) / G;
+  while (I > 0 && static_cast<long long>(G) * I * (G * I + 1) > t) --I;
+  while (G * (I + 1) < TI && static_cast<long long>(G) * (I + 1) * (G * (I + 1) + 1) <= t) ++I;
+  const int r0 = G * I, h = min(G, TI - r0);
+  int u = t - r0 * (r0 + 1);
+  const int full = h * (2 * r0 + 2);
+  if (u < full) {
+    tj = u / h;
+    ti = r0 + u % h;
+    return;
+  }
+  u -= full;
+  for (int s = 0; s < h - 1; ++s) {
+    const int n = h - 1 - s;
+    if (u < 2 * n) {
+      tj = 2 * r0 + 2 + 2 * s + u / n;
+      ti = r0 + s + 1 + u % n;
+      return;
+    }
+    u -= 2 * n;
+  }
+  ti = tj = 0;
+}
+
+DNGD_DEV void goz_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(256);
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant__ GozParams p) {
+  extern __shared__ uint8_t go_smem_raw[];
+  uint8_t* smem = smem_align(go_smem_raw, 1024);
+  constexpr int ABYTES = S * OZ_BM * 32, STAGE = S * (OZ_BM + OZ_BN) * 32;
+  double* PH = reinterpret_cast<double*>(smem + GO_STAGES * STAGE);  // [64 cols][128 rows]
+  uint64_t* full = reinterpret_cast<uint64_t*>(PH + OZ_BM * OZ_BN);
+  uint64_t* empty = full + GO_STAGES;
+  uint64_t* tfull = empty + GO_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tempty + 1);
+  __shared__ double sA[OZ_BM], sB[OZ_BN], zA[OZ_BM], zB[OZ_BN];
+
+  // ---- tile decode
+  int pi = 0;
+  const int tile = static_cast<int>(blockIdx.x) + p.tile0;
+  while (pi + 1 < p.npairs && tile >= p.tstart[pi + 1]) ++pi;
+  const int t = tile - p.tstart[pi];
+  const int c = p.pc[pi], cp = p.pcp[pi];
+  int ti, tj;
+  if (c == cp) {
+    goz_decode_tri(t, p.ti_n[pi], ti, tj);
+  } else {  // rectangle, column-major: CTAs in flight share the column tiles
+    tj = t / p.ti_n[pi];
+    ti = t - tj * p.ti_n[pi];
+  }
+  const int na = p.nch[c], nb = p.nch[cp];
+  const int np_r = 2 * p.ppc[c], np_c = p.ppc[cp];
+  const int P0 = ti * np_r, Q0 = tj * np_c;
+  const ClassDev& Ca = p.T.c[c];
+  const ClassDev& Cb = p.T.c[cp];
+  const long long arow0 = Ca.act0 + static_cast<long long>(P0) * na;
+  const long long brow0 = Cb.act0 + static_cast<long long>(Q0) * nb;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < GO_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 8);
+    fence_barrier_init();
+  }
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + OZ_BM) {  // row seeds / value flags
+    const int g = threadIdx.x - 64;
+    const int cha = g % na, pa = P0 + g / na;
+    const bool ok = g < np_r * na && pa < Ca.count;
+    sA[g] = ok ? seedc(p.T, Ca, cha, Ca.row0 + pa) : 0.0;
+    zA[g] = (ok && cha == 0) ? 1.0 : 0.0;
+  } else if (threadIdx.x >= 64 + OZ_BM && threadIdx.x < 64 + OZ_BM + OZ_BN) {
+    const int g = threadIdx.x - 64 - OZ_BM;
+    const int chb = g % nb, pb = Q0 + g / nb;
+    const bool ok = g < np_c * nb && pb < Cb.count;
+    sB[g] = ok ? seedc(p.T, Cb, chb, Cb.row0 + pb) : 0.0;
+    zB[g] = (ok && chb == 0) ? 1.0 : 0.0;
+  }
+  if (warp == 1) tmem_alloc(taddr_sh, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *taddr_sh;
+
+  if (warp == 0) {
+    // ---- TMA producer: every phase's K-chunks through the ring
+    if (lane == 0) {
+      int f = 0;
+      for (int k = 0; k < p.L; ++k) {
+        for (int part = 0; part < 2; ++part) {
+          const int nk = p.nk[k][part];
+          for (int kc = 0; kc < nk; ++kc, ++f) {
+            const int st = f % GO_STAGES;
+            if (f >= GO_STAGES) mbar_wait(&empty[st], ((f / GO_STAGES) - 1) & 1);
+            uint8_t* sa = smem + st * STAGE;
+            mbar_arrive_expect_tx(&full[st], STAGE);
+            tma_load_3d(sa, &p.mA[k][part], &full[st], kc * 32, static_cast<int>(arow0), 0);
+            tma_load_3d(sa + ABYTES, &p.mB[k][part], &full[st], kc * 32, static_cast<int>(brow0), 0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer
+    constexpr uint32_t idesc = umma_idesc_s8(OZ_BM, OZ_BN);
+    int f = 0, ph = 0;
+    for (int k = 0; k < p.L; ++k) {
+      for (int part = 0; part < 2; ++part) {
+        const int nk = p.nk[k][part];
+        if (nk == 0) continue;
+        if (ph > 0) mbar_wait(tempty, (ph - 1) & 1);  // epilogue drained the last phase
+        tc_fence_after();
+        for (int kc = 0; kc < nk; ++kc, ++f) {
+          const int st = f % GO_STAGES;
+          mbar_wait(&full[st], (f / GO_STAGES) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(smem + st * STAGE);
+            if (p.dbg != 2) oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, kc == 0);
+            umma_commit(&empty[st]);
+            if (kc == nk - 1) umma_commit(tfull);
+          }
+          __syncwarp();
+        }
+        ++ph;
+      }
+    }
+  } else {
+    // ---- epilogue: thread owns G-row `row`, G-columns col0 .. col0 + 31
+    const int q = warp & 3, hh = (warp - 2) >> 2;
+    const int row = 32 * q + lane, col0 = 32 * hh;
+    const uint32_t tl = tbase + (static_cast<uint32_t>(32 * q) << 16);
+    const long long arow = arow0 + row;
+    double G[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) G[j] = 0.0;
+    int ph = 0;
+    for (int k = 0; k < p.L; ++k) {
+      const bool seeds = p.nk[k][1] == 0;  // output layer: G^Z = seed_row seed_col
+      for (int part = 0; part < 2; ++part) {
+        if (p.nk[k][part] == 0) continue;
+        mbar_wait(tfull, ph & 1);
+        tc_fence_after();
+        const double* scv = p.sc[k][part];
+        const double sr = arow < p.R ? scv[arow] : 0.0;
+        // this warp's 32 column scales: lane j holds column col0 + j (shuffled below)
+        const long long bl = brow0 + col0 + lane;
+        const double scl = bl < p.R ? scv[bl] : 0.0;
+        const double za = zA[row], sar = sA[row];
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          int32_t acc[S][8];
+#pragma unroll
+          for (int d = 0; d < S; ++d) tmem_ld8(tl + d * OZ_BN + col0 + 8 * cc, acc[d]);
+          tmem_ld_wait();
+          if (p.dbg == 1) {
+            if (cc == 3) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(tempty);
+            }
+            G[cc] += acc[0][0] + acc[S - 1][7];
+            continue;
+          }
+          if (cc == 3) {  // every diagonal is in registers: hand TMEM to the next phase
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int gc = col0 + 8 * cc + j;
+            const double scol = __shfl_sync(0xffffffffu, scl, 8 * cc + j);
+            int32_t a[S];
+#pragma unroll
+            for (int d = 0; d < S; ++d) a[d] = acc[d][j];
+            const double v = oz_combine<S>(a) * (sr * scol);
+            if (part == 0) {
+              const double vh = fma(za, zB[gc], v);  // + bias entry (value channels)
+              if (seeds) {
+                G[8 * cc + j] = fma(vh, sar * sB[gc], G[8 * cc + j]);
+              } else {
+                PH[gc * OZ_BM + row] = vh;
+              }
+            } else {
+              G[8 * cc + j] = fma(PH[gc * OZ_BM + row], v, G[8 * cc + j]);
+            }
+          }
+        }
+        ++ph;
+      }
+    }
+    // ---- G tile to shared memory (PH is free: the last phase was the output layer's H)
+#pragma unroll
+    for (int j = 0; j < 32; ++j) PH[(col0 + j) * OZ_BM + row] = G[j];
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const long long cnt_r = Ca.count, cnt_c = Cb.count;
+    for (int e = threadIdx.x - 64; e < np_r * np_c; e += 256) {
+      const int r = e / np_c, cc = e - (e / np_c) * np_c;
+      const long long pr = P0 + r, pcl = Q0 + cc;
+      if (pr >= cnt_r || pcl >= cnt_c) continue;
+      const long long grow = Ca.row0 + pr, gcol = Cb.row0 + pcl;
+      if (c == cp && gcol > grow) continue;
+      double v = 0.0;
+      for (int a = 0; a < na; ++a)
+        for (int b = 0; b < nb; ++b) v += PH[(cc * nb + b) * OZ_BM + r * na + a];
+      p.K[grow * p.ldK + gcol] = v;
+      p.K[gcol * p.ldK + grow] = v;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
+static size_t gram_oz_smem(int S) {
+  return oz_smem_bytes(S, GO_STAGES) + static_cast<size_t>(OZ_BM) * OZ_BN * 8 + 64;
+}

@@ -66,4 +66,14 @@ int syrk_plan(dngd_ctx* ctx, long long m, long long ncols, int* splits, long lon
 int syrk(dngd_ctx* ctx, cudaStream_t s, const double* J, long long m, long long ncols,
          long long ldJ, double* K, long long ldK, int accumulate, void* work, size_t wb);
 
+// Ozaki slicing (ozaki.cu): rows x K doubles (pitch ld) -> int8 digits Q[slices][rows][kpad]
+// (kpad = K rounded up to 32, zero digits past K) and per-row power-of-two scales;
+// a row with a non-finite entry gets scale NaN.
+int oz_slice(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows, long long K,
+             long long ld, int slices, int8_t* Q, double* scale);
+// 3-D TMA map over Q: box {32 bytes, box_rows, slices}, 32-byte swizzle, rows past
+// the end read as zero digits
+int oz_encode(dngd_ctx* ctx, CUtensorMap* map, const int8_t* Q, long long rows, long long kpad,
+              int slices, int box_rows);
+
 }  // namespace dngd

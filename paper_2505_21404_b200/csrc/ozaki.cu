@@ -1,0 +1,266 @@
+// Emulated FP64 GEMM on the int8 tensor cores (Ozaki scheme, slices of 7 bits).
+//
+// FP64 has no tcgen05 kind; the FP64 DMMA pipe peaks at ~35 TFLOP/s on B200
+// while kind::i8 runs ~4.5 POPS.  Each row of A (and of B) is written as
+//     x = 2^e sum_{t<S} d_t 2^{-7(t+1)},  d_t int8,
+// with 2^e >= max|row| (k_oz_slice).  Then
+//     (A B^T)_ij = 2^{e_i + f_j} sum_D 2^{-7(D+2)} sum_{t+u=D} (A_t B_u^T)_ij
+// and every A_t B_u^T is an exact int32 product on the tensor cores.  Products
+// with t + u >= S sit below the slicing error and are skipped, so one K-chunk
+// costs S(S+1)/2 MMAs accumulating into S diagonals in TMEM (S x 64 columns of
+// a 128 x 64 tile; S = 8 fills the 512 columns).  Relative accuracy per entry is
+// ~K 2^{-7S} max|a_i| max|b_j|: S = 8 is at the level of an FP64 dot product,
+// S = 7 about 16x coarser.
+//
+// This file holds the slicing kernel and a plain C = A B^T GEMM over sliced
+// operands (dngd_oz_gemm_nt); the factored dual Gram uses the same machinery
+// with its own epilogue (gram_oz.cuh).
+
+#include <algorithm>
+#include <cmath>
+
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "internal.h"
+#include "oz_common.cuh"
+#include "tc05.cuh"
+
+namespace dngd {
+
+// One warp per row: max |x| (non-finite flagged), scale 2^e with
+// max 2^-e 128 < 127.5, then S exact remainder digits per entry
+// (y *= 128; d = rint(y); y -= d), written as 4-digit words per slice.
+template <int S>
+__global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ X, long long rows,
+                                                  long long K, long long ld, long long kpad,
+                                                  int8_t* __restrict__ Q,
+                                                  double* __restrict__ scale) {
+  const long long row = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const double* x = X + row * ld;
+  double mx = 0.0;
+  bool bad = false;
+  for (long long k = lane; k < K; k += 32) {
+    const double v = x[k];
+    bad |= !isfinite(v);
+    mx = fmax(mx, fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad ? 1 : 0, o) != 0;
+  }
+  int e = 0;
+  if (mx > 0.0 && !bad) {
+    const double f = frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)
+    if (f * 128.0 >= 127.5) ++e;     // first digit stays within int8
+  }
+  if (lane == 0) scale[row] = bad ? CUDART_NAN : ldexp(1.0, e);
+  const long long words = kpad / 4;
+  const size_t plane = static_cast<size_t>(rows) * kpad;
+  for (long long w = lane; w < words; w += 32) {
+    uint32_t packed[S];
+#pragma unroll
+    for (int t = 0; t < S; ++t) packed[t] = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const long long k = 4 * w + b;
+      double y = (k < K && !bad) ? ldexp(x[k], -e) : 0.0;
+#pragma unroll
+      for (int t = 0; t < S; ++t) {
+        y *= 128.0;
+        const double d = rint(y);
+        y -= d;
+        packed[t] |= (static_cast<uint32_t>(static_cast<int>(d)) & 0xffu) << (8 * b);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < S; ++t)
+      reinterpret_cast<uint32_t*>(Q + t * plane + row * kpad)[w] = packed[t];
+  }
+}
+
+int oz_slice(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows, long long K,
+             long long ld, int slices, int8_t* Q, double* scale) {
+  if (rows <= 0) return DNGD_OK;
+  const long long kp = oz_kpad(K);
+  const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
+  switch (slices) {
+    case 6: k_oz_slice<6><<<grid, 256, 0, s>>>(X, rows, K, ld, kp, Q, scale); break;
+    case 7: k_oz_slice<7><<<grid, 256, 0, s>>>(X, rows, K, ld, kp, Q, scale); break;
+    case 8: k_oz_slice<8><<<grid, 256, 0, s>>>(X, rows, K, ld, kp, Q, scale); break;
+    default: return set_error(ctx, DNGD_ERR_DIMENSION, "oz_slice: slices must be 6, 7 or 8");
+  }
+  return cuda_status(ctx, cudaGetLastError(), "oz_slice");
+}
+
+int oz_encode(dngd_ctx* ctx, CUtensorMap* map, const int8_t* Q, long long rows, long long kpad,
+              int slices, int box_rows) {
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(std::max(rows, 1LL)),
+                        static_cast<cuuint64_t>(slices)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(kpad),
+                           static_cast<cuuint64_t>(kpad) * static_cast<cuuint64_t>(std::max(rows, 1LL))};
+  cuuint32_t box[3] = {32, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(slices)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(Q), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? DNGD_OK : set_error(ctx, DNGD_ERR_CUDA, "oz: tensor map encode failed");
+}
+
+template <int S, int STAGES>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    k_oz_gemm(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
+              const double* __restrict__ scA, const double* __restrict__ scB,
+              double* __restrict__ C, long long ldc, int M, int N, int nk) {
+  extern __shared__ uint8_t oz_smem_raw[];
+  uint8_t* smem = smem_align(oz_smem_raw, 1024);
+  constexpr int ABYTES = S * OZ_BM * 32, STAGE = S * (OZ_BM + OZ_BN) * 32;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * OZ_BM, n0 = blockIdx.x * OZ_BN;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(taddr_sh, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *taddr_sh;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kc = 0; kc < nk; ++kc) {
+        const int st = kc % STAGES;
+        if (kc >= STAGES) mbar_wait(&empty[st], ((kc / STAGES) - 1) & 1);
+        uint8_t* sa = smem + st * STAGE;
+        mbar_arrive_expect_tx(&full[st], STAGE);
+        tma_load_3d(sa, &mA, &full[st], kc * 32, m0, 0);
+        tma_load_3d(sa + ABYTES, &mB, &full[st], kc * 32, n0, 0);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = umma_idesc_s8(OZ_BM, OZ_BN);
+    for (int kc = 0; kc < nk; ++kc) {
+      const int st = kc % STAGES;
+      mbar_wait(&full[st], (kc / STAGES) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(smem + st * STAGE);
+        oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, kc == 0);
+        umma_commit(&empty[st]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) umma_commit(tfull);
+    __syncwarp();
+  } else {
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    const int row = 32 * q + lane;
+    const double sa = m0 + row < M ? scA[m0 + row] : 0.0;
+#pragma unroll 1
+    for (int c = 0; c < OZ_BN / 2 / 8; ++c) {
+      const int col0 = h * (OZ_BN / 2) + 8 * c;
+      int32_t acc[S][8];
+#pragma unroll
+      for (int d = 0; d < S; ++d) tmem_ld8(tbase + (static_cast<uint32_t>(32 * q) << 16) + d * OZ_BN + col0, acc[d]);
+      tmem_ld_wait();
+      if (m0 + row < M) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int col = n0 + col0 + j;
+          if (col >= N) continue;
+          int32_t a[S];
+#pragma unroll
+          for (int d = 0; d < S; ++d) a[d] = acc[d][j];
+          C[static_cast<long long>(m0 + row) * ldc + col] = oz_combine<S>(a) * (sa * scB[col]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, 512);
+  }
+}
+
+template <int S>
+static int oz_gemm_launch(dngd_ctx* ctx, cudaStream_t s, const CUtensorMap& mA,
+                          const CUtensorMap& mB, const double* scA, const double* scB, double* C,
+                          long long ldc, long long M, long long N, int nk) {
+  constexpr int STAGES = 3;
+  const size_t smem = oz_smem_bytes(S, STAGES);
+  auto kern = k_oz_gemm<S, STAGES>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return cuda_status(ctx, e, "oz_gemm smem attribute");
+  dim3 grid(static_cast<unsigned>((N + OZ_BN - 1) / OZ_BN), static_cast<unsigned>((M + OZ_BM - 1) / OZ_BM));
+  kern<<<grid, OZ_THREADS, smem, s>>>(mA, mB, scA, scB, C, ldc, static_cast<int>(M),
+                                       static_cast<int>(N), nk);
+  return cuda_status(ctx, cudaGetLastError(), "oz_gemm");
+}
+
+}  // namespace dngd
+
+using namespace dngd;
+
+static size_t oz_al(size_t b) { return (b + 255) / 256 * 256; }
+
+extern "C" int dngd_oz_gemm_workspace(dngd_ctx* ctx, int64_t M, int64_t N, int64_t K, int slices,
+                                      size_t* bytes) {
+  (void)ctx;
+  const long long kp = oz_kpad(K);
+  *bytes = oz_al(static_cast<size_t>(slices) * M * kp) + oz_al(static_cast<size_t>(slices) * N * kp) +
+           oz_al(static_cast<size_t>(M) * 8) + oz_al(static_cast<size_t>(N) * 8);
+  return DNGD_OK;
+}
+
+extern "C" int dngd_oz_gemm_nt(dngd_ctx* ctx, void* stream, int64_t M, int64_t N, int64_t K,
+                               const double* A, int64_t lda, const double* B, int64_t ldb,
+                               double* C, int64_t ldc, int slices, void* work, size_t work_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (M <= 0 || N <= 0) return DNGD_OK;
+  if (K <= 0 || K > kOzMaxK) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm: K outside [1, 32768]");
+  if (slices < 6 || slices > 8) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm: slices must be 6, 7 or 8");
+  size_t need = 0;
+  dngd_oz_gemm_workspace(ctx, M, N, K, slices, &need);
+  if (work_bytes < need) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm: workspace too small");
+  const long long kp = oz_kpad(K);
+  char* w = static_cast<char*>(work);
+  int8_t* qa = reinterpret_cast<int8_t*>(w);
+  w += oz_al(static_cast<size_t>(slices) * M * kp);
+  int8_t* qb = reinterpret_cast<int8_t*>(w);
+  w += oz_al(static_cast<size_t>(slices) * N * kp);
+  double* sa = reinterpret_cast<double*>(w);
+  w += oz_al(static_cast<size_t>(M) * 8);
+  double* sb = reinterpret_cast<double*>(w);
+  int rc = oz_slice(ctx, s, A, M, K, lda, slices, qa, sa);
+  if (rc) return rc;
+  rc = oz_slice(ctx, s, B, N, K, ldb, slices, qb, sb);
+  if (rc) return rc;
+  CUtensorMap mA, mB;
+  rc = oz_encode(ctx, &mA, qa, M, kp, slices, OZ_BM);
+  if (rc) return rc;
+  rc = oz_encode(ctx, &mB, qb, N, kp, slices, OZ_BN);
+  if (rc) return rc;
+  const int nk = static_cast<int>(kp / 32);
+  switch (slices) {
+    case 6: return oz_gemm_launch<6>(ctx, s, mA, mB, sa, sb, C, ldc, M, N, nk);
+    case 7: return oz_gemm_launch<7>(ctx, s, mA, mB, sa, sb, C, ldc, M, N, nk);
+    default: return oz_gemm_launch<8>(ctx, s, mA, mB, sa, sb, C, ldc, M, N, nk);
+  }
+}

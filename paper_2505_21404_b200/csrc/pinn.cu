@@ -24,6 +24,8 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "oz_common.cuh"
+#include "tc05.cuh"
 
 namespace dngd {
 
@@ -1591,6 +1593,7 @@ __global__ void k_chunk_reduce(const double* __restrict__ part, int nchunks, lon
 }
 
 #include "gram_factored.cuh"
+#include "gram_oz.cuh"
 
 // ------------------------------------------------------------------ fused line search
 // Line-search losses for narrow nets (every width <= 64) in one launch: a CTA
@@ -2364,6 +2367,153 @@ extern "C" int dngd_gram_factored_act(dngd_ctx* ctx, void* stream, const dngd_ml
   carve_assemble(P, A, B);
   P.T.u0 = B.u0;
   return gram_from_act(ctx, s, P, B, K, ldK, part, nparts);
+}
+
+// ------------------------------------------------------------------ emulated-FP64 Gram
+// dngd_gram_oz_act: the factored Gram over the activations in act_work with every
+// G-space GEMM on the int8 tensor cores (gram_oz.cuh).  oz_work holds, per layer
+// and part (H_k, Zbar_k), the R x kpad x S digit planes and R row scales.
+
+static size_t oz_al256(size_t b) { return (b + 255) / 256 * 256; }
+
+static long long goz_kdim(const Plan& P, int k, int part) {
+  if (part == 0) return k == 0 ? P.T.din : P.w[k];
+  return k <= P.L - 2 ? P.w[k + 1] : 0;
+}
+
+static size_t gram_oz_bytes(const Plan& P, int S) {
+  size_t b = 0;
+  for (int k = 0; k < P.L; ++k)
+    for (int part = 0; part < 2; ++part) {
+      const long long kd = goz_kdim(P, k, part);
+      if (kd == 0) continue;
+      b += oz_al256(static_cast<size_t>(S) * P.R * oz_kpad(kd)) + oz_al256(static_cast<size_t>(P.R) * 8);
+    }
+  return b;
+}
+
+static int goz_check(dngd_ctx* ctx, const Plan& P, int slices) {
+  if (slices < 7 || slices > 8) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_oz: slices must be 7 or 8");
+  if (P.wide_in) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: wide input layer");
+  if (P.T.din > DNGD_MAX_GRAD) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: input dim > 12");
+  if (P.R >= (1LL << 31)) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: too many activation rows");
+  for (int k = 0; k < P.L; ++k)
+    if (goz_kdim(P, k, 0) > kOzMaxK || goz_kdim(P, k, 1) > kOzMaxK)
+      return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: layer wider than 32768");
+  for (int c = 0; c < P.T.n; ++c)
+    if (P.T.c[c].nch > OZ_BN) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: more than 64 channels per point");
+  return DNGD_OK;
+}
+
+extern "C" int dngd_gram_oz_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp,
+                                      const dngd_class_desc* classes, int nclass, int slices,
+                                      size_t* bytes) {
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  rc = goz_check(ctx, P, slices);
+  if (rc) return rc;
+  *bytes = gram_oz_bytes(P, slices);
+  return DNGD_OK;
+}
+
+extern "C" int dngd_gram_oz_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
+                                const dngd_class_desc* classes, int nclass, double* K,
+                                int64_t ldK, int part, int nparts, int slices, void* act_work,
+                                size_t act_bytes, void* oz_work, size_t oz_bytes) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nparts < 1 || part < 0 || part >= nparts) {
+    return set_error(ctx, DNGD_ERR_DIMENSION, "gram_oz: part outside [0, nparts)");
+  }
+  Plan P;
+  int rc = make_plan(ctx, mlp, classes, nclass, P);
+  if (rc) return rc;
+  if (bytes_of(P, 0, 1) > act_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_oz: activation workspace too small");
+  if (P.m == 0) return DNGD_OK;
+  rc = goz_check(ctx, P, slices);
+  if (rc) return rc;
+  if (gram_oz_bytes(P, slices) > oz_bytes) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_oz: workspace too small");
+  Arena A{static_cast<char*>(act_work)};
+  AsmBufs B;
+  carve_assemble(P, A, B);
+  P.T.u0 = B.u0;
+  thread_local GozParams gp;
+  memset(&gp, 0, sizeof gp);
+  gp.T = P.T;
+  gp.L = P.L;
+  gp.R = P.R;
+  char* w = static_cast<char*>(oz_work);
+  for (int k = 0; k < P.L; ++k) {
+    for (int pt = 0; pt < 2; ++pt) {
+      const long long kd = goz_kdim(P, k, pt);
+      gp.nk[k][pt] = static_cast<int>(oz_kpad(kd) / 32);
+      if (kd == 0) continue;
+      const double* src;
+      long long ld;
+      if (pt == 0) {
+        src = k == 0 ? B.H0 : B.H[k];
+        ld = k == 0 ? GF_H0_LD : P.ld[k];
+      } else {
+        src = B.Zb[k];
+        ld = P.ld[k + 1];
+      }
+      int8_t* Q = reinterpret_cast<int8_t*>(w);
+      w += oz_al256(static_cast<size_t>(slices) * P.R * oz_kpad(kd));
+      double* sc = reinterpret_cast<double*>(w);
+      w += oz_al256(static_cast<size_t>(P.R) * 8);
+      rc = oz_slice(ctx, s, src, P.R, kd, ld, slices, Q, sc);
+      if (rc) return rc;
+      rc = oz_encode(ctx, &gp.mA[k][pt], Q, P.R, oz_kpad(kd), slices, OZ_BM);
+      if (rc) return rc;
+      rc = oz_encode(ctx, &gp.mB[k][pt], Q, P.R, oz_kpad(kd), slices, OZ_BN);
+      if (rc) return rc;
+      gp.sc[k][pt] = sc;
+    }
+  }
+  int np = 0, tiles = 0;
+  gp.tstart[0] = 0;
+  for (int c = 0; c < P.T.n; ++c) {
+    gp.nch[c] = P.T.c[c].nch;
+    gp.ppc[c] = OZ_BN / P.T.c[c].nch;
+  }
+  for (int c = 0; c < P.T.n; ++c) {
+    for (int cp = 0; cp <= c; ++cp) {
+      const int TI = static_cast<int>((P.T.c[c].count + 2 * gp.ppc[c] - 1) / (2 * gp.ppc[c]));
+      const int TJ = static_cast<int>((P.T.c[cp].count + gp.ppc[cp] - 1) / gp.ppc[cp]);
+      gp.pc[np] = c;
+      gp.pcp[np] = cp;
+      gp.ti_n[np] = TI;
+      gp.tj_n[np] = TJ;
+      tiles += c == cp ? TI * (TI + 1) : TI * TJ;
+      gp.tstart[np + 1] = tiles;
+      ++np;
+    }
+  }
+  gp.npairs = np;
+  gp.K = K;
+  gp.ldK = ldK;
+  const long long t0 = static_cast<long long>(tiles) * part / nparts;
+  const long long t1 = static_cast<long long>(tiles) * (part + 1) / nparts;
+  gp.tile0 = static_cast<int>(t0);
+  gp.dbg = getenv("DNGD_GOZ_DBG") ? atoi(getenv("DNGD_GOZ_DBG")) : 0;
+  if (t1 <= t0) return DNGD_OK;
+  const size_t smem = gram_oz_smem(slices);
+  auto kern = slices == 8 ? k_gram_oz<8> : k_gram_oz<7>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return cuda_status(ctx, e, "gram_oz smem attribute");
+  kern<<<static_cast<unsigned>(t1 - t0), OZ_THREADS, smem, s>>>(gp);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, kern);
+    return set_error(ctx, DNGD_ERR_CUDA,
+                     std::string("gram_oz: ") + cudaGetErrorString(e) + " (regs " +
+                         std::to_string(fa.numRegs) + ", max threads " +
+                         std::to_string(fa.maxThreadsPerBlock) + ", static smem " +
+                         std::to_string(fa.sharedSizeBytes) + ", dynamic " + std::to_string(smem) + ")");
+  }
+  return DNGD_OK;
 }
 
 // ------------------------------------------------------------------ K[:, I] without J

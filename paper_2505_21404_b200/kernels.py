@@ -186,6 +186,24 @@ def gemm_nt(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor | None = None, K: 
     return C
 
 
+def oz_gemm_nt(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor | None = None,
+               slices: int = 8) -> torch.Tensor:
+    """C = A B^T, emulated FP64 on the int8 tensor cores (Ozaki slices, ozaki.cu)."""
+    _check2d(A, "A")
+    _check2d(B, "B")
+    M, N, K = A.shape[0], B.shape[0], A.shape[1]
+    if B.shape[1] != K:
+        raise DimensionError("oz_gemm_nt: A and B need the same number of columns")
+    if C is None:
+        C = torch.empty((M, pad_ld(N, 2)), dtype=F64, device=A.device)[:, :N]
+    nb = c_size(0)
+    call("dngd_oz_gemm_workspace", ctx(), M, N, K, int(slices), ctypes.byref(nb))
+    ws = workspace("oz_gemm", nb.value)
+    call("dngd_oz_gemm_nt", ctx(), stream_handle(), M, N, K, ptr(A), A.stride(0), ptr(B),
+         B.stride(0), ptr(C), C.stride(0), int(slices), ptr(ws), ws.numel())
+    return C
+
+
 def dot(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     if out is None:
         out = torch.empty(1, dtype=F64, device=x.device)
@@ -264,8 +282,40 @@ def gram_factored(mlp, theta, classes_arr, nclass, r, K, ws, part=0, nparts=1):
              ws.numel())
 
 
-def gram_factored_act(mlp, classes_arr, nclass, K, act_ws, part=0, nparts=1):
-    """K (or part `part` of nparts of its tiles) from the activations in act_ws."""
+def gram_emulation_slices(mlp=None) -> int:
+    """Ozaki digit count of the factored Gram's G-space products (0 = FP64 DMMA).
+    DNGD_GRAM_SLICES (0, 7 or 8) overrides; by default layers 128 wide or more run
+    emulated with 7 digits (int8 tcgen05, ~2x the DMMA kernel at config 3, K within
+    5e-16 of it) and narrower nets stay on DMMA (the int8 tile's fixed costs win
+    nothing at K = 64)."""
+    import os
+
+    env = os.environ.get("DNGD_GRAM_SLICES")
+    if env is not None:
+        v = int(env)
+        if v not in (0, 7, 8):
+            raise DimensionError("DNGD_GRAM_SLICES must be 0, 7 or 8")
+        return v
+    if mlp is None:
+        return 7
+    hidden = [mlp.widths[k] for k in range(1, mlp.nlayers)]
+    return 7 if hidden and max(hidden) >= 128 else 0
+
+
+def gram_factored_act(mlp, classes_arr, nclass, K, act_ws, part=0, nparts=1, slices=None):
+    """K (or part `part` of nparts of its tiles) from the activations in act_ws: the
+    G-space products on the int8 tensor cores (Ozaki slices, gram_oz.cuh) unless
+    slices == 0, then on the FP64 DMMA pipe (gram_factored.cuh)."""
+    slices = gram_emulation_slices(mlp) if slices is None else int(slices)
+    if slices:
+        nb = c_size(0)
+        call("dngd_gram_oz_workspace", ctx(), ctypes.byref(mlp), classes_arr, nclass, slices,
+             ctypes.byref(nb))
+        ows = workspace("gram_oz", nb.value)
+        call("dngd_gram_oz_act", ctx(), stream_handle(), ctypes.byref(mlp), classes_arr, nclass,
+             ptr(K), K.stride(0), int(part), int(nparts), slices, ptr(act_ws), act_ws.numel(),
+             ptr(ows), ows.numel())
+        return
     call("dngd_gram_factored_act", ctx(), stream_handle(), ctypes.byref(mlp), classes_arr, nclass,
          ptr(K), K.stride(0), int(part), int(nparts), ptr(act_ws), act_ws.numel())
 

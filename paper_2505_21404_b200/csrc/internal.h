@@ -75,5 +75,11 @@ int oz_slice(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows, lon
 // the end read as zero digits
 int oz_encode(dngd_ctx* ctx, CUtensorMap* map, const int8_t* Q, long long rows, long long kpad,
               int slices, int box_rows);
+// C_z = A_z B_z^T (z < batch) over sliced operands: A_z rows z a_brows .. + M of the
+// a_rows-row digit planes QA (scales scA), likewise B; C_z = C + z sC (pitch ldc)
+int oz_gemm_batched(dngd_ctx* ctx, cudaStream_t s, const int8_t* QA, const double* scA,
+                    long long a_rows, long long a_brows, const int8_t* QB, const double* scB,
+                    long long b_rows, long long b_brows, long long kpad, int slices, long long M,
+                    long long N, int batch, double* C, long long ldc, long long sC);
 
 }  // namespace dngd

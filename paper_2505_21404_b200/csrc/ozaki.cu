@@ -115,7 +115,8 @@ template <int S, int STAGES>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
               const double* __restrict__ scA, const double* __restrict__ scB,
-              double* __restrict__ C, long long ldc, int M, int N, int nk) {
+              double* __restrict__ C, long long ldc, int M, int N, int nk, long long a_brows,
+              long long b_brows, long long sC) {
   extern __shared__ uint8_t oz_smem_raw[];
   uint8_t* smem = smem_align(oz_smem_raw, 1024);
   constexpr int ABYTES = S * OZ_BM * 32, STAGE = S * (OZ_BM + OZ_BN) * 32;
@@ -125,6 +126,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * OZ_BM, n0 = blockIdx.x * OZ_BN;
+  // batch z: A rows z a_brows + m, B rows z b_brows + n, C + z sC
+  const long long za = static_cast<long long>(blockIdx.z) * a_brows;
+  const long long zb = static_cast<long long>(blockIdx.z) * b_brows;
+  scA += za;
+  scB += zb;
+  C += static_cast<long long>(blockIdx.z) * sC;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
@@ -145,8 +152,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         if (kc >= STAGES) mbar_wait(&empty[st], ((kc / STAGES) - 1) & 1);
         uint8_t* sa = smem + st * STAGE;
         mbar_arrive_expect_tx(&full[st], STAGE);
-        tma_load_3d(sa, &mA, &full[st], kc * 32, m0, 0);
-        tma_load_3d(sa + ABYTES, &mB, &full[st], kc * 32, n0, 0);
+        tma_load_3d(sa, &mA, &full[st], kc * 32, static_cast<int>(za + m0), 0);
+        tma_load_3d(sa + ABYTES, &mB, &full[st], kc * 32, static_cast<int>(zb + n0), 0);
       }
     }
   } else if (warp == 1) {
@@ -201,17 +208,37 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 template <int S>
 static int oz_gemm_launch(dngd_ctx* ctx, cudaStream_t s, const CUtensorMap& mA,
                           const CUtensorMap& mB, const double* scA, const double* scB, double* C,
-                          long long ldc, long long M, long long N, int nk) {
+                          long long ldc, long long M, long long N, int nk, int batch,
+                          long long a_brows, long long b_brows, long long sC) {
   constexpr int STAGES = 3;
   const size_t smem = oz_smem_bytes(S, STAGES);
   auto kern = k_oz_gemm<S, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_status(ctx, e, "oz_gemm smem attribute");
-  dim3 grid(static_cast<unsigned>((N + OZ_BN - 1) / OZ_BN), static_cast<unsigned>((M + OZ_BM - 1) / OZ_BM));
+  dim3 grid(static_cast<unsigned>((N + OZ_BN - 1) / OZ_BN), static_cast<unsigned>((M + OZ_BM - 1) / OZ_BM),
+            static_cast<unsigned>(batch));
   kern<<<grid, OZ_THREADS, smem, s>>>(mA, mB, scA, scB, C, ldc, static_cast<int>(M),
-                                       static_cast<int>(N), nk);
+                                       static_cast<int>(N), nk, a_brows, b_brows, sC);
   return cuda_status(ctx, cudaGetLastError(), "oz_gemm");
+}
+
+int oz_gemm_batched(dngd_ctx* ctx, cudaStream_t s, const int8_t* QA, const double* scA,
+                    long long a_rows, long long a_brows, const int8_t* QB, const double* scB,
+                    long long b_rows, long long b_brows, long long kpad, int slices, long long M,
+                    long long N, int batch, double* C, long long ldc, long long sC) {
+  if (M <= 0 || N <= 0 || batch <= 0) return DNGD_OK;
+  CUtensorMap mA, mB;
+  int rc = oz_encode(ctx, &mA, QA, a_rows, kpad, slices, OZ_BM);
+  if (rc) return rc;
+  rc = oz_encode(ctx, &mB, QB, b_rows, kpad, slices, OZ_BN);
+  if (rc) return rc;
+  const int nk = static_cast<int>(kpad / 32);
+  switch (slices) {
+    case 6: return oz_gemm_launch<6>(ctx, s, mA, mB, scA, scB, C, ldc, M, N, nk, batch, a_brows, b_brows, sC);
+    case 7: return oz_gemm_launch<7>(ctx, s, mA, mB, scA, scB, C, ldc, M, N, nk, batch, a_brows, b_brows, sC);
+    default: return oz_gemm_launch<8>(ctx, s, mA, mB, scA, scB, C, ldc, M, N, nk, batch, a_brows, b_brows, sC);
+  }
 }
 
 }  // namespace dngd
@@ -252,15 +279,5 @@ extern "C" int dngd_oz_gemm_nt(dngd_ctx* ctx, void* stream, int64_t M, int64_t N
   if (rc) return rc;
   rc = oz_slice(ctx, s, B, N, K, ldb, slices, qb, sb);
   if (rc) return rc;
-  CUtensorMap mA, mB;
-  rc = oz_encode(ctx, &mA, qa, M, kp, slices, OZ_BM);
-  if (rc) return rc;
-  rc = oz_encode(ctx, &mB, qb, N, kp, slices, OZ_BN);
-  if (rc) return rc;
-  const int nk = static_cast<int>(kp / 32);
-  switch (slices) {
-    case 6: return oz_gemm_launch<6>(ctx, s, mA, mB, sa, sb, C, ldc, M, N, nk);
-    case 7: return oz_gemm_launch<7>(ctx, s, mA, mB, sa, sb, C, ldc, M, N, nk);
-    default: return oz_gemm_launch<8>(ctx, s, mA, mB, sa, sb, C, ldc, M, N, nk);
-  }
+  return oz_gemm_batched(ctx, s, qa, sa, M, 0, qb, sb, N, 0, kp, slices, M, N, 1, C, ldc, 0);
 }

@@ -1337,7 +1337,24 @@ struct LossBufs {
   double *thetas, *Hping, *Hpong, *Z, *r;
   std::vector<double*> Wt;
   BigIn big;
+  // emulated-FP64 hidden-layer GEMMs (ozaki.cu): digit planes of cb candidates
+  int oz_S = 0, oz_cb = 0;
+  int8_t *ozQA = nullptr, *ozQB = nullptr;
+  double *ozsA = nullptr, *ozsB = nullptr;
 };
+
+// Ozaki digits of the line-search forward's hidden-layer GEMMs: DNGD_LS_SLICES
+// (0, 7, 8) overrides; default 7 when a hidden layer is 128 wide or more (the
+// int8 tensor cores beat the FP64 DMMA GEMM there), else the DMMA GEMM
+static int oz_ls_slices(const Plan& P) {
+  if (const char* e = getenv("DNGD_LS_SLICES")) {
+    const int v = atoi(e);
+    return (v == 7 || v == 8) ? v : 0;
+  }
+  long long wmax = 0;
+  for (int k = 1; k <= P.L - 2; ++k) wmax = std::max(wmax, std::max(P.w[k], P.w[k + 1]));
+  return wmax >= 128 ? 7 : 0;
+}
 
 static void carve_loss(const Plan& P, Arena& A, LossBufs& B, int C) {
   B.thetas = A.take(static_cast<size_t>(C) * P.n);
@@ -1348,6 +1365,23 @@ static void carve_loss(const Plan& P, Arena& A, LossBufs& B, int C) {
   B.Wt.assign(P.L, nullptr);
   for (int k = 1; k <= P.L - 2; ++k) B.Wt[k] = A.take(static_cast<size_t>(C) * P.w[k + 1] * P.ld[k]);
   carve_bigin(P, A, B.big, true);
+  B.oz_S = P.L >= 3 ? oz_ls_slices(P) : 0;
+  if (B.oz_S) {
+    long long kp = 0, nmax = 0;
+    for (int k = 1; k <= P.L - 2; ++k) {
+      kp = std::max(kp, oz_kpad(P.w[k]));
+      nmax = std::max(nmax, P.w[k + 1]);
+    }
+    // candidates per slicing pass: A digit planes within ~2 GiB
+    const long long per = static_cast<long long>(B.oz_S) * P.R * kp;
+    B.oz_cb = static_cast<int>(std::max(1LL, std::min<long long>(C, (2LL << 30) / std::max(per, 1LL))));
+    const size_t qa = static_cast<size_t>(per) * B.oz_cb;
+    const size_t qb = static_cast<size_t>(B.oz_S) * nmax * kp * B.oz_cb;
+    B.ozQA = reinterpret_cast<int8_t*>(A.take((qa + 7) / 8));
+    B.ozQB = reinterpret_cast<int8_t*>(A.take((qb + 7) / 8));
+    B.ozsA = A.take(static_cast<size_t>(P.R) * B.oz_cb);
+    B.ozsB = A.take(static_cast<size_t>(nmax) * B.oz_cb);
+  }
 }
 
 static inline unsigned nblk(long long n, int t = 256) {
@@ -1455,7 +1489,24 @@ static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const d
     g.ldc = P.ldmax;
     g.sC = act_s;
     g.batch = C;
-    int rc = gemm_nt(ctx, s, g);
+    int rc = DNGD_OK;
+    if (B.oz_S) {
+      // emulated FP64 on the int8 tensor cores, oz_cb candidates per slicing pass
+      const long long N = P.w[k + 1], Kd = P.w[k];
+      for (int b0 = 0; b0 < C && rc == DNGD_OK; b0 += B.oz_cb) {
+        const int nb = std::min(B.oz_cb, C - b0);
+        rc = oz_slice(ctx, s, Hcur + b0 * act_s, nb * P.R, Kd, P.ldmax, B.oz_S, B.ozQA, B.ozsA);
+        if (rc == DNGD_OK) {
+          rc = oz_slice(ctx, s, B.Wt[k] + b0 * g.sB, nb * N, Kd, P.ld[k], B.oz_S, B.ozQB, B.ozsB);
+        }
+        if (rc == DNGD_OK) {
+          rc = oz_gemm_batched(ctx, s, B.ozQA, B.ozsA, nb * P.R, P.R, B.ozQB, B.ozsB, nb * N, N,
+                               oz_kpad(Kd), B.oz_S, P.R, N, nb, B.Z + b0 * act_s, P.ldmax, act_s);
+        }
+      }
+    } else {
+      rc = gemm_nt(ctx, s, g);
+    }
     if (rc) return rc;
     dim3 gr(nblk(P.m * P.w[k + 1]), C);
     k_tanh_fwd<<<gr, 256, 0, s>>>(P.T, B.Z, Hnext, static_cast<int>(P.w[k + 1]), P.ldmax,

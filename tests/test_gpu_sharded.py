@@ -138,15 +138,19 @@ def _sharded_trace(P, comm, layout, pname, widths, counts, cfg, seed=3, steps=3)
     ("columns", "poisson2d", (2, 32, 32, 1), (300, 60),
      dict(lam_cap=1e-3, dense_threshold=100, nystrom_rank=24, cg_max_iters=100, cg_tol=1e-13)),
 ])
-def test_sharded_run_two_thread_ranks_match_one(P, layout, pname, widths, counts, cfg):
+def test_sharded_run_two_thread_ranks_match_one(P, layout, pname, widths, counts, cfg, monkeypatch):
     """The whole sharded loop at world 2 (two thread-ranks on this GPU, host-barrier
-    collectives) against world 1 and against the single-GPU dngd_run."""
+    collectives) against world 1 and against the single-GPU dngd_run (on the same
+    Gram kernel: the tile layout is J-free, so the reference is held to the factored
+    Gram rather than the size heuristic's materialised SYRK)."""
     from paper_2505_21404_b200.sharded import LocalComm
     from tests.gpu_util import run_ranks
 
     one = _sharded_trace(P, LocalComm(), layout, pname, widths, counts, cfg)
     two = run_ranks(2, lambda comm: _sharded_trace(P, comm, layout, pname, widths, counts, cfg))
     config = P.OptimizerConfig(max_iters=3, deterministic_timing=True, **cfg)
+    if layout == "tiles":
+        monkeypatch.setattr(P.PinnResidualMap, "gram_mode", "factored")
     ref = P.dngd_run(P.make_problem(pname), P.MlpSpec(widths), config, 3, counts=counts,
                      init="xavier_normal", track_rel_l2=False)
     ref_loss = [r.loss for r in ref.rows]
@@ -156,5 +160,7 @@ def test_sharded_run_two_thread_ranks_match_one(P, layout, pname, widths, counts
         assert _rel(res[2], one[2]) <= 1e-7
         assert max(abs(a - b) for a, b in zip(res[3], one[3])) <= 1
     np.testing.assert_array_equal(two[0][2], two[1][2])  # replicated theta on every rank
-    np.testing.assert_allclose(one[0], ref_loss, rtol=1e-8)
+    # different reduction orders (J_p^T w by column ranges, f_vv by point rows):
+    # held to 10x inside the north star's trajectory tolerance (1e-6 over 20 steps)
+    np.testing.assert_allclose(one[0], ref_loss, rtol=1e-7)
     assert _rel(one[2], ref.final_theta.data) <= 1e-7

@@ -15,7 +15,7 @@ inline long long oz_kpad(long long K) { return (K + 31) / 32 * 32; }
 // ring of STAGES K-chunks (32 int8 of every slice of a 128-row and a 64-row tile)
 // + mbarriers + the TMEM address, after 1024-byte alignment of the base
 inline size_t oz_smem_bytes(int S, int stages) {
-  return 1024 + static_cast<size_t>(stages) * S * (OZ_BM + OZ_BN) * 32 + (2 * stages + 2) * 8 + 16;
+  return 1024 + static_cast<size_t>(stages) * S * (OZ_BM + OZ_BN) * 32 + (2 * stages + 3) * 8 + 16;
 }
 
 }  // namespace dngd

@@ -111,33 +111,36 @@ int oz_encode(dngd_ctx* ctx, CUtensorMap* map, const int8_t* Q, long long rows, 
   return r == CUDA_SUCCESS ? DNGD_OK : set_error(ctx, DNGD_ERR_CUDA, "oz: tensor map encode failed");
 }
 
+// Persistent: one CTA per SM walks tiles (z, m-tile, n-tile), n fastest (the CTAs
+// in flight share the 128-row A tile through L2).  Warp 0 streams K-chunks of
+// consecutive tiles through the ring without waiting for epilogues; warp 1 issues
+// a tile's MMAs once the epilogue has drained the previous tile's accumulators;
+// warps 2-9 drain TMEM (fold -> FP64 in registers), release it, then scale and
+// store while the next tile's MMAs run.
 template <int S, int STAGES>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
               const double* __restrict__ scA, const double* __restrict__ scB,
               double* __restrict__ C, long long ldc, int M, int N, int nk, long long a_brows,
-              long long b_brows, long long sC) {
+              long long b_brows, long long sC, int batch) {
   extern __shared__ uint8_t oz_smem_raw[];
   uint8_t* smem = smem_align(oz_smem_raw, 1024);
   constexpr int ABYTES = S * OZ_BM * 32, STAGE = S * (OZ_BM + OZ_BN) * 32;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tempty = tfull + 1;
+  uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tempty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * OZ_BM, n0 = blockIdx.x * OZ_BN;
-  // batch z: A rows z a_brows + m, B rows z b_brows + n, C + z sC
-  const long long za = static_cast<long long>(blockIdx.z) * a_brows;
-  const long long zb = static_cast<long long>(blockIdx.z) * b_brows;
-  scA += za;
-  scB += zb;
-  C += static_cast<long long>(blockIdx.z) * sC;
+  const int tn = (N + OZ_BN - 1) / OZ_BN, tm = (M + OZ_BM - 1) / OZ_BM;
+  const int ntiles = tn * tm * batch;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     mbar_init(tfull, 1);
+    mbar_init(tempty, 8);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(taddr_sh, 512);
@@ -145,54 +148,94 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *taddr_sh;
+  auto decode = [&](int tile, int& z, int& m0, int& n0) {
+    z = tile / (tn * tm);
+    const int r = tile - z * tn * tm;
+    m0 = (r / tn) * OZ_BM;
+    n0 = (r - (r / tn) * tn) * OZ_BN;
+  };
   if (warp == 0) {
     if (lane == 0) {
-      for (int kc = 0; kc < nk; ++kc) {
-        const int st = kc % STAGES;
-        if (kc >= STAGES) mbar_wait(&empty[st], ((kc / STAGES) - 1) & 1);
-        uint8_t* sa = smem + st * STAGE;
-        mbar_arrive_expect_tx(&full[st], STAGE);
-        tma_load_3d(sa, &mA, &full[st], kc * 32, static_cast<int>(za + m0), 0);
-        tma_load_3d(sa + ABYTES, &mB, &full[st], kc * 32, static_cast<int>(zb + n0), 0);
+      int f = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int z, m0, n0;
+        decode(tile, z, m0, n0);
+        const int ar = static_cast<int>(z * a_brows + m0), br = static_cast<int>(z * b_brows + n0);
+        for (int kc = 0; kc < nk; ++kc, ++f) {
+          const int st = f % STAGES;
+          if (f >= STAGES) mbar_wait(&empty[st], ((f / STAGES) - 1) & 1);
+          uint8_t* sa = smem + st * STAGE;
+          mbar_arrive_expect_tx(&full[st], STAGE);
+          tma_load_3d(sa, &mA, &full[st], kc * 32, ar, 0);
+          tma_load_3d(sa + ABYTES, &mB, &full[st], kc * 32, br, 0);
+        }
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = umma_idesc_s8(OZ_BM, OZ_BN);
-    for (int kc = 0; kc < nk; ++kc) {
-      const int st = kc % STAGES;
-      mbar_wait(&full[st], (kc / STAGES) & 1);
+    int f = 0, it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      if (it > 0) mbar_wait(tempty, (it - 1) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t a0 = smem_u32(smem + st * STAGE);
-        oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, kc == 0);
-        umma_commit(&empty[st]);
+      for (int kc = 0; kc < nk; ++kc, ++f) {
+        const int st = f % STAGES;
+        mbar_wait(&full[st], (f / STAGES) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(smem + st * STAGE);
+          oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, kc == 0);
+          umma_commit(&empty[st]);
+          if (kc == nk - 1) umma_commit(tfull);
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
-    if (lane == 0) umma_commit(tfull);
-    __syncwarp();
   } else {
-    mbar_wait(tfull, 0);
-    tc_fence_after();
     const int q = warp & 3, h = (warp - 2) >> 2;
     const int row = 32 * q + lane;
-    const double sa = m0 + row < M ? scA[m0 + row] : 0.0;
-#pragma unroll 1
-    for (int c = 0; c < OZ_BN / 2 / 8; ++c) {
-      const int col0 = h * (OZ_BN / 2) + 8 * c;
-      int32_t acc[S][8];
+    const uint32_t tl = tbase + (static_cast<uint32_t>(32 * q) << 16);
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      int z, m0, n0;
+      decode(tile, z, m0, n0);
+      const double* sa_z = scA + z * a_brows;
+      const double* sb_z = scB + z * b_brows;
+      const double sa = m0 + row < M ? sa_z[m0 + row] : 0.0;
+      const int cl = n0 + h * (OZ_BN / 2) + lane;
+      const double scl = cl < N ? sb_z[cl] : 0.0;
+      double v[OZ_BN / 2];
+      mbar_wait(tfull, it & 1);
+      tc_fence_after();
 #pragma unroll
-      for (int d = 0; d < S; ++d) tmem_ld8(tbase + (static_cast<uint32_t>(32 * q) << 16) + d * OZ_BN + col0, acc[d]);
-      tmem_ld_wait();
-      if (m0 + row < M) {
+      for (int c = 0; c < OZ_BN / 2 / 8; ++c) {
+        int32_t acc[S][8];
+#pragma unroll
+        for (int d = 0; d < S; ++d) tmem_ld8(tl + d * OZ_BN + h * (OZ_BN / 2) + 8 * c, acc[d]);
+        tmem_ld_wait();
+        if (c == OZ_BN / 2 / 8 - 1) {  // all diagonals in registers: release TMEM
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty);
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int col = n0 + col0 + j;
-          if (col >= N) continue;
           int32_t a[S];
 #pragma unroll
           for (int d = 0; d < S; ++d) a[d] = acc[d][j];
-          C[static_cast<long long>(m0 + row) * ldc + col] = oz_combine<S>(a) * (sa * scB[col]);
+          v[8 * c + j] = oz_combine<S>(a) * (sa * __shfl_sync(0xffffffffu, scl, 8 * c + j));
+        }
+      }
+      if (m0 + row < M) {
+        double* crow = C + z * sC + static_cast<long long>(m0 + row) * ldc + n0 + h * (OZ_BN / 2);
+        const int nvalid = N - (n0 + h * (OZ_BN / 2));
+        if (nvalid >= OZ_BN / 2 && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
+#pragma unroll
+          for (int j = 0; j < OZ_BN / 2; j += 2)
+            *reinterpret_cast<double2*>(crow + j) = make_double2(v[j], v[j + 1]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < OZ_BN / 2; ++j)
+            if (j < nvalid) crow[j] = v[j];
         }
       }
     }
@@ -216,10 +259,11 @@ static int oz_gemm_launch(dngd_ctx* ctx, cudaStream_t s, const CUtensorMap& mA,
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_status(ctx, e, "oz_gemm smem attribute");
-  dim3 grid(static_cast<unsigned>((N + OZ_BN - 1) / OZ_BN), static_cast<unsigned>((M + OZ_BM - 1) / OZ_BM),
-            static_cast<unsigned>(batch));
+  const long long tiles = ((N + OZ_BN - 1) / OZ_BN) * ((M + OZ_BM - 1) / OZ_BM) * batch;
+  if (tiles >= (1LL << 31)) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm: too many tiles");
+  const unsigned grid = static_cast<unsigned>(std::min<long long>(tiles, ctx->num_sms));
   kern<<<grid, OZ_THREADS, smem, s>>>(mA, mB, scA, scB, C, ldc, static_cast<int>(M),
-                                       static_cast<int>(N), nk, a_brows, b_brows, sC);
+                                      static_cast<int>(N), nk, a_brows, b_brows, sC, batch);
   return cuda_status(ctx, cudaGetLastError(), "oz_gemm");
 }
 

@@ -1275,6 +1275,64 @@ static void carve_bigin(const Plan& P, Arena& A, BigIn& G, bool dir) {
   if (dir) G.Dx = A.take(static_cast<size_t>(P.m) * P.ld[1]);
 }
 
+// Ozaki digits of the hidden-layer GEMMs (activation pass, f_vv, line-search
+// forward): DNGD_GEMM_SLICES (0, 7, 8) overrides; default 7 when a hidden layer is
+// 128 wide or more (the int8 tensor cores beat the FP64 DMMA GEMM there), else the
+// DMMA GEMM
+static int oz_ls_slices(const Plan& P) {
+  if (const char* e = getenv("DNGD_GEMM_SLICES")) {
+    const int v = atoi(e);
+    return (v == 7 || v == 8) ? v : 0;
+  }
+  if (P.L < 3) return 0;
+  long long wmax = 0;
+  for (int k = 1; k <= P.L - 2; ++k) wmax = std::max(wmax, std::max(P.w[k], P.w[k + 1]));
+  return wmax >= 128 ? 7 : 0;
+}
+
+// digit planes for one emulated GEMM of up to rows_a x K by rows_b x K
+struct OzScratch {
+  int S = 0;
+  long long cap_a = 0, cap_b = 0, kcap = 0;
+  int8_t *QA = nullptr, *QB = nullptr;
+  double *sA = nullptr, *sB = nullptr;
+};
+
+static void carve_oz(const Plan& P, Arena& A, OzScratch& O, long long rows_a, long long rows_b,
+                     long long kmax) {
+  O.S = oz_ls_slices(P);
+  if (!O.S) return;
+  O.cap_a = rows_a;
+  O.cap_b = rows_b;
+  O.kcap = oz_kpad(kmax);
+  O.QA = reinterpret_cast<int8_t*>(A.take((static_cast<size_t>(O.S) * rows_a * O.kcap + 7) / 8));
+  O.QB = reinterpret_cast<int8_t*>(A.take((static_cast<size_t>(O.S) * rows_b * O.kcap + 7) / 8));
+  O.sA = A.take(static_cast<size_t>(rows_a));
+  O.sB = A.take(static_cast<size_t>(rows_b));
+}
+
+static long long hidden_wmax(const Plan& P) {
+  long long w = 1;
+  for (int k = 1; k <= P.L - 1; ++k) w = std::max(w, P.w[k]);
+  return w;
+}
+
+// C = A B^T (alpha 1, beta 0, one batch) on the int8 tensor cores when the
+// scratch allows it, else the FP64 DMMA GEMM
+static int gemm_nt_hidden(dngd_ctx* ctx, cudaStream_t s, const GemmCall& g, const OzScratch& O) {
+  if (!O.S || g.batch != 1 || g.alpha != 1.0 || g.beta != 0.0 || g.lower || g.M > O.cap_a ||
+      g.N > O.cap_b || oz_kpad(g.K) > O.kcap || g.K < 64) {
+    return gemm_nt(ctx, s, g);
+  }
+  int rc = oz_slice(ctx, s, g.A, g.M, g.K, g.lda, O.S, O.QA, O.sA);
+  if (rc == DNGD_OK) rc = oz_slice(ctx, s, g.B, g.N, g.K, g.ldb, O.S, O.QB, O.sB);
+  if (rc == DNGD_OK) {
+    rc = oz_gemm_batched(ctx, s, O.QA, O.sA, g.M, 0, O.QB, O.sB, g.N, 0, oz_kpad(g.K), O.S, g.M,
+                         g.N, 1, g.C, g.ldc, 0);
+  }
+  return rc;
+}
+
 struct AsmBufs {
   std::vector<double*> Z, H, Zb, Wt, Wp;
   BigIn big;
@@ -1283,6 +1341,7 @@ struct AsmBufs {
   double* u0;  // per-point network value (cubic-term adjoint seeds), m
   // wide input layer: hidden/output columns of J, SYRK partials, X X^T (+ partials)
   double *Jh = nullptr, *syrk_work = nullptr, *XX = nullptr, *xx_part = nullptr;
+  OzScratch oz;  // emulated hidden-layer GEMMs of the activation pass (carved last)
 };
 
 static void carve_assemble(const Plan& P, Arena& A, AsmBufs& B) {
@@ -1309,12 +1368,14 @@ static void carve_assemble(const Plan& P, Arena& A, AsmBufs& B) {
     B.XX = A.take(static_cast<size_t>(P.m) * P.wi_ldxx);
     if (P.wi_xx_part) B.xx_part = A.take(P.wi_xx_part / sizeof(double));
   }
+  carve_oz(P, A, B.oz, P.R, hidden_wmax(P), hidden_wmax(P));
 }
 
 struct FvvBufs {
   std::vector<double*> H3, Wt, Vt;
   double *P3, *Q2;
   BigIn big;
+  OzScratch oz;
 };
 
 static void carve_fvv(const Plan& P, Arena& A, FvvBufs& B) {
@@ -1331,6 +1392,7 @@ static void carve_fvv(const Plan& P, Arena& A, FvvBufs& B) {
     B.Vt[k] = A.take(P.w[k + 1] * P.ld[k]);
   }
   carve_bigin(P, A, B.big, true);
+  carve_oz(P, A, B.oz, 3 * P.R, hidden_wmax(P), hidden_wmax(P));
 }
 
 struct LossBufs {
@@ -1342,19 +1404,6 @@ struct LossBufs {
   int8_t *ozQA = nullptr, *ozQB = nullptr;
   double *ozsA = nullptr, *ozsB = nullptr;
 };
-
-// Ozaki digits of the line-search forward's hidden-layer GEMMs: DNGD_LS_SLICES
-// (0, 7, 8) overrides; default 7 when a hidden layer is 128 wide or more (the
-// int8 tensor cores beat the FP64 DMMA GEMM there), else the DMMA GEMM
-static int oz_ls_slices(const Plan& P) {
-  if (const char* e = getenv("DNGD_LS_SLICES")) {
-    const int v = atoi(e);
-    return (v == 7 || v == 8) ? v : 0;
-  }
-  long long wmax = 0;
-  for (int k = 1; k <= P.L - 2; ++k) wmax = std::max(wmax, std::max(P.w[k], P.w[k + 1]));
-  return wmax >= 128 ? 7 : 0;
-}
 
 static void carve_loss(const Plan& P, Arena& A, LossBufs& B, int C) {
   B.thetas = A.take(static_cast<size_t>(C) * P.n);
@@ -2096,7 +2145,7 @@ static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& 
     g.ldb = P.ld[k];
     g.C = B.Z[k];
     g.ldc = P.ld[k + 1];
-    rc = gemm_nt(ctx, s, g);
+    rc = gemm_nt_hidden(ctx, s, g, B.oz);
     if (rc) return rc;
     k_tanh_fwd<<<nblk(P.m * P.w[k + 1]), 256, 0, s>>>(P.T, B.Z[k], B.H[k + 1],
                                                       static_cast<int>(P.w[k + 1]), P.ld[k + 1],
@@ -2175,7 +2224,7 @@ static int assemble_impl(dngd_ctx* ctx, cudaStream_t s, const Plan& P, AsmBufs& 
       g.ldb = P.ld[k + 1];
       g.C = B.Hb;
       g.ldc = P.ld[k];
-      rc = gemm_nt(ctx, s, g);
+      rc = gemm_nt_hidden(ctx, s, g, B.oz);
       if (rc) return rc;
     }
   }
@@ -2804,12 +2853,12 @@ static int fvv_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const
     g.ldb = P.ld[k];
     g.C = B.P3;
     g.ldc = ld;
-    rc = gemm_nt(ctx, s, g);
+    rc = gemm_nt_hidden(ctx, s, g, B.oz);
     if (rc) return rc;
     g.M = (order == 1 ? 1 : 2) * P.R;
     g.B = B.Vt[k];
     g.C = B.Q2;
-    rc = gemm_nt(ctx, s, g);
+    rc = gemm_nt_hidden(ctx, s, g, B.oz);
     if (rc) return rc;
     const long long boff = P.off[k] + P.w[k] * P.w[k + 1];
     k_fvv_hidden<<<nblk(P.m * P.w[k + 1]), 256, 0, s>>>(P.T, B.P3, B.Q2, theta + boff, v + boff,

@@ -214,6 +214,45 @@ def _count_our_kernels(fn):
     return n
 
 
+# tcgen05 kind::i8 dense MMA rate measured on this pool's B200 by tools/micro/umma_rate.cu
+# (M = 128, N >= 128, operands resident in shared memory, all 148 SMs): the int8
+# tensor peak the emulated-FP64 kernels run against.  At N = 64 -- the widest tile
+# TMEM allows with 7-8 diagonal accumulators -- the same benchmark floors at ~44.6
+# cycles per MMA, i.e. 3.2 POPS.
+INT8_PEAK_TOPS = 4498.0
+INT8_N64_FLOOR_TOPS = 3207.0
+INT8_PEAK_SOURCE = ("tcgen05.mma kind::i8 M=128 N=128 K=32 issue rate measured by "
+                    "tools/micro/umma_rate.cu (4498 TOPS; 4549 at N=256)")
+
+
+def _emulated_gram(rmap):
+    """(issued int8 ops, useful int8 ops, slices) of one emulated factored-Gram launch,
+    or None when the Gram runs on the FP64 DMMA kernel (kernels.gram_emulation_slices)."""
+    from paper_2505_21404_b200 import kernels as K
+
+    mlp = rmap._device()["mlp"]
+    S = K.gram_emulation_slices(mlp)
+    if not S:
+        return None
+    widths = [mlp.widths[k] for k in range(mlp.nlayers + 1)]
+    L = mlp.nlayers
+    kp = lambda k: (k + 31) // 32 * 32  # noqa: E731
+    chunks = sum(kp(widths[0] if k == 0 else widths[k]) // 32 for k in range(L))
+    chunks += sum(kp(widths[k + 1]) // 32 for k in range(L - 1))
+    cls = [(c.count, rmap._nch(c)) for c in rmap.collocation.classes]
+    tiles = 0
+    for a in range(len(cls)):
+        for b in range(a + 1):
+            ppa, ppb = 64 // cls[a][1], 64 // cls[b][1]
+            TI = -(-cls[a][0] // (2 * ppa))
+            TJ = -(-cls[b][0] // ppb)
+            tiles += TI * (TI + 1) if a == b else TI * TJ
+    per_chunk = S * (S + 1) // 2 * 2.0 * 128 * 64 * 32
+    ops = tiles * chunks * per_chunk
+    useful = S * (S + 1) // 2 * rmap.factored_gram_flops()
+    return ops, useful, S
+
+
 def _profiled_traffic(workload, kernel):
     """DRAM bytes per launch of the roofline kernel from the committed ncu capture
     (profiles/<round>/traffic.json), or None when this kernel/workload has none."""
@@ -531,6 +570,27 @@ def run_ours(args, cfg):
         flops = maps[0].factored_gram_flops()
         flops_x = maps[0].factored_gram_flops(executed=True)
         ach = flops / gk_avg / 1e12
+        emu = _emulated_gram(maps[0])
+        if emu is not None:
+            ops, useful_ops, slices = emu
+            roof = {"kernel": f"dngd::k_gram_oz<{slices}> (factored Gram, emulated FP64: "
+                              f"{slices} int8 Ozaki digits per activation row, tcgen05 kind::i8)",
+                    "bound": "tensor", "achieved": ops / gk_avg / 1e12, "peak": INT8_PEAK_TOPS,
+                    "unit": "TOPS (int8)", "frac": ops / gk_avg / 1e12 / INT8_PEAK_TOPS,
+                    "traffic": None,
+                    "peak_source": INT8_PEAK_SOURCE,
+                    "algorithmic": f"{ops:.4e} int8 ops issued per launch = S(S+1)/2 digit "
+                                   "products x 2 x 128 x 64 x 32 per K-chunk x chunks x tiles "
+                                   f"({useful_ops:.4e} on useful rows = {slices * (slices + 1) // 2}"
+                                   f" x the {flops:.4e} useful FP64 FLOP)",
+                    "useful_frac": useful_ops / gk_avg / 1e12 / INT8_PEAK_TOPS,
+                    "kernel_ms": gk_avg * 1e3,
+                    "fp64_equivalent_tflops": ach,
+                    "fp64_equivalent_frac_of_dmma_peak": ach / fp64_peak,
+                    "n64_mma_floor_tops": INT8_N64_FLOOR_TOPS}
+        else:
+            roof = None
+    if gk_avg > 0 and roof is None:
         roof = {"kernel": "dngd::k_gram_factored (K = sum_k S (G^H_k o G^Z_k) S^T, J-free)",
                 "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": ach / fp64_peak, "traffic": None,

@@ -29,8 +29,8 @@
 namespace dngd {
 
 // One warp per row: max |x| (non-finite flagged), scale 2^e with
-// max 2^-e 128 < 127.5, then S exact remainder digits per entry
-// (y *= 128; d = rint(y); y -= d), written as 4-digit words per slice.
+// max 2^-e 128 < 127, then S digits per entry (oz_digits4), written as
+// 4-digit words per slice.
 template <int S>
 __global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ X, long long rows,
                                                   long long K, long long ld, long long kpad,
@@ -40,42 +40,48 @@ __global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ X, 
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
   const double* x = X + row * ld;
+  // 4 consecutive entries per lane and word (two 16-byte loads when aligned)
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  auto load4 = [&](long long w, double (&v)[4]) {
+    const long long k0 = 4 * w;
+    if (vec && k0 + 3 < K) {
+      const double2 a = *reinterpret_cast<const double2*>(x + k0);
+      const double2 b = *reinterpret_cast<const double2*>(x + k0 + 2);
+      v[0] = a.x;
+      v[1] = a.y;
+      v[2] = b.x;
+      v[3] = b.y;
+    } else {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) v[b] = k0 + b < K ? x[k0 + b] : 0.0;
+    }
+  };
+  const long long words = kpad / 4;
   double mx = 0.0;
   bool bad = false;
-  for (long long k = lane; k < K; k += 32) {
-    const double v = x[k];
-    bad |= !isfinite(v);
-    mx = fmax(mx, fabs(v));
+  for (long long w = lane; w < words; w += 32) {
+    double v[4];
+    load4(w, v);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      bad |= !isfinite(v[b]);
+      mx = fmax(mx, fabs(v[b]));
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     bad |= __shfl_xor_sync(0xffffffffu, bad ? 1 : 0, o) != 0;
   }
-  int e = 0;
-  if (mx > 0.0 && !bad) {
-    const double f = frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)
-    if (f * 128.0 >= 127.5) ++e;     // first digit stays within int8
-  }
+  const int e = bad ? 0 : oz_row_exponent(mx);
   if (lane == 0) scale[row] = bad ? CUDART_NAN : ldexp(1.0, e);
-  const long long words = kpad / 4;
+  const double sinv = ldexp(1.0, 7 * S - e);
   const size_t plane = static_cast<size_t>(rows) * kpad;
   for (long long w = lane; w < words; w += 32) {
+    double v[4];
+    load4(w, v);
     uint32_t packed[S];
-#pragma unroll
-    for (int t = 0; t < S; ++t) packed[t] = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const long long k = 4 * w + b;
-      double y = (k < K && !bad) ? ldexp(x[k], -e) : 0.0;
-#pragma unroll
-      for (int t = 0; t < S; ++t) {
-        y *= 128.0;
-        const double d = rint(y);
-        y -= d;
-        packed[t] |= (static_cast<uint32_t>(static_cast<int>(d)) & 0xffu) << (8 * b);
-      }
-    }
+    oz_digits4<S>(v, sinv, bad, packed);
 #pragma unroll
     for (int t = 0; t < S; ++t)
       reinterpret_cast<uint32_t*>(Q + t * plane + row * kpad)[w] = packed[t];
@@ -129,8 +135,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tempty = tfull + 1;  // [S]: per-diagonal release
+  uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tempty + S);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tn = (N + OZ_BN - 1) / OZ_BN, tm = (M + OZ_BM - 1) / OZ_BM;
   const int ntiles = tn * tm * batch;
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       mbar_init(&empty[i], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 8);
+    for (int d = 0; d < S; ++d) mbar_init(&tempty[d], 8);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(taddr_sh, 512);
@@ -175,15 +181,18 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     constexpr uint32_t idesc = umma_idesc_s8(OZ_BM, OZ_BN);
     int f = 0, it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      if (it > 0) mbar_wait(tempty, (it - 1) & 1);
-      tc_fence_after();
       for (int kc = 0; kc < nk; ++kc, ++f) {
         const int st = f % STAGES;
         mbar_wait(&full[st], (f / STAGES) & 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a0 = smem_u32(smem + st * STAGE);
-          oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, kc == 0);
+          if (kc == 0) {
+            oz_issue_first_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc,
+                                    tempty, it > 0 ? ((it - 1) & 1) : -1);
+          } else {
+            oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, false);
+          }
           umma_commit(&empty[st]);
           if (kc == nk - 1) umma_commit(tfull);
         }
@@ -206,25 +215,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       double v[OZ_BN / 2];
       mbar_wait(tfull, it & 1);
       tc_fence_after();
+      oz_drain32<S>(tl, OZ_BN, h * (OZ_BN / 2), tempty, v);
 #pragma unroll
-      for (int c = 0; c < OZ_BN / 2 / 8; ++c) {
-        int32_t acc[S][8];
-#pragma unroll
-        for (int d = 0; d < S; ++d) tmem_ld8(tl + d * OZ_BN + h * (OZ_BN / 2) + 8 * c, acc[d]);
-        tmem_ld_wait();
-        if (c == OZ_BN / 2 / 8 - 1) {  // all diagonals in registers: release TMEM
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(tempty);
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          int32_t a[S];
-#pragma unroll
-          for (int d = 0; d < S; ++d) a[d] = acc[d][j];
-          v[8 * c + j] = oz_combine<S>(a) * (sa * __shfl_sync(0xffffffffu, scl, 8 * c + j));
-        }
-      }
+      for (int j = 0; j < OZ_BN / 2; ++j) v[j] *= sa * __shfl_sync(0xffffffffu, scl, j);
       if (m0 + row < M) {
         double* crow = C + z * sC + static_cast<long long>(m0 + row) * ldc + n0 + h * (OZ_BN / 2);
         const int nvalid = N - (n0 + h * (OZ_BN / 2));

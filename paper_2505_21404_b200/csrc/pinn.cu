@@ -22,6 +22,8 @@
 #include <cmath>
 #include <vector>
 
+#include <math_constants.h>
+
 #include "common.cuh"
 #include "internal.h"
 #include "oz_common.cuh"
@@ -201,6 +203,115 @@ __global__ void k_tanh_fwd(Classes T, double* __restrict__ Z, double* __restrict
       G = fma(dz, dz, G);
     }
     H[base + (C.nch - 1) * ld] = s * Z[base + (C.nch - 1) * ld] - 2.0 * t * s * G;
+  }
+}
+
+// k_tanh_fwd fused with the Ozaki slicing of its output (line-search forward):
+// one CTA per (point, candidate), thread g owns neurons 4g..4g+3 of every channel
+// row; the channel map is k_tanh_fwd's, each row's scale and digits follow
+// k_oz_slice exactly (same scale rule, same digits), and H itself never reaches
+// HBM -- only the next GEMM's digit planes (rows cand R + act row) and scales.
+constexpr int kTsMaxCh = 8;
+template <int S, int NCH>
+__global__ void k_tanh_slice(Classes T, int cls, const double* __restrict__ Z, int w, long long ld,
+                             const double* __restrict__ bias, long long bias_s, long long act_s,
+                             long long R, long long kpad, int8_t* __restrict__ Q,
+                             double* __restrict__ scale) {
+  __shared__ double red[NCH][32];
+  __shared__ int redbad[NCH][32];
+  const ClassDev& C = T.c[cls];
+  const long long i = blockIdx.x;
+  const int cand = blockIdx.y;
+  const double* z0 = Z + cand * act_s + (C.act0 + i * NCH) * ld;
+  const double* bs = bias + cand * bias_s;
+  const long long row0 = cand * R + C.act0 + i * NCH;
+  const int g = threadIdx.x, lane = g & 31, wp = g >> 5;
+  const int q0 = 4 * g;
+  double v[NCH][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int q = q0 + j;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) v[ch][j] = 0.0;
+    if (q < w) {
+      const double z = z0[q] + bs[q];
+      const double t = tanh(z), sd = 1.0 - t * t;
+      v[0][j] = t;
+#pragma unroll
+      for (int gi = 0; gi < NCH - 1; ++gi)
+        if (gi < C.ngrad) v[1 + gi][j] = sd * z0[(1 + gi) * ld + q];
+      if (NCH > 1 && C.nlap) {
+        double G = 0.0;
+        for (int l = 0; l < C.nlap; ++l) {
+          const double dz = z0[C.lap_ch[l] * ld + q];
+          G = fma(dz, dz, G);
+        }
+        v[NCH - 1][j] = sd * z0[(NCH - 1) * ld + q] - 2.0 * t * sd * G;
+      }
+    }
+  }
+  // per channel row: max |v| and non-finite flag over the block
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    double mx = 0.0;
+    int bad = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      bad |= !isfinite(v[ch][j]);
+      mx = fmax(mx, fabs(v[ch][j]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if (lane == 0) {
+      red[ch][wp] = mx;
+      redbad[ch][wp] = bad;
+    }
+  }
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  const size_t plane = static_cast<size_t>(gridDim.y) * R * kpad;
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    double mx = 0.0;
+    int bad = 0;
+    for (int k = 0; k < nw; ++k) {
+      mx = fmax(mx, red[ch][k]);
+      bad |= redbad[ch][k];
+    }
+    const int e = bad ? 0 : oz_row_exponent(mx);
+    if (g == 0) scale[row0 + ch] = bad ? CUDART_NAN : ldexp(1.0, e);
+    if (q0 < kpad) {
+      uint32_t packed[S];
+      oz_digits4<S>(v[ch], ldexp(1.0, 7 * S - e), bad != 0, packed);
+#pragma unroll
+      for (int t = 0; t < S; ++t)
+        reinterpret_cast<uint32_t*>(Q + t * plane + (row0 + ch) * kpad)[g] = packed[t];
+    }
+  }
+}
+
+// k_tanh_slice for every class (the channel count is a template parameter)
+template <int S>
+static void launch_tanh_slice(cudaStream_t s, const Classes& T, const double* Z, int w,
+                              long long ld, const double* bias, long long bias_s, long long act_s,
+                              long long R, long long kpad, int nb, int8_t* Q, double* scale) {
+  const unsigned thr = static_cast<unsigned>((kpad / 4 + 31) / 32 * 32);
+  for (int c = 0; c < T.n; ++c) {
+    if (T.c[c].count == 0) continue;
+    const dim3 grid(static_cast<unsigned>(T.c[c].count), nb);
+#define DNGD_TS(N)                                                                       \
+  case N:                                                                                \
+    k_tanh_slice<S, N><<<grid, thr, 0, s>>>(T, c, Z, w, ld, bias, bias_s, act_s, R, kpad, Q, \
+                                            scale);                                      \
+    break;
+    switch (T.c[c].nch) {
+      DNGD_TS(1) DNGD_TS(2) DNGD_TS(3) DNGD_TS(4) DNGD_TS(5) DNGD_TS(6) DNGD_TS(7) DNGD_TS(8)
+      default: break;
+    }
+#undef DNGD_TS
   }
 }
 
@@ -1521,6 +1632,52 @@ static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const d
   }
   double* Hcur = B.Hping;
   double* Hnext = B.Hpong;
+  if (B.oz_S) {
+    // emulated FP64: candidate chunks of oz_cb, layer by layer inside a chunk; the
+    // tanh channel map of every layer that feeds another GEMM writes that GEMM's
+    // digit planes directly (k_tanh_slice), the last hidden layer writes H_{L-1}
+    int maxch = 0;
+    for (int c = 0; c < P.T.n; ++c) maxch = std::max(maxch, P.T.c[c].nch);
+    const bool fuse = maxch <= kTsMaxCh;
+    for (int k = 1; k <= L - 2; ++k)
+      launch_transpose(s, thetas + P.off[k], P.n, static_cast<int>(P.w[k]),
+                       static_cast<int>(P.w[k + 1]), B.Wt[k], P.ld[k], P.w[k + 1] * P.ld[k], C);
+    int rc = DNGD_OK;
+    for (int b0 = 0; b0 < C && rc == DNGD_OK; b0 += B.oz_cb) {
+      const int nb = std::min(B.oz_cb, C - b0);
+      rc = oz_slice(ctx, s, B.Hping + b0 * act_s, nb * P.R, P.w[1], P.ldmax, B.oz_S, B.ozQA, B.ozsA);
+      for (int k = 1; k <= L - 2 && rc == DNGD_OK; ++k) {
+        const long long N = P.w[k + 1], Kd = P.w[k];
+        const long long wst = P.w[k + 1] * P.ld[k];
+        rc = oz_slice(ctx, s, B.Wt[k] + b0 * wst, nb * N, Kd, P.ld[k], B.oz_S, B.ozQB, B.ozsB);
+        if (rc) break;
+        rc = oz_gemm_batched(ctx, s, B.ozQA, B.ozsA, nb * P.R, P.R, B.ozQB, B.ozsB, nb * N, N,
+                             oz_kpad(Kd), B.oz_S, P.R, N, nb, B.Z + b0 * act_s, P.ldmax, act_s);
+        if (rc) break;
+        const double* bias = thetas + static_cast<long long>(b0) * P.n + P.off[k] + P.w[k] * P.w[k + 1];
+        if (k < L - 2 && fuse) {
+          if (B.oz_S == 8) {
+            launch_tanh_slice<8>(s, P.T, B.Z + b0 * act_s, static_cast<int>(N), P.ldmax, bias, P.n,
+                                 act_s, P.R, oz_kpad(N), nb, B.ozQA, B.ozsA);
+          } else {
+            launch_tanh_slice<7>(s, P.T, B.Z + b0 * act_s, static_cast<int>(N), P.ldmax, bias, P.n,
+                                 act_s, P.R, oz_kpad(N), nb, B.ozQA, B.ozsA);
+          }
+        } else {
+          k_tanh_fwd<<<dim3(nblk(P.m * N), nb), 256, 0, s>>>(P.T, B.Z + b0 * act_s,
+                                                             B.Hpong + b0 * act_s, static_cast<int>(N),
+                                                             P.ldmax, bias, P.n, act_s);
+          if (k < L - 2) {
+            rc = oz_slice(ctx, s, B.Hpong + b0 * act_s, nb * P.R, N, P.ldmax, B.oz_S, B.ozQA,
+                          B.ozsA);
+          }
+        }
+      }
+    }
+    if (rc) return rc;
+    *Hlast = B.Hpong;
+    return cuda_status(ctx, cudaGetLastError(), "forward");
+  }
   for (int k = 1; k <= L - 2; ++k) {
     launch_transpose(s, thetas + P.off[k], P.n, static_cast<int>(P.w[k]),
                      static_cast<int>(P.w[k + 1]), B.Wt[k], P.ld[k], P.w[k + 1] * P.ld[k], C);
@@ -1538,24 +1695,7 @@ static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const d
     g.ldc = P.ldmax;
     g.sC = act_s;
     g.batch = C;
-    int rc = DNGD_OK;
-    if (B.oz_S) {
-      // emulated FP64 on the int8 tensor cores, oz_cb candidates per slicing pass
-      const long long N = P.w[k + 1], Kd = P.w[k];
-      for (int b0 = 0; b0 < C && rc == DNGD_OK; b0 += B.oz_cb) {
-        const int nb = std::min(B.oz_cb, C - b0);
-        rc = oz_slice(ctx, s, Hcur + b0 * act_s, nb * P.R, Kd, P.ldmax, B.oz_S, B.ozQA, B.ozsA);
-        if (rc == DNGD_OK) {
-          rc = oz_slice(ctx, s, B.Wt[k] + b0 * g.sB, nb * N, Kd, P.ld[k], B.oz_S, B.ozQB, B.ozsB);
-        }
-        if (rc == DNGD_OK) {
-          rc = oz_gemm_batched(ctx, s, B.ozQA, B.ozsA, nb * P.R, P.R, B.ozQB, B.ozsB, nb * N, N,
-                               oz_kpad(Kd), B.oz_S, P.R, N, nb, B.Z + b0 * act_s, P.ldmax, act_s);
-        }
-      }
-    } else {
-      rc = gemm_nt(ctx, s, g);
-    }
+    const int rc = gemm_nt(ctx, s, g);
     if (rc) return rc;
     dim3 gr(nblk(P.m * P.w[k + 1]), C);
     k_tanh_fwd<<<gr, 256, 0, s>>>(P.T, B.Z, Hnext, static_cast<int>(P.w[k + 1]), P.ldmax,
@@ -2595,7 +2735,6 @@ extern "C" int dngd_gram_oz_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   const long long t0 = static_cast<long long>(tiles) * part / nparts;
   const long long t1 = static_cast<long long>(tiles) * (part + 1) / nparts;
   gp.tile0 = static_cast<int>(t0);
-  gp.dbg = getenv("DNGD_GOZ_DBG") ? atoi(getenv("DNGD_GOZ_DBG")) : 0;
   if (t1 <= t0) return DNGD_OK;
   const size_t smem = gram_oz_smem(slices);
   auto kern = slices == 8 ? k_gram_oz<8> : k_gram_oz<7>;

@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
   uint64_t* full = reinterpret_cast<uint64_t*>(PH + OZ_BM * OZ_BN);
   uint64_t* empty = full + GO_STAGES;
   uint64_t* tfull = empty + GO_STAGES;
-  uint64_t* tempty = tfull + 1;  // [S]: per-diagonal release
-  uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tempty + S);
+  uint64_t* tempty = tfull + 1;
+  uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tempty + 1);
   __shared__ double sA[OZ_BM], sB[OZ_BN], zA[OZ_BM], zB[OZ_BN];
 
   // ---- tile decode
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
       mbar_init(&empty[i], 1);
     }
     mbar_init(tfull, 1);
-    for (int d = 0; d < S; ++d) mbar_init(&tempty[d], 8);
+    mbar_init(tempty, 8);
     fence_barrier_init();
   }
   if (threadIdx.x >= 64 && threadIdx.x < 64 + OZ_BM) {  // row seeds / value flags
@@ -178,18 +178,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
       for (int part = 0; part < 2; ++part) {
         const int nk = p.nk[k][part];
         if (nk == 0) continue;
+        if (ph > 0) mbar_wait(tempty, (ph - 1) & 1);  // epilogue drained the last phase
+        tc_fence_after();
         for (int kc = 0; kc < nk; ++kc, ++f) {
           const int st = f % GO_STAGES;
           mbar_wait(&full[st], (f / GO_STAGES) & 1);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a0 = smem_u32(smem + st * STAGE);
-            if (kc == 0) {  // diagonals as the epilogue releases them
-              oz_issue_first_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc,
-                                      tempty, ph > 0 ? ((ph - 1) & 1) : -1);
-            } else {
-              oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, false);
-            }
+            oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, kc == 0);
             umma_commit(&empty[st]);
             if (kc == nk - 1) umma_commit(tfull);
           }
@@ -214,27 +211,41 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
         if (p.nk[k][part] == 0) continue;
         mbar_wait(tfull, ph & 1);
         tc_fence_after();
-        double v[32];
-        oz_drain32<S>(tl, OZ_BN, col0, tempty, v);  // TMEM free for the next phase
         const double* scv = p.sc[k][part];
         const double sr = arow < p.R ? scv[arow] : 0.0;
-        // this warp's 32 column scales: lane j holds column col0 + j
+        // this warp's 32 column scales: lane j holds column col0 + j (shuffled below)
         const long long bl = brow0 + col0 + lane;
         const double scl = bl < p.R ? scv[bl] : 0.0;
         const double za = zA[row], sar = sA[row];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int gc = col0 + j;
-          const double x = v[j] * (sr * __shfl_sync(0xffffffffu, scl, j));
-          if (part == 0) {
-            const double vh = fma(za, zB[gc], x);  // + bias entry (value channels)
-            if (seeds) {
-              G[j] = fma(vh, sar * sB[gc], G[j]);
+        for (int cc = 0; cc < 4; ++cc) {
+          int32_t acc[S][8];
+#pragma unroll
+          for (int d = 0; d < S; ++d) tmem_ld8(tl + d * OZ_BN + col0 + 8 * cc, acc[d]);
+          tmem_ld_wait();
+          if (cc == 3) {  // every diagonal is in registers: hand TMEM to the next phase
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int gc = col0 + 8 * cc + j;
+            const double scol = __shfl_sync(0xffffffffu, scl, 8 * cc + j);
+            int32_t a[S];
+#pragma unroll
+            for (int d = 0; d < S; ++d) a[d] = acc[d][j];
+            const double v = oz_combine<S>(a) * (sr * scol);
+            if (part == 0) {
+              const double vh = fma(za, zB[gc], v);  // + bias entry (value channels)
+              if (seeds) {
+                G[8 * cc + j] = fma(vh, sar * sB[gc], G[8 * cc + j]);
+              } else {
+                PH[gc * OZ_BM + row] = vh;
+              }
             } else {
-              PH[gc * OZ_BM + row] = vh;
+              G[8 * cc + j] = fma(PH[gc * OZ_BM + row], v, G[8 * cc + j]);
             }
-          } else {
-            G[j] = fma(PH[gc * OZ_BM + row], x, G[j]);
           }
         }
         ++ph;

@@ -135,8 +135,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 1;  // [S]: per-diagonal release
-  uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tempty + S);
+  uint64_t* tempty = tfull + 1;
+  uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tempty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tn = (N + OZ_BN - 1) / OZ_BN, tm = (M + OZ_BM - 1) / OZ_BM;
   const int ntiles = tn * tm * batch;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       mbar_init(&empty[i], 1);
     }
     mbar_init(tfull, 1);
-    for (int d = 0; d < S; ++d) mbar_init(&tempty[d], 8);
+    mbar_init(tempty, 8);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(taddr_sh, 512);
@@ -181,18 +181,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     constexpr uint32_t idesc = umma_idesc_s8(OZ_BM, OZ_BN);
     int f = 0, it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      if (it > 0) mbar_wait(tempty, (it - 1) & 1);
+      tc_fence_after();
       for (int kc = 0; kc < nk; ++kc, ++f) {
         const int st = f % STAGES;
         mbar_wait(&full[st], (f / STAGES) & 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a0 = smem_u32(smem + st * STAGE);
-          if (kc == 0) {
-            oz_issue_first_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc,
-                                    tempty, it > 0 ? ((it - 1) & 1) : -1);
-          } else {
-            oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, false);
-          }
+          oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, kc == 0);
           umma_commit(&empty[st]);
           if (kc == nk - 1) umma_commit(tfull);
         }
@@ -215,9 +212,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       double v[OZ_BN / 2];
       mbar_wait(tfull, it & 1);
       tc_fence_after();
-      oz_drain32<S>(tl, OZ_BN, h * (OZ_BN / 2), tempty, v);
 #pragma unroll
-      for (int j = 0; j < OZ_BN / 2; ++j) v[j] *= sa * __shfl_sync(0xffffffffu, scl, j);
+      for (int c = 0; c < OZ_BN / 2 / 8; ++c) {
+        int32_t acc[S][8];
+#pragma unroll
+        for (int d = 0; d < S; ++d) tmem_ld8(tl + d * OZ_BN + h * (OZ_BN / 2) + 8 * c, acc[d]);
+        tmem_ld_wait();
+        if (c == OZ_BN / 2 / 8 - 1) {  // all diagonals in registers: release TMEM
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          int32_t a[S];
+#pragma unroll
+          for (int d = 0; d < S; ++d) a[d] = acc[d][j];
+          v[8 * c + j] = oz_combine<S>(a) * (sa * __shfl_sync(0xffffffffu, scl, 8 * c + j));
+        }
+      }
       if (m0 + row < M) {
         double* crow = C + z * sC + static_cast<long long>(m0 + row) * ldc + n0 + h * (OZ_BN / 2);
         const int nvalid = N - (n0 + h * (OZ_BN / 2));
@@ -241,12 +254,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
 }
 
-template <int S>
+template <int S, int STAGES = 4>
 static int oz_gemm_launch(dngd_ctx* ctx, cudaStream_t s, const CUtensorMap& mA,
                           const CUtensorMap& mB, const double* scA, const double* scB, double* C,
                           long long ldc, long long M, long long N, int nk, int batch,
                           long long a_brows, long long b_brows, long long sC) {
-  constexpr int STAGES = 3;
   const size_t smem = oz_smem_bytes(S, STAGES);
   auto kern = k_oz_gemm<S, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

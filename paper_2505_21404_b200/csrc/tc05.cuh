@@ -119,52 +119,6 @@ DNGD_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" :::
 
 DNGD_DEV bool elect_lane0() { return (threadIdx.x & 31) == 0; }
 
-// First K-chunk of a tile/phase when the epilogue is still draining the previous
-// accumulators: diagonal-major, highest diagonal first, waiting for each
-// diagonal's release (tempty[D], one arrive per epilogue warp) right before its
-// first write.  The epilogue drains in the same order, so the MMAs start as soon
-// as the first diagonal is free instead of after the whole drain.
-template <int S>
-DNGD_DEV void oz_issue_first_chunk(uint32_t tmem, int ncols, uint32_t a0, int abytes, uint32_t b0,
-                                   int bbytes, uint32_t idesc, uint64_t* tempty, int wait_parity) {
-#pragma unroll
-  for (int D = S - 1; D >= 0; --D) {
-    if (wait_parity >= 0) {
-      mbar_wait(&tempty[D], static_cast<uint32_t>(wait_parity));
-      tc_fence_after();
-    }
-#pragma unroll
-    for (int t = 0; t <= D; ++t)
-      umma_i8<0>(tmem + D * ncols, umma_desc_sw32(a0 + t * abytes),
-                 umma_desc_sw32(b0 + (D - t) * bbytes), idesc, t > 0 ? 1u : 0u);
-  }
-}
-
-// Epilogue drain of one warp's 32 lanes x 32 columns (col0 ..): diagonal-major,
-// highest first, each diagonal released (tempty[D]) as soon as it is in registers;
-// v = sum_D acc_D 2^{-7(D+2)} accumulated smallest term first (FP64, ~1 ulp).
-template <int S>
-DNGD_DEV void oz_drain32(uint32_t tl, int ncols, int col0, uint64_t* tempty, double (&v)[32]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = 0.0;
-#pragma unroll
-  for (int D = S - 1; D >= 0; --D) {
-    int32_t acc[4][8];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_ld8(tl + D * ncols + col0 + 8 * c, acc[c]);
-    tmem_ld_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&tempty[D]);
-    const double w = exp2(-7.0 * (D + 2));
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[8 * c + j] = fma(static_cast<double>(acc[c][j]), w, v[8 * c + j]);
-  }
-}
-
 // ---------------------------------------------------------------- Ozaki digits
 // x = scale * sum_{t<S} d_t 2^{-7(t+1)} + O(scale 2^{-7S-1}), |d_0| <= 127,
 // |d_t| <= 64, scale a power of two >= max|row| (oz_digits4).  A product of two sliced values is

@@ -24,11 +24,10 @@
 // as tall, in super-rows of GO_GROUP row tiles walked column by column, so the
 // ~148 CTAs in flight share their operand tiles through L2.
 
-constexpr int GO_STAGES = 3;
 constexpr int GO_GROUP = 8;
 
 struct GozParams {
-  CUtensorMap mA[DNGD_MAX_LAYERS][2];  // sliced H_k / Zbar_k, box 32 B x 128 rows x S
+  CUtensorMap mA[DNGD_MAX_LAYERS][2];  // sliced H_k / Zbar_k, box 64 B x 128 rows x S
   CUtensorMap mB[DNGD_MAX_LAYERS][2];  // same buffers, box 32 B x 64 rows x S
   const double* sc[DNGD_MAX_LAYERS][2];  // per activation row: 2^e (NaN = non-finite row)
   long long R;                           // activation rows
@@ -44,6 +43,7 @@ struct GozParams {
   double* K;
   long long ldK;
   int tile0;
+  int dbg;  // timing experiments only: 1 = issue only the products with t + u <= 3
 };
 
 // lower-triangle tile t of TI row tiles (row tile ti spans column tiles 2ti, 2ti+1)
@@ -89,15 +89,25 @@ DNGD_DEV void goz_wait_sleep(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Operand rings: A (the 128-row tile) in 64-wide K slabs of 64-byte TMA rows, GO_SA
+// deep; B (64 rows) in 32-wide K chunks of 32-byte rows, GO_SB deep.  TMA serves one
+// box row per cycle per SM (tools/micro/tma_rate.cu), so A's rows carry two MMA
+// K-steps each; B keeps the narrow rows so the whole ring + G^H fits in 227 KB.
+constexpr int GO_SA = 2, GO_SB = 3;
+
 template <int S>
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant__ GozParams p) {
   extern __shared__ uint8_t go_smem_raw[];
   uint8_t* smem = smem_align(go_smem_raw, 1024);
-  constexpr int ABYTES = S * OZ_BM * 32, STAGE = S * (OZ_BM + OZ_BN) * 32;
-  double* PH = reinterpret_cast<double*>(smem + GO_STAGES * STAGE);  // [64 cols][128 rows]
-  uint64_t* full = reinterpret_cast<uint64_t*>(PH + OZ_BM * OZ_BN);
-  uint64_t* empty = full + GO_STAGES;
-  uint64_t* tfull = empty + GO_STAGES;
+  constexpr int ASLAB = S * OZ_BM * 64, BCHUNK = S * OZ_BN * 32;
+  uint8_t* ringA = smem;
+  uint8_t* ringB = smem + GO_SA * ASLAB;
+  double* PH = reinterpret_cast<double*>(ringB + GO_SB * BCHUNK);  // [64 cols][128 rows]
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(PH + OZ_BM * OZ_BN);
+  uint64_t* emptyA = fullA + GO_SA;
+  uint64_t* fullB = emptyA + GO_SA;
+  uint64_t* emptyB = fullB + GO_SB;
+  uint64_t* tfull = emptyB + GO_SB;
   uint64_t* tempty = tfull + 1;
   uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tempty + 1);
   __shared__ double sA[OZ_BM], sB[OZ_BN], zA[OZ_BM], zB[OZ_BN];
@@ -125,9 +135,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < GO_STAGES; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+    for (int i = 0; i < GO_SA; ++i) {
+      mbar_init(&fullA[i], 1);
+      mbar_init(&emptyA[i], 1);
+    }
+    for (int i = 0; i < GO_SB; ++i) {
+      mbar_init(&fullB[i], 1);
+      mbar_init(&emptyB[i], 1);
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 8);
@@ -153,19 +167,26 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
   const uint32_t tbase = *taddr_sh;
 
   if (warp == 0) {
-    // ---- TMA producer: every phase's K-chunks through the ring
+    // ---- TMA producer: every phase's K-chunks; an A slab every second chunk
     if (lane == 0) {
-      int f = 0;
+      int fa = 0, fb = 0;
       for (int k = 0; k < p.L; ++k) {
         for (int part = 0; part < 2; ++part) {
           const int nk = p.nk[k][part];
-          for (int kc = 0; kc < nk; ++kc, ++f) {
-            const int st = f % GO_STAGES;
-            if (f >= GO_STAGES) mbar_wait(&empty[st], ((f / GO_STAGES) - 1) & 1);
-            uint8_t* sa = smem + st * STAGE;
-            mbar_arrive_expect_tx(&full[st], STAGE);
-            tma_load_3d(sa, &p.mA[k][part], &full[st], kc * 32, static_cast<int>(arow0), 0);
-            tma_load_3d(sa + ABYTES, &p.mB[k][part], &full[st], kc * 32, static_cast<int>(brow0), 0);
+          for (int kc = 0; kc < nk; ++kc, ++fb) {
+            if ((kc & 1) == 0) {
+              const int sa = fa % GO_SA;
+              if (fa >= GO_SA) mbar_wait(&emptyA[sa], ((fa / GO_SA) - 1) & 1);
+              mbar_arrive_expect_tx(&fullA[sa], ASLAB);
+              tma_load_3d(ringA + sa * ASLAB, &p.mA[k][part], &fullA[sa], kc * 32,
+                          static_cast<int>(arow0), 0);
+              ++fa;
+            }
+            const int sb = fb % GO_SB;
+            if (fb >= GO_SB) mbar_wait(&emptyB[sb], ((fb / GO_SB) - 1) & 1);
+            mbar_arrive_expect_tx(&fullB[sb], BCHUNK);
+            tma_load_3d(ringB + sb * BCHUNK, &p.mB[k][part], &fullB[sb], kc * 32,
+                        static_cast<int>(brow0), 0);
           }
         }
       }
@@ -173,24 +194,34 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
   } else if (warp == 1) {
     // ---- MMA issuer
     constexpr uint32_t idesc = umma_idesc_s8(OZ_BM, OZ_BN);
-    int f = 0, ph = 0;
+    int fa = 0, fb = 0, ph = 0;
     for (int k = 0; k < p.L; ++k) {
       for (int part = 0; part < 2; ++part) {
         const int nk = p.nk[k][part];
         if (nk == 0) continue;
         if (ph > 0) mbar_wait(tempty, (ph - 1) & 1);  // epilogue drained the last phase
         tc_fence_after();
-        for (int kc = 0; kc < nk; ++kc, ++f) {
-          const int st = f % GO_STAGES;
-          mbar_wait(&full[st], (f / GO_STAGES) & 1);
+        for (int kc = 0; kc < nk; ++kc, ++fb) {
+          const int sa = fa % GO_SA, sb = fb % GO_SB;
+          if ((kc & 1) == 0) mbar_wait(&fullA[sa], (fa / GO_SA) & 1);
+          mbar_wait(&fullB[sb], (fb / GO_SB) & 1);
           tc_fence_after();
+          const bool last_of_slab = (kc & 1) == 1 || kc == nk - 1;
           if (lane == 0) {
-            const uint32_t a0 = smem_u32(smem + st * STAGE);
-            oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, kc == 0);
-            umma_commit(&empty[st]);
+            const uint32_t a0 = smem_u32(ringA + sa * ASLAB) + 32 * (kc & 1);
+            const uint32_t b0 = smem_u32(ringB + sb * BCHUNK);
+            if (p.dbg == 1) {
+              oz_issue_chunk<S, 64, 32>(tbase, OZ_BN, a0, OZ_BM * 64, b0, OZ_BN * 32, idesc, kc == 0);
+            } else if (p.dbg == 2 || p.dbg == 3) {
+            } else {
+              oz_issue_chunk_wide<S, 64, 32>(tbase, a0, OZ_BM * 64, b0, OZ_BN * 32, kc == 0);
+            }
+            umma_commit(&emptyB[sb]);
+            if (last_of_slab) umma_commit(&emptyA[sa]);
             if (kc == nk - 1) umma_commit(tfull);
           }
           __syncwarp();
+          if (last_of_slab) ++fa;
         }
         ++ph;
       }
@@ -211,6 +242,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
         if (p.nk[k][part] == 0) continue;
         mbar_wait(tfull, ph & 1);
         tc_fence_after();
+        if (p.dbg >= 3) {  // timing experiments: no drain
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty);
+          ++ph;
+          continue;
+        }
         const double* scv = p.sc[k][part];
         const double sr = arow < p.R ? scv[arow] : 0.0;
         // this warp's 32 column scales: lane j holds column col0 + j (shuffled below)
@@ -278,5 +316,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
 }
 
 static size_t gram_oz_smem(int S) {
-  return oz_smem_bytes(S, GO_STAGES) + static_cast<size_t>(OZ_BM) * OZ_BN * 8 + 64;
+  return 1024 + static_cast<size_t>(GO_SA) * S * OZ_BM * 64 + static_cast<size_t>(GO_SB) * S * OZ_BN * 32 +
+         static_cast<size_t>(OZ_BM) * OZ_BN * 8 + (2 * GO_SA + 2 * GO_SB + 2) * 8 + 64;
 }

@@ -71,10 +71,11 @@ int syrk(dngd_ctx* ctx, cudaStream_t s, const double* J, long long m, long long 
 // a row with a non-finite entry gets scale NaN.
 int oz_slice(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows, long long K,
              long long ld, int slices, int8_t* Q, double* scale);
-// 3-D TMA map over Q: box {32 bytes, box_rows, slices}, 32-byte swizzle, rows past
-// the end read as zero digits
+// 3-D TMA map over Q: box {box_bytes (32 or 64), box_rows, slices}, swizzle of the
+// same width; rows past the end (and K past kpad) read as zero digits.  64-byte
+// rows feed twice the bytes per TMA row request (tools/micro/tma_rate.cu)
 int oz_encode(dngd_ctx* ctx, CUtensorMap* map, const int8_t* Q, long long rows, long long kpad,
-              int slices, int box_rows);
+              int slices, int box_rows, int box_bytes = 32);
 // C_z = A_z B_z^T (z < batch) over sliced operands: A_z rows z a_brows .. + M of the
 // a_rows-row digit planes QA (scales scA), likewise B; C_z = C + z sC (pitch ldc)
 int oz_gemm_batched(dngd_ctx* ctx, cudaStream_t s, const int8_t* QA, const double* scA,

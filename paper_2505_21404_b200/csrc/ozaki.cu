@@ -103,16 +103,18 @@ int oz_slice(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows, lon
 }
 
 int oz_encode(dngd_ctx* ctx, CUtensorMap* map, const int8_t* Q, long long rows, long long kpad,
-              int slices, int box_rows) {
+              int slices, int box_rows, int box_bytes) {
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(kpad), static_cast<cuuint64_t>(std::max(rows, 1LL)),
                         static_cast<cuuint64_t>(slices)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(kpad),
                            static_cast<cuuint64_t>(kpad) * static_cast<cuuint64_t>(std::max(rows, 1LL))};
-  cuuint32_t box[3] = {32, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(slices)};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box_bytes), static_cast<cuuint32_t>(box_rows),
+                       static_cast<cuuint32_t>(slices)};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = ctx->encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(Q), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           box_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? DNGD_OK : set_error(ctx, DNGD_ERR_CUDA, "oz: tensor map encode failed");
 }
@@ -131,7 +133,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
               long long b_brows, long long sC, int batch) {
   extern __shared__ uint8_t oz_smem_raw[];
   uint8_t* smem = smem_align(oz_smem_raw, 1024);
-  constexpr int ABYTES = S * OZ_BM * 32, STAGE = S * (OZ_BM + OZ_BN) * 32;
+  // a stage is a 64-wide K-slab (two MMA K-steps) of every slice: 64-byte TMA rows
+  constexpr int ABYTES = S * OZ_BM * 64, STAGE = S * (OZ_BM + OZ_BN) * 64;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -139,6 +142,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tempty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tn = (N + OZ_BN - 1) / OZ_BN, tm = (M + OZ_BM - 1) / OZ_BM;
+  const int nslab = (nk + 1) / 2;
   const int ntiles = tn * tm * batch;
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
@@ -167,13 +171,13 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         int z, m0, n0;
         decode(tile, z, m0, n0);
         const int ar = static_cast<int>(z * a_brows + m0), br = static_cast<int>(z * b_brows + n0);
-        for (int kc = 0; kc < nk; ++kc, ++f) {
+        for (int ks = 0; ks < nslab; ++ks, ++f) {
           const int st = f % STAGES;
           if (f >= STAGES) mbar_wait(&empty[st], ((f / STAGES) - 1) & 1);
           uint8_t* sa = smem + st * STAGE;
           mbar_arrive_expect_tx(&full[st], STAGE);
-          tma_load_3d(sa, &mA, &full[st], kc * 32, ar, 0);
-          tma_load_3d(sa + ABYTES, &mB, &full[st], kc * 32, br, 0);
+          tma_load_3d(sa, &mA, &full[st], ks * 64, ar, 0);
+          tma_load_3d(sa + ABYTES, &mB, &full[st], ks * 64, br, 0);
         }
       }
     }
@@ -183,15 +187,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       if (it > 0) mbar_wait(tempty, (it - 1) & 1);
       tc_fence_after();
-      for (int kc = 0; kc < nk; ++kc, ++f) {
+      for (int ks = 0; ks < nslab; ++ks, ++f) {
         const int st = f % STAGES;
         mbar_wait(&full[st], (f / STAGES) & 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a0 = smem_u32(smem + st * STAGE);
-          oz_issue_chunk<S>(tbase, OZ_BN, a0, OZ_BM * 32, a0 + ABYTES, OZ_BN * 32, idesc, kc == 0);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (2 * ks + h >= nk) break;
+            oz_issue_chunk_wide<S, 64, 64>(tbase, a0 + 32 * h, OZ_BM * 64, a0 + ABYTES + 32 * h,
+                                           OZ_BN * 64, ks == 0 && h == 0);
+          }
           umma_commit(&empty[st]);
-          if (kc == nk - 1) umma_commit(tfull);
+          if (ks == nslab - 1) umma_commit(tfull);
         }
         __syncwarp();
       }
@@ -254,12 +263,12 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
 }
 
-template <int S, int STAGES = 4>
+template <int S, int STAGES = 2>
 static int oz_gemm_launch(dngd_ctx* ctx, cudaStream_t s, const CUtensorMap& mA,
                           const CUtensorMap& mB, const double* scA, const double* scB, double* C,
                           long long ldc, long long M, long long N, int nk, int batch,
                           long long a_brows, long long b_brows, long long sC) {
-  const size_t smem = oz_smem_bytes(S, STAGES);
+  const size_t smem = oz_smem_bytes(S, 2 * STAGES);  // 64-wide slabs = 2 chunk-stages each
   auto kern = k_oz_gemm<S, STAGES>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -278,9 +287,9 @@ int oz_gemm_batched(dngd_ctx* ctx, cudaStream_t s, const int8_t* QA, const doubl
                     long long N, int batch, double* C, long long ldc, long long sC) {
   if (M <= 0 || N <= 0 || batch <= 0) return DNGD_OK;
   CUtensorMap mA, mB;
-  int rc = oz_encode(ctx, &mA, QA, a_rows, kpad, slices, OZ_BM);
+  int rc = oz_encode(ctx, &mA, QA, a_rows, kpad, slices, OZ_BM, 64);
   if (rc) return rc;
-  rc = oz_encode(ctx, &mB, QB, b_rows, kpad, slices, OZ_BN);
+  rc = oz_encode(ctx, &mB, QB, b_rows, kpad, slices, OZ_BN, 64);
   if (rc) return rc;
   const int nk = static_cast<int>(kpad / 32);
   switch (slices) {

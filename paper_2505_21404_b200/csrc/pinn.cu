@@ -2633,7 +2633,7 @@ static size_t gram_oz_bytes(const Plan& P, int S) {
 }
 
 static int goz_check(dngd_ctx* ctx, const Plan& P, int slices) {
-  if (slices < 7 || slices > 8) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_oz: slices must be 7 or 8");
+  if (slices != 7) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_oz: 7 digit slices (8 exceeds shared memory)");
   if (P.wide_in) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: wide input layer");
   if (P.T.din > DNGD_MAX_GRAD) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: input dim > 12");
   if (P.R >= (1LL << 31)) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: too many activation rows");
@@ -2703,7 +2703,7 @@ extern "C" int dngd_gram_oz_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
       w += oz_al256(static_cast<size_t>(P.R) * 8);
       rc = oz_slice(ctx, s, src, P.R, kd, ld, slices, Q, sc);
       if (rc) return rc;
-      rc = oz_encode(ctx, &gp.mA[k][pt], Q, P.R, oz_kpad(kd), slices, OZ_BM);
+      rc = oz_encode(ctx, &gp.mA[k][pt], Q, P.R, oz_kpad(kd), slices, OZ_BM, 64);
       if (rc) return rc;
       rc = oz_encode(ctx, &gp.mB[k][pt], Q, P.R, oz_kpad(kd), slices, OZ_BN);
       if (rc) return rc;
@@ -2735,9 +2735,10 @@ extern "C" int dngd_gram_oz_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   const long long t0 = static_cast<long long>(tiles) * part / nparts;
   const long long t1 = static_cast<long long>(tiles) * (part + 1) / nparts;
   gp.tile0 = static_cast<int>(t0);
+  gp.dbg = getenv("DNGD_GOZ_DBG") ? atoi(getenv("DNGD_GOZ_DBG")) : 0;
   if (t1 <= t0) return DNGD_OK;
   const size_t smem = gram_oz_smem(slices);
-  auto kern = slices == 8 ? k_gram_oz<8> : k_gram_oz<7>;
+  auto kern = k_gram_oz<7>;  // S = 8 would need 235 KB of shared memory (refused by goz_check)
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_status(ctx, e, "gram_oz smem attribute");

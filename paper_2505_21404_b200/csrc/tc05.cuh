@@ -9,6 +9,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "oz_common.cuh"
 
 namespace dngd {
 
@@ -21,6 +22,26 @@ DNGD_DEV uint64_t umma_desc_sw32(uint32_t saddr) {
   constexpr uint64_t kLayoutSW32 = 6;
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (kLBO << 16) | (kSBO << 32) |
          (1ull << 46) | (kLayoutSW32 << 61);
+}
+
+// K-major, 64-byte rows (two 32-byte MMA K-steps per row; the second step starts
+// 32 bytes in), 128-byte swizzle... of 64-byte rows: SWIZZLE_64B, SBO = 8 rows x 64 B
+DNGD_DEV uint64_t umma_desc_sw64(uint32_t saddr) {
+  constexpr uint64_t kLBO = 1;
+  constexpr uint64_t kSBO = 512 >> 4;
+  constexpr uint64_t kLayoutSW64 = 4;
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (kLBO << 16) | (kSBO << 32) |
+         (1ull << 46) | (kLayoutSW64 << 61);
+}
+
+template <int W>
+DNGD_DEV uint64_t umma_desc_k(uint32_t saddr) {
+  static_assert(W == 32 || W == 64, "32- or 64-byte operand rows");
+  if constexpr (W == 32) {
+    return umma_desc_sw32(saddr);
+  } else {
+    return umma_desc_sw64(saddr);
+  }
 }
 
 // instruction descriptor, kind::i8: D s32 [4,6) = 2, A s8 [7,10) = 1, B s8
@@ -73,18 +94,20 @@ DNGD_DEV void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t 
 #undef DNGD_UMMA_I8
 
 // the S(S+1)/2 digit products of one K-chunk into the S diagonal accumulators
-// (tmem + D * ncols): A_t stays in the collector across its S - t products
-template <int S>
+// (tmem + D * ncols): A_t stays in the collector across its S - t products.
+// WA / WB: operand row width in bytes (32: one K-step per row; 64: a0 / b0 already
+// point at the K-step's 32-byte half of the row)
+template <int S, int WA = 32, int WB = 32>
 DNGD_DEV void oz_issue_chunk(uint32_t tmem, int ncols, uint32_t a0, int abytes, uint32_t b0,
                              int bbytes, uint32_t idesc, bool first_chunk) {
 #pragma unroll
   for (int t = 0; t < S; ++t) {
-    const uint64_t ad = umma_desc_sw32(a0 + t * abytes);
+    const uint64_t ad = umma_desc_k<WA>(a0 + t * abytes);
     const uint32_t acc = (!first_chunk || t > 0) ? 1u : 0u;
 #pragma unroll
     for (int u = 0; u < S - t; ++u) {
       const uint32_t d = tmem + (t + u) * ncols;
-      const uint64_t bd = umma_desc_sw32(b0 + u * bbytes);
+      const uint64_t bd = umma_desc_k<WB>(b0 + u * bbytes);
       if (S - t == 1) {
         umma_i8<0>(d, ad, bd, idesc, acc);
       } else if (u == 0) {
@@ -94,6 +117,33 @@ DNGD_DEV void oz_issue_chunk(uint32_t tmem, int ncols, uint32_t a0, int abytes, 
       } else {
         umma_i8<2>(d, ad, bd, idesc, acc);
       }
+    }
+  }
+}
+
+// The same S(S+1)/2 products as oz_issue_chunk, issued as ONE wide MMA per A
+// slice: B's slices 0 .. S-1-t are consecutive 64-row blocks in shared memory (one
+// operand of N = 64 (S - t) rows) and the S diagonal accumulators are consecutive
+// 64-column blocks of TMEM, so A_t x [B_0 .. B_{S-1-t}]^T written at column 64 t
+// lands block u on diagonal t + u.  N > 256 is split in two.  10 MMAs per chunk at
+// S = 7 instead of 28 N = 64 ones (each of which cost ~45-70 cycles against the
+// 32 of the tensor-core rate), A read once per t.
+template <int S, int WA = 32, int WB = 32>
+DNGD_DEV void oz_issue_chunk_wide(uint32_t tmem, uint32_t a0, int abytes, uint32_t b0, int bbytes,
+                                  bool first_chunk) {
+  static_assert(OZ_BN == 64, "diagonal blocks are 64 columns");
+#pragma unroll
+  for (int t = 0; t < S; ++t) {
+    const uint64_t ad = umma_desc_k<WA>(a0 + t * abytes);
+    const uint32_t acc = (!first_chunk || t > 0) ? 1u : 0u;
+    constexpr int kMaxBlocks = 4;  // N <= 256
+    const int nblk = S - t;
+    const int n1 = nblk < kMaxBlocks ? nblk : kMaxBlocks;
+    // compile-time N per t (the loop is unrolled)
+    umma_i8<0>(tmem + t * OZ_BN, ad, umma_desc_k<WB>(b0), umma_idesc_s8(OZ_BM, OZ_BN * n1), acc);
+    if (nblk > kMaxBlocks) {
+      umma_i8<0>(tmem + (t + kMaxBlocks) * OZ_BN, ad, umma_desc_k<WB>(b0 + kMaxBlocks * bbytes),
+                 umma_idesc_s8(OZ_BM, OZ_BN * (nblk - kMaxBlocks)), acc);
     }
   }
 }

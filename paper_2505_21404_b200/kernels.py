@@ -284,7 +284,7 @@ def gram_factored(mlp, theta, classes_arr, nclass, r, K, ws, part=0, nparts=1):
 
 def gram_emulation_slices(mlp=None) -> int:
     """Ozaki digit count of the factored Gram's G-space products (0 = FP64 DMMA).
-    DNGD_GRAM_SLICES (0, 7 or 8) overrides; by default layers 128 wide or more run
+    DNGD_GRAM_SLICES (0 or 7) overrides; by default layers 128 wide or more run
     emulated with 7 digits (int8 tcgen05, ~2x the DMMA kernel at config 3, K within
     5e-16 of it) and narrower nets stay on DMMA (the int8 tile's fixed costs win
     nothing at K = 64)."""
@@ -293,8 +293,8 @@ def gram_emulation_slices(mlp=None) -> int:
     env = os.environ.get("DNGD_GRAM_SLICES")
     if env is not None:
         v = int(env)
-        if v not in (0, 7, 8):
-            raise DimensionError("DNGD_GRAM_SLICES must be 0, 7 or 8")
+        if v not in (0, 7):
+            raise DimensionError("DNGD_GRAM_SLICES must be 0 or 7")
         return v
     if mlp is None:
         return 7

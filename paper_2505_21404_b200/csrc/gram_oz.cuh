@@ -8,14 +8,14 @@
 //
 // Tile: 128 G-rows (2 ppc whole points of the row class) x 64 G-columns (ppc =
 // floor(64 / nch) whole points of the column class).  Per layer two MMA phases
-// (H then Z; the output layer's Z is the per-row residual seeds).  Warp roles:
+// (Z then H; the output layer's Z is the per-row residual seeds).  Warp roles:
 // warp 0 streams {32 B x rows x S slices} TMA boxes of the sliced activations
 // through a 3-stage mbarrier ring; warp 1 owns TMEM (512 columns = S diagonals
 // x 64) and issues the MMAs (one elected lane, A tiles held in the collector
 // across their S - t products); warps 2-9 drain TMEM after each phase: thread
 // (q, h) owns G-row 32q + lane and G-columns 32h .. 32h + 31, folds the S int32
 // diagonals exactly into FP64 (oz_combine), applies the row/column scales and
-// the bias entry, parks G^H in shared memory (column-major, conflict-free) and
+// the bias entry, parks G^Z in shared memory (column-major, conflict-free) and
 // accumulates G^H o G^Z in registers.  After the last layer the G tile goes to
 // shared memory and every point pair sums its nch x nch' block in a fixed
 // order (deterministic K, as the DMMA kernel).
@@ -95,8 +95,39 @@ DNGD_DEV void goz_wait_sleep(uint64_t* bar, uint32_t parity) {
 // K-steps each; B keeps the narrow rows so the whole ring + G^H fits in 227 KB.
 constexpr int GO_SA = 2, GO_SB = 3;
 
+// tile t (relative to p.tile0) -> (class pair, row tile, column tile)
+struct GozTile {
+  int c, cp, ti, tj;
+};
+DNGD_DEV GozTile goz_tile(const GozParams& p, int tile) {
+  GozTile r;
+  int pi = 0;
+  while (pi + 1 < p.npairs && tile >= p.tstart[pi + 1]) ++pi;
+  const int t = tile - p.tstart[pi];
+  r.c = p.pc[pi];
+  r.cp = p.pcp[pi];
+  if (r.c == r.cp) {
+    goz_decode_tri(t, p.ti_n[pi], r.ti, r.tj);
+  } else {  // rectangle, column-major: CTAs in flight share the column tiles
+    r.tj = t / p.ti_n[pi];
+    r.ti = t - r.tj * p.ti_n[pi];
+  }
+  return r;
+}
+
+// Phase order within a layer: Z first (parked in PH), then H (multiplied in);
+// the output layer has only its H phase (G^Z = the residual seeds).  Z-first puts
+// a long phase (Z_0, w_1 wide) at the start of every tile, so the previous tile's
+// point-pair reduction (which reads PH) overlaps its MMAs.
+DNGD_DEV int goz_nphase(const GozParams& p, int k) { return p.nk[k][1] > 0 ? 2 : 1; }
+DNGD_DEV int goz_part(const GozParams& p, int k, int i) { return p.nk[k][1] > 0 ? 1 - i : 0; }
+
+// Persistent: one CTA per SM walks tiles blockIdx.x, + gridDim.x, ...  The TMA
+// producer runs ahead across tile boundaries; the MMA warp starts a tile's first
+// phase as soon as the epilogue has drained the previous tile's last one, while
+// the epilogue reduces that tile's point pairs and writes K.
 template <int S>
-__global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant__ GozParams p) {
+__global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant__ GozParams p, int ntiles) {
   extern __shared__ uint8_t go_smem_raw[];
   uint8_t* smem = smem_align(go_smem_raw, 1024);
   constexpr int ASLAB = S * OZ_BM * 64, BCHUNK = S * OZ_BN * 32;
@@ -112,27 +143,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
   uint32_t* taddr_sh = reinterpret_cast<uint32_t*>(tempty + 1);
   __shared__ double sA[OZ_BM], sB[OZ_BN], zA[OZ_BM], zB[OZ_BN];
 
-  // ---- tile decode
-  int pi = 0;
-  const int tile = static_cast<int>(blockIdx.x) + p.tile0;
-  while (pi + 1 < p.npairs && tile >= p.tstart[pi + 1]) ++pi;
-  const int t = tile - p.tstart[pi];
-  const int c = p.pc[pi], cp = p.pcp[pi];
-  int ti, tj;
-  if (c == cp) {
-    goz_decode_tri(t, p.ti_n[pi], ti, tj);
-  } else {  // rectangle, column-major: CTAs in flight share the column tiles
-    tj = t / p.ti_n[pi];
-    ti = t - tj * p.ti_n[pi];
-  }
-  const int na = p.nch[c], nb = p.nch[cp];
-  const int np_r = 2 * p.ppc[c], np_c = p.ppc[cp];
-  const int P0 = ti * np_r, Q0 = tj * np_c;
-  const ClassDev& Ca = p.T.c[c];
-  const ClassDev& Cb = p.T.c[cp];
-  const long long arow0 = Ca.act0 + static_cast<long long>(P0) * na;
-  const long long brow0 = Cb.act0 + static_cast<long long>(Q0) * nb;
-
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < GO_SA; ++i) {
@@ -147,19 +157,6 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
     mbar_init(tempty, 8);
     fence_barrier_init();
   }
-  if (threadIdx.x >= 64 && threadIdx.x < 64 + OZ_BM) {  // row seeds / value flags
-    const int g = threadIdx.x - 64;
-    const int cha = g % na, pa = P0 + g / na;
-    const bool ok = g < np_r * na && pa < Ca.count;
-    sA[g] = ok ? seedc(p.T, Ca, cha, Ca.row0 + pa) : 0.0;
-    zA[g] = (ok && cha == 0) ? 1.0 : 0.0;
-  } else if (threadIdx.x >= 64 + OZ_BM && threadIdx.x < 64 + OZ_BM + OZ_BN) {
-    const int g = threadIdx.x - 64 - OZ_BM;
-    const int chb = g % nb, pb = Q0 + g / nb;
-    const bool ok = g < np_c * nb && pb < Cb.count;
-    sB[g] = ok ? seedc(p.T, Cb, chb, Cb.row0 + pb) : 0.0;
-    zB[g] = (ok && chb == 0) ? 1.0 : 0.0;
-  }
   if (warp == 1) tmem_alloc(taddr_sh, 512);
   tc_fence_before();
   __syncthreads();
@@ -167,26 +164,30 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
   const uint32_t tbase = *taddr_sh;
 
   if (warp == 0) {
-    // ---- TMA producer: every phase's K-chunks; an A slab every second chunk
+    // ---- TMA producer: every phase's K-chunks of every tile; an A slab every second chunk
     if (lane == 0) {
       int fa = 0, fb = 0;
-      for (int k = 0; k < p.L; ++k) {
-        for (int part = 0; part < 2; ++part) {
-          const int nk = p.nk[k][part];
-          for (int kc = 0; kc < nk; ++kc, ++fb) {
-            if ((kc & 1) == 0) {
-              const int sa = fa % GO_SA;
-              if (fa >= GO_SA) mbar_wait(&emptyA[sa], ((fa / GO_SA) - 1) & 1);
-              mbar_arrive_expect_tx(&fullA[sa], ASLAB);
-              tma_load_3d(ringA + sa * ASLAB, &p.mA[k][part], &fullA[sa], kc * 32,
-                          static_cast<int>(arow0), 0);
-              ++fa;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const GozTile g = goz_tile(p, tile + p.tile0);
+        const int arow0 = static_cast<int>(p.T.c[g.c].act0 + static_cast<long long>(g.ti) * 2 * p.ppc[g.c] * p.nch[g.c]);
+        const int brow0 = static_cast<int>(p.T.c[g.cp].act0 + static_cast<long long>(g.tj) * p.ppc[g.cp] * p.nch[g.cp]);
+        for (int k = 0; k < p.L; ++k) {
+          for (int i = 0; i < goz_nphase(p, k); ++i) {
+            const int part = goz_part(p, k, i);
+            const int nk = p.nk[k][part];
+            for (int kc = 0; kc < nk; ++kc, ++fb) {
+              if ((kc & 1) == 0) {
+                const int sa = fa % GO_SA;
+                if (fa >= GO_SA) mbar_wait(&emptyA[sa], ((fa / GO_SA) - 1) & 1);
+                mbar_arrive_expect_tx(&fullA[sa], ASLAB);
+                tma_load_3d(ringA + sa * ASLAB, &p.mA[k][part], &fullA[sa], kc * 32, arow0, 0);
+                ++fa;
+              }
+              const int sb = fb % GO_SB;
+              if (fb >= GO_SB) mbar_wait(&emptyB[sb], ((fb / GO_SB) - 1) & 1);
+              mbar_arrive_expect_tx(&fullB[sb], BCHUNK);
+              tma_load_3d(ringB + sb * BCHUNK, &p.mB[k][part], &fullB[sb], kc * 32, brow0, 0);
             }
-            const int sb = fb % GO_SB;
-            if (fb >= GO_SB) mbar_wait(&emptyB[sb], ((fb / GO_SB) - 1) & 1);
-            mbar_arrive_expect_tx(&fullB[sb], BCHUNK);
-            tma_load_3d(ringB + sb * BCHUNK, &p.mB[k][part], &fullB[sb], kc * 32,
-                        static_cast<int>(brow0), 0);
           }
         }
       }
@@ -195,35 +196,36 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
     // ---- MMA issuer
     constexpr uint32_t idesc = umma_idesc_s8(OZ_BM, OZ_BN);
     int fa = 0, fb = 0, ph = 0;
-    for (int k = 0; k < p.L; ++k) {
-      for (int part = 0; part < 2; ++part) {
-        const int nk = p.nk[k][part];
-        if (nk == 0) continue;
-        if (ph > 0) mbar_wait(tempty, (ph - 1) & 1);  // epilogue drained the last phase
-        tc_fence_after();
-        for (int kc = 0; kc < nk; ++kc, ++fb) {
-          const int sa = fa % GO_SA, sb = fb % GO_SB;
-          if ((kc & 1) == 0) mbar_wait(&fullA[sa], (fa / GO_SA) & 1);
-          mbar_wait(&fullB[sb], (fb / GO_SB) & 1);
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int k = 0; k < p.L; ++k) {
+        for (int i = 0; i < goz_nphase(p, k); ++i) {
+          const int nk = p.nk[k][goz_part(p, k, i)];
+          if (ph > 0) mbar_wait(tempty, (ph - 1) & 1);  // epilogue drained the last phase
           tc_fence_after();
-          const bool last_of_slab = (kc & 1) == 1 || kc == nk - 1;
-          if (lane == 0) {
-            const uint32_t a0 = smem_u32(ringA + sa * ASLAB) + 32 * (kc & 1);
-            const uint32_t b0 = smem_u32(ringB + sb * BCHUNK);
-            if (p.dbg == 1) {
-              oz_issue_chunk<S, 64, 32>(tbase, OZ_BN, a0, OZ_BM * 64, b0, OZ_BN * 32, idesc, kc == 0);
-            } else if (p.dbg == 2 || p.dbg == 3) {
-            } else {
-              oz_issue_chunk_wide<S, 64, 32>(tbase, a0, OZ_BM * 64, b0, OZ_BN * 32, kc == 0);
+          for (int kc = 0; kc < nk; ++kc, ++fb) {
+            const int sa = fa % GO_SA, sb = fb % GO_SB;
+            if ((kc & 1) == 0) mbar_wait(&fullA[sa], (fa / GO_SA) & 1);
+            mbar_wait(&fullB[sb], (fb / GO_SB) & 1);
+            tc_fence_after();
+            const bool last_of_slab = (kc & 1) == 1 || kc == nk - 1;
+            if (lane == 0) {
+              const uint32_t a0 = smem_u32(ringA + sa * ASLAB) + 32 * (kc & 1);
+              const uint32_t b0 = smem_u32(ringB + sb * BCHUNK);
+              if (p.dbg == 1) {
+                oz_issue_chunk<S, 64, 32>(tbase, OZ_BN, a0, OZ_BM * 64, b0, OZ_BN * 32, idesc, kc == 0);
+              } else if (p.dbg == 2 || p.dbg == 3) {
+              } else {
+                oz_issue_chunk_wide<S, 64, 32>(tbase, a0, OZ_BM * 64, b0, OZ_BN * 32, kc == 0);
+              }
+              umma_commit(&emptyB[sb]);
+              if (last_of_slab) umma_commit(&emptyA[sa]);
+              if (kc == nk - 1) umma_commit(tfull);
             }
-            umma_commit(&emptyB[sb]);
-            if (last_of_slab) umma_commit(&emptyA[sa]);
-            if (kc == nk - 1) umma_commit(tfull);
+            __syncwarp();
+            if (last_of_slab) ++fa;
           }
-          __syncwarp();
-          if (last_of_slab) ++fa;
+          ++ph;
         }
-        ++ph;
       }
     }
   } else {
@@ -231,80 +233,105 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
     const int q = warp & 3, hh = (warp - 2) >> 2;
     const int row = 32 * q + lane, col0 = 32 * hh;
     const uint32_t tl = tbase + (static_cast<uint32_t>(32 * q) << 16);
-    const long long arow = arow0 + row;
-    double G[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) G[j] = 0.0;
     int ph = 0;
-    for (int k = 0; k < p.L; ++k) {
-      const bool seeds = p.nk[k][1] == 0;  // output layer: G^Z = seed_row seed_col
-      for (int part = 0; part < 2; ++part) {
-        if (p.nk[k][part] == 0) continue;
-        mbar_wait(tfull, ph & 1);
-        tc_fence_after();
-        if (p.dbg >= 3) {  // timing experiments: no drain
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(tempty);
-          ++ph;
-          continue;
-        }
-        const double* scv = p.sc[k][part];
-        const double sr = arow < p.R ? scv[arow] : 0.0;
-        // this warp's 32 column scales: lane j holds column col0 + j (shuffled below)
-        const long long bl = brow0 + col0 + lane;
-        const double scl = bl < p.R ? scv[bl] : 0.0;
-        const double za = zA[row], sar = sA[row];
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const GozTile g = goz_tile(p, tile + p.tile0);
+      const int c = g.c, cp = g.cp;
+      const int na = p.nch[c], nb = p.nch[cp];
+      const int np_r = 2 * p.ppc[c], np_c = p.ppc[cp];
+      const int P0 = g.ti * np_r, Q0 = g.tj * np_c;
+      const ClassDev& Ca = p.T.c[c];
+      const ClassDev& Cb = p.T.c[cp];
+      const long long arow0 = Ca.act0 + static_cast<long long>(P0) * na;
+      const long long brow0 = Cb.act0 + static_cast<long long>(Q0) * nb;
+      // row seeds / value flags of this tile (the previous tile's last use of them was
+      // its final drain; the barrier also orders the previous reduction's PH reads
+      // before this tile's first PH writes)
+      if (threadIdx.x < 64 + OZ_BM) {
+        const int gi = threadIdx.x - 64;
+        const int cha = gi % na, pa = P0 + gi / na;
+        const bool ok = gi < np_r * na && pa < Ca.count;
+        sA[gi] = ok ? seedc(p.T, Ca, cha, Ca.row0 + pa) : 0.0;
+        zA[gi] = (ok && cha == 0) ? 1.0 : 0.0;
+      } else if (threadIdx.x < 64 + OZ_BM + OZ_BN) {
+        const int gi = threadIdx.x - 64 - OZ_BM;
+        const int chb = gi % nb, pb = Q0 + gi / nb;
+        const bool ok = gi < np_c * nb && pb < Cb.count;
+        sB[gi] = ok ? seedc(p.T, Cb, chb, Cb.row0 + pb) : 0.0;
+        zB[gi] = (ok && chb == 0) ? 1.0 : 0.0;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const long long arow = arow0 + row;
+      double G[32];
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          int32_t acc[S][8];
-#pragma unroll
-          for (int d = 0; d < S; ++d) tmem_ld8(tl + d * OZ_BN + col0 + 8 * cc, acc[d]);
-          tmem_ld_wait();
-          if (cc == 3) {  // every diagonal is in registers: hand TMEM to the next phase
+      for (int j = 0; j < 32; ++j) G[j] = 0.0;
+      for (int k = 0; k < p.L; ++k) {
+        const bool seeds = p.nk[k][1] == 0;  // output layer: G^Z = seed_row seed_col
+        for (int i = 0; i < goz_nphase(p, k); ++i) {
+          const int part = goz_part(p, k, i);
+          mbar_wait(tfull, ph & 1);
+          tc_fence_after();
+          if (p.dbg >= 3) {  // timing experiments: no drain
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty);
+            ++ph;
+            continue;
           }
+          const double* scv = p.sc[k][part];
+          const double sr = arow < p.R ? scv[arow] : 0.0;
+          // this warp's 32 column scales: lane j holds column col0 + j (shuffled below)
+          const long long bl = brow0 + col0 + lane;
+          const double scl = bl < p.R ? scv[bl] : 0.0;
+          const double za = zA[row], sar = sA[row];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int gc = col0 + 8 * cc + j;
-            const double scol = __shfl_sync(0xffffffffu, scl, 8 * cc + j);
-            int32_t a[S];
+          for (int cc = 0; cc < 4; ++cc) {
+            int32_t acc[S][8];
 #pragma unroll
-            for (int d = 0; d < S; ++d) a[d] = acc[d][j];
-            const double v = oz_combine<S>(a) * (sr * scol);
-            if (part == 0) {
-              const double vh = fma(za, zB[gc], v);  // + bias entry (value channels)
-              if (seeds) {
-                G[8 * cc + j] = fma(vh, sar * sB[gc], G[8 * cc + j]);
+            for (int d = 0; d < S; ++d) tmem_ld8(tl + d * OZ_BN + col0 + 8 * cc, acc[d]);
+            tmem_ld_wait();
+            if (cc == 3) {  // every diagonal is in registers: hand TMEM to the next phase
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(tempty);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int gc = col0 + 8 * cc + j;
+              const double scol = __shfl_sync(0xffffffffu, scl, 8 * cc + j);
+              int32_t a[S];
+#pragma unroll
+              for (int d = 0; d < S; ++d) a[d] = acc[d][j];
+              const double v = oz_combine<S>(a) * (sr * scol);
+              if (part == 1) {
+                PH[gc * OZ_BM + row] = v;  // G^Z, parked for the H phase
               } else {
-                PH[gc * OZ_BM + row] = vh;
+                const double vh = fma(za, zB[gc], v);  // + bias entry (value channels)
+                G[8 * cc + j] = seeds ? fma(vh, sar * sB[gc], G[8 * cc + j])
+                                      : fma(PH[gc * OZ_BM + row], vh, G[8 * cc + j]);
               }
-            } else {
-              G[8 * cc + j] = fma(PH[gc * OZ_BM + row], v, G[8 * cc + j]);
             }
           }
+          ++ph;
         }
-        ++ph;
       }
-    }
-    // ---- G tile to shared memory (PH is free: the last phase was the output layer's H)
+      // ---- G tile to shared memory (PH is free: the last phase was the output layer's H)
 #pragma unroll
-    for (int j = 0; j < 32; ++j) PH[(col0 + j) * OZ_BM + row] = G[j];
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    const long long cnt_r = Ca.count, cnt_c = Cb.count;
-    for (int e = threadIdx.x - 64; e < np_r * np_c; e += 256) {
-      const int r = e / np_c, cc = e - (e / np_c) * np_c;
-      const long long pr = P0 + r, pcl = Q0 + cc;
-      if (pr >= cnt_r || pcl >= cnt_c) continue;
-      const long long grow = Ca.row0 + pr, gcol = Cb.row0 + pcl;
-      if (c == cp && gcol > grow) continue;
-      double v = 0.0;
-      for (int a = 0; a < na; ++a)
-        for (int b = 0; b < nb; ++b) v += PH[(cc * nb + b) * OZ_BM + r * na + a];
-      p.K[grow * p.ldK + gcol] = v;
-      p.K[gcol * p.ldK + grow] = v;
+      for (int j = 0; j < 32; ++j) PH[(col0 + j) * OZ_BM + row] = G[j];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const long long cnt_r = Ca.count, cnt_c = Cb.count;
+      for (int e = threadIdx.x - 64; e < np_r * np_c; e += 256) {
+        const int r = e / np_c, cc = e - (e / np_c) * np_c;
+        const long long pr = P0 + r, pcl = Q0 + cc;
+        if (pr >= cnt_r || pcl >= cnt_c) continue;
+        const long long grow = Ca.row0 + pr, gcol = Cb.row0 + pcl;
+        if (c == cp && gcol > grow) continue;
+        double v = 0.0;
+        for (int a = 0; a < na; ++a)
+          for (int b = 0; b < nb; ++b) v += PH[(cc * nb + b) * OZ_BM + r * na + a];
+        p.K[grow * p.ldK + gcol] = v;
+        p.K[gcol * p.ldK + grow] = v;
+      }
     }
   }
   tc_fence_before();

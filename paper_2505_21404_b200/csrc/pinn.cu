@@ -2742,7 +2742,8 @@ extern "C" int dngd_gram_oz_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_status(ctx, e, "gram_oz smem attribute");
-  kern<<<static_cast<unsigned>(t1 - t0), OZ_THREADS, smem, s>>>(gp);
+  const int ntiles = static_cast<int>(t1 - t0);
+  kern<<<static_cast<unsigned>(std::min(ntiles, ctx->num_sms)), OZ_THREADS, smem, s>>>(gp, ntiles);
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa;

@@ -226,7 +226,14 @@ DNGD_DEV double oz_combine(const int32_t (&acc)[S]) {
   // sum_{D<4} acc_D 2^{-7(D+2)} = hi 2^-35; sum_{4<=D<S} acc_D 2^{-7(D+2)} = lo 2^{-7(S+1)}
   static_assert(S >= 5 && S <= 8, "4 + 1..4 diagonals");
   constexpr double kLo = S == 8 ? 0x1p-63 : S == 7 ? 0x1p-56 : S == 6 ? 0x1p-49 : 0x1p-42;
-  return fma(static_cast<double>(lo), kLo, static_cast<double>(hi) * 0x1p-35);
+  // int64 -> double without I2F: |hi|, |lo| < 2^51 (K <= 32768), so adding them to
+  // the bit pattern of 1.5 2^52 ulp lands exactly on magic + hi ulp (one integer add,
+  // no carry out of the mantissa).  ulp(M1) = 2^-35, ulp(M2) = kLo.
+  constexpr double M1 = 0x1.8p17;
+  constexpr double M2 = kLo * 0x1.8p52;
+  const double a = __longlong_as_double(__double_as_longlong(M1) + hi) - (M1 + M2);  // hi 2^-35 - M2, exact
+  const double b = __longlong_as_double(__double_as_longlong(M2) + lo);              // M2 + lo kLo, exact
+  return a + b;  // = round(hi 2^-35 + lo kLo): the same single rounding as fma(lo, kLo, hi 2^-35)
 }
 
 }  // namespace dngd

@@ -43,7 +43,9 @@ struct GozParams {
   double* K;
   long long ldK;
   int tile0;
-  int dbg;  // timing experiments only: 1 = issue only the products with t + u <= 3
+  int dbg;  // timing experiments only (tools/goz_dbg.sh): 1 narrow MMAs, 2 no MMA, 3 no MMA no drain,
+           // 4 no drain, 5 no TMA no drain, 6 = 5 with narrow MMAs, 7 = 5 without the TMEM hand-off wait,
+           // 8 = 7 without operand waits (MMA issue alone)
 };
 
 // lower-triangle tile t of TI row tiles (row tile ti spans column tiles 2ti, 2ti+1)
@@ -94,6 +96,7 @@ DNGD_DEV void goz_wait_sleep(uint64_t* bar, uint32_t parity) {
 // box row per cycle per SM (tools/micro/tma_rate.cu), so A's rows carry two MMA
 // K-steps each; B keeps the narrow rows so the whole ring + G^H fits in 227 KB.
 constexpr int GO_SA = 2, GO_SB = 3;
+
 
 // tile t (relative to p.tile0) -> (class pair, row tile, column tile)
 struct GozTile {
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
       mbar_init(&emptyB[i], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 8);
+    mbar_init(tempty, OZ_EPI);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(taddr_sh, 512);
@@ -165,7 +168,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
 
   if (warp == 0) {
     // ---- TMA producer: every phase's K-chunks of every tile; an A slab every second chunk
-    if (lane == 0) {
+    if (lane == 0 && p.dbg != 8) {
       int fa = 0, fb = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const GozTile g = goz_tile(p, tile + p.tile0);
@@ -179,39 +182,49 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
               if ((kc & 1) == 0) {
                 const int sa = fa % GO_SA;
                 if (fa >= GO_SA) mbar_wait(&emptyA[sa], ((fa / GO_SA) - 1) & 1);
-                mbar_arrive_expect_tx(&fullA[sa], ASLAB);
-                tma_load_3d(ringA + sa * ASLAB, &p.mA[k][part], &fullA[sa], kc * 32, arow0, 0);
+                if (p.dbg >= 5) {
+                  mbar_arrive(&fullA[sa]);
+                } else {
+                  mbar_arrive_expect_tx(&fullA[sa], ASLAB);
+                  tma_load_3d(ringA + sa * ASLAB, &p.mA[k][part], &fullA[sa], kc * 32, arow0, 0);
+                }
                 ++fa;
               }
               const int sb = fb % GO_SB;
               if (fb >= GO_SB) mbar_wait(&emptyB[sb], ((fb / GO_SB) - 1) & 1);
-              mbar_arrive_expect_tx(&fullB[sb], BCHUNK);
-              tma_load_3d(ringB + sb * BCHUNK, &p.mB[k][part], &fullB[sb], kc * 32, brow0, 0);
+              if (p.dbg >= 5) {
+                mbar_arrive(&fullB[sb]);
+              } else {
+                mbar_arrive_expect_tx(&fullB[sb], BCHUNK);
+                tma_load_3d(ringB + sb * BCHUNK, &p.mB[k][part], &fullB[sb], kc * 32, brow0, 0);
+              }
             }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer
+    // ---- MMA issuer: lane 0 alone waits and issues (no warp-wide mbarrier polling)
     constexpr uint32_t idesc = umma_idesc_s8(OZ_BM, OZ_BN);
     int fa = 0, fb = 0, ph = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      for (int k = 0; k < p.L; ++k) {
-        for (int i = 0; i < goz_nphase(p, k); ++i) {
-          const int nk = p.nk[k][goz_part(p, k, i)];
-          if (ph > 0) mbar_wait(tempty, (ph - 1) & 1);  // epilogue drained the last phase
-          tc_fence_after();
-          for (int kc = 0; kc < nk; ++kc, ++fb) {
-            const int sa = fa % GO_SA, sb = fb % GO_SB;
-            if ((kc & 1) == 0) mbar_wait(&fullA[sa], (fa / GO_SA) & 1);
-            mbar_wait(&fullB[sb], (fb / GO_SB) & 1);
+    if (lane == 0) {
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int k = 0; k < p.L; ++k) {
+          for (int i = 0; i < goz_nphase(p, k); ++i) {
+            const int nk = p.nk[k][goz_part(p, k, i)];
+            if (ph > 0 && p.dbg < 7) mbar_wait(tempty, (ph - 1) & 1);  // epilogue drained the last phase
             tc_fence_after();
-            const bool last_of_slab = (kc & 1) == 1 || kc == nk - 1;
-            if (lane == 0) {
+            for (int kc = 0; kc < nk; ++kc, ++fb) {
+              const int sa = fa % GO_SA, sb = fb % GO_SB;
+              if (p.dbg != 8) {
+                if ((kc & 1) == 0) mbar_wait(&fullA[sa], (fa / GO_SA) & 1);
+                mbar_wait(&fullB[sb], (fb / GO_SB) & 1);
+              }
+              tc_fence_after();
+              const bool last_of_slab = (kc & 1) == 1 || kc == nk - 1;
               const uint32_t a0 = smem_u32(ringA + sa * ASLAB) + 32 * (kc & 1);
               const uint32_t b0 = smem_u32(ringB + sb * BCHUNK);
-              if (p.dbg == 1) {
+              if (p.dbg == 1 || p.dbg == 6) {
                 oz_issue_chunk<S, 64, 32>(tbase, OZ_BN, a0, OZ_BM * 64, b0, OZ_BN * 32, idesc, kc == 0);
               } else if (p.dbg == 2 || p.dbg == 3) {
               } else {
@@ -220,18 +233,19 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
               umma_commit(&emptyB[sb]);
               if (last_of_slab) umma_commit(&emptyA[sa]);
               if (kc == nk - 1) umma_commit(tfull);
+              if (last_of_slab) ++fa;
             }
-            __syncwarp();
-            if (last_of_slab) ++fa;
+            ++ph;
           }
-          ++ph;
         }
       }
     }
+    __syncwarp();
   } else {
-    // ---- epilogue: thread owns G-row `row`, G-columns col0 .. col0 + 31
+    // ---- epilogue: thread owns G-row `row`, G-columns col0 .. col0 + OZ_COLS - 1
+    // (warp w reaches TMEM lanes 32 (w % 4) ..; four consecutive warps cover all four)
     const int q = warp & 3, hh = (warp - 2) >> 2;
-    const int row = 32 * q + lane, col0 = 32 * hh;
+    const int row = 32 * q + lane, col0 = OZ_COLS * hh;
     const uint32_t tl = tbase + (static_cast<uint32_t>(32 * q) << 16);
     int ph = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -260,16 +274,20 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
         sB[gi] = ok ? seedc(p.T, Cb, chb, Cb.row0 + pb) : 0.0;
         zB[gi] = (ok && chb == 0) ? 1.0 : 0.0;
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(OZ_ETHREADS) : "memory");
       const long long arow = arow0 + row;
-      double G[32];
+      double G[OZ_COLS];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) G[j] = 0.0;
+      for (int j = 0; j < OZ_COLS; ++j) G[j] = 0.0;
       for (int k = 0; k < p.L; ++k) {
         const bool seeds = p.nk[k][1] == 0;  // output layer: G^Z = seed_row seed_col
         for (int i = 0; i < goz_nphase(p, k); ++i) {
           const int part = goz_part(p, k, i);
-          mbar_wait(tfull, ph & 1);
+          // one thread polls the mbarrier, the other epilogue warps sleep on a named
+          // barrier: eight warps spinning on try_wait took shared-memory cycles from
+          // the tensor core's operand reads (MMA issue alone ran ~35 % slower)
+          if (threadIdx.x == 64) mbar_wait(tfull, ph & 1);
+          asm volatile("bar.sync 2, %0;" ::"n"(OZ_ETHREADS) : "memory");
           tc_fence_after();
           if (p.dbg >= 3) {  // timing experiments: no drain
             tc_fence_before();
@@ -280,25 +298,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
           }
           const double* scv = p.sc[k][part];
           const double sr = arow < p.R ? scv[arow] : 0.0;
-          // this warp's 32 column scales: lane j holds column col0 + j (shuffled below)
+          // this warp's column scales: lane j < OZ_COLS holds column col0 + j (shuffled below)
           const long long bl = brow0 + col0 + lane;
           const double scl = bl < p.R ? scv[bl] : 0.0;
           const double za = zA[row], sar = sA[row];
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            int32_t acc[S][8];
+          for (int cc = 0; cc < OZ_COLS / OZ_LD; ++cc) {
+            int32_t acc[S][OZ_LD];
 #pragma unroll
-            for (int d = 0; d < S; ++d) tmem_ld8(tl + d * OZ_BN + col0 + 8 * cc, acc[d]);
+            for (int d = 0; d < S; ++d) tmem_ld<OZ_LD>(tl + d * OZ_BN + col0 + OZ_LD * cc, acc[d]);
             tmem_ld_wait();
-            if (cc == 3) {  // every diagonal is in registers: hand TMEM to the next phase
+            if (cc == OZ_COLS / OZ_LD - 1) {  // every diagonal is in registers: hand TMEM to the next phase
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(tempty);
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int gc = col0 + 8 * cc + j;
-              const double scol = __shfl_sync(0xffffffffu, scl, 8 * cc + j);
+            for (int j = 0; j < OZ_LD; ++j) {
+              const int gc = col0 + OZ_LD * cc + j;
+              const double scol = __shfl_sync(0xffffffffu, scl, OZ_LD * cc + j);
               int32_t a[S];
 #pragma unroll
               for (int d = 0; d < S; ++d) a[d] = acc[d][j];
@@ -307,8 +325,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
                 PH[gc * OZ_BM + row] = v;  // G^Z, parked for the H phase
               } else {
                 const double vh = fma(za, zB[gc], v);  // + bias entry (value channels)
-                G[8 * cc + j] = seeds ? fma(vh, sar * sB[gc], G[8 * cc + j])
-                                      : fma(PH[gc * OZ_BM + row], vh, G[8 * cc + j]);
+                G[OZ_LD * cc + j] = seeds ? fma(vh, sar * sB[gc], G[OZ_LD * cc + j])
+                                          : fma(PH[gc * OZ_BM + row], vh, G[OZ_LD * cc + j]);
               }
             }
           }
@@ -317,10 +335,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
       }
       // ---- G tile to shared memory (PH is free: the last phase was the output layer's H)
 #pragma unroll
-      for (int j = 0; j < 32; ++j) PH[(col0 + j) * OZ_BM + row] = G[j];
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      for (int j = 0; j < OZ_COLS; ++j) PH[(col0 + j) * OZ_BM + row] = G[j];
+      asm volatile("bar.sync 1, %0;" ::"n"(OZ_ETHREADS) : "memory");
       const long long cnt_r = Ca.count, cnt_c = Cb.count;
-      for (int e = threadIdx.x - 64; e < np_r * np_c; e += 256) {
+      for (int e = threadIdx.x - 64; e < np_r * np_c; e += OZ_ETHREADS) {
         const int r = e / np_c, cc = e - (e / np_c) * np_c;
         const long long pr = P0 + r, pcl = Q0 + cc;
         if (pr >= cnt_r || pcl >= cnt_c) continue;

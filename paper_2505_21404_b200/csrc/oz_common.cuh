@@ -7,7 +7,16 @@ namespace dngd {
 
 constexpr int OZ_BM = 128;  // tile rows = MMA M (TMEM lanes)
 constexpr int OZ_BN = 64;   // tile columns = MMA N; S diagonals x 64 <= 512 TMEM columns
-constexpr int OZ_THREADS = 320;  // warp 0 TMA, warp 1 TMEM + MMA, warps 2-9 epilogue
+// Warp roles: warp 0 TMA, warp 1 TMEM + MMA, warps 2 .. 2 + OZ_EPI - 1 epilogue.
+// OZ_EPI / 4 epilogue warps per TMEM lane quadrant (warp w reaches lanes 32 (w % 4)
+// ..); each thread drains OZ_COLS columns of its row in groups of OZ_LD
+// (tcgen05.ld 32x32b.x{OZ_LD}).  Sixteen warps halve the per-thread drain of eight
+// and keep four warps per scheduler: the MMA warp waits on the drain whenever the
+// S diagonals fill TMEM (S x 64 of 512 columns, no second accumulator set).
+constexpr int OZ_EPI = 16, OZ_LD = 4;
+constexpr int OZ_COLS = OZ_BN / (OZ_EPI / 4);
+constexpr int OZ_ETHREADS = 32 * OZ_EPI;
+constexpr int OZ_THREADS = 64 + OZ_ETHREADS;
 constexpr long long kOzMaxK = 32768;  // |acc_D| <= K (2 127 64 + 6 64^2) < 2^31 (tc05.cuh)
 
 inline long long oz_kpad(long long K) { return (K + 31) / 32 * 32; }

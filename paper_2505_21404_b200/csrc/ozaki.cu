@@ -123,7 +123,7 @@ int oz_encode(dngd_ctx* ctx, CUtensorMap* map, const int8_t* Q, long long rows, 
 // in flight share the 128-row A tile through L2).  Warp 0 streams K-chunks of
 // consecutive tiles through the ring without waiting for epilogues; warp 1 issues
 // a tile's MMAs once the epilogue has drained the previous tile's accumulators;
-// warps 2-9 drain TMEM (fold -> FP64 in registers), release it, then scale and
+// warps 2-17 drain TMEM (fold -> FP64 in registers), release it, then scale and
 // store while the next tile's MMAs run.
 template <int S, int STAGES>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       mbar_init(&empty[i], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 8);
+    mbar_init(tempty, OZ_EPI);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(taddr_sh, 512);
@@ -182,16 +182,15 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = umma_idesc_s8(OZ_BM, OZ_BN);
     int f = 0, it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-      if (it > 0) mbar_wait(tempty, (it - 1) & 1);
-      tc_fence_after();
-      for (int ks = 0; ks < nslab; ++ks, ++f) {
-        const int st = f % STAGES;
-        mbar_wait(&full[st], (f / STAGES) & 1);
+    if (lane == 0) {  // lane 0 alone waits and issues (no warp-wide mbarrier polling)
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        if (it > 0) mbar_wait(tempty, (it - 1) & 1);
         tc_fence_after();
-        if (lane == 0) {
+        for (int ks = 0; ks < nslab; ++ks, ++f) {
+          const int st = f % STAGES;
+          mbar_wait(&full[st], (f / STAGES) & 1);
+          tc_fence_after();
           const uint32_t a0 = smem_u32(smem + st * STAGE);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -202,11 +201,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
           umma_commit(&empty[st]);
           if (ks == nslab - 1) umma_commit(tfull);
         }
-        __syncwarp();
       }
     }
+    __syncwarp();
   } else {
-    const int q = warp & 3, h = (warp - 2) >> 2;
+    const int q = warp & 3, h = (warp - 2) >> 2;  // lane quadrant, column group
     const int row = 32 * q + lane;
     const uint32_t tl = tbase + (static_cast<uint32_t>(32 * q) << 16);
     int it = 0;
@@ -216,40 +215,42 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const double* sa_z = scA + z * a_brows;
       const double* sb_z = scB + z * b_brows;
       const double sa = m0 + row < M ? sa_z[m0 + row] : 0.0;
-      const int cl = n0 + h * (OZ_BN / 2) + lane;
+      const int c0 = h * OZ_COLS;
+      const int cl = n0 + c0 + lane;
       const double scl = cl < N ? sb_z[cl] : 0.0;
-      double v[OZ_BN / 2];
-      mbar_wait(tfull, it & 1);
+      double v[OZ_COLS];
+      if (threadIdx.x == 64) mbar_wait(tfull, it & 1);  // one poller (gram_oz.cuh)
+      asm volatile("bar.sync 1, %0;" ::"n"(OZ_ETHREADS) : "memory");
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < OZ_BN / 2 / 8; ++c) {
-        int32_t acc[S][8];
+      for (int c = 0; c < OZ_COLS / OZ_LD; ++c) {
+        int32_t acc[S][OZ_LD];
 #pragma unroll
-        for (int d = 0; d < S; ++d) tmem_ld8(tl + d * OZ_BN + h * (OZ_BN / 2) + 8 * c, acc[d]);
+        for (int d = 0; d < S; ++d) tmem_ld<OZ_LD>(tl + d * OZ_BN + c0 + OZ_LD * c, acc[d]);
         tmem_ld_wait();
-        if (c == OZ_BN / 2 / 8 - 1) {  // all diagonals in registers: release TMEM
+        if (c == OZ_COLS / OZ_LD - 1) {  // all diagonals in registers: release TMEM
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty);
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < OZ_LD; ++j) {
           int32_t a[S];
 #pragma unroll
           for (int d = 0; d < S; ++d) a[d] = acc[d][j];
-          v[8 * c + j] = oz_combine<S>(a) * (sa * __shfl_sync(0xffffffffu, scl, 8 * c + j));
+          v[OZ_LD * c + j] = oz_combine<S>(a) * (sa * __shfl_sync(0xffffffffu, scl, OZ_LD * c + j));
         }
       }
       if (m0 + row < M) {
-        double* crow = C + z * sC + static_cast<long long>(m0 + row) * ldc + n0 + h * (OZ_BN / 2);
-        const int nvalid = N - (n0 + h * (OZ_BN / 2));
-        if (nvalid >= OZ_BN / 2 && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
+        double* crow = C + z * sC + static_cast<long long>(m0 + row) * ldc + n0 + c0;
+        const int nvalid = N - (n0 + c0);
+        if (nvalid >= OZ_COLS && (reinterpret_cast<uintptr_t>(crow) & 15) == 0) {
 #pragma unroll
-          for (int j = 0; j < OZ_BN / 2; j += 2)
+          for (int j = 0; j < OZ_COLS; j += 2)
             *reinterpret_cast<double2*>(crow + j) = make_double2(v[j], v[j + 1]);
         } else {
 #pragma unroll
-          for (int j = 0; j < OZ_BN / 2; ++j)
+          for (int j = 0; j < OZ_COLS; ++j)
             if (j < nvalid) crow[j] = v[j];
         }
       }

@@ -165,6 +165,18 @@ DNGD_DEV void tmem_ld8(uint32_t taddr, int32_t (&r)[8]) {
       : "r"(taddr)
       : "memory");
 }
+template <int W>
+DNGD_DEV void tmem_ld(uint32_t taddr, int32_t (&r)[W]) {
+  static_assert(W == 4 || W == 8, "x4 / x8");
+  if constexpr (W == 8) {
+    tmem_ld8(taddr, r);
+  } else {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr)
+                 : "memory");
+  }
+}
 DNGD_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 DNGD_DEV bool elect_lane0() { return (threadIdx.x & 31) == 0; }

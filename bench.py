@@ -214,15 +214,19 @@ def _count_our_kernels(fn):
     return n
 
 
-# tcgen05 kind::i8 dense MMA rate measured on this pool's B200 by tools/micro/umma_rate.cu
-# (M = 128, N >= 128, operands resident in shared memory, all 148 SMs): the int8
-# tensor peak the emulated-FP64 kernels run against.  At N = 64 -- the widest tile
-# TMEM allows with 7-8 diagonal accumulators -- the same benchmark floors at ~44.6
-# cycles per MMA, i.e. 3.2 POPS.
-INT8_PEAK_TOPS = 4498.0
-INT8_N64_FLOOR_TOPS = 3207.0
-INT8_PEAK_SOURCE = ("tcgen05.mma kind::i8 M=128 N=128 K=32 issue rate measured by "
-                    "tools/micro/umma_rate.cu (4498 TOPS; 4549 at N=256)")
+# tcgen05 kind::i8 dense MMA rate of the Ozaki kernels' own issue pattern (one MMA
+# per digit slice, N = 64 (S - t), operands resident in shared memory, all 148 SMs;
+# tools/micro/umma_wide.cu, profiles/r02b/int8_mma_*.txt): 920 cycles per 7-digit
+# K-chunk (896 ideal).  With random operand bytes over 1.4 s of back-to-back MMAs the
+# board's power limit holds the chip at 3715 TOPS -- the SUSTAINED peak, the
+# denominator for a kernel timed inside a long step (B200_PROFILING: burst figure
+# for a kernel timed alone, sustained for one inside a step).  The burst rate (2 ms,
+# near-constant operands) is 4446 TOPS.
+INT8_PEAK_TOPS = 3715.0
+INT8_BURST_TOPS = 4446.0
+INT8_PEAK_SOURCE = ("sustained tcgen05.mma kind::i8 rate of the Ozaki chunk pattern with random "
+                    "operands, power-limited steady state (tools/micro/umma_wide.cu 30000 1 40: "
+                    "3715 TOPS; burst with near-constant operands 4446 TOPS)")
 
 
 def _emulated_gram(rmap):
@@ -587,7 +591,8 @@ def run_ours(args, cfg):
                     "kernel_ms": gk_avg * 1e3,
                     "fp64_equivalent_tflops": ach,
                     "fp64_equivalent_frac_of_dmma_peak": ach / fp64_peak,
-                    "n64_mma_floor_tops": INT8_N64_FLOOR_TOPS}
+                    "burst_peak_tops": INT8_BURST_TOPS,
+                    "frac_of_burst_peak": ops / gk_avg / 1e12 / INT8_BURST_TOPS}
         else:
             roof = None
     if gk_avg > 0 and roof is None:

@@ -127,6 +127,10 @@ int main(int argc, char** argv) {
   cudaMemcpyToSymbol(g_random, &rnd, sizeof rnd);
   long long* d;
   cudaMalloc(&d, 8);
+  if (argc > 3) {  // sustained: mode 0 repeated argv[3] times (power-limited steady state)
+    for (int r = 0; r < atoi(argv[3]); ++r) run<0>(d, "wide (N split at 256), A SW64");
+    return 0;
+  }
   run<0>(d, "wide (N split at 256), A SW64");
   run<1>(d, "narrow N=64 x 28, collector A");
   run<2>(d, "wide, A SW32");

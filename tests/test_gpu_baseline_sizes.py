@@ -225,6 +225,62 @@ def test_cfg1_lambda_1e8_divergence_statistics(P):
     assert 0.1 <= stats["final_loss_ratio"] <= 10.0
 
 
+def _traj_pair(P, c, nsteps=20):
+    rows, theta_o = O.dngd_run(c["oprob"](), c["widths"], c["counts"],
+                               O.LoopConfig(lam_cap=c["lam_cap"], max_iters=nsteps), 0,
+                               rel_l2=_eval_rel_l2(P, c))
+    trace = _gpu_trace(P, c, nsteps)
+    loss_g = np.array([r.loss for r in trace.rows])
+    loss_o = np.array([r["loss"] for r in rows])
+    rel_g = np.array([r.rel_l2 for r in trace.rows])
+    rel_o = np.array([r["rel_l2"] for r in rows])
+    eta_g = [r.eta for r in trace.rows][1:]
+    eta_o = [r["eta"] for r in rows][1:]
+    dev = np.abs(loss_g - loss_o) / np.abs(loss_o)
+    stats = {"loss_gpu": loss_g.tolist(), "loss_oracle": loss_o.tolist(),
+             "rel_l2_gpu": rel_g.tolist(), "rel_l2_oracle": rel_o.tolist(),
+             "max_rel_loss": float(np.max(dev)),
+             "max_rel_l2": float(np.max(np.abs(rel_g - rel_o) / rel_o)),
+             "first_divergence_step": next((i for i, d in enumerate(dev) if d > 1e-6), None),
+             "same_eta_rate": float(np.mean(np.array(eta_g) == np.array(eta_o))),
+             "final_loss_ratio": float(loss_g[-1] / loss_o[-1])}
+    assert len(trace.rows) == len(rows) == nsteps + 1
+    return stats, (loss_g, loss_o, rel_g, rel_o, eta_g, eta_o)
+
+
+def test_emulated_path_twenty_step_trajectory(P):
+    """The emulated-FP64 product path (Ozaki int8 tcgen05 Gram, activation, f_vv and
+    line-search GEMMs: every hidden layer >= 128 wide) under the north star's
+    20-step criterion where the problem is well conditioned: config 2's heat
+    problem and lam_cap = 1e-3 at width 128 (700 points, so the oracle's dense J
+    stays small) -- loss and rel-L2 within 1e-6 at every row, the same etas."""
+    from paper_2505_21404_b200 import kernels as K
+
+    c = dict(CFG[2], widths=(2, 128, 128, 128, 128, 1), counts=(500, 100, 100))
+    if os.environ.get("DNGD_GRAM_SLICES") is None:
+        assert K.gram_emulation_slices() == 7
+    stats, (loss_g, loss_o, rel_g, rel_o, eta_g, eta_o) = _traj_pair(P, c)
+    _log("heat1d_w128_emulated_traj20", stats)
+    np.testing.assert_allclose(loss_g, loss_o, rtol=1e-6)
+    np.testing.assert_allclose(rel_g, rel_o, rtol=1e-6)
+    np.testing.assert_array_equal(eta_g, eta_o)
+
+
+def test_cfg3_emulated_divergence_statistics(P):
+    """Config 3's problem and lam_cap = 1e-5 at width 128 (700 + 100 points) on the
+    emulated path.  Like config 1 at lambda = 1e-8 this trajectory is chaotic: the
+    all-FP64 DMMA build (DNGD_GRAM_SLICES=0 DNGD_GEMM_SLICES=0) departs from the
+    oracle by 7.6e-9 after step 1 and 1.4e-6 after step 2 exactly as the emulated
+    build does (profiles/r02b/parity), so the SURVEY 8c.3 statistics are recorded
+    and the first steps, not 20 rows, are held to 1e-6."""
+    c = dict(CFG[3], counts=(700, 100))
+    stats, (loss_g, loss_o, *_rest) = _traj_pair(P, c)
+    _log("cfg3_w128_emulated_divergence", stats)
+    assert abs(loss_g[1] - loss_o[1]) / loss_o[1] <= 1e-6
+    assert stats["first_divergence_step"] is None or stats["first_divergence_step"] >= 2
+    assert 0.1 <= stats["final_loss_ratio"] <= 10.0
+
+
 def test_cfg3_structure_width128_step(P):
     """Config 3's problem and m = 4000 (nch = 7 interior channel map, 500 faces) at
     width 128: one step vs the oracle (the materialised oracle J is 1.6 GB here)."""

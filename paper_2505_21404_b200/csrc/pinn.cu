@@ -206,113 +206,278 @@ __global__ void k_tanh_fwd(Classes T, double* __restrict__ Z, double* __restrict
   }
 }
 
-// k_tanh_fwd fused with the Ozaki slicing of its output (line-search forward):
-// one CTA per (point, candidate), thread g owns neurons 4g..4g+3 of every channel
-// row; the channel map is k_tanh_fwd's, each row's scale and digits follow
-// k_oz_slice exactly (same scale rule, same digits), and H itself never reaches
-// HBM -- only the next GEMM's digit planes (rows cand R + act row) and scales.
+// Channel map of one layer fused with the Ozaki slicing of its output (line-search
+// forward): the rows never reach HBM in FP64, only the next GEMM's digit planes
+// (rows cand R + act row) and row scales.  MODE 0: hidden layer, Z + bias -> tanh
+// channels (k_tanh_fwd's map); MODE 1: input layer from the points and W0 (plain
+// inputs; k_input_fwd's map).  Same operation order as those kernels, and the
+// scale rule and digits of k_oz_slice, so the planes equal slicing their output.
+// One warp per (point, candidate): lane l owns neurons 4 (l + 32 k) .. + 3 of every
+// channel row; pass 1 computes the channel values and the per-row max |v| (warp
+// shuffles only, no block barrier), pass 2 recomputes them (operands from L1/L2)
+// and writes the digits -- a short dependent chain per warp and many warps per SM
+// (the CTA-per-point version was latency-bound at ~1 TB/s).
 constexpr int kTsMaxCh = 8;
-template <int S, int NCH>
-__global__ void k_tanh_slice(Classes T, int cls, const double* __restrict__ Z, int w, long long ld,
-                             const double* __restrict__ bias, long long bias_s, long long act_s,
-                             long long R, long long kpad, int8_t* __restrict__ Q,
-                             double* __restrict__ scale) {
-  __shared__ double red[NCH][32];
-  __shared__ int redbad[NCH][32];
-  const ClassDev& C = T.c[cls];
-  const long long i = blockIdx.x;
-  const int cand = blockIdx.y;
-  const double* z0 = Z + cand * act_s + (C.act0 + i * NCH) * ld;
-  const double* bs = bias + cand * bias_s;
-  const long long row0 = cand * R + C.act0 + i * NCH;
-  const int g = threadIdx.x, lane = g & 31, wp = g >> 5;
-  const int q0 = 4 * g;
-  double v[NCH][4];
+constexpr int kCsWarps = 8;  // points per 256-thread CTA
+
+// per-class constants of the channel map held in registers (the kernels index the
+// Classes parameter block by a run-time class, which would otherwise be re-read
+// from a local-memory copy inside the neuron loop)
+template <int NCH>
+struct ChanRegs {
+  int ngrad;
+  unsigned lapmask;  // bit ch: channel ch is summed into the Laplacian (C.lap_ch)
+  int gd[NCH > 1 ? NCH - 1 : 1];  // derivative dims (class-wide; pgi overrides per point)
+};
+
+// channel values of neuron q of one (point, candidate) (0 past w); the Laplacian's
+// sum runs over the channels in ascending order -- k_tanh_fwd / k_input_fwd's
+// order when C.lap_ch is ascending, which the launcher requires
+template <int NCH, int MODE>
+DNGD_DEV void chan_val1(const Classes& T, const ChanRegs<NCH>& cr, const int* pgi, const double* z0,
+                        long long ld, const double* bs, const double* W0, const double* b0,
+                        const double* x, int w, int q, double (&v)[NCH]) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int q = q0 + j;
+  for (int ch = 0; ch < NCH; ++ch) v[ch] = 0.0;
+  if (q >= w) return;
+  if constexpr (MODE == 0) {
+    double zz[NCH];
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) v[ch][j] = 0.0;
-    if (q < w) {
-      const double z = z0[q] + bs[q];
-      const double t = tanh(z), sd = 1.0 - t * t;
-      v[0][j] = t;
+    for (int ch = 0; ch < NCH; ++ch) zz[ch] = z0[ch * ld + q];
+    const double z = zz[0] + bs[q];
+    const double t = tanh(z), sd = 1.0 - t * t;
+    v[0] = t;
 #pragma unroll
-      for (int gi = 0; gi < NCH - 1; ++gi)
-        if (gi < C.ngrad) v[1 + gi][j] = sd * z0[(1 + gi) * ld + q];
-      if (NCH > 1 && C.nlap) {
-        double G = 0.0;
-        for (int l = 0; l < C.nlap; ++l) {
-          const double dz = z0[C.lap_ch[l] * ld + q];
-          G = fma(dz, dz, G);
-        }
-        v[NCH - 1][j] = sd * z0[(NCH - 1) * ld + q] - 2.0 * t * sd * G;
+    for (int gi = 0; gi < NCH - 1; ++gi)
+      if (gi < cr.ngrad) v[1 + gi] = sd * zz[1 + gi];
+    if (NCH > 1 && cr.lapmask) {
+      double G = 0.0;
+#pragma unroll
+      for (int ch = 1; ch < NCH; ++ch)
+        if ((cr.lapmask >> ch) & 1u) G = fma(zz[ch], zz[ch], G);
+      v[NCH - 1] = sd * zz[NCH - 1] - 2.0 * t * sd * G;
+    }
+  } else {
+    double z = b0[q];
+    for (int d = 0; d < T.din; ++d) z = fma(x[d], W0[d * w + q], z);
+    const double t = tanh(z), sd = 1.0 - t * t;
+    v[0] = t;
+    double G = 0.0;
+#pragma unroll
+    for (int gi = 0; gi < NCH - 1; ++gi) {
+      if (gi < cr.ngrad) {
+        const double dz = W0[static_cast<long long>(pgi ? pgi[gi] : cr.gd[gi]) * w + q];
+        v[1 + gi] = sd * dz;
+        if ((cr.lapmask >> (1 + gi)) & 1u) G = fma(dz, dz, G);
       }
     }
+    if (NCH > 1 && cr.lapmask) v[NCH - 1] = -2.0 * t * sd * G;
   }
-  // per channel row: max |v| and non-finite flag over the block
+}
+
+template <int S, int NCH, int MODE>
+__global__ void __launch_bounds__(32 * kCsWarps) k_chan_slice(
+    Classes T, int cls, const double* __restrict__ Z, int w, long long ld,
+    const double* __restrict__ par, long long par_s, long long act_s, long long R, long long kpad,
+    int8_t* __restrict__ Q, double* __restrict__ scale) {
+  const ClassDev& C = T.c[cls];
+  const long long i = static_cast<long long>(blockIdx.x) * kCsWarps + (threadIdx.x >> 5);
+  if (i >= C.count) return;
+  const int lane = threadIdx.x & 31;
+  const int cand = blockIdx.y;
+  // MODE 0: par = bias of every candidate; MODE 1: par = the candidates' thetas
+  const double* z0 = MODE == 0 ? Z + cand * act_s + (C.act0 + i * NCH) * ld : nullptr;
+  const double* bs = par + cand * par_s;
+  const double* W0 = par + cand * par_s;
+  const double* b0 = W0 + static_cast<long long>(T.din) * w;
+  const double* x = MODE == 1 ? C.pts + i * T.din : nullptr;
+  const long long row0 = cand * R + C.act0 + i * NCH;
+  ChanRegs<NCH> cr;
+  cr.ngrad = C.ngrad;
+  cr.lapmask = 0;
+  for (int l = 0; l < C.nlap; ++l) cr.lapmask |= 1u << C.lap_ch[l];
+#pragma unroll
+  for (int g = 0; g < (NCH > 1 ? NCH - 1 : 1); ++g) cr.gd[g] = g < C.ngrad ? C.grad_dims[g] : 0;
+  const int* pgi = C.pgi ? C.pgi + i * C.ngrad : nullptr;
+  double mx[NCH];
+  int bad[NCH];
 #pragma unroll
   for (int ch = 0; ch < NCH; ++ch) {
-    double mx = 0.0;
-    int bad = 0;
+    mx[ch] = 0.0;
+    bad[ch] = 0;
+  }
+  // lane owns neurons lane, lane + 32, ...: coalesced operand rows, one digit byte
+  // per (slice, row) and neuron -- 32 consecutive bytes per warp store
+  for (int q = lane; q < w; q += 32) {
+    double v[NCH];
+    chan_val1<NCH, MODE>(T, cr, pgi, z0, ld, bs, W0, b0, x, w, q, v);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      bad |= !isfinite(v[ch][j]);
-      mx = fmax(mx, fabs(v[ch][j]));
+    for (int ch = 0; ch < NCH; ++ch) {
+      bad[ch] |= !isfinite(v[ch]);
+      mx[ch] = fmax(mx[ch], fabs(v[ch]));
     }
+  }
+  double sinv[NCH];
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+      mx[ch] = fmax(mx[ch], __shfl_xor_sync(0xffffffffu, mx[ch], o));
+      bad[ch] |= __shfl_xor_sync(0xffffffffu, bad[ch], o);
     }
-    if (lane == 0) {
-      red[ch][wp] = mx;
-      redbad[ch][wp] = bad;
-    }
+    const int e = bad[ch] ? 0 : oz_row_exponent(mx[ch]);
+    if (lane == ch) scale[row0 + ch] = bad[ch] ? CUDART_NAN : ldexp(1.0, e);
+    sinv[ch] = ldexp(1.0, 7 * S - e);
   }
-  __syncthreads();
-  const int nw = (blockDim.x + 31) >> 5;
   const size_t plane = static_cast<size_t>(gridDim.y) * R * kpad;
+  for (int q = lane; q < kpad; q += 32) {
+    double v[NCH];
+    chan_val1<NCH, MODE>(T, cr, pgi, z0, ld, bs, W0, b0, x, w, q, v);
 #pragma unroll
-  for (int ch = 0; ch < NCH; ++ch) {
-    double mx = 0.0;
-    int bad = 0;
-    for (int k = 0; k < nw; ++k) {
-      mx = fmax(mx, red[ch][k]);
-      bad |= redbad[ch][k];
-    }
-    const int e = bad ? 0 : oz_row_exponent(mx);
-    if (g == 0) scale[row0 + ch] = bad ? CUDART_NAN : ldexp(1.0, e);
-    if (q0 < kpad) {
-      uint32_t packed[S];
-      oz_digits4<S>(v[ch], ldexp(1.0, 7 * S - e), bad != 0, packed);
+    for (int ch = 0; ch < NCH; ++ch) {
+      // oz_digits4's balanced base-128 digits of X = rint(v 2^(7S - e)), in 32-bit
+      // integers: X = Xh 2^(7L) + Xl with Xh = floor((X + c_L) / 2^(7L)), c_L the
+      // bottom-up carry offset 64 (1 + 128 + ... + 128^(L-1)), so Xl's L balanced
+      // digits end without a carry and Xh (|Xh| < 2^28) holds the top 4 -- the same
+      // digits as the int64 recurrence, with exact FP64 splitting
+      constexpr int Ld = S - 4;
+      constexpr double cL = Ld == 4 ? 64.0 * (1 + 128 + 16384 + 2097152)
+                                    : Ld == 3 ? 64.0 * (1 + 128 + 16384) : 64.0 * (1 + 128);
+      constexpr double sh = Ld == 4 ? 0x1p28 : Ld == 3 ? 0x1p21 : 0x1p14;
+      const double X = bad[ch] ? 0.0 : rint(v[ch] * sinv[ch]);
+      const double Xh = floor((X + cL) * (1.0 / sh));
+      int ul = __double2int_rn(fma(-Xh, sh, X));
+      int uh = __double2int_rn(Xh);
+      int8_t* dst = Q + (row0 + ch) * kpad + q;
 #pragma unroll
-      for (int t = 0; t < S; ++t)
-        reinterpret_cast<uint32_t*>(Q + t * plane + (row0 + ch) * kpad)[g] = packed[t];
+      for (int t = S - 1; t >= 4; --t) {
+        const int tt = ul + 64;
+        dst[t * plane] = static_cast<int8_t>((tt & 127) - 64);
+        ul = tt >> 7;
+      }
+#pragma unroll
+      for (int t = 3; t >= 1; --t) {
+        const int tt = uh + 64;
+        dst[t * plane] = static_cast<int8_t>((tt & 127) - 64);
+        uh = tt >> 7;
+      }
+      dst[0] = static_cast<int8_t>(uh);
     }
   }
 }
 
-// k_tanh_slice for every class (the channel count is a template parameter)
+// Last hidden layer of the line-search forward fused with the output layer:
+// k_tanh_fwd's channel map of one (point, candidate) straight into k_head's
+// channel dot products and residual (same per-lane order over neurons, same warp
+// tree, same residual arithmetic), so H_{L-1} never reaches HBM.  One warp per
+// point of class cls, grid.y = candidates.
+template <int NCH>
+__global__ void __launch_bounds__(256) k_tanh_head(Classes T, int cls, const double* __restrict__ Z,
+                                                   int w, long long ld,
+                                                   const double* __restrict__ thetas,
+                                                   long long th_s, long long bias_off,
+                                                   long long wl_off, long long act_s,
+                                                   double* __restrict__ r, long long r_s) {
+  const ClassDev& C = T.c[cls];
+  const long long i = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (i >= C.count) return;
+  const int lane = threadIdx.x & 31;
+  const int cand = blockIdx.y;
+  const double* th = thetas + cand * th_s;
+  const double* bs = th + bias_off;
+  const double* WL = th + wl_off;
+  const double* z0 = Z + cand * act_s + (C.act0 + i * NCH) * ld;
+  ChanRegs<NCH> cr;
+  cr.ngrad = C.ngrad;
+  cr.lapmask = 0;
+  for (int l = 0; l < C.nlap; ++l) cr.lapmask |= 1u << C.lap_ch[l];
+  double u[NCH];
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) u[ch] = 0.0;
+  for (int q = lane; q < w; q += 32) {
+    double v[NCH];
+    chan_val1<NCH, 0>(T, cr, nullptr, z0, ld, bs, nullptr, nullptr, nullptr, w, q, v);
+    const double wq = WL[q];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) u[ch] = fma(v[ch], wq, u[ch]);
+  }
+  double res = 0.0, uv = 0.0;
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    double uc = warp_sum(u[ch]);
+    if (ch == 0) {
+      uc += WL[w];
+      uv = uc;
+    }
+    res = fma(coefp(C, ch, i), uc, res);
+  }
+  if (C.c3 != 0.0) res = fma(C.c3 * uv * uv, uv, res);
+  const long long p = C.row0 + i;
+  if (lane == 0) {
+    r[p + cand * r_s] = C.weight * (res - C.f[i]);
+    if (T.u0 != nullptr && cand == 0) T.u0[p] = uv;
+  }
+}
+
+static void launch_tanh_head(cudaStream_t s, const Classes& T, const double* Z, int w, long long ld,
+                             const double* thetas, long long th_s, long long bias_off,
+                             long long wl_off, long long act_s, int nb, double* r, long long r_s) {
+  for (int c = 0; c < T.n; ++c) {
+    if (T.c[c].count == 0) continue;
+    const dim3 grid(static_cast<unsigned>((T.c[c].count + 7) / 8), nb);
+#define DNGD_TH(N)                                                                                \
+  case N:                                                                                         \
+    k_tanh_head<N><<<grid, 256, 0, s>>>(T, c, Z, w, ld, thetas, th_s, bias_off, wl_off, act_s, r, \
+                                         r_s);                                                    \
+    break;
+    switch (T.c[c].nch) {
+      DNGD_TH(1) DNGD_TH(2) DNGD_TH(3) DNGD_TH(4) DNGD_TH(5) DNGD_TH(6) DNGD_TH(7) DNGD_TH(8)
+      default: break;
+    }
+#undef DNGD_TH
+  }
+}
+
+// k_chan_slice sums the Laplacian's channels in ascending order
+static bool lap_ascending(const Classes& T) {
+  for (int c = 0; c < T.n; ++c)
+    for (int l = 1; l < T.c[c].nlap; ++l)
+      if (T.c[c].lap_ch[l] <= T.c[c].lap_ch[l - 1]) return false;
+  return true;
+}
+
+template <int S, int MODE>
+static void launch_chan_slice(cudaStream_t s, const Classes& T, const double* Z, int w, long long ld,
+                              const double* par, long long par_s, long long act_s, long long R,
+                              long long kpad, int nb, int8_t* Q, double* scale) {
+  for (int c = 0; c < T.n; ++c) {
+    if (T.c[c].count == 0) continue;
+    const dim3 grid(static_cast<unsigned>((T.c[c].count + kCsWarps - 1) / kCsWarps), nb);
+#define DNGD_CS(N)                                                                                 \
+  case N:                                                                                          \
+    k_chan_slice<S, N, MODE><<<grid, 32 * kCsWarps, 0, s>>>(T, c, Z, w, ld, par, par_s, act_s, R, \
+                                                           kpad, Q, scale);                        \
+    break;
+    switch (T.c[c].nch) {
+      DNGD_CS(1) DNGD_CS(2) DNGD_CS(3) DNGD_CS(4) DNGD_CS(5) DNGD_CS(6) DNGD_CS(7) DNGD_CS(8)
+      default: break;
+    }
+#undef DNGD_CS
+  }
+}
+
 template <int S>
 static void launch_tanh_slice(cudaStream_t s, const Classes& T, const double* Z, int w,
                               long long ld, const double* bias, long long bias_s, long long act_s,
                               long long R, long long kpad, int nb, int8_t* Q, double* scale) {
-  const unsigned thr = static_cast<unsigned>((kpad / 4 + 31) / 32 * 32);
-  for (int c = 0; c < T.n; ++c) {
-    if (T.c[c].count == 0) continue;
-    const dim3 grid(static_cast<unsigned>(T.c[c].count), nb);
-#define DNGD_TS(N)                                                                       \
-  case N:                                                                                \
-    k_tanh_slice<S, N><<<grid, thr, 0, s>>>(T, c, Z, w, ld, bias, bias_s, act_s, R, kpad, Q, \
-                                            scale);                                      \
-    break;
-    switch (T.c[c].nch) {
-      DNGD_TS(1) DNGD_TS(2) DNGD_TS(3) DNGD_TS(4) DNGD_TS(5) DNGD_TS(6) DNGD_TS(7) DNGD_TS(8)
-      default: break;
-    }
-#undef DNGD_TS
-  }
+  launch_chan_slice<S, 0>(s, T, Z, w, ld, bias, bias_s, act_s, R, kpad, nb, Q, scale);
+}
+
+template <int S>
+static void launch_input_slice(cudaStream_t s, const Classes& T, const double* thetas,
+                               long long th_s, int w1, long long R, long long kpad, int nb,
+                               int8_t* Q, double* scale) {
+  launch_chan_slice<S, 1>(s, T, nullptr, w1, 0, thetas, th_s, 0, R, kpad, nb, Q, scale);
 }
 
 // output layer (width 1): one warp per point; channel dot products, residual.
@@ -1608,10 +1773,14 @@ static int input_gemm(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const BigIn&
 static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const double* thetas,
                            int C, LossBufs& B, double** Hlast, const double* theta,
                            const double* delta, const double* etas,
-                           const double* zx_act = nullptr) {
+                           const double* zx_act = nullptr, double* r_fused = nullptr) {
   const int L = P.L;
   const long long act_s = P.R * P.ldmax;
-  {
+  // emulated GEMMs with plain inputs: the input layer is fused with the slicing of
+  // H_1 (k_input_slice) inside the candidate-chunk loop below
+  bool in_fused = B.oz_S != 0 && !P.bigin && oz_kpad(P.w[1]) <= 4LL * 1024 && lap_ascending(P.T);
+  for (int c = 0; c < P.T.n; ++c) in_fused = in_fused && P.T.c[c].inp == nullptr && P.T.c[c].nch <= kTsMaxCh;
+  if (!in_fused) {
     const double *Zx = nullptr, *Dx = nullptr;
     if (P.bigin && delta != nullptr) {  // x (W0 + eta V0) = x W0 + eta x V0
       int rc = DNGD_OK;
@@ -1638,14 +1807,26 @@ static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const d
     // digit planes directly (k_tanh_slice), the last hidden layer writes H_{L-1}
     int maxch = 0;
     for (int c = 0; c < P.T.n; ++c) maxch = std::max(maxch, P.T.c[c].nch);
-    const bool fuse = maxch <= kTsMaxCh;
+    const bool fuse = maxch <= kTsMaxCh && lap_ascending(P.T);
     for (int k = 1; k <= L - 2; ++k)
       launch_transpose(s, thetas + P.off[k], P.n, static_cast<int>(P.w[k]),
                        static_cast<int>(P.w[k + 1]), B.Wt[k], P.ld[k], P.w[k + 1] * P.ld[k], C);
     int rc = DNGD_OK;
     for (int b0 = 0; b0 < C && rc == DNGD_OK; b0 += B.oz_cb) {
       const int nb = std::min(B.oz_cb, C - b0);
-      rc = oz_slice(ctx, s, B.Hping + b0 * act_s, nb * P.R, P.w[1], P.ldmax, B.oz_S, B.ozQA, B.ozsA);
+      if (in_fused) {
+        const long long kp1 = oz_kpad(P.w[1]);
+        if (B.oz_S == 8) {
+          launch_input_slice<8>(s, P.T, thetas + static_cast<long long>(b0) * P.n, P.n,
+                                static_cast<int>(P.w[1]), P.R, kp1, nb, B.ozQA, B.ozsA);
+        } else {
+          launch_input_slice<7>(s, P.T, thetas + static_cast<long long>(b0) * P.n, P.n,
+                                static_cast<int>(P.w[1]), P.R, kp1, nb, B.ozQA, B.ozsA);
+        }
+        rc = cuda_status(ctx, cudaGetLastError(), "input_slice");
+      } else {
+        rc = oz_slice(ctx, s, B.Hping + b0 * act_s, nb * P.R, P.w[1], P.ldmax, B.oz_S, B.ozQA, B.ozsA);
+      }
       for (int k = 1; k <= L - 2 && rc == DNGD_OK; ++k) {
         const long long N = P.w[k + 1], Kd = P.w[k];
         const long long wst = P.w[k + 1] * P.ld[k];
@@ -1663,6 +1844,12 @@ static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const d
             launch_tanh_slice<7>(s, P.T, B.Z + b0 * act_s, static_cast<int>(N), P.ldmax, bias, P.n,
                                  act_s, P.R, oz_kpad(N), nb, B.ozQA, B.ozsA);
           }
+        } else if (k == L - 2 && r_fused != nullptr && fuse) {
+          // last hidden layer + output layer: residuals of the chunk's candidates
+          launch_tanh_head(s, P.T, B.Z + b0 * act_s, static_cast<int>(N), P.ldmax,
+                           thetas + static_cast<long long>(b0) * P.n, P.n,
+                           P.off[k] + P.w[k] * P.w[k + 1], P.off[L - 1], act_s, nb,
+                           r_fused + static_cast<long long>(b0) * P.m, P.m);
         } else {
           k_tanh_fwd<<<dim3(nblk(P.m * N), nb), 256, 0, s>>>(P.T, B.Z + b0 * act_s,
                                                              B.Hpong + b0 * act_s, static_cast<int>(N),
@@ -1675,7 +1862,7 @@ static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const d
       }
     }
     if (rc) return rc;
-    *Hlast = B.Hpong;
+    *Hlast = (r_fused != nullptr && fuse) ? nullptr : B.Hpong;  // nullptr: residuals written
     return cuda_status(ctx, cudaGetLastError(), "forward");
   }
   for (int k = 1; k <= L - 2; ++k) {
@@ -3096,11 +3283,13 @@ static int loss_many_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
   k_candidates<<<dim3(nblk(P.n - k0), ncand), 256, 0, s>>>(theta, delta, etas, P.n, B.thetas, k0);
   double* Hlast;
   rc = forward_batched(ctx, s, P, B.thetas, ncand, B, &Hlast, theta, delta, etas,
-                       act_input_products(P, act_work, act_bytes));
+                       act_input_products(P, act_work, act_bytes), B.r);
   if (rc) return rc;
-  k_head<<<dim3(nblk(P.m, 8), ncand), 256, 0, s>>>(P.T, Hlast, static_cast<int>(P.w[P.L - 1]),
-                                                    P.ldmax, B.thetas, P.n, P.off[P.L - 1],
-                                                    P.R * P.ldmax, B.r, P.m);
+  if (Hlast != nullptr) {  // (else the last hidden layer wrote the residuals: k_tanh_head)
+    k_head<<<dim3(nblk(P.m, 8), ncand), 256, 0, s>>>(P.T, Hlast, static_cast<int>(P.w[P.L - 1]),
+                                                      P.ldmax, B.thetas, P.n, P.off[P.L - 1],
+                                                      P.R * P.ldmax, B.r, P.m);
+  }
   k_half_sumsq<<<ncand, 256, 0, s>>>(B.r, P.m, losses);
   return cuda_status(ctx, cudaGetLastError(), "loss_many");
 }

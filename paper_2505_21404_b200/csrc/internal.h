@@ -69,6 +69,13 @@ int syrk(dngd_ctx* ctx, cudaStream_t s, const double* J, long long m, long long 
 // Ozaki slicing (ozaki.cu): rows x K doubles (pitch ld) -> int8 digits Q[slices][rows][kpad]
 // (kpad = K rounded up to 32, zero digits past K) and per-row power-of-two scales;
 // a row with a non-finite entry gets scale NaN.
+int oz_slice_into(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows, long long K,
+                  long long ld, long long kpad, size_t plane, int slices, int8_t* Q, double* scale);
+size_t oz_splitk_bytes(long long M, long long N, long long K, int slices, int splits);
+int oz_splitk_choose(dngd_ctx* ctx, long long M, long long N, long long K);
+int oz_gemm_splitk(dngd_ctx* ctx, cudaStream_t s, const double* A, long long lda, const double* B,
+                   long long ldb, long long M, long long N, long long K, double alpha, double* C,
+                   long long ldc, int slices, int splits, void* work, size_t work_bytes);
 int oz_slice(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows, long long K,
              long long ld, int slices, int8_t* Q, double* scale);
 // 3-D TMA map over Q: box {box_bytes (32 or 64), box_rows, slices}, swizzle of the

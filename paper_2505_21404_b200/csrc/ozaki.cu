@@ -34,7 +34,7 @@ namespace dngd {
 template <int S>
 __global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ X, long long rows,
                                                   long long K, long long ld, long long kpad,
-                                                  int8_t* __restrict__ Q,
+                                                  size_t plane, int8_t* __restrict__ Q,
                                                   double* __restrict__ scale) {
   const long long row = static_cast<long long>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -76,7 +76,6 @@ __global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ X, 
   const int e = bad ? 0 : oz_row_exponent(mx);
   if (lane == 0) scale[row] = bad ? CUDART_NAN : ldexp(1.0, e);
   const double sinv = ldexp(1.0, 7 * S - e);
-  const size_t plane = static_cast<size_t>(rows) * kpad;
   for (long long w = lane; w < words; w += 32) {
     double v[4];
     load4(w, v);
@@ -88,18 +87,178 @@ __global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ X, 
   }
 }
 
-int oz_slice(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows, long long K,
-             long long ld, int slices, int8_t* Q, double* scale) {
+int oz_slice_into(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows, long long K,
+                  long long ld, long long kpad, size_t plane, int slices, int8_t* Q,
+                  double* scale) {
   if (rows <= 0) return DNGD_OK;
-  const long long kp = oz_kpad(K);
+  if (kpad < oz_kpad(K) || kpad % 32 != 0) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_slice: bad kpad");
   const unsigned grid = static_cast<unsigned>((rows + 7) / 8);
   switch (slices) {
-    case 6: k_oz_slice<6><<<grid, 256, 0, s>>>(X, rows, K, ld, kp, Q, scale); break;
-    case 7: k_oz_slice<7><<<grid, 256, 0, s>>>(X, rows, K, ld, kp, Q, scale); break;
-    case 8: k_oz_slice<8><<<grid, 256, 0, s>>>(X, rows, K, ld, kp, Q, scale); break;
+    case 6: k_oz_slice<6><<<grid, 256, 0, s>>>(X, rows, K, ld, kpad, plane, Q, scale); break;
+    case 7: k_oz_slice<7><<<grid, 256, 0, s>>>(X, rows, K, ld, kpad, plane, Q, scale); break;
+    case 8: k_oz_slice<8><<<grid, 256, 0, s>>>(X, rows, K, ld, kpad, plane, Q, scale); break;
     default: return set_error(ctx, DNGD_ERR_DIMENSION, "oz_slice: slices must be 6, 7 or 8");
   }
   return cuda_status(ctx, cudaGetLastError(), "oz_slice");
+}
+
+int oz_slice(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows, long long K,
+             long long ld, int slices, int8_t* Q, double* scale) {
+  const long long kp = oz_kpad(K);
+  return oz_slice_into(ctx, s, X, rows, K, ld, kp, static_cast<size_t>(rows) * kp, slices, Q, scale);
+}
+
+// Split-K slicing of short, long rows (J^T w: 513 neuron rows x 25,000 activation
+// rows): one 256-thread CTA per (row, split) -- the one-warp-per-row k_oz_slice left
+// most SMs idle here.  Same scale rule and digits as k_oz_slice over the split's
+// range [z kl, min(K, (z + 1) kl)); rows of split z land at z M + row.
+template <int S>
+__global__ void __launch_bounds__(256) k_oz_slice_split(const double* __restrict__ X, long long M,
+                                                        long long K, long long ld, long long kl,
+                                                        long long kpad, size_t plane,
+                                                        int8_t* __restrict__ Q,
+                                                        double* __restrict__ scale) {
+  __shared__ double red[8];
+  __shared__ int redbad[8];
+  const long long row = blockIdx.x;
+  const int z = blockIdx.y;
+  const long long k0 = z * kl;
+  const long long len = max(0LL, min(K, k0 + kl) - k0);
+  const double* x = X + row * ld + k0;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  auto load4 = [&](long long w, double (&v)[4]) {
+    const long long c0 = 4 * w;
+    if (vec && c0 + 3 < len) {
+      const double2 a = *reinterpret_cast<const double2*>(x + c0);
+      const double2 b = *reinterpret_cast<const double2*>(x + c0 + 2);
+      v[0] = a.x;
+      v[1] = a.y;
+      v[2] = b.x;
+      v[3] = b.y;
+    } else {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) v[b] = c0 + b < len ? x[c0 + b] : 0.0;
+    }
+  };
+  const long long words = kpad / 4;
+  double mx = 0.0;
+  int bad = 0;
+  for (long long w = tid; w < words; w += 256) {
+    double v[4];
+    load4(w, v);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      bad |= !isfinite(v[b]);
+      mx = fmax(mx, fabs(v[b]));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if (lane == 0) {
+    red[wp] = mx;
+    redbad[wp] = bad;
+  }
+  __syncthreads();
+  mx = 0.0;
+  bad = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    mx = fmax(mx, red[k]);
+    bad |= redbad[k];
+  }
+  const int e = bad ? 0 : oz_row_exponent(mx);
+  const long long orow = z * M + row;
+  if (tid == 0) scale[orow] = bad ? CUDART_NAN : ldexp(1.0, e);
+  const double sinv = ldexp(1.0, 7 * S - e);
+  for (long long w = tid; w < words; w += 256) {
+    double v[4];
+    load4(w, v);
+    uint32_t packed[S];
+    oz_digits4<S>(v, sinv, bad != 0, packed);
+#pragma unroll
+    for (int t = 0; t < S; ++t) reinterpret_cast<uint32_t*>(Q + t * plane + orow * kpad)[w] = packed[t];
+  }
+}
+
+static int oz_slice_split(dngd_ctx* ctx, cudaStream_t s, const double* X, long long M, long long K,
+                          long long ld, long long kl, long long kpad, int splits, int slices,
+                          int8_t* Q, double* scale) {
+  const dim3 grid(static_cast<unsigned>(M), static_cast<unsigned>(splits));
+  const size_t plane = static_cast<size_t>(splits) * M * kpad;
+  switch (slices) {
+    case 6: k_oz_slice_split<6><<<grid, 256, 0, s>>>(X, M, K, ld, kl, kpad, plane, Q, scale); break;
+    case 7: k_oz_slice_split<7><<<grid, 256, 0, s>>>(X, M, K, ld, kl, kpad, plane, Q, scale); break;
+    case 8: k_oz_slice_split<8><<<grid, 256, 0, s>>>(X, M, K, ld, kl, kpad, plane, Q, scale); break;
+    default: return set_error(ctx, DNGD_ERR_DIMENSION, "oz_slice: slices must be 6, 7 or 8");
+  }
+  return cuda_status(ctx, cudaGetLastError(), "oz_slice_split");
+}
+
+// C = alpha sum_z P_z (the split-K partials of oz_gemm_splitk), fixed order
+__global__ void k_oz_splitk_sum(const double* __restrict__ part, int splits, long long M,
+                                long long N, long long ldc, double alpha, double* __restrict__ C) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= M * N) return;
+  double v = 0.0;
+  for (int z = 0; z < splits; ++z) v += part[z * M * N + e];
+  const long long r = e / N, c = e - (e / N) * N;
+  C[r * ldc + c] = alpha * v;
+}
+
+size_t oz_splitk_bytes(long long M, long long N, long long K, int slices, int splits) {
+  const long long kl = oz_kpad((K + splits - 1) / splits);
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  return al(static_cast<size_t>(slices) * splits * M * kl) + al(static_cast<size_t>(slices) * splits * N * kl) +
+         al(static_cast<size_t>(splits) * M * 8) + al(static_cast<size_t>(splits) * N * 8) +
+         al(static_cast<size_t>(splits) * M * N * 8);
+}
+
+int oz_splitk_choose(dngd_ctx* ctx, long long M, long long N, long long K) {
+  const long long tiles = ((M + OZ_BM - 1) / OZ_BM) * ((N + OZ_BN - 1) / OZ_BN);
+  long long sp = (ctx->num_sms + tiles - 1) / tiles;            // about one wave
+  sp = std::min(sp, std::max(1LL, K / 1024));                   // >= 1024 of K per split
+  return static_cast<int>(std::max(1LL, std::min(sp, 32LL)));
+}
+
+// C (M x N, ldc) = alpha A B^T with A (M x K, lda) and B (N x K, ldb) K-major and K
+// large (the J^T w contraction over activation rows): K cut into `splits` ranges,
+// each sliced with its own row scales into one batch entry of the int8 engine, the
+// partials summed in a fixed order.  work: oz_splitk_bytes.
+int oz_gemm_splitk(dngd_ctx* ctx, cudaStream_t s, const double* A, long long lda, const double* B,
+                   long long ldb, long long M, long long N, long long K, double alpha, double* C,
+                   long long ldc, int slices, int splits, void* work, size_t work_bytes) {
+  if (M <= 0 || N <= 0) return DNGD_OK;
+  if (work_bytes < oz_splitk_bytes(M, N, K, slices, splits)) {
+    return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm_splitk: workspace too small");
+  }
+  const long long kl = (K + splits - 1) / splits;
+  const long long kp = oz_kpad(kl);
+  if (kp > kOzMaxK) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm_splitk: split longer than 32768");
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  char* w = static_cast<char*>(work);
+  int8_t* qa = reinterpret_cast<int8_t*>(w);
+  w += al(static_cast<size_t>(slices) * splits * M * kp);
+  int8_t* qb = reinterpret_cast<int8_t*>(w);
+  w += al(static_cast<size_t>(slices) * splits * N * kp);
+  double* sa = reinterpret_cast<double*>(w);
+  w += al(static_cast<size_t>(splits) * M * 8);
+  double* sb = reinterpret_cast<double*>(w);
+  w += al(static_cast<size_t>(splits) * N * 8);
+  double* part = reinterpret_cast<double*>(w);
+  int rc = oz_slice_split(ctx, s, A, M, K, lda, kl, kp, splits, slices, qa, sa);
+  if (rc) return rc;
+  rc = oz_slice_split(ctx, s, B, N, K, ldb, kl, kp, splits, slices, qb, sb);
+  if (rc) return rc;
+  rc = oz_gemm_batched(ctx, s, qa, sa, splits * M, M, qb, sb, splits * N, N, kp, slices, M, N,
+                           splits, part, N, M * N);
+  if (rc) return rc;
+  k_oz_splitk_sum<<<static_cast<unsigned>((M * N + 255) / 256), 256, 0, s>>>(part, splits, M, N, ldc,
+                                                                          alpha, C);
+  return cuda_status(ctx, cudaGetLastError(), "oz_splitk_sum");
 }
 
 int oz_encode(dngd_ctx* ctx, CUtensorMap* map, const int8_t* Q, long long rows, long long kpad,

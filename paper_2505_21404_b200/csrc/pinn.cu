@@ -3306,6 +3306,8 @@ struct JtScratch {
   int tiles, tsplits;
   long long rows_per_split;
   size_t off_tmp = 0;  // column-range mode: the input / output layer block before slicing
+  int oz = 0;           // hidden-layer GEMMs on the int8 engine (Ozaki digits; 0 = DMMA)
+  size_t off_oz = 0, oz_bytes = 0;
 };
 
 // narrow nets: every layer in one tiled launch; wide ones: per-layer split-K GEMM
@@ -3365,6 +3367,16 @@ JtScratch jt_plan(dngd_ctx* ctx, const Plan& P) {
   }
   S.off_tmp = (S.bytes + 255) / 256 * 256;  // column-range mode: the small edge layers
   S.bytes = S.off_tmp + static_cast<size_t>(std::max((P.w[0] + 1) * P.w[1], P.w[P.L - 1] + 1)) * 8;
+  // hidden layers >= 128 wide: split-K over activation rows on the int8 tensor cores
+  S.oz = oz_ls_slices(P);
+  if (S.oz) {
+    for (int k = 1; k <= P.L - 2; ++k) {
+      const int sp = oz_splitk_choose(ctx, P.w[k] + 1, P.w[k + 1], P.R);
+      S.oz_bytes = std::max(S.oz_bytes, oz_splitk_bytes(P.w[k] + 1, P.w[k + 1], P.R, S.oz, sp));
+    }
+    S.off_oz = (S.bytes + 255) / 256 * 256;
+    S.bytes = S.off_oz + S.oz_bytes;
+  }
   return S;
 }
 
@@ -3539,6 +3551,14 @@ static int jt_range(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
     g.ldc = wk1;
     g.alpha = scale;
     g.beta = 0.0;
+    if (S.oz) {
+      int sp = oz_splitk_choose(ctx, g.M, g.N, g.K);
+      while (sp > 1 && oz_splitk_bytes(g.M, g.N, g.K, S.oz, sp) > S.oz_bytes) --sp;
+      rc = oz_gemm_splitk(ctx, s, g.A, g.lda, g.B, g.ldb, g.M, g.N, g.K, g.alpha, g.C, g.ldc, S.oz,
+                          sp, sc0 + S.off_oz, S.oz_bytes);
+      if (rc) return rc;
+      continue;
+    }
     int sp = gemm_splitk_choose(ctx, g.M, g.N, g.K);
     while (sp > 1 && gemm_splitk_bytes(g.M, g.N, sp) > S.part_bytes) --sp;
     rc = gemm_nt_splitk(ctx, s, g, sp, part, S.part_bytes);

@@ -894,6 +894,20 @@ def cpu_baseline(cfg, max_seconds=25.0, warmup=1):
     big = 8.0 * m * n > 1e10
     if big:
         warmup = 0  # one step is tens of seconds: no untimed warm-up step
+    # the streamed oracle holds one layer block J_k (m x (w_k + 1) w_{k+1}) at a time
+    w = cfg["widths"]
+    block = max(8.0 * m * (w[k] + 1) * w[k + 1] for k in range(len(w) - 1))
+    try:
+        import psutil
+
+        avail = float(psutil.virtual_memory().available)
+    except Exception:  # noqa: BLE001
+        avail = float("inf")
+    if block > 0.5 * avail:
+        return {"value": None, "unit": UNIT, "cores": cores, "kind": "port",
+                "unavailable": f"one oracle step needs a {block / 1e9:.0f} GB layer block of J "
+                               f"(host memory available: {avail / 1e9:.0f} GB)",
+                "sample": "none"}
     times = []
     t_start = time.perf_counter()
     rng = np.random.default_rng(0)
@@ -944,6 +958,10 @@ def run_reference(args, cfg):
         return
     budget = float(os.environ.get("DNGD_REF_SECONDS", "150"))
     res = cpu_baseline(cfg, max_seconds=budget, warmup=min(args.warmup, 1))
+    if res["value"] is None:
+        print(json.dumps({"impl": "reference", "unavailable": res["unavailable"],
+                          "config": {"workload": cfg["name"]}}), flush=True)
+        return
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / res["value"],

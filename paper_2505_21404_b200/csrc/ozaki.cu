@@ -221,7 +221,10 @@ int oz_splitk_choose(dngd_ctx* ctx, long long M, long long N, long long K) {
   const long long tiles = ((M + OZ_BM - 1) / OZ_BM) * ((N + OZ_BN - 1) / OZ_BN);
   long long sp = (ctx->num_sms + tiles - 1) / tiles;            // about one wave
   sp = std::min(sp, std::max(1LL, K / 1024));                   // >= 1024 of K per split
-  return static_cast<int>(std::max(1LL, std::min(sp, 32LL)));
+  sp = std::min(sp, 32LL);
+  // the int32 diagonal accumulators hold K <= 32768 (kOzMaxK) per split
+  sp = std::max(sp, (K + (kOzMaxK - 32) - 1) / (kOzMaxK - 32));
+  return static_cast<int>(std::max(1LL, sp));
 }
 
 // C (M x N, ldc) = alpha A B^T with A (M x K, lda) and B (N x K, ldb) K-major and K

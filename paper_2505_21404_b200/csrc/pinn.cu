@@ -3552,8 +3552,10 @@ static int jt_range(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp,
     g.alpha = scale;
     g.beta = 0.0;
     if (S.oz) {
-      int sp = oz_splitk_choose(ctx, g.M, g.N, g.K);
-      while (sp > 1 && oz_splitk_bytes(g.M, g.N, g.K, S.oz, sp) > S.oz_bytes) --sp;
+      const int sp0 = oz_splitk_choose(ctx, g.M, g.N, g.K);
+      const int spmin = static_cast<int>((g.K + (kOzMaxK - 32) - 1) / (kOzMaxK - 32));
+      int sp = sp0;
+      while (sp > spmin && oz_splitk_bytes(g.M, g.N, g.K, S.oz, sp) > S.oz_bytes) --sp;
       rc = oz_gemm_splitk(ctx, s, g.A, g.lda, g.B, g.ldb, g.M, g.N, g.K, g.alpha, g.C, g.ldc, S.oz,
                           sp, sc0 + S.off_oz, S.oz_bytes);
       if (rc) return rc;

@@ -89,6 +89,25 @@ def test_potrf_potrs(K, m):
     assert np.linalg.norm(res) / (np.linalg.norm(Km) * np.linalg.norm(y) + np.linalg.norm(b)) <= 1e-14
 
 
+@pytest.mark.parametrize("m", [4864, 8000])
+def test_potrf_panels_in_waves(K, m):
+    """Panels wider than one wave of CTAs (m > 64 + 148 x 32): every CTA must read
+    the unfactored diagonal block before CTA 0 writes L_pp in place (config 4's
+    m = 8000 factored garbage below row 4768 before the per-panel arrival count)."""
+    A = torch.randn(m, m, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(m))
+    Km = A @ A.T / m + torch.eye(m, dtype=torch.float64, device="cuda")
+    fac = K.CholeskyFactor(m, Km.device)
+    fac.factor(Km, 0.0)
+    assert int(fac.info.item()) == 0
+    Lref = torch.linalg.cholesky(Km)
+    L = torch.tril(fac.L[:, :m])
+    assert float(torch.linalg.norm(L - Lref) / torch.linalg.norm(Lref)) <= 1e-13
+    b = torch.randn(m, dtype=torch.float64, device="cuda")
+    x = b.clone()
+    fac.solve_(x)
+    assert float(torch.linalg.norm(Km @ x - b) / torch.linalg.norm(b)) <= 1e-12
+
+
 def test_potrf_reports_failing_column(K):
     from tests.gpu_util import dev
     m = 130

@@ -321,6 +321,42 @@ def test_cfg3_full_width_factored_equals_materialised(P):
     assert dr <= 1e-8
 
 
+def test_cfg4_full_size_gram_and_factor(P):
+    """Config 4 at full size (5 -> 1792 x 5 -> 1, n = 12.85 M, m = 8000): the oracle
+    cannot form J (822 GB), so the emulated-FP64 Gram's K and the Cholesky of
+    K + lam I are checked on the device -- K symmetric positive semidefinite to
+    rounding, the hand-written potrf equal to cuSOLVER's and the solve backward
+    stable (m = 8000 takes the panel kernel past one wave of CTAs)."""
+    from paper_2505_21404_b200.solver import _chol_with_retries
+
+    c = dict(CFG[3], widths=(5, 1792, 1792, 1792, 1792, 1792, 1), counts=(7000, 1000))
+    rng = np.random.default_rng(0)
+    oclasses = c["oprob"]().sample(c["counts"], rng)
+    rmap, spec = _gpu_map(P, c, oclasses)
+    assert rmap.n == 12_864_769 and rmap.m == 8000
+    theta = P.xavier_normal_params(spec)
+    Kt = P.assemble_gramian(rmap, theta).tensor
+    m = rmap.m
+    asym = float(torch.linalg.norm(Kt - Kt.T) / torch.linalg.norm(Kt))
+    loss = rmap.loss(theta)
+    lam = max(min(loss, 1e-5), 1e-12)
+    fac, lam_used = _chol_with_retries(Kt, lam)
+    Ks = Kt + lam_used * torch.eye(m, dtype=torch.float64, device="cuda")
+    Lref = torch.linalg.cholesky(Ks)
+    lrel = float(torch.linalg.norm(torch.tril(fac.L[:, :m]) - Lref) / torch.linalg.norm(Lref))
+    b = torch.randn(m, dtype=torch.float64, device="cuda")
+    y = fac.solve_(b.clone())
+    berr = float(torch.linalg.norm(Ks @ y - b) / (torch.linalg.matrix_norm(Ks, 2) * torch.linalg.norm(y)
+                                                 + torch.linalg.norm(b)))
+    _log("cfg4_full_gram_factor", {"K_asym": asym, "lam": lam, "lam_used": lam_used,
+                                   "L_vs_cusolver": lrel, "backward_error": berr})
+    del Ks, Lref
+    torch.cuda.empty_cache()
+    assert asym == 0.0  # both triangles written from one point-pair sum
+    assert lrel <= 1e-10
+    assert berr <= 1e-14
+
+
 def test_cfg5_pcg_full_m(P):
     """Config 5's m = 32000 and Nystrom rank 512 (width 32, n = 3297): one PCG step
     vs the oracle (landmarks from the same Generator state), then a 3-step PCG

@@ -1,4 +1,4 @@
-for d in 0 4; do DNGD_GOZ_DBG=$d python - <<PY
+for d in 0; do DNGD_GOZ_DBG=$d python - <<PY
 import sys, numpy as np, torch
 sys.path.insert(0,".")
 import paper_2505_21404_b200 as P

@@ -43,6 +43,15 @@ struct GozParams {
   double* K;
   long long ldK;
   int tile0;
+  // rect: K[:, I] of the Nystrom sketch (solver.py:259-261) -- column tiles over the
+  // gathered landmark activations (mB / scB over Rb gathered rows; landmarks of class
+  // c are columns lcol0[c] .. + lcnt[c] - 1 of K, global points lpt[.]), every class
+  // pair a full rectangle, one write per entry
+  int rect;
+  const double* scB[DNGD_MAX_LAYERS][2];
+  long long Rb;
+  long long lcol0[DNGD_MAX_CLASSES], lcnt[DNGD_MAX_CLASSES], lrow0[DNGD_MAX_CLASSES];
+  const long long* lpt;
   int dbg;  // timing experiments only (tools/goz_dbg.sh): 1 narrow MMAs, 2 no MMA, 3 no MMA no drain,
            // 4 no drain, 5 no TMA no drain, 6 = 5 with narrow MMAs, 7 = 5 without the TMEM hand-off wait,
            // 8 = 7 without operand waits (MMA issue alone)
@@ -109,7 +118,7 @@ DNGD_DEV GozTile goz_tile(const GozParams& p, int tile) {
   const int t = tile - p.tstart[pi];
   r.c = p.pc[pi];
   r.cp = p.pcp[pi];
-  if (r.c == r.cp) {
+  if (r.c == r.cp && !p.rect) {
     goz_decode_tri(t, p.ti_n[pi], r.ti, r.tj);
   } else {  // rectangle, column-major: CTAs in flight share the column tiles
     r.tj = t / p.ti_n[pi];
@@ -173,7 +182,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const GozTile g = goz_tile(p, tile + p.tile0);
         const int arow0 = static_cast<int>(p.T.c[g.c].act0 + static_cast<long long>(g.ti) * 2 * p.ppc[g.c] * p.nch[g.c]);
-        const int brow0 = static_cast<int>(p.T.c[g.cp].act0 + static_cast<long long>(g.tj) * p.ppc[g.cp] * p.nch[g.cp]);
+        const int brow0 = static_cast<int>((p.rect ? p.lrow0[g.cp] : p.T.c[g.cp].act0) +
+                                           static_cast<long long>(g.tj) * p.ppc[g.cp] * p.nch[g.cp]);
         for (int k = 0; k < p.L; ++k) {
           for (int i = 0; i < goz_nphase(p, k); ++i) {
             const int part = goz_part(p, k, i);
@@ -257,7 +267,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
       const ClassDev& Ca = p.T.c[c];
       const ClassDev& Cb = p.T.c[cp];
       const long long arow0 = Ca.act0 + static_cast<long long>(P0) * na;
-      const long long brow0 = Cb.act0 + static_cast<long long>(Q0) * nb;
+      const long long brow0 = (p.rect ? p.lrow0[cp] : Cb.act0) + static_cast<long long>(Q0) * nb;
+      const long long ccount = p.rect ? p.lcnt[cp] : Cb.count;  // column points
       // row seeds / value flags of this tile (the previous tile's last use of them was
       // its final drain; the barrier also orders the previous reduction's PH reads
       // before this tile's first PH writes)
@@ -270,8 +281,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
       } else if (threadIdx.x < 64 + OZ_BM + OZ_BN) {
         const int gi = threadIdx.x - 64 - OZ_BM;
         const int chb = gi % nb, pb = Q0 + gi / nb;
-        const bool ok = gi < np_c * nb && pb < Cb.count;
-        sB[gi] = ok ? seedc(p.T, Cb, chb, Cb.row0 + pb) : 0.0;
+        const bool ok = gi < np_c * nb && pb < ccount;
+        sB[gi] = ok ? seedc(p.T, Cb, chb, p.rect ? p.lpt[p.lcol0[cp] + pb] : Cb.row0 + pb) : 0.0;
         zB[gi] = (ok && chb == 0) ? 1.0 : 0.0;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(OZ_ETHREADS) : "memory");
@@ -300,7 +311,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
           const double sr = arow < p.R ? scv[arow] : 0.0;
           // this warp's column scales: lane j < OZ_COLS holds column col0 + j (shuffled below)
           const long long bl = brow0 + col0 + lane;
-          const double scl = bl < p.R ? scv[bl] : 0.0;
+          const double scl = p.rect ? (bl < p.Rb ? p.scB[k][part][bl] : 0.0) : (bl < p.R ? scv[bl] : 0.0);
           const double za = zA[row], sar = sA[row];
 #pragma unroll
           for (int cc = 0; cc < OZ_COLS / OZ_LD; ++cc) {
@@ -337,18 +348,18 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_gram_oz(const __grid_constant
 #pragma unroll
       for (int j = 0; j < OZ_COLS; ++j) PH[(col0 + j) * OZ_BM + row] = G[j];
       asm volatile("bar.sync 1, %0;" ::"n"(OZ_ETHREADS) : "memory");
-      const long long cnt_r = Ca.count, cnt_c = Cb.count;
+      const long long cnt_r = Ca.count, cnt_c = ccount;
       for (int e = threadIdx.x - 64; e < np_r * np_c; e += OZ_ETHREADS) {
         const int r = e / np_c, cc = e - (e / np_c) * np_c;
         const long long pr = P0 + r, pcl = Q0 + cc;
         if (pr >= cnt_r || pcl >= cnt_c) continue;
-        const long long grow = Ca.row0 + pr, gcol = Cb.row0 + pcl;
-        if (c == cp && gcol > grow) continue;
+        const long long grow = Ca.row0 + pr, gcol = (p.rect ? p.lcol0[cp] : Cb.row0) + pcl;
+        if (!p.rect && c == cp && gcol > grow) continue;
         double v = 0.0;
         for (int a = 0; a < na; ++a)
           for (int b = 0; b < nb; ++b) v += PH[(cc * nb + b) * OZ_BM + r * na + a];
         p.K[grow * p.ldK + gcol] = v;
-        p.K[gcol * p.ldK + grow] = v;
+        if (!p.rect) p.K[gcol * p.ldK + grow] = v;
       }
     }
   }

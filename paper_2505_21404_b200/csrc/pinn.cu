@@ -2995,13 +2995,44 @@ static size_t cols_scratch_bytes(const Plan& P, long long rows) {
   return b;
 }
 
+// K[:, I] on the int8 engine (gram_oz.cuh rect mode) under the same rule as the
+// factored Gram (kernels.gram_emulation_slices: hidden layers >= 128 wide,
+// DNGD_GRAM_SLICES=0 keeps the DMMA kernel); 0 where the emulated kernel does not apply
+static int goz_cols_slices(const Plan& P) {
+  if (const char* e = getenv("DNGD_GRAM_SLICES")) {
+    if (atoi(e) == 0) return 0;
+  }
+  long long hmax = 0;
+  for (int k = 1; k < P.L; ++k) hmax = std::max(hmax, P.w[k]);
+  if (hmax < 128 || P.wide_in || P.T.din > DNGD_MAX_GRAD || P.R >= (1LL << 31)) return 0;
+  for (int k = 0; k < P.L; ++k)
+    if (goz_kdim(P, k, 0) > kOzMaxK || goz_kdim(P, k, 1) > kOzMaxK) return 0;
+  for (int c = 0; c < P.T.n; ++c)
+    if (P.T.c[c].nch > OZ_BN) return 0;
+  return 7;
+}
+
+// digit planes of the full activations (R rows) and of the gathered landmark rows
+static size_t cols_oz_bytes(const Plan& P, long long rows, int S) {
+  size_t b = gram_oz_bytes(P, S);
+  for (int k = 0; k < P.L; ++k)
+    for (int part = 0; part < 2; ++part) {
+      const long long kd = goz_kdim(P, k, part);
+      if (kd == 0) continue;
+      b += oz_al256(static_cast<size_t>(S) * rows * oz_kpad(kd)) + oz_al256(static_cast<size_t>(rows) * 8);
+    }
+  return b + oz_al256(static_cast<size_t>(rows) * 8);  // + the landmarks' global points
+}
+
 extern "C" int dngd_gram_cols_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp,
                                         const dngd_class_desc* classes, int nclass, int ell,
                                         size_t* bytes) {
   Plan P;
   int rc = make_plan(ctx, mlp, classes, nclass, P);
   if (rc) return rc;
-  *bytes = cols_scratch_bytes(P, static_cast<long long>(std::max(ell, 1)) * 8);
+  const long long rows = static_cast<long long>(std::max(ell, 1)) * 8;
+  *bytes = cols_scratch_bytes(P, rows);
+  if (const int S = goz_cols_slices(P)) *bytes = (*bytes + 255) / 256 * 256 + cols_oz_bytes(P, rows, S);
   return DNGD_OK;
 }
 
@@ -3048,6 +3079,99 @@ extern "C" int dngd_gram_factored_cols(dngd_ctx* ctx, void* stream, const dngd_m
   std::vector<double*> gH(P.L, nullptr), gZ(P.L, nullptr);
   for (int k = 1; k <= P.L - 1; ++k) gH[k] = gather(B.H[k], P.ld[k]);
   for (int k = 0; k <= P.L - 2; ++k) gZ[k] = gather(B.Zb[k], P.ld[k + 1]);
+  if (const int S = goz_cols_slices(P)) {
+    // emulated FP64: the full activations give the row tiles, the gathered landmark
+    // activations the column tiles (gram_oz.cuh rect mode)
+    const long long rows_cap = static_cast<long long>(std::max(ell, 1)) * 8;
+    char* w = static_cast<char*>(scratch) + (cols_scratch_bytes(P, rows_cap) + 255) / 256 * 256;
+    if (scratch_bytes < static_cast<size_t>(w - static_cast<char*>(scratch)) + cols_oz_bytes(P, rows_cap, S)) {
+      return set_error(ctx, DNGD_ERR_DIMENSION, "gram_cols: scratch too small for the int8 planes");
+    }
+    thread_local GozParams gq;
+    memset(&gq, 0, sizeof gq);
+    gq.T = P.T;
+    gq.L = P.L;
+    gq.R = P.R;
+    gq.Rb = Q.rows;
+    gq.rect = 1;
+    for (int k = 0; k < P.L; ++k) {
+      for (int pt = 0; pt < 2; ++pt) {
+        const long long kd = goz_kdim(P, k, pt);
+        gq.nk[k][pt] = static_cast<int>(oz_kpad(kd) / 32);
+        if (kd == 0) continue;
+        const double *src, *gsrc;
+        long long ld;
+        if (pt == 0) {
+          src = k == 0 ? B.H0 : B.H[k];
+          gsrc = k == 0 ? gH0 : gH[k];
+          ld = k == 0 ? GF_H0_LD : P.ld[k];
+        } else {
+          src = B.Zb[k];
+          gsrc = gZ[k];
+          ld = P.ld[k + 1];
+        }
+        int8_t* Qa = reinterpret_cast<int8_t*>(w);
+        w += oz_al256(static_cast<size_t>(S) * P.R * oz_kpad(kd));
+        double* sa = reinterpret_cast<double*>(w);
+        w += oz_al256(static_cast<size_t>(P.R) * 8);
+        int8_t* Qb = reinterpret_cast<int8_t*>(w);
+        w += oz_al256(static_cast<size_t>(S) * rows_cap * oz_kpad(kd));
+        double* sb = reinterpret_cast<double*>(w);
+        w += oz_al256(static_cast<size_t>(rows_cap) * 8);
+        rc = oz_slice(ctx, s, src, P.R, kd, ld, S, Qa, sa);
+        if (rc == DNGD_OK) rc = oz_slice(ctx, s, gsrc, Q.rows, kd, ld, S, Qb, sb);
+        if (rc == DNGD_OK) rc = oz_encode(ctx, &gq.mA[k][pt], Qa, P.R, oz_kpad(kd), S, OZ_BM, 64);
+        if (rc == DNGD_OK) rc = oz_encode(ctx, &gq.mB[k][pt], Qb, Q.rows, oz_kpad(kd), S, OZ_BN);
+        if (rc) return rc;
+        gq.sc[k][pt] = sa;
+        gq.scB[k][pt] = sb;
+      }
+    }
+    // global point index of every landmark (column order = class order)
+    std::vector<long long> lpt(static_cast<size_t>(ell));
+    for (int j = 0; j < ell; ++j) lpt[j] = landmarks[j];
+    long long* lpt_dev = reinterpret_cast<long long*>(w);
+    e = cudaMemcpyAsync(lpt_dev, lpt.data(), static_cast<size_t>(ell) * sizeof(long long),
+                        cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_status(ctx, e, "gram_cols landmark upload");
+    gq.lpt = lpt_dev;
+    long long lc0 = 0;
+    for (int c = 0; c < P.T.n; ++c) {
+      gq.nch[c] = P.T.c[c].nch;
+      gq.ppc[c] = OZ_BN / P.T.c[c].nch;
+      gq.lcol0[c] = lc0;
+      gq.lcnt[c] = Q.lc[c];
+      gq.lrow0[c] = Q.lrow0[c];
+      lc0 += Q.lc[c];
+    }
+    int npairs = 0, ntile = 0;
+    gq.tstart[0] = 0;
+    for (int c = 0; c < P.T.n; ++c) {
+      for (int cp = 0; cp < P.T.n; ++cp) {
+        if (Q.lc[cp] == 0 || P.T.c[c].count == 0) continue;
+        const int TI = static_cast<int>((P.T.c[c].count + 2 * gq.ppc[c] - 1) / (2 * gq.ppc[c]));
+        const int TJ = static_cast<int>((Q.lc[cp] + gq.ppc[cp] - 1) / gq.ppc[cp]);
+        gq.pc[npairs] = c;
+        gq.pcp[npairs] = cp;
+        gq.ti_n[npairs] = TI;
+        gq.tj_n[npairs] = TJ;
+        ntile += TI * TJ;
+        gq.tstart[npairs + 1] = ntile;
+        ++npairs;
+      }
+    }
+    gq.npairs = npairs;
+    gq.K = Kc;
+    gq.ldK = ldKc;
+    gq.tile0 = 0;
+    if (ntile == 0) return DNGD_OK;
+    const size_t smem = gram_oz_smem(S);
+    auto kern = k_gram_oz<7>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return cuda_status(ctx, e, "gram_cols oz smem attribute");
+    kern<<<static_cast<unsigned>(std::min(ntile, ctx->num_sms)), OZ_THREADS, smem, s>>>(gq, ntile);
+    return cuda_status(ctx, cudaGetLastError(), "gram_cols oz");
+  }
   long long col0 = 0;
   for (int c = 0; c < P.T.n; ++c) {
     const ClassDev& Cc = P.T.c[c];

@@ -150,3 +150,33 @@ def test_gram_emulated_rejects_8_slices(K):
     Ke = torch.empty((m, m), dtype=torch.float64, device="cuda")
     with pytest.raises(DngdError):
         K.gram_factored_act(mlp, arr, len(classes), Ke, ws, slices=8)
+
+
+COLS_CASES = [
+    ("heat1d_w128", O.OracleHeat1d(), (2, 128, 128, 128, 1), (150, 40, 40)),
+    ("cfg3_structure", O.OraclePoissonSin(5), (5, 256, 256, 1), (120, 40)),
+    ("cfg5_structure", O.OraclePoisson2d(), (2, 256, 256, 256, 1), (400, 60)),
+]
+
+
+@pytest.mark.parametrize("name,problem,widths,counts", COLS_CASES)
+def test_gram_cols_emulated_matches_full_gram(K, name, problem, widths, counts):
+    """Nystrom sketch columns K[:, I] on the int8 engine (gram_oz.cuh rect mode:
+    full activations as row tiles, gathered landmark activations as column tiles)
+    against the emulated full Gram's columns and the oracle's J J_I^T."""
+    classes, theta, arr, keep, mlp, ws, m = _act_setup(K, problem, widths, counts, 3)
+    rng = np.random.default_rng(5)
+    ell = min(m - 1, 97)
+    landmarks = np.sort(rng.choice(m, size=ell, replace=False)).astype(np.int64)
+    Kf = torch.zeros((m, m), dtype=torch.float64, device="cuda")
+    K.gram_factored_act(mlp, arr, len(classes), Kf, ws, slices=7)
+    Kc = torch.full((m, ell + ell % 2), float("nan"), dtype=torch.float64, device="cuda")
+    K.gram_factored_cols(mlp, arr, len(classes), landmarks, Kc, ws)
+    torch.cuda.synchronize()
+    kc = Kc[:, :ell].cpu().numpy()
+    kf = Kf.cpu().numpy()[:, landmarks]
+    assert np.isfinite(kc).all()
+    assert np.linalg.norm(kc - kf) / np.linalg.norm(kf) <= 1e-14
+    r, J = O.linearize(theta, widths, classes)
+    ko = J @ J[landmarks].T
+    assert np.linalg.norm(kc - ko) / np.linalg.norm(ko) <= 1e-12

@@ -549,6 +549,14 @@ def run_ours(args, cfg):
         e2e = {"value": args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "aborted": tr.aborted}
 
+    # PCG configurations: CG iterations per step of the end-to-end run (the device
+    # loop's count, read once per step)
+    cg_per_step = None
+    if tr is not None:
+        its = [r.cg_iterations for r in tr.rows[1:] if getattr(r, "cg_iterations", None) is not None]
+        if its and max(its) > 0:  # (dense steps record 0)
+            cg_per_step = float(np.mean(its))
+
     # -------- roofline of the dominant kernel
     m = sum(cfg["counts"])
     n = spec.param_count()
@@ -626,12 +634,26 @@ def run_ours(args, cfg):
         rows = sum(c * maps[0]._nch(cl) for c, cl in zip(cfg["counts"], maps[0].collocation.classes))
         flops = 31 * 2.0 * rows * sum(w[k] * w[k + 1] for k in range(1, len(w) - 2))
         ach = flops / ls_avg / 1e12
-        roof = {"kernel": "dngd::k_gemm_nt<128,128> (31-candidate line-search forward, batched)",
-                "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": ach / fp64_peak, "traffic": None,
-                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
-                "algorithmic": f"31 x 2 R sum_k w_k w_k+1 = {flops:.3e} FLOP per line search "
-                               "(hidden layers; R = channel rows)"}
+        emulated = (os.environ.get("DNGD_GEMM_SLICES", "7" if max(w[1:-1]) >= 128 else "0")
+                    in ("7", "8"))
+        if emulated:  # int8 engine (pinn.cu oz_ls_slices): S(S+1)/2 = 28 digit products
+            ops = 28 * flops
+            roof = {"kernel": "dngd::k_oz_gemm<7,2> (31-candidate line-search forward, emulated "
+                              "FP64, batched; stage time includes k_chan_slice / k_tanh_head)",
+                    "bound": "tensor", "achieved": ops / ls_avg / 1e12, "peak": INT8_PEAK_TOPS,
+                    "unit": "TOPS (int8)", "frac": ops / ls_avg / 1e12 / INT8_PEAK_TOPS,
+                    "traffic": None, "peak_source": INT8_PEAK_SOURCE,
+                    "algorithmic": f"28 x 31 x 2 R sum_k w_k w_k+1 = {ops:.3e} useful int8 ops per "
+                                   f"line search ({flops:.3e} FP64 FLOP; hidden layers, R = channel rows)",
+                    "fp64_equivalent_tflops": ach,
+                    "fp64_equivalent_frac_of_dmma_peak": ach / fp64_peak}
+        else:
+            roof = {"kernel": "dngd::k_gemm_nt<128,128> (31-candidate line-search forward, batched)",
+                    "bound": "tensor", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": ach / fp64_peak, "traffic": None,
+                    "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 DMMA)",
+                    "algorithmic": f"31 x 2 R sum_k w_k w_k+1 = {flops:.3e} FLOP per line search "
+                                   "(hidden layers; R = channel rows)"}
     if roof is not None:
         roof["traffic"] = _profiled_traffic(cfg["name"], roof["kernel"])
     gram_chol = None
@@ -700,6 +722,7 @@ def run_ours(args, cfg):
         "gpu_launches": launches * args.steps,
         "clocks": clk,
         "final_loss": float(0.5 * float(maps[-1].residuals_t(theta).norm().item() ** 2)),
+        "cg_iterations_per_step": cg_per_step,
     }
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         line["cpu_baseline"] = (cpu_baseline(cfg, max_seconds=args.cpu_seconds)

@@ -1198,6 +1198,7 @@ DNGD_DEV void tanh_tjet(const ClassDev& C, ZGet zget, HPut hput) {
 }
 
 // input layer of the f_vv pass: H3 holds [a; b; c] blocks of R rows each.
+template <int ORD>  // 2: f_vv (a, b, c jets); 1: J v (a, b only -- the c block is never read)
 __global__ void k_fvv_input(Classes T, const double* __restrict__ theta,
                             const double* __restrict__ v, int w1, long long ld,
                             double* __restrict__ H3, const double* __restrict__ Zx,
@@ -1215,7 +1216,7 @@ __global__ void k_fvv_input(Classes T, const double* __restrict__ theta,
     const long long o = base + ch * ld;
     H3[o] = h.a;
     H3[o + blk] = h.b;
-    H3[o + 2 * blk] = h.c;
+    if (ORD == 2) H3[o + 2 * blk] = h.c;
   };
   if (C.inp) {
     // embedded inputs: channel ch is inputs_ch . (W0 + t V0) (+ bias on the value channel)
@@ -1254,6 +1255,7 @@ __global__ void k_fvv_input(Classes T, const double* __restrict__ theta,
 }
 
 // hidden layer: P = [Ha;Hb;Hc] W (3R rows), Q = [Ha;Hb] V (2R rows)
+template <int ORD>  // 2: f_vv; 1: J v (first-order jets: P holds 2R rows, Q R rows)
 __global__ void k_fvv_hidden(Classes T, const double* __restrict__ P, const double* __restrict__ Q,
                              const double* __restrict__ b, const double* __restrict__ vb, int w,
                              long long ld, double* __restrict__ H3) {
@@ -1267,7 +1269,7 @@ __global__ void k_fvv_hidden(Classes T, const double* __restrict__ P, const doub
   const long long blk = T.R * ld;
   auto zget = [&](int ch) -> T2 {
     const long long o = base + ch * ld;
-    T2 z = {P[o], P[o + blk] + Q[o], P[o + 2 * blk] + 2.0 * Q[o + blk]};
+    T2 z = {P[o], P[o + blk] + Q[o], ORD == 2 ? P[o + 2 * blk] + 2.0 * Q[o + blk] : 0.0};
     if (ch == 0) {
       z.a += b[q];
       z.b += vb[q];
@@ -1278,7 +1280,7 @@ __global__ void k_fvv_hidden(Classes T, const double* __restrict__ P, const doub
     const long long o = base + ch * ld;
     H3[o] = h.a;
     H3[o + blk] = h.b;
-    H3[o + 2 * blk] = h.c;
+    if (ORD == 2) H3[o + 2 * blk] = h.c;
   };
   tanh_tjet(C, zget, hput);
 }
@@ -3290,8 +3292,13 @@ static int fvv_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const
     rc = input_gemm(ctx, s, P, B.big, v, B.big.Dx);
     if (rc) return rc;
   }
-  k_fvv_input<<<nblk(P.m * P.w[1]), 256, 0, s>>>(P.T, theta, v, static_cast<int>(P.w[1]), ld,
-                                                  Hcur, zx, B.big.Dx, P.ld[1]);
+  if (order == 1) {
+    k_fvv_input<1><<<nblk(P.m * P.w[1]), 256, 0, s>>>(P.T, theta, v, static_cast<int>(P.w[1]), ld,
+                                                     Hcur, zx, B.big.Dx, P.ld[1]);
+  } else {
+    k_fvv_input<2><<<nblk(P.m * P.w[1]), 256, 0, s>>>(P.T, theta, v, static_cast<int>(P.w[1]), ld,
+                                                     Hcur, zx, B.big.Dx, P.ld[1]);
+  }
   transpose_hidden(s, P, theta, B.Wt);
   transpose_hidden(s, P, v, B.Vt);
   for (int k = 1; k <= L - 2; ++k) {
@@ -3313,8 +3320,13 @@ static int fvv_impl(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp, const
     rc = gemm_nt_hidden(ctx, s, g, B.oz);
     if (rc) return rc;
     const long long boff = P.off[k] + P.w[k] * P.w[k + 1];
-    k_fvv_hidden<<<nblk(P.m * P.w[k + 1]), 256, 0, s>>>(P.T, B.P3, B.Q2, theta + boff, v + boff,
-                                                        static_cast<int>(P.w[k + 1]), ld, Hnext);
+    if (order == 1) {
+      k_fvv_hidden<1><<<nblk(P.m * P.w[k + 1]), 256, 0, s>>>(P.T, B.P3, B.Q2, theta + boff, v + boff,
+                                                             static_cast<int>(P.w[k + 1]), ld, Hnext);
+    } else {
+      k_fvv_hidden<2><<<nblk(P.m * P.w[k + 1]), 256, 0, s>>>(P.T, B.P3, B.Q2, theta + boff, v + boff,
+                                                             static_cast<int>(P.w[k + 1]), ld, Hnext);
+    }
     std::swap(Hcur, Hnext);
   }
   k_fvv_head<<<nblk(P.m, 8), 256, 0, s>>>(P.T, Hcur, static_cast<int>(P.w[L - 1]), ld,

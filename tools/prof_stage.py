@@ -1,5 +1,5 @@
 """Kernel breakdown of one device stage at a BASELINE config (CUPTI via torch.profiler):
-  python tools/prof_stage.py {ls|vjp|fvv|act} [config 3|4]"""
+  python tools/prof_stage.py {ls|vjp|jvp|fvv|act} [config 3|4|5]"""
 import collections
 import os
 import sys
@@ -13,9 +13,10 @@ import paper_2505_21404_b200 as P  # noqa: E402
 
 stage = sys.argv[1] if len(sys.argv) > 1 else "fvv"
 cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-widths, counts = {3: ((5, 512, 512, 512, 512, 1), (3500, 500)),
-                  4: ((5, 1792, 1792, 1792, 1792, 1792, 1), (7000, 1000))}[cfg]
-prob = P.make_problem("poisson5d_sin")
+widths, counts, pname = {3: ((5, 512, 512, 512, 512, 1), (3500, 500), "poisson5d_sin"),
+                         4: ((5, 1792, 1792, 1792, 1792, 1792, 1), (7000, 1000), "poisson5d_sin"),
+                         5: ((2, 256, 256, 256, 256, 1), (30000, 2000), "poisson2d")}[cfg]
+prob = P.make_problem(pname)
 spec = P.MlpSpec(widths)
 rmap = P.PinnResidualMap(prob, spec, prob.sample(counts, np.random.default_rng(0)))
 theta = P.xavier_normal_params(spec)
@@ -26,6 +27,7 @@ wv = torch.randn(rmap.m, dtype=torch.float64, device="cuda")
 fn = {"ls": lambda: rmap.losses_along_t(theta, dev, etas),
       "vjp": lambda: rmap.vjp_t(theta, wv),
       "fvv": lambda: rmap.fvv_t(theta, dev),
+      "jvp": lambda: rmap.jvp_t(theta, dev),
       "act": lambda: (rmap._invalidate() if hasattr(rmap, "_invalidate") else None,
                       rmap.residuals_act_t(P.ParameterVector(theta.data + 0.0, spec.layout())))}[stage]
 for _ in range(2):

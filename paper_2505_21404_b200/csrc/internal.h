@@ -73,6 +73,14 @@ int oz_slice_into(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows
                   long long ld, long long kpad, size_t plane, int slices, int8_t* Q, double* scale);
 size_t oz_splitk_bytes(long long M, long long N, long long K, int slices, int splits);
 int oz_splitk_choose(dngd_ctx* ctx, long long M, long long N, long long K);
+struct OzSplitK {  // oz_gemm_splitk's workspace: planes, scales, partials
+  long long kl, kp;
+  int8_t *qa, *qb;
+  double *sa, *sb, *part;
+};
+OzSplitK oz_splitk_layout(void* work, long long M, long long N, long long K, int slices, int splits);
+int oz_splitk_finish(dngd_ctx* ctx, cudaStream_t s, const OzSplitK& L, long long M, long long N,
+                     int slices, int splits, double alpha, double* C, long long ldc);
 int oz_gemm_splitk(dngd_ctx* ctx, cudaStream_t s, const double* A, long long lda, const double* B,
                    long long ldb, long long M, long long N, long long K, double alpha, double* C,
                    long long ldc, int slices, int splits, void* work, size_t work_bytes);

@@ -231,6 +231,35 @@ int oz_splitk_choose(dngd_ctx* ctx, long long M, long long N, long long K) {
 // large (the J^T w contraction over activation rows): K cut into `splits` ranges,
 // each sliced with its own row scales into one batch entry of the int8 engine, the
 // partials summed in a fixed order.  work: oz_splitk_bytes.
+OzSplitK oz_splitk_layout(void* work, long long M, long long N, long long K, int slices, int splits) {
+  OzSplitK L;
+  L.kl = (K + splits - 1) / splits;
+  L.kp = oz_kpad(L.kl);
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  char* w = static_cast<char*>(work);
+  L.qa = reinterpret_cast<int8_t*>(w);
+  w += al(static_cast<size_t>(slices) * splits * M * L.kp);
+  L.qb = reinterpret_cast<int8_t*>(w);
+  w += al(static_cast<size_t>(slices) * splits * N * L.kp);
+  L.sa = reinterpret_cast<double*>(w);
+  w += al(static_cast<size_t>(splits) * M * 8);
+  L.sb = reinterpret_cast<double*>(w);
+  w += al(static_cast<size_t>(splits) * N * 8);
+  L.part = reinterpret_cast<double*>(w);
+  return L;
+}
+
+// the batched GEMM over planes already in the oz_splitk_layout and the fixed-order sum
+int oz_splitk_finish(dngd_ctx* ctx, cudaStream_t s, const OzSplitK& L, long long M, long long N,
+                     int slices, int splits, double alpha, double* C, long long ldc) {
+  int rc = oz_gemm_batched(ctx, s, L.qa, L.sa, splits * M, M, L.qb, L.sb, splits * N, N, L.kp, slices,
+                           M, N, splits, L.part, N, M * N);
+  if (rc) return rc;
+  k_oz_splitk_sum<<<static_cast<unsigned>((M * N + 255) / 256), 256, 0, s>>>(L.part, splits, M, N, ldc,
+                                                                          alpha, C);
+  return cuda_status(ctx, cudaGetLastError(), "oz_splitk_sum");
+}
+
 int oz_gemm_splitk(dngd_ctx* ctx, cudaStream_t s, const double* A, long long lda, const double* B,
                    long long ldb, long long M, long long N, long long K, double alpha, double* C,
                    long long ldc, int slices, int splits, void* work, size_t work_bytes) {
@@ -238,30 +267,13 @@ int oz_gemm_splitk(dngd_ctx* ctx, cudaStream_t s, const double* A, long long lda
   if (work_bytes < oz_splitk_bytes(M, N, K, slices, splits)) {
     return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm_splitk: workspace too small");
   }
-  const long long kl = (K + splits - 1) / splits;
-  const long long kp = oz_kpad(kl);
-  if (kp > kOzMaxK) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm_splitk: split longer than 32768");
-  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-  char* w = static_cast<char*>(work);
-  int8_t* qa = reinterpret_cast<int8_t*>(w);
-  w += al(static_cast<size_t>(slices) * splits * M * kp);
-  int8_t* qb = reinterpret_cast<int8_t*>(w);
-  w += al(static_cast<size_t>(slices) * splits * N * kp);
-  double* sa = reinterpret_cast<double*>(w);
-  w += al(static_cast<size_t>(splits) * M * 8);
-  double* sb = reinterpret_cast<double*>(w);
-  w += al(static_cast<size_t>(splits) * N * 8);
-  double* part = reinterpret_cast<double*>(w);
-  int rc = oz_slice_split(ctx, s, A, M, K, lda, kl, kp, splits, slices, qa, sa);
+  const OzSplitK L = oz_splitk_layout(work, M, N, K, slices, splits);
+  if (L.kp > kOzMaxK) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm_splitk: split longer than 32768");
+  int rc = oz_slice_split(ctx, s, A, M, K, lda, L.kl, L.kp, splits, slices, L.qa, L.sa);
   if (rc) return rc;
-  rc = oz_slice_split(ctx, s, B, N, K, ldb, kl, kp, splits, slices, qb, sb);
+  rc = oz_slice_split(ctx, s, B, N, K, ldb, L.kl, L.kp, splits, slices, L.qb, L.sb);
   if (rc) return rc;
-  rc = oz_gemm_batched(ctx, s, qa, sa, splits * M, M, qb, sb, splits * N, N, kp, slices, M, N,
-                           splits, part, N, M * N);
-  if (rc) return rc;
-  k_oz_splitk_sum<<<static_cast<unsigned>((M * N + 255) / 256), 256, 0, s>>>(part, splits, M, N, ldc,
-                                                                          alpha, C);
-  return cuda_status(ctx, cudaGetLastError(), "oz_splitk_sum");
+  return oz_splitk_finish(ctx, s, L, M, N, slices, splits, alpha, C, ldc);
 }
 
 int oz_encode(dngd_ctx* ctx, CUtensorMap* map, const int8_t* Q, long long rows, long long kpad,

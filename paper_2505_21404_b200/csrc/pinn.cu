@@ -2998,7 +2998,7 @@ static size_t cols_scratch_bytes(const Plan& P, long long rows) {
 }
 
 // K[:, I] on the int8 engine (gram_oz.cuh rect mode) under the same rule as the
-// factored Gram (kernels.gram_emulation_slices: hidden layers >= 128 wide,
+// factored Gram (kernels.gram_emulation_slices: hidden layers >= 64 wide,
 // DNGD_GRAM_SLICES=0 keeps the DMMA kernel); 0 where the emulated kernel does not apply
 static int goz_cols_slices(const Plan& P) {
   if (const char* e = getenv("DNGD_GRAM_SLICES")) {
@@ -3006,7 +3006,7 @@ static int goz_cols_slices(const Plan& P) {
   }
   long long hmax = 0;
   for (int k = 1; k < P.L; ++k) hmax = std::max(hmax, P.w[k]);
-  if (hmax < 128 || P.wide_in || P.T.din > DNGD_MAX_GRAD || P.R >= (1LL << 31)) return 0;
+  if (hmax < 64 || P.wide_in || P.T.din > DNGD_MAX_GRAD || P.R >= (1LL << 31)) return 0;
   for (int k = 0; k < P.L; ++k)
     if (goz_kdim(P, k, 0) > kOzMaxK || goz_kdim(P, k, 1) > kOzMaxK) return 0;
   for (int c = 0; c < P.T.n; ++c)

@@ -284,10 +284,10 @@ def gram_factored(mlp, theta, classes_arr, nclass, r, K, ws, part=0, nparts=1):
 
 def gram_emulation_slices(mlp=None) -> int:
     """Ozaki digit count of the factored Gram's G-space products (0 = FP64 DMMA).
-    DNGD_GRAM_SLICES (0 or 7) overrides; by default layers 128 wide or more run
-    emulated with 7 digits (int8 tcgen05, ~2x the DMMA kernel at config 3, K within
-    5e-16 of it) and narrower nets stay on DMMA (the int8 tile's fixed costs win
-    nothing at K = 64)."""
+    DNGD_GRAM_SLICES (0 or 7) overrides; by default hidden layers 64 wide or more run
+    emulated with 7 digits (int8 tcgen05: ~2.5x the DMMA kernel at config 3, 1.15x at
+    config 2's width 64; K within 5e-16 of it) and narrower nets stay on DMMA (a
+    32-wide layer is one K-chunk per phase: the TMEM drains would dominate)."""
     import os
 
     env = os.environ.get("DNGD_GRAM_SLICES")
@@ -299,7 +299,7 @@ def gram_emulation_slices(mlp=None) -> int:
     if mlp is None:
         return 7
     hidden = [mlp.widths[k] for k in range(1, mlp.nlayers)]
-    return 7 if hidden and max(hidden) >= 128 else 0
+    return 7 if hidden and max(hidden) >= 64 else 0
 
 
 def gram_factored_act(mlp, classes_arr, nclass, K, act_ws, part=0, nparts=1, slices=None):

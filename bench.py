@@ -852,7 +852,17 @@ def run_sharded(args, cfg):
     ops0 = ops_list[0]
     gk = stages.get("gram_kernel", 0.0) / max(counts.get("gram_kernel", 1), 1) * 1e-3
     sy = stages.get("syrk", 0.0) / max(counts.get("syrk", 1), 1) * 1e-3
-    if gk > 0:
+    emu = _emulated_gram(ops0.rmap) if gk > 0 else None
+    if gk > 0 and emu is not None:
+        ops, useful_ops, slices = emu
+        ops, useful_ops = ops / world, useful_ops / world
+        roof = {"kernel": f"dngd::k_gram_oz<{slices}> (this rank's 1/N of the tiles; emulated FP64)",
+                "bound": "tensor", "achieved": ops / gk / 1e12, "peak": INT8_PEAK_TOPS,
+                "unit": "TOPS (int8)", "frac": ops / gk / 1e12 / INT8_PEAK_TOPS, "traffic": None,
+                "peak_source": INT8_PEAK_SOURCE,
+                "algorithmic": f"{ops:.4e} int8 ops issued per rank per launch "
+                               f"({useful_ops:.4e} on useful rows)"}
+    elif gk > 0:
         flops = ops0.rmap.factored_gram_flops() / world
         roof = {"kernel": "dngd::k_gram_factored (this rank's 1/N of the tiles)",
                 "bound": "tensor", "achieved": flops / gk / 1e12, "peak": fp64_peak,

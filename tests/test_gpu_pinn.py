@@ -13,6 +13,10 @@ CASES = [
     ("heat1d", O.OracleHeat1d(), (2, 64, 64, 64, 64, 1), (60, 20, 20)),
     ("poisson5d", O.OraclePoissonSin(5), (5, 32, 32, 32, 32, 1), (40, 12)),
     ("poisson5d_wide", O.OraclePoissonSin(5), (5, 128, 96, 1), (20, 10)),
+    # emulated GEMMs through the fused line-search maps (k_chan_slice, k_tanh_head)
+    ("poisson5d_deep_wide", O.OraclePoissonSin(5), (5, 128, 128, 128, 1), (20, 8)),
+    # nch = 12 > 8: the unfused emulated line search (k_tanh_fwd + slicing, k_head)
+    ("poisson10d_wide", O.OraclePoissonSin(10), (10, 128, 128, 1), (24, 8)),
     # reference Allen-Cahn: periodic input embedding + cubic reaction term
     ("allen_cahn", O.OracleAllenCahn(), (3, 32, 32, 32, 1), (60, 20)),
     ("allen_cahn_wide", O.OracleAllenCahn(), (3, 160, 96, 1), (30, 10)),

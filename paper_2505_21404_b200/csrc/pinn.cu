@@ -346,22 +346,17 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_chan_slice(
       constexpr double sh = Ld == 4 ? 0x1p28 : Ld == 3 ? 0x1p21 : 0x1p14;
       const double X = bad[ch] ? 0.0 : rint(v[ch] * sinv[ch]);
       const double Xh = floor((X + cL) * (1.0 / sh));
-      int ul = __double2int_rn(fma(-Xh, sh, X));
-      int uh = __double2int_rn(Xh);
+      // with the carry offsets added up front (T = u + 64 (1 + 128 + ...)), digit j is
+      // the j-th 7-bit field of T minus 64 and the leading digit is T >> 21 -- the
+      // recurrence's digits without its serial adds
+      const int Tl = __double2int_rn(fma(-Xh, sh, X)) + static_cast<int>(cL);
+      const int Th = __double2int_rn(Xh) + 64 * (1 + 128 + 16384);
       int8_t* dst = Q + (row0 + ch) * kpad + q;
 #pragma unroll
-      for (int t = S - 1; t >= 4; --t) {
-        const int tt = ul + 64;
-        dst[t * plane] = static_cast<int8_t>((tt & 127) - 64);
-        ul = tt >> 7;
-      }
+      for (int t = S - 1; t >= 4; --t) dst[t * plane] = static_cast<int8_t>(((Tl >> (7 * (S - 1 - t))) & 127) - 64);
 #pragma unroll
-      for (int t = 3; t >= 1; --t) {
-        const int tt = uh + 64;
-        dst[t * plane] = static_cast<int8_t>((tt & 127) - 64);
-        uh = tt >> 7;
-      }
-      dst[0] = static_cast<int8_t>(uh);
+      for (int t = 3; t >= 1; --t) dst[t * plane] = static_cast<int8_t>(((Th >> (7 * (3 - t))) & 127) - 64);
+      dst[0] = static_cast<int8_t>(Th >> 21);
     }
   }
 }

@@ -306,11 +306,18 @@ def gram_factored_act(mlp, classes_arr, nclass, K, act_ws, part=0, nparts=1, sli
     """K (or part `part` of nparts of its tiles) from the activations in act_ws: the
     G-space products on the int8 tensor cores (Ozaki slices, gram_oz.cuh) unless
     slices == 0, then on the FP64 DMMA pipe (gram_factored.cuh)."""
-    slices = gram_emulation_slices(mlp) if slices is None else int(slices)
+    auto = slices is None
+    slices = gram_emulation_slices(mlp) if auto else int(slices)
     if slices:
         nb = c_size(0)
-        call("dngd_gram_oz_workspace", ctx(), ctypes.byref(mlp), classes_arr, nclass, slices,
-             ctypes.byref(nb))
+        lib = _lib.load_library()
+        rc = lib.dngd_gram_oz_workspace(ctx(), ctypes.byref(mlp), classes_arr, nclass, slices,
+                                        ctypes.byref(nb))
+        if rc == _lib.DNGD_ERR_UNSUPPORTED and auto:
+            # outside the emulated kernel's shapes (goz_check: input dim, channels per
+            # point, layer width): the FP64 DMMA kernel computes the same K
+            return gram_factored_act(mlp, classes_arr, nclass, K, act_ws, part, nparts, 0)
+        _lib.check(rc, "dngd_gram_oz_workspace")
         ows = workspace("gram_oz", nb.value)
         call("dngd_gram_oz_act", ctx(), stream_handle(), ctypes.byref(mlp), classes_arr, nclass,
              ptr(K), K.stride(0), int(part), int(nparts), slices, ptr(act_ws), act_ws.numel(),

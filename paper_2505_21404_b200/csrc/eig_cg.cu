@@ -330,7 +330,7 @@ struct JacShape {
 
 static JacShape jac_shape(long long n) {
   JacShape sh;
-  static const int bs_env = getenv("DNGD_JACOBI_BS") ? atoi(getenv("DNGD_JACOBI_BS")) : 16;
+  static const int bs_env = getenv("DNGD_JACOBI_BS") ? atoi(getenv("DNGD_JACOBI_BS")) : 8;
   int bs = std::max(2, std::min(16, bs_env));
   while (bs > 2 && static_cast<size_t>(2 * bs) * (n + 1) * 8 > 150 * 1024) bs /= 2;
   sh.bs = bs;

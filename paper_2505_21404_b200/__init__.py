@@ -19,7 +19,7 @@ from .errors import (
     FactorizationError,
     NonFiniteError,
 )
-from .model import MlpSpec, init_params, xavier_normal_params
+from .model import MlpSpec, OutputTransform, init_params, point_columns, xavier_normal_params
 from .optimizer import (
     LineSearchResult,
     OptimizerConfig,
@@ -58,6 +58,7 @@ from .residuals import (
     INTERIOR,
     CollocationClass,
     CollocationSet,
+    IcShiftResidualMap,
     LinearResidualMap,
     PinnResidualMap,
     RegressionResidualMap,

@@ -685,6 +685,9 @@ class _ValueProblem:
         self.input_dim = getattr(problem, "input_dim", dim) if problem is not None else dim
         if problem is not None and hasattr(problem, "value_factor"):
             self.point_coefs = self._coefs
+        tr = getattr(problem, "transform", None)
+        if tr is not None and tr.kind == "ic_shift":
+            self.transform = tr  # u = phi - phi(0, .) + q0 on the grid too (model.py:237-248)
 
     def class_operator(self, class_id):
         from .problems import VALUE

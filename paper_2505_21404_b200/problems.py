@@ -25,6 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .errors import DomainError
+from .model import OutputTransform
 from .residuals import BOUNDARY, INITIAL, INTERIOR, CollocationClass, CollocationSet
 
 
@@ -103,6 +104,7 @@ def _cls(class_id, points, aux=None):
 class PdeProblem:
     name: str
     raw_dim: int
+    transform = OutputTransform("identity")  # model.py:181-197; ic_shift -> IcShiftResidualMap
     default_counts: dict
     default_widths: tuple
     default_lam_cap: float = 1e-5
@@ -420,6 +422,7 @@ class PoissonBallStde(PdeProblem):
     derivative dims S and coefficients (2d, 4 (d/k) x_j, -(d/k)(1 - |x|^2))."""
 
     name = "poisson_ball_stde"
+    transform = OutputTransform("dirichlet_ball")  # stated as per-point coefficients below
     default_lam_cap = 1e3
     has_exact = True
 

@@ -396,6 +396,14 @@ class PinnResidualMap(ResidualMap):
 
     LOSS_WS_BUDGET = 8 * 1024**3  # bytes of line-search activations per chunk
 
+    def __new__(cls, *args, **kwargs):
+        # problems with the ic_shift output transform get the two-map form
+        if cls is PinnResidualMap:
+            problem = args[0] if args else kwargs.get("problem")
+            if _is_ic_shift(problem):
+                return IcShiftResidualMap(*args, **kwargs)
+        return super().__new__(cls)
+
     def __init__(self, problem, spec, collocation: CollocationSet, col_range=None):
         from .model import MlpSpec
 
@@ -868,3 +876,160 @@ class RegressionResidualMap(PinnResidualMap):
     def rebind(self, collocation):
         cls = collocation.classes[0]
         return RegressionResidualMap(self.spec, cls.points, cls.aux["targets"], cls.weight)
+
+
+# -- ic_shift output transform (reference model.py:181-277) ------------------------------------
+
+
+def _is_ic_shift(problem) -> bool:
+    tr = getattr(problem, "transform", None)
+    return tr is not None and getattr(tr, "kind", "identity") == "ic_shift"
+
+
+class _IcShiftPart:
+    """One half of an ic_shift problem as a plain device problem.
+
+    u(t, x) = phi(t, x) - phi(0, x) + q0(x) (model.py:237-277), so for a linear class
+    operator L the residual splits as r = r_A + r_B with
+      A: L phi at the points, data f - L q0 (q0's derivatives by host 2-jets);
+      B: -L' phi at the points moved to t = 0, data 0, where L' drops every
+         time-derivative term (the reference's shift is constant along t,
+         model.py:270-272).
+    """
+
+    def __init__(self, base, shifted: bool):
+        self.base = base
+        self.shifted = shifted
+        self.name = f"{getattr(base, 'name', 'problem')}:{'shift' if shifted else 'base'}"
+        self.raw_dim = base.raw_dim
+        self.input_dim = getattr(base, "input_dim", base.raw_dim)
+        if hasattr(base, "input_channels"):
+            self.input_channels = base.input_channels
+        if hasattr(base, "point_grad_dims") or hasattr(base, "point_coefs"):
+            raise DomainError("ic_shift with per-point derivative sets is not supported")
+
+    def class_operator(self, class_id):
+        from .problems import ClassOperator
+
+        op = self.base.class_operator(class_id)
+        if getattr(op, "c3", 0.0):
+            raise DomainError("ic_shift needs a linear class operator (u^3 term present)")
+        if not self.shifted:
+            return op
+        keep = [g for g, j in enumerate(op.grad_dims) if j != 0]
+        return ClassOperator(cu=-op.cu, grad_dims=tuple(op.grad_dims[g] for g in keep),
+                             cg=tuple(-op.cg[g] for g in keep),
+                             lap_dims=tuple(j for j in op.lap_dims if j != 0), cl=-op.cl)
+
+    def class_data(self, cls):
+        if self.shifted:
+            return np.zeros(cls.count)
+        from .model import jet_value, point_columns
+
+        op = self.base.class_operator(cls.class_id)
+        q0 = self.base.transform.q0
+        pts = cls.points
+        n = pts.shape[0]
+        lq = op.cu * jet_value(q0(point_columns(pts)), n).v
+        jets = {j: jet_value(q0(point_columns(pts, j)), n)
+                for j in set(op.grad_dims) | set(op.lap_dims)}
+        for g, j in enumerate(op.grad_dims):
+            lq = lq + op.cg[g] * jets[j].d1
+        if op.lap_dims:
+            lq = lq + op.cl * sum(jets[j].d2 for j in op.lap_dims)
+        return np.asarray(self.base.class_data(cls), dtype=np.float64) - lq
+
+
+class IcShiftResidualMap(ResidualMap):
+    """PINN residual map of a problem with the ic_shift output transform
+    (model.py:181-277): two device maps (`_IcShiftPart`) whose residuals, Jacobian
+    rows and second directional derivatives add; J is materialised (J = J_A + J_B)
+    and the Gram is the SYRK over it.  `PinnResidualMap(problem, ...)` returns this
+    map for such problems, so callers construct it exactly as the reference does."""
+
+    graph_capable = False  # candidates' losses need per-candidate residual vectors
+    gram_mode = "materialized"
+
+    def __init__(self, problem, spec, collocation: CollocationSet, col_range=None):
+        from .model import MlpSpec
+
+        if not isinstance(spec, MlpSpec):
+            raise DimensionError("PinnResidualMap needs an MlpSpec")
+        if col_range is not None and tuple(col_range) != (0, spec.layout().size):
+            raise DomainError("ic_shift maps are not column-sharded")
+        self.problem = problem
+        self.spec = spec
+        self.layout = spec.layout()
+        self.collocation = collocation
+        self.col_range = (0, self.layout.size)
+        shifted = []
+        for c in collocation.classes:
+            p0 = np.array(c.points, dtype=np.float64, copy=True)
+            p0[:, 0] = 0.0
+            shifted.append(CollocationClass(c.class_id, p0, c.weight, dict(c.aux)))
+        self.A = PinnResidualMap(_IcShiftPart(problem, False), spec, collocation)
+        self.B = PinnResidualMap(_IcShiftPart(problem, True), spec, CollocationSet(shifted))
+        for part in (self.A, self.B):
+            part.gram_mode = "materialized"
+        self._cache = None
+        self._J = None
+
+    def rebind(self, collocation):
+        return IcShiftResidualMap(self.problem, self.spec, collocation)
+
+    def jfree(self) -> bool:
+        return False
+
+    def jfree_pcg(self) -> bool:
+        return False
+
+    def use_factored_gram(self) -> bool:
+        return False
+
+    def _key(self, th):
+        return (th.data_ptr(), th._version, id(self.collocation))
+
+    def linearize_t(self, theta):
+        import torch
+
+        from . import kernels as K
+
+        th = self._theta_t(theta)
+        key = self._key(th)
+        if self._cache is not None and self._cache[0] == key:
+            return self._cache[1], self._cache[2]
+        rA, JA = self.A.linearize_t(th)
+        rB, JB = self.B.linearize_t(th)
+        if self._J is None or self._J.shape != JA.shape:
+            self._J = torch.empty_like(JA)
+        r = K.axpby(1.0, rA, 1.0, rB)
+        K.axpby(1.0, JA, 1.0, JB, out=self._J)
+        self._cache = (key, r, self._J, th)
+        return r, self._J
+
+    def residuals_t(self, theta):
+        from . import kernels as K
+
+        th = self._theta_t(theta)
+        if self._cache is not None and self._cache[0] == self._key(th):
+            return self._cache[1]
+        return K.axpby(1.0, self.A.residuals_t(th), 1.0, self.B.residuals_t(th))
+
+    def fvv_t(self, theta, v_t):
+        from . import kernels as K
+
+        th = self._theta_t(theta)
+        return K.axpby(1.0, self.A.fvv_t(th, v_t), 1.0, self.B.fvv_t(th, v_t))
+
+    def loss_many_t(self, cands_t):
+        import torch
+
+        from . import kernels as K
+
+        C = cands_t.shape[0]
+        out = torch.empty(C, dtype=torch.float64, device=cands_t.device)
+        for c in range(C):
+            th = cands_t[c]
+            r = K.axpby(1.0, self.A.residuals_t(th), 1.0, self.B.residuals_t(th))
+            K.dot(r, r, out=out[c:c + 1])
+        return K.axpby(0.5, out)

@@ -303,8 +303,29 @@ def main_stde():
                        {INTERIOR: 48}, 10, 1e3, 3)
 
 
+def main_ic_shift():
+    """ic_shift output transform (model.py:181-277): the reference's own Heat(1) with
+    u = phi(t, x) - phi(0, x) + q0(x), q0 = sin(2 pi x) (its exact initial trace)."""
+    from dngd.model import OutputTransform
+    from dngd.problems import Heat
+
+    class HeatIcShift(Heat):
+        def __init__(self):
+            super().__init__(1)
+            self.name = "heat1d_ic_shift"
+            self.transform = OutputTransform(
+                "ic_shift", q0=lambda cols: ops.sin(ops.mul(2.0 * np.pi, cols[1])))
+
+    step_fixture("icshift_step", HeatIcShift(), (2, 24, 24, 1), {INTERIOR: 40, BOUNDARY: 16}, 11,
+                 [1e-3, 1e-6])
+    trajectory_fixture("icshift_traj", HeatIcShift(), (2, 16, 16, 1),
+                       {INTERIOR: 60, BOUNDARY: 20}, 12, 1e-3, 4)
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["allen_cahn"]:
+    if sys.argv[1:] == ["ic_shift"]:
+        main_ic_shift()
+    elif sys.argv[1:] == ["allen_cahn"]:
         main_allen_cahn()
     elif sys.argv[1:] == ["stde"]:
         main_stde()
@@ -316,3 +337,4 @@ if __name__ == "__main__":
         main()
         main_allen_cahn()
         main_stde()
+        main_ic_shift()

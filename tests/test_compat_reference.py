@@ -110,3 +110,37 @@ def test_install_routes_reference_steps(dngd):
         compat.uninstall(dngd, orig)
     assert (dngd.solver.dense_dual_solve, dngd.optimizer.dense_dual_solve,
             dngd.solver.pcg_step, dngd.optimizer.pcg_step) == before
+
+
+def test_ic_shift_reference_problem_reproduces_reference_residuals(dngd):
+    """A reference Heat(1) with OutputTransform("ic_shift", q0) written against the
+    reference's ops module (model.py:181-277): the adapter yields the two-map
+    IcShiftResidualMap, the reference q0 evaluates on host jets, and the two parts'
+    operators + data reproduce the reference residuals (oracle evaluation)."""
+    from oracle import dngd_oracle as O
+    from paper_2505_21404_b200 import compat
+
+    ops = dngd.ops
+
+    class HeatIc(dngd.problems.Heat):
+        def __init__(self):
+            super().__init__(1)
+            self.transform = dngd.model.OutputTransform(
+                "ic_shift", q0=lambda c: ops.mul(ops.sin(ops.mul(np.pi, c[1])),
+                                                 ops.exp(ops.mul(0.5, c[1]))))
+
+    ref_problem = HeatIc()
+    colloc = dngd.problems.sample_collocation(ref_problem, (50, 30), np.random.default_rng(5))
+    spec = dngd.model.MlpSpec((2, 10, 10, 1), seed=4)
+    ref_map = dngd.residuals.PinnResidualMap(ref_problem, spec, colloc)
+    theta = dngd.model.init_params(spec)
+    ref_r = ref_map.residual_batch(theta).values
+
+    ours = compat.map_from_reference(ref_map)
+    assert type(ours).__name__ == "IcShiftResidualMap"
+    a = _oracle_classes(ours.A.problem, ours.A.collocation)
+    b = _oracle_classes(ours.B.problem, ours.B.collocation)
+    for ca, cb in zip(a, b):
+        ca.shift = cb
+    r = O.residuals(np.asarray(theta.data), (2, 10, 10, 1), a)
+    np.testing.assert_allclose(r, ref_r, rtol=1e-12, atol=1e-13 * np.abs(ref_r).max())

@@ -37,6 +37,7 @@ STEP = {
     "cfg3_step": ("poisson5d_sin", ("interior", "boundary"), O.OraclePoissonSin(5)),
     "ac_step": ("allen_cahn", ("interior", "initial"), O.OracleAllenCahn()),
     "stde_step": ("poisson_ball_stde", ("interior",), O.OraclePoissonBallStde(10, 3)),
+    "icshift_step": ("heat1d_ic_shift", ("interior", "boundary"), O.OracleHeatIcShift()),
 }
 
 PROBLEM_KW = {"poisson_ball_stde": dict(dim=10, index_set_size=3)}
@@ -48,8 +49,18 @@ def _oclasses(oprob, fx, ids):
     return oprob.classes(*[fx[f"pts_{c}"] for c in ids])
 
 
+def _problem(P, name, **kw):
+    """make_problem, plus the reference Heat(1) with the ic_shift output transform
+    (u = phi(t, x) - phi(0, x) + sin(2 pi x); golden fixtures icshift_*)."""
+    if name == "heat1d_ic_shift":
+        problem = P.Heat(1)
+        problem.transform = P.OutputTransform("ic_shift", q0=lambda c: np.sin(2.0 * np.pi * c[1]))
+        return problem
+    return P.make_problem(name, **kw)
+
+
 def _map(P, fx, problem_name, ids):
-    problem = P.make_problem(problem_name, **PROBLEM_KW.get(problem_name, {}))
+    problem = _problem(P, problem_name, **PROBLEM_KW.get(problem_name, {}))
     widths = tuple(int(w) for w in fx["widths"])
     spec = P.MlpSpec(widths)
     classes = [P.CollocationClass(c, fx[f"pts_{c}"], 1.0 / np.sqrt(len(fx[f"pts_{c}"])),
@@ -104,7 +115,7 @@ def test_dense_step_matches_reference(P, golden_dir, name):
         np.testing.assert_allclose(rmap.loss_many(cands), fx[f"ls_losses_{i}"], rtol=1e-10)
 
 
-@pytest.mark.parametrize("name", sorted(STEP))
+@pytest.mark.parametrize("name", sorted(set(STEP) - {"icshift_step"}))  # ic_shift: J only
 @pytest.mark.parametrize("mode", ["factored", "materialized"])
 def test_gram_modes_match_reference(P, golden_dir, name, mode):
     """Both Gram paths (SYRK over J; factored from the activations) reproduce the
@@ -135,6 +146,7 @@ TRAJ = {
                        dict(dim=200, index_set_size=4)),
     "pcg_traj": ("poisson2d", (60, 20),
                  dict(lam_cap=1e-3, dense_threshold=10, nystrom_rank=16, cg_max_iters=100)),
+    "icshift_traj": ("heat1d_ic_shift", (60, 20), dict(lam_cap=1e-3)),
 }
 
 
@@ -146,7 +158,7 @@ def test_trajectory_matches_reference(P, golden_dir, name):
     widths = tuple(int(w) for w in fx["widths"])
     n_steps = len(fx["loss"]) - 1
     config = P.OptimizerConfig(max_iters=n_steps, deterministic_timing=True, **cfg)
-    trace = P.dngd_run(P.make_problem(pname, **pkw), P.MlpSpec(widths),
+    trace = P.dngd_run(_problem(P, pname, **pkw), P.MlpSpec(widths),
                        config, int(fx["seed"]), counts=counts, init="xavier_normal")
     assert not trace.aborted, trace.abort_reason
     loss = np.array([r.loss for r in trace.rows])
@@ -454,3 +466,41 @@ def test_timing_sweep_regime_winners(P):
     for r in rows:
         assert r["primal_s"] > 0.0 and r["dual_s"] > 0.0
         assert set(r) == {"m", "n", "primal_s", "dual_s", "winner"}
+
+
+def test_ic_shift_at_size_matches_oracle(P):
+    """ic_shift (model.py:181-277) at m = 1210, width 64: residuals, J, K, f_vv, the GN
+    and GA directions and the line-search losses against the oracle; rows at t = 0
+    are exact (u = q0 there, so their J rows vanish)."""
+    oprob = O.OracleHeatIcShift()
+    rng = np.random.default_rng(31)
+    ocls = oprob.sample((1000, 210), rng)
+    widths = (2, 64, 64, 1)
+    spec = P.MlpSpec(widths)
+    problem = _problem(P, "heat1d_ic_shift")
+    classes = [P.CollocationClass(c.class_id, c.points, c.weight) for c in ocls]
+    rmap = P.PinnResidualMap(problem, spec, P.CollocationSet(classes))
+    assert isinstance(rmap, P.IcShiftResidualMap)
+    theta_np = O.xavier_normal_init(widths, 31)
+    theta = P.ParameterVector(theta_np, spec.layout())
+    ro, Jo = O.linearize(theta_np, widths, ocls)
+    batch, g = rmap.residuals_and_gradient(theta)
+    assert _rel(batch.values, ro) <= 1e-12
+    Jg = rmap.jacobian(theta)
+    assert _rel(Jg, Jo) <= 1e-12
+    t0 = np.flatnonzero(ocls[1].points[:, 0] == 0.0) + ocls[0].count
+    assert t0.size > 0 and np.all(Jg[t0] == 0.0)
+    gram = P.assemble_gramian(rmap, theta)
+    assert _rel(gram.K, O.gram(Jo)) <= 1e-12
+    lam = 1e-4
+    fvv_fn = lambda v: O.second_directional(theta_np, widths, ocls, v)
+    ores = O.dense_dual_solve(Jo, Jo.T @ ro, lam, True, fvv_fn)
+    fl = O.direction_floors(Jo, Jo.T @ ro, lam, fvv_fn, j_rel=max(_rel(Jg, Jo), 1e-16))
+    res = P.dense_dual_solve(rmap, theta, g, lam=lam, use_ga=True)
+    assert _rel(res.delta.data, ores.delta) <= max(1e-8, 10 * fl["delta"])
+    v = ores.extras["v"]
+    assert _rel(rmap.second_directional(theta, v), fvv_fn(v)) <= 1e-10
+    etas = 2.0 ** -np.arange(31, dtype=np.float64)
+    cands = theta_np[None, :] + etas[:, None] * ores.delta[None, :]
+    np.testing.assert_allclose(rmap.loss_many(cands), O.loss_many(cands, widths, ocls),
+                               rtol=1e-10)

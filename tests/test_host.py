@@ -226,3 +226,58 @@ def test_stde_index_draw_matches_reference_argsort():
     want = rng_b.random((50, 300)).argsort(axis=1)[:, :8]
     assert np.array_equal(np.asarray(got), want)
     assert rng_a.random() == rng_b.random()
+
+
+def test_output_transform_and_host_jets():
+    """OutputTransform validation (model.py:181-197) and the host 2-jets that give
+    ic_shift its L q0 data term, against central differences."""
+    from paper_2505_21404_b200.errors import DomainError
+    from paper_2505_21404_b200.model import OutputTransform, point_columns
+
+    with pytest.raises(DomainError):
+        OutputTransform("sideways")
+    with pytest.raises(DomainError):
+        OutputTransform("ic_shift")
+    p = np.random.default_rng(0).uniform(size=(7, 2))
+
+    def q(c):
+        return np.sin(2 * np.pi * c[1]) * np.exp(-c[0]) + c[1] ** 3 / (1 + c[1]) - np.tanh(c[0] * c[1])
+
+    h = 1e-4
+    for d in (0, 1):
+        jet = q(point_columns(p, d))
+        e = np.zeros(2)
+        e[d] = h
+        f = lambda x: q([x[:, 0], x[:, 1]])
+        np.testing.assert_allclose(jet.v, f(p), rtol=1e-15)
+        np.testing.assert_allclose(jet.d1, (f(p + e) - f(p - e)) / (2 * h), atol=1e-6)
+        np.testing.assert_allclose(jet.d2, (f(p + e) - 2 * f(p) + f(p - e)) / h**2, atol=1e-4)
+
+
+def test_ic_shift_parts_match_oracle_classes():
+    """The two device problems of an ic_shift map (residuals._IcShiftPart) state the
+    same operators and data as the oracle's ic_shift_class restatement."""
+    from oracle import dngd_oracle as O
+    from paper_2505_21404_b200 import Heat, MlpSpec, OutputTransform, PinnResidualMap
+    from paper_2505_21404_b200.errors import DomainError
+
+    prob = Heat(1)
+    prob.transform = OutputTransform("ic_shift", q0=lambda c: np.sin(2.0 * np.pi * c[1]))
+    colloc = prob.sample({"interior": 30, "boundary": 12}, np.random.default_rng(2))
+    rmap = PinnResidualMap(prob, MlpSpec((2, 8, 1)), colloc)
+    ocls = O.OracleHeatIcShift().classes(*[c.points for c in colloc.classes])
+    for part, shifted in ((rmap.A, False), (rmap.B, True)):
+        for c, oc in zip(part.collocation.classes, ocls):
+            oc = oc.shift if shifted else oc
+            op = part.problem.class_operator(c.class_id)
+            assert (op.cu, tuple(op.grad_dims), tuple(op.cg), tuple(op.lap_dims), op.cl) == \
+                (oc.cu, tuple(oc.grad_dims), tuple(oc.cg), tuple(oc.lap_dims), oc.cl)
+            np.testing.assert_array_equal(c.points, oc.points)
+            np.testing.assert_allclose(part.problem.class_data(c), oc.f, rtol=1e-13, atol=1e-13)
+    from paper_2505_21404_b200 import AllenCahn
+
+    ac = AllenCahn()
+    ac.transform = OutputTransform("ic_shift", q0=lambda c: c[1])
+    with pytest.raises(DomainError, match="linear"):
+        PinnResidualMap(ac, MlpSpec((3, 8, 1)), ac.sample(None, np.random.default_rng(0))).A \
+            .problem.class_operator("interior")

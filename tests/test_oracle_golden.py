@@ -26,6 +26,7 @@ PROBLEMS = {
     "cfg3_step": (O.OraclePoissonSin(5), ("interior", "boundary")),
     "ac_step": (O.OracleAllenCahn(), ("interior", "initial")),
     "stde_step": (O.OraclePoissonBallStde(10, 3), ("interior",)),
+    "icshift_step": (O.OracleHeatIcShift(), ("interior", "boundary")),
 }
 
 
@@ -101,6 +102,7 @@ TRAJ = {
     "stde_traj": (O.OraclePoissonBallStde(10, 3), (40,), O.LoopConfig(lam_cap=1e3, max_iters=3)),
     "stde_wide_traj": (O.OraclePoissonBallStde(200, 4), (48,),
                        O.LoopConfig(lam_cap=1e3, max_iters=3)),
+    "icshift_traj": (O.OracleHeatIcShift(), (60, 20), O.LoopConfig(lam_cap=1e-3, max_iters=4)),
     "pcg_traj": (O.OraclePoisson2d(), (60, 20),
                  O.LoopConfig(lam_cap=1e-3, max_iters=3, dense_threshold=10, nystrom_rank=16,
                               cg_max_iters=100)),

@@ -634,16 +634,17 @@ def run_ours(args, cfg):
         rows = sum(c * maps[0]._nch(cl) for c, cl in zip(cfg["counts"], maps[0].collocation.classes))
         flops = 31 * 2.0 * rows * sum(w[k] * w[k + 1] for k in range(1, len(w) - 2))
         ach = flops / ls_avg / 1e12
-        emulated = (os.environ.get("DNGD_GEMM_SLICES", "7" if max(w[1:-1]) >= 128 else "0")
-                    in ("7", "8"))
-        if emulated:  # int8 engine (pinn.cu oz_ls_slices): S(S+1)/2 = 28 digit products
-            ops = 28 * flops
-            roof = {"kernel": "dngd::k_oz_gemm<7,2> (31-candidate line-search forward, emulated "
+        ls_S = int(os.environ.get("DNGD_GEMM_SLICES", "6" if max(w[1:-1]) >= 128 else "0"))
+        emulated = ls_S in (6, 7)
+        if emulated:  # int8 engine (pinn.cu oz_ls_slices): S(S+1)/2 digit products
+            nprod = ls_S * (ls_S + 1) // 2
+            ops = nprod * flops
+            roof = {"kernel": f"dngd::k_oz_gemm<{ls_S},2> (31-candidate line-search forward, emulated "
                               "FP64, batched; stage time includes k_chan_slice / k_tanh_head)",
                     "bound": "tensor", "achieved": ops / ls_avg / 1e12, "peak": INT8_PEAK_TOPS,
                     "unit": "TOPS (int8)", "frac": ops / ls_avg / 1e12 / INT8_PEAK_TOPS,
                     "traffic": None, "peak_source": INT8_PEAK_SOURCE,
-                    "algorithmic": f"28 x 31 x 2 R sum_k w_k w_k+1 = {ops:.3e} useful int8 ops per "
+                    "algorithmic": f"{nprod} x 31 x 2 R sum_k w_k w_k+1 = {ops:.3e} useful int8 ops per "
                                    f"line search ({flops:.3e} FP64 FLOP; hidden layers, R = channel rows)",
                     "fp64_equivalent_tflops": ach,
                     "fp64_equivalent_frac_of_dmma_peak": ach / fp64_peak}

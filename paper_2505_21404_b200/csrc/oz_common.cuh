@@ -17,7 +17,12 @@ constexpr int OZ_EPI = 16, OZ_LD = 4;
 constexpr int OZ_COLS = OZ_BN / (OZ_EPI / 4);
 constexpr int OZ_ETHREADS = 32 * OZ_EPI;
 constexpr int OZ_THREADS = 64 + OZ_ETHREADS;
-constexpr long long kOzMaxK = 32768;  // |acc_D| <= K (2 127 64 + 6 64^2) < 2^31 (tc05.cuh)
+// Digit base 2^OZ_BITS: balanced base-256 digits fill the int8 range [-128, 127]
+// (round 2 start: base 128, 7 digits = 28 products per FP64 product; base 256 needs
+// 6 digits = 21 products for the same ~48 bits below the row maximum).
+constexpr int OZ_BITS = 8;
+constexpr int OZ_SMIN = 6, OZ_SMAX = 7;  // 48 / 56 bits; 8 digits would overflow the int64 X
+constexpr long long kOzMaxK = 16384;  // |acc_D| <= K (2 127 128 + 5 128^2) < 2^31 (tc05.cuh)
 
 inline long long oz_kpad(long long K) { return (K + 31) / 32 * 32; }
 

@@ -1,16 +1,18 @@
-// Emulated FP64 GEMM on the int8 tensor cores (Ozaki scheme, slices of 7 bits).
+// Emulated FP64 GEMM on the int8 tensor cores (Ozaki scheme, balanced base-256 digits).
 //
 // FP64 has no tcgen05 kind; the FP64 DMMA pipe peaks at ~35 TFLOP/s on B200
 // while kind::i8 runs ~4.5 POPS.  Each row of A (and of B) is written as
-//     x = 2^e sum_{t<S} d_t 2^{-7(t+1)},  d_t int8,
-// with 2^e >= max|row| (k_oz_slice).  Then
-//     (A B^T)_ij = 2^{e_i + f_j} sum_D 2^{-7(D+2)} sum_{t+u=D} (A_t B_u^T)_ij
+//     x = 2^e sum_{t<S} d_t 2^{-8(t+1)},  d_t int8 (the whole range [-128, 127]),
+// with 2^e > 2 max|row| (k_oz_slice).  Then
+//     (A B^T)_ij = 2^{e_i + f_j} sum_D 2^{-8(D+2)} sum_{t+u=D} (A_t B_u^T)_ij
 // and every A_t B_u^T is an exact int32 product on the tensor cores.  Products
 // with t + u >= S sit below the slicing error and are skipped, so one K-chunk
 // costs S(S+1)/2 MMAs accumulating into S diagonals in TMEM (S x 64 columns of
-// a 128 x 64 tile; S = 8 fills the 512 columns).  Relative accuracy per entry is
-// ~K 2^{-7S} max|a_i| max|b_j|: S = 8 is at the level of an FP64 dot product,
-// S = 7 about 16x coarser.
+// a 128 x 64 tile).  Relative accuracy per entry is ~sqrt(K) 2^{-8S+4} max|a_i|
+// max|b_j| (balanced digits: the dropped products average out): S = 6 (21 products,
+// the default) is at the level of an FP64 dot product's own rounding for K ~ 512,
+// S = 7 (28 products, 56 bits) is below it.  Round 2 started with base-128 digits
+// (S = 7, 28 products for 50 bits); base 256 gives 48 bits in 21 products.
 //
 // This file holds the slicing kernel and a plain C = A B^T GEMM over sliced
 // operands (dngd_oz_gemm_nt); the factored dual Gram uses the same machinery
@@ -29,7 +31,7 @@
 namespace dngd {
 
 // One warp per row: max |x| (non-finite flagged), scale 2^e with
-// max 2^-e 128 < 127, then S digits per entry (oz_digits4), written as
+// max 2^-e 256 <= 127, then S digits per entry (oz_digits4), written as
 // 4-digit words per slice.
 template <int S>
 __global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ X, long long rows,
@@ -75,7 +77,7 @@ __global__ void __launch_bounds__(256) k_oz_slice(const double* __restrict__ X, 
   }
   const int e = bad ? 0 : oz_row_exponent(mx);
   if (lane == 0) scale[row] = bad ? CUDART_NAN : ldexp(1.0, e);
-  const double sinv = ldexp(1.0, 7 * S - e);
+  const double sinv = ldexp(1.0, OZ_BITS * S - e);
   for (long long w = lane; w < words; w += 32) {
     double v[4];
     load4(w, v);
@@ -96,8 +98,7 @@ int oz_slice_into(dngd_ctx* ctx, cudaStream_t s, const double* X, long long rows
   switch (slices) {
     case 6: k_oz_slice<6><<<grid, 256, 0, s>>>(X, rows, K, ld, kpad, plane, Q, scale); break;
     case 7: k_oz_slice<7><<<grid, 256, 0, s>>>(X, rows, K, ld, kpad, plane, Q, scale); break;
-    case 8: k_oz_slice<8><<<grid, 256, 0, s>>>(X, rows, K, ld, kpad, plane, Q, scale); break;
-    default: return set_error(ctx, DNGD_ERR_DIMENSION, "oz_slice: slices must be 6, 7 or 8");
+    default: return set_error(ctx, DNGD_ERR_DIMENSION, "oz_slice: slices must be 6 or 7");
   }
   return cuda_status(ctx, cudaGetLastError(), "oz_slice");
 }
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(256) k_oz_slice_split(const double* __restrict
   const int e = bad ? 0 : oz_row_exponent(mx);
   const long long orow = z * M + row;
   if (tid == 0) scale[orow] = bad ? CUDART_NAN : ldexp(1.0, e);
-  const double sinv = ldexp(1.0, 7 * S - e);
+  const double sinv = ldexp(1.0, OZ_BITS * S - e);
   for (long long w = tid; w < words; w += 256) {
     double v[4];
     load4(w, v);
@@ -192,8 +193,7 @@ static int oz_slice_split(dngd_ctx* ctx, cudaStream_t s, const double* X, long l
   switch (slices) {
     case 6: k_oz_slice_split<6><<<grid, 256, 0, s>>>(X, M, K, ld, kl, kpad, plane, Q, scale); break;
     case 7: k_oz_slice_split<7><<<grid, 256, 0, s>>>(X, M, K, ld, kl, kpad, plane, Q, scale); break;
-    case 8: k_oz_slice_split<8><<<grid, 256, 0, s>>>(X, M, K, ld, kl, kpad, plane, Q, scale); break;
-    default: return set_error(ctx, DNGD_ERR_DIMENSION, "oz_slice: slices must be 6, 7 or 8");
+    default: return set_error(ctx, DNGD_ERR_DIMENSION, "oz_slice: slices must be 6 or 7");
   }
   return cuda_status(ctx, cudaGetLastError(), "oz_slice_split");
 }
@@ -222,7 +222,7 @@ int oz_splitk_choose(dngd_ctx* ctx, long long M, long long N, long long K) {
   long long sp = (ctx->num_sms + tiles - 1) / tiles;            // about one wave
   sp = std::min(sp, std::max(1LL, K / 1024));                   // >= 1024 of K per split
   sp = std::min(sp, 32LL);
-  // the int32 diagonal accumulators hold K <= 32768 (kOzMaxK) per split
+  // the int32 diagonal accumulators hold K <= 16384 (kOzMaxK) per split
   sp = std::max(sp, (K + (kOzMaxK - 32) - 1) / (kOzMaxK - 32));
   return static_cast<int>(std::max(1LL, sp));
 }
@@ -268,7 +268,7 @@ int oz_gemm_splitk(dngd_ctx* ctx, cudaStream_t s, const double* A, long long lda
     return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm_splitk: workspace too small");
   }
   const OzSplitK L = oz_splitk_layout(work, M, N, K, slices, splits);
-  if (L.kp > kOzMaxK) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm_splitk: split longer than 32768");
+  if (L.kp > kOzMaxK) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm_splitk: split longer than 16384");
   int rc = oz_slice_split(ctx, s, A, M, K, lda, L.kl, L.kp, splits, slices, L.qa, L.sa);
   if (rc) return rc;
   rc = oz_slice_split(ctx, s, B, N, K, ldb, L.kl, L.kp, splits, slices, L.qb, L.sb);
@@ -470,7 +470,7 @@ int oz_gemm_batched(dngd_ctx* ctx, cudaStream_t s, const int8_t* QA, const doubl
   switch (slices) {
     case 6: return oz_gemm_launch<6>(ctx, s, mA, mB, scA, scB, C, ldc, M, N, nk, batch, a_brows, b_brows, sC);
     case 7: return oz_gemm_launch<7>(ctx, s, mA, mB, scA, scB, C, ldc, M, N, nk, batch, a_brows, b_brows, sC);
-    default: return oz_gemm_launch<8>(ctx, s, mA, mB, scA, scB, C, ldc, M, N, nk, batch, a_brows, b_brows, sC);
+    default: return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm: slices must be 6 or 7");
   }
 }
 
@@ -494,8 +494,8 @@ extern "C" int dngd_oz_gemm_nt(dngd_ctx* ctx, void* stream, int64_t M, int64_t N
                                double* C, int64_t ldc, int slices, void* work, size_t work_bytes) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (M <= 0 || N <= 0) return DNGD_OK;
-  if (K <= 0 || K > kOzMaxK) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm: K outside [1, 32768]");
-  if (slices < 6 || slices > 8) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm: slices must be 6, 7 or 8");
+  if (K <= 0 || K > kOzMaxK) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm: K outside [1, 16384]");
+  if (slices < OZ_SMIN || slices > OZ_SMAX) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm: slices must be 6 or 7");
   size_t need = 0;
   dngd_oz_gemm_workspace(ctx, M, N, K, slices, &need);
   if (work_bytes < need) return set_error(ctx, DNGD_ERR_DIMENSION, "oz_gemm: workspace too small");

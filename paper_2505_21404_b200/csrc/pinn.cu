@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_chan_slice(
     }
     const int e = bad[ch] ? 0 : oz_row_exponent(mx[ch]);
     if (lane == ch) scale[row0 + ch] = bad[ch] ? CUDART_NAN : ldexp(1.0, e);
-    sinv[ch] = ldexp(1.0, 7 * S - e);
+    sinv[ch] = ldexp(1.0, OZ_BITS * S - e);
   }
   const size_t plane = static_cast<size_t>(gridDim.y) * R * kpad;
   for (int q = lane; q < kpad; q += 32) {
@@ -335,28 +335,16 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_chan_slice(
     chan_val1<NCH, MODE>(T, cr, pgi, z0, ld, bs, W0, b0, x, w, q, v);
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
-      // oz_digits4's balanced base-128 digits of X = rint(v 2^(7S - e)), in 32-bit
-      // integers: X = Xh 2^(7L) + Xl with Xh = floor((X + c_L) / 2^(7L)), c_L the
-      // bottom-up carry offset 64 (1 + 128 + ... + 128^(L-1)), so Xl's L balanced
-      // digits end without a carry and Xh (|Xh| < 2^28) holds the top 4 -- the same
-      // digits as the int64 recurrence, with exact FP64 splitting
-      constexpr int Ld = S - 4;
-      constexpr double cL = Ld == 4 ? 64.0 * (1 + 128 + 16384 + 2097152)
-                                    : Ld == 3 ? 64.0 * (1 + 128 + 16384) : 64.0 * (1 + 128);
-      constexpr double sh = Ld == 4 ? 0x1p28 : Ld == 3 ? 0x1p21 : 0x1p14;
-      const double X = bad[ch] ? 0.0 : rint(v[ch] * sinv[ch]);
-      const double Xh = floor((X + cL) * (1.0 / sh));
-      // with the carry offsets added up front (T = u + 64 (1 + 128 + ...)), digit j is
-      // the j-th 7-bit field of T minus 64 and the leading digit is T >> 21 -- the
-      // recurrence's digits without its serial adds
-      const int Tl = __double2int_rn(fma(-Xh, sh, X)) + static_cast<int>(cL);
-      const int Th = __double2int_rn(Xh) + 64 * (1 + 128 + 16384);
+      // oz_digits4's digits: byte S-1-t of (X + offset) ^ offset is digit t
+      const long long y = oz_digit_bytes<S>(v[ch], sinv[ch], bad[ch] != 0);
+      const uint32_t ylo = static_cast<uint32_t>(y);
+      const uint32_t yhi = static_cast<uint32_t>(static_cast<unsigned long long>(y) >> 32);
       int8_t* dst = Q + (row0 + ch) * kpad + q;
 #pragma unroll
-      for (int t = S - 1; t >= 4; --t) dst[t * plane] = static_cast<int8_t>(((Tl >> (7 * (S - 1 - t))) & 127) - 64);
-#pragma unroll
-      for (int t = 3; t >= 1; --t) dst[t * plane] = static_cast<int8_t>(((Th >> (7 * (3 - t))) & 127) - 64);
-      dst[0] = static_cast<int8_t>(Th >> 21);
+      for (int t = 0; t < S; ++t) {
+        const int byte = S - 1 - t;
+        dst[t * plane] = static_cast<int8_t>((byte < 4 ? ylo : yhi) >> (8 * (byte & 3)));
+      }
     }
   }
 }
@@ -1549,18 +1537,18 @@ static void carve_bigin(const Plan& P, Arena& A, BigIn& G, bool dir) {
 }
 
 // Ozaki digits of the hidden-layer GEMMs (activation pass, f_vv, line-search
-// forward): DNGD_GEMM_SLICES (0, 7, 8) overrides; default 7 when a hidden layer is
+// forward): DNGD_GEMM_SLICES (0, 6, 7) overrides; default 6 when a hidden layer is
 // 128 wide or more (the int8 tensor cores beat the FP64 DMMA GEMM there), else the
 // DMMA GEMM
 static int oz_ls_slices(const Plan& P) {
   if (const char* e = getenv("DNGD_GEMM_SLICES")) {
     const int v = atoi(e);
-    return (v == 7 || v == 8) ? v : 0;
+    return (v == 6 || v == 7) ? v : 0;
   }
   if (P.L < 3) return 0;
   long long wmax = 0;
   for (int k = 1; k <= P.L - 2; ++k) wmax = std::max(wmax, std::max(P.w[k], P.w[k + 1]));
-  return wmax >= 128 ? 7 : 0;
+  return wmax >= 128 ? 6 : 0;
 }
 
 // digit planes for one emulated GEMM of up to rows_a x K by rows_b x K
@@ -1813,11 +1801,11 @@ static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const d
       const int nb = std::min(B.oz_cb, C - b0);
       if (in_fused) {
         const long long kp1 = oz_kpad(P.w[1]);
-        if (B.oz_S == 8) {
-          launch_input_slice<8>(s, P.T, thetas + static_cast<long long>(b0) * P.n, P.n,
+        if (B.oz_S == 7) {
+          launch_input_slice<7>(s, P.T, thetas + static_cast<long long>(b0) * P.n, P.n,
                                 static_cast<int>(P.w[1]), P.R, kp1, nb, B.ozQA, B.ozsA);
         } else {
-          launch_input_slice<7>(s, P.T, thetas + static_cast<long long>(b0) * P.n, P.n,
+          launch_input_slice<6>(s, P.T, thetas + static_cast<long long>(b0) * P.n, P.n,
                                 static_cast<int>(P.w[1]), P.R, kp1, nb, B.ozQA, B.ozsA);
         }
         rc = cuda_status(ctx, cudaGetLastError(), "input_slice");
@@ -1834,11 +1822,11 @@ static int forward_batched(dngd_ctx* ctx, cudaStream_t s, const Plan& P, const d
         if (rc) break;
         const double* bias = thetas + static_cast<long long>(b0) * P.n + P.off[k] + P.w[k] * P.w[k + 1];
         if (k < L - 2 && fuse) {
-          if (B.oz_S == 8) {
-            launch_tanh_slice<8>(s, P.T, B.Z + b0 * act_s, static_cast<int>(N), P.ldmax, bias, P.n,
+          if (B.oz_S == 7) {
+            launch_tanh_slice<7>(s, P.T, B.Z + b0 * act_s, static_cast<int>(N), P.ldmax, bias, P.n,
                                  act_s, P.R, oz_kpad(N), nb, B.ozQA, B.ozsA);
           } else {
-            launch_tanh_slice<7>(s, P.T, B.Z + b0 * act_s, static_cast<int>(N), P.ldmax, bias, P.n,
+            launch_tanh_slice<6>(s, P.T, B.Z + b0 * act_s, static_cast<int>(N), P.ldmax, bias, P.n,
                                  act_s, P.R, oz_kpad(N), nb, B.ozQA, B.ozsA);
           }
         } else if (k == L - 2 && r_fused != nullptr && fuse) {
@@ -2817,13 +2805,13 @@ static size_t gram_oz_bytes(const Plan& P, int S) {
 }
 
 static int goz_check(dngd_ctx* ctx, const Plan& P, int slices) {
-  if (slices != 7) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_oz: 7 digit slices (8 exceeds shared memory)");
+  if (slices != 6 && slices != 7) return set_error(ctx, DNGD_ERR_DIMENSION, "gram_oz: 6 or 7 digit slices");
   if (P.wide_in) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: wide input layer");
   if (P.T.din > DNGD_MAX_GRAD) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: input dim > 12");
   if (P.R >= (1LL << 31)) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: too many activation rows");
   for (int k = 0; k < P.L; ++k)
     if (goz_kdim(P, k, 0) > kOzMaxK || goz_kdim(P, k, 1) > kOzMaxK)
-      return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: layer wider than 32768");
+      return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: layer wider than 16384");
   for (int c = 0; c < P.T.n; ++c)
     if (P.T.c[c].nch > OZ_BN) return set_error(ctx, DNGD_ERR_UNSUPPORTED, "gram_oz: more than 64 channels per point");
   return DNGD_OK;
@@ -2922,7 +2910,7 @@ extern "C" int dngd_gram_oz_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc
   gp.dbg = getenv("DNGD_GOZ_DBG") ? atoi(getenv("DNGD_GOZ_DBG")) : 0;
   if (t1 <= t0) return DNGD_OK;
   const size_t smem = gram_oz_smem(slices);
-  auto kern = k_gram_oz<7>;  // S = 8 would need 235 KB of shared memory (refused by goz_check)
+  auto kern = slices == 7 ? k_gram_oz<7> : k_gram_oz<6>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_status(ctx, e, "gram_oz smem attribute");
@@ -2995,18 +2983,22 @@ static size_t cols_scratch_bytes(const Plan& P, long long rows) {
 // K[:, I] on the int8 engine (gram_oz.cuh rect mode) under the same rule as the
 // factored Gram (kernels.gram_emulation_slices: hidden layers >= 64 wide,
 // DNGD_GRAM_SLICES=0 keeps the DMMA kernel); 0 where the emulated kernel does not apply
-static int goz_cols_slices(const Plan& P) {
-  if (const char* e = getenv("DNGD_GRAM_SLICES")) {
-    if (atoi(e) == 0) return 0;
-  }
+static bool goz_cols_slices_ok(const Plan& P) {
   long long hmax = 0;
   for (int k = 1; k < P.L; ++k) hmax = std::max(hmax, P.w[k]);
   if (hmax < 64 || P.wide_in || P.T.din > DNGD_MAX_GRAD || P.R >= (1LL << 31)) return 0;
   for (int k = 0; k < P.L; ++k)
     if (goz_kdim(P, k, 0) > kOzMaxK || goz_kdim(P, k, 1) > kOzMaxK) return 0;
   for (int c = 0; c < P.T.n; ++c)
-    if (P.T.c[c].nch > OZ_BN) return 0;
-  return 7;
+    if (P.T.c[c].nch > OZ_BN) return false;
+  return true;
+}
+static int goz_cols_slices(const Plan& P) {
+  if (const char* e = getenv("DNGD_GRAM_SLICES")) {
+    if (atoi(e) == 0) return 0;
+    if (atoi(e) == 7) return goz_cols_slices_ok(P) ? 7 : 0;
+  }
+  return goz_cols_slices_ok(P) ? 6 : 0;
 }
 
 // digit planes of the full activations (R rows) and of the gathered landmark rows
@@ -3163,7 +3155,7 @@ extern "C" int dngd_gram_factored_cols(dngd_ctx* ctx, void* stream, const dngd_m
     gq.tile0 = 0;
     if (ntile == 0) return DNGD_OK;
     const size_t smem = gram_oz_smem(S);
-    auto kern = k_gram_oz<7>;
+    auto kern = S == 7 ? k_gram_oz<7> : k_gram_oz<6>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return cuda_status(ctx, e, "gram_cols oz smem attribute");
     kern<<<static_cast<unsigned>(std::min(ntile, ctx->num_sms)), OZ_THREADS, smem, s>>>(gq, ntile);

@@ -182,70 +182,96 @@ DNGD_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" :::
 DNGD_DEV bool elect_lane0() { return (threadIdx.x & 31) == 0; }
 
 // ---------------------------------------------------------------- Ozaki digits
-// x = scale * sum_{t<S} d_t 2^{-7(t+1)} + O(scale 2^{-7S-1}), |d_0| <= 127,
-// |d_t| <= 64, scale a power of two >= max|row| (oz_digits4).  A product of two sliced values is
-// sum_D acc_D 2^{-7(D+2)} with acc_D = sum_{t+u=D} d_t e_u; the diagonals
+// x = scale * sum_{t<S} d_t 2^{-8(t+1)} + O(scale 2^{-8S-1}), |d_0| <= 127,
+// d_t in [-128, 127] (balanced base-256 digits: the whole int8 range), scale = 2^e
+// with max|row| 2^-e 256 <= 127 (oz_row_exponent).  A product of two sliced values
+// is sum_D acc_D 2^{-8(D+2)} with acc_D = sum_{t+u=D} d_t e_u; the diagonals
 // D >= S are dropped (below the slicing error).  oz_combine folds the int32
-// diagonals exactly into two int64 (|acc_D| < 2^31 for K <= 32768) and rounds
+// diagonals exactly into two int64 (|acc_D| < 2^31 for K <= 16384) and rounds
 // once.
-// Digits of 4 values of one row with scale 2^e: X = rint(v 2^(7S - e)) (exact
-// power-of-two scaling, one rounding; |X| < 2^(7S) 127/128), then balanced
-// base-128 digits from the bottom -- t = u + 64, d = (t & 127) - 64 in [-64, 63],
-// u = t >> 7 -- and d_0 = the final u (|d_0| <= 127), so that
-// v = 2^e sum_t d_t 2^{-7(t+1)} + O(2^(e - 7S - 1)).  Balanced digits matter: the
-// products dropped below diagonal S then average out over K instead of adding up.
-// One conversion per value, integer ops per digit (the FP64 rint/convert per digit
-// was the slicing kernels' bottleneck).  Byte b of word t holds digit t of value b.
+// Digits of a value with row scale 2^e: X = rint(v 2^(8S - e)) (exact power-of-two
+// scaling, one rounding; |X| <= 2^(8S) 127/256).  With the carry offsets added up
+// front, Y = X + 128 (1 + 256 + ... + 256^(S-2)), the balanced digit t >= 1 is byte
+// S-1-t of Y minus 128 -- i.e. that byte with its top bit flipped, read as int8 --
+// and d_0 = Y >> 8(S-1) (arithmetic).  No per-digit arithmetic at all: one
+// conversion, one 64-bit add, one XOR mask, byte extracts.  Balanced digits matter:
+// the products dropped below diagonal S then average out over K instead of adding
+// up.  Byte b of word t holds digit t of value b.
+template <int S>
+DNGD_DEV constexpr long long oz_offset() {
+  long long o = 0;
+  for (int t = 0; t < S - 1; ++t) o |= 0x80LL << (8 * t);
+  return o;
+}
+// Y ^ mask: bytes 0 .. S-2 are the digits S-1 .. 1 (as int8), byte S-1 is d_0
+template <int S>
+DNGD_DEV long long oz_digit_bytes(double v, double sinv, bool bad) {
+  const long long X = bad ? 0LL : __double2ll_rn(v * sinv);
+  return (X + oz_offset<S>()) ^ oz_offset<S>();
+}
 template <int S>
 DNGD_DEV void oz_digits4(const double (&v)[4], double sinv, bool bad, uint32_t (&packed)[S]) {
-#pragma unroll
-  for (int t = 0; t < S; ++t) packed[t] = 0;
+  static_assert(S >= 5 && S <= 7, "X must fit 2^55");
+  uint32_t lo[4], hi[4];
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    long long u = bad ? 0LL : __double2ll_rn(v[b] * sinv);
+    const long long y = oz_digit_bytes<S>(v[b], sinv, bad);
+    lo[b] = static_cast<uint32_t>(y);
+    hi[b] = static_cast<uint32_t>(static_cast<unsigned long long>(y) >> 32);
+  }
+  // digit t = byte (S-1-t) of y: gather that byte of the four values into one word
 #pragma unroll
-    for (int t = S - 1; t >= 1; --t) {
-      const long long tt = u + 64;
-      const int d = static_cast<int>(tt & 127) - 64;
-      packed[t] |= (static_cast<uint32_t>(d) & 0xffu) << (8 * b);
-      u = tt >> 7;
-    }
-    packed[0] |= (static_cast<uint32_t>(static_cast<int>(u)) & 0xffu) << (8 * b);
+  for (int t = 0; t < S; ++t) {
+    const int byte = S - 1 - t;
+    const uint32_t* w = byte < 4 ? lo : hi;
+    const uint32_t sel = 0x4u * 0 + (byte & 3);  // byte index inside each word
+    // __byte_perm(x, y, s): nibble k of s picks byte (0-3 from x, 4-7 from y)
+    const uint32_t p01 = __byte_perm(w[0], w[1], sel | ((4u + sel) << 4));
+    const uint32_t p23 = __byte_perm(w[2], w[3], sel | ((4u + sel) << 4));
+    packed[t] = __byte_perm(p01, p23, 0x5410);
   }
 }
 
-// row scale exponent: 2^e >= max|row| with max 2^-e 128 < 127, so that the leading
-// balanced digit (X - lower digits) / 2^(7(S-1)) < 127 + 0.504 stays inside int8
+// row scale exponent: 2^e with max|row| 2^-e 256 <= 127, so that the leading digit
+// floor((X + offset) / 2^(8(S-1))) stays inside [-127, 127]
 DNGD_DEV int oz_row_exponent(double mx) {
   int e = 0;
   if (mx > 0.0) {
     const double f = frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)
-    if (f * 128.0 >= 127.0) ++e;
+    e += (f * 128.0 > 127.0) ? 2 : 1;
   }
   return e;
 }
 
 template <int S>
 DNGD_DEV double oz_combine(const int32_t (&acc)[S]) {
-  // 32 x 32 -> 64-bit multiply-adds (IMAD.WIDE), exact
-  long long hi = static_cast<long long>(acc[0]) * (1LL << 21);
-  hi = static_cast<long long>(acc[1]) * (1LL << 14) + hi;
-  hi = static_cast<long long>(acc[2]) * (1LL << 7) + hi;
-  hi = static_cast<long long>(acc[3]) + hi;
-  long long lo = static_cast<long long>(acc[4]) * (1LL << (7 * (S - 5)));
+  static_assert(S >= 5 && S <= 7, "two int64 halves");
+  constexpr int B = OZ_BITS;
+  constexpr int H = S / 2;  // diagonals 0 .. H-1 in hi, H .. S-1 in lo
+  // 32 x 32 -> 64-bit multiply-adds (IMAD.WIDE), exact: |hi| < 2^31 2^(8(H-1)) 1.01
+  // < 2^48, |lo| < 2^31 2^(8(S-H-1)) 1.01 < 2^56 (S = 7) -- the magic-constant
+  // conversion below needs < 2^51, so S = 7 converts lo with I2F instead
+  long long hi = static_cast<long long>(acc[0]);
 #pragma unroll
-  for (int d = 5; d < S; ++d) lo = static_cast<long long>(acc[d]) * (1LL << (7 * (S - 1 - d))) + lo;
-  // sum_{D<4} acc_D 2^{-7(D+2)} = hi 2^-35; sum_{4<=D<S} acc_D 2^{-7(D+2)} = lo 2^{-7(S+1)}
-  static_assert(S >= 5 && S <= 8, "4 + 1..4 diagonals");
-  constexpr double kLo = S == 8 ? 0x1p-63 : S == 7 ? 0x1p-56 : S == 6 ? 0x1p-49 : 0x1p-42;
-  // int64 -> double without I2F: |hi|, |lo| < 2^51 (K <= 32768), so adding them to
-  // the bit pattern of 1.5 2^52 ulp lands exactly on magic + hi ulp (one integer add,
-  // no carry out of the mantissa).  ulp(M1) = 2^-35, ulp(M2) = kLo.
-  constexpr double M1 = 0x1.8p17;
-  constexpr double M2 = kLo * 0x1.8p52;
-  const double a = __longlong_as_double(__double_as_longlong(M1) + hi) - (M1 + M2);  // hi 2^-35 - M2, exact
-  const double b = __longlong_as_double(__double_as_longlong(M2) + lo);              // M2 + lo kLo, exact
-  return a + b;  // = round(hi 2^-35 + lo kLo): the same single rounding as fma(lo, kLo, hi 2^-35)
+  for (int d = 1; d < H; ++d) hi = hi * (1LL << B) + static_cast<long long>(acc[d]);
+  long long lo = static_cast<long long>(acc[H]);
+#pragma unroll
+  for (int d = H + 1; d < S; ++d) lo = lo * (1LL << B) + static_cast<long long>(acc[d]);
+  // sum_{D<H} acc_D 2^{-B(D+2)} = hi 2^{-B(H+1)}; sum_{H<=D<S} acc_D 2^{-B(D+2)} = lo 2^{-B(S+1)}
+  constexpr double kHi = 1.0 / static_cast<double>(1ULL << (B * (H + 1)));
+  constexpr double kLo = kHi / static_cast<double>(1ULL << (B * (S - H)));
+  if constexpr (S - H - 1 <= 2) {
+    // int64 -> double without I2F: |hi|, |lo| < 2^51, so adding them to the bit
+    // pattern of 1.5 2^52 ulp lands exactly on magic + hi ulp (one integer add, no
+    // carry out of the mantissa).  ulp(M1) = kHi, ulp(M2) = kLo.
+    constexpr double M1 = kHi * 0x1.8p52;
+    constexpr double M2 = kLo * 0x1.8p52;
+    const double a = __longlong_as_double(__double_as_longlong(M1) + hi) - (M1 + M2);  // hi kHi - M2, exact
+    const double b = __longlong_as_double(__double_as_longlong(M2) + lo);              // M2 + lo kLo, exact
+    return a + b;  // = round(hi kHi + lo kLo): the same single rounding as an fma
+  } else {
+    return fma(static_cast<double>(lo), kLo, static_cast<double>(hi) * kHi);
+  }
 }
 
 }  // namespace dngd

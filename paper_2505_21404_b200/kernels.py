@@ -187,7 +187,7 @@ def gemm_nt(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor | None = None, K: 
 
 
 def oz_gemm_nt(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor | None = None,
-               slices: int = 8) -> torch.Tensor:
+               slices: int = 6) -> torch.Tensor:
     """C = A B^T, emulated FP64 on the int8 tensor cores (Ozaki slices, ozaki.cu)."""
     _check2d(A, "A")
     _check2d(B, "B")
@@ -284,22 +284,23 @@ def gram_factored(mlp, theta, classes_arr, nclass, r, K, ws, part=0, nparts=1):
 
 def gram_emulation_slices(mlp=None) -> int:
     """Ozaki digit count of the factored Gram's G-space products (0 = FP64 DMMA).
-    DNGD_GRAM_SLICES (0 or 7) overrides; by default hidden layers 64 wide or more run
-    emulated with 7 digits (int8 tcgen05: ~2.5x the DMMA kernel at config 3, 1.15x at
-    config 2's width 64; K within 5e-16 of it) and narrower nets stay on DMMA (a
-    32-wide layer is one K-chunk per phase: the TMEM drains would dominate)."""
+    DNGD_GRAM_SLICES (0, 6 or 7) overrides; by default hidden layers 64 wide or more
+    run emulated with 6 balanced base-256 digits (48 bits below each row's maximum, 21
+    int8 products per FP64 product; 7 digits = 56 bits, 28 products) and narrower nets
+    stay on DMMA (a 32-wide layer is one K-chunk per phase: the TMEM drains would
+    dominate)."""
     import os
 
     env = os.environ.get("DNGD_GRAM_SLICES")
     if env is not None:
         v = int(env)
-        if v not in (0, 7):
-            raise DimensionError("DNGD_GRAM_SLICES must be 0 or 7")
+        if v not in (0, 6, 7):
+            raise DimensionError("DNGD_GRAM_SLICES must be 0, 6 or 7")
         return v
     if mlp is None:
-        return 7
+        return 6
     hidden = [mlp.widths[k] for k in range(1, mlp.nlayers)]
-    return 7 if hidden and max(hidden) >= 64 else 0
+    return 6 if hidden and max(hidden) >= 64 else 0
 
 
 def gram_factored_act(mlp, classes_arr, nclass, K, act_ws, part=0, nparts=1, slices=None):

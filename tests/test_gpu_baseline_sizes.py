@@ -258,7 +258,7 @@ def test_emulated_path_twenty_step_trajectory(P):
 
     c = dict(CFG[2], widths=(2, 128, 128, 128, 128, 1), counts=(500, 100, 100))
     if os.environ.get("DNGD_GRAM_SLICES") is None:
-        assert K.gram_emulation_slices() == 7
+        assert K.gram_emulation_slices() == 6
     stats, (loss_g, loss_o, rel_g, rel_o, eta_g, eta_o) = _traj_pair(P, c)
     _log("heat1d_w128_emulated_traj20", stats)
     np.testing.assert_allclose(loss_g, loss_o, rtol=1e-6)

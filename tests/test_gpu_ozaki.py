@@ -23,7 +23,7 @@ def _ref(A, B):
 
 
 @pytest.mark.parametrize("M,N,Kd", [(128, 64, 32), (300, 200, 512), (1, 7, 5), (257, 130, 1000)])
-@pytest.mark.parametrize("slices", [8, 7])
+@pytest.mark.parametrize("slices", [7, 6])
 def test_oz_gemm_matches_fp64(K, M, N, Kd, slices):
     rng = np.random.default_rng(M * 7 + N + Kd)
     A = rng.standard_normal((M, Kd)) * np.exp(rng.uniform(-3, 3, size=(M, 1)))
@@ -35,7 +35,7 @@ def test_oz_gemm_matches_fp64(K, M, N, Kd, slices):
     # normwise per entry: |C - R| <= tol * |a_i| |b_j|
     bound = np.outer(np.linalg.norm(A, axis=1), np.linalg.norm(B, axis=1))
     err = np.max(np.abs(C - R) / bound)
-    tol = {8: 1e-15, 7: 2e-14}[slices]
+    tol = {7: 1e-15, 6: 1e-13}[slices]
     print(f"M={M} N={N} K={Kd} S={slices}: max normwise err {err:.2e}")
     assert err <= tol
     # and against the FP64 tensor-core GEMM of the library
@@ -96,7 +96,7 @@ def _act_setup(K, problem, widths, counts, seed):
 
 
 @pytest.mark.parametrize("name,problem,widths,counts", GRAM_CASES)
-@pytest.mark.parametrize("slices", [7])
+@pytest.mark.parametrize("slices", [7, 6])
 def test_gram_emulated_matches_oracle(K, name, problem, widths, counts, slices):
     """Emulated-FP64 factored Gram (int8 tcgen05) == oracle J J^T to 1e-12 (the
     north-star Gram tolerance) and to the FP64 DMMA kernel at the FP64 rounding level."""
@@ -114,7 +114,7 @@ def test_gram_emulated_matches_oracle(K, name, problem, widths, counts, slices):
     rel_d = np.linalg.norm(Kg - Kdm) / np.linalg.norm(Kdm)
     print(f"{name} S={slices}: vs oracle {rel:.2e}, vs DMMA {rel_d:.2e}")
     assert rel <= 1e-12
-    assert rel_d <= 1e-14
+    assert rel_d <= {7: 2e-15, 6: 1e-13}[slices]
     # deterministic: a second launch is bit-identical
     Ke2 = torch.empty_like(Ke)
     K.gram_factored_act(mlp, arr, len(classes), Ke2, ws, slices=slices)
@@ -128,14 +128,14 @@ def test_gram_emulated_parts_sum_to_full(K, nparts):
     classes, theta, arr, keep, mlp, ws, m = _act_setup(K, O.OraclePoissonSin(5), (5, 128, 128, 1),
                                                        (150, 40), 13)
     full = torch.empty((m, m), dtype=torch.float64, device="cuda")
-    K.gram_factored_act(mlp, arr, len(classes), full, ws, slices=7)
+    K.gram_factored_act(mlp, arr, len(classes), full, ws, slices=6)
     acc = torch.zeros((m, m), dtype=torch.float64, device="cuda")
     cover = torch.zeros((m, m), dtype=torch.int32, device="cuda")
     for p in range(nparts):
         part = torch.zeros((m, m), dtype=torch.float64, device="cuda")
         sentinel = torch.full((m, m), np.nan, dtype=torch.float64, device="cuda")
-        K.gram_factored_act(mlp, arr, len(classes), part, ws, p, nparts, slices=7)
-        K.gram_factored_act(mlp, arr, len(classes), sentinel, ws, p, nparts, slices=7)
+        K.gram_factored_act(mlp, arr, len(classes), part, ws, p, nparts, slices=6)
+        K.gram_factored_act(mlp, arr, len(classes), sentinel, ws, p, nparts, slices=6)
         cover += (~torch.isnan(sentinel)).to(torch.int32)
         acc += part
     assert int(cover.min()) == 1 and int(cover.max()) == 1
@@ -169,7 +169,7 @@ def test_gram_cols_emulated_matches_full_gram(K, name, problem, widths, counts):
     ell = min(m - 1, 97)
     landmarks = np.sort(rng.choice(m, size=ell, replace=False)).astype(np.int64)
     Kf = torch.zeros((m, m), dtype=torch.float64, device="cuda")
-    K.gram_factored_act(mlp, arr, len(classes), Kf, ws, slices=7)
+    K.gram_factored_act(mlp, arr, len(classes), Kf, ws, slices=6)
     Kc = torch.full((m, ell + ell % 2), float("nan"), dtype=torch.float64, device="cuda")
     K.gram_factored_cols(mlp, arr, len(classes), landmarks, Kc, ws)
     torch.cuda.synchronize()

@@ -44,13 +44,13 @@ for name, widths, counts in CASES:
     ws = rmap._act_workspace()
     out = {"case": name, "widths": widths, "m": m, "n": rmap.n}
     Ks = {}
-    for s in (0, 7):
+    for s in (0, 6, 7):
         Kt = torch.zeros(m, m, dtype=torch.float64, device="cuda")
         out[f"ms_s{s}"] = timed(lambda: K.gram_factored_act(d["mlp"], d["arr"], d["nclass"], Kt, ws, slices=s))
         Ks[s] = Kt
     ref = Ks[0]
     nrm = float(ref.norm())
-    for s in (7,):
+    for s in (6, 7):
         dK = Ks[s] - ref
         out[f"rel_fro_s{s}"] = float(dK.norm()) / nrm
         out[f"rel_max_s{s}"] = float(dK.abs().max() / ref.abs().max())
@@ -60,7 +60,7 @@ for name, widths, counts in CASES:
         _, J = rmap.linearize_t(theta)
         Km = K.syrk(J, rmap.n)
         torch.cuda.synchronize()
-        for s in (0, 7):
+        for s in (0, 6, 7):
             out[f"vs_JJt_s{s}"] = float((Ks[s] - Km).norm()) / float(Km.norm())
         del J, Km
     print(json.dumps(out), flush=True)

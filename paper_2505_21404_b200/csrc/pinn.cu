@@ -233,10 +233,12 @@ struct ChanRegs {
 // channel values of neuron q of one (point, candidate) (0 past w); the Laplacian's
 // sum runs over the channels in ascending order -- k_tanh_fwd / k_input_fwd's
 // order when C.lap_ch is ascending, which the launcher requires
-template <int NCH, int MODE>
+// TC: 1 = store tanh into the warp's shared cache tc (when given), 2 = read it back
+// instead of evaluating tanh again (k_chan_slice's second pass; same value, same lane)
+template <int NCH, int MODE, int TC = 0>
 DNGD_DEV void chan_val1(const Classes& T, const ChanRegs<NCH>& cr, const int* pgi, const double* z0,
                         long long ld, const double* bs, const double* W0, const double* b0,
-                        const double* x, int w, int q, double (&v)[NCH]) {
+                        const double* x, int w, int q, double (&v)[NCH], double* tc = nullptr) {
 #pragma unroll
   for (int ch = 0; ch < NCH; ++ch) v[ch] = 0.0;
   if (q >= w) return;
@@ -244,8 +246,14 @@ DNGD_DEV void chan_val1(const Classes& T, const ChanRegs<NCH>& cr, const int* pg
     double zz[NCH];
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) zz[ch] = z0[ch * ld + q];
-    const double z = zz[0] + bs[q];
-    const double t = tanh(z), sd = 1.0 - t * t;
+    double t;
+    if (TC == 2 && tc) {
+      t = tc[q];
+    } else {
+      t = tanh(zz[0] + bs[q]);
+      if (TC == 1 && tc) tc[q] = t;
+    }
+    const double sd = 1.0 - t * t;
     v[0] = t;
 #pragma unroll
     for (int gi = 0; gi < NCH - 1; ++gi)
@@ -258,9 +266,16 @@ DNGD_DEV void chan_val1(const Classes& T, const ChanRegs<NCH>& cr, const int* pg
       v[NCH - 1] = sd * zz[NCH - 1] - 2.0 * t * sd * G;
     }
   } else {
-    double z = b0[q];
-    for (int d = 0; d < T.din; ++d) z = fma(x[d], W0[d * w + q], z);
-    const double t = tanh(z), sd = 1.0 - t * t;
+    double t;
+    if (TC == 2 && tc) {
+      t = tc[q];
+    } else {
+      double z = b0[q];
+      for (int d = 0; d < T.din; ++d) z = fma(x[d], W0[d * w + q], z);
+      t = tanh(z);
+      if (TC == 1 && tc) tc[q] = t;
+    }
+    const double sd = 1.0 - t * t;
     v[0] = t;
     double G = 0.0;
 #pragma unroll
@@ -276,14 +291,16 @@ DNGD_DEV void chan_val1(const Classes& T, const ChanRegs<NCH>& cr, const int* pg
 }
 
 template <int S, int NCH, int MODE>
-__global__ void __launch_bounds__(32 * kCsWarps) k_chan_slice(
+__global__ void __launch_bounds__(32 * kCsWarps, MODE == 1 ? 3 : 0) k_chan_slice(
     Classes T, int cls, const double* __restrict__ Z, int w, long long ld,
     const double* __restrict__ par, long long par_s, long long act_s, long long R, long long kpad,
-    int8_t* __restrict__ Q, double* __restrict__ scale) {
+    int8_t* __restrict__ Q, double* __restrict__ scale, int cache) {
+  extern __shared__ double cs_tanh[];  // cache: kCsWarps x w tanh values (pass 1 -> pass 2)
   const ClassDev& C = T.c[cls];
   const long long i = static_cast<long long>(blockIdx.x) * kCsWarps + (threadIdx.x >> 5);
   if (i >= C.count) return;
   const int lane = threadIdx.x & 31;
+  double* tc = cache ? cs_tanh + static_cast<size_t>(threadIdx.x >> 5) * w : nullptr;
   const int cand = blockIdx.y;
   // MODE 0: par = bias of every candidate; MODE 1: par = the candidates' thetas
   const double* z0 = MODE == 0 ? Z + cand * act_s + (C.act0 + i * NCH) * ld : nullptr;
@@ -310,7 +327,7 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_chan_slice(
   // per (slice, row) and neuron -- 32 consecutive bytes per warp store
   for (int q = lane; q < w; q += 32) {
     double v[NCH];
-    chan_val1<NCH, MODE>(T, cr, pgi, z0, ld, bs, W0, b0, x, w, q, v);
+    chan_val1<NCH, MODE, MODE == 1 ? 1 : 0>(T, cr, pgi, z0, ld, bs, W0, b0, x, w, q, v, tc);
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       bad[ch] |= !isfinite(v[ch]);
@@ -330,9 +347,10 @@ __global__ void __launch_bounds__(32 * kCsWarps) k_chan_slice(
     sinv[ch] = ldexp(1.0, OZ_BITS * S - e);
   }
   const size_t plane = static_cast<size_t>(gridDim.y) * R * kpad;
+  __syncwarp();
   for (int q = lane; q < kpad; q += 32) {
     double v[NCH];
-    chan_val1<NCH, MODE>(T, cr, pgi, z0, ld, bs, W0, b0, x, w, q, v);
+    chan_val1<NCH, MODE, MODE == 1 ? 2 : 0>(T, cr, pgi, z0, ld, bs, W0, b0, x, w, q, v, tc);
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
       // oz_digits4's digits: byte S-1-t of (X + offset) ^ offset is digit t
@@ -436,10 +454,15 @@ static void launch_chan_slice(cudaStream_t s, const Classes& T, const double* Z,
   for (int c = 0; c < T.n; ++c) {
     if (T.c[c].count == 0) continue;
     const dim3 grid(static_cast<unsigned>((T.c[c].count + kCsWarps - 1) / kCsWarps), nb);
+    // tanh cache between the two passes while it fits the default 48 KB of shared memory
+    const size_t cbytes = static_cast<size_t>(kCsWarps) * w * sizeof(double);
+    // (input-layer mode only: the hidden-layer mode is bound by its Z reads and digit
+    // writes, and the cache costs it a resident CTA -- measured 0.81 -> 0.94 ms)
+    const int cache = (MODE == 1 && cbytes <= 48 * 1024) ? 1 : 0;
 #define DNGD_CS(N)                                                                                 \
   case N:                                                                                          \
-    k_chan_slice<S, N, MODE><<<grid, 32 * kCsWarps, 0, s>>>(T, c, Z, w, ld, par, par_s, act_s, R, \
-                                                           kpad, Q, scale);                        \
+    k_chan_slice<S, N, MODE><<<grid, 32 * kCsWarps, cache ? cbytes : 0, s>>>(                      \
+        T, c, Z, w, ld, par, par_s, act_s, R, kpad, Q, scale, cache);                              \
     break;
     switch (T.c[c].nch) {
       DNGD_CS(1) DNGD_CS(2) DNGD_CS(3) DNGD_CS(4) DNGD_CS(5) DNGD_CS(6) DNGD_CS(7) DNGD_CS(8)

@@ -25,7 +25,7 @@ pynvml.nvmlInit()
 h = pynvml.nvmlDeviceGetHandleByIndex(0)
 for dbg in sys.argv[1:] or ["0"]:
     os.environ["DNGD_GOZ_DBG"] = dbg
-    K.gram_factored_act(d["mlp"], d["arr"], d["nclass"], Kt, ws, slices=7)
+    K.gram_factored_act(d["mlp"], d["arr"], d["nclass"], Kt, ws, slices=int(os.environ.get("GOZ_S", "6")))
     torch.cuda.synchronize()
     samples, stop = [], threading.Event()
 
@@ -41,7 +41,7 @@ for dbg in sys.argv[1:] or ["0"]:
     a.record()
     n = 40
     for _ in range(n):
-        K.gram_factored_act(d["mlp"], d["arr"], d["nclass"], Kt, ws, slices=7)
+        K.gram_factored_act(d["mlp"], d["arr"], d["nclass"], Kt, ws, slices=int(os.environ.get("GOZ_S", "6")))
     b.record()
     torch.cuda.synchronize()
     stop.set()

@@ -281,7 +281,7 @@ DNGD_DEV void chan_val1(const Classes& T, const ChanRegs<NCH>& cr, const int* pg
 #pragma unroll
     for (int gi = 0; gi < NCH - 1; ++gi) {
       if (gi < cr.ngrad) {
-        const double dz = W0[static_cast<long long>(pgi ? pgi[gi] : cr.gd[gi]) * w + q];
+        const double dz = W0[cr.gd[gi] + q];  // gd: first-layer row offsets (k_chan_slice)
         v[1 + gi] = sd * dz;
         if ((cr.lapmask >> (1 + gi)) & 1u) G = fma(dz, dz, G);
       }
@@ -314,8 +314,11 @@ __global__ void __launch_bounds__(32 * kCsWarps, MODE == 1 ? 3 : 0) k_chan_slice
   cr.lapmask = 0;
   for (int l = 0; l < C.nlap; ++l) cr.lapmask |= 1u << C.lap_ch[l];
 #pragma unroll
-  for (int g = 0; g < (NCH > 1 ? NCH - 1 : 1); ++g) cr.gd[g] = g < C.ngrad ? C.grad_dims[g] : 0;
+  // input-layer mode: gd = offset of the derivative dim's row of W0 (class-wide dims,
+  // or this point's own: pgi), resolved once per warp instead of per neuron
   const int* pgi = C.pgi ? C.pgi + i * C.ngrad : nullptr;
+  for (int g = 0; g < (NCH > 1 ? NCH - 1 : 1); ++g)
+    cr.gd[g] = g < C.ngrad ? (MODE == 1 ? (pgi ? pgi[g] : C.grad_dims[g]) * w : C.grad_dims[g]) : 0;
   double mx[NCH];
   int bad[NCH];
 #pragma unroll

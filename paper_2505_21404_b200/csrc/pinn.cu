@@ -351,20 +351,24 @@ __global__ void __launch_bounds__(32 * kCsWarps, MODE == 1 ? 3 : 0) k_chan_slice
   }
   const size_t plane = static_cast<size_t>(gridDim.y) * R * kpad;
   __syncwarp();
-  for (int q = lane; q < kpad; q += 32) {
+  // store addresses by pointer increments (row pitch kpad, plane pitch `plane`): the
+  // 64-bit multiplies per (channel, digit) were a third of the loop's instructions
+  int8_t* prow = Q + row0 * kpad + lane;
+  for (int q = lane; q < kpad; q += 32, prow += 32) {
     double v[NCH];
     chan_val1<NCH, MODE, MODE == 1 ? 2 : 0>(T, cr, pgi, z0, ld, bs, W0, b0, x, w, q, v, tc);
+    int8_t* pch = prow;
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) {
+    for (int ch = 0; ch < NCH; ++ch, pch += kpad) {
       // oz_digits4's digits: byte S-1-t of (X + offset) ^ offset is digit t
       const long long y = oz_digit_bytes<S>(v[ch], sinv[ch], bad[ch] != 0);
       const uint32_t ylo = static_cast<uint32_t>(y);
       const uint32_t yhi = static_cast<uint32_t>(static_cast<unsigned long long>(y) >> 32);
-      int8_t* dst = Q + (row0 + ch) * kpad + q;
+      int8_t* dst = pch;
 #pragma unroll
-      for (int t = 0; t < S; ++t) {
+      for (int t = 0; t < S; ++t, dst += plane) {
         const int byte = S - 1 - t;
-        dst[t * plane] = static_cast<int8_t>((byte < 4 ? ylo : yhi) >> (8 * (byte & 3)));
+        *dst = static_cast<int8_t>((byte < 4 ? ylo : yhi) >> (8 * (byte & 3)));
       }
     }
   }

@@ -112,10 +112,10 @@ int dngd_gemm_nt(dngd_ctx* ctx, void* stream, int64_t M, int64_t N, int64_t K,
 
 /* ---- emulated-FP64 GEMM on the int8 tensor cores (Ozaki scheme) ------------
  * C = A B^T with A (M x K, lda), B (N x K, ldb) row-major doubles, C (M x N, ldc).
- * Every row is split into `slices` (6..8) int8 digits of 7 bits below a per-row
+ * Every row is split into `slices` (6 or 7) balanced base-256 int8 digits below a per-row
  * power-of-two scale; the S(S+1)/2 digit products that reach FP64 accuracy run
  * as exact int32 tcgen05 MMAs (kind::i8).  Same contract as the FP64 products
- * of solver.py:153 / model.py:88-97 it can replace; K <= 32768.  A row with a
+ * of solver.py:153 / model.py:88-97 it can replace; K <= 16384.  A row with a
  * non-finite entry yields NaN in its C row/column. */
 int dngd_oz_gemm_workspace(dngd_ctx* ctx, int64_t M, int64_t N, int64_t K, int slices,
                            size_t* bytes);
@@ -234,7 +234,7 @@ int dngd_gram_factored_act(dngd_ctx* ctx, void* stream, const dngd_mlp_desc* mlp
 /* ---- factored dual Gram with emulated-FP64 products (solver.py:142-155) -----
  * Same result and tile sharding as dngd_gram_factored_act (K = J J^T from the
  * activations left in act_work by dngd_activations), with every G-space GEMM
- * computed from `slices` (7 or 8) int8 Ozaki digits per activation row on the
+ * computed from `slices` (6 or 7) balanced base-256 int8 Ozaki digits per activation row on the
  * tcgen05 tensor cores.  oz_work: dngd_gram_oz_workspace bytes (digit planes). */
 int dngd_gram_oz_workspace(dngd_ctx* ctx, const dngd_mlp_desc* mlp,
                            const dngd_class_desc* classes, int nclass, int slices,

@@ -13,6 +13,8 @@ import paper_2505_21404_b200 as P  # noqa: E402
 
 widths = tuple(int(x) for x in sys.argv[1].split(",")) if len(sys.argv) > 1 else (5, 512, 512, 512, 512, 1)
 counts = tuple(int(x) for x in sys.argv[2].split(",")) if len(sys.argv) > 2 else (3500, 500)
+if os.environ.get("LS_BUDGET_GB"):  # line-search activation chunk budget (experiment)
+    P.PinnResidualMap.LOSS_WS_BUDGET = int(float(os.environ["LS_BUDGET_GB"]) * 2**30)
 prob = P.make_problem(sys.argv[3] if len(sys.argv) > 3 else "poisson5d_sin")
 spec = P.MlpSpec(widths)
 rmap = P.PinnResidualMap(prob, spec, prob.sample(counts, np.random.default_rng(0)))

@@ -394,9 +394,7 @@ def _upload(arr, dev):
 class PinnResidualMap(ResidualMap):
     """Weighted PDE residuals of a tanh MLP, evaluated by the CUDA library."""
 
-    # bytes of line-search activations per chunk: all 31 candidates of config 3 in one
-    # chunk (10.9 GB; 8 GB split them 23 + 8: two pipeline ramps and tails, +0.4 ms)
-    LOSS_WS_BUDGET = 16 * 1024**3
+    LOSS_WS_BUDGET = 8 * 1024**3  # bytes of line-search activations per chunk
 
     def __new__(cls, *args, **kwargs):
         # problems with the ic_shift output transform get the two-map form
